@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""bench.py — GRASS layer-wise update hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl grass|reference]
+
+One STEP = one pass of the whole hot path on the
+BASELINE.json configs[1] workload: LLaMA-2-7B-shaped stack (32 decoder layers
+of N_p = 202,383,360 fp32 parameters), gamma = 2 active layers, optimizer
+states resident (no offload), 1 B200:
+    fused Eq. 2 norm + AdamW of the 2 active layers        (a1 + a5, one kernel)
+    MGN window accumulation                                (a2, in the kernel)
+    window commit + Eq. 4 EMA + Eq. 3 softmax              (a2 + a3, host fp64)
+    gamma-of-N_L resampling                                (a4, host)
+i.e. the bench resamples EVERY step (T_s = T_u = 1), the most expensive legal
+schedule.  Row a6 (layer-wise offload, configs[2]) is measured in the same run
+and reported under "offload"; the probing pass (a1 alone over all 32 layers)
+under "probe".
+
+Timing: CUDA events on the stream the library launches on, W untimed warm-up
+steps, K timed steps bracketed by barrier + synchronize, max over ranks.  Every
+step streams 11.3 GB through HBM (>> 126 MB L2), so no L2 flush is needed.
+For N > 1 (torchrun) the same total work is element-sharded over the ranks
+(gradients reduce-scattered and parameters all-gathered over NCCL): strong
+scaling.  `--impl reference` times the fp64 CPU oracle on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "active-layer params updated/s and offloaded step ms; % of HBM / host-link roofline"
+UNIT = "params/s"
+BYTES_PER_PARAM_UPDATE = 28      # read g, theta, m, v + write theta, m, v (fp32)
+BYTES_PER_PARAM_PROBE = 4        # read g
+FALLBACK_HBM_GBS = 6650.0        # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="grass", choices=["grass", "reference"])
+    ap.add_argument("--model", default="llama2-7b")
+    ap.add_argument("--gamma", type=int, default=2)
+    ap.add_argument("--legs", default="main,probe,offload,e2e,cpu",
+                    help="comma list of legs to run (main is always run)")
+    ap.add_argument("--offload-steps", type=int, default=10)
+    ap.add_argument("--lr", type=float, default=3e-5)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- utils
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "grass" else "gloo"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend, init_method="env://")
+    return rank, world, local
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------ oracle (CPU)
+def oracle_sample_time(n_p: int, gamma: int, sample_per_layer: int, lr: float, reps: int = 1):
+    """Times the fp64 oracle (oracle/, as it stands) on a bounded sample of one
+    step: Eq. 2 norms + AdamW over `sample_per_layer` elements of each of the
+    gamma active layers, then commit/EMA/softmax/sampling over N_L = 32."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle import grass_oracle as O
+    from synth import grad_sigmas, layer_grad, layer_params
+    sig = grad_sigmas(32, 0)
+    th = [layer_params(sample_per_layer, l).numpy() for l in range(gamma)]
+    g = [layer_grad(sample_per_layer, l, sig[l]).numpy() for l in range(gamma)]
+    m = [np.zeros(sample_per_layer, np.float32) for _ in range(gamma)]
+    v = [np.zeros(sample_per_layer, np.float32) for _ in range(gamma)]
+    st = O.MgnState(32)
+    for l in range(32):
+        st.record(l, 1e-4 * (l + 1))
+    st.commit(0.5)
+    times = []
+    with threadpool_limits(limits=1):
+        for r in range(reps):
+            t0 = time.perf_counter()
+            for l in range(gamma):
+                ss = O.sq_norm(g[l])
+                st.record(l, O.rms_norm(ss, n_p))
+                O.adamw_step(th[l], m[l], v[l], g[l], r + 1, lr, weight_decay=0.0)
+            mm = st.commit(0.5)
+            p = O.softmax_probs(mm, 1.0, True)
+            O.sample_layers(p, gamma, 1234, r)
+            times.append(time.perf_counter() - t0)
+    return times
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from synth import MODELS
+    n_p = MODELS[args.model].layer_numel
+    sample = 1 << 22                   # 4 Mi elements per active layer per step
+    times = oracle_sample_time(n_p, args.gamma, sample, args.lr, reps=args.warmup + args.steps)
+    timed = times[args.warmup:]
+    per_step = sum(timed) / len(timed)
+    value = args.gamma * sample / per_step
+    desc = (f"{args.gamma} x {sample} elements (of N_p = {n_p}) per step: fp64 Eq. 2 norm + AdamW, "
+            "MGN commit/EMA/softmax/sampling over 32 layers; single thread (threadpoolctl)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.model}-stack gamma={args.gamma} no-offload (configs[1]), oracle sample",
+                   "n_layers": 32, "layer_numel": n_p, "sample_per_layer": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ GRASS arm
+def run_grass(args, rank, world, local):
+    import torch
+
+    import paper_2604_07808_b200 as G
+    from synth import MODELS, grad_sigmas, layer_grad, layer_params
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    legs = set(args.legs.split(","))
+    shape = MODELS[args.model]
+    NL, n_p, gamma = shape.n_layers, shape.layer_numel, args.gamma
+    sig = grad_sigmas(NL, 0)
+    params = [layer_params(n_p, l, device=dev, norm_numel=shape.norm_numel) for l in range(NL)]
+    grads = [layer_grad(n_p, l, sig[l], step=0, device=dev, rank=rank) for l in range(NL)]
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream(device=dev)
+    ctx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, device=local,
+                  rank=rank, world=world)
+    hbm_peak, peak_kind = peaks()
+    out = {}
+
+    # ---- probing pass (a1 alone over every layer) -> MGN initialisation
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    probe_ms = []
+    for it in range(3 if "probe" in legs else 1):
+        ev[0].record(s)
+        ctx.mgn_accumulate(list(range(NL)), grads, stream=s)
+        ev[1].record(s)
+        torch.cuda.synchronize()
+        probe_ms.append(ev[0].elapsed_time(ev[1]))
+    probs = ctx.update_probs()
+    ids = ctx.sample_layers(0)
+    if "probe" in legs:
+        t = min(probe_ms[1:]) / 1e3
+        gbs = BYTES_PER_PARAM_PROBE * NL * n_p / world / t / 1e9
+        out["probe"] = {"ms": t * 1e3, "layers": NL, "GBps": gbs, "frac_hbm": gbs / hbm_peak,
+                        "bytes": BYTES_PER_PARAM_PROBE * NL * n_p // world}
+
+    # ---- main leg: configs[1]
+    def one_step(step, timing):
+        nonlocal ids
+        if timing is not None:
+            timing[0].record(s)
+        ctx.step_layers(ids, [params[l] for l in ids], [grads[l] for l in ids], args.lr, stream=s)
+        if timing is not None:
+            timing[1].record(s)
+        ctx.update_probs()
+        ids = ctx.sample_layers(step + 1)
+
+    for w in range(args.warmup):
+        one_step(w, None)
+    torch.cuda.synchronize()
+    barrier(world)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launch_count
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0.record(s)
+        for k in range(args.steps):
+            one_step(args.warmup + k, kev[k])
+        t1.record(s)
+        torch.cuda.synchronize()
+    launches = ctx.launch_count - launches0
+    barrier(world)
+    elapsed = max_over_ranks(t0.elapsed_time(t1) / 1e3, world, dev)
+    kernel_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    active = gamma * n_p
+    value = args.steps * active / elapsed
+    achieved = BYTES_PER_PARAM_UPDATE * active / world / (kernel_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"fused_update/{args.model}/g{gamma}/w{world}")
+
+    # ---- e2e: same step through the C ABI from pinned HOST gradients
+    e2e = None
+    if "e2e" in legs:
+        host_g = [grads[l].to("cpu").pin_memory() for l in range(gamma)]
+        h2d = sum(h.numel() * 4 for h in host_g)
+        d2h = NL * 16 + 4
+        for w in range(2):
+            one_step(w, None)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ksteps = max(3, min(args.steps, 10))
+        e0.record(s)
+        for k in range(ksteps):
+            with torch.cuda.stream(s):
+                for j, l in enumerate(ids):
+                    grads[l].copy_(host_g[j], non_blocking=True)
+            one_step(1000 + k, None)            # update_probs reads S, c back (d2h)
+        e1.record(s)
+        torch.cuda.synchronize()
+        et = max_over_ranks(e0.elapsed_time(e1) / 1e3, world, dev)
+        e2e = {"value": ksteps * active / et, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": et / ksteps * 1e3, "steps": ksteps}
+        del host_g
+
+    # ---- offload leg: configs[2] (row a6)
+    offload = None
+    if "offload" in legs:
+        del ctx
+        torch.cuda.empty_cache()
+        t_pin = time.perf_counter()
+        octx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, device=local,
+                       offload=True, rank=rank, world=world)
+        t_pin = time.perf_counter() - t_pin
+        duplex = measure_duplex(dev)
+        octx.mgn_accumulate(list(range(NL)), grads, stream=s)
+        octx.update_probs()
+        oids = octx.sample_layers(0)
+
+        def ostep(step):
+            nonlocal oids
+            octx.step_layers(oids, [params[l] for l in oids], [grads[l] for l in oids], args.lr, stream=s)
+            octx.update_probs()
+            oids = octx.sample_layers(step + 1)
+        for w in range(2):
+            ostep(w)
+        torch.cuda.synchronize()
+        barrier(world)
+        o0, o1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ok = args.offload_steps
+        o0.record(s)
+        for k in range(ok):
+            ostep(10 + k)
+        o1.record(s)
+        torch.cuda.synchronize()
+        ot = max_over_ranks(o0.elapsed_time(o1) / 1e3, world, dev) / ok
+        link_bytes = 8 * active // world                       # per direction per rank
+        floor = link_bytes / (duplex * 1e9)
+        offload = {"workload": f"{args.model}-stack gamma={gamma} offload (configs[2])",
+                   "step_ms": ot * 1e3, "params_per_s": active / ot,
+                   "h2d_bytes": link_bytes, "d2h_bytes": link_bytes,
+                   "link_GBps_per_dir": link_bytes / ot / 1e9,
+                   "duplex_GBps_per_dir_measured": duplex,
+                   "floor_ms": floor * 1e3, "frac_of_link_floor": floor / ot,
+                   "R1_within_10pct_of_link_floor": ot <= 1.10 * floor,
+                   "R2_offload_over_resident": ot / (elapsed / args.steps),
+                   "pinned_host_GB": octx.host_bytes / 1e9, "create_s": t_pin,
+                   "device_state_bytes": octx.device_bytes}
+        del octx
+
+    # ---- CPU oracle baseline
+    cpu = None
+    if "cpu" in legs and rank == 0 and world == 1:
+        sample = 1 << 23
+        times = oracle_sample_time(n_p, gamma, sample, args.lr, reps=2)
+        v = gamma * sample / min(times)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{gamma} x {sample} elements of one step (fp64 norm + AdamW) + commit/"
+                         f"softmax/sampling over {NL} layers, best of 2, single thread"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{args.model}-stack gamma={gamma} no-offload (configs[1])",
+                       "n_layers": NL, "layer_numel": n_p, "gamma": gamma,
+                       "active_params_per_step": active, "schedule": "resample every step (T_s=T_u=1)",
+                       "l2": "no flush: 11.3 GB streamed per step >> 126 MB L2",
+                       "parallelism": f"dp{world} element-sharded" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "kernel": "grass_fused_kernel<true> (fused Eq.2 norm + AdamW)",
+                         "kernel_ms": kernel_ms, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "probe": out.get("probe"), "offload": offload,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def measure_duplex(dev) -> float:
+    """Pinned H2D || D2H copy bandwidth per direction (GB/s), plumbing only."""
+    import torch
+    n = 1 << 28
+    h1 = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    h2 = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    d1 = torch.empty(n, dtype=torch.float32, device=dev)
+    d2 = torch.empty(n, dtype=torch.float32, device=dev)
+    a, b = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = 1e9
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        with torch.cuda.stream(a):
+            d1.copy_(h1, non_blocking=True)
+        with torch.cuda.stream(b):
+            h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t)
+    return n * 4 / best / 1e9
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_grass(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,235 @@
+/*
+ * grass.h — C ABI of the GRASS layer-wise update hot path on B200 (sm_100a).
+ *
+ * Paper: arxiv 2604.07808 (PAPER.md = the paper's LaTeX source).  The four
+ * hot-path calls follow the paper's statement of the problem:
+ *
+ *   grass_mgn_accumulate  Eq. 2 inner term r_{l,t} = sqrt(||g_t^(l)||^2 / N_p^(l))
+ *                         for the listed layers (probing
+ *                         PAPER.md:111-113).
+ *   grass_update_probs    Eq. 2 window mean + Eq. 4 EMA + Eq. 3 softmax
+ *                         (PAPER.md:91-93, 122-127, 115-120).
+ *   grass_sample_layers   "samples gamma layers out of N_L".
+ *   grass_step_layers     optimizer update of the trainable layers with the
+ *                         layer-wise optimizer-state offload
+ *                         (Fig. 4),
+ *                         fused with the Eq. 2 norm of the same gradients.
+ *
+ * Readings where the paper is silent are DESIGN.md R1-R14 (referenced below).
+ *
+ * Conventions (all calls):
+ *   - Every entry point returns a grass_status; no C++ exception ever crosses
+ *     this boundary.  On error nothing has been enqueued, the context is
+ *     unchanged, and grass_last_error() describes the failure.
+ *   - A "layer" is ONE flat, contiguous, 16-byte aligned fp32 buffer of N_p(l)
+ *     elements in device memory (the decoder block's tensors viewed back to back).
+ *   - Device pointers (params, grads) are CALLER-owned and must stay valid until
+ *     the work enqueued on `stream` has completed.  Host arrays passed in
+ *     (ids, pointer arrays, probs) are read before the call returns.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     grass_mgn_accumulate / grass_step_layers are stream-ordered and return
+ *     before the GPU work completes; grass_update_probs / grass_sync /
+ *     grass_read_state synchronise.
+ *   - Optimizer state (m, v, per-layer step t_l), the MGN state and the
+ *     probabilities are CONTEXT-owned.
+ *   - Non-finite gradients set a sticky device flag holding the smallest
+ *     offending layer id; the next synchronising call returns
+ *     GRASS_E_NONFINITE.  The fused update is single pass, so the
+ *     update of that step has already been applied; the caller aborts the step.
+ */
+#ifndef GRASS_H_
+#define GRASS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRASS_ABI_VERSION 1
+#define GRASS_NCCL_ID_BYTES 128
+
+typedef struct grass_ctx grass_ctx; /* opaque; one per process (= per rank / GPU) */
+
+typedef enum {
+  GRASS_OK = 0,
+  GRASS_E_INVALID = 1,   /* bad argument; nothing enqueued */
+  GRASS_E_STATE = 2,     /* call not valid in the current state */
+  GRASS_E_CUDA = 3,      /* CUDA runtime error (message in grass_last_error) */
+  GRASS_E_NCCL = 4,      /* NCCL error or NCCL unavailable when world > 1 */
+  GRASS_E_OOM = 5,       /* device or pinned-host allocation failed */
+  GRASS_E_NONFINITE = 6  /* a gradient contained inf/nan (sticky, see above) */
+} grass_status;
+
+typedef enum {
+  GRASS_POLICY_ADAPTIVE = 0, /* GRASS: EMA-refreshed MGN probabilities */
+  GRASS_POLICY_STATIC = 1,   /* GRASS*: probabilities frozen after probing */
+  GRASS_POLICY_UNIFORM = 2   /* LISA-style uniform sampling p = 1/N_L */
+} grass_policy;
+
+typedef enum {
+  GRASS_DECIDE_PROBE = 0,    /* step < T_p: norms only, no update */
+  GRASS_DECIDE_COMMIT_RESAMPLE = 1, /* commit window (+EMA), new probs, resample */
+  GRASS_DECIDE_RESAMPLE = 2, /* new sampling period with unchanged probs */
+  GRASS_DECIDE_CONTINUE = 3  /* keep the current trainable set */
+} grass_decision;
+
+typedef struct grass_config {
+  int32_t n_layers;            /* N_L >= 1 */
+  const int64_t* layer_numel;  /* host [N_L]; N_p(l) >= 1, true counts (R10); copied */
+  int32_t gamma;               /* active layers per period, 1 <= gamma <= N_L */
+  int32_t T_p, T_s, T_u;       /* schedule; T_u multiple of T_s (R11) */
+  double tau;                  /* Eq. 3 temperature > 0 (R3, default 1.0) */
+  double alpha;                /* Eq. 4 EMA factor in [0,1] (R13, default 0.5) */
+  int32_t normalize_mgn;       /* 1: max-normalise m before Eq. 3 (R3) */
+  int32_t policy;              /* grass_policy */
+  double beta1, beta2, eps, weight_decay; /* AdamW (R1): 0.9, 0.999, 1e-8, 0.0 */
+  uint64_t seed;               /* sampler seed (R7) */
+  int32_t device;              /* CUDA device ordinal this context lives on */
+  int32_t offload;             /* 0: m/v resident in HBM; 1: m/v in pinned host memory,
+                                  streamed per step */
+  int32_t overlap;             /* offload pipeline: 1 overlapped (Fig. 4 right),
+                                  0 vanilla serial HtoD->update->DtoH (Fig. 4 left) */
+  int64_t chunk_elems;         /* offload chunk (elements); multiple of grass_tile_elems();
+                                  0 = default (8 Mi elements) */
+  int32_t ring_slots;          /* device staging slots for the offload ring (>= 1; 0 = 3) */
+  int32_t rank, world;         /* data-parallel rank / world size (world = 1: no NCCL) */
+  const void* nccl_unique_id;  /* host, GRASS_NCCL_ID_BYTES; required when world > 1 */
+} grass_config;
+
+/* Fills *cfg with the defaults above (layer_numel = NULL, n_layers = 0). */
+grass_status grass_config_init(grass_config* cfg);
+
+/* Validates cfg, allocates: per layer m/v (HBM, or pinned host when offload;
+ * when world > 1 only this rank's shard), zeroed, t_l = 0; MGN accumulators;
+ * staging ring and copy streams (offload); NCCL communicator (world > 1, which
+ * requires every N_p divisible by 4*world).  *out receives the context.
+ * Errors: GRASS_E_INVALID (bad config: gamma > N_L, tau <= 0
+ * (SPEC.md:270), alpha outside [0,1], ...), GRASS_E_OOM,
+ * GRASS_E_CUDA, GRASS_E_NCCL.  On error *out = NULL. */
+grass_status grass_create(const grass_config* cfg, grass_ctx** out);
+
+/* Synchronises all context streams, frees everything.  NULL is a no-op. */
+void grass_destroy(grass_ctx* ctx);
+
+/* Message of the last failed call on ctx (ctx == NULL: last failed
+ * grass_create / context-free helper on this thread).  Never NULL. */
+const char* grass_last_error(const grass_ctx* ctx);
+
+/* Waits for all work the context enqueued; surfaces the sticky non-finite
+ * flag (GRASS_E_NONFINITE) and asynchronous CUDA errors. */
+grass_status grass_sync(grass_ctx* ctx);
+
+/* Eq. 2 inner term (probing): for each listed layer,
+ * ss_l = sum_i g_i^2 accumulated in fp64 over a FIXED tile decomposition
+ * (bit-reproducible, independent of grid size), r_l = sqrt(ss_l / N_p(l)),
+ * window S_l += r_l, c_l += 1.  No optimizer state is read or written (R14).
+ *   layer_ids: host [n] distinct ids in [0, N_L).
+ *   grads:     host [n] array of DEVICE pointers, grads[i] = N_p(layer_ids[i])
+ *              fp32, 16-byte aligned.  World > 1: this rank's local gradient;
+ *              the norm is of the DP average (R9).
+ *   stream:    cudaStream_t.  Asynchronous; nothing syncs the host. */
+grass_status grass_mgn_accumulate(grass_ctx* ctx, const int32_t* layer_ids, int32_t n,
+                                  const float* const* grads, void* stream);
+
+/* Eq. 2 window mean w_l = S_l / c_l (R4), then: first call m_l = w_l (R8);
+ * later calls m_l = alpha*w_l + (1-alpha)*m_l for observed layers, unobserved
+ * (frozen) layers keep m_l (Eq. 4); window reset; then Eq. 3
+ * p = softmax(m~/tau) (R3) according to cfg.policy.  Synchronises once (waits
+ * for the accumulations in flight and reads N_L * 16 bytes).
+ *   probs_out: host [N_L] or NULL.
+ * Errors: GRASS_E_STATE if no layer was observed in the window,
+ * GRASS_E_NONFINITE. */
+grass_status grass_update_probs(grass_ctx* ctx, double* probs_out);
+
+/* gamma distinct layer ids drawn without replacement, sequentially
+ * proportional to p with renormalisation (R6), with the counter-based
+ * SplitMix64 RNG keyed by (cfg.seed, period, draw index) (R7).  Pure host;
+ * bit-exact contract.  ids_out in DRAW order.
+ *   probs: host [N_L] or NULL (= the context's current probabilities).
+ *   ids_out: host [gamma]. */
+grass_status grass_sample_layers(grass_ctx* ctx, const double* probs, uint64_t period,
+                                 int32_t* ids_out);
+
+/* One AdamW step (R1, R2) on every listed layer, in ascending layer order
+ * (R12), in place, fused single-pass with the Eq. 2 norm of the same gradient
+ * (which feeds the MGN window exactly as grass_mgn_accumulate does):
+ *   t_l += 1; theta = theta*(1 - lr*wd); m = b1*m + (1-b1)*g;
+ *   v = b2*v + (1-b2)*g^2; theta -= lr/(1-b1^t) * m / (sqrt(v)/sqrt(1-b2^t) + eps)
+ * With cfg.offload the layer's m/v stream from pinned host memory through the
+ * device staging ring and back; results are bit-identical
+ * to offload = 0 (R12).  World > 1: gradients are reduce-scattered (average)
+ * over NCCL, each rank updates its element shard with its own m/v slice, and
+ * parameters are all-gathered back into params[i].
+ *   params: host [n] array of DEVICE pointers (fp32, N_p each, updated in place)
+ *   grads:  host [n] array of DEVICE pointers (fp32, N_p each, read only)
+ *   lr:     learning rate eta for this step (> 0 or == 0)
+ * Stream-ordered on `stream`: when `stream` reaches this point the update, the
+ * write-back of m/v to host and the MGN accumulation have all completed. */
+grass_status grass_step_layers(grass_ctx* ctx, const int32_t* layer_ids, int32_t n,
+                               float* const* params, const float* const* grads, float lr,
+                               void* stream);
+
+/* Copies this rank's m/v shard of `layer` into host buffers m_out/v_out
+ * (count = the shard length, grass_shard_range) and its step count; any
+ * pointer may be NULL.  Synchronises the context first. */
+grass_status grass_read_state(grass_ctx* ctx, int32_t layer, float* m_out, float* v_out,
+                              int64_t* t_out);
+
+/* Overwrites this rank's m/v shard and step count of `layer` (checkpoint
+ * restore).  Synchronises the context first. */
+grass_status grass_write_state(grass_ctx* ctx, int32_t layer, const float* m_in,
+                               const float* v_in, int64_t t_in);
+
+/* Introspection of the MGN state (host arrays [N_L], any may be NULL):
+ * committed m_l, window sum S_l, window count c_l, last fp64 squared norm of
+ * layer l (DP-averaged gradient when world > 1), current probabilities.
+ * Synchronises the context first. */
+grass_status grass_get_mgn(grass_ctx* ctx, double* m_out, double* window_sum_out,
+                           int64_t* window_count_out, double* last_sqnorm_out,
+                           double* probs_out);
+
+/* Bytes of HBM this context owns (m/v, staging ring, MGN state, scratch). */
+int64_t grass_device_bytes(const grass_ctx* ctx);
+/* Bytes of pinned host memory this context owns. */
+int64_t grass_host_bytes(const grass_ctx* ctx);
+/* Number of kernel launches and NCCL calls this context has issued so far. */
+int64_t grass_launch_count(const grass_ctx* ctx);
+
+/* ----- context-free host helpers (no GPU needed; used by tests) ----------- */
+
+/* Elements per norm tile: the fixed decomposition unit of the fp64 norm. */
+int64_t grass_tile_elems(void);
+const char* grass_version(void);
+
+/* Standard SplitMix64 output of state x (R7). */
+uint64_t grass_splitmix64(uint64_t x);
+/* u in [0,1): (splitmix64(splitmix64(seed) ^ (period*2^16 + k)) >> 11) * 2^-53. */
+double grass_uniform(uint64_t seed, uint64_t period, uint32_t k);
+
+/* Eq. 3 with reading R3 on host fp64: p[i] for m[0..n). */
+grass_status grass_softmax_probs(const double* m, int32_t n, double tau, int32_t normalize,
+                                 double* p_out);
+
+/* The sampler of grass_sample_layers without a context. */
+grass_status grass_sample_from_probs(const double* p, int32_t n, int32_t gamma, uint64_t seed,
+                                     uint64_t period, int32_t* ids_out);
+
+/* Element shard of a layer of `numel` elements for `rank` of `world`: the
+ * contiguous range [offset, offset + count).  Requires numel % (4*world) == 0
+ * when world > 1 (every rank's shard is equal and 16-byte aligned). */
+grass_status grass_shard_range(int64_t numel, int32_t world, int32_t rank, int64_t* offset,
+                               int64_t* count);
+
+/* Schedule decision for training step `step` (0-based). */
+int32_t grass_schedule_decision(int64_t step, int32_t T_p, int32_t T_s, int32_t T_u);
+
+/* Creates an NCCL unique id (128 bytes) on the calling host; rank 0 calls it
+ * and broadcasts the bytes to the other ranks (e.g. via a torch process group). */
+grass_status grass_nccl_get_unique_id(void* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRASS_H_ */

@@ -1,0 +1,305 @@
+"""Thin ctypes binding of libgrass.so (include/grass.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels / NCCL calls.  torch supplies device memory, streams and process
+groups.  There is NO fallback: if libgrass.so is missing or fails to load,
+every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Sequence
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgrass.so")
+
+OK, E_INVALID, E_STATE, E_CUDA, E_NCCL, E_OOM, E_NONFINITE = range(7)
+POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM = range(3)
+DECIDE_PROBE, DECIDE_COMMIT_RESAMPLE, DECIDE_RESAMPLE, DECIDE_CONTINUE = range(4)
+NCCL_ID_BYTES = 128
+
+_STATUS = {0: "GRASS_OK", 1: "GRASS_E_INVALID", 2: "GRASS_E_STATE", 3: "GRASS_E_CUDA",
+           4: "GRASS_E_NCCL", 5: "GRASS_E_OOM", 6: "GRASS_E_NONFINITE"}
+
+
+class GrassError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class GrassConfig(C.Structure):
+    _fields_ = [
+        ("n_layers", C.c_int32), ("layer_numel", C.POINTER(C.c_int64)), ("gamma", C.c_int32),
+        ("T_p", C.c_int32), ("T_s", C.c_int32), ("T_u", C.c_int32),
+        ("tau", C.c_double), ("alpha", C.c_double), ("normalize_mgn", C.c_int32),
+        ("policy", C.c_int32),
+        ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+        ("weight_decay", C.c_double), ("seed", C.c_uint64), ("device", C.c_int32),
+        ("offload", C.c_int32), ("overlap", C.c_int32), ("chunk_elems", C.c_int64),
+        ("ring_slots", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
+        ("nccl_unique_id", C.c_void_p),
+    ]
+
+
+_lib = None
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "grass_config_init": (C.c_int, [C.POINTER(GrassConfig)]),
+    "grass_create": (C.c_int, [C.POINTER(GrassConfig), C.POINTER(C.c_void_p)]),
+    "grass_destroy": (None, [C.c_void_p]),
+    "grass_last_error": (C.c_char_p, [C.c_void_p]),
+    "grass_sync": (C.c_int, [C.c_void_p]),
+    "grass_mgn_accumulate": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32,
+                                       C.POINTER(C.c_void_p), C.c_void_p]),
+    "grass_update_probs": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    "grass_sample_layers": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_uint64,
+                                      C.POINTER(C.c_int32)]),
+    "grass_step_layers": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32,
+                                    C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_float,
+                                    C.c_void_p]),
+    "grass_read_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                   C.POINTER(C.c_int64)]),
+    "grass_write_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64]),
+    "grass_get_mgn": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                C.POINTER(C.c_double)]),
+    "grass_device_bytes": (C.c_int64, [C.c_void_p]),
+    "grass_host_bytes": (C.c_int64, [C.c_void_p]),
+    "grass_launch_count": (C.c_int64, [C.c_void_p]),
+    "grass_tile_elems": (C.c_int64, []),
+    "grass_version": (C.c_char_p, []),
+    "grass_splitmix64": (C.c_uint64, [C.c_uint64]),
+    "grass_uniform": (C.c_double, [C.c_uint64, C.c_uint64, C.c_uint32]),
+    "grass_softmax_probs": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_double, C.c_int32,
+                                      C.POINTER(C.c_double)]),
+    "grass_sample_from_probs": (C.c_int, [C.POINTER(C.c_double), C.c_int32, C.c_int32,
+                                          C.c_uint64, C.c_uint64, C.POINTER(C.c_int32)]),
+    "grass_shard_range": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int64)]),
+    "grass_schedule_decision": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, C.c_int32]),
+    "grass_nccl_get_unique_id": (C.c_int, [C.c_void_p]),
+}
+
+
+def lib() -> C.CDLL:
+    """Loads libgrass.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                              "(python -m paper_2604_07808_b200.build)")
+        h = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(h, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = h
+    return _lib
+
+
+def exported_symbols():
+    return sorted(_SIGS)
+
+
+def _check(status: int, ctx=None):
+    if status != OK:
+        msg = lib().grass_last_error(ctx)
+        raise GrassError(status, msg.decode() if msg else "")
+
+
+def _dbl(xs):
+    return (C.c_double * len(xs))(*[float(x) for x in xs])
+
+
+# ----------------------------------------------------------- context-free helpers
+def tile_elems() -> int:
+    return int(lib().grass_tile_elems())
+
+
+def splitmix64(x: int) -> int:
+    return int(lib().grass_splitmix64(x & ((1 << 64) - 1)))
+
+
+def uniform(seed: int, period: int, k: int) -> float:
+    return float(lib().grass_uniform(seed, period, k))
+
+
+def softmax_probs(m: Sequence[float], tau: float, normalize: bool = True):
+    out = (C.c_double * len(m))()
+    _check(lib().grass_softmax_probs(_dbl(m), len(m), tau, int(normalize), out))
+    return list(out)
+
+
+def sample_from_probs(p: Sequence[float], gamma: int, seed: int, period: int):
+    out = (C.c_int32 * gamma)()
+    _check(lib().grass_sample_from_probs(_dbl(p), len(p), gamma, seed, period, out))
+    return list(out)
+
+
+def shard_range(numel: int, world: int, rank: int):
+    off, cnt = C.c_int64(), C.c_int64()
+    _check(lib().grass_shard_range(numel, world, rank, C.byref(off), C.byref(cnt)))
+    return off.value, cnt.value
+
+
+def schedule_decision(step: int, T_p: int, T_s: int, T_u: int | None = None) -> int:
+    return int(lib().grass_schedule_decision(step, T_p, T_s, T_s if T_u is None else T_u))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    _check(lib().grass_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+# ------------------------------------------------------------------ context
+def _stream_ptr(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptrs(tensors):
+    arr = (C.c_void_p * len(tensors))()
+    for i, t in enumerate(tensors):
+        if not t.is_cuda or not t.is_contiguous() or t.dtype.itemsize != 4:
+            raise ValueError("layer buffers must be contiguous fp32 CUDA tensors")
+        arr[i] = t.data_ptr()
+    return arr
+
+
+class Grass:
+    """One GRASS hot-path context (one per process / GPU).
+
+    Parameters mirror ``grass_config`` (include/grass.h).  For world > 1 pass a
+    torch.distributed process group (any backend): rank 0 creates the NCCL id
+    and it is broadcast through the group.
+    """
+
+    def __init__(self, layer_numel: Sequence[int], gamma: int, *, T_p: int = 150, T_s: int = 25,
+                 T_u: int | None = None, tau: float = 1.0, alpha: float = 0.5,
+                 normalize_mgn: bool = True, policy: int = POLICY_ADAPTIVE, beta1: float = 0.9,
+                 beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0,
+                 seed: int = 1234, device: int = 0, offload: bool = False, overlap: bool = True,
+                 chunk_elems: int = 0, ring_slots: int = 0, rank: int = 0, world: int = 1,
+                 process_group=None):
+        L = lib()
+        self.layer_numel = [int(x) for x in layer_numel]
+        self.n_layers = len(self.layer_numel)
+        self.gamma = gamma
+        self._numel = (C.c_int64 * self.n_layers)(*self.layer_numel)
+        cfg = GrassConfig()
+        _check(L.grass_config_init(C.byref(cfg)))
+        cfg.n_layers = self.n_layers
+        cfg.layer_numel = self._numel
+        cfg.gamma = gamma
+        cfg.T_p, cfg.T_s, cfg.T_u = T_p, T_s, (T_s if T_u is None else T_u)
+        cfg.tau, cfg.alpha, cfg.normalize_mgn, cfg.policy = tau, alpha, int(normalize_mgn), policy
+        cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay = beta1, beta2, eps, weight_decay
+        cfg.seed = seed & ((1 << 64) - 1)
+        cfg.device = device
+        cfg.offload, cfg.overlap = int(offload), int(overlap)
+        cfg.chunk_elems, cfg.ring_slots = chunk_elems, ring_slots
+        cfg.rank, cfg.world = rank, world
+        self._uid = None
+        if world > 1:
+            import torch.distributed as dist
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=process_group)
+            self._uid = C.create_string_buffer(obj[0], NCCL_ID_BYTES)
+            cfg.nccl_unique_id = C.cast(self._uid, C.c_void_p)
+        self.cfg = cfg
+        self.rank, self.world = rank, world
+        h = C.c_void_p()
+        _check(L.grass_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+
+    # lifetime ---------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().grass_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # hot path ---------------------------------------------------------------
+    def mgn_accumulate(self, layer_ids: Sequence[int], grads, stream=None):
+        ids = (C.c_int32 * len(layer_ids))(*layer_ids)
+        _check(lib().grass_mgn_accumulate(self._h, ids, len(layer_ids), _ptrs(grads),
+                                          _stream_ptr(stream)), self._h)
+
+    def update_probs(self):
+        out = (C.c_double * self.n_layers)()
+        _check(lib().grass_update_probs(self._h, out), self._h)
+        return list(out)
+
+    def sample_layers(self, period: int, probs: Sequence[float] | None = None):
+        out = (C.c_int32 * self.gamma)()
+        p = _dbl(probs) if probs is not None else None
+        if probs is not None and len(probs) != self.n_layers:
+            raise ValueError("probs must have N_L entries")
+        _check(lib().grass_sample_layers(self._h, p, period, out), self._h)
+        return list(out)
+
+    def step_layers(self, layer_ids: Sequence[int], params, grads, lr: float, stream=None):
+        ids = (C.c_int32 * len(layer_ids))(*layer_ids)
+        _check(lib().grass_step_layers(self._h, ids, len(layer_ids), _ptrs(params), _ptrs(grads),
+                                       float(lr), _stream_ptr(stream)), self._h)
+
+    def sync(self):
+        _check(lib().grass_sync(self._h), self._h)
+
+    # state ------------------------------------------------------------------
+    def shard(self, layer: int):
+        return shard_range(self.layer_numel[layer], self.world, self.rank)
+
+    def read_state(self, layer: int):
+        import numpy as np
+        n = self.shard(layer)[1]
+        m = np.empty(n, np.float32)
+        v = np.empty(n, np.float32)
+        t = C.c_int64()
+        _check(lib().grass_read_state(self._h, layer, m.ctypes.data, v.ctypes.data, C.byref(t)), self._h)
+        return m, v, t.value
+
+    def write_state(self, layer: int, m, v, t: int):
+        import numpy as np
+        m = np.ascontiguousarray(m, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        n = self.shard(layer)[1]
+        if m.size != n or v.size != n:
+            raise ValueError("state size must equal the shard length")
+        _check(lib().grass_write_state(self._h, layer, m.ctypes.data, v.ctypes.data, t), self._h)
+
+    def get_mgn(self):
+        n = self.n_layers
+        m, S, ss, p = ((C.c_double * n)() for _ in range(4))
+        c = (C.c_int64 * n)()
+        _check(lib().grass_get_mgn(self._h, m, S, c, ss, p), self._h)
+        return {"m": list(m), "S": list(S), "c": list(c), "last_ss": list(ss), "probs": list(p)}
+
+    @property
+    def device_bytes(self) -> int:
+        return int(lib().grass_device_bytes(self._h))
+
+    @property
+    def host_bytes(self) -> int:
+        return int(lib().grass_host_bytes(self._h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().grass_launch_count(self._h))

@@ -1,0 +1,85 @@
+"""Builds libgrass.so in-tree for sm_100a (nvcc + g++; no torch extension).
+
+    python -m paper_2604_07808_b200.build      # or __graft_entry__.build()
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT = os.path.join(PKG, "libgrass.so")
+BUILD = os.path.join(ROOT, "build")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _cuda_home() -> str:
+    for c in (os.environ.get("CUDA_HOME"), "/usr/local/cuda"):
+        if c and os.path.exists(os.path.join(c, "bin", "nvcc")):
+            return c
+    nvcc = shutil.which("nvcc")
+    if nvcc:
+        return os.path.dirname(os.path.dirname(nvcc))
+    raise RuntimeError("nvcc not found")
+
+
+def _nccl_include() -> str:
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        inc = os.path.join(base, "nccl", "include")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    if os.path.exists("/usr/include/nccl.h"):
+        return "/usr/include"
+    raise RuntimeError("nccl.h not found")
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return r.stdout + r.stderr
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    cuda = _cuda_home()
+    nvcc = os.path.join(cuda, "bin", "nvcc")
+    srcs = sorted(os.listdir(CSRC))
+    deps = [os.path.join(CSRC, f) for f in srcs] + [os.path.join(ROOT, "include", "grass.h"), __file__]
+    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
+        return OUT
+    os.makedirs(BUILD, exist_ok=True)
+    inc = ["-I" + os.path.join(ROOT, "include"), "-I" + _nccl_include(), "-I" + os.path.join(cuda, "include")]
+    objs = []
+    log = []
+    for f in srcs:
+        src = os.path.join(CSRC, f)
+        obj = os.path.join(BUILD, f + ".o")
+        if f.endswith(".cu"):
+            log.append(_run([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
+                             "-Xptxas", "-v", "-Xcompiler", "-fPIC,-ffp-contract=off",
+                             *inc, "-c", src, "-o", obj], verbose))
+        elif f.endswith(".cpp"):
+            log.append(_run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall",
+                             *inc, "-c", src, "-o", obj], verbose))
+        else:
+            continue
+        objs.append(obj)
+    tmp = OUT + ".tmp"
+    _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
+          "-ldl", "-lpthread", "-lrt"], verbose)
+    os.replace(tmp, OUT)
+    with open(os.path.join(BUILD, "ptxas.log"), "w") as fh:
+        fh.write("\n".join(log))
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(verbose=True, force="--force" in sys.argv))

@@ -1,0 +1,777 @@
+// grass_api.cpp — the C ABI (include/grass.h): validation, context, the MGN
+// commit / EMA on host (fp64), the offload pipeline and the data-parallel
+// orchestration.  Compiled with -ffp-contract=off (host fp64 rounds as written).
+#include <cuda_runtime_api.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "comm.h"
+#include "grass_internal.h"
+
+using namespace grass;
+
+namespace {
+
+thread_local std::string g_thread_err;
+
+constexpr int64_t kDefaultChunk = 8ll << 20;  // 8 Mi elements = 32 MiB per moment
+constexpr int kDefaultSlots = 3;
+constexpr int64_t kAlignElems = 64;           // 256-byte alignment of every state slice
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+int64_t tiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
+
+}  // namespace
+
+struct grass_ctx {
+  grass_config cfg{};
+  int nl = 0;
+  std::vector<int64_t> numel, shard_off, shard_len, tiles, part_base;
+  int64_t max_shard = 0;
+
+  // device reduction / MGN state
+  DevState st{};
+  double* d_gather = nullptr;   // world x N_L fp64 (all-gathered shard partials)
+  float* d_gscratch = nullptr;  // world > 1: this rank's averaged-gradient shard
+
+  // optimizer state: this rank's shard of every layer
+  float* state_block = nullptr;  // device (resident) or pinned host (offload)
+  std::vector<float*> m, v;
+  std::vector<int64_t> t;
+
+  // offload ring
+  float* d_ring = nullptr;
+  int slots = 0;
+  int64_t chunk = 0;
+  int64_t ring_pos = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr, aux = nullptr;
+  std::vector<cudaEvent_t> ev_h2d, ev_comp, ev_free;
+  std::vector<char> slot_used;
+  std::vector<cudaEvent_t> ev_layer_done;  // last write-back of each layer
+  std::vector<char> layer_done_valid;
+
+  // outstanding stream-ordered work (for the synchronising calls)
+  std::vector<cudaEvent_t> ev_free_list, ev_pending;
+
+  // host MGN state (fp64)
+  std::vector<double> mgn, probs;
+  bool committed = false;
+
+  Comm comm;
+  bool has_comm = false;
+  int grid_update = 0, grid_norm = 0;
+  int64_t launches = 0, dev_bytes = 0, host_bytes = 0;
+  std::string err;
+
+  grass_status fail(grass_status s, const std::string& msg) {
+    err = msg;
+    return s;
+  }
+};
+
+namespace {
+
+#define CUDA_TRY(ctx, expr)                                                          \
+  do {                                                                               \
+    cudaError_t e_ = (expr);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return (ctx)->fail(e_ == cudaErrorMemoryAllocation ? GRASS_E_OOM : GRASS_E_CUDA, \
+                         std::string(#expr) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+grass_status set_thread_err(grass_status s, const std::string& msg) {
+  g_thread_err = msg;
+  return s;
+}
+
+cudaEvent_t take_event(grass_ctx* c) {
+  cudaEvent_t e = nullptr;
+  if (!c->ev_free_list.empty()) {
+    e = c->ev_free_list.back();
+    c->ev_free_list.pop_back();
+  } else if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+    return nullptr;
+  }
+  return e;
+}
+
+grass_status mark_pending(grass_ctx* c, cudaStream_t s) {
+  cudaEvent_t e = take_event(c);
+  if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
+  CUDA_TRY(c, cudaEventRecord(e, s));
+  c->ev_pending.push_back(e);
+  return GRASS_OK;
+}
+
+// Waits for everything the context enqueued; checks the sticky flag.
+grass_status drain(grass_ctx* c, bool check_flag) {
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  for (cudaEvent_t e : c->ev_pending) {
+    CUDA_TRY(c, cudaEventSynchronize(e));
+    c->ev_free_list.push_back(e);
+  }
+  c->ev_pending.clear();
+  if (c->h2d) CUDA_TRY(c, cudaStreamSynchronize(c->h2d));
+  if (c->d2h) CUDA_TRY(c, cudaStreamSynchronize(c->d2h));
+  if (check_flag) {
+    int flag = INT_MAX;
+    CUDA_TRY(c, cudaMemcpyAsync(&flag, c->st.flag, sizeof(int), cudaMemcpyDeviceToHost, c->aux));
+    CUDA_TRY(c, cudaStreamSynchronize(c->aux));
+    if (flag != INT_MAX) {
+      const int reset = INT_MAX;
+      CUDA_TRY(c, cudaMemcpyAsync(c->st.flag, &reset, sizeof(int), cudaMemcpyHostToDevice, c->aux));
+      CUDA_TRY(c, cudaStreamSynchronize(c->aux));
+      return c->fail(GRASS_E_NONFINITE,
+                     "non-finite gradient in layer " + std::to_string(flag) +
+                         " (its update of that step was applied; abort the step)");
+    }
+  }
+  return GRASS_OK;
+}
+
+grass_status validate_config(const grass_config* cfg, std::string* why) {
+  auto bad = [&](const char* m) {
+    *why = m;
+    return GRASS_E_INVALID;
+  };
+  if (!cfg) return bad("cfg is NULL");
+  if (cfg->n_layers < 1) return bad("n_layers must be >= 1");
+  if (!cfg->layer_numel) return bad("layer_numel is NULL");
+  for (int i = 0; i < cfg->n_layers; ++i)
+    if (cfg->layer_numel[i] < 1) return bad("every layer_numel must be >= 1");
+  if (cfg->gamma < 1 || cfg->gamma > cfg->n_layers) return bad("gamma must lie in [1, N_L]");
+  if (!(cfg->tau > 0.0) || !std::isfinite(cfg->tau)) return bad("tau must be positive");
+  if (!(cfg->alpha >= 0.0 && cfg->alpha <= 1.0)) return bad("alpha must lie in [0, 1]");
+  if (cfg->T_p < 0 || cfg->T_s < 1 || cfg->T_u < 1 || cfg->T_u % cfg->T_s != 0)
+    return bad("schedule needs T_p >= 0, T_s >= 1, T_u a positive multiple of T_s");
+  if (!(cfg->beta1 >= 0.0 && cfg->beta1 < 1.0) || !(cfg->beta2 >= 0.0 && cfg->beta2 < 1.0))
+    return bad("beta1, beta2 must lie in [0, 1)");
+  if (!(cfg->eps > 0.0) || !(cfg->weight_decay >= 0.0)) return bad("eps > 0, weight_decay >= 0");
+  if (cfg->policy < GRASS_POLICY_ADAPTIVE || cfg->policy > GRASS_POLICY_UNIFORM)
+    return bad("unknown policy");
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return bad("bad rank/world");
+  if (cfg->world > 1) {
+    if (!cfg->nccl_unique_id) return bad("world > 1 needs nccl_unique_id");
+    for (int i = 0; i < cfg->n_layers; ++i)
+      if (cfg->layer_numel[i] % (4 * (int64_t)cfg->world) != 0)
+        return bad("world > 1 needs every layer_numel divisible by 4*world");
+  }
+  if (cfg->offload) {
+    if (cfg->chunk_elems < 0 || cfg->chunk_elems % kTile != 0)
+      return bad("chunk_elems must be a non-negative multiple of grass_tile_elems()");
+    if (cfg->ring_slots < 0) return bad("ring_slots must be >= 0");
+  }
+  return GRASS_OK;
+}
+
+// Resolve, validate and order the layer list of a hot-path call.
+grass_status check_call(grass_ctx* c, const int32_t* ids, int32_t n, const void* const* p1,
+                        const void* const* p2, std::vector<int>* order) {
+  if (!ids || n < 1 || n > c->nl) return c->fail(GRASS_E_INVALID, "need 1 <= n <= N_L layer ids");
+  std::vector<char> seen(c->nl, 0);
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] < 0 || ids[i] >= c->nl) return c->fail(GRASS_E_INVALID, "layer id out of range");
+    if (seen[ids[i]]) return c->fail(GRASS_E_INVALID, "duplicate layer id");
+    seen[ids[i]] = 1;
+  }
+  for (const void* const* arr : {p1, p2}) {
+    if (arr == nullptr) continue;
+    for (int i = 0; i < n; ++i) {
+      const void* p = arr[i];
+      if (!p) return c->fail(GRASS_E_INVALID, "NULL buffer pointer");
+      if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+        return c->fail(GRASS_E_INVALID, "layer buffers must be 16-byte aligned");
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return c->fail(GRASS_E_INVALID, "not a CUDA pointer");
+      }
+      if (!(a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ||
+          a.device != c->cfg.device)
+        return c->fail(GRASS_E_INVALID, "layer buffers must be device memory on the context's GPU");
+    }
+  }
+  order->resize(n);
+  for (int i = 0; i < n; ++i) (*order)[i] = i;
+  std::sort(order->begin(), order->end(), [&](int a, int b) { return ids[a] < ids[b]; });
+  return GRASS_OK;
+}
+
+Batch make_batch(const grass_ctx* c, int32_t mode) {
+  Batch b;
+  std::memset(&b, 0, sizeof(b));
+  b.mode = mode;
+  b.beta1 = (float)c->cfg.beta1;
+  b.one_minus_beta1 = (float)(1.0 - c->cfg.beta1);
+  b.beta2 = (float)c->cfg.beta2;
+  b.one_minus_beta2 = (float)(1.0 - c->cfg.beta2);
+  b.eps = (float)c->cfg.eps;
+  return b;
+}
+
+void push_seg(Batch* b, const Seg& s) {
+  b->seg[b->nseg] = s;
+  b->tile_prefix[b->nseg + 1] = b->tile_prefix[b->nseg] + s.tiles;
+  b->nseg++;
+}
+
+grass_status flush(grass_ctx* c, Batch* b, bool update, cudaStream_t s) {
+  if (b->nseg == 0) return GRASS_OK;
+  CUDA_TRY(c, launch_fused(update, *b, c->st, update ? c->grid_update : c->grid_norm, s));
+  c->launches++;
+  const int32_t mode = b->mode;
+  *b = make_batch(c, mode);
+  return GRASS_OK;
+}
+
+// Seg for [off, off+n) of layer l's shard (off a multiple of kTile).
+Seg range_seg(const grass_ctx* c, int l, const float* g, int64_t off, int64_t n) {
+  Seg s;
+  std::memset(&s, 0, sizeof(s));
+  s.g = g + off;
+  s.n = n;
+  s.tiles = (int32_t)tiles_of(n);
+  s.layer = l;
+  s.layer_tiles = (int32_t)c->tiles[l];
+  s.part_layer_base = c->part_base[l];
+  s.part_index = c->part_base[l] + off / kTile;
+  s.layer_numel = c->numel[l];
+  return s;
+}
+
+void adam_scalars(const grass_ctx* c, int l, float lr, Seg* s) {
+  const double t = (double)c->t[l];
+  const double bc1 = 1.0 - std::pow(c->cfg.beta1, t);
+  const double bc2 = 1.0 - std::pow(c->cfg.beta2, t);
+  s->decay = (float)(1.0 - (double)lr * c->cfg.weight_decay);
+  s->step_size = (float)((double)lr / bc1);
+  s->inv_bc2_sqrt = (float)(1.0 / std::sqrt(bc2));
+}
+
+// All-gather the shard partials of this call's layers and finish the MGN
+// update with a fixed ascending-rank sum (world > 1).
+grass_status cross_rank_finish(grass_ctx* c, const int32_t* ids, const std::vector<int>& order,
+                               cudaStream_t s) {
+  const int n = (int)order.size();
+  if (!c->comm.all_gather_f64(c->st.shard_ss, c->d_gather, (size_t)n, s, &c->err))
+    return GRASS_E_NCCL;
+  c->launches++;
+  for (int j0 = 0; j0 < n; j0 += kMaxSeg) {
+    RankSumArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.world = c->cfg.world;
+    a.total_slots = n;
+    a.slot0 = j0;
+    a.n = std::min(kMaxSeg, n - j0);
+    for (int j = 0; j < a.n; ++j) {
+      a.layer[j] = ids[order[j0 + j]];
+      a.numel[j] = c->numel[a.layer[j]];
+    }
+    CUDA_TRY(c, launch_rank_sum(c->d_gather, a, c->st, s));
+    c->launches++;
+  }
+  return GRASS_OK;
+}
+
+// Offload pipeline for one layer range (Fig. 4): per chunk
+// HtoD(m,v) on h2d -> fused update on the caller stream -> DtoH(m,v) on d2h,
+// chained by events through a ring of device slots.  overlap = 0 runs the
+// three stages serially on the caller stream (Fig. 4 "vanilla").
+grass_status offload_layer(grass_ctx* c, int l, Seg base, float* theta, const float* g, float lr,
+                           int32_t mode, cudaStream_t s) {
+  const int64_t len = c->shard_len[l];
+  const bool overlap = c->cfg.overlap != 0;
+  float* hm = c->m[l];
+  float* hv = c->v[l];
+  if (overlap && c->layer_done_valid[l])  // previous write-back of this layer
+    CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, c->ev_layer_done[l], 0));
+  for (int64_t off = 0; off < len; off += c->chunk) {
+    const int64_t n = std::min(c->chunk, len - off);
+    const int slot = (int)(c->ring_pos++ % c->slots);
+    float* dm = c->d_ring + (int64_t)slot * 2 * c->chunk;
+    float* dv = dm + c->chunk;
+    const size_t bytes = (size_t)n * sizeof(float);
+    cudaStream_t sh = overlap ? c->h2d : s, sd = overlap ? c->d2h : s;
+    if (overlap && c->slot_used[slot]) CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_free[slot], 0));
+    CUDA_TRY(c, cudaMemcpyAsync(dm, hm + off, bytes, cudaMemcpyHostToDevice, sh));
+    CUDA_TRY(c, cudaMemcpyAsync(dv, hv + off, bytes, cudaMemcpyHostToDevice, sh));
+    if (overlap) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_h2d[slot], sh));
+      CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_h2d[slot], 0));
+    }
+    Seg sg = range_seg(c, l, g, off, n);
+    sg.theta = theta + off;
+    sg.m = dm;
+    sg.v = dv;
+    sg.decay = base.decay;
+    sg.step_size = base.step_size;
+    sg.inv_bc2_sqrt = base.inv_bc2_sqrt;
+    sg.out_slot = base.out_slot;
+    Batch b = make_batch(c, mode);
+    push_seg(&b, sg);
+    grass_status st = flush(c, &b, true, s);
+    if (st != GRASS_OK) return st;
+    if (overlap) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_comp[slot], s));
+      CUDA_TRY(c, cudaStreamWaitEvent(sd, c->ev_comp[slot], 0));
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(hm + off, dm, bytes, cudaMemcpyDeviceToHost, sd));
+    CUDA_TRY(c, cudaMemcpyAsync(hv + off, dv, bytes, cudaMemcpyDeviceToHost, sd));
+    if (overlap) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_free[slot], sd));
+      c->slot_used[slot] = 1;
+    }
+  }
+  (void)lr;
+  if (overlap) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_layer_done[l], c->d2h));
+    c->layer_done_valid[l] = 1;
+  }
+  return GRASS_OK;
+}
+
+void free_ctx(grass_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->cfg.device);
+  cudaDeviceSynchronize();
+  if (c->has_comm) c->comm.destroy();
+  auto dfree = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  dfree(c->st.partials);
+  dfree(c->st.counters);
+  dfree(c->st.S);
+  dfree(c->st.c);
+  dfree(c->st.last_ss);
+  dfree(c->st.flag);
+  dfree(c->st.shard_ss);
+  dfree(c->d_gather);
+  dfree(c->d_gscratch);
+  dfree(c->d_ring);
+  if (c->state_block) {
+    if (c->cfg.offload)
+      cudaFreeHost(c->state_block);
+    else
+      cudaFree(c->state_block);
+  }
+  for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free, &c->ev_layer_done, &c->ev_free_list,
+                  &c->ev_pending})
+    for (cudaEvent_t e : *v)
+      if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : {c->h2d, c->d2h, c->aux})
+    if (s) cudaStreamDestroy(s);
+  delete c;
+}
+
+grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
+  c->cfg = *cfg;
+  c->nl = cfg->n_layers;
+  c->numel.assign(cfg->layer_numel, cfg->layer_numel + cfg->n_layers);
+  c->cfg.layer_numel = nullptr;
+  c->cfg.nccl_unique_id = nullptr;
+  const int W = cfg->world;
+  c->shard_off.resize(c->nl);
+  c->shard_len.resize(c->nl);
+  c->tiles.resize(c->nl);
+  c->part_base.resize(c->nl);
+  int64_t parts = 0, state_elems = 0;
+  for (int l = 0; l < c->nl; ++l) {
+    shard_range(c->numel[l], W, cfg->rank, &c->shard_off[l], &c->shard_len[l]);
+    c->tiles[l] = tiles_of(c->shard_len[l]);
+    if (c->tiles[l] > INT32_MAX) return c->fail(GRASS_E_INVALID, "layer too large");
+    c->part_base[l] = parts;
+    parts += c->tiles[l];
+    state_elems += round_up(c->shard_len[l], kAlignElems);
+    c->max_shard = std::max(c->max_shard, c->shard_len[l]);
+  }
+  c->t.assign(c->nl, 0);
+  c->mgn.assign(c->nl, 0.0);
+  c->probs.assign(c->nl, 1.0 / c->nl);
+
+  CUDA_TRY(c, cudaSetDevice(cfg->device));
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  auto dalloc = [&](void** p, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess) {
+      c->dev_bytes += (int64_t)bytes;
+      e = cudaMemset(*p, 0, bytes);
+    }
+    return e;
+  };
+  CUDA_TRY(c, dalloc((void**)&c->st.partials, sizeof(double) * (size_t)std::max<int64_t>(parts, 1)));
+  CUDA_TRY(c, dalloc((void**)&c->st.counters, sizeof(unsigned) * c->nl));
+  CUDA_TRY(c, dalloc((void**)&c->st.S, sizeof(double) * c->nl));
+  CUDA_TRY(c, dalloc((void**)&c->st.c, sizeof(long long) * c->nl));
+  CUDA_TRY(c, dalloc((void**)&c->st.last_ss, sizeof(double) * c->nl));
+  CUDA_TRY(c, dalloc((void**)&c->st.flag, sizeof(int)));
+  CUDA_TRY(c, dalloc((void**)&c->st.shard_ss, sizeof(double) * c->nl));
+  const int flag0 = INT_MAX;
+  CUDA_TRY(c, cudaMemcpy(c->st.flag, &flag0, sizeof(int), cudaMemcpyHostToDevice));
+
+  // optimizer state (m, v) for this rank's shard of every layer, zeroed
+  const size_t state_bytes = sizeof(float) * 2 * (size_t)state_elems;
+  if (cfg->offload) {
+    CUDA_TRY(c, cudaHostAlloc((void**)&c->state_block, state_bytes, cudaHostAllocPortable));
+    c->host_bytes += (int64_t)state_bytes;
+    // zero in parallel (first touch also faults the pages in)
+    const int nt = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    const size_t per = (state_bytes + nt - 1) / nt;
+    for (int i = 0; i < nt; ++i) {
+      const size_t b0 = std::min(state_bytes, per * i), b1 = std::min(state_bytes, per * (i + 1));
+      th.emplace_back([=] { std::memset(reinterpret_cast<char*>(c->state_block) + b0, 0, b1 - b0); });
+    }
+    for (auto& x : th) x.join();
+  } else {
+    CUDA_TRY(c, dalloc((void**)&c->state_block, state_bytes));
+  }
+  c->m.resize(c->nl);
+  c->v.resize(c->nl);
+  int64_t o = 0;
+  for (int l = 0; l < c->nl; ++l) {
+    c->m[l] = c->state_block + o;
+    o += round_up(c->shard_len[l], kAlignElems);
+  }
+  for (int l = 0; l < c->nl; ++l) {
+    c->v[l] = c->state_block + o;
+    o += round_up(c->shard_len[l], kAlignElems);
+  }
+
+  if (cfg->offload) {
+    c->chunk = cfg->chunk_elems ? cfg->chunk_elems : kDefaultChunk;
+    c->chunk = std::min(c->chunk, round_up(c->max_shard, kTile));
+    c->slots = cfg->ring_slots ? cfg->ring_slots : kDefaultSlots;
+    CUDA_TRY(c, dalloc((void**)&c->d_ring, sizeof(float) * 2 * (size_t)c->chunk * c->slots));
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free}) {
+      v->assign(c->slots, nullptr);
+      for (auto& e : *v) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    c->slot_used.assign(c->slots, 0);
+    c->ev_layer_done.assign(c->nl, nullptr);
+    for (auto& e : c->ev_layer_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->layer_done_valid.assign(c->nl, 0);
+  }
+
+  if (W > 1) {
+    CUDA_TRY(c, dalloc((void**)&c->d_gather, sizeof(double) * (size_t)W * c->nl));
+    CUDA_TRY(c, dalloc((void**)&c->d_gscratch, sizeof(float) * (size_t)c->max_shard));
+    if (!c->comm.init(cfg->nccl_unique_id, cfg->rank, W, &c->err)) return GRASS_E_NCCL;
+    c->has_comm = true;
+  }
+  c->grid_update = fused_grid(true, cfg->device);
+  c->grid_norm = fused_grid(false, cfg->device);
+  if (c->grid_update < 1 || c->grid_norm < 1) return c->fail(GRASS_E_CUDA, "occupancy query failed");
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  return GRASS_OK;
+}
+
+}  // namespace
+
+// =========================== exported C ABI ================================
+extern "C" {
+
+grass_status grass_config_init(grass_config* cfg) {
+  if (!cfg) return set_thread_err(GRASS_E_INVALID, "cfg is NULL");
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->gamma = 2;
+  cfg->T_p = 150;
+  cfg->T_s = 25;
+  cfg->T_u = 25;
+  cfg->tau = 1.0;
+  cfg->alpha = 0.5;
+  cfg->normalize_mgn = 1;
+  cfg->policy = GRASS_POLICY_ADAPTIVE;
+  cfg->beta1 = 0.9;
+  cfg->beta2 = 0.999;
+  cfg->eps = 1e-8;
+  cfg->weight_decay = 0.0;
+  cfg->seed = 1234;
+  cfg->overlap = 1;
+  cfg->world = 1;
+  return GRASS_OK;
+}
+
+grass_status grass_create(const grass_config* cfg, grass_ctx** out) {
+  if (!out) return set_thread_err(GRASS_E_INVALID, "out is NULL");
+  *out = nullptr;
+  std::string why;
+  grass_status s = validate_config(cfg, &why);
+  if (s != GRASS_OK) return set_thread_err(s, why);
+  grass_ctx* c = nullptr;
+  try {
+    c = new grass_ctx();
+    s = create_impl(cfg, c);
+  } catch (const std::exception& e) {
+    s = GRASS_E_OOM;
+    if (c) c->err = e.what();
+  }
+  if (s != GRASS_OK) {
+    g_thread_err = c ? c->err : "allocation failed";
+    free_ctx(c);
+    return s;
+  }
+  *out = c;
+  return GRASS_OK;
+}
+
+void grass_destroy(grass_ctx* ctx) { free_ctx(ctx); }
+
+const char* grass_last_error(const grass_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_thread_err.c_str();
+}
+
+grass_status grass_sync(grass_ctx* ctx) {
+  if (!ctx) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  return drain(ctx, true);
+}
+
+grass_status grass_mgn_accumulate(grass_ctx* c, const int32_t* ids, int32_t n,
+                                  const float* const* grads, void* stream) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!grads) return c->fail(GRASS_E_INVALID, "grads is NULL");
+  std::vector<int> order;
+  grass_status s = check_call(c, ids, n, reinterpret_cast<const void* const*>(grads), nullptr, &order);
+  if (s != GRASS_OK) return s;
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (c->cfg.world == 1) {
+    Batch b = make_batch(c, kFinalizeMgn);
+    for (int i : order) {
+      if (b.nseg == kMaxSeg && (s = flush(c, &b, false, st)) != GRASS_OK) return s;
+      push_seg(&b, range_seg(c, ids[i], grads[i], 0, c->numel[ids[i]]));
+    }
+    if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
+  } else {
+    for (int j = 0; j < (int)order.size(); ++j) {
+      const int i = order[j], l = ids[i];
+      if (!c->comm.reduce_scatter_avg_f32(grads[i], c->d_gscratch, (size_t)c->shard_len[l], st, &c->err))
+        return GRASS_E_NCCL;
+      c->launches++;
+      Batch b = make_batch(c, kFinalizeShard);
+      Seg sg = range_seg(c, l, c->d_gscratch, 0, c->shard_len[l]);
+      sg.out_slot = j;
+      push_seg(&b, sg);
+      if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
+    }
+    if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+  }
+  return mark_pending(c, st);
+}
+
+grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, float* const* params,
+                               const float* const* grads, float lr, void* stream) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!params || !grads) return c->fail(GRASS_E_INVALID, "params/grads is NULL");
+  if (!(lr >= 0.0f) || !std::isfinite(lr)) return c->fail(GRASS_E_INVALID, "lr must be finite, >= 0");
+  std::vector<int> order;
+  grass_status s = check_call(c, ids, n, reinterpret_cast<const void* const*>(params),
+                              reinterpret_cast<const void* const*>(grads), &order);
+  if (s != GRASS_OK) return s;
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool sharded = c->cfg.world > 1;
+  const int32_t mode = sharded ? kFinalizeShard : kFinalizeMgn;
+  Batch b = make_batch(c, mode);
+  for (int j = 0; j < (int)order.size(); ++j) {
+    const int i = order[j], l = ids[i];
+    c->t[l] += 1;  // per-layer step count (R2); validated above, so this step happens
+    const int64_t off = c->shard_off[l], len = c->shard_len[l];
+    const float* g = grads[i];
+    if (sharded) {
+      if (!c->comm.reduce_scatter_avg_f32(grads[i], c->d_gscratch, (size_t)len, st, &c->err))
+        return GRASS_E_NCCL;
+      c->launches++;
+      g = c->d_gscratch;  // shard-local gradient: index 0 = element `off`
+    }
+    float* theta = params[i] + off;
+    if (c->cfg.offload) {
+      Seg base = range_seg(c, l, g, 0, len);
+      adam_scalars(c, l, lr, &base);
+      base.out_slot = j;
+      if ((s = offload_layer(c, l, base, theta, g, lr, mode, st)) != GRASS_OK) return s;
+    } else {
+      Seg sg = range_seg(c, l, g, 0, len);
+      sg.theta = theta;
+      sg.m = c->m[l];
+      sg.v = c->v[l];
+      sg.out_slot = j;
+      adam_scalars(c, l, lr, &sg);
+      if (b.nseg == kMaxSeg && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+      push_seg(&b, sg);
+      // world > 1 launches per layer: the shard gradient scratch is reused
+      if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+    }
+    if (sharded) {
+      if (!c->comm.all_gather_f32(params[i] + off, params[i], (size_t)len, st, &c->err))
+        return GRASS_E_NCCL;
+      c->launches++;
+    }
+  }
+  if ((s = flush(c, &b, true, st)) != GRASS_OK) return s;
+  if (sharded && (s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+  if (c->cfg.offload && c->cfg.overlap) {
+    // join: the caller stream reaches "done" only after every write-back
+    cudaEvent_t e = take_event(c);
+    if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
+    CUDA_TRY(c, cudaEventRecord(e, c->d2h));
+    CUDA_TRY(c, cudaStreamWaitEvent(st, e, 0));
+    c->ev_free_list.push_back(e);
+  }
+  return mark_pending(c, st);
+}
+
+grass_status grass_update_probs(grass_ctx* c, double* probs_out) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  grass_status s = drain(c, true);
+  if (s != GRASS_OK) return s;
+  std::vector<double> S(c->nl);
+  std::vector<long long> cnt(c->nl);
+  CUDA_TRY(c, cudaMemcpyAsync(S.data(), c->st.S, sizeof(double) * c->nl, cudaMemcpyDeviceToHost, c->aux));
+  CUDA_TRY(c, cudaMemcpyAsync(cnt.data(), c->st.c, sizeof(long long) * c->nl, cudaMemcpyDeviceToHost, c->aux));
+  CUDA_TRY(c, cudaStreamSynchronize(c->aux));
+  long long total = 0;
+  for (long long x : cnt) total += x;
+  if (total == 0) return c->fail(GRASS_E_STATE, "commit with zero observations in the window");
+  // Eq. 2 window mean (R4), first commit (R8) / Eq. 4 EMA (R5), retention of frozen layers
+  const double a = c->cfg.alpha;
+  for (int l = 0; l < c->nl; ++l) {
+    if (cnt[l] > 0) {
+      const double w = S[l] / (double)cnt[l];
+      c->mgn[l] = c->committed ? a * w + (1.0 - a) * c->mgn[l] : w;
+    } else if (!c->committed) {
+      c->mgn[l] = 0.0;
+    }
+  }
+  const bool first = !c->committed;
+  c->committed = true;
+  CUDA_TRY(c, cudaMemsetAsync(c->st.S, 0, sizeof(double) * c->nl, c->aux));
+  CUDA_TRY(c, cudaMemsetAsync(c->st.c, 0, sizeof(long long) * c->nl, c->aux));
+  CUDA_TRY(c, cudaStreamSynchronize(c->aux));
+  // Eq. 3 per policy
+  if (c->cfg.policy == GRASS_POLICY_UNIFORM) {
+    for (int l = 0; l < c->nl; ++l) c->probs[l] = 1.0 / c->nl;
+  } else if (c->cfg.policy == GRASS_POLICY_ADAPTIVE || first) {
+    softmax_probs(c->mgn.data(), c->nl, c->cfg.tau, c->cfg.normalize_mgn != 0, c->probs.data());
+  }
+  if (probs_out) std::memcpy(probs_out, c->probs.data(), sizeof(double) * c->nl);
+  return GRASS_OK;
+}
+
+grass_status grass_sample_layers(grass_ctx* c, const double* probs, uint64_t period, int32_t* ids_out) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!ids_out) return c->fail(GRASS_E_INVALID, "ids_out is NULL");
+  const double* p = probs ? probs : c->probs.data();
+  for (int l = 0; l < c->nl; ++l)
+    if (!(p[l] >= 0.0) || !std::isfinite(p[l])) return c->fail(GRASS_E_INVALID, "probs must be finite, >= 0");
+  sample_from_probs(p, c->nl, c->cfg.gamma, c->cfg.seed, period, ids_out);
+  return GRASS_OK;
+}
+
+grass_status grass_read_state(grass_ctx* c, int32_t layer, float* m_out, float* v_out, int64_t* t_out) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (layer < 0 || layer >= c->nl) return c->fail(GRASS_E_INVALID, "layer id out of range");
+  grass_status s = drain(c, false);
+  if (s != GRASS_OK) return s;
+  const size_t bytes = sizeof(float) * (size_t)c->shard_len[layer];
+  if (c->cfg.offload) {
+    if (m_out) std::memcpy(m_out, c->m[layer], bytes);
+    if (v_out) std::memcpy(v_out, c->v[layer], bytes);
+  } else {
+    if (m_out) CUDA_TRY(c, cudaMemcpy(m_out, c->m[layer], bytes, cudaMemcpyDeviceToHost));
+    if (v_out) CUDA_TRY(c, cudaMemcpy(v_out, c->v[layer], bytes, cudaMemcpyDeviceToHost));
+  }
+  if (t_out) *t_out = c->t[layer];
+  return GRASS_OK;
+}
+
+grass_status grass_write_state(grass_ctx* c, int32_t layer, const float* m_in, const float* v_in, int64_t t_in) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (layer < 0 || layer >= c->nl) return c->fail(GRASS_E_INVALID, "layer id out of range");
+  if (t_in < 0) return c->fail(GRASS_E_INVALID, "step count must be >= 0");
+  grass_status s = drain(c, false);
+  if (s != GRASS_OK) return s;
+  const size_t bytes = sizeof(float) * (size_t)c->shard_len[layer];
+  if (c->cfg.offload) {
+    if (m_in) std::memcpy(c->m[layer], m_in, bytes);
+    if (v_in) std::memcpy(c->v[layer], v_in, bytes);
+  } else {
+    if (m_in) CUDA_TRY(c, cudaMemcpy(c->m[layer], m_in, bytes, cudaMemcpyHostToDevice));
+    if (v_in) CUDA_TRY(c, cudaMemcpy(c->v[layer], v_in, bytes, cudaMemcpyHostToDevice));
+  }
+  c->t[layer] = t_in;
+  return GRASS_OK;
+}
+
+grass_status grass_get_mgn(grass_ctx* c, double* m_out, double* S_out, int64_t* c_out,
+                           double* ss_out, double* probs_out) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  grass_status s = drain(c, false);
+  if (s != GRASS_OK) return s;
+  if (S_out) CUDA_TRY(c, cudaMemcpy(S_out, c->st.S, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));
+  if (c_out) {
+    std::vector<long long> tmp(c->nl);
+    CUDA_TRY(c, cudaMemcpy(tmp.data(), c->st.c, sizeof(long long) * c->nl, cudaMemcpyDeviceToHost));
+    for (int l = 0; l < c->nl; ++l) c_out[l] = tmp[l];
+  }
+  if (ss_out) CUDA_TRY(c, cudaMemcpy(ss_out, c->st.last_ss, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));
+  if (m_out) std::memcpy(m_out, c->mgn.data(), sizeof(double) * c->nl);
+  if (probs_out) std::memcpy(probs_out, c->probs.data(), sizeof(double) * c->nl);
+  return GRASS_OK;
+}
+
+int64_t grass_device_bytes(const grass_ctx* c) { return c ? c->dev_bytes : 0; }
+int64_t grass_host_bytes(const grass_ctx* c) { return c ? c->host_bytes : 0; }
+int64_t grass_launch_count(const grass_ctx* c) { return c ? c->launches : 0; }
+
+int64_t grass_tile_elems(void) { return kTile; }
+const char* grass_version(void) { return "grass-b200 1.0 (sm_100a)"; }
+uint64_t grass_splitmix64(uint64_t x) { return splitmix64(x); }
+double grass_uniform(uint64_t seed, uint64_t period, uint32_t k) { return uniform01(seed, period, k); }
+
+grass_status grass_softmax_probs(const double* m, int32_t n, double tau, int32_t normalize, double* p_out) {
+  if (!m || !p_out || n < 1) return set_thread_err(GRASS_E_INVALID, "bad arguments");
+  if (!(tau > 0.0)) return set_thread_err(GRASS_E_INVALID, "tau must be positive");
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(m[i]) || m[i] < 0.0) return set_thread_err(GRASS_E_INVALID, "m must be finite, >= 0");
+  softmax_probs(m, n, tau, normalize != 0, p_out);
+  return GRASS_OK;
+}
+
+grass_status grass_sample_from_probs(const double* p, int32_t n, int32_t gamma, uint64_t seed,
+                                     uint64_t period, int32_t* ids_out) {
+  if (!p || !ids_out || n < 1) return set_thread_err(GRASS_E_INVALID, "bad arguments");
+  if (gamma < 1 || gamma > n) return set_thread_err(GRASS_E_INVALID, "gamma must lie in [1, N_L]");
+  for (int i = 0; i < n; ++i)
+    if (!(p[i] >= 0.0) || !std::isfinite(p[i])) return set_thread_err(GRASS_E_INVALID, "probs must be finite, >= 0");
+  sample_from_probs(p, n, gamma, seed, period, ids_out);
+  return GRASS_OK;
+}
+
+grass_status grass_shard_range(int64_t numel, int32_t world, int32_t rank, int64_t* offset, int64_t* count) {
+  if (!offset || !count) return set_thread_err(GRASS_E_INVALID, "NULL output");
+  if (!shard_range(numel, world, rank, offset, count))
+    return set_thread_err(GRASS_E_INVALID, "numel must be >= 1 (and divisible by 4*world when world > 1)");
+  return GRASS_OK;
+}
+
+int32_t grass_schedule_decision(int64_t step, int32_t T_p, int32_t T_s, int32_t T_u) {
+  if (step < 0 || T_s < 1) return -1;
+  return schedule_decision(step, T_p, T_s, T_u);
+}
+
+grass_status grass_nccl_get_unique_id(void* out) {
+  if (!out) return set_thread_err(GRASS_E_INVALID, "out is NULL");
+  std::string err;
+  if (!nccl_unique_id(out, &err)) return set_thread_err(GRASS_E_NCCL, err);
+  return GRASS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// grass_internal.h — shared declarations of the GRASS B200 library (not ABI).
+#pragma once
+#include <cstdint>
+
+#include "../../include/grass.h"
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#else
+#include <cuda_runtime_api.h>
+#endif
+
+namespace grass {
+
+// ----- fixed norm decomposition -------------------------------------------
+// A layer (or layer shard) is cut into tiles of kTile elements.  Each tile's
+// squared-norm partial is computed by ONE thread block with a fixed
+// thread->element map and a fixed fp64 reduction tree, and the per-layer total
+// is the fixed-order sum of its tile partials.  The result therefore depends
+// only on the data, never on the grid size, SM count or launch split
+// (offload chunks are whole tiles).
+constexpr int kThreads = 256;                  // threads per block
+constexpr int kVec = 4;                        // fp32 per 128-bit access
+constexpr int kUnroll = 4;                     // 128-bit accesses per array per thread per tile
+constexpr int64_t kTile = (int64_t)kThreads * kVec * kUnroll;  // 4096 elements
+constexpr int kMaxSeg = 64;                    // segments per launch
+
+enum FinalizeMode : int32_t { kFinalizeMgn = 0, kFinalizeShard = 1 };
+
+// One contiguous range of one layer processed by a launch.
+struct Seg {
+  float* theta;            // params (UPDATE) — range start
+  const float* g;          // gradient — range start
+  float* m;                // first moment — range start (HBM or staging slot)
+  float* v;                // second moment — range start
+  int64_t n;               // valid elements in this range
+  int64_t part_index;      // index into partials of this range's first tile
+  int64_t part_layer_base; // index into partials of the layer's tile 0
+  int64_t layer_numel;     // N_p(l), the TRUE count (R10)
+  int32_t tiles;           // ceil(n / kTile)
+  int32_t layer_tiles;     // tiles of the whole layer (shard) this step
+  int32_t layer;           // layer id
+  int32_t out_slot;        // kFinalizeShard: slot in shard_ss
+  float decay;             // 1 - lr*wd           (fp64 on host, rounded once)
+  float step_size;         // lr / (1 - b1^t)
+  float inv_bc2_sqrt;      // 1 / sqrt(1 - b2^t)
+  float pad_;
+};
+
+struct Batch {
+  Seg seg[kMaxSeg];
+  int32_t tile_prefix[kMaxSeg + 1];
+  int32_t nseg;
+  int32_t mode;            // FinalizeMode
+  float beta1, one_minus_beta1, beta2, one_minus_beta2, eps;
+};
+
+// Device-resident MGN / reduction state (all arrays indexed by layer id unless noted).
+struct DevState {
+  double* partials;        // tile partials, all layers back to back
+  unsigned int* counters;  // tiles finished per layer (reset by the finalizer)
+  double* S;               // window sum of r_l   (Eq. 2)
+  long long* c;            // window count
+  double* last_ss;         // last squared norm
+  int* flag;               // smallest layer id with a non-finite norm, or INT_MAX
+  double* shard_ss;        // [slot] this rank's shard squared norm (world > 1)
+};
+
+// kernels.cu
+cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int grid,
+                         cudaStream_t s);
+// world > 1: per-layer total = fixed ascending-rank sum of the all-gathered
+// shard partials gathered[r * total_slots + slot], then the MGN update.
+struct RankSumArgs {
+  int32_t n;               // layers in this launch
+  int32_t world;
+  int32_t total_slots;     // row length of `gathered`
+  int32_t slot0;           // first slot of this launch
+  int32_t layer[kMaxSeg];
+  int64_t numel[kMaxSeg];
+};
+cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const DevState& st,
+                            cudaStream_t s);
+int fused_grid(bool update, int device);
+
+// host_policy.cpp
+uint64_t splitmix64(uint64_t x);
+double uniform01(uint64_t seed, uint64_t period, uint32_t k);
+bool softmax_probs(const double* m, int n, double tau, bool normalize, double* p);
+bool sample_from_probs(const double* p, int n, int gamma, uint64_t seed, uint64_t period,
+                       int32_t* ids);
+bool shard_range(int64_t numel, int world, int rank, int64_t* off, int64_t* cnt);
+int schedule_decision(int64_t step, int T_p, int T_s, int T_u);
+
+}  // namespace grass

@@ -1,0 +1,359 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Tolerances (BASELINE.json north_star):
+  * per-layer squared norms: |ss_gpu - ss_orc| <= 1e-6 * ss_orc
+    (exact equality for integer-valued gradients: every partial is an exact
+    integer in fp64);
+  * theta, m, v: |x_gpu - x_orc| <= 1e-5 * scale + 1e-30, where scale is the
+    magnitude of the operands of the final rounding step (theta: max(|theta'|,
+    |theta_in|); m: max(|m'|, |m_in|, (1-b1)|g|); v: |v'|).  With theta_in = 0
+    and wd = 0 (the "sensitivity" cases) this is a pure 1e-5 relative check
+    of the update itself;
+  * sampled ids: bit-exact given identical probabilities;
+  * offload on vs off: bit-identical.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_07808_b200 as G
+from oracle import grass_oracle as O
+from synth import grad_sigmas, integer_grad, layer_grad, layer_params, MODELS
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+B1, B2, EPS = 0.9, 0.999, 1e-8
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def assert_state_close(th, m, v, th_o, m_o, v_o, th_in, m_in, g, rtol=1e-5):
+    th, m, v = (np.asarray(x, np.float64) for x in (th, m, v))
+    th_o, m_o, v_o = (np.asarray(x, np.float64) for x in (th_o, m_o, v_o))
+    th_in, m_in, g = (np.asarray(x, np.float64) for x in (th_in, m_in, g))
+    s_th = np.maximum(np.abs(th_o), np.abs(th_in))
+    s_m = np.maximum.reduce([np.abs(m_o), np.abs(m_in), (1 - B1) * np.abs(g)])
+    s_v = np.abs(v_o)
+    for name, a, b, s in (("theta", th, th_o, s_th), ("m", m, m_o, s_m), ("v", v, v_o, s_v)):
+        err = np.abs(a - b)
+        bad = err > rtol * s + 1e-30
+        assert not bad.any(), (name, int(bad.sum()), float((err / np.maximum(s, 1e-300)).max()))
+
+
+def assert_ss_close(got, want, rtol=1e-6):
+    assert abs(got - want) <= rtol * abs(want), (got, want, abs(got - want) / max(abs(want), 1e-300))
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+# ------------------------------------------------------------ a1: Eq. 2 norms
+RAGGED = [1, 3, 4, 5, 4095, 4096, 4097, 3 * 4096 + 7, 65_536, 65_536 + 5, 1_000_003]
+
+
+def test_norms_ragged_sizes_vs_oracle():
+    numel = RAGGED
+    gr = G.Grass(numel, gamma=1)
+    sig = grad_sigmas(len(numel), 0)
+    grads = [layer_grad(n, l, sig[l], device=DEV) for l, n in enumerate(numel)]
+    gr.mgn_accumulate(list(range(len(numel))), grads)
+    st = gr.get_mgn()
+    for l, g in enumerate(grads):
+        ss = O.sq_norm(_np(g))
+        assert_ss_close(st["last_ss"][l], ss)
+        assert st["c"][l] == 1
+        assert st["S"][l] == pytest.approx(O.rms_norm(ss, numel[l]), rel=1e-6)
+
+
+def test_norms_integer_grads_exact():
+    numel = [65_536, 65_536 + 5, 2_000_000]
+    gr = G.Grass(numel, gamma=1)
+    grads = [integer_grad(n, l, device=DEV) for l, n in enumerate(numel)]
+    gr.mgn_accumulate([2, 0, 1], [grads[2], grads[0], grads[1]])
+    st = gr.get_mgn()
+    for l, g in enumerate(grads):
+        exact = int((_np(g).astype(np.int64) ** 2).sum())
+        assert st["last_ss"][l] == float(exact)
+        assert st["S"][l] == math.sqrt(exact / numel[l])     # Eq. 2 inner term, fp64 IEEE sqrt
+
+
+def test_norms_special_cases():
+    gr = G.Grass([4096, 8, 2], gamma=1)
+    z = torch.zeros(4096, device=DEV)
+    c = torch.full((8,), -0.75, device=DEV)
+    t = torch.tensor([3.0, 4.0], device=DEV)
+    gr.mgn_accumulate([0, 1, 2], [z, c, t])
+    st = gr.get_mgn()
+    assert st["S"] == [0.0, 0.75, 3.5355339059327378]        # SPEC.md:245-247 and constant g
+
+
+def test_norm_bit_reproducible_and_same_in_fused_update():
+    numel = [3 * 4096 + 7, 65_536]
+    gr = G.Grass(numel, gamma=2)
+    grads = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
+    params = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    gr.mgn_accumulate([0, 1], grads)
+    a = gr.get_mgn()["last_ss"]
+    gr.mgn_accumulate([1, 0], grads[::-1])
+    b = gr.get_mgn()["last_ss"]
+    gr.step_layers([0, 1], params, grads, 1e-3)
+    c = gr.get_mgn()["last_ss"]
+    assert a == b == c      # fixed tile decomposition: identical bits in every path
+
+
+# --------------------------------------------------- a5: fused norm + AdamW
+@pytest.mark.parametrize("wd,theta0,lr", [(0.0, "zero", 1e-3), (0.01, "randn", 3e-5),
+                                          (0.1, "randn", 0.1), (0.0, "randn", 1.0)])
+def test_step_layers_vs_oracle_multi_step(wd, theta0, lr):
+    numel = [65_536, 4097, 3, 65_536 + 12]
+    gr = G.Grass(numel, gamma=2, weight_decay=wd)
+    sig = grad_sigmas(len(numel), 1)
+    params = [(torch.zeros(n, device=DEV) if theta0 == "zero" else layer_params(n, l, device=DEV))
+              for l, n in enumerate(numel)]
+    m_o = [np.zeros(n, np.float32) for n in numel]
+    v_o = [np.zeros(n, np.float32) for n in numel]
+    for step in range(6):
+        ids = [[0, 1], [3, 2], [1, 3], [0, 2], [2, 1], [3, 0]][step]
+        grads = [layer_grad(numel[l], l, sig[l] * (1 + step), step=step, device=DEV) for l in ids]
+        th_in = [_np(params[l]).copy() for l in ids]
+        gr.step_layers(ids, [params[l] for l in ids], grads, lr)
+        for k, l in enumerate(ids):
+            m_gpu, v_gpu, t = gr.read_state(l)
+            # oracle re-seeded from the GPU's previous state
+            th_o, m1, v1 = O.adamw_step(th_in[k], m_o[l], v_o[l], _np(grads[k]), t, float(np.float32(lr)),
+                                        B1, B2, EPS, wd)
+            assert_state_close(_np(params[l]), m_gpu, v_gpu, th_o, m1, v1, th_in[k], m_o[l], _np(grads[k]))
+            m_o[l], v_o[l] = m_gpu, v_gpu
+        st = gr.get_mgn()
+        for k, l in enumerate(ids):
+            assert_ss_close(st["last_ss"][l], O.sq_norm(_np(grads[k])))
+
+
+def test_step_layers_drift_100_steps_without_reseeding():
+    numel = [8192 + 3, 4096]
+    lr, wd = 1e-3, 0.01
+    gr = G.Grass(numel, gamma=2, weight_decay=wd)
+    params = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    th = [_np(p).copy() for p in params]
+    m = [np.zeros(n, np.float32) for n in numel]
+    v = [np.zeros(n, np.float32) for n in numel]
+    for step in range(100):
+        grads = [layer_grad(n, l, 1e-3, step=step, device=DEV) for l, n in enumerate(numel)]
+        gr.step_layers([0, 1], params, grads, lr)
+        for l in range(2):
+            th[l], m[l], v[l] = O.adamw_step(th[l], m[l], v[l], _np(grads[l]), step + 1,
+                                             float(np.float32(lr)), B1, B2, EPS, wd)
+    for l in range(2):
+        mg, vg, t = gr.read_state(l)
+        assert t == 100
+        # drift bound: fp32 rounding ~6e-8/step accumulates far below 1e-5
+        assert_state_close(_np(params[l]), mg, vg, th[l], m[l], v[l], th[l], m[l], _np(grads[l]))
+
+
+def test_zero_grad_zero_state_is_identity_on_theta():
+    gr = G.Grass([4096], gamma=1)
+    p = layer_params(4096, 0, device=DEV)
+    p0 = p.clone()
+    gr.step_layers([0], [p], [torch.zeros(4096, device=DEV)], 0.1)
+    assert torch.equal(p, p0)
+    m, v, t = gr.read_state(0)
+    assert t == 1 and not m.any() and not v.any()
+
+
+# ------------------------------------------------ a6: offload bit-identity
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("slots", [1, 2, 3])
+def test_offload_bit_identical_to_resident(overlap, slots):
+    numel = [5 * 4096 + 17, 12 * 4096, 4096, 7]
+    sig = grad_sigmas(4, 3)
+    ctxs = [G.Grass(numel, gamma=2, weight_decay=0.01),
+            G.Grass(numel, gamma=2, weight_decay=0.01, offload=True, overlap=overlap,
+                    chunk_elems=2 * 4096, ring_slots=slots)]
+    params = [[layer_params(n, l, device=DEV) for l, n in enumerate(numel)] for _ in ctxs]
+    for step in range(5):
+        ids = [[0, 1], [1, 2], [3, 0], [0, 1], [2, 3]][step]
+        grads = [layer_grad(numel[l], l, sig[l], step=step, device=DEV) for l in ids]
+        for gr, ps in zip(ctxs, params):
+            gr.step_layers(ids, [ps[l] for l in ids], grads, 1e-3)
+    torch.cuda.synchronize()
+    for l in range(4):
+        assert torch.equal(params[0][l], params[1][l]), l
+        a, b = ctxs[0].read_state(l), ctxs[1].read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+    assert ctxs[0].get_mgn()["S"] == ctxs[1].get_mgn()["S"]
+
+
+def test_offload_under_stream_jitter():
+    # random-length busy kernels on the caller stream between steps must not
+    # change the result
+    numel = [9 * 4096 + 1, 9 * 4096 + 1]
+    ref = G.Grass(numel, gamma=2)
+    off = G.Grass(numel, gamma=2, offload=True, chunk_elems=4096, ring_slots=2)
+    p_ref = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    p_off = [p.clone() for p in p_ref]
+    s = torch.cuda.Stream()
+    rng = np.random.default_rng(0)
+    junk = torch.empty(1 << 22, device=DEV)
+    for step in range(8):
+        grads = [layer_grad(n, l, 1e-3, step=step, device=DEV) for l, n in enumerate(numel)]
+        ref.step_layers([0, 1], p_ref, grads, 1e-2)
+        with torch.cuda.stream(s):
+            s.wait_stream(torch.cuda.current_stream())
+            for _ in range(int(rng.integers(0, 4))):
+                junk.mul_(1.0001).add_(0.5)
+            off.step_layers([1, 0], [p_off[1], p_off[0]], [grads[1], grads[0]], 1e-2, stream=s)
+        torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    for l in range(2):
+        assert torch.equal(p_ref[l], p_off[l])
+
+
+# -------------------------------------------- a2-a4: whole path vs oracle
+def test_full_schedule_tiny_config_vs_oracle():
+    """configs[0]: 4 layers x 65,536 fp32, gamma = 2, fixed seed; probing,
+    commit, probabilities, sampling, adaptive steps and a second commit."""
+    numel = [65_536] * 4
+    T_p, T_s, lr, seed = 3, 2, 3e-5, 1234
+    gr = G.Grass(numel, gamma=2, T_p=T_p, T_s=T_s, seed=seed)
+    orc = O.GrassOracle(numel, gamma=2, seed=seed)
+    sig = grad_sigmas(4, 0)
+    params = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    ids = None
+    for step in range(T_p + 3 * T_s):
+        d = O.schedule_decision(step, T_p, T_s)
+        assert G.schedule_decision(step, T_p, T_s) == {"probe": 0, "commit+resample": 1,
+                                                       "resample": 2, "continue": 3}[d]
+        if "commit" in d:
+            p_gpu = gr.update_probs()
+            p_orc = orc.update_probs()
+            assert p_gpu == pytest.approx(p_orc, rel=1e-9)
+            assert abs(math.fsum(p_gpu) - 1) < 1e-12
+            st = gr.get_mgn()
+            assert st["m"] == pytest.approx(orc.mgn.m, rel=1e-7)
+        if "resample" in d:
+            period = (step - T_p) // T_s
+            ids = gr.sample_layers(period)
+            assert ids == O.sample_layers(p_gpu, 2, seed, period)    # bit-exact given the same p
+            assert ids == gr.sample_layers(period, p_gpu)
+        if d == "probe":
+            grads = [layer_grad(65_536, l, sig[l], step=step, device=DEV) for l in range(4)]
+            gr.mgn_accumulate([0, 1, 2, 3], grads)
+            orc.accumulate([0, 1, 2, 3], [_np(g) for g in grads])
+            continue
+        grads = [layer_grad(65_536, l, sig[l], step=step, device=DEV) for l in ids]
+        th_in = [_np(params[l]).copy() for l in ids]
+        m_in = [orc.m[l].copy() for l in ids]
+        gr.step_layers(ids, [params[l] for l in ids], grads, lr)
+        host = [th.copy() for th in th_in]
+        orc.step_layers(ids, host, [_np(g) for g in grads], float(np.float32(lr)))
+        for k, l in enumerate(ids):
+            m_gpu, v_gpu, t = gr.read_state(l)
+            assert t == orc.t[l]
+            assert_state_close(_np(params[l]), m_gpu, v_gpu, host[k], orc.m[l], orc.v[l],
+                               th_in[k], m_in[k], _np(grads[k]))
+            # keep the oracle's state equal to the GPU's (re-seed)
+            orc.m[l], orc.v[l] = m_gpu, v_gpu
+    st = gr.get_mgn()
+    assert st["S"] == pytest.approx(orc.mgn.S, rel=1e-7)
+    assert st["c"] == orc.mgn.c
+
+
+@pytest.mark.parametrize("policy", [G.POLICY_STATIC, G.POLICY_UNIFORM])
+def test_policy_variants(policy):
+    numel = [4096] * 5
+    gr = G.Grass(numel, gamma=2, policy=policy)
+    gs = [layer_grad(4096, l, 10.0 ** (-l), device=DEV) for l in range(5)]
+    gr.mgn_accumulate(list(range(5)), gs)
+    p1 = gr.update_probs()
+    gr.mgn_accumulate([4], [gs[0] * 100])
+    p2 = gr.update_probs()
+    if policy == G.POLICY_UNIFORM:
+        assert p1 == p2 == [0.2] * 5
+    else:   # GRASS*: probabilities from the probing MGN, never refreshed
+        assert p1 == p2 and p1 != [0.2] * 5
+    m = gr.get_mgn()["m"]
+    assert m[4] > 1e-2        # the MGN itself is still committed (EMA) under every policy
+
+
+# ------------------------------------------------------------ errors
+def test_nonfinite_gradient_reported_and_not_recorded():
+    gr = G.Grass([4096, 4096, 4096], gamma=2)
+    g = [layer_grad(4096, l, 1e-3, device=DEV) for l in range(3)]
+    g[2][17] = float("inf")
+    g[1][5] = float("nan")
+    gr.mgn_accumulate([0, 1, 2], g)
+    with pytest.raises(G.GrassError) as e:
+        gr.sync()
+    assert e.value.status == G.binding.E_NONFINITE and "layer 1" in str(e.value)
+    st = gr.get_mgn()
+    assert st["c"] == [1, 0, 0]
+    gr.sync()    # flag cleared after it was reported
+
+
+def test_invalid_calls_enqueue_nothing():
+    gr = G.Grass([4096, 4096], gamma=1)
+    g = torch.zeros(4096 + 4, device=DEV)
+    p = torch.zeros(4096, device=DEV)
+    with pytest.raises(G.GrassError):
+        gr.update_probs()                                  # zero observations
+    with pytest.raises(G.GrassError):
+        gr.mgn_accumulate([0, 0], [p, p])                  # duplicate id
+    with pytest.raises(G.GrassError):
+        gr.mgn_accumulate([2], [p])                        # unknown id
+    with pytest.raises(G.GrassError):
+        gr.mgn_accumulate([0], [g[1:]])                    # misaligned view
+    with pytest.raises((G.GrassError, ValueError)):
+        gr.mgn_accumulate([0], [torch.zeros(4096)])        # host memory
+    with pytest.raises(G.GrassError):
+        gr.step_layers([0], [p], [p], float("nan"))
+    st = gr.get_mgn()
+    assert st["c"] == [0, 0] and gr.read_state(0)[2] == 0
+
+
+def test_state_roundtrip():
+    gr = G.Grass([4096 + 4], gamma=1, offload=True, chunk_elems=4096)
+    m = np.arange(4100, dtype=np.float32)
+    v = m[::-1].copy()
+    gr.write_state(0, m, v, 41)
+    m2, v2, t = gr.read_state(0)
+    assert np.array_equal(m, m2) and np.array_equal(v, v2) and t == 41
+
+
+# --------------------------------------- full BASELINE sizes (sampled parity)
+def test_llama2_7b_layers_sampled_parity():
+    """Two LLaMA-2-7B decoder layers (N_p = 202,383,360) in the launch
+    configuration bench.py times: full norms vs the oracle, AdamW checked on
+    sampled elements (the oracle computes them one by one)."""
+    shape = MODELS["llama2-7b"]
+    n = shape.layer_numel
+    numel = [n] * 3
+    gr = G.Grass(numel, gamma=2, weight_decay=0.01)
+    sig = grad_sigmas(3, 0)
+    ids = [2, 0]
+    params = [layer_params(n, l, device=DEV, norm_numel=shape.norm_numel) for l in ids]
+    grads = [layer_grad(n, l, sig[l], device=DEV) for l in ids]
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([np.arange(4096), n - 1 - np.arange(4096),
+                                    rng.integers(0, n, 200_000)]))
+    ti = torch.from_numpy(idx).to(DEV)
+    th_in = [_np(p[ti]) for p in params]
+    g_s = [_np(g[ti]) for g in grads]
+    gr.step_layers(ids, params, grads, 3e-5)
+    st = gr.get_mgn()
+    for k, l in enumerate(ids):
+        assert_ss_close(st["last_ss"][l], O.sq_norm(_np(grads[k])))
+        th_o, m_o, v_o = O.adamw_step(th_in[k], np.zeros_like(th_in[k]), np.zeros_like(th_in[k]),
+                                      g_s[k], 1, float(np.float32(3e-5)), B1, B2, EPS, 0.01)
+        m_gpu, v_gpu, t = gr.read_state(l)
+        assert t == 1
+        assert_state_close(_np(params[k][ti]), m_gpu[idx], v_gpu[idx], th_o, m_o, v_o, th_in[k],
+                           np.zeros_like(th_in[k]), g_s[k])
