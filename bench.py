@@ -377,7 +377,7 @@ def run_grass(args, rank, world, local):
                        "parallelism": f"dp{world} element-sharded" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "grass_fused_kernel<true> (fused Eq.2 norm + AdamW)",
+                         "kernel": "grass_stream_kernel<true,1,2> (fused Eq.2 norm + AdamW, TMA bulk-copy ring)",
                          "kernel_ms": kernel_ms, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

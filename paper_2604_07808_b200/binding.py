@@ -12,7 +12,9 @@ import os
 from typing import Sequence
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgrass.so")
+# GRASS_LIB_PATH: developer override to load an A/B build variant of the same
+# library (tools/variants.py); the default is the in-tree product build.
+LIB_PATH = os.environ.get("GRASS_LIB_PATH") or os.path.join(_PKG, "libgrass.so")
 
 OK, E_INVALID, E_STATE, E_CUDA, E_NCCL, E_OOM, E_NONFINITE = range(7)
 POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM = range(3)

@@ -48,37 +48,41 @@ def _run(cmd, verbose):
     return r.stdout + r.stderr
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
+    """defines/out: developer A/B variants (e.g. tools/variants.py); the product is OUT."""
+    out_path = out or OUT
     cuda = _cuda_home()
     nvcc = os.path.join(cuda, "bin", "nvcc")
     srcs = sorted(os.listdir(CSRC))
     deps = [os.path.join(CSRC, f) for f in srcs] + [os.path.join(ROOT, "include", "grass.h"), __file__]
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
-        return OUT
-    os.makedirs(BUILD, exist_ok=True)
+    if not force and os.path.exists(out_path) and os.path.getmtime(out_path) >= max(os.path.getmtime(d) for d in deps):
+        return out_path
+    build_dir = BUILD if out is None else BUILD + "_" + os.path.basename(out_path).replace(".so", "")
+    os.makedirs(build_dir, exist_ok=True)
+    dflags = ["-D" + d for d in defines]
     inc = ["-I" + os.path.join(ROOT, "include"), "-I" + _nccl_include(), "-I" + os.path.join(cuda, "include")]
     objs = []
     log = []
     for f in srcs:
         src = os.path.join(CSRC, f)
-        obj = os.path.join(BUILD, f + ".o")
+        obj = os.path.join(build_dir, f + ".o")
         if f.endswith(".cu"):
             log.append(_run([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
                              "-Xptxas", "-v", "-Xcompiler", "-fPIC,-ffp-contract=off",
-                             *inc, "-c", src, "-o", obj], verbose))
+                             *dflags, *inc, "-c", src, "-o", obj], verbose))
         elif f.endswith(".cpp"):
             log.append(_run(["g++", "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall",
-                             *inc, "-c", src, "-o", obj], verbose))
+                             *dflags, *inc, "-c", src, "-o", obj], verbose))
         else:
             continue
         objs.append(obj)
-    tmp = OUT + ".tmp"
+    tmp = out_path + ".tmp"
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
           "-ldl", "-lpthread", "-lrt"], verbose)
-    os.replace(tmp, OUT)
-    with open(os.path.join(BUILD, "ptxas.log"), "w") as fh:
+    os.replace(tmp, out_path)
+    with open(os.path.join(build_dir, "ptxas.log"), "w") as fh:
         fh.write("\n".join(log))
-    return OUT
+    return out_path
 
 
 if __name__ == "__main__":

@@ -35,8 +35,12 @@ struct grass_ctx {
   std::vector<int64_t> numel, shard_off, shard_len, tiles, part_base;
   int64_t max_shard = 0;
 
-  // device reduction / MGN state
+  // device reduction / MGN state; S, c and flag live in ONE block so a commit
+  // is a single stream-ordered D2H copy into a pinned mirror.
   DevState st{};
+  void* d_mgn = nullptr;        // [S: N_L fp64][c: N_L int64][flag: int32]
+  void* h_mgn = nullptr;        // pinned host mirror of d_mgn
+  size_t mgn_bytes = 0;
   double* d_gather = nullptr;   // world x N_L fp64 (all-gathered shard partials)
   float* d_gscratch = nullptr;  // world > 1: this rank's averaged-gradient shard
 
@@ -109,30 +113,47 @@ grass_status mark_pending(grass_ctx* c, cudaStream_t s) {
   return GRASS_OK;
 }
 
-// Waits for everything the context enqueued; checks the sticky flag.
-grass_status drain(grass_ctx* c, bool check_flag) {
+// Non-finite flag encoding: 0 = none, else INT_MAX - (smallest layer id)
+// (kernels use atomicMax, so a memset to 0 clears it).
+int flag_layer(int enc) { return INT_MAX - enc; }
+
+// Stream-ordered snapshot of the MGN block: waits (on the aux stream) for all
+// work the context enqueued, copies S, c, flag to the pinned mirror, optionally
+// zeroes the window (S, c) and/or the flag, then synchronises once.
+grass_status fetch_mgn(grass_ctx* c, bool reset_window, bool take_flag) {
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
-  for (cudaEvent_t e : c->ev_pending) {
-    CUDA_TRY(c, cudaEventSynchronize(e));
-    c->ev_free_list.push_back(e);
-  }
+  for (cudaEvent_t e : c->ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(c->aux, e, 0));
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_mgn, c->d_mgn, c->mgn_bytes, cudaMemcpyDeviceToHost, c->aux));
+  if (reset_window) CUDA_TRY(c, cudaMemsetAsync(c->d_mgn, 0, 16 * (size_t)c->nl, c->aux));
+  if (take_flag) CUDA_TRY(c, cudaMemsetAsync(c->st.flag, 0, sizeof(int), c->aux));
+  CUDA_TRY(c, cudaStreamSynchronize(c->aux));
+  for (cudaEvent_t e : c->ev_pending) c->ev_free_list.push_back(e);
   c->ev_pending.clear();
+  return GRASS_OK;
+}
+
+const double* h_S(const grass_ctx* c) { return static_cast<const double*>(c->h_mgn); }
+const long long* h_c(const grass_ctx* c) {
+  return reinterpret_cast<const long long*>(static_cast<const char*>(c->h_mgn) + 8 * (size_t)c->nl);
+}
+int h_flag(const grass_ctx* c) {
+  return *reinterpret_cast<const int*>(static_cast<const char*>(c->h_mgn) + 16 * (size_t)c->nl);
+}
+
+grass_status report_flag(grass_ctx* c) {
+  const int enc = h_flag(c);
+  if (enc == 0) return GRASS_OK;
+  return c->fail(GRASS_E_NONFINITE, "non-finite gradient in layer " + std::to_string(flag_layer(enc)) +
+                                        " (its update of that step was applied; abort the step)");
+}
+
+// Waits for everything the context enqueued (incl. offload copy streams).
+grass_status drain(grass_ctx* c, bool take_flag) {
+  grass_status s = fetch_mgn(c, false, take_flag);
+  if (s != GRASS_OK) return s;
   if (c->h2d) CUDA_TRY(c, cudaStreamSynchronize(c->h2d));
   if (c->d2h) CUDA_TRY(c, cudaStreamSynchronize(c->d2h));
-  if (check_flag) {
-    int flag = INT_MAX;
-    CUDA_TRY(c, cudaMemcpyAsync(&flag, c->st.flag, sizeof(int), cudaMemcpyDeviceToHost, c->aux));
-    CUDA_TRY(c, cudaStreamSynchronize(c->aux));
-    if (flag != INT_MAX) {
-      const int reset = INT_MAX;
-      CUDA_TRY(c, cudaMemcpyAsync(c->st.flag, &reset, sizeof(int), cudaMemcpyHostToDevice, c->aux));
-      CUDA_TRY(c, cudaStreamSynchronize(c->aux));
-      return c->fail(GRASS_E_NONFINITE,
-                     "non-finite gradient in layer " + std::to_string(flag) +
-                         " (its update of that step was applied; abort the step)");
-    }
-  }
-  return GRASS_OK;
+  return take_flag ? report_flag(c) : GRASS_OK;
 }
 
 grass_status validate_config(const grass_config* cfg, std::string* why) {
@@ -346,10 +367,9 @@ void free_ctx(grass_ctx* c) {
   };
   dfree(c->st.partials);
   dfree(c->st.counters);
-  dfree(c->st.S);
-  dfree(c->st.c);
+  dfree(c->d_mgn);
   dfree(c->st.last_ss);
-  dfree(c->st.flag);
+  if (c->h_mgn) cudaFreeHost(c->h_mgn);
   dfree(c->st.shard_ss);
   dfree(c->d_gather);
   dfree(c->d_gscratch);
@@ -406,13 +426,15 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   };
   CUDA_TRY(c, dalloc((void**)&c->st.partials, sizeof(double) * (size_t)std::max<int64_t>(parts, 1)));
   CUDA_TRY(c, dalloc((void**)&c->st.counters, sizeof(unsigned) * c->nl));
-  CUDA_TRY(c, dalloc((void**)&c->st.S, sizeof(double) * c->nl));
-  CUDA_TRY(c, dalloc((void**)&c->st.c, sizeof(long long) * c->nl));
+  c->mgn_bytes = 16 * (size_t)c->nl + 8;
+  CUDA_TRY(c, dalloc(&c->d_mgn, c->mgn_bytes));
+  CUDA_TRY(c, cudaHostAlloc(&c->h_mgn, c->mgn_bytes, cudaHostAllocDefault));
+  std::memset(c->h_mgn, 0, c->mgn_bytes);
+  c->st.S = static_cast<double*>(c->d_mgn);
+  c->st.c = reinterpret_cast<long long*>(static_cast<char*>(c->d_mgn) + 8 * (size_t)c->nl);
+  c->st.flag = reinterpret_cast<int*>(static_cast<char*>(c->d_mgn) + 16 * (size_t)c->nl);
   CUDA_TRY(c, dalloc((void**)&c->st.last_ss, sizeof(double) * c->nl));
-  CUDA_TRY(c, dalloc((void**)&c->st.flag, sizeof(int)));
   CUDA_TRY(c, dalloc((void**)&c->st.shard_ss, sizeof(double) * c->nl));
-  const int flag0 = INT_MAX;
-  CUDA_TRY(c, cudaMemcpy(c->st.flag, &flag0, sizeof(int), cudaMemcpyHostToDevice));
 
   // optimizer state (m, v) for this rank's shard of every layer, zeroed
   const size_t state_bytes = sizeof(float) * 2 * (size_t)state_elems;
@@ -630,15 +652,18 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
 
 grass_status grass_update_probs(grass_ctx* c, double* probs_out) {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
-  grass_status s = drain(c, true);
+  // one stream-ordered snapshot: S, c, flag -> host; window and flag reset
+  grass_status s = fetch_mgn(c, true, true);
   if (s != GRASS_OK) return s;
-  std::vector<double> S(c->nl);
-  std::vector<long long> cnt(c->nl);
-  CUDA_TRY(c, cudaMemcpyAsync(S.data(), c->st.S, sizeof(double) * c->nl, cudaMemcpyDeviceToHost, c->aux));
-  CUDA_TRY(c, cudaMemcpyAsync(cnt.data(), c->st.c, sizeof(long long) * c->nl, cudaMemcpyDeviceToHost, c->aux));
-  CUDA_TRY(c, cudaStreamSynchronize(c->aux));
+  const double* S = h_S(c);
+  const long long* cnt = h_c(c);
   long long total = 0;
-  for (long long x : cnt) total += x;
+  for (int l = 0; l < c->nl; ++l) total += cnt[l];
+  if ((s = report_flag(c)) != GRASS_OK) {
+    // the window was consumed; restore it so the caller may retry after aborting the step
+    CUDA_TRY(c, cudaMemcpy(c->d_mgn, c->h_mgn, 16 * (size_t)c->nl, cudaMemcpyHostToDevice));
+    return s;
+  }
   if (total == 0) return c->fail(GRASS_E_STATE, "commit with zero observations in the window");
   // Eq. 2 window mean (R4), first commit (R8) / Eq. 4 EMA (R5), retention of frozen layers
   const double a = c->cfg.alpha;
@@ -652,9 +677,6 @@ grass_status grass_update_probs(grass_ctx* c, double* probs_out) {
   }
   const bool first = !c->committed;
   c->committed = true;
-  CUDA_TRY(c, cudaMemsetAsync(c->st.S, 0, sizeof(double) * c->nl, c->aux));
-  CUDA_TRY(c, cudaMemsetAsync(c->st.c, 0, sizeof(long long) * c->nl, c->aux));
-  CUDA_TRY(c, cudaStreamSynchronize(c->aux));
   // Eq. 3 per policy
   if (c->cfg.policy == GRASS_POLICY_UNIFORM) {
     for (int l = 0; l < c->nl; ++l) c->probs[l] = 1.0 / c->nl;
@@ -715,12 +737,9 @@ grass_status grass_get_mgn(grass_ctx* c, double* m_out, double* S_out, int64_t* 
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
-  if (S_out) CUDA_TRY(c, cudaMemcpy(S_out, c->st.S, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));
-  if (c_out) {
-    std::vector<long long> tmp(c->nl);
-    CUDA_TRY(c, cudaMemcpy(tmp.data(), c->st.c, sizeof(long long) * c->nl, cudaMemcpyDeviceToHost));
-    for (int l = 0; l < c->nl; ++l) c_out[l] = tmp[l];
-  }
+  if (S_out) std::memcpy(S_out, h_S(c), sizeof(double) * c->nl);
+  if (c_out)
+    for (int l = 0; l < c->nl; ++l) c_out[l] = h_c(c)[l];
   if (ss_out) CUDA_TRY(c, cudaMemcpy(ss_out, c->st.last_ss, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));
   if (m_out) std::memcpy(m_out, c->mgn.data(), sizeof(double) * c->nl);
   if (probs_out) std::memcpy(probs_out, c->probs.data(), sizeof(double) * c->nl);

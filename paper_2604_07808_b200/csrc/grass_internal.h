@@ -14,14 +14,14 @@ namespace grass {
 
 // ----- fixed norm decomposition -------------------------------------------
 // A layer (or layer shard) is cut into tiles of kTile elements.  Each tile's
-// squared-norm partial is computed by ONE thread block with a fixed
-// thread->element map and a fixed fp64 reduction tree, and the per-layer total
+// squared-norm partial is computed by the consumer warps of ONE CTA with a
+// fixed thread->element map and a fixed fp64 reduction tree (kernels.cu), and the per-layer total
 // is the fixed-order sum of its tile partials.  The result therefore depends
 // only on the data, never on the grid size, SM count or launch split
 // (offload chunks are whole tiles).
-constexpr int kThreads = 256;                  // threads per block
+constexpr int kThreads = 512;                  // consumer threads per tile (16 warps)
 constexpr int kVec = 4;                        // fp32 per 128-bit access
-constexpr int kUnroll = 4;                     // 128-bit accesses per array per thread per tile
+constexpr int kUnroll = 2;                     // 128-bit accesses per array per thread per tile
 constexpr int64_t kTile = (int64_t)kThreads * kVec * kUnroll;  // 4096 elements
 constexpr int kMaxSeg = 64;                    // segments per launch
 
@@ -62,7 +62,7 @@ struct DevState {
   double* S;               // window sum of r_l   (Eq. 2)
   long long* c;            // window count
   double* last_ss;         // last squared norm
-  int* flag;               // smallest layer id with a non-finite norm, or INT_MAX
+  int* flag;               // INT_MAX - (smallest layer id with a non-finite norm), 0 = none
   double* shard_ss;        // [slot] this rank's shard squared norm (world > 1)
 };
 

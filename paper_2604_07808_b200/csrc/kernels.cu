@@ -1,19 +1,30 @@
 // kernels.cu — sm_100a kernels of the GRASS hot path.
 //
-//   K1  grass_fused_kernel<false>: Eq. 2 squared norm only (probing,
+//   K1  grass_stream_kernel<false>: Eq. 2 squared norm only (probing,
 //       PAPER.md:111-113) — reads g once (4 B/param).
-//   K2  grass_fused_kernel<true>:  single-pass Eq. 2 norm + AdamW (DESIGN.md
+//   K2  grass_stream_kernel<true>:  single-pass Eq. 2 norm + AdamW (DESIGN.md
 //       R1/R2) of the trainable layers — reads g, theta, m, v,
 //       writes theta, m, v (28 B/param).
-//   K3  finalize (inside K1/K2, last block of each layer): fixed-order fp64 sum
-//       of the layer's tile partials, then S_l += sqrt(ss_l / N_p), c_l += 1
-//       (Eq. 2), or the shard value for the cross-rank sum.
+//   K3  finalize (inside K1/K2, by the CTA that completes a layer): fixed-order
+//       fp64 sum of the layer's tile partials, then S_l += sqrt(ss_l / N_p),
+//       c_l += 1 (Eq. 2), or the shard value for the rank sum.
 //   K4  grass_rank_sum_kernel (world > 1): ascending-rank fp64 sum of the
 //       all-gathered shard partials, then the same MGN update.
 //
-// Nothing here is a contraction: these kernels are HBM-bound streams (about
-// 0.5 flop/B), so they use 128-bit coalesced loads/stores with streaming
-// cache hints, enough bytes in flight per SM, and no tensor cores.
+// Nothing here is a contraction: K1/K2 are HBM-bound streams (~0.5 flop/B),
+// so there are no tensor cores.  The Blackwell-native part is the data
+// movement: a persistent, warp-specialised kernel (one CTA per SM) in which a
+// producer warp streams tiles HBM -> shared memory with cp.async.bulk (TMA
+// bulk copies, SASS UBLKCP) into a STAGES-deep ring guarded by mbarriers,
+// while 16 consumer warps compute and write results back with streaming
+// 128-bit stores.  The HBM pipe never drains on a block barrier.
+//
+// The tile partial (grass_internal.h) is a FIXED function of the tile's data:
+// consumer thread t owns elements (q*kThreads + t)*4 + j, j = 0..3, q = 0..
+// kUnroll-1; it keeps 4 fp64 accumulators acc_j (acc_j += g^2 in q order),
+// its value is (acc_0 + acc_1) + (acc_2 + acc_3); warps reduce with a fixed
+// shuffle tree and the 16 warp sums are added in ascending order.  Squares of
+// fp32 values are exact in fp64, so only the sums round.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -24,120 +35,123 @@
 namespace grass {
 namespace {
 
+constexpr int kConsumerWarps = kThreads / 32;  // 16
+constexpr int kStreamThreads = kThreads + 32;  // + 1 producer warp
+
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
   return x;  // lane 0 holds the fixed-tree sum
 }
 
-// Fixed-shape block reduction: warp trees, then warp 0 sums the 8 warp
-// results in ascending order.  Result valid in thread 0.
-__device__ __forceinline__ double block_sum(double x, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  x = warp_sum(x);
-  if (lane == 0) red[warp] = x;
-  __syncthreads();
-  double t = 0.0;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) t += red[w];
-  }
-  return t;
-}
-
 struct AdamScalars {
   float b1, omb1, b2, omb2, eps, decay, step, inv_bc2s;
 };
 
-// One element of AdamW (torch.optim.AdamW semantics, R1), fp32 storage.
+// One element of AdamW (torch.optim.AdamW semantics, R1), fp32 storage:
+//   theta1 = theta*(1 - lr*wd); m' = b1*m + (1-b1)*g; v' = b2*v + (1-b2)*g^2
+//   theta' = theta1 - lr/bc1 * m' / (sqrt(v')/sqrt(bc2) + eps)
+// sqrt and the division use the hardware approximations (MUFU; relative error
+// <= 2^-22, subnormals kept) instead of the multi-instruction IEEE sequences:
+// the error they add to theta' is < 1e-6 of the update, far inside the 1e-5
+// parity bar, and the IEEE sequences cost ~3% of K2's time (measured A/B).
 __device__ __forceinline__ void adamw1(float g, float& th, float& m, float& v,
                                        const AdamScalars& s) {
-  const float t1 = th * s.decay;                          // theta * (1 - lr*wd)
-  const float m1 = fmaf(s.b1, m, s.omb1 * g);             // b1*m + (1-b1)*g
-  const float v1 = fmaf(s.b2, v, (s.omb2 * g) * g);       // b2*v + (1-b2)*g^2
-  const float den = fmaf(__fsqrt_rn(v1), s.inv_bc2s, s.eps);  // sqrt(v)/sqrt(bc2) + eps
-  th = fmaf(-s.step, __fdiv_rn(m1, den), t1);             // - lr/bc1 * m/den
+  const float t1 = th * s.decay;
+  const float m1 = fmaf(s.b1, m, s.omb1 * g);
+  const float v1 = fmaf(s.b2, v, (s.omb2 * g) * g);
+#ifdef GRASS_IEEE_MATH
+  const float den = fmaf(__fsqrt_rn(v1), s.inv_bc2s, s.eps);
+  th = fmaf(-s.step, __fdiv_rn(m1, den), t1);
+#else
+  float sq;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(v1));
+  const float den = fmaf(sq, s.inv_bc2s, s.eps);
+  th = fmaf(-s.step, __fdividef(m1, den), t1);
+#endif
   m = m1;
   v = v1;
 }
 
-template <bool UPDATE>
-__device__ __forceinline__ double tile_body_full(const Seg& sg, int64_t base, const AdamScalars& s) {
-  // thread -> element map: e(u) = base + (u*kThreads + tid)*4, u = 0..kUnroll-1
-  const int64_t e0 = base + (int64_t)threadIdx.x * kVec;
-  constexpr int64_t kStride = (int64_t)kThreads * kVec;
-  float4 g4[kUnroll], t4[kUnroll], m4[kUnroll], v4[kUnroll];
-#pragma unroll
-  for (int u = 0; u < kUnroll; ++u)
-    g4[u] = __ldcs(reinterpret_cast<const float4*>(sg.g + e0 + u * kStride));
-  if (UPDATE) {
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      t4[u] = __ldcs(reinterpret_cast<const float4*>(sg.theta + e0 + u * kStride));
-      m4[u] = __ldcs(reinterpret_cast<const float4*>(sg.m + e0 + u * kStride));
-      v4[u] = __ldcs(reinterpret_cast<const float4*>(sg.v + e0 + u * kStride));
-    }
-  }
-  double acc = 0.0;
-#pragma unroll
-  for (int u = 0; u < kUnroll; ++u) {
-    acc = fma((double)g4[u].x, (double)g4[u].x, acc);
-    acc = fma((double)g4[u].y, (double)g4[u].y, acc);
-    acc = fma((double)g4[u].z, (double)g4[u].z, acc);
-    acc = fma((double)g4[u].w, (double)g4[u].w, acc);
-  }
-  if (UPDATE) {
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      adamw1(g4[u].x, t4[u].x, m4[u].x, v4[u].x, s);
-      adamw1(g4[u].y, t4[u].y, m4[u].y, v4[u].y, s);
-      adamw1(g4[u].z, t4[u].z, m4[u].z, v4[u].z, s);
-      adamw1(g4[u].w, t4[u].w, m4[u].w, v4[u].w, s);
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      __stcs(reinterpret_cast<float4*>(sg.theta + e0 + u * kStride), t4[u]);
-      __stcs(reinterpret_cast<float4*>(sg.m + e0 + u * kStride), m4[u]);
-      __stcs(reinterpret_cast<float4*>(sg.v + e0 + u * kStride), v4[u]);
-    }
-  }
-  return acc;
+// Streaming stores of theta, m, v (written once per step).
+__device__ __forceinline__ void st_stream(float* p, const float4& x) {
+#ifdef GRASS_ST_DEFAULT
+  *reinterpret_cast<float4*>(p) = x;
+#else
+  __stcs(reinterpret_cast<float4*>(p), x);
+#endif
 }
 
-// Ragged last tile: same element map and accumulation order, scalar and
-// bounds-checked.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// L2 policy of the bulk loads: the update stream (K2) measured faster with
+// evict_normal, the norm-only stream (K1) with evict_first.
 template <bool UPDATE>
-__device__ __forceinline__ double tile_body_tail(const Seg& sg, int64_t base, const AdamScalars& s) {
-  double acc = 0.0;
-  for (int u = 0; u < kUnroll; ++u) {
-    const int64_t e = base + ((int64_t)u * kThreads + threadIdx.x) * kVec;
-#pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      const int64_t i = e + j;
-      if (i < sg.n) {
-        const float g = sg.g[i];
-        acc = fma((double)g, (double)g, acc);
-        if (UPDATE) {
-          float th = sg.theta[i], m = sg.m[i], v = sg.v[i];
-          adamw1(g, th, m, v, s);
-          sg.theta[i] = th;
-          sg.m[i] = m;
-          sg.v[i] = v;
-        }
-      }
-    }
-  }
-  return acc;
+__device__ __forceinline__ uint64_t l2_load_policy() {
+  uint64_t pol;
+  if (UPDATE)
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// TMA bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                          uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+// Barrier over the consumer warps only (the producer warp never waits on it).
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
 }
 
-// K3: the last block to finish a layer sums its tile partials in a fixed order.
+// Fixed-shape reduction over the consumer threads; result valid in thread 0.
+__device__ __forceinline__ double consumer_sum(double x, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  x = warp_sum(x);
+  if (lane == 0) red[warp] = x;
+  consumer_sync();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) t += red[w];
+  }
+  return t;
+}
+
+// K3: the layer total is the fixed-order sum of its tile partials.
 __device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, double* red) {
   __threadfence();
   const double* P = st.partials + sg.part_layer_base;
   double a = 0.0;
   for (int i = threadIdx.x; i < sg.layer_tiles; i += kThreads) a += __ldcg(P + i);
-  __syncthreads();  // red[] reuse
-  const double ss = block_sum(a, red);
+  const double ss = consumer_sum(a, red);
   if (threadIdx.x == 0) {
     st.last_ss[sg.layer] = ss;
     if (mode == kFinalizeMgn) {
@@ -145,43 +159,167 @@ __device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, 
         st.S[sg.layer] += sqrt(ss / (double)sg.layer_numel);  // Eq. 2 inner term
         st.c[sg.layer] += 1;
       } else {
-        atomicMin(st.flag, sg.layer);
+        atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins
       }
     } else {
       st.shard_ss[sg.out_slot] = ss;
     }
     st.counters[sg.layer] = 0u;  // ready for the next step
   }
+  consumer_sync();
 }
 
-template <bool UPDATE>
-__global__ void __launch_bounds__(kThreads)
-grass_fused_kernel(const __grid_constant__ Batch b, const DevState st) {
-  __shared__ double red[kThreads / 32];
-  __shared__ int last;
-  const int total = b.tile_prefix[b.nseg];
-  int s = 0;
-  for (int t = blockIdx.x; t < total; t += gridDim.x) {
-    while (t >= b.tile_prefix[s + 1]) ++s;
+template <bool UPDATE, int TPS, int STAGES>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
+  constexpr int NARR = UPDATE ? 4 : 1;
+  constexpr int kUnit = TPS * (int)kTile;  // elements per unit (one ring stage)
+  extern __shared__ __align__(1024) float sbuf[];  // [STAGES][NARR][kUnit]
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ int unit_prefix[kMaxSeg + 1];
+  __shared__ int seg_done[kMaxSeg];
+  __shared__ double red[2][TPS][kConsumerWarps];
+  __shared__ double fred[kConsumerWarps];
+  __shared__ int fin[kMaxSeg];
+  __shared__ int nfin;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    unit_prefix[0] = 0;
+    for (int s = 0; s < b.nseg; ++s) {
+      unit_prefix[s + 1] = unit_prefix[s] + (b.seg[s].tiles + TPS - 1) / TPS;
+      seg_done[s] = 0;
+    }
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int total = unit_prefix[b.nseg];
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      const uint64_t pol = l2_load_policy<UPDATE>();
+      int s = 0, i = 0;
+      for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
+        const int stage = i % STAGES;
+        if (i >= STAGES) mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
+        while (u >= unit_prefix[s + 1]) ++s;
+        const Seg& sg = b.seg[s];
+        const int64_t e0 = (int64_t)(u - unit_prefix[s]) * kUnit;
+        const int64_t ne = min((int64_t)kUnit, sg.n - e0);
+        const uint32_t bytes = (uint32_t)(ne & ~(int64_t)3) * 4u;
+        float* dst = sbuf + (size_t)stage * NARR * kUnit;
+        if (bytes) {
+          mbar_arrive_expect_tx(&full_bar[stage], NARR * bytes);
+          bulk_load(dst, sg.g + e0, bytes, &full_bar[stage], pol);
+          if (UPDATE) {
+            bulk_load(dst + kUnit, sg.theta + e0, bytes, &full_bar[stage], pol);
+            bulk_load(dst + 2 * kUnit, sg.m + e0, bytes, &full_bar[stage], pol);
+            bulk_load(dst + 3 * kUnit, sg.v + e0, bytes, &full_bar[stage], pol);
+          }
+        } else {
+          mbar_arrive(&full_bar[stage]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------ consumers -------------------------------
+  int s = 0, i = 0;
+  for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
+    const int stage = i % STAGES;
+    while (u >= unit_prefix[s + 1]) ++s;
     const Seg& sg = b.seg[s];
     AdamScalars sc;
     sc.b1 = b.beta1; sc.omb1 = b.one_minus_beta1; sc.b2 = b.beta2; sc.omb2 = b.one_minus_beta2;
     sc.eps = b.eps; sc.decay = sg.decay; sc.step = sg.step_size; sc.inv_bc2s = sg.inv_bc2_sqrt;
-    const int lt = t - b.tile_prefix[s];
-    const int64_t base = (int64_t)lt * kTile;
-    const double acc = (base + kTile <= sg.n) ? tile_body_full<UPDATE>(sg, base, sc)
-                                              : tile_body_tail<UPDATE>(sg, base, sc);
-    const double part = block_sum(acc, red);
-    if (threadIdx.x == 0) {
-      st.partials[sg.part_index + lt] = part;
-      __threadfence();
-      const unsigned prev = atomicAdd(st.counters + sg.layer, 1u);
-      last = (prev == (unsigned)sg.layer_tiles - 1u);
+    const int ui = u - unit_prefix[s];
+    const int64_t e0 = (int64_t)ui * kUnit;
+    const int ne = (int)min((int64_t)kUnit, sg.n - e0);
+    const int nv = ne & ~3;  // bulk-copied prefix; the 0-3 element tail is read from HBM
+    const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
+    const float* sg_ = sbuf + (size_t)stage * NARR * kUnit;
+    mbar_wait(&full_bar[stage], (i / STAGES) & 1);
+#pragma unroll
+    for (int k = 0; k < TPS; ++k) {
+      if (k < ntiles) {
+        double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+          const int e = k * (int)kTile + (q * kThreads + tid) * kVec;  // relative to e0
+          if (e < nv) {
+            const float4 g4 = *reinterpret_cast<const float4*>(sg_ + e);
+            acc[0] = fma((double)g4.x, (double)g4.x, acc[0]);
+            acc[1] = fma((double)g4.y, (double)g4.y, acc[1]);
+            acc[2] = fma((double)g4.z, (double)g4.z, acc[2]);
+            acc[3] = fma((double)g4.w, (double)g4.w, acc[3]);
+            if (UPDATE) {
+              float4 t4 = *reinterpret_cast<const float4*>(sg_ + kUnit + e);
+              float4 m4 = *reinterpret_cast<const float4*>(sg_ + 2 * kUnit + e);
+              float4 v4 = *reinterpret_cast<const float4*>(sg_ + 3 * kUnit + e);
+              adamw1(g4.x, t4.x, m4.x, v4.x, sc);
+              adamw1(g4.y, t4.y, m4.y, v4.y, sc);
+              adamw1(g4.z, t4.z, m4.z, v4.z, sc);
+              adamw1(g4.w, t4.w, m4.w, v4.w, sc);
+              st_stream(sg.theta + e0 + e, t4);
+              st_stream(sg.m + e0 + e, m4);
+              st_stream(sg.v + e0 + e, v4);
+            }
+          } else if (e < ne) {
+#pragma unroll
+            for (int j = 0; j < kVec; ++j) {
+              if (e + j < ne) {
+                const int64_t idx = e0 + e + j;
+                const float g = sg.g[idx];
+                acc[j] = fma((double)g, (double)g, acc[j]);
+                if (UPDATE) {
+                  float th = sg.theta[idx], m = sg.m[idx], v = sg.v[idx];
+                  adamw1(g, th, m, v, sc);
+                  sg.theta[idx] = th;
+                  sg.m[idx] = m;
+                  sg.v[idx] = v;
+                }
+              }
+            }
+          }
+        }
+        const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+        if (lane == 0) red[i & 1][k][warp] = t;
+      }
     }
-    __syncthreads();
-    if (last) finalize_layer(sg, st, b.mode, red);
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[stage]);  // this warp is done with the stage
+    consumer_sync();
+    if (tid < ntiles) {  // lane k of warp 0 finishes tile k (warp sums in ascending order)
+      double p = 0.0;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) p += red[i & 1][tid][w];
+      st.partials[sg.part_index + (int64_t)ui * TPS + tid] = p;
+    }
+    if (tid == 0) seg_done[s] += ntiles;
   }
+  // Publish this CTA's partials (one fence, one atomic per segment) and
+  // detect the layers this CTA completed.
+  consumer_sync();
+  if (tid == 0) {
+    __threadfence();
+    int nf = 0;
+    for (int s2 = 0; s2 < b.nseg; ++s2) {
+      const int c = seg_done[s2];
+      if (c == 0) continue;
+      const unsigned prev = atomicAdd(st.counters + b.seg[s2].layer, (unsigned)c);
+      if (prev + (unsigned)c == (unsigned)b.seg[s2].layer_tiles) fin[nf++] = s2;
+    }
+    nfin = nf;
+  }
+  consumer_sync();
+  for (int f = 0; f < nfin; ++f) finalize_layer(b.seg[fin[f]], st, b.mode, fred);
 }
 
 __global__ void grass_rank_sum_kernel(const double* __restrict__ gathered,
@@ -196,22 +334,47 @@ __global__ void grass_rank_sum_kernel(const double* __restrict__ gathered,
     st.S[l] += sqrt(ss / (double)a.numel[j]);
     st.c[l] += 1;
   } else {
-    atomicMin(st.flag, l);
+    atomicMax(st.flag, INT_MAX - l);
   }
+}
+
+// Production configuration.
+#ifndef GRASS_UPD_STAGES
+#define GRASS_UPD_STAGES 2
+#endif
+#ifndef GRASS_NORM_TPS
+#define GRASS_NORM_TPS 4
+#endif
+#ifndef GRASS_NORM_STAGES
+#define GRASS_NORM_STAGES 3
+#endif
+constexpr int kUpdTPS = 1, kUpdStages = GRASS_UPD_STAGES;  // 4 arrays x 16 KiB per stage -> 128 KiB ring
+constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 64 KiB x 3 -> 192 KiB
+
+template <bool U, int TPS, int ST>
+cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStream_t s) {
+  constexpr size_t smem = (size_t)ST * (U ? 4 : 1) * TPS * (size_t)kTile * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(grass_stream_kernel<U, TPS, ST>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int units = 0;
+  for (int i = 0; i < b.nseg; ++i) units += (b.seg[i].tiles + TPS - 1) / TPS;
+  const int g = grid < units ? grid : units;
+  grass_stream_kernel<U, TPS, ST><<<g, kStreamThreads, smem, s>>>(b, st);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int grid,
                          cudaStream_t s) {
-  const int total = b.tile_prefix[b.nseg];
-  if (total <= 0) return cudaSuccess;
-  if (grid > total) grid = total;
-  if (update)
-    grass_fused_kernel<true><<<grid, kThreads, 0, s>>>(b, st);
-  else
-    grass_fused_kernel<false><<<grid, kThreads, 0, s>>>(b, st);
-  return cudaGetLastError();
+  if (b.nseg <= 0 || b.tile_prefix[b.nseg] <= 0) return cudaSuccess;
+  return update ? launch_stream<true, kUpdTPS, kUpdStages>(b, st, grid, s)
+                : launch_stream<false, kNormTPS, kNormStages>(b, st, grid, s);
 }
 
 cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const DevState& st,
@@ -221,17 +384,13 @@ cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const 
   return cudaGetLastError();
 }
 
-// Persistent grid: every SM holds as many blocks as fit (results never depend
-// on this number — see kTile in grass_internal.h).
+// Persistent grid: one streaming CTA per SM (results never depend on the grid
+// size — see kTile in grass_internal.h).
 int fused_grid(bool update, int device) {
-  int sms = 0, per_sm = 0;
+  (void)update;
+  int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
-  cudaError_t e = update ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                               &per_sm, grass_fused_kernel<true>, kThreads, 0)
-                         : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                               &per_sm, grass_fused_kernel<false>, kThreads, 0);
-  if (e != cudaSuccess || per_sm < 1) per_sm = 1;
-  return sms * per_sm;
+  return sms;
 }
 
 }  // namespace grass
