@@ -169,6 +169,11 @@ __device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, 
   consumer_sync();
 }
 
+// The branch-free full-unit path pays off for the norm-only stream (K1: +18%)
+// but not for K2, whose interleaved compute/store order measured ~0.5% faster
+// (profiles/r01_variants_*.json).
+constexpr bool kUpdFastPath = false;
+
 template <bool UPDATE, int TPS, int STAGES>
 __global__ void __launch_bounds__(kStreamThreads, 1)
 grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
@@ -246,6 +251,51 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
     const float* sg_ = sbuf + (size_t)stage * NARR * kUnit;
     mbar_wait(&full_bar[stage], (i / STAGES) & 1);
+    if (ne == kUnit && (!UPDATE || kUpdFastPath)) {
+      // Full unit (all but the last unit of a segment): branch-free, every
+      // shared-memory read issued before the math.  Same element map and
+      // accumulation order as the guarded path below.
+      float4 g4[TPS][kUnroll];
+#pragma unroll
+      for (int k = 0; k < TPS; ++k)
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q)
+          g4[k][q] = *reinterpret_cast<const float4*>(sg_ + k * (int)kTile + (q * kThreads + tid) * kVec);
+#pragma unroll
+      for (int k = 0; k < TPS; ++k) {
+        double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+          acc[0] = fma((double)g4[k][q].x, (double)g4[k][q].x, acc[0]);
+          acc[1] = fma((double)g4[k][q].y, (double)g4[k][q].y, acc[1]);
+          acc[2] = fma((double)g4[k][q].z, (double)g4[k][q].z, acc[2]);
+          acc[3] = fma((double)g4[k][q].w, (double)g4[k][q].w, acc[3]);
+        }
+        if (UPDATE) {
+          float4 t4[kUnroll], m4[kUnroll], v4[kUnroll];
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const int e = k * (int)kTile + (q * kThreads + tid) * kVec;
+            t4[q] = *reinterpret_cast<const float4*>(sg_ + kUnit + e);
+            m4[q] = *reinterpret_cast<const float4*>(sg_ + 2 * kUnit + e);
+            v4[q] = *reinterpret_cast<const float4*>(sg_ + 3 * kUnit + e);
+          }
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const int e = k * (int)kTile + (q * kThreads + tid) * kVec;
+            adamw1(g4[k][q].x, t4[q].x, m4[q].x, v4[q].x, sc);
+            adamw1(g4[k][q].y, t4[q].y, m4[q].y, v4[q].y, sc);
+            adamw1(g4[k][q].z, t4[q].z, m4[q].z, v4[q].z, sc);
+            adamw1(g4[k][q].w, t4[q].w, m4[q].w, v4[q].w, sc);
+            st_stream(sg.theta + e0 + e, t4[q]);
+            st_stream(sg.m + e0 + e, m4[q]);
+            st_stream(sg.v + e0 + e, v4[q]);
+          }
+        }
+        const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+        if (lane == 0) red[i & 1][k][warp] = t;
+      }
+    } else {
 #pragma unroll
     for (int k = 0; k < TPS; ++k) {
       if (k < ntiles) {
@@ -292,6 +342,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
         if (lane == 0) red[i & 1][k][warp] = t;
       }
+    }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[stage]);  // this warp is done with the stage
@@ -343,13 +394,13 @@ __global__ void grass_rank_sum_kernel(const double* __restrict__ gathered,
 #define GRASS_UPD_STAGES 2
 #endif
 #ifndef GRASS_NORM_TPS
-#define GRASS_NORM_TPS 4
+#define GRASS_NORM_TPS 6
 #endif
 #ifndef GRASS_NORM_STAGES
-#define GRASS_NORM_STAGES 3
+#define GRASS_NORM_STAGES 2
 #endif
 constexpr int kUpdTPS = 1, kUpdStages = GRASS_UPD_STAGES;  // 4 arrays x 16 KiB per stage -> 128 KiB ring
-constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 64 KiB x 3 -> 192 KiB
+constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 96 KiB x 2 -> 192 KiB
 
 template <bool U, int TPS, int ST>
 cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStream_t s) {

@@ -11,12 +11,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "upd_st2": ["GRASS_UPD_STAGES=2"],
-    "upd_st2_stdef": ["GRASS_UPD_STAGES=2", "GRASS_ST_DEFAULT"],
-    "upd_st2_n4x2": ["GRASS_UPD_STAGES=2", "GRASS_NORM_TPS=4", "GRASS_NORM_STAGES=2"],
-    "upd_st2_n2x3": ["GRASS_UPD_STAGES=2", "GRASS_NORM_TPS=2", "GRASS_NORM_STAGES=3"],
-    "upd_st2_n2x4": ["GRASS_UPD_STAGES=2", "GRASS_NORM_TPS=2", "GRASS_NORM_STAGES=4"],
-    "upd_st2_n3x3": ["GRASS_UPD_STAGES=2", "GRASS_NORM_TPS=3", "GRASS_NORM_STAGES=3"],
+    "base": [],
+    "k2_nofast": ["GRASS_K2_NOFAST"],
+    "base_again": [],
+    "k2_nofast_again": ["GRASS_K2_NOFAST"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
