@@ -81,7 +81,7 @@ def traffic(rep, key_upd="fused_update/llama2-7b/g2/w1", key_norm="probe/llama2-
     d = json.load(open(p)) if os.path.exists(p) else {}
     for r in rows:
         t = gb(r, "dram__bytes_read.sum") + gb(r, "dram__bytes_write.sum")
-        key = key_upd if "ILb1E" in r[ki] else key_norm
+        key = key_upd if ("ILb1E" in r[ki] or "_kernel<1" in r[ki]) else key_norm
         d[key] = t
     json.dump(d, open(p, "w"), indent=1)
     print(json.dumps(d, indent=1))
