@@ -95,7 +95,9 @@ typedef struct grass_config {
                                   0 = default (8 Mi elements) */
   int32_t ring_slots;          /* device staging slots for the offload ring (>= 1; 0 = 3) */
   int32_t rank, world;         /* data-parallel rank / world size (world = 1: no NCCL) */
-  const void* nccl_unique_id;  /* host, GRASS_NCCL_ID_BYTES; required when world > 1 */
+  const void* nccl_unique_id;  /* host, GRASS_NCCL_ID_BYTES; required when world > 1.  With
+                                  world = 1 a non-NULL id runs the same NCCL path on a 1-rank
+                                  communicator (used to test it on one GPU) */
 } grass_config;
 
 /* Fills *cfg with the defaults above (layer_numel = NULL, n_layers = 0). */

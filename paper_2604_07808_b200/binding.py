@@ -188,7 +188,7 @@ class Grass:
                  beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0,
                  seed: int = 1234, device: int = 0, offload: bool = False, overlap: bool = True,
                  chunk_elems: int = 0, ring_slots: int = 0, rank: int = 0, world: int = 1,
-                 process_group=None):
+                 process_group=None, force_nccl: bool = False):
         L = lib()
         self.layer_numel = [int(x) for x in layer_numel]
         self.n_layers = len(self.layer_numel)
@@ -208,7 +208,10 @@ class Grass:
         cfg.chunk_elems, cfg.ring_slots = chunk_elems, ring_slots
         cfg.rank, cfg.world = rank, world
         self._uid = None
-        if world > 1:
+        if world == 1 and force_nccl:
+            self._uid = C.create_string_buffer(nccl_unique_id(), NCCL_ID_BYTES)
+            cfg.nccl_unique_id = C.cast(self._uid, C.c_void_p)
+        elif world > 1:
             import torch.distributed as dist
             obj = [nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0, group=process_group)

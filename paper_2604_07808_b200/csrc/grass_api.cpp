@@ -69,6 +69,7 @@ struct grass_ctx {
 
   Comm comm;
   bool has_comm = false;
+  bool dp = false;  // data-parallel (NCCL) path: world > 1, or world = 1 with a unique id
   int grid_update = 0, grid_norm = 0;
   int64_t launches = 0, dev_bytes = 0, host_bytes = 0;
   std::string err;
@@ -482,7 +483,8 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     c->layer_done_valid.assign(c->nl, 0);
   }
 
-  if (W > 1) {
+  c->dp = W > 1 || cfg->nccl_unique_id != nullptr;
+  if (c->dp) {
     CUDA_TRY(c, dalloc((void**)&c->d_gather, sizeof(double) * (size_t)W * c->nl));
     CUDA_TRY(c, dalloc((void**)&c->d_gscratch, sizeof(float) * (size_t)c->max_shard));
     if (!c->comm.init(cfg->nccl_unique_id, cfg->rank, W, &c->err)) return GRASS_E_NCCL;
@@ -564,7 +566,7 @@ grass_status grass_mgn_accumulate(grass_ctx* c, const int32_t* ids, int32_t n,
   if (s != GRASS_OK) return s;
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (c->cfg.world == 1) {
+  if (!c->dp) {
     Batch b = make_batch(c, kFinalizeMgn);
     for (int i : order) {
       if (b.nseg == kMaxSeg && (s = flush(c, &b, false, st)) != GRASS_OK) return s;
@@ -599,7 +601,7 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
   if (s != GRASS_OK) return s;
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const bool sharded = c->cfg.world > 1;
+  const bool sharded = c->dp;
   const int32_t mode = sharded ? kFinalizeShard : kFinalizeMgn;
   Batch b = make_batch(c, mode);
   for (int j = 0; j < (int)order.size(); ++j) {

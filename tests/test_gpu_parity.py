@@ -222,6 +222,37 @@ def test_offload_under_stream_jitter():
         assert torch.equal(p_ref[l], p_off[l])
 
 
+# --------------------------------- data-parallel (NCCL) path on one GPU
+@pytest.mark.parametrize("offload", [False, True])
+def test_nccl_path_one_rank_bit_identical(offload):
+    """world = 1 with a unique id runs the DP code path (N1 reduce-scatter avg,
+    shard update, N2 in-place all-gather, N3 fp64 partial all-gather + rank sum)
+    over a real 1-rank NCCL communicator: every result must equal the plain
+    path bit for bit."""
+    numel = [3 * 4096 + 8, 65_536, 4096]
+    kw = dict(gamma=2, weight_decay=0.01, offload=offload, chunk_elems=4096 if offload else 0)
+    ref = G.Grass(numel, **kw)
+    dp = G.Grass(numel, force_nccl=True, **kw)
+    p_ref = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    p_dp = [p.clone() for p in p_ref]
+    for step in range(4):
+        ids = [[0, 1], [2, 0], [1, 2], [0, 2]][step]
+        grads = [layer_grad(numel[l], l, 1e-3, step=step, device=DEV) for l in ids]
+        ref.step_layers(ids, [p_ref[l] for l in ids], grads, 1e-3)
+        dp.step_layers(ids, [p_dp[l] for l in ids], grads, 1e-3)
+    allg = [layer_grad(n, l, 1e-3, step=9, device=DEV) for l, n in enumerate(numel)]
+    ref.mgn_accumulate([0, 1, 2], allg)
+    dp.mgn_accumulate([0, 1, 2], allg)
+    torch.cuda.synchronize()
+    for l in range(3):
+        assert torch.equal(p_ref[l], p_dp[l])
+        a, b = ref.read_state(l), dp.read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+    sa, sb = ref.get_mgn(), dp.get_mgn()
+    assert sa["S"] == sb["S"] and sa["c"] == sb["c"] and sa["last_ss"] == sb["last_ss"]
+    assert dp.launch_count > ref.launch_count          # the NCCL calls were issued
+
+
 # -------------------------------------------- a2-a4: whole path vs oracle
 def test_full_schedule_tiny_config_vs_oracle():
     """configs[0]: 4 layers x 65,536 fp32, gamma = 2, fixed seed; probing,
