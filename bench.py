@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--impl", default="grass", choices=["grass", "reference"])
     ap.add_argument("--model", default="llama2-7b")
     ap.add_argument("--gamma", type=int, default=2)
-    ap.add_argument("--legs", default="main,probe,offload,e2e,cpu",
+    ap.add_argument("--legs", default="main,probe,offload,period,e2e,cpu",
                     help="comma list of legs to run (main is always run)")
     ap.add_argument("--offload-steps", type=int, default=10)
     ap.add_argument("--lr", type=float, default=3e-5)
@@ -354,6 +354,49 @@ def run_grass(args, rank, world, local):
                    "device_state_bytes": octx.device_bytes}
         del octx
 
+    # ---- period residency: paper schedule T_s = T_u = 25
+    offload_period = None
+    if "period" in legs:
+        torch.cuda.empty_cache()
+        T_s = 25
+        pctx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=T_s, T_u=T_s, seed=1234, device=local,
+                       offload=True, residency=G.RESIDENCY_PERIOD, rank=rank, world=world)
+        pctx.mgn_accumulate(list(range(NL)), grads, stream=s)
+        pctx.update_probs()
+        pids = pctx.sample_layers(0)
+        swaps = 0
+
+        def pstep(step):
+            nonlocal pids, swaps
+            if step > 0 and step % T_s == 0:          # period boundary: commit, probs, resample
+                pctx.update_probs()
+                new = pctx.sample_layers(step // T_s)
+                swaps += len(set(new) - set(pids))
+                pids = new
+            pctx.step_layers(pids, [params[l] for l in pids], [grads[l] for l in pids], args.lr,
+                             stream=s)
+        for w in range(T_s):                          # warm: one full period (cache filled)
+            pstep(w)
+        torch.cuda.synchronize()
+        barrier(world)
+        swaps = 0
+        nper = 2 * T_s
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(s)
+        for k in range(nper):
+            pstep(T_s + k)                            # starts at a period boundary
+        p1.record(s)
+        torch.cuda.synchronize()
+        pt = max_over_ranks(p0.elapsed_time(p1) / 1e3, world, dev) / nper
+        offload_period = {"workload": f"{args.model}-stack gamma={gamma} offload, period residency "
+                                      f"(SURVEY 8(f) f1), T_s=T_u={T_s}",
+                          "steps": nper, "layer_swaps": swaps, "step_ms_amortized": pt * 1e3,
+                          "params_per_s": active / pt,
+                          "link_bytes_per_dir": swaps * 8 * n_p // world,
+                          "over_resident": pt / (elapsed / args.steps),
+                          "device_cache_bytes": pctx.device_bytes}
+        del pctx
+
     # ---- CPU oracle baseline
     cpu = None
     if "cpu" in legs and rank == 0 and world == 1:
@@ -382,6 +425,7 @@ def run_grass(args, rank, world, local):
                          "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "probe": out.get("probe"), "offload": offload,
+            "offload_period": offload_period,
         }
         print(json.dumps(line), flush=True)
 

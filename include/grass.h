@@ -98,7 +98,18 @@ typedef struct grass_config {
   const void* nccl_unique_id;  /* host, GRASS_NCCL_ID_BYTES; required when world > 1.  With
                                   world = 1 a non-NULL id runs the same NCCL path on a 1-rank
                                   communicator (used to test it on one GPU) */
+  int32_t residency;           /* offload only: GRASS_RESIDENCY_STEP (paper: every step
+                                  round-trips the active layers' m/v) or
+                                  GRASS_RESIDENCY_PERIOD (a layer's m/v stay
+                                  in HBM while it stays trainable; swapped only when the
+                                  sampled set changes) */
+  int32_t cache_layers;        /* GRASS_RESIDENCY_PERIOD: device layer slots (>= gamma; 0 = gamma) */
 } grass_config;
+
+typedef enum {
+  GRASS_RESIDENCY_STEP = 0,
+  GRASS_RESIDENCY_PERIOD = 1
+} grass_residency;
 
 /* Fills *cfg with the defaults above (layer_numel = NULL, n_layers = 0). */
 grass_status grass_config_init(grass_config* cfg);
@@ -178,6 +189,11 @@ grass_status grass_step_layers(grass_ctx* ctx, const int32_t* layer_ids, int32_t
  * pointer may be NULL.  Synchronises the context first. */
 grass_status grass_read_state(grass_ctx* ctx, int32_t layer, float* m_out, float* v_out,
                               int64_t* t_out);
+
+/* GRASS_RESIDENCY_PERIOD: writes the m/v of every layer cached in HBM back to
+ * its pinned host home (the cache stays valid).  No-op otherwise.
+ * Synchronises. */
+grass_status grass_flush_states(grass_ctx* ctx);
 
 /* Overwrites this rank's m/v shard and step count of `layer` (checkpoint
  * restore).  Synchronises the context first. */

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("GRASS_LIB_PATH") or os.path.join(_PKG, "libgrass.so")
 OK, E_INVALID, E_STATE, E_CUDA, E_NCCL, E_OOM, E_NONFINITE = range(7)
 POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM = range(3)
 DECIDE_PROBE, DECIDE_COMMIT_RESAMPLE, DECIDE_RESAMPLE, DECIDE_CONTINUE = range(4)
+RESIDENCY_STEP, RESIDENCY_PERIOD = range(2)
 NCCL_ID_BYTES = 128
 
 _STATUS = {0: "GRASS_OK", 1: "GRASS_E_INVALID", 2: "GRASS_E_STATE", 3: "GRASS_E_CUDA",
@@ -41,7 +42,7 @@ class GrassConfig(C.Structure):
         ("weight_decay", C.c_double), ("seed", C.c_uint64), ("device", C.c_int32),
         ("offload", C.c_int32), ("overlap", C.c_int32), ("chunk_elems", C.c_int64),
         ("ring_slots", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
-        ("nccl_unique_id", C.c_void_p),
+        ("nccl_unique_id", C.c_void_p), ("residency", C.c_int32), ("cache_layers", C.c_int32),
     ]
 
 
@@ -65,6 +66,7 @@ _SIGS = {
     "grass_read_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.POINTER(C.c_int64)]),
     "grass_write_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64]),
+    "grass_flush_states": (C.c_int, [C.c_void_p]),
     "grass_get_mgn": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                 C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                 C.POINTER(C.c_double)]),
@@ -188,7 +190,8 @@ class Grass:
                  beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0,
                  seed: int = 1234, device: int = 0, offload: bool = False, overlap: bool = True,
                  chunk_elems: int = 0, ring_slots: int = 0, rank: int = 0, world: int = 1,
-                 process_group=None, force_nccl: bool = False):
+                 process_group=None, force_nccl: bool = False, residency: int = RESIDENCY_STEP,
+                 cache_layers: int = 0):
         L = lib()
         self.layer_numel = [int(x) for x in layer_numel]
         self.n_layers = len(self.layer_numel)
@@ -207,6 +210,7 @@ class Grass:
         cfg.offload, cfg.overlap = int(offload), int(overlap)
         cfg.chunk_elems, cfg.ring_slots = chunk_elems, ring_slots
         cfg.rank, cfg.world = rank, world
+        cfg.residency, cfg.cache_layers = residency, cache_layers
         self._uid = None
         if world == 1 and force_nccl:
             self._uid = C.create_string_buffer(nccl_unique_id(), NCCL_ID_BYTES)
@@ -289,6 +293,9 @@ class Grass:
         if m.size != n or v.size != n:
             raise ValueError("state size must equal the shard length")
         _check(lib().grass_write_state(self._h, layer, m.ctypes.data, v.ctypes.data, t), self._h)
+
+    def flush_states(self):
+        _check(lib().grass_flush_states(self._h), self._h)
 
     def get_mgn(self):
         n = self.n_layers

@@ -60,8 +60,19 @@ struct grass_ctx {
   std::vector<cudaEvent_t> ev_layer_done;  // last write-back of each layer
   std::vector<char> layer_done_valid;
 
-  // outstanding stream-ordered work (for the synchronising calls)
-  std::vector<cudaEvent_t> ev_free_list, ev_pending;
+  // period residency: HBM cache of whole-layer m/v slots
+  float* d_cache = nullptr;          // cache_slots x [m | v] of max_shard floats each
+  int cache_slots = 0;
+  std::vector<int> slot_layer, layer_slot;
+  std::vector<int64_t> slot_use;
+  std::vector<char> slot_dirty;
+  int64_t call_seq = 0;
+  cudaEvent_t ev_call = nullptr, ev_evict = nullptr, ev_fill = nullptr;
+
+  // outstanding stream-ordered work (for the synchronising calls): the last
+  // event recorded on each stream the caller used
+  std::vector<cudaEvent_t> ev_free_list;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> ev_pending;
 
   // host MGN state (fp64)
   std::vector<double> mgn, probs;
@@ -107,10 +118,21 @@ cudaEvent_t take_event(grass_ctx* c) {
 }
 
 grass_status mark_pending(grass_ctx* c, cudaStream_t s) {
+  for (auto& pe : c->ev_pending)
+    if (pe.first == s) {  // newest record on a stream implies all earlier work on it
+      CUDA_TRY(c, cudaEventRecord(pe.second, s));
+      return GRASS_OK;
+    }
   cudaEvent_t e = take_event(c);
   if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
   CUDA_TRY(c, cudaEventRecord(e, s));
-  c->ev_pending.push_back(e);
+  c->ev_pending.emplace_back(s, e);
+  return GRASS_OK;
+}
+
+// Makes stream `s` wait for all outstanding work the context enqueued.
+grass_status wait_pending(grass_ctx* c, cudaStream_t s) {
+  for (auto& pe : c->ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, pe.second, 0));
   return GRASS_OK;
 }
 
@@ -123,12 +145,13 @@ int flag_layer(int enc) { return INT_MAX - enc; }
 // zeroes the window (S, c) and/or the flag, then synchronises once.
 grass_status fetch_mgn(grass_ctx* c, bool reset_window, bool take_flag) {
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
-  for (cudaEvent_t e : c->ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(c->aux, e, 0));
+  grass_status s = wait_pending(c, c->aux);
+  if (s != GRASS_OK) return s;
   CUDA_TRY(c, cudaMemcpyAsync(c->h_mgn, c->d_mgn, c->mgn_bytes, cudaMemcpyDeviceToHost, c->aux));
   if (reset_window) CUDA_TRY(c, cudaMemsetAsync(c->d_mgn, 0, 16 * (size_t)c->nl, c->aux));
   if (take_flag) CUDA_TRY(c, cudaMemsetAsync(c->st.flag, 0, sizeof(int), c->aux));
   CUDA_TRY(c, cudaStreamSynchronize(c->aux));
-  for (cudaEvent_t e : c->ev_pending) c->ev_free_list.push_back(e);
+  for (auto& pe : c->ev_pending) c->ev_free_list.push_back(pe.second);
   c->ev_pending.clear();
   return GRASS_OK;
 }
@@ -188,6 +211,10 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
     if (cfg->chunk_elems < 0 || cfg->chunk_elems % kTile != 0)
       return bad("chunk_elems must be a non-negative multiple of grass_tile_elems()");
     if (cfg->ring_slots < 0) return bad("ring_slots must be >= 0");
+    if (cfg->residency != GRASS_RESIDENCY_STEP && cfg->residency != GRASS_RESIDENCY_PERIOD)
+      return bad("unknown residency");
+    if (cfg->cache_layers < 0 || cfg->cache_layers > cfg->n_layers)
+      return bad("cache_layers must lie in [0, N_L]");
   }
   return GRASS_OK;
 }
@@ -358,6 +385,118 @@ grass_status offload_layer(grass_ctx* c, int l, Seg base, float* theta, const fl
   return GRASS_OK;
 }
 
+// ---- period residency -----------------------------------
+float* cache_m(grass_ctx* c, int slot) { return c->d_cache + (size_t)slot * 2 * c->max_shard; }
+float* cache_v(grass_ctx* c, int slot) { return cache_m(c, slot) + c->max_shard; }
+
+// Slot for every listed layer: hits keep their slot; misses take an empty slot
+// or evict the least recently used layer that is not trainable in this call.
+void cache_plan(grass_ctx* c, const int32_t* ids, const std::vector<int>& order,
+                std::vector<int>* slot_of, std::vector<int>* victim_of) {
+  const int n = (int)order.size();
+  slot_of->assign(n, -1);
+  victim_of->assign(n, -1);
+  std::vector<char> taken(c->cache_slots, 0);
+  for (int j = 0; j < n; ++j) {
+    const int l = ids[order[j]];
+    if (c->layer_slot[l] >= 0) {
+      (*slot_of)[j] = c->layer_slot[l];
+      taken[c->layer_slot[l]] = 1;
+    }
+  }
+  for (int j = 0; j < n; ++j) {
+    if ((*slot_of)[j] >= 0) continue;
+    int best = -1;
+    for (int k = 0; k < c->cache_slots; ++k) {
+      if (taken[k]) continue;
+      if (c->slot_layer[k] < 0) {
+        best = k;
+        break;
+      }
+      if (best < 0 || c->slot_use[k] < c->slot_use[best]) best = k;
+    }
+    taken[best] = 1;  // cache_slots >= gamma >= n, so a slot always exists
+    (*slot_of)[j] = best;
+    (*victim_of)[j] = c->slot_layer[best];
+  }
+}
+
+// Brings layer l's m/v into `slot` (evicting `victim` to its host home first,
+// chunk by chunk, so write-back and fetch overlap on the duplex link) and
+// updates l chunk by chunk as its states arrive.  Nothing is written back
+// after the update: the slot stays resident and dirty.
+grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, Seg base, float* theta,
+                           const float* g, int32_t mode, cudaStream_t s) {
+  const bool overlap = c->cfg.overlap != 0;
+  cudaStream_t sh = overlap ? c->h2d : s, sd = overlap ? c->d2h : s;
+  float* sm = cache_m(c, slot);
+  float* sv = cache_v(c, slot);
+  const int64_t ll = c->shard_len[l];
+  const int64_t lv = (victim >= 0 && c->slot_dirty[slot]) ? c->shard_len[victim] : 0;
+  if (overlap && c->layer_done_valid[l])  // l's host copy must be final
+    CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_layer_done[l], 0));
+  for (int64_t off = 0; off < std::max(ll, lv); off += c->chunk) {
+    if (off < lv) {
+      const size_t vb = sizeof(float) * (size_t)std::min(c->chunk, lv - off);
+      CUDA_TRY(c, cudaMemcpyAsync(c->m[victim] + off, sm + off, vb, cudaMemcpyDeviceToHost, sd));
+      CUDA_TRY(c, cudaMemcpyAsync(c->v[victim] + off, sv + off, vb, cudaMemcpyDeviceToHost, sd));
+      if (overlap && off < ll) {
+        CUDA_TRY(c, cudaEventRecord(c->ev_evict, sd));
+        CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_evict, 0));
+      }
+    }
+    if (off < ll) {
+      const int64_t n = std::min(c->chunk, ll - off);
+      const size_t bytes = sizeof(float) * (size_t)n;
+      CUDA_TRY(c, cudaMemcpyAsync(sm + off, c->m[l] + off, bytes, cudaMemcpyHostToDevice, sh));
+      CUDA_TRY(c, cudaMemcpyAsync(sv + off, c->v[l] + off, bytes, cudaMemcpyHostToDevice, sh));
+      if (overlap) {
+        CUDA_TRY(c, cudaEventRecord(c->ev_fill, sh));
+        CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_fill, 0));
+      }
+      Seg sg = range_seg(c, l, g, off, n);
+      sg.theta = theta + off;
+      sg.m = sm + off;
+      sg.v = sv + off;
+      sg.decay = base.decay;
+      sg.step_size = base.step_size;
+      sg.inv_bc2_sqrt = base.inv_bc2_sqrt;
+      sg.out_slot = base.out_slot;
+      Batch b = make_batch(c, mode);
+      push_seg(&b, sg);
+      grass_status st = flush(c, &b, true, s);
+      if (st != GRASS_OK) return st;
+    }
+  }
+  if (victim >= 0) {
+    if (lv > 0 && overlap) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_layer_done[victim], sd));
+      c->layer_done_valid[victim] = 1;
+    }
+    c->layer_slot[victim] = -1;
+  }
+  c->slot_layer[slot] = l;
+  c->layer_slot[l] = slot;
+  return GRASS_OK;
+}
+
+// Writes every dirty cached layer back to its host home (synchronous).
+grass_status flush_cache(grass_ctx* c) {
+  if (c->cache_slots == 0) return GRASS_OK;
+  grass_status s = wait_pending(c, c->d2h);
+  if (s != GRASS_OK) return s;
+  for (int k = 0; k < c->cache_slots; ++k) {
+    const int l = c->slot_layer[k];
+    if (l < 0 || !c->slot_dirty[k]) continue;
+    const size_t bytes = sizeof(float) * (size_t)c->shard_len[l];
+    CUDA_TRY(c, cudaMemcpyAsync(c->m[l], cache_m(c, k), bytes, cudaMemcpyDeviceToHost, c->d2h));
+    CUDA_TRY(c, cudaMemcpyAsync(c->v[l], cache_v(c, k), bytes, cudaMemcpyDeviceToHost, c->d2h));
+    c->slot_dirty[k] = 0;
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(c->d2h));
+  return GRASS_OK;
+}
+
 void free_ctx(grass_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->cfg.device);
@@ -381,10 +520,13 @@ void free_ctx(grass_ctx* c) {
     else
       cudaFree(c->state_block);
   }
-  for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free, &c->ev_layer_done, &c->ev_free_list,
-                  &c->ev_pending})
+  for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free, &c->ev_layer_done, &c->ev_free_list})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
+  for (auto& pe : c->ev_pending) cudaEventDestroy(pe.second);
+  for (cudaEvent_t e : {c->ev_call, c->ev_evict, c->ev_fill})
+    if (e) cudaEventDestroy(e);
+  dfree(c->d_cache);
   for (cudaStream_t s : {c->h2d, c->d2h, c->aux})
     if (s) cudaStreamDestroy(s);
   delete c;
@@ -470,7 +612,18 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     c->chunk = cfg->chunk_elems ? cfg->chunk_elems : kDefaultChunk;
     c->chunk = std::min(c->chunk, round_up(c->max_shard, kTile));
     c->slots = cfg->ring_slots ? cfg->ring_slots : kDefaultSlots;
-    CUDA_TRY(c, dalloc((void**)&c->d_ring, sizeof(float) * 2 * (size_t)c->chunk * c->slots));
+    if (cfg->residency == GRASS_RESIDENCY_PERIOD) {
+      c->cache_slots = std::max(cfg->gamma, cfg->cache_layers);
+      CUDA_TRY(c, dalloc((void**)&c->d_cache, sizeof(float) * 2 * (size_t)c->max_shard * c->cache_slots));
+      c->slot_layer.assign(c->cache_slots, -1);
+      c->layer_slot.assign(c->nl, -1);
+      c->slot_use.assign(c->cache_slots, 0);
+      c->slot_dirty.assign(c->cache_slots, 0);
+      for (cudaEvent_t* e : {&c->ev_call, &c->ev_evict, &c->ev_fill})
+        CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    } else {
+      CUDA_TRY(c, dalloc((void**)&c->d_ring, sizeof(float) * 2 * (size_t)c->chunk * c->slots));
+    }
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
     for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free}) {
@@ -603,6 +756,14 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool sharded = c->dp;
   const int32_t mode = sharded ? kFinalizeShard : kFinalizeMgn;
+  const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
+  std::vector<int> slot_of, victim_of;
+  if (period) {
+    cache_plan(c, ids, order, &slot_of, &victim_of);
+    c->call_seq++;
+    // write-backs read cache slots last written by earlier steps' updates
+    if (c->cfg.overlap && (s = wait_pending(c, c->d2h)) != GRASS_OK) return s;
+  }
   Batch b = make_batch(c, mode);
   for (int j = 0; j < (int)order.size(); ++j) {
     const int i = order[j], l = ids[i];
@@ -616,7 +777,24 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
       g = c->d_gscratch;  // shard-local gradient: index 0 = element `off`
     }
     float* theta = params[i] + off;
-    if (c->cfg.offload) {
+    if (period) {
+      const int slot = slot_of[j];
+      Seg sg = range_seg(c, l, g, 0, len);
+      adam_scalars(c, l, lr, &sg);
+      sg.out_slot = j;
+      if (c->slot_layer[slot] == l) {  // hit: update in place in HBM, no link traffic
+        sg.theta = theta;
+        sg.m = cache_m(c, slot);
+        sg.v = cache_v(c, slot);
+        if (b.nseg == kMaxSeg && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+        push_seg(&b, sg);
+        if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+      } else if ((s = swap_in_layer(c, l, slot, victim_of[j], sg, theta, g, mode, st)) != GRASS_OK) {
+        return s;
+      }
+      c->slot_use[slot] = c->call_seq;
+      c->slot_dirty[slot] = 1;
+    } else if (c->cfg.offload) {
       Seg base = range_seg(c, l, g, 0, len);
       adam_scalars(c, l, lr, &base);
       base.out_slot = j;
@@ -705,7 +883,11 @@ grass_status grass_read_state(grass_ctx* c, int32_t layer, float* m_out, float* 
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
   const size_t bytes = sizeof(float) * (size_t)c->shard_len[layer];
-  if (c->cfg.offload) {
+  const int slot = c->cache_slots ? c->layer_slot[layer] : -1;
+  if (slot >= 0) {  // cached in HBM: the device copy is the current one
+    if (m_out) CUDA_TRY(c, cudaMemcpy(m_out, cache_m(c, slot), bytes, cudaMemcpyDeviceToHost));
+    if (v_out) CUDA_TRY(c, cudaMemcpy(v_out, cache_v(c, slot), bytes, cudaMemcpyDeviceToHost));
+  } else if (c->cfg.offload) {
     if (m_out) std::memcpy(m_out, c->m[layer], bytes);
     if (v_out) std::memcpy(v_out, c->v[layer], bytes);
   } else {
@@ -723,7 +905,12 @@ grass_status grass_write_state(grass_ctx* c, int32_t layer, const float* m_in, c
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
   const size_t bytes = sizeof(float) * (size_t)c->shard_len[layer];
-  if (c->cfg.offload) {
+  const int slot = c->cache_slots ? c->layer_slot[layer] : -1;
+  if (slot >= 0) {  // cached in HBM: the device copy stays authoritative (dirty)
+    if (m_in) CUDA_TRY(c, cudaMemcpy(cache_m(c, slot), m_in, bytes, cudaMemcpyHostToDevice));
+    if (v_in) CUDA_TRY(c, cudaMemcpy(cache_v(c, slot), v_in, bytes, cudaMemcpyHostToDevice));
+    c->slot_dirty[slot] = 1;
+  } else if (c->cfg.offload) {
     if (m_in) std::memcpy(c->m[layer], m_in, bytes);
     if (v_in) std::memcpy(c->v[layer], v_in, bytes);
   } else {
@@ -732,6 +919,13 @@ grass_status grass_write_state(grass_ctx* c, int32_t layer, const float* m_in, c
   }
   c->t[layer] = t_in;
   return GRASS_OK;
+}
+
+grass_status grass_flush_states(grass_ctx* c) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  grass_status s = drain(c, false);
+  if (s != GRASS_OK) return s;
+  return flush_cache(c);
 }
 
 grass_status grass_get_mgn(grass_ctx* c, double* m_out, double* S_out, int64_t* c_out,

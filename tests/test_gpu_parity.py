@@ -197,6 +197,42 @@ def test_offload_bit_identical_to_resident(overlap, slots):
     assert ctxs[0].get_mgn()["S"] == ctxs[1].get_mgn()["S"]
 
 
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("cache", [0, 3])
+def test_period_residency_bit_identical_to_resident(overlap, cache):
+    """states of trainable layers stay in HBM across steps and
+    are swapped (write-back of the victim || fetch of the new layer, chunked)
+    only when the set changes; numerically still a no-op (R12)."""
+    numel = [5 * 4096 + 17, 12 * 4096, 4096, 7, 3 * 4096]
+    sig = grad_sigmas(5, 4)
+    ref = G.Grass(numel, gamma=2, weight_decay=0.01)
+    per = G.Grass(numel, gamma=2, weight_decay=0.01, offload=True, overlap=overlap,
+                  chunk_elems=2 * 4096, residency=G.RESIDENCY_PERIOD, cache_layers=cache)
+    p_ref = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    p_per = [p.clone() for p in p_ref]
+    sets = [[0, 1], [0, 1], [1, 2], [3, 1], [3, 1], [4, 0], [2, 4], [1, 0], [1, 0]]
+    for step, ids in enumerate(sets):
+        grads = [layer_grad(numel[l], l, sig[l], step=step, device=DEV) for l in ids]
+        ref.step_layers(ids, [p_ref[l] for l in ids], grads, 1e-3)
+        per.step_layers(ids, [p_per[l] for l in ids], grads, 1e-3)
+        if step == 4:   # read/write state of cached and host-resident layers mid-run
+            for l in (1, 2):
+                a, b = ref.read_state(l), per.read_state(l)
+                assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+    torch.cuda.synchronize()
+    for l in range(5):
+        assert torch.equal(p_ref[l], p_per[l]), l
+        a, b = ref.read_state(l), per.read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2], l
+    per.flush_states()
+    for l in range(5):
+        a, b = ref.read_state(l), per.read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert ref.get_mgn()["S"] == per.get_mgn()["S"]
+    # cache footprint: max(gamma, cache) whole-layer slots of m and v
+    assert per.device_bytes >= max(2, cache) * 2 * 4 * max(numel)
+
+
 def test_offload_under_stream_jitter():
     # random-length busy kernels on the caller stream between steps must not
     # change the result (SPEC.md:360, 373)
