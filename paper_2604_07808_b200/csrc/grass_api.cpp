@@ -20,7 +20,9 @@ namespace {
 
 thread_local std::string g_thread_err;
 
-constexpr int64_t kDefaultChunk = 8ll << 20;  // 8 Mi elements = 32 MiB per moment
+// 16 Mi elements = 64 MiB per moment per chunk; with 3 ring slots this measured
+// best on the 7B stack (profiles/r01_offload_sweep.json).
+constexpr int64_t kDefaultChunk = 16ll << 20;
 constexpr int kDefaultSlots = 3;
 constexpr int64_t kAlignElems = 64;           // 256-byte alignment of every state slice
 

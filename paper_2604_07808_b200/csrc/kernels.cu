@@ -16,8 +16,13 @@
 // movement: a persistent, warp-specialised kernel (one CTA per SM) in which a
 // producer warp streams tiles HBM -> shared memory with cp.async.bulk (TMA
 // bulk copies, SASS UBLKCP) into a STAGES-deep ring guarded by mbarriers,
-// while 16 consumer warps compute and write results back with streaming
-// 128-bit stores.  The HBM pipe never drains on a block barrier.
+// while 16 consumer warps compute.  K2's consumers write theta', m', v' back
+// into the stage and the producer bulk-stores them (smem -> HBM, TMA) before
+// refilling it.  The HBM pipe never drains on a block barrier.
+//
+// Compile-time A/B knobs (tools/variants.py; defaults are the measured best):
+// GRASS_IEEE_MATH, GRASS_K2_STG_STORE, GRASS_K2_LOAD_EF, GRASS_K2_STORE_EF,
+// GRASS_UPD_STAGES, GRASS_NORM_TPS, GRASS_NORM_STAGES.
 //
 // The tile partial (grass_internal.h) is a FIXED function of the tile's data:
 // consumer thread t owns elements (q*kThreads + t)*4 + j, j = 0..3, q = 0..
@@ -111,7 +116,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 template <bool UPDATE>
 __device__ __forceinline__ uint64_t l2_load_policy() {
   uint64_t pol;
+#ifdef GRASS_K2_LOAD_EF
+  if (false)
+#else
   if (UPDATE)
+#endif
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
   else
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -126,6 +135,39 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
       : "memory");
 }
+// TMA bulk copy shared -> global (bulk-group completion).
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+#ifdef GRASS_K2_STORE_EF
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes), "l"(pol)
+               : "memory");
+#else
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+#endif
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Bulk-stores the theta, m, v results of one unit from its stage.
+__device__ __forceinline__ void store_unit(const Seg& sg, int64_t e0, uint32_t bytes, const float* stage,
+                                           int unit) {
+  if (bytes) {
+    bulk_store(sg.theta + e0, stage + unit, bytes);
+    bulk_store(sg.m + e0, stage + 2 * unit, bytes);
+    bulk_store(sg.v + e0, stage + 3 * unit, bytes);
+    bulk_commit();
+  }
+}
+
 // Barrier over the consumer warps only (the producer warp never waits on it).
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
@@ -173,6 +215,13 @@ __device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, 
 // but not for K2, whose interleaved compute/store order measured ~0.5% faster
 // (profiles/r01_variants_*.json).
 constexpr bool kUpdFastPath = false;
+// K2 writes its results back into the stage and the producer bulk-stores them
+// (TMA, SASS UBLKCP.G.S): measured 2.4% faster than per-thread 128-bit stores.
+#ifdef GRASS_K2_STG_STORE
+constexpr bool kTmaStore = false;
+#else
+constexpr bool kTmaStore = true;
+#endif
 
 template <bool UPDATE, int TPS, int STAGES>
 __global__ void __launch_bounds__(kStreamThreads, 1)
@@ -209,15 +258,32 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     // ------------------------------ producer ------------------------------
     if (lane == 0) {
       const uint64_t pol = l2_load_policy<UPDATE>();
+      constexpr bool TS = UPDATE && kTmaStore;
+      // TMA-store mode: the unit each stage last held (its results go out first)
+      int pend_s[STAGES];
+      int64_t pend_e0[STAGES];
+      uint32_t pend_bytes[STAGES];
       int s = 0, i = 0;
       for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
         const int stage = i % STAGES;
-        if (i >= STAGES) mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
+        if (i >= STAGES) {
+          mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
+          if (TS) {
+            store_unit(b.seg[pend_s[stage]], pend_e0[stage], pend_bytes[stage],
+                       sbuf + (size_t)stage * NARR * kUnit, kUnit);
+            bulk_wait_read_all();  // stage readable again
+          }
+        }
         while (u >= unit_prefix[s + 1]) ++s;
         const Seg& sg = b.seg[s];
         const int64_t e0 = (int64_t)(u - unit_prefix[s]) * kUnit;
         const int64_t ne = min((int64_t)kUnit, sg.n - e0);
         const uint32_t bytes = (uint32_t)(ne & ~(int64_t)3) * 4u;
+        if (TS) {
+          pend_s[stage] = s;
+          pend_e0[stage] = e0;
+          pend_bytes[stage] = bytes;
+        }
         float* dst = sbuf + (size_t)stage * NARR * kUnit;
         if (bytes) {
           mbar_arrive_expect_tx(&full_bar[stage], NARR * bytes);
@@ -230,6 +296,16 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         } else {
           mbar_arrive(&full_bar[stage]);
         }
+      }
+      if (TS) {  // drain: results of the last (up to STAGES) units
+        const int n_units = i;
+        for (int j = (n_units > STAGES ? n_units - STAGES : 0); j < n_units; ++j) {
+          const int stage = j % STAGES;
+          mbar_wait(&empty_bar[stage], (j / STAGES) & 1);
+          store_unit(b.seg[pend_s[stage]], pend_e0[stage], pend_bytes[stage],
+                     sbuf + (size_t)stage * NARR * kUnit, kUnit);
+        }
+        bulk_wait_all();
       }
     }
     return;
@@ -317,9 +393,16 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
               adamw1(g4.y, t4.y, m4.y, v4.y, sc);
               adamw1(g4.z, t4.z, m4.z, v4.z, sc);
               adamw1(g4.w, t4.w, m4.w, v4.w, sc);
-              st_stream(sg.theta + e0 + e, t4);
-              st_stream(sg.m + e0 + e, m4);
-              st_stream(sg.v + e0 + e, v4);
+              if (kTmaStore) {  // results back into the stage; the producer bulk-stores them
+                float* w = const_cast<float*>(sg_);
+                *reinterpret_cast<float4*>(w + kUnit + e) = t4;
+                *reinterpret_cast<float4*>(w + 2 * kUnit + e) = m4;
+                *reinterpret_cast<float4*>(w + 3 * kUnit + e) = v4;
+              } else {
+                st_stream(sg.theta + e0 + e, t4);
+                st_stream(sg.m + e0 + e, m4);
+                st_stream(sg.v + e0 + e, v4);
+              }
             }
           } else if (e < ne) {
 #pragma unroll
@@ -344,6 +427,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       }
     }
     }
+    if (UPDATE && kTmaStore) fence_proxy_async_smem();  // results visible to the bulk store
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[stage]);  // this warp is done with the stage
     consumer_sync();

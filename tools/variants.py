@@ -12,9 +12,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "k2_nofast": ["GRASS_K2_NOFAST"],
+    "store_ef": ["GRASS_K2_STORE_EF"],
+    "load_ef": ["GRASS_K2_LOAD_EF"],
+    "load_ef_store_ef": ["GRASS_K2_LOAD_EF", "GRASS_K2_STORE_EF"],
+    "stg": ["GRASS_K2_STG_STORE"],
     "base_again": [],
-    "k2_nofast_again": ["GRASS_K2_NOFAST"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
