@@ -401,31 +401,75 @@ def test_state_roundtrip():
 
 
 # --------------------------------------- full BASELINE sizes (sampled parity)
-def test_llama2_7b_layers_sampled_parity():
-    """Two LLaMA-2-7B decoder layers (N_p = 202,383,360) in the launch
-    configuration bench.py times: full norms vs the oracle, AdamW checked on
-    sampled elements (the oracle computes them one by one)."""
-    shape = MODELS["llama2-7b"]
+@pytest.mark.parametrize("model", ["llama2-7b", "llama3-8b", "llama2-13b"])
+def test_full_size_layers_sampled_parity(model):
+    """Decoder layers of the BASELINE.json model shapes (7B: N_p = 202,383,360;
+    8B: 218,112,000; 13B: 317,204,480) in the launch configuration bench.py
+    times: probe norms (K1) and fused-update norms (K2) of the full layers vs
+    the oracle, AdamW over two steps checked on sampled elements (first/last
+    4096 and 200k random; the oracle computes them one by one)."""
+    shape = MODELS[model]
     n = shape.layer_numel
     numel = [n] * 3
     gr = G.Grass(numel, gamma=2, weight_decay=0.01)
     sig = grad_sigmas(3, 0)
     ids = [2, 0]
     params = [layer_params(n, l, device=DEV, norm_numel=shape.norm_numel) for l in ids]
-    grads = [layer_grad(n, l, sig[l], device=DEV) for l in ids]
     rng = np.random.default_rng(0)
     idx = np.unique(np.concatenate([np.arange(4096), n - 1 - np.arange(4096),
                                     rng.integers(0, n, 200_000)]))
     ti = torch.from_numpy(idx).to(DEV)
-    th_in = [_np(p[ti]) for p in params]
-    g_s = [_np(g[ti]) for g in grads]
-    gr.step_layers(ids, params, grads, 3e-5)
+    # probing pass over all three layers (K1)
+    probe = [layer_grad(n, l, sig[l], step=99, device=DEV) for l in range(3)]
+    gr.mgn_accumulate([0, 1, 2], probe)
     st = gr.get_mgn()
-    for k, l in enumerate(ids):
-        assert_ss_close(st["last_ss"][l], O.sq_norm(_np(grads[k])))
-        th_o, m_o, v_o = O.adamw_step(th_in[k], np.zeros_like(th_in[k]), np.zeros_like(th_in[k]),
-                                      g_s[k], 1, float(np.float32(3e-5)), B1, B2, EPS, 0.01)
-        m_gpu, v_gpu, t = gr.read_state(l)
-        assert t == 1
-        assert_state_close(_np(params[k][ti]), m_gpu[idx], v_gpu[idx], th_o, m_o, v_o, th_in[k],
-                           np.zeros_like(th_in[k]), g_s[k])
+    for l in range(3):
+        assert_ss_close(st["last_ss"][l], O.sq_norm(_np(probe[l])))
+    del probe
+    m_o = [np.zeros(idx.size, np.float32) for _ in ids]
+    v_o = [np.zeros(idx.size, np.float32) for _ in ids]
+    for step in range(2):
+        grads = [layer_grad(n, l, sig[l], step=step, device=DEV) for l in ids]
+        th_in = [_np(p[ti]) for p in params]
+        g_s = [_np(g[ti]) for g in grads]
+        gr.step_layers(ids, params, grads, 3e-5)
+        st = gr.get_mgn()
+        for k, l in enumerate(ids):
+            assert_ss_close(st["last_ss"][l], O.sq_norm(_np(grads[k])))
+            m_gpu, v_gpu, t = gr.read_state(l)
+            assert t == step + 1
+            th_o, m1, v1 = O.adamw_step(th_in[k], m_o[k], v_o[k], g_s[k], t, float(np.float32(3e-5)),
+                                        B1, B2, EPS, 0.01)
+            assert_state_close(_np(params[k][ti]), m_gpu[idx], v_gpu[idx], th_o, m1, v1, th_in[k],
+                               m_o[k], g_s[k])
+            m_o[k], v_o[k] = m_gpu[idx], v_gpu[idx]
+        del grads
+
+
+def test_full_size_offload_and_period_bit_identical():
+    """configs[2] shapes: 7B layers through the default offload pipeline
+    (16 Mi chunks, 3 ring slots) and through period residency are
+    bit-identical to the resident update."""
+    shape = MODELS["llama2-7b"]
+    n = shape.layer_numel
+    numel = [n] * 3
+    ctxs = [G.Grass(numel, gamma=2), G.Grass(numel, gamma=2, offload=True),
+            G.Grass(numel, gamma=2, offload=True, residency=G.RESIDENCY_PERIOD)]
+    base = [layer_params(n, l, device=DEV, norm_numel=shape.norm_numel) for l in range(3)]
+    params = [[p.clone() for p in base] for _ in ctxs]
+    del base
+    for step, ids in enumerate([[0, 1], [1, 2], [1, 2]]):
+        grads = [layer_grad(n, l, 1e-4, step=step, device=DEV) for l in ids]
+        for gr, ps in zip(ctxs, params):
+            gr.step_layers(ids, [ps[l] for l in ids], grads, 3e-5)
+        del grads
+    torch.cuda.synchronize()
+    for l in range(3):
+        for k in (1, 2):
+            assert torch.equal(params[0][l], params[k][l]), (l, k)
+    for l in (0, 1):
+        ref = ctxs[0].read_state(l)
+        for k in (1, 2):
+            got = ctxs[k].read_state(l)
+            assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1]), (l, k)
+    assert ctxs[0].get_mgn()["S"] == ctxs[1].get_mgn()["S"] == ctxs[2].get_mgn()["S"]
