@@ -59,7 +59,9 @@ typedef enum {
   GRASS_E_CUDA = 3,      /* CUDA runtime error (message in grass_last_error) */
   GRASS_E_NCCL = 4,      /* NCCL error or NCCL unavailable when world > 1 */
   GRASS_E_OOM = 5,       /* device or pinned-host allocation failed */
-  GRASS_E_NONFINITE = 6  /* a gradient contained inf/nan (sticky, see above) */
+  GRASS_E_NONFINITE = 6, /* a gradient contained inf/nan (sticky, see above) */
+  GRASS_E_IO = 7         /* checkpoint file error: open/short read/write, corrupt length
+                            or CRC32 mismatch (integrity error) */
 } grass_status;
 
 typedef enum {
@@ -199,6 +201,21 @@ grass_status grass_flush_states(grass_ctx* ctx);
  * restore).  Synchronises the context first. */
 grass_status grass_write_state(grass_ctx* ctx, int32_t layer, const float* m_in,
                                const float* v_in, int64_t t_in);
+
+/* Checkpoint of this rank's whole optimizer + sampler state (
+ * SPEC.md:192-199 shard serialisation): header {magic "GRASSCK1", version,
+ * N_L, world, rank, committed, N_p[], shard_len[], t_l[], m_l[] (committed
+ * MGN), p[], S[], c[]} with a CRC32, then per layer one blob (m shard then v
+ * shard, fp32) preceded by its 64-bit byte length and its CRC32 (zlib
+ * polynomial).  Synchronises; period-resident layers are flushed first.
+ * Errors: GRASS_E_IO (cannot write). */
+grass_status grass_save_state(grass_ctx* ctx, const char* path);
+
+/* Restores a checkpoint written by grass_save_state into a context created
+ * with the same N_L, N_p[], world and rank (else GRASS_E_INVALID).  A short
+ * file, a wrong length or a CRC mismatch is an integrity error (GRASS_E_IO)
+ * and leaves the context unchanged. */
+grass_status grass_load_state(grass_ctx* ctx, const char* path);
 
 /* Introspection of the MGN state (host arrays [N_L], any may be NULL):
  * committed m_l, window sum S_l, window count c_l, last fp64 squared norm of

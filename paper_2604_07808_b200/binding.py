@@ -16,14 +16,14 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # library (tools/variants.py); the default is the in-tree product build.
 LIB_PATH = os.environ.get("GRASS_LIB_PATH") or os.path.join(_PKG, "libgrass.so")
 
-OK, E_INVALID, E_STATE, E_CUDA, E_NCCL, E_OOM, E_NONFINITE = range(7)
+OK, E_INVALID, E_STATE, E_CUDA, E_NCCL, E_OOM, E_NONFINITE, E_IO = range(8)
 POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM = range(3)
 DECIDE_PROBE, DECIDE_COMMIT_RESAMPLE, DECIDE_RESAMPLE, DECIDE_CONTINUE = range(4)
 RESIDENCY_STEP, RESIDENCY_PERIOD = range(2)
 NCCL_ID_BYTES = 128
 
 _STATUS = {0: "GRASS_OK", 1: "GRASS_E_INVALID", 2: "GRASS_E_STATE", 3: "GRASS_E_CUDA",
-           4: "GRASS_E_NCCL", 5: "GRASS_E_OOM", 6: "GRASS_E_NONFINITE"}
+           4: "GRASS_E_NCCL", 5: "GRASS_E_OOM", 6: "GRASS_E_NONFINITE", 7: "GRASS_E_IO"}
 
 
 class GrassError(RuntimeError):
@@ -67,6 +67,8 @@ _SIGS = {
                                    C.POINTER(C.c_int64)]),
     "grass_write_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64]),
     "grass_flush_states": (C.c_int, [C.c_void_p]),
+    "grass_save_state": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "grass_load_state": (C.c_int, [C.c_void_p, C.c_char_p]),
     "grass_get_mgn": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                 C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                 C.POINTER(C.c_double)]),
@@ -293,6 +295,12 @@ class Grass:
         if m.size != n or v.size != n:
             raise ValueError("state size must equal the shard length")
         _check(lib().grass_write_state(self._h, layer, m.ctypes.data, v.ctypes.data, t), self._h)
+
+    def save_state(self, path: str):
+        _check(lib().grass_save_state(self._h, os.fsencode(path)), self._h)
+
+    def load_state(self, path: str):
+        _check(lib().grass_load_state(self._h, os.fsencode(path)), self._h)
 
     def flush_states(self):
         _check(lib().grass_flush_states(self._h), self._h)

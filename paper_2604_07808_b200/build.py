@@ -78,7 +78,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str | Non
         objs.append(obj)
     tmp = out_path + ".tmp"
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
-          "-ldl", "-lpthread", "-lrt"], verbose)
+          "-ldl", "-lpthread", "-lrt", "-lz"], verbose)
     os.replace(tmp, out_path)
     with open(os.path.join(build_dir, "ptxas.log"), "w") as fh:
         fh.write("\n".join(log))

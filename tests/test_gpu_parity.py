@@ -473,3 +473,67 @@ def test_full_size_offload_and_period_bit_identical():
             got = ctxs[k].read_state(l)
             assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1]), (l, k)
     assert ctxs[0].get_mgn()["S"] == ctxs[1].get_mgn()["S"] == ctxs[2].get_mgn()["S"]
+
+
+# ------------------------------------------------ f4: checkpoint (CRC32)
+@pytest.mark.parametrize("mode", ["resident", "offload", "period"])
+def test_checkpoint_roundtrip_and_integrity(tmp_path, mode):
+    import struct
+    import zlib
+    numel = [4096 * 3 + 8, 4096, 20]
+    kw = {"resident": {}, "offload": {"offload": True, "chunk_elems": 4096},
+          "period": {"offload": True, "chunk_elems": 4096, "residency": G.RESIDENCY_PERIOD}}[mode]
+    a = G.Grass(numel, gamma=2, **kw)
+    params = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    a.mgn_accumulate([0, 1, 2], [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)])
+    a.update_probs()
+    for step, ids in enumerate([[0, 1], [2, 1], [2, 1]]):
+        a.step_layers(ids, [params[l] for l in ids],
+                      [layer_grad(numel[l], l, 1e-3, step=step, device=DEV) for l in ids], 1e-3)
+    path = str(tmp_path / "ck.bin")
+    a.save_state(path)
+    # the file format is checkable with an independent CRC32 (zlib)
+    raw = open(path, "rb").read()
+    assert raw[:8] == b"GRASSCK1"
+    (hlen,) = struct.unpack_from("<Q", raw, 12)
+    (hcrc,) = struct.unpack_from("<I", raw, 20)
+    assert zlib.crc32(raw[24:24 + hlen]) == hcrc
+    off = 24 + hlen
+    for n in numel:
+        ln, crc = struct.unpack_from("<QI", raw, off)
+        assert ln == 8 * n and zlib.crc32(raw[off + 12:off + 12 + ln]) == crc
+        off += 12 + ln
+    assert off == len(raw)
+    b = G.Grass(numel, gamma=2, **kw)
+    b.load_state(path)
+    for l in range(3):
+        x, y = a.read_state(l), b.read_state(l)
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]) and x[2] == y[2]
+    ma, mb = a.get_mgn(), b.get_mgn()
+    assert ma["m"] == mb["m"] and ma["probs"] == mb["probs"] and ma["S"] == mb["S"] and ma["c"] == mb["c"]
+    # continuing from the restored state gives the same update as continuing the original
+    pa = [p.clone() for p in params]
+    g = [layer_grad(numel[l], l, 1e-3, step=7, device=DEV) for l in (0, 2)]
+    a.step_layers([0, 2], [params[0], params[2]], g, 1e-3)
+    b.step_layers([0, 2], [pa[0], pa[2]], g, 1e-3)
+    torch.cuda.synchronize()
+    assert torch.equal(params[0], pa[0]) and torch.equal(params[2], pa[2])
+    # corruption: one flipped byte in a blob, a truncated file -> integrity error, state unchanged
+    bad = bytearray(raw)
+    bad[-5] ^= 0x40
+    open(path, "wb").write(bytes(bad))
+    before = b.read_state(2)
+    with pytest.raises(G.GrassError) as e:
+        b.load_state(path)
+    assert e.value.status == G.binding.E_IO and "CRC32" in str(e.value)
+    after = b.read_state(2)
+    assert np.array_equal(before[0], after[0]) and np.array_equal(before[1], after[1])
+    open(path, "wb").write(raw[:-100])
+    with pytest.raises(G.GrassError) as e:
+        b.load_state(path)
+    assert e.value.status == G.binding.E_IO
+    open(path, "wb").write(raw)
+    c = G.Grass(numel[:2], gamma=2, **kw)
+    with pytest.raises(G.GrassError) as e:
+        c.load_state(path)
+    assert e.value.status == G.binding.E_INVALID
