@@ -106,6 +106,11 @@ typedef struct grass_config {
                                   in HBM while it stays trainable; swapped only when the
                                   sampled set changes) */
   int32_t cache_layers;        /* GRASS_RESIDENCY_PERIOD: device layer slots (>= gamma; 0 = gamma) */
+  double max_grad_norm;        /* > 0: clip each grass_step_layers call's gradients by their
+                                  global norm, coef = min(1, max/(||g||+1e-6)) (torch
+                                  clip_grad_norm_; paper silent; DESIGN R17).
+                                  Two passes (norm, then update: 32 B/param); the MGN
+                                  still sees the raw norm (R9).  0 = off (default). */
 } grass_config;
 
 typedef enum {

@@ -283,6 +283,16 @@ def adamw_step(theta, m, v, g, t: int, lr: float, beta1: float = 0.9,
     return th2.astype(np.float32), m1.astype(np.float32), v1.astype(np.float32)
 
 
+def clip_coefficient(sq_norms, max_norm: float) -> float:
+    """Optional global-norm clipping (paper silent; "optional
+    global-norm clip flag", reading R17): total = sqrt(sum of the trainable
+    layers' squared norms), coef = min(1, max_norm / (total + 1e-6)) —
+    torch.nn.utils.clip_grad_norm_ semantics.  The clipped gradient g*coef
+    feeds AdamW; the MGN still sees the raw norm (R9)."""
+    total = math.sqrt(math.fsum(sq_norms))
+    return min(1.0, max_norm / (total + 1e-6))
+
+
 # ---------------------------------------------------------------------------
 # Schedule   (PAPER.md:111-121; reading R11: T_u = T_s)
 # ---------------------------------------------------------------------------
@@ -344,14 +354,21 @@ class GrassOracle:
         return sample_layers(self.probs if probs is None else probs, self.gamma,
                              self.seed, period)
 
-    def step_layers(self, layer_ids, params, grads, lr):
+    def step_layers(self, layer_ids, params, grads, lr, max_grad_norm=None):
         """AdamW on each listed layer (ascending id, reading R12) and MGN
-        accumulation of its gradient norm; params updated in place (fp32)."""
+        accumulation of its (raw) gradient norm; params updated in place
+        (fp32).  With max_grad_norm the gradients of this call are clipped by
+        their global norm first (R17), rounded to fp32 like a stored grad."""
         order = sorted(range(len(layer_ids)), key=lambda i: layer_ids[i])
+        if max_grad_norm:
+            coef = clip_coefficient([sq_norm(g) for g in grads], max_grad_norm)
+            eff = [(np.asarray(g, np.float64) * coef).astype(np.float32) for g in grads]
+        else:
+            eff = grads
         for i in order:
             l = layer_ids[i]
             self.t[l] += 1
-            th, m1, v1 = adamw_step(params[i], self.m[l], self.v[l], grads[i],
+            th, m1, v1 = adamw_step(params[i], self.m[l], self.v[l], eff[i],
                                     self.t[l], lr, self.beta1, self.beta2,
                                     self.eps, self.wd)
             params[i][...] = th

@@ -43,6 +43,7 @@ class GrassConfig(C.Structure):
         ("offload", C.c_int32), ("overlap", C.c_int32), ("chunk_elems", C.c_int64),
         ("ring_slots", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("residency", C.c_int32), ("cache_layers", C.c_int32),
+        ("max_grad_norm", C.c_double),
     ]
 
 
@@ -193,7 +194,7 @@ class Grass:
                  seed: int = 1234, device: int = 0, offload: bool = False, overlap: bool = True,
                  chunk_elems: int = 0, ring_slots: int = 0, rank: int = 0, world: int = 1,
                  process_group=None, force_nccl: bool = False, residency: int = RESIDENCY_STEP,
-                 cache_layers: int = 0):
+                 cache_layers: int = 0, max_grad_norm: float = 0.0):
         L = lib()
         self.layer_numel = [int(x) for x in layer_numel]
         self.n_layers = len(self.layer_numel)
@@ -213,6 +214,7 @@ class Grass:
         cfg.chunk_elems, cfg.ring_slots = chunk_elems, ring_slots
         cfg.rank, cfg.world = rank, world
         cfg.residency, cfg.cache_layers = residency, cache_layers
+        cfg.max_grad_norm = max_grad_norm
         self._uid = None
         if world == 1 and force_nccl:
             self._uid = C.create_string_buffer(nccl_unique_id(), NCCL_ID_BYTES)

@@ -83,6 +83,11 @@ struct grass_ctx {
   std::vector<double> mgn, probs;
   bool committed = false;
 
+  // global-norm clipping (R17): device coefficient, and the multiplier the
+  // next launches use (NULL = none)
+  float* d_coef = nullptr;
+  const float* cur_coef = nullptr;
+
   Comm comm;
   bool has_comm = false;
   bool dp = false;  // data-parallel (NCCL) path: world > 1, or world = 1 with a unique id
@@ -221,6 +226,10 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
     if (cfg->cache_layers < 0 || cfg->cache_layers > cfg->n_layers)
       return bad("cache_layers must lie in [0, N_L]");
   }
+  if (!(cfg->max_grad_norm >= 0.0) || !std::isfinite(cfg->max_grad_norm))
+    return bad("max_grad_norm must be finite and >= 0");
+  if (cfg->max_grad_norm > 0.0 && cfg->n_layers > kMaxClipLayers)
+    return bad("clipping supports at most 1024 layers");
   return GRASS_OK;
 }
 
@@ -266,6 +275,7 @@ Batch make_batch(const grass_ctx* c, int32_t mode) {
   b.beta2 = (float)c->cfg.beta2;
   b.one_minus_beta2 = (float)(1.0 - c->cfg.beta2);
   b.eps = (float)c->cfg.eps;
+  b.coef = c->cur_coef;
   return b;
 }
 
@@ -518,6 +528,7 @@ void free_ctx(grass_ctx* c) {
   dfree(c->st.shard_ss);
   dfree(c->d_gather);
   dfree(c->d_gscratch);
+  dfree(c->d_coef);
   dfree(c->d_ring);
   if (c->state_block) {
     if (c->cfg.offload)
@@ -641,10 +652,13 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     c->layer_done_valid.assign(c->nl, 0);
   }
 
+  CUDA_TRY(c, dalloc((void**)&c->d_coef, sizeof(float)));
   c->dp = W > 1 || cfg->nccl_unique_id != nullptr;
   if (c->dp) {
     CUDA_TRY(c, dalloc((void**)&c->d_gather, sizeof(double) * (size_t)W * c->nl));
-    CUDA_TRY(c, dalloc((void**)&c->d_gscratch, sizeof(float) * (size_t)c->max_shard));
+    // clipping needs every active layer's averaged shard across its two passes
+    const size_t scratch_layers = cfg->max_grad_norm > 0.0 ? (size_t)cfg->gamma : 1;
+    CUDA_TRY(c, dalloc((void**)&c->d_gscratch, sizeof(float) * (size_t)c->max_shard * scratch_layers));
     if (!c->comm.init(cfg->nccl_unique_id, cfg->rank, W, &c->err)) return GRASS_E_NCCL;
     c->has_comm = true;
   }
@@ -760,8 +774,47 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool sharded = c->dp;
-  const int32_t mode = sharded ? kFinalizeShard : kFinalizeMgn;
+  const bool clip = c->cfg.max_grad_norm > 0.0;
+  const int32_t mode = clip ? kFinalizeNone : (sharded ? kFinalizeShard : kFinalizeMgn);
   const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
+  struct CoefReset {  // the clip multiplier only applies inside this call
+    grass_ctx* c;
+    ~CoefReset() { c->cur_coef = nullptr; }
+  } coef_reset{c};
+  if (clip) {
+    // pass 1 (R17): raw norms of this call's (DP-averaged) gradients; they feed
+    // the MGN window (R9) and the global clip coefficient
+    if (!sharded) {
+      Batch b1 = make_batch(c, kFinalizeMgn);
+      for (int i : order) {
+        if (b1.nseg == kMaxSeg && (s = flush(c, &b1, false, st)) != GRASS_OK) return s;
+        push_seg(&b1, range_seg(c, ids[i], grads[i], 0, c->numel[ids[i]]));
+      }
+      if ((s = flush(c, &b1, false, st)) != GRASS_OK) return s;
+    } else {
+      for (int j = 0; j < (int)order.size(); ++j) {
+        const int i = order[j], l = ids[i];
+        float* gs = c->d_gscratch + (size_t)j * c->max_shard;
+        if (!c->comm.reduce_scatter_avg_f32(grads[i], gs, (size_t)c->shard_len[l], st, &c->err))
+          return GRASS_E_NCCL;
+        c->launches++;
+        Batch b1 = make_batch(c, kFinalizeShard);
+        Seg sg = range_seg(c, l, gs, 0, c->shard_len[l]);
+        sg.out_slot = j;
+        push_seg(&b1, sg);
+        if ((s = flush(c, &b1, false, st)) != GRASS_OK) return s;
+      }
+      if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+    }
+    ClipArgs ca;
+    std::memset(&ca, 0, sizeof(ca));
+    ca.n = (int32_t)order.size();
+    ca.max_norm = c->cfg.max_grad_norm;
+    for (int j = 0; j < ca.n; ++j) ca.layer[j] = ids[order[j]];
+    CUDA_TRY(c, launch_clip_coef(ca, c->st, c->d_coef, st));
+    c->launches++;
+    c->cur_coef = c->d_coef;
+  }
   std::vector<int> slot_of, victim_of;
   if (period) {
     cache_plan(c, ids, order, &slot_of, &victim_of);
@@ -775,7 +828,9 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
     c->t[l] += 1;  // per-layer step count (R2); validated above, so this step happens
     const int64_t off = c->shard_off[l], len = c->shard_len[l];
     const float* g = grads[i];
-    if (sharded) {
+    if (sharded && clip) {
+      g = c->d_gscratch + (size_t)j * c->max_shard;  // averaged in pass 1
+    } else if (sharded) {
       if (!c->comm.reduce_scatter_avg_f32(grads[i], c->d_gscratch, (size_t)len, st, &c->err))
         return GRASS_E_NCCL;
       c->launches++;
@@ -823,7 +878,7 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
     }
   }
   if ((s = flush(c, &b, true, st)) != GRASS_OK) return s;
-  if (sharded && (s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+  if (sharded && !clip && (s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
   if (c->cfg.offload && c->cfg.overlap) {
     // join: the caller stream reaches "done" only after every write-back
     cudaEvent_t e = take_event(c);

@@ -25,7 +25,11 @@ constexpr int kUnroll = 2;                     // 128-bit accesses per array per
 constexpr int64_t kTile = (int64_t)kThreads * kVec * kUnroll;  // 4096 elements
 constexpr int kMaxSeg = 64;                    // segments per launch
 
-enum FinalizeMode : int32_t { kFinalizeMgn = 0, kFinalizeShard = 1 };
+// kFinalizeMgn: S_l += sqrt(ss/N_p), c_l += 1; kFinalizeShard: write this rank's
+// shard ss for the cross-rank sum; kFinalizeNone: pass 2 of clipped updates
+// (the MGN already saw the raw norm in pass 1).
+enum FinalizeMode : int32_t { kFinalizeMgn = 0, kFinalizeShard = 1, kFinalizeNone = 2 };
+constexpr int kMaxClipLayers = 1024;
 
 // One contiguous range of one layer processed by a launch.
 struct Seg {
@@ -53,6 +57,7 @@ struct Batch {
   int32_t nseg;
   int32_t mode;            // FinalizeMode
   float beta1, one_minus_beta1, beta2, one_minus_beta2, eps;
+  const float* coef;       // device scalar multiplying g in the update (clipping), or NULL
 };
 
 // Device-resident MGN / reduction state (all arrays indexed by layer id unless noted).
@@ -82,6 +87,14 @@ struct RankSumArgs {
 cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const DevState& st,
                             cudaStream_t s);
 int fused_grid(bool update, int device);
+// Global-norm clip coefficient of the listed layers from last_ss (fp64,
+// ascending layer order): coef = min(1, max_norm / (sqrt(sum) + 1e-6)).
+struct ClipArgs {
+  int32_t n;
+  double max_norm;
+  int32_t layer[kMaxClipLayers];
+};
+cudaError_t launch_clip_coef(const ClipArgs& a, const DevState& st, float* coef, cudaStream_t s);
 
 // host_policy.cpp
 uint64_t splitmix64(uint64_t x);

@@ -51,6 +51,7 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 struct AdamScalars {
   float b1, omb1, b2, omb2, eps, decay, step, inv_bc2s;
+  float cf;  // gradient multiplier of the update: global-norm clip coefficient, else 1
 };
 
 // One element of AdamW (torch.optim.AdamW semantics, R1), fp32 storage:
@@ -62,6 +63,7 @@ struct AdamScalars {
 // parity bar, and the IEEE sequences cost ~3% of K2's time (measured A/B).
 __device__ __forceinline__ void adamw1(float g, float& th, float& m, float& v,
                                        const AdamScalars& s) {
+  g *= s.cf;  // exact when cf == 1
   const float t1 = th * s.decay;
   const float m1 = fmaf(s.b1, m, s.omb1 * g);
   const float v1 = fmaf(s.b2, v, (s.omb2 * g) * g);
@@ -195,15 +197,15 @@ __device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, 
   for (int i = threadIdx.x; i < sg.layer_tiles; i += kThreads) a += __ldcg(P + i);
   const double ss = consumer_sum(a, red);
   if (threadIdx.x == 0) {
-    st.last_ss[sg.layer] = ss;
     if (mode == kFinalizeMgn) {
+      st.last_ss[sg.layer] = ss;
       if (isfinite(ss)) {
         st.S[sg.layer] += sqrt(ss / (double)sg.layer_numel);  // Eq. 2 inner term
         st.c[sg.layer] += 1;
       } else {
         atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins
       }
-    } else {
+    } else if (mode == kFinalizeShard) {
       st.shard_ss[sg.out_slot] = ss;
     }
     st.counters[sg.layer] = 0u;  // ready for the next step
@@ -312,6 +314,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   }
 
   // ------------------------------ consumers -------------------------------
+  const float cf = (UPDATE && b.coef) ? *b.coef : 1.0f;
   int s = 0, i = 0;
   for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
     const int stage = i % STAGES;
@@ -320,6 +323,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     AdamScalars sc;
     sc.b1 = b.beta1; sc.omb1 = b.one_minus_beta1; sc.b2 = b.beta2; sc.omb2 = b.one_minus_beta2;
     sc.eps = b.eps; sc.decay = sg.decay; sc.step = sg.step_size; sc.inv_bc2s = sg.inv_bc2_sqrt;
+    sc.cf = cf;
     const int ui = u - unit_prefix[s];
     const int64_t e0 = (int64_t)ui * kUnit;
     const int ne = (int)min((int64_t)kUnit, sg.n - e0);
@@ -473,6 +477,14 @@ __global__ void grass_rank_sum_kernel(const double* __restrict__ gathered,
   }
 }
 
+__global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const DevState st,
+                                       float* coef) {
+  if (threadIdx.x != 0) return;
+  double tot = 0.0;
+  for (int j = 0; j < a.n; ++j) tot += st.last_ss[a.layer[j]];
+  coef[0] = (float)fmin(1.0, a.max_norm / (sqrt(tot) + 1e-6));
+}
+
 // Production configuration.
 #ifndef GRASS_UPD_STAGES
 #define GRASS_UPD_STAGES 2
@@ -516,6 +528,11 @@ cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const 
                             cudaStream_t s) {
   if (a.n <= 0) return cudaSuccess;
   grass_rank_sum_kernel<<<1, 64, 0, s>>>(gathered, a, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_clip_coef(const ClipArgs& a, const DevState& st, float* coef, cudaStream_t s) {
+  grass_clip_coef_kernel<<<1, 32, 0, s>>>(a, st, coef);
   return cudaGetLastError();
 }
 

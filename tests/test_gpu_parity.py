@@ -537,3 +537,51 @@ def test_checkpoint_roundtrip_and_integrity(tmp_path, mode):
     with pytest.raises(G.GrassError) as e:
         c.load_state(path)
     assert e.value.status == G.binding.E_INVALID
+
+
+# ------------------------------------- f4: optional global-norm clipping (R17)
+@pytest.mark.parametrize("max_norm", [1e-3, 10.0])
+def test_clipping_vs_oracle(max_norm):
+    numel = [65_536, 4097, 3 * 4096]
+    lr, wd = 1e-3, 0.01
+    gr = G.Grass(numel, gamma=2, weight_decay=wd, max_grad_norm=max_norm)
+    orc = O.GrassOracle(numel, gamma=2, weight_decay=wd)
+    sig = grad_sigmas(3, 2)
+    params = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    for step, ids in enumerate([[0, 1], [2, 0], [1, 2]]):
+        grads = [layer_grad(numel[l], l, sig[l] * 100, step=step, device=DEV) for l in ids]
+        th_in = [_np(params[l]).copy() for l in ids]
+        m_in = [orc.m[l].copy() for l in ids]
+        gr.step_layers(ids, [params[l] for l in ids], grads, lr)
+        host = [t.copy() for t in th_in]
+        orc.step_layers(ids, host, [_np(g) for g in grads], float(np.float32(lr)), max_grad_norm=max_norm)
+        for k, l in enumerate(ids):
+            m_gpu, v_gpu, t = gr.read_state(l)
+            assert_state_close(_np(params[l]), m_gpu, v_gpu, host[k], orc.m[l], orc.v[l], th_in[k],
+                               m_in[k], _np(grads[k]))
+            orc.m[l], orc.v[l] = m_gpu, v_gpu
+    st = gr.get_mgn()   # the MGN saw the RAW norms (R9), exactly once per step
+    assert st["c"] == orc.mgn.c
+    assert st["S"] == pytest.approx(orc.mgn.S, rel=1e-7)
+
+
+def test_clipping_inactive_is_bit_identical_and_paths_agree():
+    numel = [3 * 4096 + 8, 65_536]
+    ref = G.Grass(numel, gamma=2)
+    big = G.Grass(numel, gamma=2, max_grad_norm=1e9)                 # coef == 1
+    kw = dict(gamma=2, max_grad_norm=1e-2)
+    clips = [G.Grass(numel, **kw), G.Grass(numel, force_nccl=True, **kw),
+             G.Grass(numel, offload=True, chunk_elems=4096, **kw),
+             G.Grass(numel, offload=True, chunk_elems=4096, residency=G.RESIDENCY_PERIOD, **kw)]
+    ps = [[layer_params(n, l, device=DEV) for l, n in enumerate(numel)] for _ in range(2 + len(clips))]
+    for step in range(3):
+        grads = [layer_grad(n, l, 1e-2, step=step, device=DEV) for l, n in enumerate(numel)]
+        for gr, p in zip([ref, big] + clips, ps):
+            gr.step_layers([0, 1], p, grads, 1e-3)
+    torch.cuda.synchronize()
+    for l in range(2):
+        assert torch.equal(ps[0][l], ps[1][l])                     # no clipping -> same bits
+        for k in range(3, 2 + len(clips)):
+            assert torch.equal(ps[2][l], ps[k][l]), k              # DP / offload / period agree
+        assert not torch.equal(ps[0][l], ps[2][l])                 # and clipping did act
+    assert ref.get_mgn()["S"] == big.get_mgn()["S"] == clips[0].get_mgn()["S"] == clips[1].get_mgn()["S"]

@@ -340,3 +340,19 @@ def test_gamma_equals_NL_degenerates_to_plain_adamw():
         for p, tp in zip(params, tparams):
             np.testing.assert_allclose(p, tp.detach().numpy(), rtol=1e-6, atol=1e-9)
     assert orc.t == [4, 4, 4]
+
+
+# ------------------------------------------------ R17: global-norm clipping
+def test_clip_coefficient_matches_torch_clip_grad_norm():
+    rng = np.random.default_rng(11)
+    for max_norm in (1e-3, 0.05, 1.0, 1e3):
+        gs = [rng.standard_normal(k).astype(np.float32) * 0.01 for k in (17, 300, 5)]
+        ps = [torch.nn.Parameter(torch.zeros(len(g), dtype=torch.float64)) for g in gs]
+        for p, g in zip(ps, gs):
+            p.grad = torch.from_numpy(g.astype(np.float64))
+        total = torch.nn.utils.clip_grad_norm_(ps, max_norm)
+        coef = O.clip_coefficient([O.sq_norm(g) for g in gs], max_norm)
+        assert math.sqrt(sum(O.sq_norm(g) for g in gs)) == pytest.approx(float(total), rel=1e-14)
+        for p, g in zip(ps, gs):
+            np.testing.assert_allclose(p.grad.numpy(), g.astype(np.float64) * coef, rtol=1e-14)
+        assert coef <= 1.0 and (coef == 1.0) == (max_norm >= float(total) + 1e-6)
