@@ -88,6 +88,12 @@ struct grass_ctx {
   float* d_coef = nullptr;
   const float* cur_coef = nullptr;
 
+  // data-parallel overlap: NCCL runs on its own stream so that
+  // RS(l+1) || K2(l) || AG(l-1); gradient shards are double-buffered
+  cudaStream_t comm_s = nullptr;
+  cudaEvent_t ev_cs_start = nullptr, ev_cs_end = nullptr, ev_rs[2] = {nullptr, nullptr},
+              ev_k2[2] = {nullptr, nullptr};
+
   Comm comm;
   bool has_comm = false;
   bool dp = false;  // data-parallel (NCCL) path: world > 1, or world = 1 with a unique id
@@ -343,6 +349,58 @@ grass_status cross_rank_finish(grass_ctx* c, const int32_t* ids, const std::vect
   return GRASS_OK;
 }
 
+// ---- data-parallel schedule on the comm stream --------------
+// Shard buffer slot of the j-th layer of a call (double-buffered).
+float* rs_slot(grass_ctx* c, int j) { return c->d_gscratch + (size_t)(j & 1) * c->max_shard; }
+
+// Comm stream starts after everything already enqueued on the caller stream
+// (the gradients are produced there).
+grass_status comm_begin(grass_ctx* c, cudaStream_t s) {
+  CUDA_TRY(c, cudaEventRecord(c->ev_cs_start, s));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->comm_s, c->ev_cs_start, 0));
+  return GRASS_OK;
+}
+
+// N1 for the j-th layer of the call: reduce-scatter(avg) into its slot once
+// the update that last read the slot (layer j-2) has finished.
+grass_status comm_rs(grass_ctx* c, int j, const float* grad, int64_t len) {
+  const int k = j & 1;
+  if (j >= 2) CUDA_TRY(c, cudaStreamWaitEvent(c->comm_s, c->ev_k2[k], 0));
+  if (!c->comm.reduce_scatter_avg_f32(grad, rs_slot(c, j), (size_t)len, c->comm_s, &c->err))
+    return GRASS_E_NCCL;
+  c->launches++;
+  CUDA_TRY(c, cudaEventRecord(c->ev_rs[k], c->comm_s));
+  return GRASS_OK;
+}
+
+// The caller stream waits for the j-th layer's shard.
+grass_status comm_wait_rs(grass_ctx* c, int j, cudaStream_t s) {
+  CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_rs[j & 1], 0));
+  return GRASS_OK;
+}
+
+// After the j-th layer's update on the caller stream: free its slot and (when
+// params != NULL) all-gather the updated parameter shards on the comm stream.
+grass_status comm_after_update(grass_ctx* c, int j, float* params, int64_t off, int64_t len,
+                               cudaStream_t s) {
+  const int k = j & 1;
+  CUDA_TRY(c, cudaEventRecord(c->ev_k2[k], s));
+  if (params) {
+    CUDA_TRY(c, cudaStreamWaitEvent(c->comm_s, c->ev_k2[k], 0));
+    if (!c->comm.all_gather_f32(params + off, params, (size_t)len, c->comm_s, &c->err))
+      return GRASS_E_NCCL;
+    c->launches++;
+  }
+  return GRASS_OK;
+}
+
+// The caller stream joins the comm stream.
+grass_status comm_end(grass_ctx* c, cudaStream_t s) {
+  CUDA_TRY(c, cudaEventRecord(c->ev_cs_end, c->comm_s));
+  CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_cs_end, 0));
+  return GRASS_OK;
+}
+
 // Offload pipeline for one layer range (Fig. 4): per chunk
 // HtoD(m,v) on h2d -> fused update on the caller stream -> DtoH(m,v) on d2h,
 // chained by events through a ring of device slots.  overlap = 0 runs the
@@ -540,10 +598,11 @@ void free_ctx(grass_ctx* c) {
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
   for (auto& pe : c->ev_pending) cudaEventDestroy(pe.second);
-  for (cudaEvent_t e : {c->ev_call, c->ev_evict, c->ev_fill})
+  for (cudaEvent_t e : {c->ev_call, c->ev_evict, c->ev_fill, c->ev_cs_start, c->ev_cs_end, c->ev_rs[0],
+                        c->ev_rs[1], c->ev_k2[0], c->ev_k2[1]})
     if (e) cudaEventDestroy(e);
   dfree(c->d_cache);
-  for (cudaStream_t s : {c->h2d, c->d2h, c->aux})
+  for (cudaStream_t s : {c->h2d, c->d2h, c->aux, c->comm_s})
     if (s) cudaStreamDestroy(s);
   delete c;
 }
@@ -656,8 +715,12 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   c->dp = W > 1 || cfg->nccl_unique_id != nullptr;
   if (c->dp) {
     CUDA_TRY(c, dalloc((void**)&c->d_gather, sizeof(double) * (size_t)W * c->nl));
-    // clipping needs every active layer's averaged shard across its two passes
-    const size_t scratch_layers = cfg->max_grad_norm > 0.0 ? (size_t)cfg->gamma : 1;
+    // two shard buffers for the RS || update overlap; clipping keeps every
+    // active layer's averaged shard across its two passes
+    const size_t scratch_layers = std::max<size_t>(2, cfg->max_grad_norm > 0.0 ? (size_t)cfg->gamma : 2);
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_s, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c->ev_cs_start, &c->ev_cs_end, &c->ev_rs[0], &c->ev_rs[1], &c->ev_k2[0], &c->ev_k2[1]})
+      CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     CUDA_TRY(c, dalloc((void**)&c->d_gscratch, sizeof(float) * (size_t)c->max_shard * scratch_layers));
     if (!c->comm.init(cfg->nccl_unique_id, cfg->rank, W, &c->err)) return GRASS_E_NCCL;
     c->has_comm = true;
@@ -746,17 +809,25 @@ grass_status grass_mgn_accumulate(grass_ctx* c, const int32_t* ids, int32_t n,
     }
     if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
   } else {
-    for (int j = 0; j < (int)order.size(); ++j) {
-      const int i = order[j], l = ids[i];
-      if (!c->comm.reduce_scatter_avg_f32(grads[i], c->d_gscratch, (size_t)c->shard_len[l], st, &c->err))
-        return GRASS_E_NCCL;
-      c->launches++;
+    // N1 of layer j+1 on the comm stream overlaps K1 of layer j
+    const int nact = (int)order.size();
+    if ((s = comm_begin(c, st)) != GRASS_OK) return s;
+    if ((s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
+    for (int j = 0; j < nact; ++j) {
+      const int l = ids[order[j]];
+      if (j + 1 < nact) {
+        const int l1 = ids[order[j + 1]];
+        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
+      }
+      if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
       Batch b = make_batch(c, kFinalizeShard);
-      Seg sg = range_seg(c, l, c->d_gscratch, 0, c->shard_len[l]);
+      Seg sg = range_seg(c, l, rs_slot(c, j), 0, c->shard_len[l]);
       sg.out_slot = j;
       push_seg(&b, sg);
       if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
+      if ((s = comm_after_update(c, j, nullptr, 0, 0, st)) != GRASS_OK) return s;
     }
+    if ((s = comm_end(c, st)) != GRASS_OK) return s;
     if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
   }
   return mark_pending(c, st);
@@ -823,7 +894,12 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
     if (c->cfg.overlap && (s = wait_pending(c, c->d2h)) != GRASS_OK) return s;
   }
   Batch b = make_batch(c, mode);
-  for (int j = 0; j < (int)order.size(); ++j) {
+  const int nact = (int)order.size();
+  if (sharded) {
+    if ((s = comm_begin(c, st)) != GRASS_OK) return s;
+    if (!clip && (s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
+  }
+  for (int j = 0; j < nact; ++j) {
     const int i = order[j], l = ids[i];
     c->t[l] += 1;  // per-layer step count (R2); validated above, so this step happens
     const int64_t off = c->shard_off[l], len = c->shard_len[l];
@@ -831,10 +907,12 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
     if (sharded && clip) {
       g = c->d_gscratch + (size_t)j * c->max_shard;  // averaged in pass 1
     } else if (sharded) {
-      if (!c->comm.reduce_scatter_avg_f32(grads[i], c->d_gscratch, (size_t)len, st, &c->err))
-        return GRASS_E_NCCL;
-      c->launches++;
-      g = c->d_gscratch;  // shard-local gradient: index 0 = element `off`
+      if (j + 1 < nact) {  // N1 of the next layer overlaps this layer's update
+        const int l1 = ids[order[j + 1]];
+        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
+      }
+      if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
+      g = rs_slot(c, j);  // shard-local gradient: index 0 = element `off`
     }
     float* theta = params[i] + off;
     if (period) {
@@ -871,13 +949,10 @@ grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, floa
       // world > 1 launches per layer: the shard gradient scratch is reused
       if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
     }
-    if (sharded) {
-      if (!c->comm.all_gather_f32(params[i] + off, params[i], (size_t)len, st, &c->err))
-        return GRASS_E_NCCL;
-      c->launches++;
-    }
+    if (sharded && (s = comm_after_update(c, j, params[i], off, len, st)) != GRASS_OK) return s;  // N2
   }
   if ((s = flush(c, &b, true, st)) != GRASS_OK) return s;
+  if (sharded && (s = comm_end(c, st)) != GRASS_OK) return s;
   if (sharded && !clip && (s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
   if (c->cfg.offload && c->cfg.overlap) {
     // join: the caller stream reaches "done" only after every write-back

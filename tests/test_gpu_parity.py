@@ -585,3 +585,27 @@ def test_clipping_inactive_is_bit_identical_and_paths_agree():
             assert torch.equal(ps[2][l], ps[k][l]), k              # DP / offload / period agree
         assert not torch.equal(ps[0][l], ps[2][l])                 # and clipping did act
     assert ref.get_mgn()["S"] == big.get_mgn()["S"] == clips[0].get_mgn()["S"] == clips[1].get_mgn()["S"]
+
+
+def test_nccl_path_overlap_slot_reuse_gamma4():
+    """gamma = 4 exercises the double-buffered shard slots of the overlapped
+    DP schedule (RS(l+1) || K2(l) || AG(l-1), slot reuse at l >= 2) on a
+    1-rank NCCL communicator: bit-identical to the plain path, for the update
+    and for the probing pass."""
+    numel = [4096 * 5 + 8, 65_536, 4096, 4096 * 3, 12]
+    ref = G.Grass(numel, gamma=4, weight_decay=0.01)
+    dp = G.Grass(numel, gamma=4, weight_decay=0.01, force_nccl=True)
+    p_ref = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    p_dp = [p.clone() for p in p_ref]
+    for step, ids in enumerate([[4, 0, 2, 1], [3, 1, 0, 2], [0, 1, 2, 3]]):
+        grads = [layer_grad(numel[l], l, 1e-3, step=step, device=DEV) for l in ids]
+        ref.step_layers(ids, [p_ref[l] for l in ids], grads, 1e-3)
+        dp.step_layers(ids, [p_dp[l] for l in ids], grads, 1e-3)
+    allg = [layer_grad(n, l, 1e-3, step=5, device=DEV) for l, n in enumerate(numel)]
+    ref.mgn_accumulate(list(range(5)), allg)
+    dp.mgn_accumulate(list(range(5)), allg)
+    torch.cuda.synchronize()
+    for l in range(5):
+        assert torch.equal(p_ref[l], p_dp[l]), l
+    a, b = ref.get_mgn(), dp.get_mgn()
+    assert a["S"] == b["S"] and a["last_ss"] == b["last_ss"] and a["c"] == b["c"]
