@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--impl", default="grass", choices=["grass", "reference"])
     ap.add_argument("--model", default="llama2-7b")
     ap.add_argument("--gamma", type=int, default=2)
-    ap.add_argument("--legs", default="main,probe,offload,period,e2e,cpu",
+    ap.add_argument("--legs", default="main,probe,offload,period,bf16,e2e,cpu",
                     help="comma list of legs to run (main is always run)")
     ap.add_argument("--offload-steps", type=int, default=10)
     ap.add_argument("--lr", type=float, default=3e-5)
@@ -397,6 +397,50 @@ def run_grass(args, rank, world, local):
                           "device_cache_bytes": pctx.device_bytes}
         del pctx
 
+    # ---- bf16 params/grads with fp32 master + moments
+    bf16 = None
+    if "bf16" in legs:
+        del params, grads
+        torch.cuda.empty_cache()
+        p16 = [layer_params(n_p, l, device=dev, norm_numel=shape.norm_numel).to(torch.bfloat16) for l in range(NL)]
+        g16 = [layer_grad(n_p, l, sig[l], step=0, device=dev, rank=rank).to(torch.bfloat16) for l in range(NL)]
+        bctx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, device=local,
+                       rank=rank, world=world, param_dtype=G.DTYPE_BF16)
+        bctx.mgn_accumulate(list(range(NL)), g16, stream=s)
+        bctx.update_probs()
+        bids = bctx.sample_layers(0)
+        bev = []
+
+        def bstep(step, timing):
+            nonlocal bids
+            if timing:
+                e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                e[0].record(s)
+            bctx.step_layers(bids, [p16[l] for l in bids], [g16[l] for l in bids], args.lr, stream=s)
+            if timing:
+                e[1].record(s)
+                bev.append(e)
+            bctx.update_probs()
+            bids = bctx.sample_layers(step + 1)
+        for w in range(args.warmup):
+            bstep(w, False)
+        torch.cuda.synchronize()
+        barrier(world)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(s)
+        for k in range(args.steps):
+            bstep(args.warmup + k, True)
+        b1.record(s)
+        torch.cuda.synchronize()
+        bt = max_over_ranks(b0.elapsed_time(b1) / 1e3, world, dev)
+        bk = statistics.mean(a.elapsed_time(b) for a, b in bev)
+        bgbs = BYTES_PER_PARAM_UPDATE * active / world / (bk / 1e3) / 1e9
+        bf16 = {"workload": f"{args.model}-stack gamma={gamma} bf16 params/grads, fp32 master+m+v, resident",
+                "params_per_s": args.steps * active / bt, "step_ms": bt / args.steps * 1e3,
+                "kernel_ms": bk, "GBps": bgbs, "frac_hbm": bgbs / hbm_peak,
+                "bytes_per_param": BYTES_PER_PARAM_UPDATE}
+        del bctx, p16, g16
+
     # ---- CPU oracle baseline
     cpu = None
     if "cpu" in legs and rank == 0 and world == 1:
@@ -425,7 +469,7 @@ def run_grass(args, rank, world, local):
                          "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "probe": out.get("probe"), "offload": offload,
-            "offload_period": offload_period,
+            "offload_period": offload_period, "bf16": bf16,
         }
         print(json.dumps(line), flush=True)
 

@@ -111,7 +111,17 @@ typedef struct grass_config {
                                   clip_grad_norm_; paper silent; DESIGN R17).
                                   Two passes (norm, then update: 32 B/param); the MGN
                                   still sees the raw norm (R9).  0 = off (default). */
+  int32_t param_dtype;         /* GRASS_DTYPE_FP32: fp32 params/grads (grass_step_layers);
+                                  GRASS_DTYPE_BF16: bf16 params/grads, the context keeps an
+                                  fp32 master copy next to m, v (grass_step_layers_bf16;
+                                  SURVEY 8(f) f3, DESIGN R18). world > 1 then needs every
+                                  N_p divisible by 8*world. */
 } grass_config;
+
+typedef enum {
+  GRASS_DTYPE_FP32 = 0,
+  GRASS_DTYPE_BF16 = 1
+} grass_dtype;
 
 typedef enum {
   GRASS_RESIDENCY_STEP = 0,
@@ -190,6 +200,26 @@ grass_status grass_sample_layers(grass_ctx* ctx, const double* probs, uint64_t p
 grass_status grass_step_layers(grass_ctx* ctx, const int32_t* layer_ids, int32_t n,
                                float* const* params, const float* const* grads, float lr,
                                void* stream);
+
+/* Mixed-precision variants for a context created with GRASS_DTYPE_BF16
+ * (SURVEY 8(f) f3, R18).  Same semantics as the fp32 calls; params/grads are
+ * arrays of DEVICE pointers to bf16 (uint16_t bit patterns), 16-byte aligned.
+ * The norm is of the bf16 gradient (widened exactly).  The update runs on the
+ * context's fp32 master copy (initialised from the bf16 parameter on the
+ * layer's first update), and params[i] receives RNE(master') as bf16.
+ * Calling the fp32 entry points on a bf16 context (or vice versa) is
+ * GRASS_E_INVALID. */
+grass_status grass_mgn_accumulate_bf16(grass_ctx* ctx, const int32_t* layer_ids, int32_t n,
+                                       const uint16_t* const* grads, void* stream);
+grass_status grass_step_layers_bf16(grass_ctx* ctx, const int32_t* layer_ids, int32_t n,
+                                    uint16_t* const* params, const uint16_t* const* grads, float lr,
+                                    void* stream);
+
+/* bf16 contexts: this rank's fp32 master shard of `layer` (host buffer,
+ * shard length) — read / overwrite (a written master counts as initialised).
+ * GRASS_E_STATE on an fp32 context or a layer whose master is not yet set. */
+grass_status grass_read_master(grass_ctx* ctx, int32_t layer, float* out);
+grass_status grass_write_master(grass_ctx* ctx, int32_t layer, const float* in);
 
 /* Copies this rank's m/v shard of `layer` into host buffers m_out/v_out
  * (count = the shard length, grass_shard_range) and its step count; any

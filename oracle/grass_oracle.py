@@ -283,6 +283,35 @@ def adamw_step(theta, m, v, g, t: int, lr: float, beta1: float = 0.9,
     return th2.astype(np.float32), m1.astype(np.float32), v1.astype(np.float32)
 
 
+def bf16_to_f32(bits):
+    """bf16 bit patterns (uint16) -> exact fp32 values (upper half of the fp32 word)."""
+    b = np.asarray(bits, dtype=np.uint16).astype(np.uint32) << np.uint32(16)
+    return b.view(np.float32)
+
+
+def f32_to_bf16(x):
+    """fp32 -> bf16 bit patterns, round to nearest even (NaN kept quiet)."""
+    u = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    nan = np.isnan(np.asarray(x, dtype=np.float32))
+    r = (u + np.uint64(0x7FFF) + ((u >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)
+    r = np.where(nan, (u >> np.uint64(16)) | np.uint64(0x40), r)
+    return r.astype(np.uint16)
+
+
+def adamw_step_bf16(master, m, v, g_bits, t: int, lr: float, beta1: float = 0.9,
+                    beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0,
+                    theta_bits=None):
+    """Mixed-precision AdamW (reading R18): bf16 gradient and
+    parameters, fp32 master copy and moments.  On a layer's first update
+    (theta_bits given) the master is the exact fp32 value of the bf16 parameter.
+    Returns (master', m', v' as fp32, theta' as bf16 bits = RNE(master'))."""
+    if theta_bits is not None:
+        master = bf16_to_f32(theta_bits)
+    g = bf16_to_f32(g_bits)
+    th, m1, v1 = adamw_step(master, m, v, g, t, lr, beta1, beta2, eps, weight_decay)
+    return th, m1, v1, f32_to_bf16(th)
+
+
 def clip_coefficient(sq_norms, max_norm: float) -> float:
     """Optional global-norm clipping (paper silent; "optional
     global-norm clip flag", reading R17): total = sqrt(sum of the trainable

@@ -4,7 +4,7 @@ The product is libgrass.so (C ABI, include/grass.h) built from csrc/; this
 package is its thin ctypes binding.  It never imports oracle/.
 """
 from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_CONTINUE, DECIDE_PROBE, DECIDE_RESAMPLE,
-                      RESIDENCY_PERIOD, RESIDENCY_STEP,
+                      RESIDENCY_PERIOD, RESIDENCY_STEP, DTYPE_BF16, DTYPE_FP32,
                       POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM, Grass, GrassError,
                       exported_symbols, lib, nccl_unique_id, sample_from_probs,
                       schedule_decision, shard_range, softmax_probs, splitmix64, tile_elems,
@@ -14,4 +14,4 @@ __all__ = ["Grass", "GrassError", "lib", "exported_symbols", "nccl_unique_id",
            "sample_from_probs", "schedule_decision", "shard_range", "softmax_probs",
            "splitmix64", "tile_elems", "uniform", "POLICY_ADAPTIVE", "POLICY_STATIC",
            "POLICY_UNIFORM", "DECIDE_PROBE", "DECIDE_COMMIT_RESAMPLE", "DECIDE_RESAMPLE",
-           "DECIDE_CONTINUE", "RESIDENCY_STEP", "RESIDENCY_PERIOD"]
+           "DECIDE_CONTINUE", "RESIDENCY_STEP", "RESIDENCY_PERIOD", "DTYPE_FP32", "DTYPE_BF16"]

@@ -20,6 +20,7 @@ OK, E_INVALID, E_STATE, E_CUDA, E_NCCL, E_OOM, E_NONFINITE, E_IO = range(8)
 POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM = range(3)
 DECIDE_PROBE, DECIDE_COMMIT_RESAMPLE, DECIDE_RESAMPLE, DECIDE_CONTINUE = range(4)
 RESIDENCY_STEP, RESIDENCY_PERIOD = range(2)
+DTYPE_FP32, DTYPE_BF16 = range(2)
 NCCL_ID_BYTES = 128
 
 _STATUS = {0: "GRASS_OK", 1: "GRASS_E_INVALID", 2: "GRASS_E_STATE", 3: "GRASS_E_CUDA",
@@ -43,7 +44,7 @@ class GrassConfig(C.Structure):
         ("offload", C.c_int32), ("overlap", C.c_int32), ("chunk_elems", C.c_int64),
         ("ring_slots", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("residency", C.c_int32), ("cache_layers", C.c_int32),
-        ("max_grad_norm", C.c_double),
+        ("max_grad_norm", C.c_double), ("param_dtype", C.c_int32),
     ]
 
 
@@ -68,6 +69,13 @@ _SIGS = {
                                    C.POINTER(C.c_int64)]),
     "grass_write_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64]),
     "grass_flush_states": (C.c_int, [C.c_void_p]),
+    "grass_mgn_accumulate_bf16": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32,
+                                            C.POINTER(C.c_void_p), C.c_void_p]),
+    "grass_step_layers_bf16": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32,
+                                         C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_float,
+                                         C.c_void_p]),
+    "grass_read_master": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "grass_write_master": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "grass_save_state": (C.c_int, [C.c_void_p, C.c_char_p]),
     "grass_load_state": (C.c_int, [C.c_void_p, C.c_char_p]),
     "grass_get_mgn": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -170,11 +178,12 @@ def _stream_ptr(stream) -> int:
     return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def _ptrs(tensors):
+def _ptrs(tensors, itemsize: int = 4):
     arr = (C.c_void_p * len(tensors))()
     for i, t in enumerate(tensors):
-        if not t.is_cuda or not t.is_contiguous() or t.dtype.itemsize != 4:
-            raise ValueError("layer buffers must be contiguous fp32 CUDA tensors")
+        if not t.is_cuda or not t.is_contiguous() or t.dtype.itemsize != itemsize:
+            raise ValueError(f"layer buffers must be contiguous CUDA tensors of {itemsize}-byte "
+                             "elements (fp32, or bf16 for a bf16 context)")
         arr[i] = t.data_ptr()
     return arr
 
@@ -194,7 +203,7 @@ class Grass:
                  seed: int = 1234, device: int = 0, offload: bool = False, overlap: bool = True,
                  chunk_elems: int = 0, ring_slots: int = 0, rank: int = 0, world: int = 1,
                  process_group=None, force_nccl: bool = False, residency: int = RESIDENCY_STEP,
-                 cache_layers: int = 0, max_grad_norm: float = 0.0):
+                 cache_layers: int = 0, max_grad_norm: float = 0.0, param_dtype: int = DTYPE_FP32):
         L = lib()
         self.layer_numel = [int(x) for x in layer_numel]
         self.n_layers = len(self.layer_numel)
@@ -215,6 +224,8 @@ class Grass:
         cfg.rank, cfg.world = rank, world
         cfg.residency, cfg.cache_layers = residency, cache_layers
         cfg.max_grad_norm = max_grad_norm
+        cfg.param_dtype = param_dtype
+        self.bf16 = param_dtype == DTYPE_BF16
         self._uid = None
         if world == 1 and force_nccl:
             self._uid = C.create_string_buffer(nccl_unique_id(), NCCL_ID_BYTES)
@@ -252,8 +263,9 @@ class Grass:
     # hot path ---------------------------------------------------------------
     def mgn_accumulate(self, layer_ids: Sequence[int], grads, stream=None):
         ids = (C.c_int32 * len(layer_ids))(*layer_ids)
-        _check(lib().grass_mgn_accumulate(self._h, ids, len(layer_ids), _ptrs(grads),
-                                          _stream_ptr(stream)), self._h)
+        f = lib().grass_mgn_accumulate_bf16 if self.bf16 else lib().grass_mgn_accumulate
+        _check(f(self._h, ids, len(layer_ids), _ptrs(grads, 2 if self.bf16 else 4),
+                 _stream_ptr(stream)), self._h)
 
     def update_probs(self):
         out = (C.c_double * self.n_layers)()
@@ -270,8 +282,10 @@ class Grass:
 
     def step_layers(self, layer_ids: Sequence[int], params, grads, lr: float, stream=None):
         ids = (C.c_int32 * len(layer_ids))(*layer_ids)
-        _check(lib().grass_step_layers(self._h, ids, len(layer_ids), _ptrs(params), _ptrs(grads),
-                                       float(lr), _stream_ptr(stream)), self._h)
+        f = lib().grass_step_layers_bf16 if self.bf16 else lib().grass_step_layers
+        isz = 2 if self.bf16 else 4
+        _check(f(self._h, ids, len(layer_ids), _ptrs(params, isz), _ptrs(grads, isz),
+                 float(lr), _stream_ptr(stream)), self._h)
 
     def sync(self):
         _check(lib().grass_sync(self._h), self._h)
@@ -303,6 +317,19 @@ class Grass:
 
     def load_state(self, path: str):
         _check(lib().grass_load_state(self._h, os.fsencode(path)), self._h)
+
+    def read_master(self, layer: int):
+        import numpy as np
+        out = np.empty(self.shard(layer)[1], np.float32)
+        _check(lib().grass_read_master(self._h, layer, out.ctypes.data), self._h)
+        return out
+
+    def write_master(self, layer: int, master):
+        import numpy as np
+        a = np.ascontiguousarray(master, np.float32)
+        if a.size != self.shard(layer)[1]:
+            raise ValueError("master size must equal the shard length")
+        _check(lib().grass_write_master(self._h, layer, a.ctypes.data), self._h)
 
     def flush_states(self):
         _check(lib().grass_flush_states(self._h), self._h)

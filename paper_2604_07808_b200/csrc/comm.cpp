@@ -102,9 +102,10 @@ void Comm::destroy() {
   comm = nullptr;
 }
 
-bool Comm::reduce_scatter_avg_f32(const float* send, float* recv, size_t count, cudaStream_t s,
-                                  std::string* err) {
-  ncclResult_t r = api().ReduceScatter(send, recv, count, ncclFloat32, ncclAvg, comm, s);
+bool Comm::reduce_scatter_avg(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
+                              std::string* err) {
+  ncclResult_t r = api().ReduceScatter(send, recv, count, bf16 ? ncclBfloat16 : ncclFloat32, ncclAvg,
+                                       comm, s);
   if (r != ncclSuccess) {
     *err = nccl_msg("ncclReduceScatter", r);
     return false;
@@ -112,11 +113,11 @@ bool Comm::reduce_scatter_avg_f32(const float* send, float* recv, size_t count, 
   return true;
 }
 
-bool Comm::all_gather_f32(const float* send, float* recv, size_t count, cudaStream_t s,
-                          std::string* err) {
-  ncclResult_t r = api().AllGather(send, recv, count, ncclFloat32, comm, s);
+bool Comm::all_gather(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
+                      std::string* err) {
+  ncclResult_t r = api().AllGather(send, recv, count, bf16 ? ncclBfloat16 : ncclFloat32, comm, s);
   if (r != ncclSuccess) {
-    *err = nccl_msg("ncclAllGather(f32)", r);
+    *err = nccl_msg("ncclAllGather", r);
     return false;
   }
   return true;

@@ -18,12 +18,12 @@ struct Comm {
   int rank = 0, world = 1;
   bool init(const void* unique_id, int rank, int world, std::string* err);
   void destroy();
-  // N1: gradient average, element-sharded (recv = this rank's shard).
-  bool reduce_scatter_avg_f32(const float* send, float* recv, size_t count, cudaStream_t s,
-                              std::string* err);
+  // N1: gradient average, element-sharded (recv = this rank's shard); fp32 or bf16.
+  bool reduce_scatter_avg(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
+                          std::string* err);
   // N2: parameter shards back to every rank (in place when send = recv + rank*count).
-  bool all_gather_f32(const float* send, float* recv, size_t count, cudaStream_t s,
-                      std::string* err);
+  bool all_gather(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
+                  std::string* err);
   // N3: per-layer fp64 shard partials of the norm.
   bool all_gather_f64(const double* send, double* recv, size_t count, cudaStream_t s,
                       std::string* err);

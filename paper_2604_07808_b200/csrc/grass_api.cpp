@@ -1,17 +1,17 @@
 // grass_api.cpp — the C ABI (include/grass.h): validation, context, the MGN
-// commit / EMA on host (fp64), the offload pipeline and the data-parallel
-// orchestration.  Compiled with -ffp-contract=off (host fp64 rounds as written).
+// commit / EMA on host (fp64), the offload pipeline, period residency, the
+// data-parallel orchestration and checkpointing.  Compiled with
+// -ffp-contract=off (host fp64 rounds exactly as written).
 #include <cuda_runtime_api.h>
+#include <zlib.h>
 
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <thread>
-#include <cstdio>
-
-#include <zlib.h>
 #include <vector>
 
 #include "comm.h"
@@ -23,11 +23,11 @@ namespace {
 
 thread_local std::string g_thread_err;
 
-// 16 Mi elements = 64 MiB per moment per chunk; with 3 ring slots this measured
-// best on the 7B stack (profiles/r01_offload_sweep.json).
+// 16 Mi elements = 64 MiB per state array per chunk; with 3 ring slots this
+// measured best on the 7B stack (profiles/r01_offload_sweep.json).
 constexpr int64_t kDefaultChunk = 16ll << 20;
 constexpr int kDefaultSlots = 3;
-constexpr int64_t kAlignElems = 64;           // 256-byte alignment of every state slice
+constexpr int64_t kAlignElems = 64;  // 256-byte alignment of every state slice
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 int64_t tiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
@@ -39,23 +39,28 @@ struct grass_ctx {
   int nl = 0;
   std::vector<int64_t> numel, shard_off, shard_len, tiles, part_base;
   int64_t max_shard = 0;
+  bool bf16 = false;  // GRASS_DTYPE_BF16: bf16 params/grads, fp32 master copy (R18)
+  int ns = 2;         // optimizer state arrays per layer: m, v [, master]
+  size_t esz = 4;     // bytes per parameter / gradient element
 
   // device reduction / MGN state; S, c and flag live in ONE block so a commit
   // is a single stream-ordered D2H copy into a pinned mirror.
   DevState st{};
-  void* d_mgn = nullptr;        // [S: N_L fp64][c: N_L int64][flag: int32]
-  void* h_mgn = nullptr;        // pinned host mirror of d_mgn
+  void* d_mgn = nullptr;  // [S: N_L fp64][c: N_L int64][flag: int32]
+  void* h_mgn = nullptr;  // pinned host mirror of d_mgn
   size_t mgn_bytes = 0;
-  double* d_gather = nullptr;   // world x N_L fp64 (all-gathered shard partials)
-  float* d_gscratch = nullptr;  // world > 1: this rank's averaged-gradient shard
+  double* d_gather = nullptr;  // world x N_L fp64 (all-gathered shard partials)
+  char* d_gscratch = nullptr;  // DP: averaged-gradient shards (2, or gamma when clipping)
 
-  // optimizer state: this rank's shard of every layer
-  float* state_block = nullptr;  // device (resident) or pinned host (offload)
-  std::vector<float*> m, v;
+  // optimizer state of this rank's shard of every layer: arr[0] = m,
+  // arr[1] = v, arr[2] = fp32 master (bf16 mode); device or pinned host
+  float* state_block = nullptr;
+  std::vector<float*> arr[3];
+  std::vector<char> master_valid;
   std::vector<int64_t> t;
 
-  // offload ring
-  float* d_ring = nullptr;
+  // offload ring (step residency)
+  float* d_ring = nullptr;  // slots x ns x chunk floats
   int slots = 0;
   int64_t chunk = 0;
   int64_t ring_pos = 0;
@@ -65,14 +70,14 @@ struct grass_ctx {
   std::vector<cudaEvent_t> ev_layer_done;  // last write-back of each layer
   std::vector<char> layer_done_valid;
 
-  // period residency: HBM cache of whole-layer m/v slots
-  float* d_cache = nullptr;          // cache_slots x [m | v] of max_shard floats each
+  // period residency: HBM cache of whole-layer state slots
+  float* d_cache = nullptr;  // cache_slots x ns x max_shard floats
   int cache_slots = 0;
   std::vector<int> slot_layer, layer_slot;
   std::vector<int64_t> slot_use;
   std::vector<char> slot_dirty;
   int64_t call_seq = 0;
-  cudaEvent_t ev_call = nullptr, ev_evict = nullptr, ev_fill = nullptr;
+  cudaEvent_t ev_evict = nullptr, ev_fill = nullptr;
 
   // outstanding stream-ordered work (for the synchronising calls): the last
   // event recorded on each stream the caller used
@@ -109,17 +114,23 @@ struct grass_ctx {
 
 namespace {
 
-#define CUDA_TRY(ctx, expr)                                                          \
-  do {                                                                               \
-    cudaError_t e_ = (expr);                                                         \
-    if (e_ != cudaSuccess)                                                           \
+#define CUDA_TRY(ctx, expr)                                                            \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
       return (ctx)->fail(e_ == cudaErrorMemoryAllocation ? GRASS_E_OOM : GRASS_E_CUDA, \
-                         std::string(#expr) + ": " + cudaGetErrorString(e_));        \
+                         std::string(#expr) + ": " + cudaGetErrorString(e_));          \
   } while (0)
 
 grass_status set_thread_err(grass_status s, const std::string& msg) {
   g_thread_err = msg;
   return s;
+}
+
+// Element `off` of a parameter / gradient buffer of the context's dtype.
+void* elem(void* p, int64_t off, size_t esz) { return static_cast<char*>(p) + off * (int64_t)esz; }
+const void* elem(const void* p, int64_t off, size_t esz) {
+  return static_cast<const char*>(p) + off * (int64_t)esz;
 }
 
 cudaEvent_t take_event(grass_ctx* c) {
@@ -216,12 +227,15 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
   if (!(cfg->eps > 0.0) || !(cfg->weight_decay >= 0.0)) return bad("eps > 0, weight_decay >= 0");
   if (cfg->policy < GRASS_POLICY_ADAPTIVE || cfg->policy > GRASS_POLICY_UNIFORM)
     return bad("unknown policy");
+  if (cfg->param_dtype != GRASS_DTYPE_FP32 && cfg->param_dtype != GRASS_DTYPE_BF16)
+    return bad("unknown param_dtype");
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return bad("bad rank/world");
   if (cfg->world > 1) {
     if (!cfg->nccl_unique_id) return bad("world > 1 needs nccl_unique_id");
+    const int64_t q = (cfg->param_dtype == GRASS_DTYPE_BF16 ? 8 : 4) * (int64_t)cfg->world;
     for (int i = 0; i < cfg->n_layers; ++i)
-      if (cfg->layer_numel[i] % (4 * (int64_t)cfg->world) != 0)
-        return bad("world > 1 needs every layer_numel divisible by 4*world");
+      if (cfg->layer_numel[i] % q != 0)
+        return bad("world > 1 needs every layer_numel divisible by 4*world (8*world for bf16)");
   }
   if (cfg->offload) {
     if (cfg->chunk_elems < 0 || cfg->chunk_elems % kTile != 0)
@@ -240,8 +254,11 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
 }
 
 // Resolve, validate and order the layer list of a hot-path call.
-grass_status check_call(grass_ctx* c, const int32_t* ids, int32_t n, const void* const* p1,
-                        const void* const* p2, std::vector<int>* order) {
+grass_status check_call(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_t n,
+                        const void* const* p1, const void* const* p2, std::vector<int>* order) {
+  if (bf16_call != c->bf16)
+    return c->fail(GRASS_E_INVALID, c->bf16 ? "bf16 context: use the *_bf16 entry points"
+                                            : "fp32 context: the *_bf16 entry points need GRASS_DTYPE_BF16");
   if (!ids || n < 1 || n > c->nl) return c->fail(GRASS_E_INVALID, "need 1 <= n <= N_L layer ids");
   std::vector<char> seen(c->nl, 0);
   for (int i = 0; i < n; ++i) {
@@ -249,20 +266,20 @@ grass_status check_call(grass_ctx* c, const int32_t* ids, int32_t n, const void*
     if (seen[ids[i]]) return c->fail(GRASS_E_INVALID, "duplicate layer id");
     seen[ids[i]] = 1;
   }
-  for (const void* const* arr : {p1, p2}) {
-    if (arr == nullptr) continue;
+  for (const void* const* a : {p1, p2}) {
+    if (a == nullptr) continue;
     for (int i = 0; i < n; ++i) {
-      const void* p = arr[i];
+      const void* p = a[i];
       if (!p) return c->fail(GRASS_E_INVALID, "NULL buffer pointer");
       if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
         return c->fail(GRASS_E_INVALID, "layer buffers must be 16-byte aligned");
-      cudaPointerAttributes a;
-      if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
         cudaGetLastError();
         return c->fail(GRASS_E_INVALID, "not a CUDA pointer");
       }
-      if (!(a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ||
-          a.device != c->cfg.device)
+      if (!(at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ||
+          at.device != c->cfg.device)
         return c->fail(GRASS_E_INVALID, "layer buffers must be device memory on the context's GPU");
     }
   }
@@ -282,6 +299,7 @@ Batch make_batch(const grass_ctx* c, int32_t mode) {
   b.one_minus_beta2 = (float)(1.0 - c->cfg.beta2);
   b.eps = (float)c->cfg.eps;
   b.coef = c->cur_coef;
+  b.bf16 = c->bf16 ? 1 : 0;
   return b;
 }
 
@@ -300,11 +318,15 @@ grass_status flush(grass_ctx* c, Batch* b, bool update, cudaStream_t s) {
   return GRASS_OK;
 }
 
-// Seg for [off, off+n) of layer l's shard (off a multiple of kTile).
-Seg range_seg(const grass_ctx* c, int l, const float* g, int64_t off, int64_t n) {
+// Seg for [off, off+n) of layer l's shard (off a multiple of kTile); `g`
+// points at element 0 of the shard-local gradient.
+Seg range_seg(const grass_ctx* c, int l, const void* g, int64_t off, int64_t n) {
   Seg s;
   std::memset(&s, 0, sizeof(s));
-  s.g = g + off;
+  if (c->bf16)
+    s.g16 = static_cast<const uint16_t*>(g) + off;
+  else
+    s.g = static_cast<const float*>(g) + off;
   s.n = n;
   s.tiles = (int32_t)tiles_of(n);
   s.layer = l;
@@ -313,6 +335,20 @@ Seg range_seg(const grass_ctx* c, int l, const float* g, int64_t off, int64_t n)
   s.part_index = c->part_base[l] + off / kTile;
   s.layer_numel = c->numel[l];
   return s;
+}
+
+// Update operands of a range: `param` is element 0 of the range in the
+// caller's parameter buffer; state[a] the m, v (, master) of the range.
+void set_update(const grass_ctx* c, Seg* s, void* param, float* const* state, bool init_master) {
+  s->m = state[0];
+  s->v = state[1];
+  if (c->bf16) {
+    s->theta = state[2];
+    s->theta16 = static_cast<uint16_t*>(param);
+    s->init_master = init_master ? 1 : 0;
+  } else {
+    s->theta = static_cast<float*>(param);
+  }
 }
 
 void adam_scalars(const grass_ctx* c, int l, float lr, Seg* s) {
@@ -329,8 +365,7 @@ void adam_scalars(const grass_ctx* c, int l, float lr, Seg* s) {
 grass_status cross_rank_finish(grass_ctx* c, const int32_t* ids, const std::vector<int>& order,
                                cudaStream_t s) {
   const int n = (int)order.size();
-  if (!c->comm.all_gather_f64(c->st.shard_ss, c->d_gather, (size_t)n, s, &c->err))
-    return GRASS_E_NCCL;
+  if (!c->comm.all_gather_f64(c->st.shard_ss, c->d_gather, (size_t)n, s, &c->err)) return GRASS_E_NCCL;
   c->launches++;
   for (int j0 = 0; j0 < n; j0 += kMaxSeg) {
     RankSumArgs a;
@@ -350,8 +385,9 @@ grass_status cross_rank_finish(grass_ctx* c, const int32_t* ids, const std::vect
 }
 
 // ---- data-parallel schedule on the comm stream --------------
-// Shard buffer slot of the j-th layer of a call (double-buffered).
-float* rs_slot(grass_ctx* c, int j) { return c->d_gscratch + (size_t)(j & 1) * c->max_shard; }
+// Shard buffer of slot k (2 double-buffered slots; gamma slots when clipping).
+void* gs_slot(grass_ctx* c, int k) { return c->d_gscratch + (size_t)k * c->max_shard * c->esz; }
+void* rs_slot(grass_ctx* c, int j) { return gs_slot(c, j & 1); }
 
 // Comm stream starts after everything already enqueued on the caller stream
 // (the gradients are produced there).
@@ -363,10 +399,10 @@ grass_status comm_begin(grass_ctx* c, cudaStream_t s) {
 
 // N1 for the j-th layer of the call: reduce-scatter(avg) into its slot once
 // the update that last read the slot (layer j-2) has finished.
-grass_status comm_rs(grass_ctx* c, int j, const float* grad, int64_t len) {
+grass_status comm_rs(grass_ctx* c, int j, const void* grad, int64_t len) {
   const int k = j & 1;
   if (j >= 2) CUDA_TRY(c, cudaStreamWaitEvent(c->comm_s, c->ev_k2[k], 0));
-  if (!c->comm.reduce_scatter_avg_f32(grad, rs_slot(c, j), (size_t)len, c->comm_s, &c->err))
+  if (!c->comm.reduce_scatter_avg(grad, rs_slot(c, j), (size_t)len, c->bf16, c->comm_s, &c->err))
     return GRASS_E_NCCL;
   c->launches++;
   CUDA_TRY(c, cudaEventRecord(c->ev_rs[k], c->comm_s));
@@ -381,13 +417,13 @@ grass_status comm_wait_rs(grass_ctx* c, int j, cudaStream_t s) {
 
 // After the j-th layer's update on the caller stream: free its slot and (when
 // params != NULL) all-gather the updated parameter shards on the comm stream.
-grass_status comm_after_update(grass_ctx* c, int j, float* params, int64_t off, int64_t len,
+grass_status comm_after_update(grass_ctx* c, int j, void* params, int64_t off, int64_t len,
                                cudaStream_t s) {
   const int k = j & 1;
   CUDA_TRY(c, cudaEventRecord(c->ev_k2[k], s));
   if (params) {
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm_s, c->ev_k2[k], 0));
-    if (!c->comm.all_gather_f32(params + off, params, (size_t)len, c->comm_s, &c->err))
+    if (!c->comm.all_gather(elem(params, off, c->esz), params, (size_t)len, c->bf16, c->comm_s, &c->err))
       return GRASS_E_NCCL;
     c->launches++;
   }
@@ -401,56 +437,59 @@ grass_status comm_end(grass_ctx* c, cudaStream_t s) {
   return GRASS_OK;
 }
 
-// Offload pipeline for one layer range (Fig. 4): per chunk
-// HtoD(m,v) on h2d -> fused update on the caller stream -> DtoH(m,v) on d2h,
-// chained by events through a ring of device slots.  overlap = 0 runs the
+// Launches the update of one range [off, off+n) of layer l whose states live
+// at `state` (already offset to `off`).
+grass_status update_range(grass_ctx* c, int l, const Seg& base, void* param, const void* g, int64_t off,
+                          int64_t n, float* const* state, bool init, int32_t mode, cudaStream_t s) {
+  Seg sg = range_seg(c, l, g, off, n);
+  set_update(c, &sg, elem(param, off, c->esz), state, init);
+  sg.decay = base.decay;
+  sg.step_size = base.step_size;
+  sg.inv_bc2_sqrt = base.inv_bc2_sqrt;
+  sg.out_slot = base.out_slot;
+  Batch b = make_batch(c, mode);
+  push_seg(&b, sg);
+  return flush(c, &b, true, s);
+}
+
+// Offload pipeline for one layer (Fig. 4): per chunk
+// HtoD(states) on h2d -> fused update on the caller stream -> DtoH(states) on
+// d2h, chained by events through a ring of device slots.  overlap = 0 runs the
 // three stages serially on the caller stream (Fig. 4 "vanilla").
-grass_status offload_layer(grass_ctx* c, int l, Seg base, float* theta, const float* g, float lr,
+grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, const void* g, bool init,
                            int32_t mode, cudaStream_t s) {
   const int64_t len = c->shard_len[l];
   const bool overlap = c->cfg.overlap != 0;
-  float* hm = c->m[l];
-  float* hv = c->v[l];
   if (overlap && c->layer_done_valid[l])  // previous write-back of this layer
     CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, c->ev_layer_done[l], 0));
   for (int64_t off = 0; off < len; off += c->chunk) {
     const int64_t n = std::min(c->chunk, len - off);
     const int slot = (int)(c->ring_pos++ % c->slots);
-    float* dm = c->d_ring + (int64_t)slot * 2 * c->chunk;
-    float* dv = dm + c->chunk;
+    float* ring[3];
+    for (int a = 0; a < c->ns; ++a) ring[a] = c->d_ring + ((int64_t)slot * c->ns + a) * c->chunk;
     const size_t bytes = (size_t)n * sizeof(float);
     cudaStream_t sh = overlap ? c->h2d : s, sd = overlap ? c->d2h : s;
     if (overlap && c->slot_used[slot]) CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_free[slot], 0));
-    CUDA_TRY(c, cudaMemcpyAsync(dm, hm + off, bytes, cudaMemcpyHostToDevice, sh));
-    CUDA_TRY(c, cudaMemcpyAsync(dv, hv + off, bytes, cudaMemcpyHostToDevice, sh));
+    for (int a = 0; a < c->ns; ++a)
+      if (!(a == 2 && init))  // an uninitialised master is written, not read
+        CUDA_TRY(c, cudaMemcpyAsync(ring[a], c->arr[a][l] + off, bytes, cudaMemcpyHostToDevice, sh));
     if (overlap) {
       CUDA_TRY(c, cudaEventRecord(c->ev_h2d[slot], sh));
       CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_h2d[slot], 0));
     }
-    Seg sg = range_seg(c, l, g, off, n);
-    sg.theta = theta + off;
-    sg.m = dm;
-    sg.v = dv;
-    sg.decay = base.decay;
-    sg.step_size = base.step_size;
-    sg.inv_bc2_sqrt = base.inv_bc2_sqrt;
-    sg.out_slot = base.out_slot;
-    Batch b = make_batch(c, mode);
-    push_seg(&b, sg);
-    grass_status st = flush(c, &b, true, s);
+    grass_status st = update_range(c, l, base, param, g, off, n, ring, init, mode, s);
     if (st != GRASS_OK) return st;
     if (overlap) {
       CUDA_TRY(c, cudaEventRecord(c->ev_comp[slot], s));
       CUDA_TRY(c, cudaStreamWaitEvent(sd, c->ev_comp[slot], 0));
     }
-    CUDA_TRY(c, cudaMemcpyAsync(hm + off, dm, bytes, cudaMemcpyDeviceToHost, sd));
-    CUDA_TRY(c, cudaMemcpyAsync(hv + off, dv, bytes, cudaMemcpyDeviceToHost, sd));
+    for (int a = 0; a < c->ns; ++a)
+      CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][l] + off, ring[a], bytes, cudaMemcpyDeviceToHost, sd));
     if (overlap) {
       CUDA_TRY(c, cudaEventRecord(c->ev_free[slot], sd));
       c->slot_used[slot] = 1;
     }
   }
-  (void)lr;
   if (overlap) {
     CUDA_TRY(c, cudaEventRecord(c->ev_layer_done[l], c->d2h));
     c->layer_done_valid[l] = 1;
@@ -459,13 +498,14 @@ grass_status offload_layer(grass_ctx* c, int l, Seg base, float* theta, const fl
 }
 
 // ---- period residency -----------------------------------
-float* cache_m(grass_ctx* c, int slot) { return c->d_cache + (size_t)slot * 2 * c->max_shard; }
-float* cache_v(grass_ctx* c, int slot) { return cache_m(c, slot) + c->max_shard; }
+float* cache_arr(grass_ctx* c, int slot, int a) {
+  return c->d_cache + ((size_t)slot * c->ns + a) * c->max_shard;
+}
 
 // Slot for every listed layer: hits keep their slot; misses take an empty slot
 // or evict the least recently used layer that is not trainable in this call.
-void cache_plan(grass_ctx* c, const int32_t* ids, const std::vector<int>& order,
-                std::vector<int>* slot_of, std::vector<int>* victim_of) {
+void cache_plan(grass_ctx* c, const int32_t* ids, const std::vector<int>& order, std::vector<int>* slot_of,
+                std::vector<int>* victim_of) {
   const int n = (int)order.size();
   slot_of->assign(n, -1);
   victim_of->assign(n, -1);
@@ -494,16 +534,14 @@ void cache_plan(grass_ctx* c, const int32_t* ids, const std::vector<int>& order,
   }
 }
 
-// Brings layer l's m/v into `slot` (evicting `victim` to its host home first,
-// chunk by chunk, so write-back and fetch overlap on the duplex link) and
-// updates l chunk by chunk as its states arrive.  Nothing is written back
+// Brings layer l's states into `slot` (evicting `victim` to its host home
+// first, chunk by chunk, so write-back and fetch overlap on the duplex link)
+// and updates l chunk by chunk as its states arrive.  Nothing is written back
 // after the update: the slot stays resident and dirty.
-grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, Seg base, float* theta,
-                           const float* g, int32_t mode, cudaStream_t s) {
+grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, const Seg& base, void* param,
+                           const void* g, bool init, int32_t mode, cudaStream_t s) {
   const bool overlap = c->cfg.overlap != 0;
   cudaStream_t sh = overlap ? c->h2d : s, sd = overlap ? c->d2h : s;
-  float* sm = cache_m(c, slot);
-  float* sv = cache_v(c, slot);
   const int64_t ll = c->shard_len[l];
   const int64_t lv = (victim >= 0 && c->slot_dirty[slot]) ? c->shard_len[victim] : 0;
   if (overlap && c->layer_done_valid[l])  // l's host copy must be final
@@ -511,8 +549,9 @@ grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, Seg base, 
   for (int64_t off = 0; off < std::max(ll, lv); off += c->chunk) {
     if (off < lv) {
       const size_t vb = sizeof(float) * (size_t)std::min(c->chunk, lv - off);
-      CUDA_TRY(c, cudaMemcpyAsync(c->m[victim] + off, sm + off, vb, cudaMemcpyDeviceToHost, sd));
-      CUDA_TRY(c, cudaMemcpyAsync(c->v[victim] + off, sv + off, vb, cudaMemcpyDeviceToHost, sd));
+      for (int a = 0; a < c->ns; ++a)
+        CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][victim] + off, cache_arr(c, slot, a) + off, vb,
+                                    cudaMemcpyDeviceToHost, sd));
       if (overlap && off < ll) {
         CUDA_TRY(c, cudaEventRecord(c->ev_evict, sd));
         CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_evict, 0));
@@ -521,23 +560,17 @@ grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, Seg base, 
     if (off < ll) {
       const int64_t n = std::min(c->chunk, ll - off);
       const size_t bytes = sizeof(float) * (size_t)n;
-      CUDA_TRY(c, cudaMemcpyAsync(sm + off, c->m[l] + off, bytes, cudaMemcpyHostToDevice, sh));
-      CUDA_TRY(c, cudaMemcpyAsync(sv + off, c->v[l] + off, bytes, cudaMemcpyHostToDevice, sh));
+      for (int a = 0; a < c->ns; ++a)
+        if (!(a == 2 && init))
+          CUDA_TRY(c, cudaMemcpyAsync(cache_arr(c, slot, a) + off, c->arr[a][l] + off, bytes,
+                                      cudaMemcpyHostToDevice, sh));
       if (overlap) {
         CUDA_TRY(c, cudaEventRecord(c->ev_fill, sh));
         CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_fill, 0));
       }
-      Seg sg = range_seg(c, l, g, off, n);
-      sg.theta = theta + off;
-      sg.m = sm + off;
-      sg.v = sv + off;
-      sg.decay = base.decay;
-      sg.step_size = base.step_size;
-      sg.inv_bc2_sqrt = base.inv_bc2_sqrt;
-      sg.out_slot = base.out_slot;
-      Batch b = make_batch(c, mode);
-      push_seg(&b, sg);
-      grass_status st = flush(c, &b, true, s);
+      float* st_ptr[3];
+      for (int a = 0; a < c->ns; ++a) st_ptr[a] = cache_arr(c, slot, a) + off;
+      grass_status st = update_range(c, l, base, param, g, off, n, st_ptr, init, mode, s);
       if (st != GRASS_OK) return st;
     }
   }
@@ -562,11 +595,47 @@ grass_status flush_cache(grass_ctx* c) {
     const int l = c->slot_layer[k];
     if (l < 0 || !c->slot_dirty[k]) continue;
     const size_t bytes = sizeof(float) * (size_t)c->shard_len[l];
-    CUDA_TRY(c, cudaMemcpyAsync(c->m[l], cache_m(c, k), bytes, cudaMemcpyDeviceToHost, c->d2h));
-    CUDA_TRY(c, cudaMemcpyAsync(c->v[l], cache_v(c, k), bytes, cudaMemcpyDeviceToHost, c->d2h));
+    for (int a = 0; a < c->ns; ++a)
+      CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][l], cache_arr(c, k, a), bytes, cudaMemcpyDeviceToHost, c->d2h));
     c->slot_dirty[k] = 0;
   }
   CUDA_TRY(c, cudaStreamSynchronize(c->d2h));
+  return GRASS_OK;
+}
+
+// Where the current copy of state array `a` of `layer` lives: device (HBM
+// resident or period cache) or pinned host.
+float* state_ptr(grass_ctx* c, int a, int layer, bool* on_device) {
+  const int slot = c->cache_slots ? c->layer_slot[layer] : -1;
+  if (slot >= 0) {
+    *on_device = true;
+    return cache_arr(c, slot, a);
+  }
+  *on_device = !c->cfg.offload;
+  return c->arr[a][layer];
+}
+
+grass_status copy_state_out(grass_ctx* c, int a, int layer, float* out) {
+  bool dev = false;
+  float* src = state_ptr(c, a, layer, &dev);
+  const size_t bytes = sizeof(float) * (size_t)c->shard_len[layer];
+  if (dev)
+    CUDA_TRY(c, cudaMemcpy(out, src, bytes, cudaMemcpyDeviceToHost));
+  else
+    std::memcpy(out, src, bytes);
+  return GRASS_OK;
+}
+
+grass_status copy_state_in(grass_ctx* c, int a, int layer, const float* in) {
+  bool dev = false;
+  float* dst = state_ptr(c, a, layer, &dev);
+  const size_t bytes = sizeof(float) * (size_t)c->shard_len[layer];
+  if (dev)
+    CUDA_TRY(c, cudaMemcpy(dst, in, bytes, cudaMemcpyHostToDevice));
+  else
+    std::memcpy(dst, in, bytes);
+  const int slot = c->cache_slots ? c->layer_slot[layer] : -1;
+  if (slot >= 0) c->slot_dirty[slot] = 1;  // the cached copy stays authoritative
   return GRASS_OK;
 }
 
@@ -588,6 +657,7 @@ void free_ctx(grass_ctx* c) {
   dfree(c->d_gscratch);
   dfree(c->d_coef);
   dfree(c->d_ring);
+  dfree(c->d_cache);
   if (c->state_block) {
     if (c->cfg.offload)
       cudaFreeHost(c->state_block);
@@ -598,10 +668,9 @@ void free_ctx(grass_ctx* c) {
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
   for (auto& pe : c->ev_pending) cudaEventDestroy(pe.second);
-  for (cudaEvent_t e : {c->ev_call, c->ev_evict, c->ev_fill, c->ev_cs_start, c->ev_cs_end, c->ev_rs[0],
-                        c->ev_rs[1], c->ev_k2[0], c->ev_k2[1]})
+  for (cudaEvent_t e : {c->ev_evict, c->ev_fill, c->ev_cs_start, c->ev_cs_end, c->ev_rs[0], c->ev_rs[1],
+                        c->ev_k2[0], c->ev_k2[1]})
     if (e) cudaEventDestroy(e);
-  dfree(c->d_cache);
   for (cudaStream_t s : {c->h2d, c->d2h, c->aux, c->comm_s})
     if (s) cudaStreamDestroy(s);
   delete c;
@@ -613,6 +682,9 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   c->numel.assign(cfg->layer_numel, cfg->layer_numel + cfg->n_layers);
   c->cfg.layer_numel = nullptr;
   c->cfg.nccl_unique_id = nullptr;
+  c->bf16 = cfg->param_dtype == GRASS_DTYPE_BF16;
+  c->ns = c->bf16 ? 3 : 2;
+  c->esz = c->bf16 ? 2 : 4;
   const int W = cfg->world;
   c->shard_off.resize(c->nl);
   c->shard_len.resize(c->nl);
@@ -629,6 +701,7 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     c->max_shard = std::max(c->max_shard, c->shard_len[l]);
   }
   c->t.assign(c->nl, 0);
+  c->master_valid.assign(c->nl, 0);
   c->mgn.assign(c->nl, 0.0);
   c->probs.assign(c->nl, 1.0 / c->nl);
 
@@ -654,8 +727,8 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   CUDA_TRY(c, dalloc((void**)&c->st.last_ss, sizeof(double) * c->nl));
   CUDA_TRY(c, dalloc((void**)&c->st.shard_ss, sizeof(double) * c->nl));
 
-  // optimizer state (m, v) for this rank's shard of every layer, zeroed
-  const size_t state_bytes = sizeof(float) * 2 * (size_t)state_elems;
+  // optimizer state (m, v [, master]) for this rank's shard of every layer, zeroed
+  const size_t state_bytes = sizeof(float) * (size_t)c->ns * (size_t)state_elems;
   if (cfg->offload) {
     CUDA_TRY(c, cudaHostAlloc((void**)&c->state_block, state_bytes, cudaHostAllocPortable));
     c->host_bytes += (int64_t)state_bytes;
@@ -671,16 +744,13 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   } else {
     CUDA_TRY(c, dalloc((void**)&c->state_block, state_bytes));
   }
-  c->m.resize(c->nl);
-  c->v.resize(c->nl);
   int64_t o = 0;
-  for (int l = 0; l < c->nl; ++l) {
-    c->m[l] = c->state_block + o;
-    o += round_up(c->shard_len[l], kAlignElems);
-  }
-  for (int l = 0; l < c->nl; ++l) {
-    c->v[l] = c->state_block + o;
-    o += round_up(c->shard_len[l], kAlignElems);
+  for (int a = 0; a < c->ns; ++a) {
+    c->arr[a].resize(c->nl);
+    for (int l = 0; l < c->nl; ++l) {
+      c->arr[a][l] = c->state_block + o;
+      o += round_up(c->shard_len[l], kAlignElems);
+    }
   }
 
   if (cfg->offload) {
@@ -689,15 +759,16 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     c->slots = cfg->ring_slots ? cfg->ring_slots : kDefaultSlots;
     if (cfg->residency == GRASS_RESIDENCY_PERIOD) {
       c->cache_slots = std::max(cfg->gamma, cfg->cache_layers);
-      CUDA_TRY(c, dalloc((void**)&c->d_cache, sizeof(float) * 2 * (size_t)c->max_shard * c->cache_slots));
+      CUDA_TRY(c, dalloc((void**)&c->d_cache,
+                         sizeof(float) * (size_t)c->ns * (size_t)c->max_shard * c->cache_slots));
       c->slot_layer.assign(c->cache_slots, -1);
       c->layer_slot.assign(c->nl, -1);
       c->slot_use.assign(c->cache_slots, 0);
       c->slot_dirty.assign(c->cache_slots, 0);
-      for (cudaEvent_t* e : {&c->ev_call, &c->ev_evict, &c->ev_fill})
+      for (cudaEvent_t* e : {&c->ev_evict, &c->ev_fill})
         CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     } else {
-      CUDA_TRY(c, dalloc((void**)&c->d_ring, sizeof(float) * 2 * (size_t)c->chunk * c->slots));
+      CUDA_TRY(c, dalloc((void**)&c->d_ring, sizeof(float) * (size_t)c->ns * (size_t)c->chunk * c->slots));
     }
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
@@ -717,11 +788,11 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     CUDA_TRY(c, dalloc((void**)&c->d_gather, sizeof(double) * (size_t)W * c->nl));
     // two shard buffers for the RS || update overlap; clipping keeps every
     // active layer's averaged shard across its two passes
-    const size_t scratch_layers = std::max<size_t>(2, cfg->max_grad_norm > 0.0 ? (size_t)cfg->gamma : 2);
+    const size_t nslots = std::max<size_t>(2, cfg->max_grad_norm > 0.0 ? (size_t)cfg->gamma : 2);
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_s, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&c->ev_cs_start, &c->ev_cs_end, &c->ev_rs[0], &c->ev_rs[1], &c->ev_k2[0], &c->ev_k2[1]})
       CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    CUDA_TRY(c, dalloc((void**)&c->d_gscratch, sizeof(float) * (size_t)c->max_shard * scratch_layers));
+    CUDA_TRY(c, dalloc((void**)&c->d_gscratch, c->esz * (size_t)c->max_shard * nslots));
     if (!c->comm.init(cfg->nccl_unique_id, cfg->rank, W, &c->err)) return GRASS_E_NCCL;
     c->has_comm = true;
   }
@@ -730,6 +801,215 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   if (c->grid_update < 1 || c->grid_norm < 1) return c->fail(GRASS_E_CUDA, "occupancy query failed");
   CUDA_TRY(c, cudaDeviceSynchronize());
   return GRASS_OK;
+}
+
+// ---- the hot path ----------------------------------------------------------
+
+// Eq. 2 inner term for the listed layers (probing); fp32 or bf16 gradients.
+grass_status mgn_accumulate_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_t n,
+                                 const void* const* grads, void* stream) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!grads) return c->fail(GRASS_E_INVALID, "grads is NULL");
+  std::vector<int> order;
+  grass_status s = check_call(c, bf16_call, ids, n, grads, nullptr, &order);
+  if (s != GRASS_OK) return s;
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!c->dp) {
+    Batch b = make_batch(c, kFinalizeMgn);
+    for (int i : order) {
+      if (b.nseg == kMaxSeg && (s = flush(c, &b, false, st)) != GRASS_OK) return s;
+      push_seg(&b, range_seg(c, ids[i], grads[i], 0, c->numel[ids[i]]));
+    }
+    if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
+  } else {
+    // N1 of layer j+1 on the comm stream overlaps K1 of layer j
+    const int nact = (int)order.size();
+    if ((s = comm_begin(c, st)) != GRASS_OK) return s;
+    if ((s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
+    for (int j = 0; j < nact; ++j) {
+      const int l = ids[order[j]];
+      if (j + 1 < nact) {
+        const int l1 = ids[order[j + 1]];
+        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
+      }
+      if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
+      Batch b = make_batch(c, kFinalizeShard);
+      Seg sg = range_seg(c, l, rs_slot(c, j), 0, c->shard_len[l]);
+      sg.out_slot = j;
+      push_seg(&b, sg);
+      if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
+      if ((s = comm_after_update(c, j, nullptr, 0, 0, st)) != GRASS_OK) return s;
+    }
+    if ((s = comm_end(c, st)) != GRASS_OK) return s;
+    if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+  }
+  return mark_pending(c, st);
+}
+
+// Fused norm + AdamW of the listed layers, with offload / residency / DP /
+// clipping as configured; fp32 or bf16 (master in the context) parameters.
+grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_t n,
+                              void* const* params, const void* const* grads, float lr, void* stream) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!params || !grads) return c->fail(GRASS_E_INVALID, "params/grads is NULL");
+  if (!(lr >= 0.0f) || !std::isfinite(lr)) return c->fail(GRASS_E_INVALID, "lr must be finite, >= 0");
+  std::vector<int> order;
+  grass_status s = check_call(c, bf16_call, ids, n, reinterpret_cast<const void* const*>(params), grads, &order);
+  if (s != GRASS_OK) return s;
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool sharded = c->dp;
+  const bool clip = c->cfg.max_grad_norm > 0.0;
+  const int32_t mode = clip ? kFinalizeNone : (sharded ? kFinalizeShard : kFinalizeMgn);
+  const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
+  const int nact = (int)order.size();
+  struct CoefReset {  // the clip multiplier only applies inside this call
+    grass_ctx* c;
+    ~CoefReset() { c->cur_coef = nullptr; }
+  } coef_reset{c};
+  if (clip) {
+    // pass 1 (R17): raw norms of this call's (DP-averaged) gradients; they feed
+    // the MGN window (R9) and the global clip coefficient
+    if (!sharded) {
+      Batch b1 = make_batch(c, kFinalizeMgn);
+      for (int i : order) {
+        if (b1.nseg == kMaxSeg && (s = flush(c, &b1, false, st)) != GRASS_OK) return s;
+        push_seg(&b1, range_seg(c, ids[i], grads[i], 0, c->numel[ids[i]]));
+      }
+      if ((s = flush(c, &b1, false, st)) != GRASS_OK) return s;
+    } else {
+      for (int j = 0; j < nact; ++j) {
+        const int i = order[j], l = ids[i];
+        if (!c->comm.reduce_scatter_avg(grads[i], gs_slot(c, j), (size_t)c->shard_len[l], c->bf16, st, &c->err))
+          return GRASS_E_NCCL;
+        c->launches++;
+        Batch b1 = make_batch(c, kFinalizeShard);
+        Seg sg = range_seg(c, l, gs_slot(c, j), 0, c->shard_len[l]);
+        sg.out_slot = j;
+        push_seg(&b1, sg);
+        if ((s = flush(c, &b1, false, st)) != GRASS_OK) return s;
+      }
+      if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+    }
+    ClipArgs ca;
+    std::memset(&ca, 0, sizeof(ca));
+    ca.n = nact;
+    ca.max_norm = c->cfg.max_grad_norm;
+    for (int j = 0; j < ca.n; ++j) ca.layer[j] = ids[order[j]];
+    CUDA_TRY(c, launch_clip_coef(ca, c->st, c->d_coef, st));
+    c->launches++;
+    c->cur_coef = c->d_coef;
+  }
+  std::vector<int> slot_of, victim_of;
+  if (period) {
+    cache_plan(c, ids, order, &slot_of, &victim_of);
+    c->call_seq++;
+    // write-backs read cache slots last written by earlier steps' updates
+    if (c->cfg.overlap && (s = wait_pending(c, c->d2h)) != GRASS_OK) return s;
+  }
+  Batch b = make_batch(c, mode);
+  if (sharded) {
+    if ((s = comm_begin(c, st)) != GRASS_OK) return s;
+    if (!clip && (s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
+  }
+  for (int j = 0; j < nact; ++j) {
+    const int i = order[j], l = ids[i];
+    c->t[l] += 1;  // per-layer step count (R2); validated above, so this step happens
+    const bool init = c->bf16 && !c->master_valid[l];
+    c->master_valid[l] = 1;
+    const int64_t off = c->shard_off[l], len = c->shard_len[l];
+    const void* g = grads[i];
+    if (sharded && clip) {
+      g = gs_slot(c, j);  // averaged in pass 1
+    } else if (sharded) {
+      if (j + 1 < nact) {  // N1 of the next layer overlaps this layer's update
+        const int l1 = ids[order[j + 1]];
+        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
+      }
+      if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
+      g = rs_slot(c, j);  // shard-local gradient: index 0 = element `off`
+    }
+    void* param = elem(params[i], off, c->esz);  // this rank's range of the layer
+    Seg base = range_seg(c, l, g, 0, len);
+    adam_scalars(c, l, lr, &base);
+    base.out_slot = j;
+    if (period) {
+      const int slot = slot_of[j];
+      if (c->slot_layer[slot] == l) {  // hit: update in place in HBM, no link traffic
+        float* sp[3];
+        for (int a = 0; a < c->ns; ++a) sp[a] = cache_arr(c, slot, a);
+        set_update(c, &base, param, sp, init);
+        if (b.nseg == kMaxSeg && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+        push_seg(&b, base);
+        if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+      } else if ((s = swap_in_layer(c, l, slot, victim_of[j], base, param, g, init, mode, st)) != GRASS_OK) {
+        return s;
+      }
+      c->slot_use[slot] = c->call_seq;
+      c->slot_dirty[slot] = 1;
+    } else if (c->cfg.offload) {
+      if ((s = offload_layer(c, l, base, param, g, init, mode, st)) != GRASS_OK) return s;
+    } else {
+      float* sp[3];
+      for (int a = 0; a < c->ns; ++a) sp[a] = c->arr[a][l];
+      set_update(c, &base, param, sp, init);
+      if (b.nseg == kMaxSeg && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+      push_seg(&b, base);
+      // DP launches per layer: the shard gradient slot is released after it
+      if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+    }
+    if (sharded && (s = comm_after_update(c, j, params[i], off, len, st)) != GRASS_OK) return s;  // N2
+  }
+  if ((s = flush(c, &b, true, st)) != GRASS_OK) return s;
+  if (sharded && (s = comm_end(c, st)) != GRASS_OK) return s;
+  if (sharded && !clip && (s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+  if (c->cfg.offload && c->cfg.overlap) {
+    // join: the caller stream reaches "done" only after every write-back
+    cudaEvent_t e = take_event(c);
+    if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
+    CUDA_TRY(c, cudaEventRecord(e, c->d2h));
+    CUDA_TRY(c, cudaStreamWaitEvent(st, e, 0));
+    c->ev_free_list.push_back(e);
+  }
+  return mark_pending(c, st);
+}
+
+// ---- checkpoint ------------------------------------------------------------
+const char kCkMagic[8] = {'G', 'R', 'A', 'S', 'S', 'C', 'K', '1'};
+const uint32_t kCkVersion = 1;
+
+uint32_t crc_update(uint32_t crc, const void* p, size_t n) {
+  const Bytef* b = static_cast<const Bytef*>(p);
+  while (n > 0) {
+    const uInt k = (uInt)std::min<size_t>(n, 1u << 30);
+    crc = (uint32_t)crc32(crc, b, k);
+    b += k;
+    n -= k;
+  }
+  return crc;
+}
+
+template <class T>
+void put(std::vector<char>* h, const T* p, size_t n) {
+  const char* b = reinterpret_cast<const char*>(p);
+  h->insert(h->end(), b, b + sizeof(T) * n);
+}
+
+constexpr int kCkInts = 5;  // N_L, world, rank, committed, dtype
+
+std::vector<char> ck_header(grass_ctx* c) {
+  std::vector<char> h;
+  const int32_t ints[kCkInts] = {c->nl, c->cfg.world, c->cfg.rank, c->committed ? 1 : 0, c->cfg.param_dtype};
+  put(&h, ints, kCkInts);
+  put(&h, c->numel.data(), c->nl);
+  put(&h, c->shard_len.data(), c->nl);
+  put(&h, c->t.data(), c->nl);
+  put(&h, c->mgn.data(), c->nl);
+  put(&h, c->probs.data(), c->nl);
+  put(&h, h_S(c), c->nl);
+  put(&h, h_c(c), c->nl);
+  return h;
 }
 
 }  // namespace
@@ -783,186 +1063,33 @@ grass_status grass_create(const grass_config* cfg, grass_ctx** out) {
 
 void grass_destroy(grass_ctx* ctx) { free_ctx(ctx); }
 
-const char* grass_last_error(const grass_ctx* ctx) {
-  return ctx ? ctx->err.c_str() : g_thread_err.c_str();
-}
+const char* grass_last_error(const grass_ctx* ctx) { return ctx ? ctx->err.c_str() : g_thread_err.c_str(); }
 
 grass_status grass_sync(grass_ctx* ctx) {
   if (!ctx) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   return drain(ctx, true);
 }
 
-grass_status grass_mgn_accumulate(grass_ctx* c, const int32_t* ids, int32_t n,
-                                  const float* const* grads, void* stream) {
-  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
-  if (!grads) return c->fail(GRASS_E_INVALID, "grads is NULL");
-  std::vector<int> order;
-  grass_status s = check_call(c, ids, n, reinterpret_cast<const void* const*>(grads), nullptr, &order);
-  if (s != GRASS_OK) return s;
-  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (!c->dp) {
-    Batch b = make_batch(c, kFinalizeMgn);
-    for (int i : order) {
-      if (b.nseg == kMaxSeg && (s = flush(c, &b, false, st)) != GRASS_OK) return s;
-      push_seg(&b, range_seg(c, ids[i], grads[i], 0, c->numel[ids[i]]));
-    }
-    if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
-  } else {
-    // N1 of layer j+1 on the comm stream overlaps K1 of layer j
-    const int nact = (int)order.size();
-    if ((s = comm_begin(c, st)) != GRASS_OK) return s;
-    if ((s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
-    for (int j = 0; j < nact; ++j) {
-      const int l = ids[order[j]];
-      if (j + 1 < nact) {
-        const int l1 = ids[order[j + 1]];
-        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
-      }
-      if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
-      Batch b = make_batch(c, kFinalizeShard);
-      Seg sg = range_seg(c, l, rs_slot(c, j), 0, c->shard_len[l]);
-      sg.out_slot = j;
-      push_seg(&b, sg);
-      if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
-      if ((s = comm_after_update(c, j, nullptr, 0, 0, st)) != GRASS_OK) return s;
-    }
-    if ((s = comm_end(c, st)) != GRASS_OK) return s;
-    if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
-  }
-  return mark_pending(c, st);
+grass_status grass_mgn_accumulate(grass_ctx* c, const int32_t* ids, int32_t n, const float* const* grads,
+                                  void* stream) {
+  return mgn_accumulate_impl(c, false, ids, n, reinterpret_cast<const void* const*>(grads), stream);
+}
+
+grass_status grass_mgn_accumulate_bf16(grass_ctx* c, const int32_t* ids, int32_t n,
+                                       const uint16_t* const* grads, void* stream) {
+  return mgn_accumulate_impl(c, true, ids, n, reinterpret_cast<const void* const*>(grads), stream);
 }
 
 grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, float* const* params,
                                const float* const* grads, float lr, void* stream) {
-  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
-  if (!params || !grads) return c->fail(GRASS_E_INVALID, "params/grads is NULL");
-  if (!(lr >= 0.0f) || !std::isfinite(lr)) return c->fail(GRASS_E_INVALID, "lr must be finite, >= 0");
-  std::vector<int> order;
-  grass_status s = check_call(c, ids, n, reinterpret_cast<const void* const*>(params),
-                              reinterpret_cast<const void* const*>(grads), &order);
-  if (s != GRASS_OK) return s;
-  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const bool sharded = c->dp;
-  const bool clip = c->cfg.max_grad_norm > 0.0;
-  const int32_t mode = clip ? kFinalizeNone : (sharded ? kFinalizeShard : kFinalizeMgn);
-  const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
-  struct CoefReset {  // the clip multiplier only applies inside this call
-    grass_ctx* c;
-    ~CoefReset() { c->cur_coef = nullptr; }
-  } coef_reset{c};
-  if (clip) {
-    // pass 1 (R17): raw norms of this call's (DP-averaged) gradients; they feed
-    // the MGN window (R9) and the global clip coefficient
-    if (!sharded) {
-      Batch b1 = make_batch(c, kFinalizeMgn);
-      for (int i : order) {
-        if (b1.nseg == kMaxSeg && (s = flush(c, &b1, false, st)) != GRASS_OK) return s;
-        push_seg(&b1, range_seg(c, ids[i], grads[i], 0, c->numel[ids[i]]));
-      }
-      if ((s = flush(c, &b1, false, st)) != GRASS_OK) return s;
-    } else {
-      for (int j = 0; j < (int)order.size(); ++j) {
-        const int i = order[j], l = ids[i];
-        float* gs = c->d_gscratch + (size_t)j * c->max_shard;
-        if (!c->comm.reduce_scatter_avg_f32(grads[i], gs, (size_t)c->shard_len[l], st, &c->err))
-          return GRASS_E_NCCL;
-        c->launches++;
-        Batch b1 = make_batch(c, kFinalizeShard);
-        Seg sg = range_seg(c, l, gs, 0, c->shard_len[l]);
-        sg.out_slot = j;
-        push_seg(&b1, sg);
-        if ((s = flush(c, &b1, false, st)) != GRASS_OK) return s;
-      }
-      if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
-    }
-    ClipArgs ca;
-    std::memset(&ca, 0, sizeof(ca));
-    ca.n = (int32_t)order.size();
-    ca.max_norm = c->cfg.max_grad_norm;
-    for (int j = 0; j < ca.n; ++j) ca.layer[j] = ids[order[j]];
-    CUDA_TRY(c, launch_clip_coef(ca, c->st, c->d_coef, st));
-    c->launches++;
-    c->cur_coef = c->d_coef;
-  }
-  std::vector<int> slot_of, victim_of;
-  if (period) {
-    cache_plan(c, ids, order, &slot_of, &victim_of);
-    c->call_seq++;
-    // write-backs read cache slots last written by earlier steps' updates
-    if (c->cfg.overlap && (s = wait_pending(c, c->d2h)) != GRASS_OK) return s;
-  }
-  Batch b = make_batch(c, mode);
-  const int nact = (int)order.size();
-  if (sharded) {
-    if ((s = comm_begin(c, st)) != GRASS_OK) return s;
-    if (!clip && (s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
-  }
-  for (int j = 0; j < nact; ++j) {
-    const int i = order[j], l = ids[i];
-    c->t[l] += 1;  // per-layer step count (R2); validated above, so this step happens
-    const int64_t off = c->shard_off[l], len = c->shard_len[l];
-    const float* g = grads[i];
-    if (sharded && clip) {
-      g = c->d_gscratch + (size_t)j * c->max_shard;  // averaged in pass 1
-    } else if (sharded) {
-      if (j + 1 < nact) {  // N1 of the next layer overlaps this layer's update
-        const int l1 = ids[order[j + 1]];
-        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
-      }
-      if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
-      g = rs_slot(c, j);  // shard-local gradient: index 0 = element `off`
-    }
-    float* theta = params[i] + off;
-    if (period) {
-      const int slot = slot_of[j];
-      Seg sg = range_seg(c, l, g, 0, len);
-      adam_scalars(c, l, lr, &sg);
-      sg.out_slot = j;
-      if (c->slot_layer[slot] == l) {  // hit: update in place in HBM, no link traffic
-        sg.theta = theta;
-        sg.m = cache_m(c, slot);
-        sg.v = cache_v(c, slot);
-        if (b.nseg == kMaxSeg && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
-        push_seg(&b, sg);
-        if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
-      } else if ((s = swap_in_layer(c, l, slot, victim_of[j], sg, theta, g, mode, st)) != GRASS_OK) {
-        return s;
-      }
-      c->slot_use[slot] = c->call_seq;
-      c->slot_dirty[slot] = 1;
-    } else if (c->cfg.offload) {
-      Seg base = range_seg(c, l, g, 0, len);
-      adam_scalars(c, l, lr, &base);
-      base.out_slot = j;
-      if ((s = offload_layer(c, l, base, theta, g, lr, mode, st)) != GRASS_OK) return s;
-    } else {
-      Seg sg = range_seg(c, l, g, 0, len);
-      sg.theta = theta;
-      sg.m = c->m[l];
-      sg.v = c->v[l];
-      sg.out_slot = j;
-      adam_scalars(c, l, lr, &sg);
-      if (b.nseg == kMaxSeg && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
-      push_seg(&b, sg);
-      // world > 1 launches per layer: the shard gradient scratch is reused
-      if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
-    }
-    if (sharded && (s = comm_after_update(c, j, params[i], off, len, st)) != GRASS_OK) return s;  // N2
-  }
-  if ((s = flush(c, &b, true, st)) != GRASS_OK) return s;
-  if (sharded && (s = comm_end(c, st)) != GRASS_OK) return s;
-  if (sharded && !clip && (s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
-  if (c->cfg.offload && c->cfg.overlap) {
-    // join: the caller stream reaches "done" only after every write-back
-    cudaEvent_t e = take_event(c);
-    if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
-    CUDA_TRY(c, cudaEventRecord(e, c->d2h));
-    CUDA_TRY(c, cudaStreamWaitEvent(st, e, 0));
-    c->ev_free_list.push_back(e);
-  }
-  return mark_pending(c, st);
+  return step_layers_impl(c, false, ids, n, reinterpret_cast<void* const*>(params),
+                          reinterpret_cast<const void* const*>(grads), lr, stream);
+}
+
+grass_status grass_step_layers_bf16(grass_ctx* c, const int32_t* ids, int32_t n, uint16_t* const* params,
+                                    const uint16_t* const* grads, float lr, void* stream) {
+  return step_layers_impl(c, true, ids, n, reinterpret_cast<void* const*>(params),
+                          reinterpret_cast<const void* const*>(grads), lr, stream);
 }
 
 grass_status grass_update_probs(grass_ctx* c, double* probs_out) {
@@ -1016,21 +1143,10 @@ grass_status grass_read_state(grass_ctx* c, int32_t layer, float* m_out, float* 
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (layer < 0 || layer >= c->nl) return c->fail(GRASS_E_INVALID, "layer id out of range");
   grass_status s = drain(c, false);
-  if (s != GRASS_OK) return s;
-  const size_t bytes = sizeof(float) * (size_t)c->shard_len[layer];
-  const int slot = c->cache_slots ? c->layer_slot[layer] : -1;
-  if (slot >= 0) {  // cached in HBM: the device copy is the current one
-    if (m_out) CUDA_TRY(c, cudaMemcpy(m_out, cache_m(c, slot), bytes, cudaMemcpyDeviceToHost));
-    if (v_out) CUDA_TRY(c, cudaMemcpy(v_out, cache_v(c, slot), bytes, cudaMemcpyDeviceToHost));
-  } else if (c->cfg.offload) {
-    if (m_out) std::memcpy(m_out, c->m[layer], bytes);
-    if (v_out) std::memcpy(v_out, c->v[layer], bytes);
-  } else {
-    if (m_out) CUDA_TRY(c, cudaMemcpy(m_out, c->m[layer], bytes, cudaMemcpyDeviceToHost));
-    if (v_out) CUDA_TRY(c, cudaMemcpy(v_out, c->v[layer], bytes, cudaMemcpyDeviceToHost));
-  }
-  if (t_out) *t_out = c->t[layer];
-  return GRASS_OK;
+  if (s == GRASS_OK && m_out) s = copy_state_out(c, 0, layer, m_out);
+  if (s == GRASS_OK && v_out) s = copy_state_out(c, 1, layer, v_out);
+  if (s == GRASS_OK && t_out) *t_out = c->t[layer];
+  return s;
 }
 
 grass_status grass_write_state(grass_ctx* c, int32_t layer, const float* m_in, const float* v_in, int64_t t_in) {
@@ -1038,22 +1154,29 @@ grass_status grass_write_state(grass_ctx* c, int32_t layer, const float* m_in, c
   if (layer < 0 || layer >= c->nl) return c->fail(GRASS_E_INVALID, "layer id out of range");
   if (t_in < 0) return c->fail(GRASS_E_INVALID, "step count must be >= 0");
   grass_status s = drain(c, false);
-  if (s != GRASS_OK) return s;
-  const size_t bytes = sizeof(float) * (size_t)c->shard_len[layer];
-  const int slot = c->cache_slots ? c->layer_slot[layer] : -1;
-  if (slot >= 0) {  // cached in HBM: the device copy stays authoritative (dirty)
-    if (m_in) CUDA_TRY(c, cudaMemcpy(cache_m(c, slot), m_in, bytes, cudaMemcpyHostToDevice));
-    if (v_in) CUDA_TRY(c, cudaMemcpy(cache_v(c, slot), v_in, bytes, cudaMemcpyHostToDevice));
-    c->slot_dirty[slot] = 1;
-  } else if (c->cfg.offload) {
-    if (m_in) std::memcpy(c->m[layer], m_in, bytes);
-    if (v_in) std::memcpy(c->v[layer], v_in, bytes);
-  } else {
-    if (m_in) CUDA_TRY(c, cudaMemcpy(c->m[layer], m_in, bytes, cudaMemcpyHostToDevice));
-    if (v_in) CUDA_TRY(c, cudaMemcpy(c->v[layer], v_in, bytes, cudaMemcpyHostToDevice));
-  }
-  c->t[layer] = t_in;
-  return GRASS_OK;
+  if (s == GRASS_OK && m_in) s = copy_state_in(c, 0, layer, m_in);
+  if (s == GRASS_OK && v_in) s = copy_state_in(c, 1, layer, v_in);
+  if (s == GRASS_OK) c->t[layer] = t_in;
+  return s;
+}
+
+grass_status grass_read_master(grass_ctx* c, int32_t layer, float* out) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (layer < 0 || layer >= c->nl || !out) return c->fail(GRASS_E_INVALID, "bad layer or NULL output");
+  if (!c->bf16) return c->fail(GRASS_E_STATE, "fp32 context: the parameters are the master");
+  if (!c->master_valid[layer]) return c->fail(GRASS_E_STATE, "master of this layer not initialised yet");
+  grass_status s = drain(c, false);
+  return s == GRASS_OK ? copy_state_out(c, 2, layer, out) : s;
+}
+
+grass_status grass_write_master(grass_ctx* c, int32_t layer, const float* in) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (layer < 0 || layer >= c->nl || !in) return c->fail(GRASS_E_INVALID, "bad layer or NULL input");
+  if (!c->bf16) return c->fail(GRASS_E_STATE, "fp32 context: the parameters are the master");
+  grass_status s = drain(c, false);
+  if (s == GRASS_OK) s = copy_state_in(c, 2, layer, in);
+  if (s == GRASS_OK) c->master_valid[layer] = 1;
+  return s;
 }
 
 grass_status grass_flush_states(grass_ctx* c) {
@@ -1063,8 +1186,8 @@ grass_status grass_flush_states(grass_ctx* c) {
   return flush_cache(c);
 }
 
-grass_status grass_get_mgn(grass_ctx* c, double* m_out, double* S_out, int64_t* c_out,
-                           double* ss_out, double* probs_out) {
+grass_status grass_get_mgn(grass_ctx* c, double* m_out, double* S_out, int64_t* c_out, double* ss_out,
+                           double* probs_out) {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
@@ -1076,62 +1199,6 @@ grass_status grass_get_mgn(grass_ctx* c, double* m_out, double* S_out, int64_t* 
   if (probs_out) std::memcpy(probs_out, c->probs.data(), sizeof(double) * c->nl);
   return GRASS_OK;
 }
-
-}  // extern "C"
-
-// ---------------------------------------------------------------- checkpoint
-static const char kCkMagic[8] = {'G', 'R', 'A', 'S', 'S', 'C', 'K', '1'};
-static const uint32_t kCkVersion = 1;
-
-static uint32_t crc_update(uint32_t crc, const void* p, size_t n) {
-  const Bytef* b = static_cast<const Bytef*>(p);
-  while (n > 0) {
-    const uInt k = (uInt)std::min<size_t>(n, 1u << 30);
-    crc = (uint32_t)crc32(crc, b, k);
-    b += k;
-    n -= k;
-  }
-  return crc;
-}
-
-template <class T>
-static void put(std::vector<char>* h, const T* p, size_t n) {
-  const char* b = reinterpret_cast<const char*>(p);
-  h->insert(h->end(), b, b + sizeof(T) * n);
-}
-
-static std::vector<char> ck_header(grass_ctx* c) {
-  std::vector<char> h;
-  const int32_t ints[4] = {c->nl, c->cfg.world, c->cfg.rank, c->committed ? 1 : 0};
-  put(&h, ints, 4);
-  put(&h, c->numel.data(), c->nl);
-  put(&h, c->shard_len.data(), c->nl);
-  put(&h, c->t.data(), c->nl);
-  put(&h, c->mgn.data(), c->nl);
-  put(&h, c->probs.data(), c->nl);
-  put(&h, h_S(c), c->nl);
-  put(&h, h_c(c), c->nl);
-  return h;
-}
-
-// Host view of layer l's m and v shards (staged through `tmp` when in HBM).
-static grass_status layer_state_host(grass_ctx* c, int l, std::vector<float>* tmp, const float** m,
-                                     const float** v) {
-  const size_t n = (size_t)c->shard_len[l];
-  if (c->cfg.offload) {  // period cache was flushed by the caller
-    *m = c->m[l];
-    *v = c->v[l];
-    return GRASS_OK;
-  }
-  tmp->resize(2 * n);
-  CUDA_TRY(c, cudaMemcpy(tmp->data(), c->m[l], 4 * n, cudaMemcpyDeviceToHost));
-  CUDA_TRY(c, cudaMemcpy(tmp->data() + n, c->v[l], 4 * n, cudaMemcpyDeviceToHost));
-  *m = tmp->data();
-  *v = tmp->data() + n;
-  return GRASS_OK;
-}
-
-extern "C" {
 
 grass_status grass_save_state(grass_ctx* c, const char* path) {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
@@ -1152,16 +1219,18 @@ grass_status grass_save_state(grass_ctx* c, const char* path) {
   ok = ok && std::fwrite(hdr.data(), 1, hdr.size(), f) == hdr.size();
   std::vector<float> tmp;
   for (int l = 0; ok && l < c->nl; ++l) {
-    const float *m, *v;
-    if ((s = layer_state_host(c, l, &tmp, &m, &v)) != GRASS_OK) {
+    // one blob per layer: m, v [, master] shards, fp32
+    const size_t n = (size_t)c->shard_len[l];
+    tmp.resize((size_t)c->ns * n);
+    for (int a = 0; a < c->ns && s == GRASS_OK; ++a) s = copy_state_out(c, a, l, tmp.data() + a * n);
+    if (s != GRASS_OK) {
       std::fclose(f);
       return s;
     }
-    const size_t n = (size_t)c->shard_len[l];
-    const uint64_t len = 8 * (uint64_t)n;
-    const uint32_t crc = crc_update(crc_update(0, m, 4 * n), v, 4 * n);
+    const uint64_t len = 4 * (uint64_t)tmp.size();
+    const uint32_t crc = crc_update(0, tmp.data(), len);
     ok = ok && std::fwrite(&len, 8, 1, f) == 1 && std::fwrite(&crc, 4, 1, f) == 1;
-    ok = ok && std::fwrite(m, 4, n, f) == n && std::fwrite(v, 4, n, f) == n;
+    ok = ok && std::fwrite(tmp.data(), 4, tmp.size(), f) == tmp.size();
   }
   ok = (std::fclose(f) == 0) && ok;
   if (!ok) return c->fail(GRASS_E_IO, std::string("short write to ") + path);
@@ -1185,21 +1254,20 @@ grass_status grass_load_state(grass_ctx* c, const char* path) {
   if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, kCkMagic, 8) != 0)
     return bad(GRASS_E_IO, "not a GRASS checkpoint (bad magic)");
   if (std::fread(&ver, 4, 1, f) != 1 || ver != kCkVersion) return bad(GRASS_E_IO, "unsupported version");
-  if (std::fread(&hlen, 8, 1, f) != 1 || std::fread(&hcrc, 4, 1, f) != 1)
-    return bad(GRASS_E_IO, "truncated header");
-  const size_t want = 16 + (size_t)c->nl * (3 * 8 + 4 * 8);
+  if (std::fread(&hlen, 8, 1, f) != 1 || std::fread(&hcrc, 4, 1, f) != 1) return bad(GRASS_E_IO, "truncated header");
+  const int nl = c->nl;
+  const size_t want = 4 * kCkInts + (size_t)nl * (3 * 8 + 4 * 8);
   if (hlen != want) return bad(GRASS_E_INVALID, "checkpoint was written for a different layer count");
   std::vector<char> hdr(hlen);
   if (std::fread(hdr.data(), 1, hlen, f) != hlen) return bad(GRASS_E_IO, "truncated header");
   if (crc_update(0, hdr.data(), hlen) != hcrc) return bad(GRASS_E_IO, "header CRC32 mismatch (integrity error)");
   const char* p = hdr.data();
-  auto take = [&](void* dst, size_t n) {
-    std::memcpy(dst, p, n);
-    p += n;
+  auto take = [&](void* dst, size_t k) {
+    std::memcpy(dst, p, k);
+    p += k;
   };
-  int32_t ints[4];
-  take(ints, 16);
-  const int nl = c->nl;
+  int32_t ints[kCkInts];
+  take(ints, sizeof(ints));
   std::vector<int64_t> numel(nl), slen(nl), t(nl);
   std::vector<double> mgn(nl), probs(nl), S(nl);
   std::vector<long long> cnt(nl);
@@ -1210,9 +1278,9 @@ grass_status grass_load_state(grass_ctx* c, const char* path) {
   take(probs.data(), 8 * nl);
   take(S.data(), 8 * nl);
   take(cnt.data(), 8 * nl);
-  if (ints[0] != nl || ints[1] != c->cfg.world || ints[2] != c->cfg.rank || numel != c->numel ||
-      slen != c->shard_len)
-    return bad(GRASS_E_INVALID, "checkpoint does not match this context (N_L, N_p, world or rank)");
+  if (ints[0] != nl || ints[1] != c->cfg.world || ints[2] != c->cfg.rank || ints[4] != c->cfg.param_dtype ||
+      numel != c->numel || slen != c->shard_len)
+    return bad(GRASS_E_INVALID, "checkpoint does not match this context (N_L, N_p, dtype, world or rank)");
   const long blobs = std::ftell(f);
   // pass 1: verify every blob's length and CRC32 before touching the context
   std::vector<char> buf(64u << 20);
@@ -1221,7 +1289,8 @@ grass_status grass_load_state(grass_ctx* c, const char* path) {
     uint32_t crc = 0;
     if (std::fread(&len, 8, 1, f) != 1 || std::fread(&crc, 4, 1, f) != 1)
       return bad(GRASS_E_IO, "truncated layer blob header");
-    if (len != 8 * (uint64_t)slen[l]) return bad(GRASS_E_IO, "corrupt layer blob length (integrity error)");
+    if (len != 4 * (uint64_t)c->ns * (uint64_t)slen[l])
+      return bad(GRASS_E_IO, "corrupt layer blob length (integrity error)");
     uint32_t got = 0;
     for (uint64_t done = 0; done < len;) {
       const size_t k = (size_t)std::min<uint64_t>(buf.size(), len - done);
@@ -1231,9 +1300,9 @@ grass_status grass_load_state(grass_ctx* c, const char* path) {
     }
     if (got != crc) return bad(GRASS_E_IO, "layer " + std::to_string(l) + " CRC32 mismatch (integrity error)");
   }
-  // pass 2: apply
+  // pass 2: apply (cached copies are superseded by the checkpoint)
   std::fseek(f, blobs, SEEK_SET);
-  if (c->cache_slots) {  // cached copies are superseded by the checkpoint
+  if (c->cache_slots) {
     for (int k = 0; k < c->cache_slots; ++k) {
       c->slot_layer[k] = -1;
       c->slot_dirty[k] = 0;
@@ -1244,15 +1313,15 @@ grass_status grass_load_state(grass_ctx* c, const char* path) {
   for (int l = 0; l < nl; ++l) {
     std::fseek(f, 12, SEEK_CUR);
     const size_t n = (size_t)slen[l];
-    if (c->cfg.offload) {
-      if (std::fread(c->m[l], 4, n, f) != n || std::fread(c->v[l], 4, n, f) != n)
-        return bad(GRASS_E_IO, "read failed");
-    } else {
-      tmp.resize(2 * n);
-      if (std::fread(tmp.data(), 4, 2 * n, f) != 2 * n) return bad(GRASS_E_IO, "read failed");
-      CUDA_TRY(c, cudaMemcpy(c->m[l], tmp.data(), 4 * n, cudaMemcpyHostToDevice));
-      CUDA_TRY(c, cudaMemcpy(c->v[l], tmp.data() + n, 4 * n, cudaMemcpyHostToDevice));
+    tmp.resize((size_t)c->ns * n);
+    if (std::fread(tmp.data(), 4, tmp.size(), f) != tmp.size()) return bad(GRASS_E_IO, "read failed");
+    for (int a = 0; a < c->ns; ++a) {
+      if ((s = copy_state_in(c, a, l, tmp.data() + a * n)) != GRASS_OK) {
+        std::fclose(f);
+        return s;
+      }
     }
+    if (c->bf16) c->master_valid[l] = t[l] > 0 ? 1 : 0;
   }
   std::fclose(f);
   c->t = t;
@@ -1284,8 +1353,8 @@ grass_status grass_softmax_probs(const double* m, int32_t n, double tau, int32_t
   return GRASS_OK;
 }
 
-grass_status grass_sample_from_probs(const double* p, int32_t n, int32_t gamma, uint64_t seed,
-                                     uint64_t period, int32_t* ids_out) {
+grass_status grass_sample_from_probs(const double* p, int32_t n, int32_t gamma, uint64_t seed, uint64_t period,
+                                     int32_t* ids_out) {
   if (!p || !ids_out || n < 1) return set_thread_err(GRASS_E_INVALID, "bad arguments");
   if (gamma < 1 || gamma > n) return set_thread_err(GRASS_E_INVALID, "gamma must lie in [1, N_L]");
   for (int i = 0; i < n; ++i)

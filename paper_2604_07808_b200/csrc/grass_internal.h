@@ -48,7 +48,11 @@ struct Seg {
   float decay;             // 1 - lr*wd           (fp64 on host, rounded once)
   float step_size;         // lr / (1 - b1^t)
   float inv_bc2_sqrt;      // 1 / sqrt(1 - b2^t)
-  float pad_;
+  int32_t init_master;     // bf16 mode: first update of the layer, master := bf16 param
+  // bf16 mode: `theta` is the fp32 master, these are the
+  // bf16 model copy (updated as RNE(master')) and the bf16 gradient
+  uint16_t* theta16;
+  const uint16_t* g16;
 };
 
 struct Batch {
@@ -58,6 +62,7 @@ struct Batch {
   int32_t mode;            // FinalizeMode
   float beta1, one_minus_beta1, beta2, one_minus_beta2, eps;
   const float* coef;       // device scalar multiplying g in the update (clipping), or NULL
+  int32_t bf16;            // 1: bf16 gradients / parameters with fp32 master (Seg::g16, theta16)
 };
 
 // Device-resident MGN / reduction state (all arrays indexed by layer id unless noted).

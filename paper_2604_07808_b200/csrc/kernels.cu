@@ -30,6 +30,7 @@
 // its value is (acc_0 + acc_1) + (acc_2 + acc_3); warps reduce with a fixed
 // shuffle tree and the 16 warp sums are added in ascending order.  Squares of
 // fp32 values are exact in fp64, so only the sums round.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -213,10 +214,6 @@ __device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, 
   consumer_sync();
 }
 
-// The branch-free full-unit path pays off for the norm-only stream (K1: +18%)
-// but not for K2, whose interleaved compute/store order measured ~0.5% faster
-// (profiles/r01_variants_*.json).
-constexpr bool kUpdFastPath = false;
 // K2 writes its results back into the stage and the producer bulk-stores them
 // (TMA, SASS UBLKCP.G.S): measured 2.4% faster than per-thread 128-bit stores.
 #ifdef GRASS_K2_STG_STORE
@@ -225,241 +222,11 @@ constexpr bool kTmaStore = false;
 constexpr bool kTmaStore = true;
 #endif
 
-template <bool UPDATE, int TPS, int STAGES>
-__global__ void __launch_bounds__(kStreamThreads, 1)
-grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
-  constexpr int NARR = UPDATE ? 4 : 1;
-  constexpr int kUnit = TPS * (int)kTile;  // elements per unit (one ring stage)
-  extern __shared__ __align__(1024) float sbuf[];  // [STAGES][NARR][kUnit]
-  __shared__ __align__(8) uint64_t full_bar[STAGES];
-  __shared__ __align__(8) uint64_t empty_bar[STAGES];
-  __shared__ int unit_prefix[kMaxSeg + 1];
-  __shared__ int seg_done[kMaxSeg];
-  __shared__ double red[2][TPS][kConsumerWarps];
-  __shared__ double fred[kConsumerWarps];
-  __shared__ int fin[kMaxSeg];
-  __shared__ int nfin;
+// The branch-free full-unit path (inside the kernel) is used for the
+// norm-only stream only: +18% for K1, while K2's interleaved compute/store
+// order measured ~0.5% faster without it (profiles/r01_variants_*.json).
+#include "stream_kernel.cuh"
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    unit_prefix[0] = 0;
-    for (int s = 0; s < b.nseg; ++s) {
-      unit_prefix[s + 1] = unit_prefix[s] + (b.seg[s].tiles + TPS - 1) / TPS;
-      seg_done[s] = 0;
-    }
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], kConsumerWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const int total = unit_prefix[b.nseg];
-
-  if (warp == kConsumerWarps) {
-    // ------------------------------ producer ------------------------------
-    if (lane == 0) {
-      const uint64_t pol = l2_load_policy<UPDATE>();
-      constexpr bool TS = UPDATE && kTmaStore;
-      // TMA-store mode: the unit each stage last held (its results go out first)
-      int pend_s[STAGES];
-      int64_t pend_e0[STAGES];
-      uint32_t pend_bytes[STAGES];
-      int s = 0, i = 0;
-      for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
-        const int stage = i % STAGES;
-        if (i >= STAGES) {
-          mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
-          if (TS) {
-            store_unit(b.seg[pend_s[stage]], pend_e0[stage], pend_bytes[stage],
-                       sbuf + (size_t)stage * NARR * kUnit, kUnit);
-            bulk_wait_read_all();  // stage readable again
-          }
-        }
-        while (u >= unit_prefix[s + 1]) ++s;
-        const Seg& sg = b.seg[s];
-        const int64_t e0 = (int64_t)(u - unit_prefix[s]) * kUnit;
-        const int64_t ne = min((int64_t)kUnit, sg.n - e0);
-        const uint32_t bytes = (uint32_t)(ne & ~(int64_t)3) * 4u;
-        if (TS) {
-          pend_s[stage] = s;
-          pend_e0[stage] = e0;
-          pend_bytes[stage] = bytes;
-        }
-        float* dst = sbuf + (size_t)stage * NARR * kUnit;
-        if (bytes) {
-          mbar_arrive_expect_tx(&full_bar[stage], NARR * bytes);
-          bulk_load(dst, sg.g + e0, bytes, &full_bar[stage], pol);
-          if (UPDATE) {
-            bulk_load(dst + kUnit, sg.theta + e0, bytes, &full_bar[stage], pol);
-            bulk_load(dst + 2 * kUnit, sg.m + e0, bytes, &full_bar[stage], pol);
-            bulk_load(dst + 3 * kUnit, sg.v + e0, bytes, &full_bar[stage], pol);
-          }
-        } else {
-          mbar_arrive(&full_bar[stage]);
-        }
-      }
-      if (TS) {  // drain: results of the last (up to STAGES) units
-        const int n_units = i;
-        for (int j = (n_units > STAGES ? n_units - STAGES : 0); j < n_units; ++j) {
-          const int stage = j % STAGES;
-          mbar_wait(&empty_bar[stage], (j / STAGES) & 1);
-          store_unit(b.seg[pend_s[stage]], pend_e0[stage], pend_bytes[stage],
-                     sbuf + (size_t)stage * NARR * kUnit, kUnit);
-        }
-        bulk_wait_all();
-      }
-    }
-    return;
-  }
-
-  // ------------------------------ consumers -------------------------------
-  const float cf = (UPDATE && b.coef) ? *b.coef : 1.0f;
-  int s = 0, i = 0;
-  for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
-    const int stage = i % STAGES;
-    while (u >= unit_prefix[s + 1]) ++s;
-    const Seg& sg = b.seg[s];
-    AdamScalars sc;
-    sc.b1 = b.beta1; sc.omb1 = b.one_minus_beta1; sc.b2 = b.beta2; sc.omb2 = b.one_minus_beta2;
-    sc.eps = b.eps; sc.decay = sg.decay; sc.step = sg.step_size; sc.inv_bc2s = sg.inv_bc2_sqrt;
-    sc.cf = cf;
-    const int ui = u - unit_prefix[s];
-    const int64_t e0 = (int64_t)ui * kUnit;
-    const int ne = (int)min((int64_t)kUnit, sg.n - e0);
-    const int nv = ne & ~3;  // bulk-copied prefix; the 0-3 element tail is read from HBM
-    const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
-    const float* sg_ = sbuf + (size_t)stage * NARR * kUnit;
-    mbar_wait(&full_bar[stage], (i / STAGES) & 1);
-    if (ne == kUnit && (!UPDATE || kUpdFastPath)) {
-      // Full unit (all but the last unit of a segment): branch-free, every
-      // shared-memory read issued before the math.  Same element map and
-      // accumulation order as the guarded path below.
-      float4 g4[TPS][kUnroll];
-#pragma unroll
-      for (int k = 0; k < TPS; ++k)
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q)
-          g4[k][q] = *reinterpret_cast<const float4*>(sg_ + k * (int)kTile + (q * kThreads + tid) * kVec);
-#pragma unroll
-      for (int k = 0; k < TPS; ++k) {
-        double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-          acc[0] = fma((double)g4[k][q].x, (double)g4[k][q].x, acc[0]);
-          acc[1] = fma((double)g4[k][q].y, (double)g4[k][q].y, acc[1]);
-          acc[2] = fma((double)g4[k][q].z, (double)g4[k][q].z, acc[2]);
-          acc[3] = fma((double)g4[k][q].w, (double)g4[k][q].w, acc[3]);
-        }
-        if (UPDATE) {
-          float4 t4[kUnroll], m4[kUnroll], v4[kUnroll];
-#pragma unroll
-          for (int q = 0; q < kUnroll; ++q) {
-            const int e = k * (int)kTile + (q * kThreads + tid) * kVec;
-            t4[q] = *reinterpret_cast<const float4*>(sg_ + kUnit + e);
-            m4[q] = *reinterpret_cast<const float4*>(sg_ + 2 * kUnit + e);
-            v4[q] = *reinterpret_cast<const float4*>(sg_ + 3 * kUnit + e);
-          }
-#pragma unroll
-          for (int q = 0; q < kUnroll; ++q) {
-            const int e = k * (int)kTile + (q * kThreads + tid) * kVec;
-            adamw1(g4[k][q].x, t4[q].x, m4[q].x, v4[q].x, sc);
-            adamw1(g4[k][q].y, t4[q].y, m4[q].y, v4[q].y, sc);
-            adamw1(g4[k][q].z, t4[q].z, m4[q].z, v4[q].z, sc);
-            adamw1(g4[k][q].w, t4[q].w, m4[q].w, v4[q].w, sc);
-            st_stream(sg.theta + e0 + e, t4[q]);
-            st_stream(sg.m + e0 + e, m4[q]);
-            st_stream(sg.v + e0 + e, v4[q]);
-          }
-        }
-        const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
-        if (lane == 0) red[i & 1][k][warp] = t;
-      }
-    } else {
-#pragma unroll
-    for (int k = 0; k < TPS; ++k) {
-      if (k < ntiles) {
-        double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-          const int e = k * (int)kTile + (q * kThreads + tid) * kVec;  // relative to e0
-          if (e < nv) {
-            const float4 g4 = *reinterpret_cast<const float4*>(sg_ + e);
-            acc[0] = fma((double)g4.x, (double)g4.x, acc[0]);
-            acc[1] = fma((double)g4.y, (double)g4.y, acc[1]);
-            acc[2] = fma((double)g4.z, (double)g4.z, acc[2]);
-            acc[3] = fma((double)g4.w, (double)g4.w, acc[3]);
-            if (UPDATE) {
-              float4 t4 = *reinterpret_cast<const float4*>(sg_ + kUnit + e);
-              float4 m4 = *reinterpret_cast<const float4*>(sg_ + 2 * kUnit + e);
-              float4 v4 = *reinterpret_cast<const float4*>(sg_ + 3 * kUnit + e);
-              adamw1(g4.x, t4.x, m4.x, v4.x, sc);
-              adamw1(g4.y, t4.y, m4.y, v4.y, sc);
-              adamw1(g4.z, t4.z, m4.z, v4.z, sc);
-              adamw1(g4.w, t4.w, m4.w, v4.w, sc);
-              if (kTmaStore) {  // results back into the stage; the producer bulk-stores them
-                float* w = const_cast<float*>(sg_);
-                *reinterpret_cast<float4*>(w + kUnit + e) = t4;
-                *reinterpret_cast<float4*>(w + 2 * kUnit + e) = m4;
-                *reinterpret_cast<float4*>(w + 3 * kUnit + e) = v4;
-              } else {
-                st_stream(sg.theta + e0 + e, t4);
-                st_stream(sg.m + e0 + e, m4);
-                st_stream(sg.v + e0 + e, v4);
-              }
-            }
-          } else if (e < ne) {
-#pragma unroll
-            for (int j = 0; j < kVec; ++j) {
-              if (e + j < ne) {
-                const int64_t idx = e0 + e + j;
-                const float g = sg.g[idx];
-                acc[j] = fma((double)g, (double)g, acc[j]);
-                if (UPDATE) {
-                  float th = sg.theta[idx], m = sg.m[idx], v = sg.v[idx];
-                  adamw1(g, th, m, v, sc);
-                  sg.theta[idx] = th;
-                  sg.m[idx] = m;
-                  sg.v[idx] = v;
-                }
-              }
-            }
-          }
-        }
-        const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
-        if (lane == 0) red[i & 1][k][warp] = t;
-      }
-    }
-    }
-    if (UPDATE && kTmaStore) fence_proxy_async_smem();  // results visible to the bulk store
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[stage]);  // this warp is done with the stage
-    consumer_sync();
-    if (tid < ntiles) {  // lane k of warp 0 finishes tile k (warp sums in ascending order)
-      double p = 0.0;
-#pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) p += red[i & 1][tid][w];
-      st.partials[sg.part_index + (int64_t)ui * TPS + tid] = p;
-    }
-    if (tid == 0) seg_done[s] += ntiles;
-  }
-  // Publish this CTA's partials (one fence, one atomic per segment) and
-  // detect the layers this CTA completed.
-  consumer_sync();
-  if (tid == 0) {
-    __threadfence();
-    int nf = 0;
-    for (int s2 = 0; s2 < b.nseg; ++s2) {
-      const int c = seg_done[s2];
-      if (c == 0) continue;
-      const unsigned prev = atomicAdd(st.counters + b.seg[s2].layer, (unsigned)c);
-      if (prev + (unsigned)c == (unsigned)b.seg[s2].layer_tiles) fin[nf++] = s2;
-    }
-    nfin = nf;
-  }
-  consumer_sync();
-  for (int f = 0; f < nfin; ++f) finalize_layer(b.seg[fin[f]], st, b.mode, fred);
-}
 
 __global__ void grass_rank_sum_kernel(const double* __restrict__ gathered,
                                       const __grid_constant__ RankSumArgs a, const DevState st) {
@@ -498,12 +265,13 @@ __global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const
 constexpr int kUpdTPS = 1, kUpdStages = GRASS_UPD_STAGES;  // 4 arrays x 16 KiB per stage -> 128 KiB ring
 constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 96 KiB x 2 -> 192 KiB
 
-template <bool U, int TPS, int ST>
+template <bool U, int TPS, int ST, bool BF16>
 cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStream_t s) {
-  constexpr size_t smem = (size_t)ST * (U ? 4 : 1) * TPS * (size_t)kTile * sizeof(float);
+  constexpr size_t smem = (size_t)ST * StageLayout<U, BF16, TPS>::bytes;
+  static_assert(smem <= 227 * 1024, "ring exceeds the 227 KiB shared-memory limit");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grass_stream_kernel<U, TPS, ST>,
+    cudaError_t e = cudaFuncSetAttribute(grass_stream_kernel<U, TPS, ST, BF16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -511,7 +279,7 @@ cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStre
   int units = 0;
   for (int i = 0; i < b.nseg; ++i) units += (b.seg[i].tiles + TPS - 1) / TPS;
   const int g = grid < units ? grid : units;
-  grass_stream_kernel<U, TPS, ST><<<g, kStreamThreads, smem, s>>>(b, st);
+  grass_stream_kernel<U, TPS, ST, BF16><<<g, kStreamThreads, smem, s>>>(b, st);
   return cudaGetLastError();
 }
 
@@ -520,8 +288,11 @@ cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStre
 cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int grid,
                          cudaStream_t s) {
   if (b.nseg <= 0 || b.tile_prefix[b.nseg] <= 0) return cudaSuccess;
-  return update ? launch_stream<true, kUpdTPS, kUpdStages>(b, st, grid, s)
-                : launch_stream<false, kNormTPS, kNormStages>(b, st, grid, s);
+  if (b.bf16)
+    return update ? launch_stream<true, kUpdTPS, kUpdStages, true>(b, st, grid, s)
+                  : launch_stream<false, kNormTPS, kNormStages, true>(b, st, grid, s);
+  return update ? launch_stream<true, kUpdTPS, kUpdStages, false>(b, st, grid, s)
+                : launch_stream<false, kNormTPS, kNormStages, false>(b, st, grid, s);
 }
 
 cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const DevState& st,

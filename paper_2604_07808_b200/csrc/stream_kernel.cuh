@@ -1,0 +1,303 @@
+// stream_kernel.cuh — K1 / K2: the persistent, warp-specialised streaming
+// kernel (included by kernels.cu inside its anonymous namespace; uses the
+// helpers defined there).
+//
+// Template parameters
+//   UPDATE  false: K1, Eq. 2 squared norm only (probing)
+//           true:  K2, fused Eq. 2 norm + AdamW (R1/R2)
+//   TPS     tiles per ring stage ("unit")
+//   STAGES  depth of the shared-memory ring
+//   BF16    false: fp32 theta and g (28 B/param for K2, 4 B/param for K1)
+//           true:  bf16 model parameters and gradients with an fp32 master
+//                  copy and fp32 moments: K2 reads g
+//                  (2 B), master (4 B; on a layer's first update the bf16
+//                  parameter, 2 B, instead), m, v (4 B each) and writes master,
+//                  m, v (4 B each) and the bf16 parameter RNE(master') (2 B):
+//                  28 B/param; K1 reads 2 B/param.
+//
+// Stage layout (bytes, every region 16-byte aligned):
+//   [g: kUnit*GB][theta/master: kUnit*4][m: kUnit*4][v: kUnit*4][bf16 theta: kUnit*2 (BF16)]
+// The bulk copies move the largest prefix of a unit whose narrowest array is a
+// multiple of 16 bytes (4 elements fp32, 8 elements bf16); the 0-7 element
+// tail of a segment is read and written directly in HBM by the consumers.
+
+template <bool UPDATE, bool BF16, int TPS>
+struct StageLayout {
+  static constexpr int kUnit = TPS * (int)kTile;
+  static constexpr int GB = BF16 ? 2 : 4;
+  static constexpr int off_g = 0;
+  static constexpr int off_t = kUnit * GB;
+  static constexpr int off_m = off_t + kUnit * 4;
+  static constexpr int off_v = off_m + kUnit * 4;
+  static constexpr int off_tb = off_v + kUnit * 4;
+  static constexpr int bytes = UPDATE ? off_tb + (BF16 ? kUnit * 2 : 0) : kUnit * GB;
+  static constexpr int vec = BF16 ? 8 : 4;
+};
+
+__device__ __forceinline__ float bf2f(uint32_t b) { return __uint_as_float(b << 16); }
+__device__ __forceinline__ uint32_t f2bf(float f) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+__device__ __forceinline__ float4 unpack_bf16x4(uint2 u) {
+  return make_float4(bf2f(u.x & 0xffffu), bf2f(u.x >> 16), bf2f(u.y & 0xffffu), bf2f(u.y >> 16));
+}
+__device__ __forceinline__ uint2 pack_bf16x4(float4 f) {
+  return make_uint2(f2bf(f.x) | (f2bf(f.y) << 16), f2bf(f.z) | (f2bf(f.w) << 16));
+}
+// 4 gradient values at (unit-relative) element e of a stage
+template <bool BF16>
+__device__ __forceinline__ float4 stage_g4(const char* stg, int e) {
+  if (BF16) return unpack_bf16x4(*reinterpret_cast<const uint2*>(stg + 2 * e));
+  return *reinterpret_cast<const float4*>(stg + 4 * e);
+}
+template <bool BF16>
+__device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
+  return BF16 ? bf2f(sg.g16[idx]) : sg.g[idx];
+}
+
+// Bulk-stores the results of one unit from its stage: master/theta, m, v
+// (and the bf16 parameter copy).
+template <bool BF16, class L>
+__device__ __forceinline__ void store_unit_t(const Seg& sg, int64_t e0, uint32_t nv, const char* stg) {
+  if (nv) {
+    bulk_store(sg.theta + e0, stg + L::off_t, nv * 4u);
+    bulk_store(sg.m + e0, stg + L::off_m, nv * 4u);
+    bulk_store(sg.v + e0, stg + L::off_v, nv * 4u);
+    if (BF16) bulk_store(sg.theta16 + e0, stg + L::off_tb, nv * 2u);
+    bulk_commit();
+  }
+}
+
+template <bool UPDATE, int TPS, int STAGES, bool BF16>
+__global__ void __launch_bounds__(kStreamThreads, 1)
+grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
+  using L = StageLayout<UPDATE, BF16, TPS>;
+  constexpr int kUnit = L::kUnit;
+  extern __shared__ __align__(1024) char sbuf[];  // [STAGES][L::bytes]
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ int unit_prefix[kMaxSeg + 1];
+  __shared__ int seg_done[kMaxSeg];
+  __shared__ double red[2][TPS][kConsumerWarps];
+  __shared__ double fred[kConsumerWarps];
+  __shared__ int fin[kMaxSeg];
+  __shared__ int nfin;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    unit_prefix[0] = 0;
+    for (int s = 0; s < b.nseg; ++s) {
+      unit_prefix[s + 1] = unit_prefix[s] + (b.seg[s].tiles + TPS - 1) / TPS;
+      seg_done[s] = 0;
+    }
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int total = unit_prefix[b.nseg];
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      const uint64_t pol = l2_load_policy<UPDATE>();
+      constexpr bool TS = UPDATE && kTmaStore;
+      // TMA-store mode: the unit each stage last held (its results go out first)
+      int pend_s[STAGES];
+      int64_t pend_e0[STAGES];
+      uint32_t pend_nv[STAGES];
+      int s = 0, i = 0;
+      for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
+        const int stage = i % STAGES;
+        char* stg = sbuf + (size_t)stage * L::bytes;
+        if (i >= STAGES) {
+          mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
+          if (TS) {
+            store_unit_t<BF16, L>(b.seg[pend_s[stage]], pend_e0[stage], pend_nv[stage], stg);
+            bulk_wait_read_all();  // stage readable again
+          }
+        }
+        while (u >= unit_prefix[s + 1]) ++s;
+        const Seg& sg = b.seg[s];
+        const int64_t e0 = (int64_t)(u - unit_prefix[s]) * kUnit;
+        const int64_t ne = min((int64_t)kUnit, sg.n - e0);
+        const uint32_t nv = (uint32_t)(ne & ~(int64_t)(L::vec - 1));
+        if (TS) {
+          pend_s[stage] = s;
+          pend_e0[stage] = e0;
+          pend_nv[stage] = nv;
+        }
+        if (nv) {
+          const bool init = BF16 && UPDATE && sg.init_master;
+          const uint32_t tx = nv * (uint32_t)L::GB + (UPDATE ? nv * (init ? 2u : 4u) + 8u * nv : 0u);
+          mbar_arrive_expect_tx(&full_bar[stage], tx);
+          bulk_load(stg + L::off_g, BF16 ? (const void*)(sg.g16 + e0) : (const void*)(sg.g + e0),
+                    nv * (uint32_t)L::GB, &full_bar[stage], pol);
+          if (UPDATE) {
+            if (init)
+              bulk_load(stg + L::off_tb, sg.theta16 + e0, nv * 2u, &full_bar[stage], pol);
+            else
+              bulk_load(stg + L::off_t, sg.theta + e0, nv * 4u, &full_bar[stage], pol);
+            bulk_load(stg + L::off_m, sg.m + e0, nv * 4u, &full_bar[stage], pol);
+            bulk_load(stg + L::off_v, sg.v + e0, nv * 4u, &full_bar[stage], pol);
+          }
+        } else {
+          mbar_arrive(&full_bar[stage]);
+        }
+      }
+      if (TS) {  // drain: results of the last (up to STAGES) units
+        const int n_units = i;
+        for (int j = (n_units > STAGES ? n_units - STAGES : 0); j < n_units; ++j) {
+          const int stage = j % STAGES;
+          mbar_wait(&empty_bar[stage], (j / STAGES) & 1);
+          store_unit_t<BF16, L>(b.seg[pend_s[stage]], pend_e0[stage], pend_nv[stage],
+                                sbuf + (size_t)stage * L::bytes);
+        }
+        bulk_wait_all();
+      }
+    }
+    return;
+  }
+
+  // ------------------------------ consumers -------------------------------
+  const float cf = (UPDATE && b.coef) ? *b.coef : 1.0f;
+  int s = 0, i = 0;
+  for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
+    const int stage = i % STAGES;
+    while (u >= unit_prefix[s + 1]) ++s;
+    const Seg& sg = b.seg[s];
+    AdamScalars sc;
+    sc.b1 = b.beta1; sc.omb1 = b.one_minus_beta1; sc.b2 = b.beta2; sc.omb2 = b.one_minus_beta2;
+    sc.eps = b.eps; sc.decay = sg.decay; sc.step = sg.step_size; sc.inv_bc2s = sg.inv_bc2_sqrt;
+    sc.cf = cf;
+    const bool init = BF16 && UPDATE && sg.init_master;
+    const int ui = u - unit_prefix[s];
+    const int64_t e0 = (int64_t)ui * kUnit;
+    const int ne = (int)min((int64_t)kUnit, sg.n - e0);
+    const int nv = ne & ~(L::vec - 1);  // bulk-copied prefix; the tail is read from HBM
+    const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
+    char* stg = sbuf + (size_t)stage * L::bytes;
+    mbar_wait(&full_bar[stage], (i / STAGES) & 1);
+    if (!UPDATE && ne == kUnit) {
+      // Full unit of the norm-only stream: branch-free, every shared-memory
+      // read issued before the math.  Same element map and accumulation order
+      // as the guarded path below.
+      constexpr int kPre = (TPS < 3 ? TPS : 3);  // tiles whose reads are issued ahead
+      float4 g4[kPre][kUnroll];
+#pragma unroll
+      for (int k = 0; k < kPre; ++k)
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q)
+          g4[k][q] = stage_g4<BF16>(stg + L::off_g, k * (int)kTile + (q * kThreads + tid) * kVec);
+#pragma unroll
+      for (int k = 0; k < TPS; ++k) {
+        double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
+        float4 cur[kUnroll];
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) cur[q] = g4[k % kPre][q];
+        if (k + kPre < TPS) {  // refill the slot just consumed
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q)
+            g4[k % kPre][q] = stage_g4<BF16>(stg + L::off_g, (k + kPre) * (int)kTile + (q * kThreads + tid) * kVec);
+        }
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+          acc[0] = fma((double)cur[q].x, (double)cur[q].x, acc[0]);
+          acc[1] = fma((double)cur[q].y, (double)cur[q].y, acc[1]);
+          acc[2] = fma((double)cur[q].z, (double)cur[q].z, acc[2]);
+          acc[3] = fma((double)cur[q].w, (double)cur[q].w, acc[3]);
+        }
+        const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+        if (lane == 0) red[i & 1][k][warp] = t;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < TPS; ++k) {
+        if (k < ntiles) {
+          double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const int e = k * (int)kTile + (q * kThreads + tid) * kVec;  // relative to e0
+            if (e < nv) {
+              const float4 g4 = stage_g4<BF16>(stg + L::off_g, e);
+              acc[0] = fma((double)g4.x, (double)g4.x, acc[0]);
+              acc[1] = fma((double)g4.y, (double)g4.y, acc[1]);
+              acc[2] = fma((double)g4.z, (double)g4.z, acc[2]);
+              acc[3] = fma((double)g4.w, (double)g4.w, acc[3]);
+              if (UPDATE) {
+                float4 t4 = init ? unpack_bf16x4(*reinterpret_cast<const uint2*>(stg + L::off_tb + 2 * e))
+                                 : *reinterpret_cast<const float4*>(stg + L::off_t + 4 * e);
+                float4 m4 = *reinterpret_cast<const float4*>(stg + L::off_m + 4 * e);
+                float4 v4 = *reinterpret_cast<const float4*>(stg + L::off_v + 4 * e);
+                adamw1(g4.x, t4.x, m4.x, v4.x, sc);
+                adamw1(g4.y, t4.y, m4.y, v4.y, sc);
+                adamw1(g4.z, t4.z, m4.z, v4.z, sc);
+                adamw1(g4.w, t4.w, m4.w, v4.w, sc);
+                if (kTmaStore) {  // results back into the stage; the producer bulk-stores them
+                  *reinterpret_cast<float4*>(stg + L::off_t + 4 * e) = t4;
+                  *reinterpret_cast<float4*>(stg + L::off_m + 4 * e) = m4;
+                  *reinterpret_cast<float4*>(stg + L::off_v + 4 * e) = v4;
+                  if (BF16) *reinterpret_cast<uint2*>(stg + L::off_tb + 2 * e) = pack_bf16x4(t4);
+                } else {
+                  st_stream(sg.theta + e0 + e, t4);
+                  st_stream(sg.m + e0 + e, m4);
+                  st_stream(sg.v + e0 + e, v4);
+                  if (BF16) *reinterpret_cast<uint2*>(sg.theta16 + e0 + e) = pack_bf16x4(t4);
+                }
+              }
+            } else if (e < ne) {
+#pragma unroll
+              for (int j = 0; j < kVec; ++j) {
+                if (e + j < ne) {
+                  const int64_t idx = e0 + e + j;
+                  const float g = seg_g<BF16>(sg, idx);
+                  acc[j] = fma((double)g, (double)g, acc[j]);
+                  if (UPDATE) {
+                    float th = init ? bf2f(sg.theta16[idx]) : sg.theta[idx];
+                    float m = sg.m[idx], v = sg.v[idx];
+                    adamw1(g, th, m, v, sc);
+                    sg.theta[idx] = th;
+                    sg.m[idx] = m;
+                    sg.v[idx] = v;
+                    if (BF16) sg.theta16[idx] = (uint16_t)f2bf(th);
+                  }
+                }
+              }
+            }
+          }
+          const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+          if (lane == 0) red[i & 1][k][warp] = t;
+        }
+      }
+    }
+    if (UPDATE && kTmaStore) fence_proxy_async_smem();  // results visible to the bulk store
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[stage]);  // this warp is done with the stage
+    consumer_sync();
+    if (tid < ntiles) {  // lane k of warp 0 finishes tile k (warp sums in ascending order)
+      double p = 0.0;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) p += red[i & 1][tid][w];
+      st.partials[sg.part_index + (int64_t)ui * TPS + tid] = p;
+    }
+    if (tid == 0) seg_done[s] += ntiles;
+  }
+  // Publish this CTA's partials (one fence, one atomic per segment) and
+  // detect the layers this CTA completed.
+  consumer_sync();
+  if (tid == 0) {
+    __threadfence();
+    int nf = 0;
+    for (int s2 = 0; s2 < b.nseg; ++s2) {
+      const int c = seg_done[s2];
+      if (c == 0) continue;
+      const unsigned prev = atomicAdd(st.counters + b.seg[s2].layer, (unsigned)c);
+      if (prev + (unsigned)c == (unsigned)b.seg[s2].layer_tiles) fin[nf++] = s2;
+    }
+    nfin = nf;
+  }
+  consumer_sync();
+  for (int f = 0; f < nfin; ++f) finalize_layer(b.seg[fin[f]], st, b.mode, fred);
+}

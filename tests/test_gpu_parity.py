@@ -609,3 +609,115 @@ def test_nccl_path_overlap_slot_reuse_gamma4():
         assert torch.equal(p_ref[l], p_dp[l]), l
     a, b = ref.get_mgn(), dp.get_mgn()
     assert a["S"] == b["S"] and a["last_ss"] == b["last_ss"] and a["c"] == b["c"]
+
+
+# ---------------------------- f3: bf16 params/grads, fp32 master + moments
+def _bits(t):
+    return t.detach().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("wd", [0.0, 0.01])
+def test_bf16_mixed_precision_vs_oracle(wd):
+    numel = [65_536, 4096 * 3 + 4, 13, 65_536 + 24]
+    lr = 1e-3
+    gr = G.Grass(numel, gamma=2, weight_decay=wd, param_dtype=G.DTYPE_BF16)
+    sig = grad_sigmas(4, 5)
+    params = [layer_params(n, l, device=DEV).to(torch.bfloat16) for l, n in enumerate(numel)]
+    p0_bits = [_bits(p).copy() for p in params]
+    master = [None] * 4
+    m_o = [np.zeros(n, np.float32) for n in numel]
+    v_o = [np.zeros(n, np.float32) for n in numel]
+    t_o = [0] * 4
+    for step, ids in enumerate([[0, 1], [3, 2], [1, 3], [0, 2], [2, 1]]):
+        grads = [layer_grad(numel[l], l, sig[l] * 10, step=step, device=DEV).to(torch.bfloat16) for l in ids]
+        gr.step_layers(ids, [params[l] for l in ids], grads, lr)
+        st = gr.get_mgn()
+        for k, l in enumerate(ids):
+            gb = _bits(grads[k])
+            assert_ss_close(st["last_ss"][l], O.sq_norm(O.bf16_to_f32(gb)))
+            t_o[l] += 1
+            first = master[l] is None
+            th_in = O.bf16_to_f32(p0_bits[l]) if first else master[l]
+            mw, m1, v1, tb = O.adamw_step_bf16(master[l], m_o[l], v_o[l], gb, t_o[l], float(np.float32(lr)),
+                                               weight_decay=wd, theta_bits=p0_bits[l] if first else None)
+            m_gpu, v_gpu, t = gr.read_state(l)
+            w_gpu = gr.read_master(l)
+            assert t == t_o[l]
+            assert_state_close(w_gpu, m_gpu, v_gpu, mw, m1, v1, th_in, m_o[l], O.bf16_to_f32(gb))
+            # the bf16 model copy is exactly RNE(master') of the GPU's own master
+            assert np.array_equal(_bits(params[l]), O.f32_to_bf16(w_gpu))
+            # re-seed the oracle from the GPU state
+            master[l], m_o[l], v_o[l] = w_gpu, m_gpu, v_gpu
+    with pytest.raises(G.GrassError):               # fp32 entry points are rejected on a bf16 context
+        G.binding.lib()
+        gr2 = G.Grass([4096], gamma=1, param_dtype=G.DTYPE_BF16)
+        gr2.bf16 = False
+        gr2.step_layers([0], [torch.zeros(4096, device=DEV)], [torch.zeros(4096, device=DEV)], 1e-3)
+
+
+def test_bf16_paths_bit_identical():
+    numel = [3 * 4096 + 8, 65_536, 4096 * 2]
+    kw = dict(gamma=2, weight_decay=0.01, param_dtype=G.DTYPE_BF16)
+    ctxs = [G.Grass(numel, **kw), G.Grass(numel, force_nccl=True, **kw),
+            G.Grass(numel, offload=True, chunk_elems=4096, **kw),
+            G.Grass(numel, offload=True, chunk_elems=4096, residency=G.RESIDENCY_PERIOD, **kw)]
+    base = [layer_params(n, l, device=DEV).to(torch.bfloat16) for l, n in enumerate(numel)]
+    ps = [[p.clone() for p in base] for _ in ctxs]
+    for step, ids in enumerate([[0, 1], [2, 1], [0, 2], [0, 2]]):
+        grads = [layer_grad(numel[l], l, 1e-2, step=step, device=DEV).to(torch.bfloat16) for l in ids]
+        for gr, p in zip(ctxs, ps):
+            gr.step_layers(ids, [p[l] for l in ids], grads, 1e-3)
+    probe = [layer_grad(n, l, 1e-2, step=9, device=DEV).to(torch.bfloat16) for l, n in enumerate(numel)]
+    for gr in ctxs:
+        gr.mgn_accumulate([0, 1, 2], probe)
+    torch.cuda.synchronize()
+    for l in range(3):
+        w0 = ctxs[0].read_master(l)
+        for k in range(1, len(ctxs)):
+            assert torch.equal(ps[0][l], ps[k][l]), (l, k)
+            assert np.array_equal(w0, ctxs[k].read_master(l)), (l, k)
+    S = [g.get_mgn()["S"] for g in ctxs]
+    assert all(x == S[0] for x in S)
+
+
+def test_bf16_checkpoint_roundtrip(tmp_path):
+    numel = [4096 + 8, 40]
+    a = G.Grass(numel, gamma=2, param_dtype=G.DTYPE_BF16, offload=True, chunk_elems=4096)
+    p = [layer_params(n, l, device=DEV).to(torch.bfloat16) for l, n in enumerate(numel)]
+    for step in range(2):
+        a.step_layers([0, 1], p, [layer_grad(n, l, 1e-2, step=step, device=DEV).to(torch.bfloat16)
+                                  for l, n in enumerate(numel)], 1e-3)
+    path = str(tmp_path / "bf16.ck")
+    a.save_state(path)
+    b = G.Grass(numel, gamma=2, param_dtype=G.DTYPE_BF16)        # resident: layout-independent
+    b.load_state(path)
+    for l in range(2):
+        assert np.array_equal(a.read_master(l), b.read_master(l))
+        x, y = a.read_state(l), b.read_state(l)
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]) and x[2] == y[2]
+    with pytest.raises(G.GrassError):
+        G.Grass(numel, gamma=2).load_state(path)                  # dtype mismatch
+
+
+def test_bf16_full_size_sampled_parity():
+    shape = MODELS["llama2-7b"]
+    n = shape.layer_numel
+    gr = G.Grass([n] * 2, gamma=2, param_dtype=G.DTYPE_BF16)
+    params = [layer_params(n, l, device=DEV, norm_numel=shape.norm_numel).to(torch.bfloat16) for l in range(2)]
+    grads = [layer_grad(n, l, 1e-4, device=DEV).to(torch.bfloat16) for l in range(2)]
+    rng = np.random.default_rng(1)
+    idx = np.unique(np.concatenate([np.arange(4096), n - 1 - np.arange(4096), rng.integers(0, n, 200_000)]))
+    ti = torch.from_numpy(idx).to(DEV)
+    p_bits = [_bits(p[ti]) for p in params]
+    g_bits = [_bits(g[ti]) for g in grads]
+    gr.step_layers([0, 1], params, grads, 3e-5)
+    st = gr.get_mgn()
+    for l in range(2):
+        assert_ss_close(st["last_ss"][l], O.sq_norm(O.bf16_to_f32(_bits(grads[l]))))
+        mw, m1, v1, tb = O.adamw_step_bf16(None, np.zeros(idx.size, np.float32), np.zeros(idx.size, np.float32),
+                                           g_bits[l], 1, float(np.float32(3e-5)), theta_bits=p_bits[l])
+        m_gpu, v_gpu, _ = gr.read_state(l)
+        w_gpu = gr.read_master(l)
+        assert_state_close(w_gpu[idx], m_gpu[idx], v_gpu[idx], mw, m1, v1, O.bf16_to_f32(p_bits[l]),
+                           np.zeros(idx.size), O.bf16_to_f32(g_bits[l]))
+        assert np.array_equal(_bits(params[l][ti]), O.f32_to_bf16(w_gpu[idx]))

@@ -356,3 +356,38 @@ def test_clip_coefficient_matches_torch_clip_grad_norm():
         for p, g in zip(ps, gs):
             np.testing.assert_allclose(p.grad.numpy(), g.astype(np.float64) * coef, rtol=1e-14)
         assert coef <= 1.0 and (coef == 1.0) == (max_norm >= float(total) + 1e-6)
+
+
+# ------------------------------------------------ R18: bf16 mixed precision
+def test_bf16_conversions_match_torch():
+    rng = np.random.default_rng(4)
+    x = np.concatenate([rng.standard_normal(100_000).astype(np.float32) * 10.0 ** rng.integers(-30, 30, 100_000),
+                        np.float32([0.0, -0.0, np.inf, -np.inf, 1.0, 1.00390625, 1.01171875, 3.4e38])])
+    x = x.astype(np.float32)
+    want = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(O.f32_to_bf16(x), want)               # round to nearest even
+    back = torch.from_numpy(want.view(np.int16)).view(torch.bfloat16).float().numpy()
+    assert np.array_equal(O.bf16_to_f32(want), back)            # exact widening
+    assert np.isnan(O.bf16_to_f32(O.f32_to_bf16(np.float32([np.nan])))).all()
+
+
+def test_adamw_bf16_matches_torch_adamw_on_fp32_master():
+    # mixed precision = torch AdamW on an fp32 master fed with the widened
+    # bf16 gradient, the bf16 model copy re-rounded from the master each step
+    rng = np.random.default_rng(6)
+    n, lr, wd = 4000, 1e-3, 0.01
+    p_bits = O.f32_to_bf16((rng.standard_normal(n) * 0.02).astype(np.float32))
+    master = torch.nn.Parameter(torch.from_numpy(O.bf16_to_f32(p_bits).astype(np.float64)))
+    opt = torch.optim.AdamW([master], lr=lr, weight_decay=wd, foreach=False)
+    m = v = np.zeros(n, np.float32)
+    mw = None
+    for t in range(1, 5):
+        g_bits = O.f32_to_bf16((rng.standard_normal(n) * 1e-3).astype(np.float32))
+        master.grad = torch.from_numpy(O.bf16_to_f32(g_bits).astype(np.float64))
+        opt.step()
+        mw, m, v, th_bits = O.adamw_step_bf16(mw, m, v, g_bits, t, lr, weight_decay=wd,
+                                              theta_bits=p_bits if t == 1 else None)
+        # torch keeps an fp64 master, the oracle rounds it to fp32 each step:
+        # differences stay at the fp32 ulp of theta (~2e-9)
+        np.testing.assert_allclose(mw, master.detach().numpy(), rtol=3e-7, atol=1e-9)
+        assert np.array_equal(th_bits, O.f32_to_bf16(mw))
