@@ -42,6 +42,7 @@ METRIC = "active-layer params updated/s and offloaded step ms; % of HBM / host-l
 UNIT = "params/s"
 BYTES_PER_PARAM_UPDATE = 28      # read g, theta, m, v + write theta, m, v (fp32)
 BYTES_PER_PARAM_PROBE = 4        # read g
+DEFAULT_LEGS = "main,probe,offload,period,bf16,e2e,cpu"
 FALLBACK_HBM_GBS = 6650.0        # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 
 
@@ -53,7 +54,7 @@ def parse():
     ap.add_argument("--impl", default="grass", choices=["grass", "reference"])
     ap.add_argument("--model", default="llama2-7b")
     ap.add_argument("--gamma", type=int, default=2)
-    ap.add_argument("--legs", default="main,probe,offload,period,bf16,e2e,cpu",
+    ap.add_argument("--legs", default=DEFAULT_LEGS,
                     help="comma list of legs to run (main is always run)")
     ap.add_argument("--offload-steps", type=int, default=10)
     ap.add_argument("--lr", type=float, default=3e-5)
@@ -216,6 +217,8 @@ def run_grass(args, rank, world, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     legs = set(args.legs.split(","))
+    if world > 1 and args.legs == DEFAULT_LEGS:
+        legs = {"main", "e2e"}
     shape = MODELS[args.model]
     NL, n_p, gamma = shape.n_layers, shape.layer_numel, args.gamma
     sig = grad_sigmas(NL, 0)
@@ -284,9 +287,28 @@ def run_grass(args, rank, world, local):
         with open(tp) as f:
             traffic = json.load(f).get(f"fused_update/{args.model}/g{gamma}/w{world}")
 
+    # Optional legs.  At world == 1 a failing optional leg is recorded under
+    # "leg_errors" instead of costing the main line; at world > 1 the default is
+    # main + e2e only (a rank-local failure inside a collective leg would hang).
+    leg_errors = {}
+
+    def guarded(name, fn):
+        if name not in legs:
+            return None
+        if world > 1:
+            return fn()
+        try:
+            return fn()
+        except Exception as ex:
+            leg_errors[name] = f"{type(ex).__name__}: {ex}"[:400]
+            try:
+                torch.cuda.synchronize()
+            except Exception:
+                pass
+            return None
+
     # ---- e2e: same step through the C ABI from pinned HOST gradients
-    e2e = None
-    if "e2e" in legs:
+    def leg_e2e():
         host_g = [grads[l].to("cpu").pin_memory() for l in range(gamma)]
         h2d = sum(h.numel() * 4 for h in host_g)
         d2h = NL * 16 + 4
@@ -305,15 +327,15 @@ def run_grass(args, rank, world, local):
         e1.record(s)
         torch.cuda.synchronize()
         et = max_over_ranks(e0.elapsed_time(e1) / 1e3, world, dev)
-        e2e = {"value": ksteps * active / et, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": et / ksteps * 1e3, "steps": ksteps}
-        del host_g
+        return {"value": ksteps * active / et, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": et / ksteps * 1e3, "steps": ksteps}
+
+    e2e = guarded("e2e", leg_e2e)
+    ctx.close()                                 # frees its 51.8 GB of HBM state
+    torch.cuda.empty_cache()
 
     # ---- offload leg: configs[2] (row a6)
-    offload = None
-    if "offload" in legs:
-        del ctx
-        torch.cuda.empty_cache()
+    def leg_offload():
         t_pin = time.perf_counter()
         octx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, device=local,
                        offload=True, rank=rank, world=world)
@@ -342,21 +364,23 @@ def run_grass(args, rank, world, local):
         ot = max_over_ranks(o0.elapsed_time(o1) / 1e3, world, dev) / ok
         link_bytes = 8 * active // world                       # per direction per rank
         floor = link_bytes / (duplex * 1e9)
-        offload = {"workload": f"{args.model}-stack gamma={gamma} offload (configs[2])",
-                   "step_ms": ot * 1e3, "params_per_s": active / ot,
-                   "h2d_bytes": link_bytes, "d2h_bytes": link_bytes,
-                   "link_GBps_per_dir": link_bytes / ot / 1e9,
-                   "duplex_GBps_per_dir_measured": duplex,
-                   "floor_ms": floor * 1e3, "frac_of_link_floor": floor / ot,
-                   "R1_within_10pct_of_link_floor": ot <= 1.10 * floor,
-                   "R2_offload_over_resident": ot / (elapsed / args.steps),
-                   "pinned_host_GB": octx.host_bytes / 1e9, "create_s": t_pin,
-                   "device_state_bytes": octx.device_bytes}
-        del octx
+        res = {"workload": f"{args.model}-stack gamma={gamma} offload (configs[2])",
+               "step_ms": ot * 1e3, "params_per_s": active / ot,
+               "h2d_bytes": link_bytes, "d2h_bytes": link_bytes,
+               "link_GBps_per_dir": link_bytes / ot / 1e9,
+               "duplex_GBps_per_dir_measured": duplex,
+               "floor_ms": floor * 1e3, "frac_of_link_floor": floor / ot,
+               "R1_within_10pct_of_link_floor": ot <= 1.10 * floor,
+               "R2_offload_over_resident": ot / (elapsed / args.steps),
+               "pinned_host_GB": octx.host_bytes / 1e9, "create_s": t_pin,
+               "device_state_bytes": octx.device_bytes}
+        octx.close()
+        return res
+
+    offload = guarded("offload", leg_offload)
 
     # ---- period residency: paper schedule T_s = T_u = 25
-    offload_period = None
-    if "period" in legs:
+    def leg_period():
         torch.cuda.empty_cache()
         T_s = 25
         pctx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=T_s, T_u=T_s, seed=1234, device=local,
@@ -388,22 +412,27 @@ def run_grass(args, rank, world, local):
         p1.record(s)
         torch.cuda.synchronize()
         pt = max_over_ranks(p0.elapsed_time(p1) / 1e3, world, dev) / nper
-        offload_period = {"workload": f"{args.model}-stack gamma={gamma} offload, period residency "
-                                      f"(SURVEY 8(f) f1), T_s=T_u={T_s}",
-                          "steps": nper, "layer_swaps": swaps, "step_ms_amortized": pt * 1e3,
-                          "params_per_s": active / pt,
-                          "link_bytes_per_dir": swaps * 8 * n_p // world,
-                          "over_resident": pt / (elapsed / args.steps),
-                          "device_cache_bytes": pctx.device_bytes}
-        del pctx
+        res = {"workload": f"{args.model}-stack gamma={gamma} offload, period residency "
+                           f"(SURVEY 8(f) f1), T_s=T_u={T_s}",
+               "steps": nper, "layer_swaps": swaps, "step_ms_amortized": pt * 1e3,
+               "params_per_s": active / pt,
+               "link_bytes_per_dir": swaps * 8 * n_p // world,
+               "over_resident": pt / (elapsed / args.steps),
+               "device_cache_bytes": pctx.device_bytes}
+        pctx.close()
+        return res
+
+    offload_period = guarded("period", leg_period)
 
     # ---- bf16 params/grads with fp32 master + moments
-    bf16 = None
-    if "bf16" in legs:
-        del params, grads
+    def leg_bf16():
+        params.clear()                            # the fp32 buffers are not needed any more
+        grads.clear()
         torch.cuda.empty_cache()
-        p16 = [layer_params(n_p, l, device=dev, norm_numel=shape.norm_numel).to(torch.bfloat16) for l in range(NL)]
-        g16 = [layer_grad(n_p, l, sig[l], step=0, device=dev, rank=rank).to(torch.bfloat16) for l in range(NL)]
+        p16 = [layer_params(n_p, l, device=dev, norm_numel=shape.norm_numel).to(torch.bfloat16)
+               for l in range(NL)]
+        g16 = [layer_grad(n_p, l, sig[l], step=0, device=dev, rank=rank).to(torch.bfloat16)
+               for l in range(NL)]
         bctx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, device=local,
                        rank=rank, world=world, param_dtype=G.DTYPE_BF16)
         bctx.mgn_accumulate(list(range(NL)), g16, stream=s)
@@ -435,21 +464,24 @@ def run_grass(args, rank, world, local):
         bt = max_over_ranks(b0.elapsed_time(b1) / 1e3, world, dev)
         bk = statistics.mean(a.elapsed_time(b) for a, b in bev)
         bgbs = BYTES_PER_PARAM_UPDATE * active / world / (bk / 1e3) / 1e9
-        bf16 = {"workload": f"{args.model}-stack gamma={gamma} bf16 params/grads, fp32 master+m+v, resident",
+        bctx.close()
+        return {"workload": f"{args.model}-stack gamma={gamma} bf16 params/grads, fp32 master+m+v, resident",
                 "params_per_s": args.steps * active / bt, "step_ms": bt / args.steps * 1e3,
                 "kernel_ms": bk, "GBps": bgbs, "frac_hbm": bgbs / hbm_peak,
                 "bytes_per_param": BYTES_PER_PARAM_UPDATE}
-        del bctx, p16, g16
 
-    # ---- CPU oracle baseline
-    cpu = None
-    if "cpu" in legs and rank == 0 and world == 1:
+    bf16 = guarded("bf16", leg_bf16)
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    def leg_cpu():
         sample = 1 << 23
         times = oracle_sample_time(n_p, gamma, sample, args.lr, reps=2)
         v = gamma * sample / min(times)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{gamma} x {sample} elements of one step (fp64 norm + AdamW) + commit/"
-                         f"softmax/sampling over {NL} layers, best of 2, single thread"}
+        return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"{gamma} x {sample} elements of one step (fp64 norm + AdamW) + commit/"
+                          f"softmax/sampling over {NL} layers, best of 2, single thread"}
+
+    cpu = guarded("cpu", leg_cpu) if (rank == 0 and world == 1) else None
 
     if rank == 0:
         line = {
@@ -471,6 +503,8 @@ def run_grass(args, rank, world, local):
             "clocks": clk.summary(), "probe": out.get("probe"), "offload": offload,
             "offload_period": offload_period, "bf16": bf16,
         }
+        if leg_errors:
+            line["leg_errors"] = leg_errors
         print(json.dumps(line), flush=True)
 
 
