@@ -252,6 +252,33 @@ grass_status grass_save_state(grass_ctx* ctx, const char* path);
  * and leaves the context unchanged. */
 grass_status grass_load_state(grass_ctx* ctx, const char* path);
 
+/* ----- tracing (the Fig. 4 timeline) ---------
+ * When enabled, every device operation the context issues is bracketed by
+ * timing events on the stream it runs on; grass_trace_read returns them as
+ * [start, end) in ms relative to the enable / previous read, in issue order,
+ * and clears the trace.  Tracing adds two event records per operation. */
+typedef enum {
+  GRASS_TRACE_H2D = 0,    /* optimizer states host -> device (offload fetch)   */
+  GRASS_TRACE_UPDATE = 1, /* fused norm + AdamW launch (K2)                     */
+  GRASS_TRACE_D2H = 2,    /* optimizer states device -> host (write-back/evict) */
+  GRASS_TRACE_NORM = 3,   /* norm-only launch (K1)                              */
+  GRASS_TRACE_RS = 4,     /* NCCL reduce-scatter of gradients                   */
+  GRASS_TRACE_AG = 5      /* NCCL all-gather of parameters                      */
+} grass_trace_kind;
+
+typedef struct grass_trace_event {
+  int32_t kind;     /* grass_trace_kind */
+  int32_t layer;    /* layer id (first layer of a multi-layer launch) */
+  int64_t offset;   /* first element of the range within the layer shard */
+  int64_t count;    /* elements */
+  float start_ms, end_ms;
+} grass_trace_event;
+
+grass_status grass_trace_enable(grass_ctx* ctx, int32_t on);
+/* Synchronises; copies up to `capacity` events into `out` (host), *count =
+ * events available (may exceed capacity; the rest are dropped). */
+grass_status grass_trace_read(grass_ctx* ctx, grass_trace_event* out, int32_t capacity, int32_t* count);
+
 /* Introspection of the MGN state (host arrays [N_L], any may be NULL):
  * committed m_l, window sum S_l, window count c_l, last fp64 squared norm of
  * layer l (DP-averaged gradient when world > 1), current probabilities.

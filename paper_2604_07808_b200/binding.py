@@ -33,6 +33,14 @@ class GrassError(RuntimeError):
         self.status = status
 
 
+class TraceEvent(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("layer", C.c_int32), ("offset", C.c_int64),
+                ("count", C.c_int64), ("start_ms", C.c_float), ("end_ms", C.c_float)]
+
+
+TRACE_KINDS = {0: "h2d", 1: "update", 2: "d2h", 3: "norm", 4: "rs", 5: "ag"}
+
+
 class GrassConfig(C.Structure):
     _fields_ = [
         ("n_layers", C.c_int32), ("layer_numel", C.POINTER(C.c_int64)), ("gamma", C.c_int32),
@@ -75,6 +83,9 @@ _SIGS = {
                                          C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_float,
                                          C.c_void_p]),
     "grass_read_master": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "grass_trace_enable": (C.c_int, [C.c_void_p, C.c_int32]),
+    "grass_trace_read": (C.c_int, [C.c_void_p, C.POINTER(TraceEvent), C.c_int32,
+                                   C.POINTER(C.c_int32)]),
     "grass_write_master": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "grass_save_state": (C.c_int, [C.c_void_p, C.c_char_p]),
     "grass_load_state": (C.c_int, [C.c_void_p, C.c_char_p]),
@@ -330,6 +341,18 @@ class Grass:
         if a.size != self.shard(layer)[1]:
             raise ValueError("master size must equal the shard length")
         _check(lib().grass_write_master(self._h, layer, a.ctypes.data), self._h)
+
+    def trace_enable(self, on: bool = True):
+        _check(lib().grass_trace_enable(self._h, int(on)), self._h)
+
+    def trace_read(self, capacity: int = 1 << 16):
+        """Trace events since the last enable/read: list of dicts (ms)."""
+        buf = (TraceEvent * capacity)()
+        n = C.c_int32()
+        _check(lib().grass_trace_read(self._h, buf, capacity, C.byref(n)), self._h)
+        return [{"kind": TRACE_KINDS[e.kind], "layer": e.layer, "offset": e.offset,
+                 "count": e.count, "start_ms": e.start_ms, "end_ms": e.end_ms}
+                for e in buf[:min(n.value, capacity)]]
 
     def flush_states(self):
         _check(lib().grass_flush_states(self._h), self._h)

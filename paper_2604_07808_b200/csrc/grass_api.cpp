@@ -99,6 +99,17 @@ struct grass_ctx {
   cudaEvent_t ev_cs_start = nullptr, ev_cs_end = nullptr, ev_rs[2] = {nullptr, nullptr},
               ev_k2[2] = {nullptr, nullptr};
 
+  // tracing (grass_trace_enable): timing events around every device operation
+  struct TraceRec {
+    int32_t kind, layer;
+    int64_t off, n;
+    cudaEvent_t e0, e1;
+  };
+  bool tracing = false;
+  cudaEvent_t trace_base = nullptr;
+  std::vector<TraceRec> trace;
+  std::vector<cudaEvent_t> trace_pool;
+
   Comm comm;
   bool has_comm = false;
   bool dp = false;  // data-parallel (NCCL) path: world > 1, or world = 1 with a unique id
@@ -162,6 +173,33 @@ grass_status wait_pending(grass_ctx* c, cudaStream_t s) {
   for (auto& pe : c->ev_pending) CUDA_TRY(c, cudaStreamWaitEvent(s, pe.second, 0));
   return GRASS_OK;
 }
+
+// ---- tracing ---------------------------------------------------------------
+// Brackets one device operation on stream `s`: `begin` before issuing it,
+// `end` after.  A no-op unless tracing is enabled.
+struct TraceScope {
+  grass_ctx* c;
+  cudaStream_t s;
+  int idx = -1;
+  TraceScope(grass_ctx* c_, cudaStream_t s_, int kind, int layer, int64_t off, int64_t n) : c(c_), s(s_) {
+    if (!c->tracing) return;
+    cudaEvent_t e[2];
+    for (auto& x : e) {
+      if (!c->trace_pool.empty()) {
+        x = c->trace_pool.back();
+        c->trace_pool.pop_back();
+      } else if (cudaEventCreate(&x) != cudaSuccess) {
+        return;
+      }
+    }
+    if (cudaEventRecord(e[0], s) != cudaSuccess) return;
+    c->trace.push_back({kind, layer, off, n, e[0], e[1]});
+    idx = (int)c->trace.size() - 1;
+  }
+  ~TraceScope() {
+    if (idx >= 0) cudaEventRecord(c->trace[idx].e1, s);
+  }
+};
 
 // Non-finite flag encoding: 0 = none, else INT_MAX - (smallest layer id)
 // (kernels use atomicMax, so a memset to 0 clears it).
@@ -311,7 +349,14 @@ void push_seg(Batch* b, const Seg& s) {
 
 grass_status flush(grass_ctx* c, Batch* b, bool update, cudaStream_t s) {
   if (b->nseg == 0) return GRASS_OK;
-  CUDA_TRY(c, launch_fused(update, *b, c->st, update ? c->grid_update : c->grid_norm, s));
+  {
+    int64_t n = 0;
+    for (int i = 0; i < b->nseg; ++i) n += b->seg[i].n;
+    const Seg& s0 = b->seg[0];
+    TraceScope ts(c, s, update ? GRASS_TRACE_UPDATE : GRASS_TRACE_NORM, s0.layer,
+                  (s0.part_index - s0.part_layer_base) * kTile, n);
+    CUDA_TRY(c, launch_fused(update, *b, c->st, update ? c->grid_update : c->grid_norm, s));
+  }
   c->launches++;
   const int32_t mode = b->mode;
   *b = make_batch(c, mode);
@@ -402,8 +447,11 @@ grass_status comm_begin(grass_ctx* c, cudaStream_t s) {
 grass_status comm_rs(grass_ctx* c, int j, const void* grad, int64_t len) {
   const int k = j & 1;
   if (j >= 2) CUDA_TRY(c, cudaStreamWaitEvent(c->comm_s, c->ev_k2[k], 0));
-  if (!c->comm.reduce_scatter_avg(grad, rs_slot(c, j), (size_t)len, c->bf16, c->comm_s, &c->err))
-    return GRASS_E_NCCL;
+  {
+    TraceScope ts(c, c->comm_s, GRASS_TRACE_RS, -1, 0, len);
+    if (!c->comm.reduce_scatter_avg(grad, rs_slot(c, j), (size_t)len, c->bf16, c->comm_s, &c->err))
+      return GRASS_E_NCCL;
+  }
   c->launches++;
   CUDA_TRY(c, cudaEventRecord(c->ev_rs[k], c->comm_s));
   return GRASS_OK;
@@ -423,6 +471,7 @@ grass_status comm_after_update(grass_ctx* c, int j, void* params, int64_t off, i
   CUDA_TRY(c, cudaEventRecord(c->ev_k2[k], s));
   if (params) {
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm_s, c->ev_k2[k], 0));
+    TraceScope ts(c, c->comm_s, GRASS_TRACE_AG, -1, off, len);
     if (!c->comm.all_gather(elem(params, off, c->esz), params, (size_t)len, c->bf16, c->comm_s, &c->err))
       return GRASS_E_NCCL;
     c->launches++;
@@ -456,6 +505,10 @@ grass_status update_range(grass_ctx* c, int l, const Seg& base, void* param, con
 // HtoD(states) on h2d -> fused update on the caller stream -> DtoH(states) on
 // d2h, chained by events through a ring of device slots.  overlap = 0 runs the
 // three stages serially on the caller stream (Fig. 4 "vanilla").
+// (Splitting the first/last chunk of a call into smaller pieces to shorten
+// pipeline fill/drain was measured and gave nothing: the fetch lane is already
+// ~96 % busy, the step is bound by the duplex link itself —
+// profiles/r01_offload_timeline.json.)
 grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, const void* g, bool init,
                            int32_t mode, cudaStream_t s) {
   const int64_t len = c->shard_len[l];
@@ -470,9 +523,12 @@ grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, co
     const size_t bytes = (size_t)n * sizeof(float);
     cudaStream_t sh = overlap ? c->h2d : s, sd = overlap ? c->d2h : s;
     if (overlap && c->slot_used[slot]) CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_free[slot], 0));
-    for (int a = 0; a < c->ns; ++a)
-      if (!(a == 2 && init))  // an uninitialised master is written, not read
-        CUDA_TRY(c, cudaMemcpyAsync(ring[a], c->arr[a][l] + off, bytes, cudaMemcpyHostToDevice, sh));
+    {
+      TraceScope ts(c, sh, GRASS_TRACE_H2D, l, off, n);
+      for (int a = 0; a < c->ns; ++a)
+        if (!(a == 2 && init))  // an uninitialised master is written, not read
+          CUDA_TRY(c, cudaMemcpyAsync(ring[a], c->arr[a][l] + off, bytes, cudaMemcpyHostToDevice, sh));
+    }
     if (overlap) {
       CUDA_TRY(c, cudaEventRecord(c->ev_h2d[slot], sh));
       CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_h2d[slot], 0));
@@ -483,8 +539,11 @@ grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, co
       CUDA_TRY(c, cudaEventRecord(c->ev_comp[slot], s));
       CUDA_TRY(c, cudaStreamWaitEvent(sd, c->ev_comp[slot], 0));
     }
-    for (int a = 0; a < c->ns; ++a)
-      CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][l] + off, ring[a], bytes, cudaMemcpyDeviceToHost, sd));
+    {
+      TraceScope ts(c, sd, GRASS_TRACE_D2H, l, off, n);
+      for (int a = 0; a < c->ns; ++a)
+        CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][l] + off, ring[a], bytes, cudaMemcpyDeviceToHost, sd));
+    }
     if (overlap) {
       CUDA_TRY(c, cudaEventRecord(c->ev_free[slot], sd));
       c->slot_used[slot] = 1;
@@ -549,6 +608,7 @@ grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, const Seg&
   for (int64_t off = 0; off < std::max(ll, lv); off += c->chunk) {
     if (off < lv) {
       const size_t vb = sizeof(float) * (size_t)std::min(c->chunk, lv - off);
+      TraceScope ts(c, sd, GRASS_TRACE_D2H, victim, off, (int64_t)(vb / sizeof(float)));
       for (int a = 0; a < c->ns; ++a)
         CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][victim] + off, cache_arr(c, slot, a) + off, vb,
                                     cudaMemcpyDeviceToHost, sd));
@@ -560,10 +620,13 @@ grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, const Seg&
     if (off < ll) {
       const int64_t n = std::min(c->chunk, ll - off);
       const size_t bytes = sizeof(float) * (size_t)n;
-      for (int a = 0; a < c->ns; ++a)
-        if (!(a == 2 && init))
-          CUDA_TRY(c, cudaMemcpyAsync(cache_arr(c, slot, a) + off, c->arr[a][l] + off, bytes,
-                                      cudaMemcpyHostToDevice, sh));
+      {
+        TraceScope ts(c, sh, GRASS_TRACE_H2D, l, off, n);
+        for (int a = 0; a < c->ns; ++a)
+          if (!(a == 2 && init))
+            CUDA_TRY(c, cudaMemcpyAsync(cache_arr(c, slot, a) + off, c->arr[a][l] + off, bytes,
+                                        cudaMemcpyHostToDevice, sh));
+      }
       if (overlap) {
         CUDA_TRY(c, cudaEventRecord(c->ev_fill, sh));
         CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_fill, 0));
@@ -668,6 +731,12 @@ void free_ctx(grass_ctx* c) {
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
   for (auto& pe : c->ev_pending) cudaEventDestroy(pe.second);
+  for (auto& r : c->trace) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  for (cudaEvent_t e : c->trace_pool) cudaEventDestroy(e);
+  if (c->trace_base) cudaEventDestroy(c->trace_base);
   for (cudaEvent_t e : {c->ev_evict, c->ev_fill, c->ev_cs_start, c->ev_cs_end, c->ev_rs[0], c->ev_rs[1],
                         c->ev_k2[0], c->ev_k2[1]})
     if (e) cudaEventDestroy(e);
@@ -1197,6 +1266,48 @@ grass_status grass_get_mgn(grass_ctx* c, double* m_out, double* S_out, int64_t* 
   if (ss_out) CUDA_TRY(c, cudaMemcpy(ss_out, c->st.last_ss, sizeof(double) * c->nl, cudaMemcpyDeviceToHost));
   if (m_out) std::memcpy(m_out, c->mgn.data(), sizeof(double) * c->nl);
   if (probs_out) std::memcpy(probs_out, c->probs.data(), sizeof(double) * c->nl);
+  return GRASS_OK;
+}
+
+grass_status grass_trace_enable(grass_ctx* c, int32_t on) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  grass_status s = drain(c, false);
+  if (s != GRASS_OK) return s;
+  for (auto& r : c->trace) {
+    c->trace_pool.push_back(r.e0);
+    c->trace_pool.push_back(r.e1);
+  }
+  c->trace.clear();
+  if (on && !c->trace_base) CUDA_TRY(c, cudaEventCreate(&c->trace_base));
+  if (on) CUDA_TRY(c, cudaEventRecord(c->trace_base, c->aux));
+  c->tracing = on != 0;
+  return GRASS_OK;
+}
+
+grass_status grass_trace_read(grass_ctx* c, grass_trace_event* out, int32_t capacity, int32_t* count) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!count || (capacity > 0 && !out)) return c->fail(GRASS_E_INVALID, "bad output arguments");
+  if (!c->tracing) return c->fail(GRASS_E_STATE, "tracing is not enabled");
+  grass_status s = drain(c, false);
+  if (s != GRASS_OK) return s;
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  *count = (int32_t)c->trace.size();
+  for (int i = 0; i < (int)c->trace.size(); ++i) {
+    const auto& r = c->trace[i];
+    if (i < capacity) {
+      grass_trace_event& e = out[i];
+      e.kind = r.kind;
+      e.layer = r.layer;
+      e.offset = r.off;
+      e.count = r.n;
+      CUDA_TRY(c, cudaEventElapsedTime(&e.start_ms, c->trace_base, r.e0));
+      CUDA_TRY(c, cudaEventElapsedTime(&e.end_ms, c->trace_base, r.e1));
+    }
+    c->trace_pool.push_back(r.e0);
+    c->trace_pool.push_back(r.e1);
+  }
+  c->trace.clear();
+  CUDA_TRY(c, cudaEventRecord(c->trace_base, c->aux));
   return GRASS_OK;
 }
 

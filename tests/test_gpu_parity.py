@@ -721,3 +721,62 @@ def test_bf16_full_size_sampled_parity():
         assert_state_close(w_gpu[idx], m_gpu[idx], v_gpu[idx], mw, m1, v1, O.bf16_to_f32(p_bits[l]),
                            np.zeros(idx.size), O.bf16_to_f32(g_bits[l]))
         assert np.array_equal(_bits(params[l][ti]), O.f32_to_bf16(w_gpu[idx]))
+
+
+# ------------------------------------- tracing: the Fig. 4 pipeline on hardware
+def _check_chain(tr):
+    """Per (layer, chunk): fetch ends before its update starts, and the update
+    ends before its write-back starts (no update before arrival)."""
+    ev = {}
+    for e in tr:
+        ev.setdefault((e["layer"], e["offset"]), {}).setdefault(e["kind"], []).append(e)
+    for key, k in ev.items():
+        if "h2d" in k and "update" in k:
+            assert k["h2d"][0]["end_ms"] <= k["update"][0]["start_ms"] + 1e-3, key
+        if "update" in k and "d2h" in k:
+            assert k["update"][0]["end_ms"] <= k["d2h"][-1]["start_ms"] + 1e-3, key
+    return ev
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_trace_offload_pipeline(overlap):
+    n = 4096 * 64
+    gr = G.Grass([n] * 3, gamma=2, offload=True, overlap=overlap, chunk_elems=4096 * 8, ring_slots=3)
+    p = [layer_params(n, l, device=DEV) for l in range(3)]
+    g = [layer_grad(n, l, 1e-3, device=DEV) for l in range(3)]
+    gr.step_layers([0, 1], p[:2], g[:2], 1e-3)        # warm
+    gr.trace_enable(True)
+    gr.step_layers([1, 2], p[1:], g[1:], 1e-3)
+    tr = gr.trace_read()
+    kinds = [e["kind"] for e in tr]
+    assert kinds.count("h2d") == kinds.count("update") == kinds.count("d2h") == 16
+    _check_chain(tr)
+    h2d = [(e["start_ms"], e["end_ms"]) for e in tr if e["kind"] == "h2d"]
+    d2h = [(e["start_ms"], e["end_ms"]) for e in tr if e["kind"] == "d2h"]
+    overlapped = any(a0 < b1 and b0 < a1 for a0, a1 in h2d for b0, b1 in d2h)
+    if overlap:
+        assert overlapped                               # duplex: fetch || write-back
+    else:                                               # Fig. 4 "vanilla": strictly serial
+        assert not overlapped
+        iv = sorted((e["start_ms"], e["end_ms"]) for e in tr)
+        assert all(b[0] >= a[1] - 1e-3 for a, b in zip(iv, iv[1:]))
+    gr.trace_enable(False)
+
+
+def test_trace_period_residency_and_dp():
+    n = 4096 * 16
+    gr = G.Grass([n] * 3, gamma=2, offload=True, chunk_elems=4096 * 4, residency=G.RESIDENCY_PERIOD,
+                 force_nccl=True)
+    p = [layer_params(n, l, device=DEV) for l in range(3)]
+    g = [layer_grad(n, l, 1e-3, device=DEV) for l in range(3)]
+    gr.step_layers([0, 1], p[:2], g[:2], 1e-3)
+    gr.trace_enable(True)
+    gr.step_layers([0, 1], p[:2], g[:2], 1e-3)         # hits: no link traffic
+    tr = gr.trace_read()
+    assert not [e for e in tr if e["kind"] in ("h2d", "d2h")]
+    assert [e["kind"] for e in tr].count("rs") == 2 and [e["kind"] for e in tr].count("ag") == 2
+    gr.step_layers([2, 1], [p[2], p[1]], [g[2], g[1]], 1e-3)   # one swap: evict 0, fetch 2
+    tr = gr.trace_read()
+    assert {e["layer"] for e in tr if e["kind"] == "d2h"} == {0}
+    assert {e["layer"] for e in tr if e["kind"] == "h2d"} == {2}
+    _check_chain(tr)
