@@ -364,7 +364,7 @@ def run_grass(args, rank, world, local):
         ot = max_over_ranks(o0.elapsed_time(o1) / 1e3, world, dev) / ok
         link_bytes = 8 * active // world                       # per direction per rank
         floor = link_bytes / (duplex * 1e9)
-        res = {"workload": f"{args.model}-stack gamma={gamma} offload (configs[2])",
+        res = {"workload": f"{args.model}-stack gamma={gamma} offload, per-step round trip (row a6)",
                "step_ms": ot * 1e3, "params_per_s": active / ot,
                "h2d_bytes": link_bytes, "d2h_bytes": link_bytes,
                "link_GBps_per_dir": link_bytes / ot / 1e9,
