@@ -35,6 +35,9 @@ fixtures in ``tests/golden/``.  Parity status per function:
   sample_layers ................. pinned (exact law enumeration, torch.multinomial)
   adamw_step .................... pinned (closed forms, torch.optim.AdamW fp64)
   schedule_decision ............. pinned (paper values T_p=150, T_s=25)
+  clip_coefficient (R17) ........ pinned (torch.nn.utils.clip_grad_norm_)
+  bf16_to_f32 / f32_to_bf16 ..... pinned (torch bfloat16 conversions, RNE)
+  adamw_step_bf16 (R18) ......... pinned (torch.optim.AdamW on an fp32 master)
   Paper-level choices of tau, alpha, the RNG and the draw scheme: **parity
   unpinned** against the paper itself (the paper gives no values); they are
   pinned only against our stated readings (R3, R5, R6, R7).
