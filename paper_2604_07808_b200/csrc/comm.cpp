@@ -102,9 +102,9 @@ void Comm::destroy() {
   comm = nullptr;
 }
 
-bool Comm::reduce_scatter_avg(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
+bool Comm::reduce_scatter_sum(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
                               std::string* err) {
-  ncclResult_t r = api().ReduceScatter(send, recv, count, bf16 ? ncclBfloat16 : ncclFloat32, ncclAvg,
+  ncclResult_t r = api().ReduceScatter(send, recv, count, bf16 ? ncclBfloat16 : ncclFloat32, ncclSum,
                                        comm, s);
   if (r != ncclSuccess) {
     *err = nccl_msg("ncclReduceScatter", r);

@@ -18,8 +18,11 @@ struct Comm {
   int rank = 0, world = 1;
   bool init(const void* unique_id, int rank, int world, std::string* err);
   void destroy();
-  // N1: gradient average, element-sharded (recv = this rank's shard); fp32 or bf16.
-  bool reduce_scatter_avg(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
+  // N1: gradient sum, element-sharded (recv = this rank's shard); fp32 or bf16.
+  // The 1/world of the average is applied by the kernels (Batch::gscale): NCCL
+  // 2.28.9's ncclAvg reduce-scatter drops the last 16 elements for counts
+  // = 16 (mod 64) on a 1-rank communicator (tools/dbg_nccl.py).
+  bool reduce_scatter_sum(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
                           std::string* err);
   // N2: parameter shards back to every rank (in place when send = recv + rank*count).
   bool all_gather(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,

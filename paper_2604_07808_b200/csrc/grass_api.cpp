@@ -39,6 +39,7 @@ struct grass_ctx {
   int nl = 0;
   std::vector<int64_t> numel, shard_off, shard_len, tiles, part_base;
   int64_t max_shard = 0;
+  int64_t slot_stride = 0;  // max_shard rounded up to 64 elements: every slot array 256-B aligned
   bool bf16 = false;  // GRASS_DTYPE_BF16: bf16 params/grads, fp32 master copy (R18)
   int ns = 2;         // optimizer state arrays per layer: m, v [, master]
   size_t esz = 4;     // bytes per parameter / gradient element
@@ -71,7 +72,7 @@ struct grass_ctx {
   std::vector<char> layer_done_valid;
 
   // period residency: HBM cache of whole-layer state slots
-  float* d_cache = nullptr;  // cache_slots x ns x max_shard floats
+  float* d_cache = nullptr;  // cache_slots x ns x slot_stride floats
   int cache_slots = 0;
   std::vector<int> slot_layer, layer_slot;
   std::vector<int64_t> slot_use;
@@ -338,6 +339,9 @@ Batch make_batch(const grass_ctx* c, int32_t mode) {
   b.eps = (float)c->cfg.eps;
   b.coef = c->cur_coef;
   b.bf16 = c->bf16 ? 1 : 0;
+  // DP: the kernels read reduce-scattered SUMS; x 1/W makes them the average
+  // (exact for power-of-two W)
+  b.gscale = c->dp ? (float)(1.0 / (double)c->cfg.world) : 1.0f;
   return b;
 }
 
@@ -431,7 +435,7 @@ grass_status cross_rank_finish(grass_ctx* c, const int32_t* ids, const std::vect
 
 // ---- data-parallel schedule on the comm stream --------------
 // Shard buffer of slot k (2 double-buffered slots; gamma slots when clipping).
-void* gs_slot(grass_ctx* c, int k) { return c->d_gscratch + (size_t)k * c->max_shard * c->esz; }
+void* gs_slot(grass_ctx* c, int k) { return c->d_gscratch + (size_t)k * c->slot_stride * c->esz; }
 void* rs_slot(grass_ctx* c, int j) { return gs_slot(c, j & 1); }
 
 // Comm stream starts after everything already enqueued on the caller stream
@@ -449,7 +453,7 @@ grass_status comm_rs(grass_ctx* c, int j, const void* grad, int64_t len) {
   if (j >= 2) CUDA_TRY(c, cudaStreamWaitEvent(c->comm_s, c->ev_k2[k], 0));
   {
     TraceScope ts(c, c->comm_s, GRASS_TRACE_RS, -1, 0, len);
-    if (!c->comm.reduce_scatter_avg(grad, rs_slot(c, j), (size_t)len, c->bf16, c->comm_s, &c->err))
+    if (!c->comm.reduce_scatter_sum(grad, rs_slot(c, j), (size_t)len, c->bf16, c->comm_s, &c->err))
       return GRASS_E_NCCL;
   }
   c->launches++;
@@ -558,7 +562,7 @@ grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, co
 
 // ---- period residency -----------------------------------
 float* cache_arr(grass_ctx* c, int slot, int a) {
-  return c->d_cache + ((size_t)slot * c->ns + a) * c->max_shard;
+  return c->d_cache + ((size_t)slot * c->ns + a) * c->slot_stride;
 }
 
 // Slot for every listed layer: hits keep their slot; misses take an empty slot
@@ -769,6 +773,8 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     state_elems += round_up(c->shard_len[l], kAlignElems);
     c->max_shard = std::max(c->max_shard, c->shard_len[l]);
   }
+  // TMA bulk copies need 16-byte aligned slot arrays whatever the layer sizes
+  c->slot_stride = round_up(c->max_shard, kAlignElems);
   c->t.assign(c->nl, 0);
   c->master_valid.assign(c->nl, 0);
   c->mgn.assign(c->nl, 0.0);
@@ -829,7 +835,7 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     if (cfg->residency == GRASS_RESIDENCY_PERIOD) {
       c->cache_slots = std::max(cfg->gamma, cfg->cache_layers);
       CUDA_TRY(c, dalloc((void**)&c->d_cache,
-                         sizeof(float) * (size_t)c->ns * (size_t)c->max_shard * c->cache_slots));
+                         sizeof(float) * (size_t)c->ns * (size_t)c->slot_stride * c->cache_slots));
       c->slot_layer.assign(c->cache_slots, -1);
       c->layer_slot.assign(c->nl, -1);
       c->slot_use.assign(c->cache_slots, 0);
@@ -861,7 +867,7 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_s, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&c->ev_cs_start, &c->ev_cs_end, &c->ev_rs[0], &c->ev_rs[1], &c->ev_k2[0], &c->ev_k2[1]})
       CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    CUDA_TRY(c, dalloc((void**)&c->d_gscratch, c->esz * (size_t)c->max_shard * nslots));
+    CUDA_TRY(c, dalloc((void**)&c->d_gscratch, c->esz * (size_t)c->slot_stride * nslots));
     if (!c->comm.init(cfg->nccl_unique_id, cfg->rank, W, &c->err)) return GRASS_E_NCCL;
     c->has_comm = true;
   }
@@ -950,7 +956,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     } else {
       for (int j = 0; j < nact; ++j) {
         const int i = order[j], l = ids[i];
-        if (!c->comm.reduce_scatter_avg(grads[i], gs_slot(c, j), (size_t)c->shard_len[l], c->bf16, st, &c->err))
+        if (!c->comm.reduce_scatter_sum(grads[i], gs_slot(c, j), (size_t)c->shard_len[l], c->bf16, st, &c->err))
           return GRASS_E_NCCL;
         c->launches++;
         Batch b1 = make_batch(c, kFinalizeShard);

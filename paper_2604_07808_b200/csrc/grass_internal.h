@@ -63,6 +63,7 @@ struct Batch {
   float beta1, one_minus_beta1, beta2, one_minus_beta2, eps;
   const float* coef;       // device scalar multiplying g in the update (clipping), or NULL
   int32_t bf16;            // 1: bf16 gradients / parameters with fp32 master (Seg::g16, theta16)
+  float gscale;            // multiplies every gradient element on load (DP: 1/world), else 1
 };
 
 // Device-resident MGN / reduction state (all arrays indexed by layer id unless noted).

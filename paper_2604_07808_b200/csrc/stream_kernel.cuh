@@ -44,6 +44,9 @@ __device__ __forceinline__ float4 unpack_bf16x4(uint2 u) {
 __device__ __forceinline__ uint2 pack_bf16x4(float4 f) {
   return make_uint2(f2bf(f.x) | (f2bf(f.y) << 16), f2bf(f.z) | (f2bf(f.w) << 16));
 }
+__device__ __forceinline__ float4 scale4(float4 v, float s) {
+  return make_float4(v.x * s, v.y * s, v.z * s, v.w * s);
+}
 // 4 gradient values at (unit-relative) element e of a stage
 template <bool BF16>
 __device__ __forceinline__ float4 stage_g4(const char* stg, int e) {
@@ -163,6 +166,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
 
   // ------------------------------ consumers -------------------------------
   const float cf = (UPDATE && b.coef) ? *b.coef : 1.0f;
+  const float gs = b.gscale;  // DP: 1/world turns reduce-scattered sums into averages (exact x1 else)
   int s = 0, i = 0;
   for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
     const int stage = i % STAGES;
@@ -196,7 +200,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
         float4 cur[kUnroll];
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q) cur[q] = g4[k % kPre][q];
+        for (int q = 0; q < kUnroll; ++q) cur[q] = scale4(g4[k % kPre][q], gs);
         if (k + kPre < TPS) {  // refill the slot just consumed
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q)
@@ -221,7 +225,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           for (int q = 0; q < kUnroll; ++q) {
             const int e = k * (int)kTile + (q * kThreads + tid) * kVec;  // relative to e0
             if (e < nv) {
-              const float4 g4 = stage_g4<BF16>(stg + L::off_g, e);
+              const float4 g4 = scale4(stage_g4<BF16>(stg + L::off_g, e), gs);
               acc[0] = fma((double)g4.x, (double)g4.x, acc[0]);
               acc[1] = fma((double)g4.y, (double)g4.y, acc[1]);
               acc[2] = fma((double)g4.z, (double)g4.z, acc[2]);
@@ -252,7 +256,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
               for (int j = 0; j < kVec; ++j) {
                 if (e + j < ne) {
                   const int64_t idx = e0 + e + j;
-                  const float g = seg_g<BF16>(sg, idx);
+                  const float g = seg_g<BF16>(sg, idx) * gs;
                   acc[j] = fma((double)g, (double)g, acc[j]);
                   if (UPDATE) {
                     float th = init ? bf2f(sg.theta16[idx]) : sg.theta[idx];

@@ -780,3 +780,77 @@ def test_trace_period_residency_and_dp():
     assert {e["layer"] for e in tr if e["kind"] == "d2h"} == {0}
     assert {e["layer"] for e in tr if e["kind"] == "h2d"} == {2}
     _check_chain(tr)
+
+
+# --------------------------------------------------------- fuzz / edge cases
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_pipelines_bit_identical(seed):
+    """Random layer counts and sizes (ragged), random trainable sets, random
+    chunk / ring / cache sizes, overlap on and off: offload (step and period)
+    and the 1-rank NCCL path must reproduce the resident update bit for bit."""
+    rng = np.random.default_rng(seed)
+    nl = int(rng.integers(2, 7))
+    numel = [int(rng.integers(1, 40_000)) * (8 if seed % 2 else 1) for _ in range(nl)]
+    gamma = int(rng.integers(1, nl + 1))
+    chunk = 4096 * int(rng.integers(1, 5))
+    kws = [dict(), dict(offload=True, chunk_elems=chunk, ring_slots=int(rng.integers(1, 4)),
+                        overlap=bool(rng.integers(0, 2))),
+           dict(offload=True, chunk_elems=chunk, residency=G.RESIDENCY_PERIOD,
+                cache_layers=int(rng.integers(0, nl + 1)), overlap=bool(rng.integers(0, 2)))]
+    if seed % 2:
+        kws.append(dict(force_nccl=True))
+    ctxs = [G.Grass(numel, gamma=gamma, weight_decay=0.01, **kw) for kw in kws]
+    base = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    ps = [[p.clone() for p in base] for _ in ctxs]
+    for step in range(6):
+        ids = [int(x) for x in rng.choice(nl, size=int(rng.integers(1, gamma + 1)), replace=False)]
+        grads = [layer_grad(numel[l], l, 1e-3, step=step, seed=seed, device=DEV) for l in ids]
+        for gr, p in zip(ctxs, ps):
+            gr.step_layers(ids, [p[l] for l in ids], grads, 1e-3)
+        if step == 3:
+            for gr in ctxs:
+                gr.update_probs()
+    torch.cuda.synchronize()
+    for k in range(1, len(ctxs)):
+        for l in range(nl):
+            assert torch.equal(ps[0][l], ps[k][l]), (k, l, kws[k])
+            a, b = ctxs[0].read_state(l), ctxs[k].read_state(l)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+        assert ctxs[0].get_mgn()["m"] == ctxs[k].get_mgn()["m"]
+
+
+def test_many_layers_multi_launch_batches():
+    """N_L = 150 > 64 segments per launch: the probing pass and a 70-layer
+    update are split over several launches (and, on the NCCL path, several
+    rank-sum launches); norms must match the oracle and the paths must agree."""
+    numel = [4096 + 8 * (l % 5) for l in range(150)]
+    ref = G.Grass(numel, gamma=70)
+    dp = G.Grass(numel, gamma=70, force_nccl=True)
+    grads = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
+    for gr in (ref, dp):
+        gr.mgn_accumulate(list(range(150)), grads)
+    st = ref.get_mgn()
+    for l in (0, 63, 64, 127, 128, 149):
+        assert_ss_close(st["last_ss"][l], O.sq_norm(_np(grads[l])))
+    assert st["last_ss"] == dp.get_mgn()["last_ss"]
+    ids = list(range(0, 140, 2))
+    p_ref = [layer_params(numel[l], l, device=DEV) for l in ids]
+    p_dp = [p.clone() for p in p_ref]
+    ref.step_layers(ids, p_ref, [grads[l] for l in ids], 1e-3)
+    dp.step_layers(ids, p_dp, [grads[l] for l in ids], 1e-3)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(p_ref, p_dp))
+    assert ref.get_mgn()["S"] == dp.get_mgn()["S"]
+
+
+def test_single_layer_single_element():
+    gr = G.Grass([1], gamma=1, T_p=0, T_s=1)
+    p = torch.tensor([0.5], device=DEV)
+    g = torch.tensor([-2.0], device=DEV)
+    gr.mgn_accumulate([0], [g])
+    assert gr.update_probs() == [1.0]
+    assert gr.sample_layers(0) == [0]
+    gr.step_layers([0], [p], [g], 0.1)
+    th, m, v = O.adamw_step(np.float32([0.5]), np.float32([0]), np.float32([0]), np.float32([-2.0]), 1, 0.1)
+    assert abs(p.item() - float(th[0])) <= 1e-5 * abs(float(th[0]))
+    assert gr.get_mgn()["S"] == [2.0]
