@@ -854,3 +854,43 @@ def test_single_layer_single_element():
     th, m, v = O.adamw_step(np.float32([0.5]), np.float32([0]), np.float32([0]), np.float32([-2.0]), 1, 0.1)
     assert abs(p.item() - float(th[0])) <= 1e-5 * abs(float(th[0]))
     assert gr.get_mgn()["S"] == [2.0]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuzz_dtypes_clip_checkpoint(seed, tmp_path):
+    """Like the pipeline fuzz, over both dtypes and random clipping, with a
+    checkpoint written by one path and restored into a fresh context of a
+    different path mid-run: every path stays bit-identical to resident."""
+    rng = np.random.default_rng(100 + seed)
+    dtype = G.DTYPE_BF16 if seed % 2 else G.DTYPE_FP32
+    tdt = torch.bfloat16 if seed % 2 else torch.float32
+    nl = int(rng.integers(2, 6))
+    numel = [int(rng.integers(1, 30_000)) for _ in range(nl)]
+    gamma = int(rng.integers(1, nl + 1))
+    clip = float(rng.choice([0.0, 1e-3, 1.0]))
+    chunk = 4096 * int(rng.integers(1, 4))
+    common = dict(gamma=gamma, weight_decay=0.01, max_grad_norm=clip, param_dtype=dtype)
+    kws = [dict(), dict(offload=True, chunk_elems=chunk, ring_slots=int(rng.integers(1, 4))),
+           dict(offload=True, chunk_elems=chunk, residency=G.RESIDENCY_PERIOD),
+           dict(force_nccl=True)]
+    ctxs = [G.Grass(numel, **common, **kw) for kw in kws]
+    base = [layer_params(n, l, device=DEV).to(tdt) for l, n in enumerate(numel)]
+    ps = [[p.clone() for p in base] for _ in ctxs]
+    for step in range(8):
+        ids = [int(x) for x in rng.choice(nl, size=int(rng.integers(1, gamma + 1)), replace=False)]
+        grads = [layer_grad(numel[l], l, 1e-2, step=step, seed=seed, device=DEV).to(tdt) for l in ids]
+        for gr, p in zip(ctxs, ps):
+            gr.step_layers(ids, [p[l] for l in ids], grads, 1e-3)
+        if step == 4:   # checkpoint the offload context, restore into a fresh period context
+            path = str(tmp_path / "ck")
+            ctxs[1].save_state(path)
+            ctxs[2] = G.Grass(numel, **common, **kws[2])
+            ctxs[2].load_state(path)
+    torch.cuda.synchronize()
+    for k in range(1, len(ctxs)):
+        for l in range(nl):
+            assert torch.equal(ps[0][l], ps[k][l]), (seed, k, l)
+            a, b = ctxs[0].read_state(l), ctxs[k].read_state(l)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+            if dtype == G.DTYPE_BF16 and a[2] > 0:
+                assert np.array_equal(ctxs[0].read_master(l), ctxs[k].read_master(l))
