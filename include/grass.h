@@ -23,6 +23,9 @@
  *     unchanged, and grass_last_error() describes the failure.
  *   - A "layer" is ONE flat, contiguous, 16-byte aligned fp32 buffer of N_p(l)
  *     elements in device memory (the decoder block's tensors viewed back to back).
+ *   - Every layer buffer is checked before anything is enqueued: 16-byte
+ *     alignment, device memory of the context's GPU, and that its allocation
+ *     (cuMemGetAddressRange; a caching allocator's segment) holds N_p elements.
  *   - Device pointers (params, grads) are CALLER-owned and must stay valid until
  *     the work enqueued on `stream` has completed.  Host arrays passed in
  *     (ids, pointer arrays, probs) are read before the call returns.

@@ -292,6 +292,24 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
   return GRASS_OK;
 }
 
+// cuMemGetAddressRange through the runtime's driver entry point (no link-time
+// libcuda dependency): lets check_call reject a buffer smaller than its layer
+// instead of letting the kernel fault.
+typedef int (*AddressRangeFn)(unsigned long long* base, size_t* size, unsigned long long ptr);
+AddressRangeFn address_range_fn() {
+  static AddressRangeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (AddressRangeFn) nullptr;
+    }
+    return reinterpret_cast<AddressRangeFn>(f);
+  }();
+  return fn;
+}
+
 // Resolve, validate and order the layer list of a hot-path call.
 grass_status check_call(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_t n,
                         const void* const* p1, const void* const* p2, std::vector<int>* order) {
@@ -320,6 +338,15 @@ grass_status check_call(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_
       if (!(at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ||
           at.device != c->cfg.device)
         return c->fail(GRASS_E_INVALID, "layer buffers must be device memory on the context's GPU");
+      if (AddressRangeFn fn = address_range_fn()) {
+        unsigned long long base = 0;
+        size_t size = 0;
+        const unsigned long long ptr = reinterpret_cast<uintptr_t>(p);
+        const unsigned long long need = (unsigned long long)c->numel[ids[i]] * c->esz;
+        if (fn(&base, &size, ptr) == 0 && ptr + need > base + size)
+          return c->fail(GRASS_E_INVALID, "buffer of layer " + std::to_string(ids[i]) +
+                                              " is smaller than its N_p elements");
+      }
     }
   }
   order->resize(n);

@@ -894,3 +894,35 @@ def test_fuzz_dtypes_clip_checkpoint(seed, tmp_path):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
             if dtype == G.DTYPE_BF16 and a[2] > 0:
                 assert np.array_equal(ctxs[0].read_master(l), ctxs[k].read_master(l))
+
+
+def test_too_small_buffer_rejected_before_launch():
+    """A buffer whose allocation ends before N_p elements is rejected before
+    anything is enqueued (cuMemGetAddressRange).  torch's caching allocator
+    sub-allocates inside larger segments, so the allocation here is a raw
+    cudaMalloc passed straight through the C ABI."""
+    import ctypes as C
+    try:
+        from cuda.bindings import runtime as rt
+    except ImportError:
+        from cuda import cudart as rt
+    gr = G.Grass([65_536, 4096], gamma=1)
+    err, ptr = rt.cudaMalloc(4 * (65_536 - 4))
+    assert int(err) == 0
+    try:
+        ids = (C.c_int32 * 1)(0)
+        arr = (C.c_void_p * 1)(int(ptr))
+        st = G.binding.lib().grass_mgn_accumulate(gr._h, ids, 1, arr, None)
+        assert st == G.binding.E_INVALID
+        assert b"smaller" in G.binding.lib().grass_last_error(gr._h)
+        ok = torch.zeros(65_536, device=DEV)
+        st = G.binding.lib().grass_step_layers(gr._h, ids, 1, (C.c_void_p * 1)(ok.data_ptr()), arr,
+                                               C.c_float(1e-3), None)
+        assert st == G.binding.E_INVALID
+    finally:
+        rt.cudaFree(ptr)
+    # views inside a big enough allocation are fine
+    big = torch.zeros(65_536 + 4096, device=DEV)
+    gr.mgn_accumulate([0, 1], [big[:65_536], big[65_536:]])
+    gr.sync()
+    assert gr.get_mgn()["c"] == [1, 1]
