@@ -230,6 +230,16 @@ grass_status grass_write_master(grass_ctx* ctx, int32_t layer, const float* in);
 grass_status grass_read_state(grass_ctx* ctx, int32_t layer, float* m_out, float* v_out,
                               int64_t* t_out);
 
+/* GRASS_RESIDENCY_PERIOD: starts bringing the optimizer states of the listed
+ * layers into the HBM cache now (evicting least-recently-used layers that are
+ * not listed), on the context's copy streams, without updating anything.
+ * Call it right after grass_sample_layers at a period boundary: the transfers
+ * then overlap the caller's forward/backward pass, and the next
+ * grass_step_layers of these layers finds them resident ("GRASS
+ * asynchronously prefetches optimizer states").  `stream` orders the evictions
+ * after the caller's earlier work.  GRASS_E_STATE without period residency. */
+grass_status grass_prefetch_layers(grass_ctx* ctx, const int32_t* layer_ids, int32_t n, void* stream);
+
 /* GRASS_RESIDENCY_PERIOD: writes the m/v of every layer cached in HBM back to
  * its pinned host home (the cache stays valid).  No-op otherwise.
  * Synchronises. */

@@ -77,6 +77,7 @@ _SIGS = {
                                    C.POINTER(C.c_int64)]),
     "grass_write_state": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64]),
     "grass_flush_states": (C.c_int, [C.c_void_p]),
+    "grass_prefetch_layers": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_void_p]),
     "grass_mgn_accumulate_bf16": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32,
                                             C.POINTER(C.c_void_p), C.c_void_p]),
     "grass_step_layers_bf16": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32,
@@ -353,6 +354,10 @@ class Grass:
         return [{"kind": TRACE_KINDS[e.kind], "layer": e.layer, "offset": e.offset,
                  "count": e.count, "start_ms": e.start_ms, "end_ms": e.end_ms}
                 for e in buf[:min(n.value, capacity)]]
+
+    def prefetch_layers(self, layer_ids: Sequence[int], stream=None):
+        ids = (C.c_int32 * len(layer_ids))(*layer_ids)
+        _check(lib().grass_prefetch_layers(self._h, ids, len(layer_ids), _stream_ptr(stream)), self._h)
 
     def flush_states(self):
         _check(lib().grass_flush_states(self._h), self._h)

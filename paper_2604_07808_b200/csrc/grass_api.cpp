@@ -79,6 +79,8 @@ struct grass_ctx {
   std::vector<char> slot_dirty;
   int64_t call_seq = 0;
   cudaEvent_t ev_evict = nullptr, ev_fill = nullptr;
+  std::vector<cudaEvent_t> ev_slot_ready;  // grass_prefetch_layers: fill of the slot done
+  std::vector<char> slot_ready_pending;
 
   // outstanding stream-ordered work (for the synchronising calls): the last
   // event recorded on each stream the caller used
@@ -680,6 +682,49 @@ grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, const Seg&
   return GRASS_OK;
 }
 
+// Prefetch (grass_prefetch_layers): the swap of swap_in_layer without the
+// update — victim write-back || fetch of l's states on the copy streams, the
+// slot marked clean and "ready" by an event the next update waits on.
+grass_status prefetch_into(grass_ctx* c, int l, int slot, int victim) {
+  const int64_t ll = c->shard_len[l];
+  const int64_t lv = (victim >= 0 && c->slot_dirty[slot]) ? c->shard_len[victim] : 0;
+  if (c->layer_done_valid[l]) CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, c->ev_layer_done[l], 0));
+  for (int64_t off = 0; off < std::max(ll, lv); off += c->chunk) {
+    if (off < lv) {
+      const size_t vb = sizeof(float) * (size_t)std::min(c->chunk, lv - off);
+      TraceScope ts(c, c->d2h, GRASS_TRACE_D2H, victim, off, (int64_t)(vb / sizeof(float)));
+      for (int a = 0; a < c->ns; ++a)
+        CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][victim] + off, cache_arr(c, slot, a) + off, vb,
+                                    cudaMemcpyDeviceToHost, c->d2h));
+      if (off < ll) {
+        CUDA_TRY(c, cudaEventRecord(c->ev_evict, c->d2h));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, c->ev_evict, 0));
+      }
+    }
+    if (off < ll) {
+      const int64_t n = std::min(c->chunk, ll - off);
+      TraceScope ts(c, c->h2d, GRASS_TRACE_H2D, l, off, n);
+      for (int a = 0; a < c->ns; ++a)
+        if (!(a == 2 && !c->master_valid[l]))
+          CUDA_TRY(c, cudaMemcpyAsync(cache_arr(c, slot, a) + off, c->arr[a][l] + off,
+                                      sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, c->h2d));
+    }
+  }
+  CUDA_TRY(c, cudaEventRecord(c->ev_slot_ready[slot], c->h2d));
+  c->slot_ready_pending[slot] = 1;
+  if (victim >= 0) {
+    if (lv > 0) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_layer_done[victim], c->d2h));
+      c->layer_done_valid[victim] = 1;
+    }
+    c->layer_slot[victim] = -1;
+  }
+  c->slot_layer[slot] = l;
+  c->layer_slot[l] = slot;
+  c->slot_dirty[slot] = 0;  // the cached copy equals the host copy
+  return GRASS_OK;
+}
+
 // Writes every dirty cached layer back to its host home (synchronous).
 grass_status flush_cache(grass_ctx* c) {
   if (c->cache_slots == 0) return GRASS_OK;
@@ -758,7 +803,7 @@ void free_ctx(grass_ctx* c) {
     else
       cudaFree(c->state_block);
   }
-  for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free, &c->ev_layer_done, &c->ev_free_list})
+  for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free, &c->ev_layer_done, &c->ev_free_list, &c->ev_slot_ready})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
   for (auto& pe : c->ev_pending) cudaEventDestroy(pe.second);
@@ -869,6 +914,9 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
       c->slot_dirty.assign(c->cache_slots, 0);
       for (cudaEvent_t* e : {&c->ev_evict, &c->ev_fill})
         CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      c->ev_slot_ready.assign(c->cache_slots, nullptr);
+      for (auto& e : c->ev_slot_ready) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->slot_ready_pending.assign(c->cache_slots, 0);
     } else {
       CUDA_TRY(c, dalloc((void**)&c->d_ring, sizeof(float) * (size_t)c->ns * (size_t)c->chunk * c->slots));
     }
@@ -1039,6 +1087,10 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     if (period) {
       const int slot = slot_of[j];
       if (c->slot_layer[slot] == l) {  // hit: update in place in HBM, no link traffic
+        if (c->slot_ready_pending[slot]) {  // prefetched: wait for its fill
+          CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_slot_ready[slot], 0));
+          c->slot_ready_pending[slot] = 0;
+        }
         float* sp[3];
         for (int a = 0; a < c->ns; ++a) sp[a] = cache_arr(c, slot, a);
         set_update(c, &base, param, sp, init);
@@ -1279,6 +1331,30 @@ grass_status grass_write_master(grass_ctx* c, int32_t layer, const float* in) {
   if (s == GRASS_OK) s = copy_state_in(c, 2, layer, in);
   if (s == GRASS_OK) c->master_valid[layer] = 1;
   return s;
+}
+
+grass_status grass_prefetch_layers(grass_ctx* c, const int32_t* ids, int32_t n, void* stream) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (c->cache_slots == 0) return c->fail(GRASS_E_STATE, "prefetch needs GRASS_RESIDENCY_PERIOD");
+  std::vector<int> order;
+  grass_status s = check_call(c, c->bf16, ids, n, nullptr, nullptr, &order);
+  if (s != GRASS_OK) return s;
+  if (n > c->cache_slots) return c->fail(GRASS_E_INVALID, "more layers than cache slots");
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<int> slot_of, victim_of;
+  cache_plan(c, ids, order, &slot_of, &victim_of);
+  c->call_seq++;
+  // write-backs read slots last written by updates enqueued before this call
+  if ((s = mark_pending(c, st)) != GRASS_OK) return s;
+  if ((s = wait_pending(c, c->d2h)) != GRASS_OK) return s;
+  for (int j = 0; j < (int)order.size(); ++j) {
+    const int l = ids[order[j]], slot = slot_of[j];
+    c->slot_use[slot] = c->call_seq;
+    if (c->slot_layer[slot] == l) continue;  // already cached
+    if ((s = prefetch_into(c, l, slot, victim_of[j])) != GRASS_OK) return s;
+  }
+  return GRASS_OK;
 }
 
 grass_status grass_flush_states(grass_ctx* c) {

@@ -926,3 +926,38 @@ def test_too_small_buffer_rejected_before_launch():
     gr.mgn_accumulate([0, 1], [big[:65_536], big[65_536:]])
     gr.sync()
     assert gr.get_mgn()["c"] == [1, 1]
+
+
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+def test_prefetch_then_step_bit_identical(dtype):
+    """grass_prefetch_layers at a period boundary: the new layers' states move
+    while the caller computes (a busy kernel stands in for fwd/bwd); the
+    following step finds them resident (no link traffic inside it) and the
+    result equals the resident path bit for bit."""
+    tdt = torch.bfloat16 if dtype == G.DTYPE_BF16 else torch.float32
+    n = 4096 * 40 + 8
+    numel = [n] * 5
+    ref = G.Grass(numel, gamma=2, param_dtype=dtype)
+    per = G.Grass(numel, gamma=2, param_dtype=dtype, offload=True, chunk_elems=4096 * 8,
+                  residency=G.RESIDENCY_PERIOD)
+    base = [layer_params(n, l, device=DEV).to(tdt) for l in range(5)]
+    pr, pp = [p.clone() for p in base], [p.clone() for p in base]
+    junk = torch.randn(4096, 4096, device=DEV)
+    for period, ids in enumerate([[0, 1], [2, 3], [4, 0], [4, 0], [1, 2]]):
+        per.prefetch_layers(ids)
+        for _ in range(3):
+            junk = torch.tanh(junk @ junk * 1e-3)          # the caller's "backward"
+        grads = [layer_grad(n, l, 1e-3, step=period, device=DEV).to(tdt) for l in ids]
+        per.trace_enable(True)
+        per.step_layers(ids, [pp[l] for l in ids], grads, 1e-3)
+        tr = per.trace_read()
+        per.trace_enable(False)
+        assert not [e for e in tr if e["kind"] in ("h2d", "d2h")], period   # all hits
+        ref.step_layers(ids, [pr[l] for l in ids], grads, 1e-3)
+    torch.cuda.synchronize()
+    for l in range(5):
+        assert torch.equal(pr[l], pp[l]), l
+        a, b = ref.read_state(l), per.read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    with pytest.raises(G.GrassError):
+        ref.prefetch_layers([0])                            # needs period residency
