@@ -19,8 +19,11 @@
  *
  * Conventions (all calls):
  *   - Every entry point returns a grass_status; no C++ exception ever crosses
- *     this boundary.  On error nothing has been enqueued, the context is
- *     unchanged, and grass_last_error() describes the failure.
+ *     this boundary (each is a function-try-block).  On a validation error
+ *     nothing has been enqueued, the context is unchanged, and
+ *     grass_last_error() describes the failure.
+ *   - A context is not thread-safe: calls on one context must not overlap.
+ *     Distinct contexts are independent.
  *   - A "layer" is ONE flat, contiguous, 16-byte aligned fp32 buffer of N_p(l)
  *     elements in device memory (the decoder block's tensors viewed back to back).
  *   - Every layer buffer is checked before anything is enqueued: 16-byte

@@ -1166,12 +1166,32 @@ std::vector<char> ck_header(grass_ctx* c) {
   return h;
 }
 
+// Every exported entry point is a function-try-block: no C++ exception
+// (std::bad_alloc from a host container, ...) ever crosses the C ABI.
+grass_status api_exception(grass_ctx* c) noexcept {
+  const char* msg = "internal error (exception)";
+  try {
+    throw;
+  } catch (const std::bad_alloc&) {
+    msg = "host memory allocation failed";
+  } catch (const std::exception& e) {
+    msg = e.what();
+  } catch (...) {
+  }
+  try {
+    if (c) c->err = msg;
+    g_thread_err = msg;
+  } catch (...) {
+  }
+  return GRASS_E_OOM;
+}
+
 }  // namespace
 
 // =========================== exported C ABI ================================
 extern "C" {
 
-grass_status grass_config_init(grass_config* cfg) {
+grass_status grass_config_init(grass_config* cfg) try {
   if (!cfg) return set_thread_err(GRASS_E_INVALID, "cfg is NULL");
   std::memset(cfg, 0, sizeof(*cfg));
   cfg->gamma = 2;
@@ -1190,9 +1210,11 @@ grass_status grass_config_init(grass_config* cfg) {
   cfg->overlap = 1;
   cfg->world = 1;
   return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
 }
 
-grass_status grass_create(const grass_config* cfg, grass_ctx** out) {
+grass_status grass_create(const grass_config* cfg, grass_ctx** out) try {
   if (!out) return set_thread_err(GRASS_E_INVALID, "out is NULL");
   *out = nullptr;
   std::string why;
@@ -1213,40 +1235,52 @@ grass_status grass_create(const grass_config* cfg, grass_ctx** out) {
   }
   *out = c;
   return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
 }
 
 void grass_destroy(grass_ctx* ctx) { free_ctx(ctx); }
 
 const char* grass_last_error(const grass_ctx* ctx) { return ctx ? ctx->err.c_str() : g_thread_err.c_str(); }
 
-grass_status grass_sync(grass_ctx* ctx) {
+grass_status grass_sync(grass_ctx* ctx) try {
   if (!ctx) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   return drain(ctx, true);
+} catch (...) {
+  return api_exception(ctx);
 }
 
 grass_status grass_mgn_accumulate(grass_ctx* c, const int32_t* ids, int32_t n, const float* const* grads,
-                                  void* stream) {
+                                  void* stream) try {
   return mgn_accumulate_impl(c, false, ids, n, reinterpret_cast<const void* const*>(grads), stream);
+} catch (...) {
+  return api_exception(c);
 }
 
 grass_status grass_mgn_accumulate_bf16(grass_ctx* c, const int32_t* ids, int32_t n,
-                                       const uint16_t* const* grads, void* stream) {
+                                       const uint16_t* const* grads, void* stream) try {
   return mgn_accumulate_impl(c, true, ids, n, reinterpret_cast<const void* const*>(grads), stream);
+} catch (...) {
+  return api_exception(c);
 }
 
 grass_status grass_step_layers(grass_ctx* c, const int32_t* ids, int32_t n, float* const* params,
-                               const float* const* grads, float lr, void* stream) {
+                               const float* const* grads, float lr, void* stream) try {
   return step_layers_impl(c, false, ids, n, reinterpret_cast<void* const*>(params),
                           reinterpret_cast<const void* const*>(grads), lr, stream);
+} catch (...) {
+  return api_exception(c);
 }
 
 grass_status grass_step_layers_bf16(grass_ctx* c, const int32_t* ids, int32_t n, uint16_t* const* params,
-                                    const uint16_t* const* grads, float lr, void* stream) {
+                                    const uint16_t* const* grads, float lr, void* stream) try {
   return step_layers_impl(c, true, ids, n, reinterpret_cast<void* const*>(params),
                           reinterpret_cast<const void* const*>(grads), lr, stream);
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_update_probs(grass_ctx* c, double* probs_out) {
+grass_status grass_update_probs(grass_ctx* c, double* probs_out) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   // one stream-ordered snapshot: S, c, flag -> host; window and flag reset
   grass_status s = fetch_mgn(c, true, true);
@@ -1281,9 +1315,11 @@ grass_status grass_update_probs(grass_ctx* c, double* probs_out) {
   }
   if (probs_out) std::memcpy(probs_out, c->probs.data(), sizeof(double) * c->nl);
   return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_sample_layers(grass_ctx* c, const double* probs, uint64_t period, int32_t* ids_out) {
+grass_status grass_sample_layers(grass_ctx* c, const double* probs, uint64_t period, int32_t* ids_out) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (!ids_out) return c->fail(GRASS_E_INVALID, "ids_out is NULL");
   const double* p = probs ? probs : c->probs.data();
@@ -1291,9 +1327,11 @@ grass_status grass_sample_layers(grass_ctx* c, const double* probs, uint64_t per
     if (!(p[l] >= 0.0) || !std::isfinite(p[l])) return c->fail(GRASS_E_INVALID, "probs must be finite, >= 0");
   sample_from_probs(p, c->nl, c->cfg.gamma, c->cfg.seed, period, ids_out);
   return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_read_state(grass_ctx* c, int32_t layer, float* m_out, float* v_out, int64_t* t_out) {
+grass_status grass_read_state(grass_ctx* c, int32_t layer, float* m_out, float* v_out, int64_t* t_out) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (layer < 0 || layer >= c->nl) return c->fail(GRASS_E_INVALID, "layer id out of range");
   grass_status s = drain(c, false);
@@ -1301,9 +1339,11 @@ grass_status grass_read_state(grass_ctx* c, int32_t layer, float* m_out, float* 
   if (s == GRASS_OK && v_out) s = copy_state_out(c, 1, layer, v_out);
   if (s == GRASS_OK && t_out) *t_out = c->t[layer];
   return s;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_write_state(grass_ctx* c, int32_t layer, const float* m_in, const float* v_in, int64_t t_in) {
+grass_status grass_write_state(grass_ctx* c, int32_t layer, const float* m_in, const float* v_in, int64_t t_in) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (layer < 0 || layer >= c->nl) return c->fail(GRASS_E_INVALID, "layer id out of range");
   if (t_in < 0) return c->fail(GRASS_E_INVALID, "step count must be >= 0");
@@ -1312,18 +1352,22 @@ grass_status grass_write_state(grass_ctx* c, int32_t layer, const float* m_in, c
   if (s == GRASS_OK && v_in) s = copy_state_in(c, 1, layer, v_in);
   if (s == GRASS_OK) c->t[layer] = t_in;
   return s;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_read_master(grass_ctx* c, int32_t layer, float* out) {
+grass_status grass_read_master(grass_ctx* c, int32_t layer, float* out) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (layer < 0 || layer >= c->nl || !out) return c->fail(GRASS_E_INVALID, "bad layer or NULL output");
   if (!c->bf16) return c->fail(GRASS_E_STATE, "fp32 context: the parameters are the master");
   if (!c->master_valid[layer]) return c->fail(GRASS_E_STATE, "master of this layer not initialised yet");
   grass_status s = drain(c, false);
   return s == GRASS_OK ? copy_state_out(c, 2, layer, out) : s;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_write_master(grass_ctx* c, int32_t layer, const float* in) {
+grass_status grass_write_master(grass_ctx* c, int32_t layer, const float* in) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (layer < 0 || layer >= c->nl || !in) return c->fail(GRASS_E_INVALID, "bad layer or NULL input");
   if (!c->bf16) return c->fail(GRASS_E_STATE, "fp32 context: the parameters are the master");
@@ -1331,9 +1375,11 @@ grass_status grass_write_master(grass_ctx* c, int32_t layer, const float* in) {
   if (s == GRASS_OK) s = copy_state_in(c, 2, layer, in);
   if (s == GRASS_OK) c->master_valid[layer] = 1;
   return s;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_prefetch_layers(grass_ctx* c, const int32_t* ids, int32_t n, void* stream) {
+grass_status grass_prefetch_layers(grass_ctx* c, const int32_t* ids, int32_t n, void* stream) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (c->cache_slots == 0) return c->fail(GRASS_E_STATE, "prefetch needs GRASS_RESIDENCY_PERIOD");
   std::vector<int> order;
@@ -1355,17 +1401,21 @@ grass_status grass_prefetch_layers(grass_ctx* c, const int32_t* ids, int32_t n, 
     if ((s = prefetch_into(c, l, slot, victim_of[j])) != GRASS_OK) return s;
   }
   return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_flush_states(grass_ctx* c) {
+grass_status grass_flush_states(grass_ctx* c) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
   return flush_cache(c);
+} catch (...) {
+  return api_exception(c);
 }
 
 grass_status grass_get_mgn(grass_ctx* c, double* m_out, double* S_out, int64_t* c_out, double* ss_out,
-                           double* probs_out) {
+                           double* probs_out) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
@@ -1376,9 +1426,11 @@ grass_status grass_get_mgn(grass_ctx* c, double* m_out, double* S_out, int64_t* 
   if (m_out) std::memcpy(m_out, c->mgn.data(), sizeof(double) * c->nl);
   if (probs_out) std::memcpy(probs_out, c->probs.data(), sizeof(double) * c->nl);
   return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_trace_enable(grass_ctx* c, int32_t on) {
+grass_status grass_trace_enable(grass_ctx* c, int32_t on) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
@@ -1391,9 +1443,11 @@ grass_status grass_trace_enable(grass_ctx* c, int32_t on) {
   if (on) CUDA_TRY(c, cudaEventRecord(c->trace_base, c->aux));
   c->tracing = on != 0;
   return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_trace_read(grass_ctx* c, grass_trace_event* out, int32_t capacity, int32_t* count) {
+grass_status grass_trace_read(grass_ctx* c, grass_trace_event* out, int32_t capacity, int32_t* count) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (!count || (capacity > 0 && !out)) return c->fail(GRASS_E_INVALID, "bad output arguments");
   if (!c->tracing) return c->fail(GRASS_E_STATE, "tracing is not enabled");
@@ -1418,9 +1472,11 @@ grass_status grass_trace_read(grass_ctx* c, grass_trace_event* out, int32_t capa
   c->trace.clear();
   CUDA_TRY(c, cudaEventRecord(c->trace_base, c->aux));
   return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_save_state(grass_ctx* c, const char* path) {
+grass_status grass_save_state(grass_ctx* c, const char* path) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (!path) return c->fail(GRASS_E_INVALID, "path is NULL");
   grass_status s = drain(c, false);
@@ -1455,9 +1511,11 @@ grass_status grass_save_state(grass_ctx* c, const char* path) {
   ok = (std::fclose(f) == 0) && ok;
   if (!ok) return c->fail(GRASS_E_IO, std::string("short write to ") + path);
   return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
 }
 
-grass_status grass_load_state(grass_ctx* c, const char* path) {
+grass_status grass_load_state(grass_ctx* c, const char* path) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (!path) return c->fail(GRASS_E_INVALID, "path is NULL");
   grass_status s = drain(c, false);
@@ -1553,6 +1611,8 @@ grass_status grass_load_state(grass_ctx* c, const char* path) {
   std::memcpy(blk.data() + 8 * (size_t)nl, cnt.data(), 8 * (size_t)nl);
   CUDA_TRY(c, cudaMemcpy(c->d_mgn, blk.data(), blk.size(), cudaMemcpyHostToDevice));
   return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
 }
 
 int64_t grass_device_bytes(const grass_ctx* c) { return c ? c->dev_bytes : 0; }
@@ -1564,30 +1624,36 @@ const char* grass_version(void) { return "grass-b200 1.0 (sm_100a)"; }
 uint64_t grass_splitmix64(uint64_t x) { return splitmix64(x); }
 double grass_uniform(uint64_t seed, uint64_t period, uint32_t k) { return uniform01(seed, period, k); }
 
-grass_status grass_softmax_probs(const double* m, int32_t n, double tau, int32_t normalize, double* p_out) {
+grass_status grass_softmax_probs(const double* m, int32_t n, double tau, int32_t normalize, double* p_out) try {
   if (!m || !p_out || n < 1) return set_thread_err(GRASS_E_INVALID, "bad arguments");
   if (!(tau > 0.0)) return set_thread_err(GRASS_E_INVALID, "tau must be positive");
   for (int i = 0; i < n; ++i)
     if (!std::isfinite(m[i]) || m[i] < 0.0) return set_thread_err(GRASS_E_INVALID, "m must be finite, >= 0");
   softmax_probs(m, n, tau, normalize != 0, p_out);
   return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
 }
 
 grass_status grass_sample_from_probs(const double* p, int32_t n, int32_t gamma, uint64_t seed, uint64_t period,
-                                     int32_t* ids_out) {
+                                     int32_t* ids_out) try {
   if (!p || !ids_out || n < 1) return set_thread_err(GRASS_E_INVALID, "bad arguments");
   if (gamma < 1 || gamma > n) return set_thread_err(GRASS_E_INVALID, "gamma must lie in [1, N_L]");
   for (int i = 0; i < n; ++i)
     if (!(p[i] >= 0.0) || !std::isfinite(p[i])) return set_thread_err(GRASS_E_INVALID, "probs must be finite, >= 0");
   sample_from_probs(p, n, gamma, seed, period, ids_out);
   return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
 }
 
-grass_status grass_shard_range(int64_t numel, int32_t world, int32_t rank, int64_t* offset, int64_t* count) {
+grass_status grass_shard_range(int64_t numel, int32_t world, int32_t rank, int64_t* offset, int64_t* count) try {
   if (!offset || !count) return set_thread_err(GRASS_E_INVALID, "NULL output");
   if (!shard_range(numel, world, rank, offset, count))
     return set_thread_err(GRASS_E_INVALID, "numel must be >= 1 (and divisible by 4*world when world > 1)");
   return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
 }
 
 int32_t grass_schedule_decision(int64_t step, int32_t T_p, int32_t T_s, int32_t T_u) {
@@ -1595,11 +1661,13 @@ int32_t grass_schedule_decision(int64_t step, int32_t T_p, int32_t T_s, int32_t 
   return schedule_decision(step, T_p, T_s, T_u);
 }
 
-grass_status grass_nccl_get_unique_id(void* out) {
+grass_status grass_nccl_get_unique_id(void* out) try {
   if (!out) return set_thread_err(GRASS_E_INVALID, "out is NULL");
   std::string err;
   if (!nccl_unique_id(out, &err)) return set_thread_err(GRASS_E_NCCL, err);
   return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
 }
 
 }  // extern "C"
