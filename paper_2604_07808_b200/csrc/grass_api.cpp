@@ -1014,6 +1014,9 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   const int32_t mode = clip ? kFinalizeNone : (sharded ? kFinalizeShard : kFinalizeMgn);
   const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
   const int nact = (int)order.size();
+  if (period && nact > c->cache_slots)
+    return c->fail(GRASS_E_INVALID, "period residency: more layers in one call than cache slots "
+                                    "(raise cache_layers)");
   struct CoefReset {  // the clip multiplier only applies inside this call
     grass_ctx* c;
     ~CoefReset() { c->cur_coef = nullptr; }

@@ -961,3 +961,18 @@ def test_prefetch_then_step_bit_identical(dtype):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     with pytest.raises(G.GrassError):
         ref.prefetch_layers([0])                            # needs period residency
+
+
+def test_period_residency_rejects_more_layers_than_slots():
+    gr = G.Grass([4096] * 4, gamma=2, offload=True, chunk_elems=4096, residency=G.RESIDENCY_PERIOD,
+                 max_grad_norm=1.0)
+    p = [torch.zeros(4096, device=DEV) for _ in range(4)]
+    g = [torch.ones(4096, device=DEV) for _ in range(4)]
+    with pytest.raises(G.GrassError) as e:
+        gr.step_layers([0, 1, 2], p[:3], g[:3], 1e-3)
+    assert e.value.status == G.binding.E_INVALID
+    assert gr.get_mgn()["c"] == [0, 0, 0, 0]          # nothing was enqueued (not even clip pass 1)
+    with pytest.raises(G.GrassError):
+        gr.prefetch_layers([0, 1, 2])
+    G.Grass([4096] * 4, gamma=2, offload=True, residency=G.RESIDENCY_PERIOD,
+            cache_layers=3).step_layers([0, 1, 2], p[:3], g[:3], 1e-3)   # enough slots: fine
