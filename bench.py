@@ -318,12 +318,16 @@ def run_grass(args, rank, world, local):
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ksteps = max(3, min(args.steps, 10))
+        def host_step(step):
+            nonlocal ids
+            # the public call with the step's gradients in pinned HOST memory: the
+            # library streams them chunk-wise into HBM, overlapped with the update
+            ctx.step_layers(ids, [params[l] for l in ids], host_g[:len(ids)], args.lr, stream=s)
+            ctx.update_probs()                  # reads S, c back (d2h)
+            ids = ctx.sample_layers(step + 1)
         e0.record(s)
         for k in range(ksteps):
-            with torch.cuda.stream(s):
-                for j, l in enumerate(ids):
-                    grads[l].copy_(host_g[j], non_blocking=True)
-            one_step(1000 + k, None)            # update_probs reads S, c back (d2h)
+            host_step(1000 + k)
         e1.record(s)
         torch.cuda.synchronize()
         et = max_over_ranks(e0.elapsed_time(e1) / 1e3, world, dev)

@@ -199,7 +199,12 @@ grass_status grass_sample_layers(grass_ctx* ctx, const double* probs, uint64_t p
  * over NCCL, each rank updates its element shard with its own m/v slice, and
  * parameters are all-gathered back into params[i].
  *   params: host [n] array of DEVICE pointers (fp32, N_p each, updated in place)
- *   grads:  host [n] array of DEVICE pointers (fp32, N_p each, read only)
+ *   grads:  host [n] array of DEVICE pointers (fp32, N_p each, read only), or
+ *           of PINNED HOST pointers (world = 1, resident or per-step offload,
+ *           no clipping): the gradient is then fetched chunk by chunk through a
+ *           device ring on the context's copy stream, overlapping the update
+ *           (the e2e "gradients live on the host" case); pageable host memory
+ *           is rejected
  *   lr:     learning rate eta for this step (> 0 or == 0)
  * Stream-ordered on `stream`: when `stream` reaches this point the update, the
  * write-back of m/v to host and the MGN accumulation have all completed. */

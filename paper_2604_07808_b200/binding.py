@@ -190,10 +190,11 @@ def _stream_ptr(stream) -> int:
     return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def _ptrs(tensors, itemsize: int = 4):
+def _ptrs(tensors, itemsize: int = 4, host_ok: bool = False):
     arr = (C.c_void_p * len(tensors))()
     for i, t in enumerate(tensors):
-        if not t.is_cuda or not t.is_contiguous() or t.dtype.itemsize != itemsize:
+        on_dev = t.is_cuda or (host_ok and t.is_pinned())
+        if not on_dev or not t.is_contiguous() or t.dtype.itemsize != itemsize:
             raise ValueError(f"layer buffers must be contiguous CUDA tensors of {itemsize}-byte "
                              "elements (fp32, or bf16 for a bf16 context)")
         arr[i] = t.data_ptr()
@@ -296,7 +297,7 @@ class Grass:
         ids = (C.c_int32 * len(layer_ids))(*layer_ids)
         f = lib().grass_step_layers_bf16 if self.bf16 else lib().grass_step_layers
         isz = 2 if self.bf16 else 4
-        _check(f(self._h, ids, len(layer_ids), _ptrs(params, isz), _ptrs(grads, isz),
+        _check(f(self._h, ids, len(layer_ids), _ptrs(params, isz), _ptrs(grads, isz, host_ok=True),
                  float(lr), _stream_ptr(stream)), self._h)
 
     def sync(self):

@@ -62,6 +62,7 @@ struct grass_ctx {
 
   // offload ring (step residency)
   float* d_ring = nullptr;  // slots x ns x chunk floats
+  char* d_gring = nullptr;  // slots x chunk gradient elements (host gradients), lazily allocated
   int slots = 0;
   int64_t chunk = 0;
   int64_t ring_pos = 0;
@@ -313,8 +314,12 @@ AddressRangeFn address_range_fn() {
 }
 
 // Resolve, validate and order the layer list of a hot-path call.
+// p2 (the gradients) may be PINNED HOST memory when `host_p2` is non-NULL
+// (grass_step_layers); (*host_p2)[i] then tells which ones are.
 grass_status check_call(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_t n,
-                        const void* const* p1, const void* const* p2, std::vector<int>* order) {
+                        const void* const* p1, const void* const* p2, std::vector<int>* order,
+                        std::vector<char>* host_p2 = nullptr) {
+  if (host_p2) host_p2->assign(n, 0);
   if (bf16_call != c->bf16)
     return c->fail(GRASS_E_INVALID, c->bf16 ? "bf16 context: use the *_bf16 entry points"
                                             : "fp32 context: the *_bf16 entry points need GRASS_DTYPE_BF16");
@@ -337,6 +342,17 @@ grass_status check_call(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_
         cudaGetLastError();
         return c->fail(GRASS_E_INVALID, "not a CUDA pointer");
       }
+      if (a == p2 && host_p2 && at.type == cudaMemoryTypeHost) {
+        if (c->dp || (c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD))
+          return c->fail(GRASS_E_INVALID, "host gradients need world = 1 and resident or per-step "
+                                          "offloaded optimizer states");
+        (*host_p2)[i] = 1;  // pinned host gradient: streamed through the gradient ring
+        continue;
+      }
+      if (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered)
+        return c->fail(GRASS_E_INVALID, a == p2 && host_p2 && at.type == cudaMemoryTypeUnregistered
+                                            ? "host gradients must be pinned (page-locked) memory"
+                                            : "layer buffers must be device memory on the context's GPU");
       if (!(at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ||
           at.device != c->cfg.device)
         return c->fail(GRASS_E_INVALID, "layer buffers must be device memory on the context's GPU");
@@ -522,8 +538,15 @@ grass_status comm_end(grass_ctx* c, cudaStream_t s) {
 // Launches the update of one range [off, off+n) of layer l whose states live
 // at `state` (already offset to `off`).
 grass_status update_range(grass_ctx* c, int l, const Seg& base, void* param, const void* g, int64_t off,
-                          int64_t n, float* const* state, bool init, int32_t mode, cudaStream_t s) {
+                          int64_t n, float* const* state, bool init, int32_t mode, cudaStream_t s,
+                          const void* g_chunk = nullptr) {
   Seg sg = range_seg(c, l, g, off, n);
+  if (g_chunk) {  // the chunk's gradient was staged in the gradient ring
+    if (c->bf16)
+      sg.g16 = static_cast<const uint16_t*>(g_chunk);
+    else
+      sg.g = static_cast<const float*>(g_chunk);
+  }
   set_update(c, &sg, elem(param, off, c->esz), state, init);
   sg.decay = base.decay;
   sg.step_size = base.step_size;
@@ -543,7 +566,7 @@ grass_status update_range(grass_ctx* c, int l, const Seg& base, void* param, con
 // ~96 % busy, the step is bound by the duplex link itself —
 // profiles/r01_offload_timeline.json.)
 grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, const void* g, bool init,
-                           int32_t mode, cudaStream_t s) {
+                           int32_t mode, cudaStream_t s, bool g_host) {
   const int64_t len = c->shard_len[l];
   const bool overlap = c->cfg.overlap != 0;
   if (overlap && c->layer_done_valid[l])  // previous write-back of this layer
@@ -556,17 +579,20 @@ grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, co
     const size_t bytes = (size_t)n * sizeof(float);
     cudaStream_t sh = overlap ? c->h2d : s, sd = overlap ? c->d2h : s;
     if (overlap && c->slot_used[slot]) CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_free[slot], 0));
+    char* gslot = g_host ? c->d_gring + (size_t)slot * c->chunk * c->esz : nullptr;
     {
       TraceScope ts(c, sh, GRASS_TRACE_H2D, l, off, n);
       for (int a = 0; a < c->ns; ++a)
         if (!(a == 2 && init))  // an uninitialised master is written, not read
           CUDA_TRY(c, cudaMemcpyAsync(ring[a], c->arr[a][l] + off, bytes, cudaMemcpyHostToDevice, sh));
+      if (g_host)
+        CUDA_TRY(c, cudaMemcpyAsync(gslot, elem(g, off, c->esz), (size_t)n * c->esz, cudaMemcpyHostToDevice, sh));
     }
     if (overlap) {
       CUDA_TRY(c, cudaEventRecord(c->ev_h2d[slot], sh));
       CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_h2d[slot], 0));
     }
-    grass_status st = update_range(c, l, base, param, g, off, n, ring, init, mode, s);
+    grass_status st = update_range(c, l, base, param, g, off, n, ring, init, mode, s, gslot);
     if (st != GRASS_OK) return st;
     if (overlap) {
       CUDA_TRY(c, cudaEventRecord(c->ev_comp[slot], s));
@@ -585,6 +611,34 @@ grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, co
   if (overlap) {
     CUDA_TRY(c, cudaEventRecord(c->ev_layer_done[l], c->d2h));
     c->layer_done_valid[l] = 1;
+  }
+  return GRASS_OK;
+}
+
+// Resident states, pinned host gradient: per chunk the gradient is fetched
+// into the gradient ring on h2d while the previous chunk updates (the caller's
+// host gradients reach HBM once, overlapped with the update).
+grass_status stream_grad_layer(grass_ctx* c, int l, const Seg& base, void* param, const void* g_host,
+                               bool init, int32_t mode, cudaStream_t s) {
+  const int64_t len = c->shard_len[l];
+  for (int64_t off = 0; off < len; off += c->chunk) {
+    const int64_t n = std::min(c->chunk, len - off);
+    const int slot = (int)(c->ring_pos++ % c->slots);
+    char* gslot = c->d_gring + (size_t)slot * c->chunk * c->esz;
+    if (c->slot_used[slot]) CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, c->ev_free[slot], 0));
+    {
+      TraceScope ts(c, c->h2d, GRASS_TRACE_H2D, l, off, n);
+      CUDA_TRY(c, cudaMemcpyAsync(gslot, elem(g_host, off, c->esz), (size_t)n * c->esz,
+                                  cudaMemcpyHostToDevice, c->h2d));
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev_h2d[slot], c->h2d));
+    CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_h2d[slot], 0));
+    float* sp[3];
+    for (int a = 0; a < c->ns; ++a) sp[a] = c->arr[a][l] + off;
+    grass_status st = update_range(c, l, base, param, g_host, off, n, sp, init, mode, s, gslot);
+    if (st != GRASS_OK) return st;
+    CUDA_TRY(c, cudaEventRecord(c->ev_free[slot], s));  // the update has consumed the slot
+    c->slot_used[slot] = 1;
   }
   return GRASS_OK;
 }
@@ -796,6 +850,7 @@ void free_ctx(grass_ctx* c) {
   dfree(c->d_gscratch);
   dfree(c->d_coef);
   dfree(c->d_ring);
+  dfree(c->d_gring);
   dfree(c->d_cache);
   if (c->state_block) {
     if (c->cfg.offload)
@@ -900,10 +955,17 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     }
   }
 
+  // chunk ring (offload states, and pinned host gradients in every mode)
+  c->chunk = cfg->chunk_elems ? cfg->chunk_elems : kDefaultChunk;
+  c->chunk = std::min(c->chunk, round_up(c->max_shard, kTile));
+  c->slots = cfg->ring_slots ? cfg->ring_slots : kDefaultSlots;
+  CUDA_TRY(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+  for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free}) {
+    v->assign(c->slots, nullptr);
+    for (auto& e : *v) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  c->slot_used.assign(c->slots, 0);
   if (cfg->offload) {
-    c->chunk = cfg->chunk_elems ? cfg->chunk_elems : kDefaultChunk;
-    c->chunk = std::min(c->chunk, round_up(c->max_shard, kTile));
-    c->slots = cfg->ring_slots ? cfg->ring_slots : kDefaultSlots;
     if (cfg->residency == GRASS_RESIDENCY_PERIOD) {
       c->cache_slots = std::max(cfg->gamma, cfg->cache_layers);
       CUDA_TRY(c, dalloc((void**)&c->d_cache,
@@ -920,13 +982,7 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     } else {
       CUDA_TRY(c, dalloc((void**)&c->d_ring, sizeof(float) * (size_t)c->ns * (size_t)c->chunk * c->slots));
     }
-    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
-    for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free}) {
-      v->assign(c->slots, nullptr);
-      for (auto& e : *v) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    c->slot_used.assign(c->slots, 0);
     c->ev_layer_done.assign(c->nl, nullptr);
     for (auto& e : c->ev_layer_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->layer_done_valid.assign(c->nl, 0);
@@ -1005,8 +1061,17 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   if (!params || !grads) return c->fail(GRASS_E_INVALID, "params/grads is NULL");
   if (!(lr >= 0.0f) || !std::isfinite(lr)) return c->fail(GRASS_E_INVALID, "lr must be finite, >= 0");
   std::vector<int> order;
-  grass_status s = check_call(c, bf16_call, ids, n, reinterpret_cast<const void* const*>(params), grads, &order);
+  std::vector<char> g_host;
+  grass_status s = check_call(c, bf16_call, ids, n, reinterpret_cast<const void* const*>(params), grads, &order,
+                              &g_host);
   if (s != GRASS_OK) return s;
+  const bool any_host = std::find(g_host.begin(), g_host.end(), 1) != g_host.end();
+  if (any_host && c->cfg.max_grad_norm > 0.0)
+    return c->fail(GRASS_E_INVALID, "clipping needs device gradients (pass 1 reads them twice)");
+  if (any_host && !c->d_gring) {  // first host-gradient call: the gradient ring
+    CUDA_TRY(c, cudaMalloc((void**)&c->d_gring, (size_t)c->slots * c->chunk * c->esz));
+    c->dev_bytes += (int64_t)((size_t)c->slots * c->chunk * c->esz);
+  }
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool sharded = c->dp;
@@ -1106,7 +1171,9 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
       c->slot_use[slot] = c->call_seq;
       c->slot_dirty[slot] = 1;
     } else if (c->cfg.offload) {
-      if ((s = offload_layer(c, l, base, param, g, init, mode, st)) != GRASS_OK) return s;
+      if ((s = offload_layer(c, l, base, param, g, init, mode, st, g_host[i] != 0)) != GRASS_OK) return s;
+    } else if (g_host[i]) {
+      if ((s = stream_grad_layer(c, l, base, param, g, init, mode, st)) != GRASS_OK) return s;
     } else {
       float* sp[3];
       for (int a = 0; a < c->ns; ++a) sp[a] = c->arr[a][l];

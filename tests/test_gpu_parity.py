@@ -976,3 +976,49 @@ def test_period_residency_rejects_more_layers_than_slots():
         gr.prefetch_layers([0, 1, 2])
     G.Grass([4096] * 4, gamma=2, offload=True, residency=G.RESIDENCY_PERIOD,
             cache_layers=3).step_layers([0, 1, 2], p[:3], g[:3], 1e-3)   # enough slots: fine
+
+
+# ------------------------------------------ pinned host gradients (e2e path)
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+@pytest.mark.parametrize("offload", [False, True])
+def test_host_gradients_bit_identical(dtype, offload):
+    tdt = torch.bfloat16 if dtype == G.DTYPE_BF16 else torch.float32
+    numel = [4096 * 9 + 8, 65_536, 1000]
+    kw = dict(gamma=2, weight_decay=0.01, param_dtype=dtype, chunk_elems=4096 * 2)
+    if offload:
+        kw.update(offload=True)
+    dev_ctx, host_ctx = G.Grass(numel, **kw), G.Grass(numel, **kw)
+    base = [layer_params(n, l, device=DEV).to(tdt) for l, n in enumerate(numel)]
+    pd, ph = [p.clone() for p in base], [p.clone() for p in base]
+    for step, ids in enumerate([[0, 1], [2, 0], [1, 2]]):
+        grads = [layer_grad(numel[l], l, 1e-3, step=step, device=DEV).to(tdt) for l in ids]
+        hgrads = [g.cpu().pin_memory() for g in grads]
+        dev_ctx.step_layers(ids, [pd[l] for l in ids], grads, 1e-3)
+        host_ctx.trace_enable(True)
+        host_ctx.step_layers(ids, [ph[l] for l in ids], hgrads, 1e-3)
+        tr = host_ctx.trace_read()
+        host_ctx.trace_enable(False)
+        assert [e for e in tr if e["kind"] == "h2d"]          # the gradients came over the link
+        _check_chain(tr)
+    torch.cuda.synchronize()
+    for l in range(3):
+        assert torch.equal(pd[l], ph[l]), l
+        a, b = dev_ctx.read_state(l), host_ctx.read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert dev_ctx.get_mgn()["S"] == host_ctx.get_mgn()["S"]
+
+
+def test_host_gradients_rejected_where_unsupported():
+    n = 4096
+    p = [torch.zeros(n, device=DEV)]
+    hg = [torch.ones(n).pin_memory()]
+    for kw in (dict(force_nccl=True), dict(offload=True, residency=G.RESIDENCY_PERIOD),
+               dict(max_grad_norm=1.0)):
+        with pytest.raises(G.GrassError):
+            G.Grass([n], gamma=1, **kw).step_layers([0], p, hg, 1e-3)
+    import ctypes as C
+    gr = G.Grass([n], gamma=1)
+    pageable = torch.ones(n)                                   # not pinned
+    st = G.binding.lib().grass_step_layers(gr._h, (C.c_int32 * 1)(0), 1, (C.c_void_p * 1)(p[0].data_ptr()),
+                                           (C.c_void_p * 1)(pageable.data_ptr()), C.c_float(1e-3), None)
+    assert st == G.binding.E_INVALID and b"pinned" in G.binding.lib().grass_last_error(gr._h)
