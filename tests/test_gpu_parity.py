@@ -1022,3 +1022,57 @@ def test_host_gradients_rejected_where_unsupported():
     st = G.binding.lib().grass_step_layers(gr._h, (C.c_int32 * 1)(0), 1, (C.c_void_p * 1)(p[0].data_ptr()),
                                            (C.c_void_p * 1)(pageable.data_ptr()), C.c_float(1e-3), None)
     assert st == G.binding.E_INVALID and b"pinned" in G.binding.lib().grass_last_error(gr._h)
+
+
+def test_empty_call_rejected():
+    gr = G.Grass([4096], gamma=1)
+    with pytest.raises(G.GrassError):
+        gr.mgn_accumulate([], [])
+    with pytest.raises(G.GrassError):
+        gr.step_layers([], [], [], 1e-3)
+
+
+def test_gamma_equals_NL_is_plain_adamw_torch_fp32():
+    """gamma = N_L and T_p = 0 (every layer trainable every step)
+    degenerates to plain AdamW: compare with torch.optim.AdamW (fp32, GPU)."""
+    numel = [4096 * 3 + 5, 65_536, 17]
+    lr, wd = 1e-3, 0.01
+    gr = G.Grass(numel, gamma=3, T_p=0, T_s=1, weight_decay=wd)
+    ps = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    tp = [torch.nn.Parameter(p.clone()) for p in ps]
+    opt = torch.optim.AdamW(tp, lr=lr, weight_decay=wd, foreach=False)
+    for step in range(20):
+        grads = [layer_grad(n, l, 1e-3, step=step, device=DEV) for l, n in enumerate(numel)]
+        gr.step_layers([0, 1, 2], ps, grads, lr)
+        for t, g in zip(tp, grads):
+            t.grad = g.clone()
+        opt.step()
+    torch.cuda.synchronize()
+    for p, t in zip(ps, tp):
+        d = (p - t.detach()).abs()
+        assert float(d.max()) <= 1e-5 * float(t.detach().abs().max()), float(d.max())
+
+
+def test_layer_beyond_2pow31_elements():
+    """64-bit element indexing end to end: a layer of 2^31 + 4099 elements
+    (8.6 GB per fp32 buffer) — norm vs the oracle, AdamW on sampled elements
+    on both sides of the 2^31 boundary."""
+    n = (1 << 31) + 4099
+    gr = G.Grass([n], gamma=1, weight_decay=0.01)
+    p = layer_params(n, 0, device=DEV)
+    g = layer_grad(n, 0, 1e-3, device=DEV)
+    idx = np.concatenate([np.arange(8), (1 << 31) - 8 + np.arange(16), n - 8 + np.arange(8),
+                          np.random.default_rng(0).integers(0, n, 50_000)])
+    idx = np.unique(idx)
+    ti = torch.from_numpy(idx).to(DEV)
+    th_in, g_s = _np(p[ti]), _np(g[ti])
+    gr.step_layers([0], [p], [g], 1e-3)
+    ss = gr.get_mgn()["last_ss"][0]
+    gh = _np(g)
+    del g
+    assert_ss_close(ss, O.sq_norm(gh))
+    del gh
+    m, v, t = gr.read_state(0)
+    th_o, m_o, v_o = O.adamw_step(th_in, np.zeros_like(th_in), np.zeros_like(th_in), g_s, 1,
+                                  float(np.float32(1e-3)), weight_decay=0.01)
+    assert_state_close(_np(p[ti]), m[idx], v[idx], th_o, m_o, v_o, th_in, np.zeros_like(th_in), g_s)
