@@ -320,9 +320,16 @@ def run_grass(args, rank, world, local):
         ksteps = max(3, min(args.steps, 10))
         def host_step(step):
             nonlocal ids
-            # the public call with the step's gradients in pinned HOST memory: the
-            # library streams them chunk-wise into HBM, overlapped with the update
-            ctx.step_layers(ids, [params[l] for l in ids], host_g[:len(ids)], args.lr, stream=s)
+            if world == 1:
+                # the public call with the step's gradients in pinned HOST memory: the
+                # library streams them chunk-wise into HBM, overlapped with the update
+                ctx.step_layers(ids, [params[l] for l in ids], host_g[:len(ids)], args.lr, stream=s)
+            else:
+                # the DP path reduce-scatters device buffers: stage the host gradients first
+                with torch.cuda.stream(s):
+                    for j, l in enumerate(ids):
+                        grads[l].copy_(host_g[j], non_blocking=True)
+                ctx.step_layers(ids, [params[l] for l in ids], [grads[l] for l in ids], args.lr, stream=s)
             ctx.update_probs()                  # reads S, c back (d2h)
             ids = ctx.sample_layers(step + 1)
         e0.record(s)
