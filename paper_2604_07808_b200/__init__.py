@@ -10,7 +10,9 @@ from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_CONTINUE, DECIDE_PROBE, DEC
                       schedule_decision, shard_range, softmax_probs, splitmix64, tile_elems,
                       uniform)
 
-__all__ = ["Grass", "GrassError", "lib", "exported_symbols", "nccl_unique_id",
+from .schedule import GrassSchedule  # noqa: E402
+
+__all__ = ["Grass", "GrassSchedule", "GrassError", "lib", "exported_symbols", "nccl_unique_id",
            "sample_from_probs", "schedule_decision", "shard_range", "softmax_probs",
            "splitmix64", "tile_elems", "uniform", "POLICY_ADAPTIVE", "POLICY_STATIC",
            "POLICY_UNIFORM", "DECIDE_PROBE", "DECIDE_COMMIT_RESAMPLE", "DECIDE_RESAMPLE",

@@ -1,0 +1,71 @@
+"""GrassSchedule — drives one Grass context through the paper's schedule
+(SURVEY.md §1 layer L5):
+
+  steps [0, T_p)        probing: every layer produces gradients, their norms
+                        feed the MGN window (grass_mgn_accumulate), no update;
+  step T_p, then every  commit the window (first commit / Eq. 4 EMA), Eq. 3
+  T_u (multiple of T_s) probabilities (grass_update_probs);
+  step T_p + k*T_s      resample the trainable set (grass_sample_layers) and,
+                        with period residency, prefetch its optimizer states
+                        (grass_prefetch_layers) so they move during fwd/bwd;
+  other steps           keep the set; update it (grass_step_layers).
+
+Host logic only: every step of the hot path runs in libgrass.so.
+
+    sched = GrassSchedule(grass)
+    for step in range(n_steps):
+        layers = sched.begin_step(step)      # which layers need gradients
+        ... forward / backward producing gradients of `layers` ...
+        sched.end_step(step, params, grads, lr)
+"""
+from __future__ import annotations
+
+from typing import Sequence
+
+from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_PROBE, DECIDE_RESAMPLE, Grass,
+                      schedule_decision)
+
+
+class GrassSchedule:
+    def __init__(self, grass: Grass, prefetch: bool | None = None):
+        self.g = grass
+        cfg = grass.cfg
+        self.T_p, self.T_s, self.T_u = cfg.T_p, cfg.T_s, cfg.T_u
+        self.n_layers = grass.n_layers
+        # prefetch only makes sense with period residency
+        period = bool(cfg.offload) and cfg.residency == 1
+        self.prefetch = period if prefetch is None else (prefetch and period)
+        self.trainable: list[int] = []
+        self.probs: list[float] | None = None
+        self.period_index = -1
+
+    def decision(self, step: int) -> int:
+        return schedule_decision(step, self.T_p, self.T_s, self.T_u)
+
+    def begin_step(self, step: int, stream=None) -> list[int]:
+        """Layers that must produce gradients this step (all of them while
+        probing).  At period boundaries commits / resamples / prefetches."""
+        d = self.decision(step)
+        if d == DECIDE_PROBE:
+            return list(range(self.n_layers))
+        if d == DECIDE_COMMIT_RESAMPLE:
+            self.probs = self.g.update_probs()
+        if d in (DECIDE_COMMIT_RESAMPLE, DECIDE_RESAMPLE) or not self.trainable:
+            self.period_index = (step - self.T_p) // self.T_s
+            self.trainable = self.g.sample_layers(self.period_index)
+            if self.prefetch:
+                self.g.prefetch_layers(self.trainable, stream=stream)
+        return list(self.trainable)
+
+    def end_step(self, step: int, params: Sequence, grads: Sequence, lr: float, stream=None):
+        """params / grads: one entry per layer of begin_step(step), same order."""
+        layers = (list(range(self.n_layers)) if self.decision(step) == DECIDE_PROBE
+                  else self.trainable)
+        if len(grads) != len(layers):
+            raise ValueError("one gradient per layer returned by begin_step")
+        if self.decision(step) == DECIDE_PROBE:
+            self.g.mgn_accumulate(layers, grads, stream=stream)   # no update
+        else:
+            if len(params) != len(layers):
+                raise ValueError("one parameter buffer per trainable layer")
+            self.g.step_layers(layers, params, grads, lr, stream=stream)

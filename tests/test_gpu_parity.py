@@ -1076,3 +1076,27 @@ def test_layer_beyond_2pow31_elements():
     th_o, m_o, v_o = O.adamw_step(th_in, np.zeros_like(th_in), np.zeros_like(th_in), g_s, 1,
                                   float(np.float32(1e-3)), weight_decay=0.01)
     assert_state_close(_np(p[ti]), m[idx], v[idx], th_o, m_o, v_o, th_in, np.zeros_like(th_in), g_s)
+
+
+def test_schedule_driver_end_to_end_vs_oracle():
+    """GrassSchedule over T_p = 2 probing steps and 3 periods of T_s = 2 on the
+    tiny config: trainable sets and MGN equal the oracle run by hand."""
+    numel = [65_536] * 4
+    gr = G.Grass(numel, gamma=2, T_p=2, T_s=2, T_u=2, seed=77)
+    sched = G.GrassSchedule(gr)
+    orc = O.GrassOracle(numel, gamma=2, seed=77)
+    sig = grad_sigmas(4, 9)
+    params = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    for step in range(8):
+        layers = sched.begin_step(step)
+        d = O.schedule_decision(step, 2, 2)
+        if "commit" in d:
+            orc.update_probs()
+        if "resample" in d:
+            assert layers == O.sample_layers(sched.probs, 2, 77, (step - 2) // 2)
+        grads = [layer_grad(65_536, l, sig[l], step=step, device=DEV) for l in layers]
+        sched.end_step(step, [params[l] for l in layers], grads, 1e-3)
+        orc.accumulate(layers, [_np(g) for g in grads])     # probing and trainable norms alike
+    st = gr.get_mgn()
+    assert st["m"] == pytest.approx(orc.mgn.m, rel=1e-7)
+    assert st["S"] == pytest.approx(orc.mgn.S, rel=1e-7)
