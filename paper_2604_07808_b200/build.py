@@ -57,7 +57,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str | Non
     deps = [os.path.join(CSRC, f) for f in srcs] + [os.path.join(ROOT, "include", "grass.h"), __file__]
     if not force and os.path.exists(out_path) and os.path.getmtime(out_path) >= max(os.path.getmtime(d) for d in deps):
         return out_path
-    build_dir = BUILD if out is None else BUILD + "_" + os.path.basename(out_path).replace(".so", "")
+    build_dir = BUILD if out is None else os.path.join(BUILD, "variant_" + os.path.basename(out_path).replace(".so", ""))
     os.makedirs(build_dir, exist_ok=True)
     dflags = ["-D" + d for d in defines]
     inc = ["-I" + os.path.join(ROOT, "include"), "-I" + _nccl_include(), "-I" + os.path.join(cuda, "include")]
