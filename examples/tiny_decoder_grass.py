@@ -1,0 +1,112 @@
+"""Training a tiny decoder-only transformer with GRASS through libgrass.
+
+What the caller does (the library's boundary, include/grass.h):
+  * each decoder block's parameters live in ONE flat fp32 buffer (the
+    parameters are views into it), and so do their gradients;
+  * the schedule (GrassSchedule) says which blocks need gradients; the other
+    blocks are frozen (requires_grad False);
+  * after backward, the flat gradient buffers go to the library: probing
+    steps only record the Eq. 2 norms, later steps run the fused norm + AdamW
+    of the trainable blocks (optimizer states offloaded to pinned host memory
+    with period residency);
+  * embeddings and the output head are always trainable (LISA convention) and
+    use torch's AdamW.
+
+    python examples/tiny_decoder_grass.py
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import torch
+import torch.nn as nn
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_07808_b200 as G  # noqa: E402
+
+
+class Block(nn.Module):
+    def __init__(self, d, heads):
+        super().__init__()
+        self.n1 = nn.LayerNorm(d)
+        self.attn = nn.MultiheadAttention(d, heads, batch_first=True)
+        self.n2 = nn.LayerNorm(d)
+        self.mlp = nn.Sequential(nn.Linear(d, 4 * d), nn.GELU(), nn.Linear(4 * d, d))
+
+    def forward(self, x, mask):
+        h = self.n1(x)
+        x = x + self.attn(h, h, h, attn_mask=mask, need_weights=False)[0]
+        return x + self.mlp(self.n2(x))
+
+
+class TinyDecoder(nn.Module):
+    def __init__(self, vocab=256, d=128, heads=4, layers=6, ctx=64):
+        super().__init__()
+        self.emb = nn.Embedding(vocab, d)
+        self.pos = nn.Parameter(torch.zeros(ctx, d))
+        self.blocks = nn.ModuleList(Block(d, heads) for _ in range(layers))
+        self.head = nn.Linear(d, vocab)
+
+    def forward(self, idx):
+        t = idx.shape[1]
+        mask = torch.triu(torch.full((t, t), float("-inf"), device=idx.device), 1)
+        x = self.emb(idx) + self.pos[:t]
+        for b in self.blocks:
+            x = b(x, mask)
+        return self.head(x)
+
+
+def flatten_block(block: nn.Module):
+    """Re-home a block's parameters and gradients into two flat fp32 buffers."""
+    params = list(block.parameters())
+    n = sum(p.numel() for p in params)
+    flat = torch.empty(n, device=params[0].device)
+    gflat = torch.zeros(n, device=params[0].device)
+    off = 0
+    for p in params:
+        k = p.numel()
+        flat[off:off + k].copy_(p.data.view(-1))
+        p.data = flat[off:off + k].view_as(p)
+        p.grad = gflat[off:off + k].view_as(p)   # autograd accumulates into it
+        off += k
+    return flat, gflat
+
+
+def train(steps=60, T_p=5, T_s=5, gamma=2, seed=0, device="cuda", log=True):
+    torch.manual_seed(seed)
+    model = TinyDecoder().to(device)
+    flats = [flatten_block(b) for b in model.blocks]
+    gr = G.Grass([f.numel() for f, _ in flats], gamma=gamma, T_p=T_p, T_s=T_s, seed=seed,
+                 offload=True, residency=G.RESIDENCY_PERIOD)
+    sched = G.GrassSchedule(gr)
+    outer = [model.emb.weight, model.pos, *model.head.parameters()]
+    opt = torch.optim.AdamW(outer, lr=1e-3)
+    # a learnable synthetic task: predict the next token of a fixed random walk
+    data = torch.cumsum(torch.randint(-2, 3, (64, 65), generator=torch.Generator().manual_seed(seed)), 1) % 256
+    data = data.to(device)
+    losses = []
+    for step in range(steps):
+        layers = set(sched.begin_step(step))
+        for l, b in enumerate(model.blocks):
+            for p in b.parameters():
+                p.requires_grad_(l in layers)
+        logits = model(data[:, :-1])
+        loss = nn.functional.cross_entropy(logits.reshape(-1, 256), data[:, 1:].reshape(-1))
+        loss.backward()
+        ids = sorted(layers)
+        sched.end_step(step, [flats[l][0] for l in ids], [flats[l][1] for l in ids], lr=1e-3)
+        if step >= T_p:                 # probing omits every parameter update
+            opt.step()
+        opt.zero_grad(set_to_none=False)
+        for _, g in flats:
+            g.zero_()
+        losses.append(float(loss.detach()))
+        if log and step % 10 == 0:
+            print(f"step {step:3d} loss {losses[-1]:.4f} trainable {ids if len(ids) < 6 else 'all (probe)'}")
+    gr.sync()
+    return losses
+
+
+if __name__ == "__main__":
+    train()
