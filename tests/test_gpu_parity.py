@@ -879,6 +879,11 @@ def test_fuzz_dtypes_clip_checkpoint(seed, tmp_path):
     for step in range(8):
         ids = [int(x) for x in rng.choice(nl, size=int(rng.integers(1, gamma + 1)), replace=False)]
         grads = [layer_grad(numel[l], l, 1e-2, step=step, seed=seed, device=DEV).to(tdt) for l in ids]
+        r = rng.random()
+        if r < 0.3:     # prefetch exactly the next set
+            ctxs[2].prefetch_layers(ids)
+        elif r < 0.5:   # prefetch a different set (evicted or reused before use)
+            ctxs[2].prefetch_layers([int(x) for x in rng.choice(nl, size=min(gamma, nl), replace=False)])
         for gr, p in zip(ctxs, ps):
             gr.step_layers(ids, [p[l] for l in ids], grads, 1e-3)
         if step == 4:   # checkpoint the offload context, restore into a fresh period context
