@@ -22,7 +22,7 @@
 //
 // Compile-time A/B knobs (tools/variants.py; defaults are the measured best):
 // GRASS_IEEE_MATH, GRASS_K2_STG_STORE, GRASS_K2_LOAD_EF, GRASS_K2_STORE_EF,
-// GRASS_UPD_STAGES, GRASS_NORM_TPS, GRASS_NORM_STAGES.
+// GRASS_K2_SEP_OUT, GRASS_UPD_STAGES, GRASS_NORM_TPS, GRASS_NORM_STAGES.
 //
 // The tile partial (grass_internal.h) is a FIXED function of the tile's data:
 // consumer thread t owns elements (q*kThreads + t)*4 + j, j = 0..3, q = 0..
@@ -220,6 +220,14 @@ __device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, 
 constexpr bool kTmaStore = false;
 #else
 constexpr bool kTmaStore = true;
+#endif
+// GRASS_K2_SEP_OUT: results go to a separate output region of the stage, so
+// the producer can refill the input region while the previous unit's bulk
+// stores are still reading shared memory (A/B knob).
+#ifdef GRASS_K2_SEP_OUT
+constexpr bool kSepOut = kTmaStore;
+#else
+constexpr bool kSepOut = false;
 #endif
 
 // The branch-free full-unit path (inside the kernel) is used for the

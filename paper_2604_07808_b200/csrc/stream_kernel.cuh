@@ -29,8 +29,17 @@ struct StageLayout {
   static constexpr int off_t = kUnit * GB;
   static constexpr int off_m = off_t + kUnit * 4;
   static constexpr int off_v = off_m + kUnit * 4;
-  static constexpr int off_tb = off_v + kUnit * 4;
-  static constexpr int bytes = UPDATE ? off_tb + (BF16 ? kUnit * 2 : 0) : kUnit * GB;
+  static constexpr bool SEP = UPDATE && kSepOut;
+  // in place: the bf16 parameters (read when the master is initialised, and
+  // written) get their own slot; separate output: the bf16 input is read from
+  // the (then unused) fp32 theta slot and the outputs follow the inputs
+  static constexpr int off_tb = SEP ? off_t : off_v + kUnit * 4;  // bf16 theta input
+  static constexpr int in_bytes = UPDATE ? off_v + kUnit * 4 + ((BF16 && !SEP) ? kUnit * 2 : 0) : kUnit * GB;
+  static constexpr int o_t = SEP ? in_bytes : off_t;  // outputs theta', m', v', bf16 theta'
+  static constexpr int o_m = SEP ? o_t + kUnit * 4 : off_m;
+  static constexpr int o_v = SEP ? o_m + kUnit * 4 : off_v;
+  static constexpr int o_tb = SEP ? o_v + kUnit * 4 : off_tb;
+  static constexpr int bytes = SEP ? o_tb + (BF16 ? kUnit * 2 : 0) : in_bytes;
   static constexpr int vec = BF16 ? 8 : 4;
 };
 
@@ -63,10 +72,10 @@ __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
 template <bool BF16, class L>
 __device__ __forceinline__ void store_unit_t(const Seg& sg, int64_t e0, uint32_t nv, const char* stg) {
   if (nv) {
-    bulk_store(sg.theta + e0, stg + L::off_t, nv * 4u);
-    bulk_store(sg.m + e0, stg + L::off_m, nv * 4u);
-    bulk_store(sg.v + e0, stg + L::off_v, nv * 4u);
-    if (BF16) bulk_store(sg.theta16 + e0, stg + L::off_tb, nv * 2u);
+    bulk_store(sg.theta + e0, stg + L::o_t, nv * 4u);
+    bulk_store(sg.m + e0, stg + L::o_m, nv * 4u);
+    bulk_store(sg.v + e0, stg + L::o_v, nv * 4u);
+    if (BF16) bulk_store(sg.theta16 + e0, stg + L::o_tb, nv * 2u);
     bulk_commit();
   }
 }
@@ -79,6 +88,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   extern __shared__ __align__(1024) char sbuf[];  // [STAGES][L::bytes]
   __shared__ __align__(8) uint64_t full_bar[STAGES];
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t outfree_bar[STAGES];  // L::SEP: output region writable
   __shared__ int unit_prefix[kMaxSeg + 1];
   __shared__ int seg_done[kMaxSeg];
   __shared__ double red[2][TPS][kConsumerWarps];
@@ -96,6 +106,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], kConsumerWarps);
+      mbar_init(&outfree_bar[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -119,7 +130,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
           if (TS) {
             store_unit_t<BF16, L>(b.seg[pend_s[stage]], pend_e0[stage], pend_nv[stage], stg);
-            bulk_wait_read_all();  // stage readable again
+            if (!L::SEP) bulk_wait_read_all();  // stage reusable again
           }
         }
         while (u >= unit_prefix[s + 1]) ++s;
@@ -148,6 +159,10 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           }
         } else {
           mbar_arrive(&full_bar[stage]);
+        }
+        if (L::SEP) {  // loads are in flight; now let the stores of unit i - STAGES finish reading
+          if (i >= STAGES) bulk_wait_read_all();
+          mbar_arrive(&outfree_bar[stage]);
         }
       }
       if (TS) {  // drain: results of the last (up to STAGES) units
@@ -184,6 +199,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
     char* stg = sbuf + (size_t)stage * L::bytes;
     mbar_wait(&full_bar[stage], (i / STAGES) & 1);
+    if (L::SEP) mbar_wait(&outfree_bar[stage], (i / STAGES) & 1);
     if (!UPDATE && ne == kUnit) {
       // Full unit of the norm-only stream: branch-free, every shared-memory
       // read issued before the math.  Same element map and accumulation order
@@ -240,10 +256,10 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
                 adamw1(g4.z, t4.z, m4.z, v4.z, sc);
                 adamw1(g4.w, t4.w, m4.w, v4.w, sc);
                 if (kTmaStore) {  // results back into the stage; the producer bulk-stores them
-                  *reinterpret_cast<float4*>(stg + L::off_t + 4 * e) = t4;
-                  *reinterpret_cast<float4*>(stg + L::off_m + 4 * e) = m4;
-                  *reinterpret_cast<float4*>(stg + L::off_v + 4 * e) = v4;
-                  if (BF16) *reinterpret_cast<uint2*>(stg + L::off_tb + 2 * e) = pack_bf16x4(t4);
+                  *reinterpret_cast<float4*>(stg + L::o_t + 4 * e) = t4;
+                  *reinterpret_cast<float4*>(stg + L::o_m + 4 * e) = m4;
+                  *reinterpret_cast<float4*>(stg + L::o_v + 4 * e) = v4;
+                  if (BF16) *reinterpret_cast<uint2*>(stg + L::o_tb + 2 * e) = pack_bf16x4(t4);
                 } else {
                   st_stream(sg.theta + e0 + e, t4);
                   st_stream(sg.m + e0 + e, m4);

@@ -12,11 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "store_ef": ["GRASS_K2_STORE_EF"],
-    "load_ef": ["GRASS_K2_LOAD_EF"],
-    "load_ef_store_ef": ["GRASS_K2_LOAD_EF", "GRASS_K2_STORE_EF"],
-    "stg": ["GRASS_K2_STG_STORE"],
+    "sep_out": ["GRASS_K2_SEP_OUT"],
     "base_again": [],
+    "sep_out_again": ["GRASS_K2_SEP_OUT"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
@@ -29,7 +27,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main,probe", extra=()):
+def run(legs="main,probe,bf16", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
@@ -39,7 +37,8 @@ def run(legs="main,probe", extra=()):
             d = json.loads(r.stdout.strip().splitlines()[-1])
             res[name] = {"kernel_ms": d["roofline"]["kernel_ms"], "frac": d["roofline"]["frac"],
                          "step_ms": d["ms_per_step"],
-                         "probe_GBps": (d.get("probe") or {}).get("GBps")}
+                         "probe_GBps": (d.get("probe") or {}).get("GBps"),
+                         "bf16_kernel_ms": (d.get("bf16") or {}).get("kernel_ms")}
         except Exception:
             res[name] = {"error": r.stderr[-2000:]}
         print(name, res[name], flush=True)
