@@ -9,8 +9,10 @@ What the caller does (the library's boundary, include/grass.h):
     steps only record the Eq. 2 norms, later steps run the fused norm + AdamW
     of the trainable blocks (optimizer states offloaded to pinned host memory
     with period residency);
-  * embeddings and the output head are always trainable (LISA convention) and
-    use torch's AdamW.
+  * the embeddings and the output head are always trainable (LISA convention,
+    SPEC.md:145): one more flat buffer, registered as an always-active group
+    (n_always = 1, DESIGN R19) — never sampled, updated by the same fused
+    kernel every adaptive step, its m/v kept in HBM.
 
     python examples/tiny_decoder_grass.py
 """
@@ -57,9 +59,9 @@ class TinyDecoder(nn.Module):
         return self.head(x)
 
 
-def flatten_block(block: nn.Module):
-    """Re-home a block's parameters and gradients into two flat fp32 buffers."""
-    params = list(block.parameters())
+def flatten_params(params):
+    """Re-home parameters and their gradients into two flat fp32 buffers."""
+    params = list(params)
     n = sum(p.numel() for p in params)
     flat = torch.empty(n, device=params[0].device)
     gflat = torch.zeros(n, device=params[0].device)
@@ -76,34 +78,32 @@ def flatten_block(block: nn.Module):
 def train(steps=60, T_p=5, T_s=5, gamma=2, seed=0, device="cuda", log=True):
     torch.manual_seed(seed)
     model = TinyDecoder().to(device)
-    flats = [flatten_block(b) for b in model.blocks]
-    gr = G.Grass([f.numel() for f, _ in flats], gamma=gamma, T_p=T_p, T_s=T_s, seed=seed,
-                 offload=True, residency=G.RESIDENCY_PERIOD)
-    sched = G.GrassSchedule(gr)
+    flats = [flatten_params(b.parameters()) for b in model.blocks]
     outer = [model.emb.weight, model.pos, *model.head.parameters()]
-    opt = torch.optim.AdamW(outer, lr=1e-3)
+    flats.append(flatten_params(outer))           # always-active group: id len(blocks)
+    gr = G.Grass([f.numel() for f, _ in flats], gamma=gamma, T_p=T_p, T_s=T_s, seed=seed,
+                 offload=True, residency=G.RESIDENCY_PERIOD, n_always=1)
+    sched = G.GrassSchedule(gr)
     # a learnable synthetic task: predict the next token of a fixed random walk
     data = torch.cumsum(torch.randint(-2, 3, (64, 65), generator=torch.Generator().manual_seed(seed)), 1) % 256
     data = data.to(device)
     losses = []
     for step in range(steps):
-        layers = set(sched.begin_step(step))
+        ids = sched.begin_step(step)   # end_step takes the buffers in THIS order
+        layers = set(ids)
         for l, b in enumerate(model.blocks):
             for p in b.parameters():
                 p.requires_grad_(l in layers)
         logits = model(data[:, :-1])
         loss = nn.functional.cross_entropy(logits.reshape(-1, 256), data[:, 1:].reshape(-1))
         loss.backward()
-        ids = sorted(layers)
+        # probing steps only record norms: no parameter update
         sched.end_step(step, [flats[l][0] for l in ids], [flats[l][1] for l in ids], lr=1e-3)
-        if step >= T_p:                 # probing omits every parameter update
-            opt.step()
-        opt.zero_grad(set_to_none=False)
         for _, g in flats:
             g.zero_()
         losses.append(float(loss.detach()))
         if log and step % 10 == 0:
-            print(f"step {step:3d} loss {losses[-1]:.4f} trainable {ids if len(ids) < 6 else 'all (probe)'}")
+            print(f"step {step:3d} loss {losses[-1]:.4f} trainable {ids if step >= T_p else 'none (probe)'}")
     gr.sync()
     return losses
 

@@ -84,8 +84,8 @@ typedef enum {
 } grass_decision;
 
 typedef struct grass_config {
-  int32_t n_layers;            /* N_L >= 1 */
-  const int64_t* layer_numel;  /* host [N_L]; N_p(l) >= 1, true counts (R10); copied */
+  int32_t n_layers;            /* N_L sampled layers + n_always groups (below), >= 1 */
+  const int64_t* layer_numel;  /* host [n_layers]; N_p(l) >= 1, true counts (R10); copied */
   int32_t gamma;               /* active layers per period, 1 <= gamma <= N_L */
   int32_t T_p, T_s, T_u;       /* schedule; T_u multiple of T_s (R11) */
   double tau;                  /* Eq. 3 temperature > 0 (R3, default 1.0) */
@@ -116,12 +116,22 @@ typedef struct grass_config {
                                   global norm, coef = min(1, max/(||g||+1e-6)) (torch
                                   clip_grad_norm_; paper silent; DESIGN R17).
                                   Two passes (norm, then update: 32 B/param); the MGN
-                                  still sees the raw norm (R9).  0 = off (default). */
+                                  still sees the raw norm (R9).  0 = off (default).  On the
+                                  NCCL path one call may then list at most gamma + n_always
+                                  layers (their averaged shards live between the passes). */
   int32_t param_dtype;         /* GRASS_DTYPE_FP32: fp32 params/grads (grass_step_layers);
                                   GRASS_DTYPE_BF16: bf16 params/grads, the context keeps an
                                   fp32 master copy next to m, v (grass_step_layers_bf16;
                                   SURVEY 8(f) f3, DESIGN R18). world > 1 then needs every
                                   N_p divisible by 8*world. */
+  int32_t n_always;            /* always-active groups (DESIGN R19): the LAST
+                                  n_always entries of layer_numel (embedding, final norm,
+                                  output head — the LISA convention) are never
+                                  sampled and are updated by every grass_step_layers call that
+                                  lists them; their m/v stay in HBM in every mode.
+                                  The sampled layers are ids [0, N_L) with N_L = n_layers -
+                                  n_always; gamma, cache_layers, probabilities and the commit
+                                  refer to those only.  0 = none (default). */
 } grass_config;
 
 typedef enum {
@@ -161,7 +171,8 @@ grass_status grass_sync(grass_ctx* ctx);
  * ss_l = sum_i g_i^2 accumulated in fp64 over a FIXED tile decomposition
  * (bit-reproducible, independent of grid size), r_l = sqrt(ss_l / N_p(l)),
  * window S_l += r_l, c_l += 1.  No optimizer state is read or written (R14).
- *   layer_ids: host [n] distinct ids in [0, N_L).
+ *   layer_ids: host [n] distinct ids in [0, n_layers) (sampled layers and
+ *              always-active groups alike).
  *   grads:     host [n] array of DEVICE pointers, grads[i] = N_p(layer_ids[i])
  *              fp32, 16-byte aligned.  World > 1: this rank's local gradient;
  *              the norm is of the DP average (R9).
@@ -174,7 +185,7 @@ grass_status grass_mgn_accumulate(grass_ctx* ctx, const int32_t* layer_ids, int3
  * (frozen) layers keep m_l (Eq. 4); window reset; then Eq. 3
  * p = softmax(m~/tau) (R3) according to cfg.policy.  Synchronises once (waits
  * for the accumulations in flight and reads N_L * 16 bytes).
- *   probs_out: host [N_L] or NULL.
+ *   probs_out: host [n_layers] or NULL (p = 0 for always-active groups).
  * Errors: GRASS_E_STATE if no layer was observed in the window,
  * GRASS_E_NONFINITE. */
 grass_status grass_update_probs(grass_ctx* ctx, double* probs_out);
@@ -183,7 +194,8 @@ grass_status grass_update_probs(grass_ctx* ctx, double* probs_out);
  * proportional to p with renormalisation (R6), with the counter-based
  * SplitMix64 RNG keyed by (cfg.seed, period, draw index) (R7).  Pure host;
  * bit-exact contract.  ids_out in DRAW order.
- *   probs: host [N_L] or NULL (= the context's current probabilities).
+ *   probs: host [n_layers] (only the first N_L entries are read) or NULL (= the
+ *          context's current probabilities).  Ids are in [0, N_L).
  *   ids_out: host [gamma]. */
 grass_status grass_sample_layers(grass_ctx* ctx, const double* probs, uint64_t period,
                                  int32_t* ids_out);
@@ -300,7 +312,8 @@ grass_status grass_trace_enable(grass_ctx* ctx, int32_t on);
  * events available (may exceed capacity; the rest are dropped). */
 grass_status grass_trace_read(grass_ctx* ctx, grass_trace_event* out, int32_t capacity, int32_t* count);
 
-/* Introspection of the MGN state (host arrays [N_L], any may be NULL):
+/* Introspection of the MGN state (host arrays [n_layers], any may be NULL;
+ * always-active groups have m = p = 0 but real S, c, last norm):
  * committed m_l, window sum S_l, window count c_l, last fp64 squared norm of
  * layer l (DP-averaged gradient when world > 1), current probabilities.
  * Synchronises the context first. */

@@ -38,6 +38,9 @@ fixtures in ``tests/golden/``.  Parity status per function:
   clip_coefficient (R17) ........ pinned (torch.nn.utils.clip_grad_norm_)
   bf16_to_f32 / f32_to_bf16 ..... pinned (torch bfloat16 conversions, RNE)
   adamw_step_bf16 (R18) ......... pinned (torch.optim.AdamW on an fp32 master)
+  GrassOracle n_always (R19) .... pinned (torch.optim.AdamW over every tensor at
+                                  gamma = N_L; MGN / p / sampler equal a run without
+                                  the groups)
   Paper-level choices of tau, alpha, the RNG and the draw scheme: **parity
   unpinned** against the paper itself (the paper gives no values); they are
   pinned only against our stated readings (R3, R5, R6, R7).
@@ -353,18 +356,25 @@ class GrassOracle:
     """The whole hot path: probing accumulation, commit/EMA, softmax, sampling,
     AdamW on the active layers with per-layer step counters t_l (reading R2),
     and MGN accumulation of the active layers' norms.  Optimizer state is kept
-    for every layer and never reset."""
+    for every layer and never reset.
+
+    n_always (reading R19): the last n_always entries of
+    layer_numel are always-trainable groups (embedding, head) -- excluded from
+    the MGN window, the probabilities and the sampler; updated like any layer
+    when listed."""
 
     def __init__(self, layer_numel, gamma, tau=1.0, alpha=0.5, normalize=True,
-                 beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, seed=0):
+                 beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, seed=0, n_always=0):
         self.numel = list(layer_numel)
         self.n = len(self.numel)
+        self.n_s = self.n - n_always          # sampled layers [0, n_s)
+        assert 1 <= self.n_s and 1 <= gamma <= self.n_s
         self.gamma = gamma
         self.tau, self.alpha, self.normalize = tau, alpha, normalize
         self.beta1, self.beta2, self.eps, self.wd = beta1, beta2, eps, weight_decay
         self.seed = seed
-        self.mgn = MgnState(self.n)
-        self.probs = [1.0 / self.n] * self.n
+        self.mgn = MgnState(self.n_s)
+        self.probs = [1.0 / self.n_s] * self.n_s + [0.0] * (self.n - self.n_s)
         self.m = [np.zeros(k, np.float32) for k in self.numel]
         self.v = [np.zeros(k, np.float32) for k in self.numel]
         self.t = [0] * self.n
@@ -375,16 +385,17 @@ class GrassOracle:
         for l, g in zip(layer_ids, grads):
             ss = sq_norm(g)
             self.last_ss[l] = ss
-            self.mgn.record(l, rms_norm(ss, self.numel[l]))
+            if l < self.n_s:                  # always-active groups are not sampled (R19)
+                self.mgn.record(l, rms_norm(ss, self.numel[l]))
 
     def update_probs(self):
         m = self.mgn.commit(self.alpha)
-        self.probs = softmax_probs(m, self.tau, self.normalize)
+        self.probs = list(softmax_probs(m, self.tau, self.normalize)) + [0.0] * (self.n - self.n_s)
         return list(self.probs)
 
     def sample(self, period, probs=None):
-        return sample_layers(self.probs if probs is None else probs, self.gamma,
-                             self.seed, period)
+        p = self.probs if probs is None else probs
+        return sample_layers(list(p)[:self.n_s], self.gamma, self.seed, period)
 
     def step_layers(self, layer_ids, params, grads, lr, max_grad_norm=None):
         """AdamW on each listed layer (ascending id, reading R12) and MGN

@@ -52,7 +52,7 @@ class GrassConfig(C.Structure):
         ("offload", C.c_int32), ("overlap", C.c_int32), ("chunk_elems", C.c_int64),
         ("ring_slots", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("residency", C.c_int32), ("cache_layers", C.c_int32),
-        ("max_grad_norm", C.c_double), ("param_dtype", C.c_int32),
+        ("max_grad_norm", C.c_double), ("param_dtype", C.c_int32), ("n_always", C.c_int32),
     ]
 
 
@@ -216,11 +216,16 @@ class Grass:
                  seed: int = 1234, device: int = 0, offload: bool = False, overlap: bool = True,
                  chunk_elems: int = 0, ring_slots: int = 0, rank: int = 0, world: int = 1,
                  process_group=None, force_nccl: bool = False, residency: int = RESIDENCY_STEP,
-                 cache_layers: int = 0, max_grad_norm: float = 0.0, param_dtype: int = DTYPE_FP32):
+                 cache_layers: int = 0, max_grad_norm: float = 0.0, param_dtype: int = DTYPE_FP32,
+                 n_always: int = 0):
         L = lib()
         self.layer_numel = [int(x) for x in layer_numel]
         self.n_layers = len(self.layer_numel)
         self.gamma = gamma
+        # the last n_always entries are always-active groups (embedding, head; R19)
+        self.n_always = int(n_always)
+        self.n_sampled = self.n_layers - self.n_always
+        self.always_ids = list(range(self.n_sampled, self.n_layers))
         self._numel = (C.c_int64 * self.n_layers)(*self.layer_numel)
         cfg = GrassConfig()
         _check(L.grass_config_init(C.byref(cfg)))
@@ -238,6 +243,7 @@ class Grass:
         cfg.residency, cfg.cache_layers = residency, cache_layers
         cfg.max_grad_norm = max_grad_norm
         cfg.param_dtype = param_dtype
+        cfg.n_always = self.n_always
         self.bf16 = param_dtype == DTYPE_BF16
         self._uid = None
         if world == 1 and force_nccl:
@@ -288,8 +294,10 @@ class Grass:
     def sample_layers(self, period: int, probs: Sequence[float] | None = None):
         out = (C.c_int32 * self.gamma)()
         p = _dbl(probs) if probs is not None else None
-        if probs is not None and len(probs) != self.n_layers:
-            raise ValueError("probs must have N_L entries")
+        if probs is not None and len(probs) == self.n_sampled and self.n_always:
+            p = _dbl(list(probs) + [0.0] * self.n_always)
+        elif probs is not None and len(probs) != self.n_layers:
+            raise ValueError("probs must have n_layers (or N_L sampled) entries")
         _check(lib().grass_sample_layers(self._h, p, period, out), self._h)
         return list(out)
 

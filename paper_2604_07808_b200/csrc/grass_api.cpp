@@ -37,6 +37,7 @@ int64_t tiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
 struct grass_ctx {
   grass_config cfg{};
   int nl = 0;
+  int nsamp = 0;  // sampled layers [0, nsamp); always-active groups [nsamp, nl) (R19)
   std::vector<int64_t> numel, shard_off, shard_len, tiles, part_base;
   int64_t max_shard = 0;
   int64_t slot_stride = 0;  // max_shard rounded up to 64 elements: every slot array 256-B aligned
@@ -51,11 +52,13 @@ struct grass_ctx {
   void* h_mgn = nullptr;  // pinned host mirror of d_mgn
   size_t mgn_bytes = 0;
   double* d_gather = nullptr;  // world x N_L fp64 (all-gathered shard partials)
-  char* d_gscratch = nullptr;  // DP: averaged-gradient shards (2, or gamma when clipping)
+  char* d_gscratch = nullptr;  // DP: averaged-gradient shards (2, or clip_slots when clipping)
+  int clip_slots = 0;          // DP + clipping: layers one call may list (gamma + n_always)
 
   // optimizer state of this rank's shard of every layer: arr[0] = m,
   // arr[1] = v, arr[2] = fp32 master (bf16 mode); device or pinned host
   float* state_block = nullptr;
+  float* always_block = nullptr;  // offload: the always-active groups' states stay in HBM (R19)
   std::vector<float*> arr[3];
   std::vector<char> master_valid;
   std::vector<int64_t> t;
@@ -141,6 +144,11 @@ grass_status set_thread_err(grass_status s, const std::string& msg) {
   g_thread_err = msg;
   return s;
 }
+
+// Always-active groups (embedding, head: cfg.n_always, R19) are never sampled
+// and keep their optimizer states in HBM in every mode.
+bool always_active(const grass_ctx* c, int l) { return l >= c->nsamp; }
+bool home_on_device(const grass_ctx* c, int l) { return !c->cfg.offload || always_active(c, l); }
 
 // Element `off` of a parameter / gradient buffer of the context's dtype.
 void* elem(void* p, int64_t off, size_t esz) { return static_cast<char*>(p) + off * (int64_t)esz; }
@@ -259,7 +267,10 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
   if (!cfg->layer_numel) return bad("layer_numel is NULL");
   for (int i = 0; i < cfg->n_layers; ++i)
     if (cfg->layer_numel[i] < 1) return bad("every layer_numel must be >= 1");
-  if (cfg->gamma < 1 || cfg->gamma > cfg->n_layers) return bad("gamma must lie in [1, N_L]");
+  if (cfg->n_always < 0 || cfg->n_always >= cfg->n_layers)
+    return bad("n_always must lie in [0, n_layers - 1] (at least one sampled layer)");
+  const int nsamp = cfg->n_layers - cfg->n_always;
+  if (cfg->gamma < 1 || cfg->gamma > nsamp) return bad("gamma must lie in [1, N_L] (N_L = n_layers - n_always)");
   if (!(cfg->tau > 0.0) || !std::isfinite(cfg->tau)) return bad("tau must be positive");
   if (!(cfg->alpha >= 0.0 && cfg->alpha <= 1.0)) return bad("alpha must lie in [0, 1]");
   if (cfg->T_p < 0 || cfg->T_s < 1 || cfg->T_u < 1 || cfg->T_u % cfg->T_s != 0)
@@ -285,7 +296,7 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
     if (cfg->ring_slots < 0) return bad("ring_slots must be >= 0");
     if (cfg->residency != GRASS_RESIDENCY_STEP && cfg->residency != GRASS_RESIDENCY_PERIOD)
       return bad("unknown residency");
-    if (cfg->cache_layers < 0 || cfg->cache_layers > cfg->n_layers)
+    if (cfg->cache_layers < 0 || cfg->cache_layers > nsamp)
       return bad("cache_layers must lie in [0, N_L]");
   }
   if (!(cfg->max_grad_norm >= 0.0) || !std::isfinite(cfg->max_grad_norm))
@@ -648,8 +659,9 @@ float* cache_arr(grass_ctx* c, int slot, int a) {
   return c->d_cache + ((size_t)slot * c->ns + a) * c->slot_stride;
 }
 
-// Slot for every listed layer: hits keep their slot; misses take an empty slot
-// or evict the least recently used layer that is not trainable in this call.
+// Slot for every listed sampled layer: hits keep their slot; misses take an
+// empty slot or evict the least recently used layer that is not trainable in
+// this call.  Always-active groups get slot -1.
 void cache_plan(grass_ctx* c, const int32_t* ids, const std::vector<int>& order, std::vector<int>* slot_of,
                 std::vector<int>* victim_of) {
   const int n = (int)order.size();
@@ -658,13 +670,14 @@ void cache_plan(grass_ctx* c, const int32_t* ids, const std::vector<int>& order,
   std::vector<char> taken(c->cache_slots, 0);
   for (int j = 0; j < n; ++j) {
     const int l = ids[order[j]];
+    if (always_active(c, l)) continue;  // HBM-resident, no slot (R19)
     if (c->layer_slot[l] >= 0) {
       (*slot_of)[j] = c->layer_slot[l];
       taken[c->layer_slot[l]] = 1;
     }
   }
   for (int j = 0; j < n; ++j) {
-    if ((*slot_of)[j] >= 0) continue;
+    if ((*slot_of)[j] >= 0 || always_active(c, ids[order[j]])) continue;
     int best = -1;
     for (int k = 0; k < c->cache_slots; ++k) {
       if (taken[k]) continue;
@@ -804,7 +817,7 @@ float* state_ptr(grass_ctx* c, int a, int layer, bool* on_device) {
     *on_device = true;
     return cache_arr(c, slot, a);
   }
-  *on_device = !c->cfg.offload;
+  *on_device = home_on_device(c, layer);
   return c->arr[a][layer];
 }
 
@@ -852,6 +865,7 @@ void free_ctx(grass_ctx* c) {
   dfree(c->d_ring);
   dfree(c->d_gring);
   dfree(c->d_cache);
+  dfree(c->always_block);
   if (c->state_block) {
     if (c->cfg.offload)
       cudaFreeHost(c->state_block);
@@ -879,6 +893,7 @@ void free_ctx(grass_ctx* c) {
 grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   c->cfg = *cfg;
   c->nl = cfg->n_layers;
+  c->nsamp = cfg->n_layers - cfg->n_always;
   c->numel.assign(cfg->layer_numel, cfg->layer_numel + cfg->n_layers);
   c->cfg.layer_numel = nullptr;
   c->cfg.nccl_unique_id = nullptr;
@@ -890,14 +905,15 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   c->shard_len.resize(c->nl);
   c->tiles.resize(c->nl);
   c->part_base.resize(c->nl);
-  int64_t parts = 0, state_elems = 0;
+  int64_t parts = 0, state_elems = 0, always_elems = 0;
   for (int l = 0; l < c->nl; ++l) {
     shard_range(c->numel[l], W, cfg->rank, &c->shard_off[l], &c->shard_len[l]);
     c->tiles[l] = tiles_of(c->shard_len[l]);
     if (c->tiles[l] > INT32_MAX) return c->fail(GRASS_E_INVALID, "layer too large");
     c->part_base[l] = parts;
     parts += c->tiles[l];
-    state_elems += round_up(c->shard_len[l], kAlignElems);
+    // offload: the always-active groups get their own HBM block
+    (cfg->offload && always_active(c, l) ? always_elems : state_elems) += round_up(c->shard_len[l], kAlignElems);
     c->max_shard = std::max(c->max_shard, c->shard_len[l]);
   }
   // TMA bulk copies need 16-byte aligned slot arrays whatever the layer sizes
@@ -905,7 +921,8 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   c->t.assign(c->nl, 0);
   c->master_valid.assign(c->nl, 0);
   c->mgn.assign(c->nl, 0.0);
-  c->probs.assign(c->nl, 1.0 / c->nl);
+  c->probs.assign(c->nl, 0.0);  // always-active groups: p = 0, never sampled
+  for (int l = 0; l < c->nsamp; ++l) c->probs[l] = 1.0 / c->nsamp;
 
   CUDA_TRY(c, cudaSetDevice(cfg->device));
   CUDA_TRY(c, cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
@@ -946,12 +963,15 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   } else {
     CUDA_TRY(c, dalloc((void**)&c->state_block, state_bytes));
   }
-  int64_t o = 0;
+  if (always_elems > 0)
+    CUDA_TRY(c, dalloc((void**)&c->always_block, sizeof(float) * (size_t)c->ns * (size_t)always_elems));
+  int64_t o = 0, oa = 0;
   for (int a = 0; a < c->ns; ++a) {
     c->arr[a].resize(c->nl);
     for (int l = 0; l < c->nl; ++l) {
-      c->arr[a][l] = c->state_block + o;
-      o += round_up(c->shard_len[l], kAlignElems);
+      int64_t& off = (cfg->offload && always_active(c, l)) ? oa : o;
+      c->arr[a][l] = ((cfg->offload && always_active(c, l)) ? c->always_block : c->state_block) + off;
+      off += round_up(c->shard_len[l], kAlignElems);
     }
   }
 
@@ -994,7 +1014,8 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     CUDA_TRY(c, dalloc((void**)&c->d_gather, sizeof(double) * (size_t)W * c->nl));
     // two shard buffers for the RS || update overlap; clipping keeps every
     // active layer's averaged shard across its two passes
-    const size_t nslots = std::max<size_t>(2, cfg->max_grad_norm > 0.0 ? (size_t)cfg->gamma : 2);
+    c->clip_slots = cfg->max_grad_norm > 0.0 ? cfg->gamma + cfg->n_always : 0;
+    const size_t nslots = std::max<size_t>(2, (size_t)c->clip_slots);
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_s, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&c->ev_cs_start, &c->ev_cs_end, &c->ev_rs[0], &c->ev_rs[1], &c->ev_k2[0], &c->ev_k2[1]})
       CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -1079,7 +1100,12 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   const int32_t mode = clip ? kFinalizeNone : (sharded ? kFinalizeShard : kFinalizeMgn);
   const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
   const int nact = (int)order.size();
-  if (period && nact > c->cache_slots)
+  int ncached = 0;
+  for (int i = 0; i < n; ++i) ncached += always_active(c, ids[i]) ? 0 : 1;
+  if (sharded && clip && nact > c->clip_slots)
+    return c->fail(GRASS_E_INVALID, "data-parallel clipping: at most gamma + n_always layers per call "
+                                    "(their averaged gradients are kept between the two passes)");
+  if (period && ncached > c->cache_slots)
     return c->fail(GRASS_E_INVALID, "period residency: more layers in one call than cache slots "
                                     "(raise cache_layers)");
   struct CoefReset {  // the clip multiplier only applies inside this call
@@ -1152,7 +1178,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     Seg base = range_seg(c, l, g, 0, len);
     adam_scalars(c, l, lr, &base);
     base.out_slot = j;
-    if (period) {
+    if (period && !always_active(c, l)) {
       const int slot = slot_of[j];
       if (c->slot_layer[slot] == l) {  // hit: update in place in HBM, no link traffic
         if (c->slot_ready_pending[slot]) {  // prefetched: wait for its fill
@@ -1170,7 +1196,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
       }
       c->slot_use[slot] = c->call_seq;
       c->slot_dirty[slot] = 1;
-    } else if (c->cfg.offload) {
+    } else if (!home_on_device(c, l)) {
       if ((s = offload_layer(c, l, base, param, g, init, mode, st, g_host[i] != 0)) != GRASS_OK) return s;
     } else if (g_host[i]) {
       if ((s = stream_grad_layer(c, l, base, param, g, init, mode, st)) != GRASS_OK) return s;
@@ -1201,7 +1227,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
 
 // ---- checkpoint ------------------------------------------------------------
 const char kCkMagic[8] = {'G', 'R', 'A', 'S', 'S', 'C', 'K', '1'};
-const uint32_t kCkVersion = 1;
+const uint32_t kCkVersion = 2;  // 2: n_always in the header
 
 uint32_t crc_update(uint32_t crc, const void* p, size_t n) {
   const Bytef* b = static_cast<const Bytef*>(p);
@@ -1220,11 +1246,12 @@ void put(std::vector<char>* h, const T* p, size_t n) {
   h->insert(h->end(), b, b + sizeof(T) * n);
 }
 
-constexpr int kCkInts = 5;  // N_L, world, rank, committed, dtype
+constexpr int kCkInts = 6;  // n_layers, world, rank, committed, dtype, n_always
 
 std::vector<char> ck_header(grass_ctx* c) {
   std::vector<char> h;
-  const int32_t ints[kCkInts] = {c->nl, c->cfg.world, c->cfg.rank, c->committed ? 1 : 0, c->cfg.param_dtype};
+  const int32_t ints[kCkInts] = {c->nl,         c->cfg.world,         c->cfg.rank, c->committed ? 1 : 0,
+                                 c->cfg.param_dtype, c->cfg.n_always};
   put(&h, ints, kCkInts);
   put(&h, c->numel.data(), c->nl);
   put(&h, c->shard_len.data(), c->nl);
@@ -1357,8 +1384,8 @@ grass_status grass_update_probs(grass_ctx* c, double* probs_out) try {
   if (s != GRASS_OK) return s;
   const double* S = h_S(c);
   const long long* cnt = h_c(c);
-  long long total = 0;
-  for (int l = 0; l < c->nl; ++l) total += cnt[l];
+  long long total = 0;  // observations of the sampled layers
+  for (int l = 0; l < c->nsamp; ++l) total += cnt[l];
   if ((s = report_flag(c)) != GRASS_OK) {
     // the window was consumed; restore it so the caller may retry after aborting the step
     CUDA_TRY(c, cudaMemcpy(c->d_mgn, c->h_mgn, 16 * (size_t)c->nl, cudaMemcpyHostToDevice));
@@ -1367,7 +1394,7 @@ grass_status grass_update_probs(grass_ctx* c, double* probs_out) try {
   if (total == 0) return c->fail(GRASS_E_STATE, "commit with zero observations in the window");
   // Eq. 2 window mean (R4), first commit (R8) / Eq. 4 EMA (R5), retention of frozen layers
   const double a = c->cfg.alpha;
-  for (int l = 0; l < c->nl; ++l) {
+  for (int l = 0; l < c->nsamp; ++l) {
     if (cnt[l] > 0) {
       const double w = S[l] / (double)cnt[l];
       c->mgn[l] = c->committed ? a * w + (1.0 - a) * c->mgn[l] : w;
@@ -1379,9 +1406,9 @@ grass_status grass_update_probs(grass_ctx* c, double* probs_out) try {
   c->committed = true;
   // Eq. 3 per policy
   if (c->cfg.policy == GRASS_POLICY_UNIFORM) {
-    for (int l = 0; l < c->nl; ++l) c->probs[l] = 1.0 / c->nl;
+    for (int l = 0; l < c->nsamp; ++l) c->probs[l] = 1.0 / c->nsamp;
   } else if (c->cfg.policy == GRASS_POLICY_ADAPTIVE || first) {
-    softmax_probs(c->mgn.data(), c->nl, c->cfg.tau, c->cfg.normalize_mgn != 0, c->probs.data());
+    softmax_probs(c->mgn.data(), c->nsamp, c->cfg.tau, c->cfg.normalize_mgn != 0, c->probs.data());
   }
   if (probs_out) std::memcpy(probs_out, c->probs.data(), sizeof(double) * c->nl);
   return GRASS_OK;
@@ -1393,9 +1420,9 @@ grass_status grass_sample_layers(grass_ctx* c, const double* probs, uint64_t per
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (!ids_out) return c->fail(GRASS_E_INVALID, "ids_out is NULL");
   const double* p = probs ? probs : c->probs.data();
-  for (int l = 0; l < c->nl; ++l)
+  for (int l = 0; l < c->nsamp; ++l)
     if (!(p[l] >= 0.0) || !std::isfinite(p[l])) return c->fail(GRASS_E_INVALID, "probs must be finite, >= 0");
-  sample_from_probs(p, c->nl, c->cfg.gamma, c->cfg.seed, period, ids_out);
+  sample_from_probs(p, c->nsamp, c->cfg.gamma, c->cfg.seed, period, ids_out);
   return GRASS_OK;
 } catch (...) {
   return api_exception(c);
@@ -1455,7 +1482,9 @@ grass_status grass_prefetch_layers(grass_ctx* c, const int32_t* ids, int32_t n, 
   std::vector<int> order;
   grass_status s = check_call(c, c->bf16, ids, n, nullptr, nullptr, &order);
   if (s != GRASS_OK) return s;
-  if (n > c->cache_slots) return c->fail(GRASS_E_INVALID, "more layers than cache slots");
+  int ncached = 0;
+  for (int i = 0; i < n; ++i) ncached += always_active(c, ids[i]) ? 0 : 1;
+  if (ncached > c->cache_slots) return c->fail(GRASS_E_INVALID, "more layers than cache slots");
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   std::vector<int> slot_of, victim_of;
@@ -1466,6 +1495,7 @@ grass_status grass_prefetch_layers(grass_ctx* c, const int32_t* ids, int32_t n, 
   if ((s = wait_pending(c, c->d2h)) != GRASS_OK) return s;
   for (int j = 0; j < (int)order.size(); ++j) {
     const int l = ids[order[j]], slot = slot_of[j];
+    if (slot < 0) continue;  // always-active group: already in HBM
     c->slot_use[slot] = c->call_seq;
     if (c->slot_layer[slot] == l) continue;  // already cached
     if ((s = prefetch_into(c, l, slot, victim_of[j])) != GRASS_OK) return s;
@@ -1627,8 +1657,9 @@ grass_status grass_load_state(grass_ctx* c, const char* path) try {
   take(S.data(), 8 * nl);
   take(cnt.data(), 8 * nl);
   if (ints[0] != nl || ints[1] != c->cfg.world || ints[2] != c->cfg.rank || ints[4] != c->cfg.param_dtype ||
-      numel != c->numel || slen != c->shard_len)
-    return bad(GRASS_E_INVALID, "checkpoint does not match this context (N_L, N_p, dtype, world or rank)");
+      ints[5] != c->cfg.n_always || numel != c->numel || slen != c->shard_len)
+    return bad(GRASS_E_INVALID,
+               "checkpoint does not match this context (N_L, n_always, N_p, dtype, world or rank)");
   const long blobs = std::ftell(f);
   // pass 1: verify every blob's length and CRC32 before touching the context
   std::vector<char> buf(64u << 20);

@@ -10,6 +10,9 @@
                         (grass_prefetch_layers) so they move during fwd/bwd;
   other steps           keep the set; update it (grass_step_layers).
 
+Always-active groups (Grass(n_always=k): embedding / head, DESIGN R19) are not
+probed or sampled; they join every adaptive step's update.
+
 Host logic only: every step of the hot path runs in libgrass.so.
 
     sched = GrassSchedule(grass)
@@ -32,6 +35,8 @@ class GrassSchedule:
         cfg = grass.cfg
         self.T_p, self.T_s, self.T_u = cfg.T_p, cfg.T_s, cfg.T_u
         self.n_layers = grass.n_layers
+        self.always = list(getattr(grass, "always_ids", []))
+        self.n_sampled = self.n_layers - len(self.always)
         # prefetch only makes sense with period residency
         period = bool(cfg.offload) and cfg.residency == 1
         self.prefetch = period if prefetch is None else (prefetch and period)
@@ -47,7 +52,7 @@ class GrassSchedule:
         probing).  At period boundaries commits / resamples / prefetches."""
         d = self.decision(step)
         if d == DECIDE_PROBE:
-            return list(range(self.n_layers))
+            return list(range(self.n_sampled))
         if d == DECIDE_COMMIT_RESAMPLE:
             self.probs = self.g.update_probs()
         if d in (DECIDE_COMMIT_RESAMPLE, DECIDE_RESAMPLE) or not self.trainable:
@@ -55,12 +60,12 @@ class GrassSchedule:
             self.trainable = self.g.sample_layers(self.period_index)
             if self.prefetch:
                 self.g.prefetch_layers(self.trainable, stream=stream)
-        return list(self.trainable)
+        return list(self.trainable) + self.always
 
     def end_step(self, step: int, params: Sequence, grads: Sequence, lr: float, stream=None):
         """params / grads: one entry per layer of begin_step(step), same order."""
-        layers = (list(range(self.n_layers)) if self.decision(step) == DECIDE_PROBE
-                  else self.trainable)
+        layers = (list(range(self.n_sampled)) if self.decision(step) == DECIDE_PROBE
+                  else self.trainable + self.always)
         if len(grads) != len(layers):
             raise ValueError("one gradient per layer returned by begin_step")
         if self.decision(step) == DECIDE_PROBE:

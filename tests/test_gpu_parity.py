@@ -858,18 +858,20 @@ def test_single_layer_single_element():
 
 @pytest.mark.parametrize("seed", range(8))
 def test_fuzz_dtypes_clip_checkpoint(seed, tmp_path):
-    """Like the pipeline fuzz, over both dtypes and random clipping, with a
-    checkpoint written by one path and restored into a fresh context of a
-    different path mid-run: every path stays bit-identical to resident."""
+    """Like the pipeline fuzz, over both dtypes, random clipping and random
+    always-active groups (R19), with a checkpoint written by one path and
+    restored into a fresh context of a different path mid-run: every path
+    stays bit-identical to resident."""
     rng = np.random.default_rng(100 + seed)
     dtype = G.DTYPE_BF16 if seed % 2 else G.DTYPE_FP32
     tdt = torch.bfloat16 if seed % 2 else torch.float32
     nl = int(rng.integers(2, 6))
-    numel = [int(rng.integers(1, 30_000)) for _ in range(nl)]
+    n_alw = int(rng.integers(0, 3))
+    numel = [int(rng.integers(1, 30_000)) for _ in range(nl + n_alw)]
     gamma = int(rng.integers(1, nl + 1))
     clip = float(rng.choice([0.0, 1e-3, 1.0]))
     chunk = 4096 * int(rng.integers(1, 4))
-    common = dict(gamma=gamma, weight_decay=0.01, max_grad_norm=clip, param_dtype=dtype)
+    common = dict(gamma=gamma, weight_decay=0.01, max_grad_norm=clip, param_dtype=dtype, n_always=n_alw)
     kws = [dict(), dict(offload=True, chunk_elems=chunk, ring_slots=int(rng.integers(1, 4))),
            dict(offload=True, chunk_elems=chunk, residency=G.RESIDENCY_PERIOD),
            dict(force_nccl=True)]
@@ -878,9 +880,10 @@ def test_fuzz_dtypes_clip_checkpoint(seed, tmp_path):
     ps = [[p.clone() for p in base] for _ in ctxs]
     for step in range(8):
         ids = [int(x) for x in rng.choice(nl, size=int(rng.integers(1, gamma + 1)), replace=False)]
+        ids += [nl + k for k in range(n_alw) if rng.random() < 0.8]   # always groups (most steps)
         grads = [layer_grad(numel[l], l, 1e-2, step=step, seed=seed, device=DEV).to(tdt) for l in ids]
         r = rng.random()
-        if r < 0.3:     # prefetch exactly the next set
+        if r < 0.3:     # prefetch exactly the next set (always groups included: no-op for them)
             ctxs[2].prefetch_layers(ids)
         elif r < 0.5:   # prefetch a different set (evicted or reused before use)
             ctxs[2].prefetch_layers([int(x) for x in rng.choice(nl, size=min(gamma, nl), replace=False)])
@@ -893,7 +896,7 @@ def test_fuzz_dtypes_clip_checkpoint(seed, tmp_path):
             ctxs[2].load_state(path)
     torch.cuda.synchronize()
     for k in range(1, len(ctxs)):
-        for l in range(nl):
+        for l in range(nl + n_alw):
             assert torch.equal(ps[0][l], ps[k][l]), (seed, k, l)
             a, b = ctxs[0].read_state(l), ctxs[k].read_state(l)
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
@@ -1105,6 +1108,92 @@ def test_schedule_driver_end_to_end_vs_oracle():
     st = gr.get_mgn()
     assert st["m"] == pytest.approx(orc.mgn.m, rel=1e-7)
     assert st["S"] == pytest.approx(orc.mgn.S, rel=1e-7)
+
+
+# ------------------------------------ R19: always-active groups (embedding/head)
+@pytest.mark.parametrize("mode", ["resident", "offload", "period"])
+def test_always_groups_schedule_vs_oracle(mode):
+    """4 sampled layers + 2 always-active groups (embedding- and head-sized,
+    ragged) driven by GrassSchedule against the oracle: the groups are never
+    probed or sampled, get p = 0, are updated every adaptive step (t = number
+    of adaptive steps) and their m/v stay in HBM even with offload."""
+    numel = [65_536] * 4 + [3 * 4096 + 7, 50_000]
+    kw = {"resident": {}, "offload": dict(offload=True, chunk_elems=16_384),
+          "period": dict(offload=True, residency=G.RESIDENCY_PERIOD)}[mode]
+    T_p, T_s, lr, seed = 2, 2, 1e-3, 5
+    gr = G.Grass(numel, gamma=2, T_p=T_p, T_s=T_s, seed=seed, weight_decay=0.01, n_always=2, **kw)
+    sched = G.GrassSchedule(gr)
+    orc = O.GrassOracle(numel, gamma=2, seed=seed, weight_decay=0.01, n_always=2)
+    if mode != "resident":   # pinned host holds only the sampled layers' m/v
+        assert gr.host_bytes == 8 * 4 * 65_536
+    sig = grad_sigmas(6, 3)
+    params = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    adaptive = 0
+    for step in range(T_p + 3 * T_s):
+        layers = sched.begin_step(step)
+        d = O.schedule_decision(step, T_p, T_s)
+        if d == "probe":
+            assert layers == [0, 1, 2, 3]
+        else:
+            assert layers[-2:] == [4, 5] and max(layers[:-2]) < 4 and len(layers) == 4
+            adaptive += 1
+        if "commit" in d:
+            p = orc.update_probs()
+            assert sched.probs == pytest.approx(p, rel=1e-9) and sched.probs[4:] == [0.0, 0.0]
+        grads = [layer_grad(numel[l], l, sig[l], step=step, device=DEV) for l in layers]
+        if d == "probe":
+            sched.end_step(step, [params[l] for l in layers], grads, lr)
+            orc.accumulate(layers, [_np(g) for g in grads])
+            continue
+        th_in = [_np(params[l]).copy() for l in layers]
+        m_in = [orc.m[l].copy() for l in layers]
+        sched.end_step(step, [params[l] for l in layers], grads, lr)
+        host = [th.copy() for th in th_in]
+        orc.step_layers(layers, host, [_np(g) for g in grads], float(np.float32(lr)))
+        for k, l in enumerate(layers):
+            m_gpu, v_gpu, t = gr.read_state(l)
+            assert t == orc.t[l]
+            assert_state_close(_np(params[l]), m_gpu, v_gpu, host[k], orc.m[l], orc.v[l],
+                               th_in[k], m_in[k], _np(grads[k]))
+            orc.m[l], orc.v[l] = m_gpu, v_gpu
+    assert gr.read_state(4)[2] == gr.read_state(5)[2] == adaptive
+    st = gr.get_mgn()
+    assert st["m"][:4] == pytest.approx(orc.mgn.m, rel=1e-7) and st["m"][4:] == [0.0, 0.0]
+    assert st["S"][:4] == pytest.approx(orc.mgn.S, rel=1e-7)
+    for l in (4, 5):   # the groups' norms are still computed (introspection)
+        assert st["c"][l] >= 1
+
+
+def test_always_groups_validation_and_checkpoint(tmp_path):
+    numel = [4096] * 3 + [8192]
+    with pytest.raises(G.GrassError):
+        G.Grass(numel, gamma=4, n_always=1)            # gamma > N_L sampled
+    with pytest.raises(G.GrassError):
+        G.Grass(numel, gamma=1, n_always=4)            # no sampled layer left
+    with pytest.raises(G.GrassError):
+        G.Grass(numel, gamma=1, n_always=-1)
+    gr = G.Grass(numel, gamma=3, n_always=1, offload=True, residency=G.RESIDENCY_PERIOD)
+    p = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    g = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
+    gr.prefetch_layers([0, 1, 2, 3])                   # 3 slots + the HBM-resident group
+    gr.step_layers([0, 1, 2, 3], p, g, 1e-3)           # 4 layers, 3 cache slots: fine
+    path = str(tmp_path / "ck")
+    gr.save_state(path)
+    other = G.Grass(numel, gamma=3, n_always=0, offload=True, residency=G.RESIDENCY_PERIOD)
+    with pytest.raises(G.GrassError):
+        other.load_state(path)                         # n_always differs
+    same = G.Grass(numel, gamma=3, n_always=1)
+    same.load_state(path)
+    for l in range(4):
+        a, b = gr.read_state(l), same.read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2] == 1
+    assert gr.sample_layers(0, [0.2, 0.3, 0.5]) == gr.sample_layers(0, [0.2, 0.3, 0.5, 0.0])
+    # the NCCL path with clipping keeps gamma + n_always averaged shards between its passes
+    dp = G.Grass(numel, gamma=1, n_always=1, force_nccl=True, max_grad_norm=1.0)
+    with pytest.raises(G.GrassError, match="gamma \\+ n_always"):
+        dp.step_layers([0, 1, 3], [p[0], p[1], p[3]], [g[0], g[1], g[3]], 1e-3)
+    dp.step_layers([0, 3], [p[0], p[3]], [g[0], g[3]], 1e-3)
+    dp.sync()
 
 
 def test_example_training_loop_loss_decreases():

@@ -342,6 +342,56 @@ def test_gamma_equals_NL_degenerates_to_plain_adamw():
     assert orc.t == [4, 4, 4]
 
 
+# ----------------------------------------------- R19: always-active groups
+def test_always_groups_gamma_equals_NL_is_plain_adamw_over_everything():
+    # SPEC.md:145 (embedding / head always trainable, excluded from sampling):
+    # with gamma = N_L sampled layers plus the always groups listed every step,
+    # every tensor follows torch.optim.AdamW (fp64) -- the always groups too.
+    rng = np.random.default_rng(6)
+    numel = [17, 64, 5, 40, 9]          # 3 sampled layers + 2 always groups
+    lr, wd = 1e-2, 0.01
+    orc = O.GrassOracle(numel, gamma=3, weight_decay=wd, seed=9, n_always=2)
+    params = [(rng.standard_normal(k) * 0.02).astype(np.float32) for k in numel]
+    tparams = [torch.nn.Parameter(torch.from_numpy(p.astype(np.float64))) for p in params]
+    opt = torch.optim.AdamW(tparams, lr=lr, weight_decay=wd, foreach=False)
+    for step in range(4):
+        grads = [(rng.standard_normal(k) * 1e-2).astype(np.float32) for k in numel]
+        if step == 0:
+            orc.accumulate([0, 1, 2], grads[:3])
+            p = orc.update_probs()
+            assert len(p) == 5 and p[3:] == [0.0, 0.0] and abs(sum(p) - 1.0) < 1e-12
+        ids = orc.sample(step)
+        assert sorted(ids) == [0, 1, 2]
+        ids = ids + [3, 4]
+        orc.step_layers(ids, [params[i] for i in ids], [grads[i] for i in ids], lr)
+        for tp, g in zip(tparams, grads):
+            tp.grad = torch.from_numpy(g.astype(np.float64))
+        opt.step()
+        for p_, tp in zip(params, tparams):
+            np.testing.assert_allclose(p_, tp.detach().numpy(), rtol=1e-6, atol=1e-9)
+    assert orc.t == [4] * 5
+
+
+def test_always_groups_do_not_touch_mgn_or_sampling():
+    # The MGN window, Eq. 3 probabilities and the sampler of a run with always
+    # groups equal those of the same run without them (they are invisible to
+    # PAPER.md:89-127); the sampler never returns an always id.
+    rng = np.random.default_rng(7)
+    numel = [33, 10, 50, 21]
+    a = O.GrassOracle(numel, gamma=2, seed=3)
+    b = O.GrassOracle(numel + [64, 8], gamma=2, seed=3, n_always=2)
+    for _ in range(3):
+        grads = [(rng.standard_normal(k) * rng.uniform(1e-3, 1)).astype(np.float32) for k in numel + [64, 8]]
+        a.accumulate([0, 1, 2, 3], grads[:4])
+        b.accumulate([0, 1, 2, 3, 4, 5], grads)
+    pa, pb = a.update_probs(), b.update_probs()
+    assert pb[:4] == pa and pb[4:] == [0.0, 0.0]
+    assert b.last_ss[4] == O.sq_norm(grads[4])
+    for period in range(200):
+        ids = b.sample(period)
+        assert ids == a.sample(period) and max(ids) < 4
+
+
 # ------------------------------------------------ R17: global-norm clipping
 def test_clip_coefficient_matches_torch_clip_grad_norm():
     rng = np.random.default_rng(11)

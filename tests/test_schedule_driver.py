@@ -63,3 +63,23 @@ def test_schedule_paper_values():
     samples = [c[1] for c in g.calls if c[0] == "sample"]
     assert samples == [0, 1, 2, 3]                                     # steps 150, 175, 200, 225
     assert sum(1 for c in g.calls if c[0] == "probe") == 150
+
+
+def test_schedule_always_groups_join_every_update_and_skip_probing():
+    # R19: always-active groups (embedding / head) are not probed or sampled;
+    # every adaptive step's update lists them after the sampled set.
+    g = FakeGrass(4, T_p=2, T_s=2, T_u=2)
+    g.n_layers = 6
+    g.always_ids = [4, 5]
+    s = GrassSchedule(g)
+    seen = []
+    for step in range(6):
+        layers = s.begin_step(step)
+        seen.append(layers)
+        s.end_step(step, [None] * len(layers), [None] * len(layers), 1e-3)
+    assert seen[0] == seen[1] == [0, 1, 2, 3]                      # probing: sampled layers only
+    for layers in seen[2:]:
+        assert layers[-2:] == [4, 5] and len(layers) == 4
+    updates = [c[1] for c in g.calls if c[0] == "update"]
+    assert all(u[-2:] == (4, 5) for u in updates) and len(updates) == 4
+    assert [c for c in g.calls if c[0] == "probe"] == [("probe", 4), ("probe", 4)]
