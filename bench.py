@@ -218,7 +218,9 @@ def run_grass(args, rank, world, local):
     torch.cuda.set_device(dev)
     legs = set(args.legs.split(","))
     if world > 1 and args.legs == DEFAULT_LEGS:
-        legs = {"main", "e2e"}
+        # the north star's per-N numbers: resident step, e2e, and the offloaded
+        # step (per-step round trip and period residency) on element shards
+        legs = {"main", "e2e", "offload", "period"}
     shape = MODELS[args.model]
     NL, n_p, gamma = shape.n_layers, shape.layer_numel, args.gamma
     sig = grad_sigmas(NL, 0)
@@ -288,8 +290,8 @@ def run_grass(args, rank, world, local):
             traffic = json.load(f).get(f"fused_update/{args.model}/g{gamma}/w{world}")
 
     # Optional legs.  At world == 1 a failing optional leg is recorded under
-    # "leg_errors" instead of costing the main line; at world > 1 the default is
-    # main + e2e only (a rank-local failure inside a collective leg would hang).
+    # "leg_errors" instead of costing the main line; at world > 1 an exception is
+    # not caught (a rank-local failure inside a collective leg would hang).
     leg_errors = {}
 
     def guarded(name, fn):
