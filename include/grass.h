@@ -132,7 +132,27 @@ typedef struct grass_config {
                                   The sampled layers are ids [0, N_L) with N_L = n_layers -
                                   n_always; gamma, cache_layers, probabilities and the commit
                                   refer to those only.  0 = none (default). */
+  int32_t dp_mode;             /* world >= 1 data parallelism:
+                                  GRASS_DP_NCCL: NCCL reduce-scatter -> update -> all-gather
+                                  (needs nccl_unique_id when world > 1);
+                                  GRASS_DP_P2P: ONE fused kernel per call reads every rank's
+                                  gradient over peer memory (NVLink), sums them in rank order,
+                                  updates this rank's shard and stores theta' into every rank's
+                                  parameters; the shard norms are published the same way.
+                                  Needs grass_p2p_attach + grass_p2p_register_layer; world <= 8;
+                                  no clipping. */
+  int32_t p2p_sync;            /* GRASS_DP_P2P: 1 (default) = each call starts and ends with a
+                                  device-side barrier over the peers (system-scope flags in the
+                                  exchange blocks) and finishes the MGN update itself;
+                                  0 = no barriers: the caller orders the ranks' calls and calls
+                                  grass_p2p_finish on every rank afterwards (single-process,
+                                  multi-context testing on one GPU). */
 } grass_config;
+
+typedef enum {
+  GRASS_DP_NCCL = 0,
+  GRASS_DP_P2P = 1
+} grass_dp_mode;
 
 typedef enum {
   GRASS_DTYPE_FP32 = 0,
@@ -296,7 +316,8 @@ typedef enum {
   GRASS_TRACE_D2H = 2,    /* optimizer states device -> host (write-back/evict) */
   GRASS_TRACE_NORM = 3,   /* norm-only launch (K1)                              */
   GRASS_TRACE_RS = 4,     /* NCCL reduce-scatter of gradients                   */
-  GRASS_TRACE_AG = 5      /* NCCL all-gather of parameters                      */
+  GRASS_TRACE_AG = 5,     /* NCCL all-gather of parameters                      */
+  GRASS_TRACE_P2P = 6     /* P2P norm publication + barrier                     */
 } grass_trace_kind;
 
 typedef struct grass_trace_event {
@@ -359,6 +380,40 @@ int32_t grass_schedule_decision(int64_t step, int32_t T_p, int32_t T_s, int32_t 
 /* Creates an NCCL unique id (128 bytes) on the calling host; rank 0 calls it
  * and broadcasts the bytes to the other ranks (e.g. via a torch process group). */
 grass_status grass_nccl_get_unique_id(void* out);
+
+/* ----- P2P data parallelism (cfg.dp_mode = GRASS_DP_P2P) ------------------
+ * Every rank's context owns an exchange block in HBM (barrier flags + gather
+ * rows of the shard norms).  Setup, collectively on every rank:
+ *   1. grass_p2p_exchange_block -> export it to the peers (grass_ipc_export,
+ *      any host transport, grass_ipc_import on the peers);
+ *   2. grass_p2p_attach with the [world] block addresses as seen by this process;
+ *   3. per layer, grass_p2p_register_layer with the [world] full-layer parameter
+ *      and gradient buffers (this rank's own at index rank) — the buffers that
+ *      every later grass_step_layers / grass_mgn_accumulate must pass.
+ * Ordering contract (p2p_sync = 1): every rank issues the same sequence of
+ * hot-path calls; a call returns to the stream only after every rank's update
+ * (and its theta' stores into this rank's buffers) is complete, so the caller
+ * may overwrite its gradients and read its parameters afterwards. */
+#define GRASS_IPC_HANDLE_BYTES 64
+grass_status grass_p2p_exchange_block(grass_ctx* ctx, void** ptr, int64_t* bytes);
+/* blocks: host [world] addresses of every rank's exchange block, valid in this
+ * process (blocks[rank] must be this context's own). */
+grass_status grass_p2p_attach(grass_ctx* ctx, void* const* blocks);
+/* params / grads: host [world] arrays of full-layer buffers (N_p elements of the
+ * context's dtype, 16-byte aligned), index = rank; this rank's entries must be
+ * device memory of the context's GPU.  Synchronous (copies the table to HBM). */
+grass_status grass_p2p_register_layer(grass_ctx* ctx, int32_t layer, void* const* params,
+                                      const void* const* grads);
+/* p2p_sync = 0 only: finishes the MGN update of the last hot-path call (the
+ * fixed rank-order sum of the published shard norms); call it on every rank
+ * after every rank's hot-path call has completed. */
+grass_status grass_p2p_finish(grass_ctx* ctx, void* stream);
+/* Exports the allocation containing ptr as a CUDA IPC handle (64 bytes) plus
+ * the byte offset of ptr inside it. */
+grass_status grass_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);
+/* Opens an IPC handle exported by another process (cached: each allocation is
+ * opened once per process) and returns base + offset. */
+grass_status grass_ipc_import(int32_t device, const void* handle, int64_t offset, void** ptr_out);
 
 #ifdef __cplusplus
 }

@@ -4,11 +4,11 @@ The product is libgrass.so (C ABI, include/grass.h) built from csrc/; this
 package is its thin ctypes binding.  It never imports oracle/.
 """
 from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_CONTINUE, DECIDE_PROBE, DECIDE_RESAMPLE,
-                      RESIDENCY_PERIOD, RESIDENCY_STEP, DTYPE_BF16, DTYPE_FP32,
+                      RESIDENCY_PERIOD, RESIDENCY_STEP, DTYPE_BF16, DTYPE_FP32, DP_NCCL, DP_P2P,
                       POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM, Grass, GrassError,
                       exported_symbols, lib, nccl_unique_id, sample_from_probs,
                       schedule_decision, shard_range, softmax_probs, splitmix64, tile_elems,
-                      uniform)
+                      uniform, ipc_export, ipc_import)
 
 from .schedule import GrassSchedule  # noqa: E402
 
@@ -16,4 +16,5 @@ __all__ = ["Grass", "GrassSchedule", "GrassError", "lib", "exported_symbols", "n
            "sample_from_probs", "schedule_decision", "shard_range", "softmax_probs",
            "splitmix64", "tile_elems", "uniform", "POLICY_ADAPTIVE", "POLICY_STATIC",
            "POLICY_UNIFORM", "DECIDE_PROBE", "DECIDE_COMMIT_RESAMPLE", "DECIDE_RESAMPLE",
-           "DECIDE_CONTINUE", "RESIDENCY_STEP", "RESIDENCY_PERIOD", "DTYPE_FP32", "DTYPE_BF16"]
+           "DECIDE_CONTINUE", "RESIDENCY_STEP", "RESIDENCY_PERIOD", "DTYPE_FP32", "DTYPE_BF16",
+           "DP_NCCL", "DP_P2P", "ipc_export", "ipc_import"]

@@ -21,6 +21,8 @@ POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM = range(3)
 DECIDE_PROBE, DECIDE_COMMIT_RESAMPLE, DECIDE_RESAMPLE, DECIDE_CONTINUE = range(4)
 RESIDENCY_STEP, RESIDENCY_PERIOD = range(2)
 DTYPE_FP32, DTYPE_BF16 = range(2)
+DP_NCCL, DP_P2P = range(2)
+IPC_HANDLE_BYTES = 64
 NCCL_ID_BYTES = 128
 
 _STATUS = {0: "GRASS_OK", 1: "GRASS_E_INVALID", 2: "GRASS_E_STATE", 3: "GRASS_E_CUDA",
@@ -38,7 +40,7 @@ class TraceEvent(C.Structure):
                 ("count", C.c_int64), ("start_ms", C.c_float), ("end_ms", C.c_float)]
 
 
-TRACE_KINDS = {0: "h2d", 1: "update", 2: "d2h", 3: "norm", 4: "rs", 5: "ag"}
+TRACE_KINDS = {0: "h2d", 1: "update", 2: "d2h", 3: "norm", 4: "rs", 5: "ag", 6: "p2p"}
 
 
 class GrassConfig(C.Structure):
@@ -53,6 +55,7 @@ class GrassConfig(C.Structure):
         ("ring_slots", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("residency", C.c_int32), ("cache_layers", C.c_int32),
         ("max_grad_norm", C.c_double), ("param_dtype", C.c_int32), ("n_always", C.c_int32),
+        ("dp_mode", C.c_int32), ("p2p_sync", C.c_int32),
     ]
 
 
@@ -108,6 +111,13 @@ _SIGS = {
                                     C.POINTER(C.c_int64)]),
     "grass_schedule_decision": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, C.c_int32]),
     "grass_nccl_get_unique_id": (C.c_int, [C.c_void_p]),
+    "grass_p2p_exchange_block": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "grass_p2p_attach": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "grass_p2p_register_layer": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p),
+                                           C.POINTER(C.c_void_p)]),
+    "grass_p2p_finish": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "grass_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "grass_ipc_import": (C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
 }
 
 
@@ -201,6 +211,21 @@ def _ptrs(tensors, itemsize: int = 4, host_ok: bool = False):
     return arr
 
 
+def ipc_export(ptr: int):
+    """(64-byte CUDA IPC handle of the allocation containing ptr, byte offset)."""
+    h = C.create_string_buffer(IPC_HANDLE_BYTES)
+    off = C.c_int64()
+    _check(lib().grass_ipc_export(C.c_void_p(ptr), h, C.byref(off)))
+    return h.raw, off.value
+
+
+def ipc_import(device: int, handle: bytes, offset: int) -> int:
+    """Address (in this process) of an allocation exported by another process."""
+    out = C.c_void_p()
+    _check(lib().grass_ipc_import(device, handle, offset, C.byref(out)))
+    return out.value
+
+
 class Grass:
     """One GRASS hot-path context (one per process / GPU).
 
@@ -217,7 +242,7 @@ class Grass:
                  chunk_elems: int = 0, ring_slots: int = 0, rank: int = 0, world: int = 1,
                  process_group=None, force_nccl: bool = False, residency: int = RESIDENCY_STEP,
                  cache_layers: int = 0, max_grad_norm: float = 0.0, param_dtype: int = DTYPE_FP32,
-                 n_always: int = 0):
+                 n_always: int = 0, dp_mode: int = DP_NCCL, p2p_sync: bool = True):
         L = lib()
         self.layer_numel = [int(x) for x in layer_numel]
         self.n_layers = len(self.layer_numel)
@@ -244,12 +269,14 @@ class Grass:
         cfg.max_grad_norm = max_grad_norm
         cfg.param_dtype = param_dtype
         cfg.n_always = self.n_always
+        cfg.dp_mode, cfg.p2p_sync = dp_mode, int(p2p_sync)
+        self.dp_mode = dp_mode
         self.bf16 = param_dtype == DTYPE_BF16
         self._uid = None
         if world == 1 and force_nccl:
             self._uid = C.create_string_buffer(nccl_unique_id(), NCCL_ID_BYTES)
             cfg.nccl_unique_id = C.cast(self._uid, C.c_void_p)
-        elif world > 1:
+        elif world > 1 and dp_mode == DP_NCCL:
             import torch.distributed as dist
             obj = [nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0, group=process_group)
@@ -332,6 +359,48 @@ class Grass:
         if m.size != n or v.size != n:
             raise ValueError("state size must equal the shard length")
         _check(lib().grass_write_state(self._h, layer, m.ctypes.data, v.ctypes.data, t), self._h)
+
+    # P2P data parallelism (dp_mode=DP_P2P) --------------------------------
+    def p2p_exchange_block(self):
+        ptr, n = C.c_void_p(), C.c_int64()
+        _check(lib().grass_p2p_exchange_block(self._h, C.byref(ptr), C.byref(n)), self._h)
+        return ptr.value, n.value
+
+    def p2p_attach(self, blocks: Sequence[int]):
+        arr = (C.c_void_p * len(blocks))(*blocks)
+        _check(lib().grass_p2p_attach(self._h, arr), self._h)
+
+    def p2p_register_layer(self, layer: int, params: Sequence, grads: Sequence):
+        """params / grads: [world] full-layer buffers (tensors or raw addresses), index = rank."""
+        def addr(x):
+            return x if isinstance(x, int) else x.data_ptr()
+        pa = (C.c_void_p * len(params))(*[addr(x) for x in params])
+        ga = (C.c_void_p * len(grads))(*[addr(x) for x in grads])
+        _check(lib().grass_p2p_register_layer(self._h, layer, pa, ga), self._h)
+
+    def p2p_finish(self, stream=None):
+        _check(lib().grass_p2p_finish(self._h, _stream_ptr(stream)), self._h)
+
+    def p2p_setup(self, layer_buffers: dict, process_group=None):
+        """Collective over the process group (any backend): exports this rank's
+        exchange block and every {layer: (param, grad)} buffer through CUDA IPC,
+        gathers every rank's handles, imports the peers' and registers them."""
+        import torch.distributed as dist
+        mine = {"exch": ipc_export(self.p2p_exchange_block()[0]),
+                "layers": {int(l): (ipc_export(p.data_ptr()), ipc_export(g.data_ptr()))
+                           for l, (p, g) in layer_buffers.items()}}
+        allr = [None] * self.world
+        dist.all_gather_object(allr, mine, group=process_group)
+        dev = self.cfg.device
+
+        def addr(q, h, own):
+            return own if q == self.rank else ipc_import(dev, *h)
+        blocks = [addr(q, allr[q]["exch"], self.p2p_exchange_block()[0]) for q in range(self.world)]
+        self.p2p_attach(blocks)
+        for l, (p, g) in layer_buffers.items():
+            ps = [addr(q, allr[q]["layers"][int(l)][0], p.data_ptr()) for q in range(self.world)]
+            gs = [addr(q, allr[q]["layers"][int(l)][1], g.data_ptr()) for q in range(self.world)]
+            self.p2p_register_layer(int(l), ps, gs)
 
     def save_state(self, path: str):
         _check(lib().grass_save_state(self._h, os.fsencode(path)), self._h)

@@ -10,6 +10,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -116,6 +118,16 @@ struct grass_ctx {
   cudaEvent_t trace_base = nullptr;
   std::vector<TraceRec> trace;
   std::vector<cudaEvent_t> trace_pool;
+
+  // P2P data parallelism (cfg.dp_mode = GRASS_DP_P2P)
+  bool p2p = false;
+  char* d_exch = nullptr;        // this rank's exchange block: barrier flags + gather rows
+  size_t exch_bytes = 0;
+  std::vector<char*> exch_peer;  // every rank's block (after grass_p2p_attach)
+  void** d_ptab = nullptr;       // device [nl][2][world]: gradient then parameter pointers
+  std::vector<const void*> own_g, own_p;  // this rank's registered full-layer buffers
+  uint64_t epoch[2] = {0, 0};    // start / end barrier generations
+  std::vector<int32_t> p2p_pending;  // p2p_sync = 0: layers whose MGN finish is pending
 
   Comm comm;
   bool has_comm = false;
@@ -226,7 +238,7 @@ grass_status fetch_mgn(grass_ctx* c, bool reset_window, bool take_flag) {
   if (s != GRASS_OK) return s;
   CUDA_TRY(c, cudaMemcpyAsync(c->h_mgn, c->d_mgn, c->mgn_bytes, cudaMemcpyDeviceToHost, c->aux));
   if (reset_window) CUDA_TRY(c, cudaMemsetAsync(c->d_mgn, 0, 16 * (size_t)c->nl, c->aux));
-  if (take_flag) CUDA_TRY(c, cudaMemsetAsync(c->st.flag, 0, sizeof(int), c->aux));
+  if (take_flag) CUDA_TRY(c, cudaMemsetAsync(c->st.flag, 0, sizeof(int), c->aux));  // (P2P error stays)
   CUDA_TRY(c, cudaStreamSynchronize(c->aux));
   for (auto& pe : c->ev_pending) c->ev_free_list.push_back(pe.second);
   c->ev_pending.clear();
@@ -242,6 +254,9 @@ int h_flag(const grass_ctx* c) {
 }
 
 grass_status report_flag(grass_ctx* c) {
+  const int p2p_err = *reinterpret_cast<const int*>(static_cast<const char*>(c->h_mgn) + 16 * (size_t)c->nl + 4);
+  if (p2p_err)
+    return c->fail(GRASS_E_CUDA, "P2P barrier timed out: a peer rank never arrived (the context is unusable)");
   const int enc = h_flag(c);
   if (enc == 0) return GRASS_OK;
   return c->fail(GRASS_E_NONFINITE, "non-finite gradient in layer " + std::to_string(flag_layer(enc)) +
@@ -284,7 +299,7 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
     return bad("unknown param_dtype");
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return bad("bad rank/world");
   if (cfg->world > 1) {
-    if (!cfg->nccl_unique_id) return bad("world > 1 needs nccl_unique_id");
+    if (!cfg->nccl_unique_id && cfg->dp_mode == GRASS_DP_NCCL) return bad("world > 1 needs nccl_unique_id");
     const int64_t q = (cfg->param_dtype == GRASS_DTYPE_BF16 ? 8 : 4) * (int64_t)cfg->world;
     for (int i = 0; i < cfg->n_layers; ++i)
       if (cfg->layer_numel[i] % q != 0)
@@ -298,6 +313,13 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
       return bad("unknown residency");
     if (cfg->cache_layers < 0 || cfg->cache_layers > nsamp)
       return bad("cache_layers must lie in [0, N_L]");
+  }
+  if (cfg->dp_mode != GRASS_DP_NCCL && cfg->dp_mode != GRASS_DP_P2P) return bad("unknown dp_mode");
+  if (cfg->dp_mode == GRASS_DP_P2P) {
+    if (cfg->world > kMaxPeers) return bad("GRASS_DP_P2P supports world <= 8");
+    if (cfg->nccl_unique_id) return bad("GRASS_DP_P2P does not use NCCL: nccl_unique_id must be NULL");
+    if (cfg->max_grad_norm > 0.0) return bad("GRASS_DP_P2P does not support clipping");
+    if (cfg->p2p_sync != 0 && cfg->p2p_sync != 1) return bad("p2p_sync must be 0 or 1");
   }
   if (!(cfg->max_grad_norm >= 0.0) || !std::isfinite(cfg->max_grad_norm))
     return bad("max_grad_norm must be finite and >= 0");
@@ -322,6 +344,29 @@ AddressRangeFn address_range_fn() {
     return reinterpret_cast<AddressRangeFn>(f);
   }();
   return fn;
+}
+
+// A buffer of `need` bytes the context's kernels access: 16-byte aligned device
+// memory of the context's GPU whose allocation holds `need` bytes from p.
+grass_status check_device_buffer(grass_ctx* c, const void* p, unsigned long long need, const std::string& what) {
+  if (!p) return c->fail(GRASS_E_INVALID, "NULL buffer pointer (" + what + ")");
+  if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+    return c->fail(GRASS_E_INVALID, "layer buffers must be 16-byte aligned (" + what + ")");
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return c->fail(GRASS_E_INVALID, "not a CUDA pointer (" + what + ")");
+  }
+  if (!(at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) || at.device != c->cfg.device)
+    return c->fail(GRASS_E_INVALID, "layer buffers must be device memory on the context's GPU (" + what + ")");
+  if (AddressRangeFn fn = address_range_fn()) {
+    unsigned long long base = 0;
+    size_t size = 0;
+    const unsigned long long ptr = reinterpret_cast<uintptr_t>(p);
+    if (fn(&base, &size, ptr) == 0 && ptr + need > base + size)
+      return c->fail(GRASS_E_INVALID, "buffer of " + what + " is smaller than its N_p elements");
+  }
+  return GRASS_OK;
 }
 
 // Resolve, validate and order the layer list of a hot-path call.
@@ -354,7 +399,7 @@ grass_status check_call(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_
         return c->fail(GRASS_E_INVALID, "not a CUDA pointer");
       }
       if (a == p2 && host_p2 && at.type == cudaMemoryTypeHost) {
-        if (c->dp || (c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD))
+        if (c->dp || c->p2p || (c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD))
           return c->fail(GRASS_E_INVALID, "host gradients need world = 1 and resident or per-step "
                                           "offloaded optimizer states");
         (*host_p2)[i] = 1;  // pinned host gradient: streamed through the gradient ring
@@ -397,7 +442,8 @@ Batch make_batch(const grass_ctx* c, int32_t mode) {
   b.bf16 = c->bf16 ? 1 : 0;
   // DP: the kernels read reduce-scattered SUMS; x 1/W makes them the average
   // (exact for power-of-two W)
-  b.gscale = c->dp ? (float)(1.0 / (double)c->cfg.world) : 1.0f;
+  b.gscale = (c->dp || c->p2p) ? (float)(1.0 / (double)c->cfg.world) : 1.0f;
+  b.npeer = c->p2p ? c->cfg.world : 0;
   return b;
 }
 
@@ -439,6 +485,12 @@ Seg range_seg(const grass_ctx* c, int l, const void* g, int64_t off, int64_t n) 
   s.part_layer_base = c->part_base[l];
   s.part_index = c->part_base[l] + off / kTile;
   s.layer_numel = c->numel[l];
+  if (c->p2p) {  // the kernel reads every rank's gradient, writes every rank's parameters
+    const int W = c->cfg.world;
+    s.gpeer = const_cast<const void* const*>(c->d_ptab + (size_t)l * 2 * W);
+    s.tpeer = c->d_ptab + (size_t)l * 2 * W + W;
+    s.poff = c->shard_off[l] + off;
+  }
   return s;
 }
 
@@ -487,6 +539,87 @@ grass_status cross_rank_finish(grass_ctx* c, const int32_t* ids, const std::vect
     c->launches++;
   }
   return GRASS_OK;
+}
+
+// ---- P2P data parallelism -----------------------------------
+// The call's buffers must be the registered ones (the peers read / write them).
+grass_status p2p_check(grass_ctx* c, const int32_t* ids, int32_t n, void* const* params,
+                       const void* const* grads) {
+  if ((int)c->exch_peer.size() != c->cfg.world)
+    return c->fail(GRASS_E_STATE, "GRASS_DP_P2P: call grass_p2p_attach first");
+  if (!c->p2p_pending.empty())
+    return c->fail(GRASS_E_STATE, "p2p_sync = 0: call grass_p2p_finish for the previous call first");
+  for (int i = 0; i < n; ++i) {
+    const int l = ids[i];
+    if (!c->own_g[l]) return c->fail(GRASS_E_STATE, "layer " + std::to_string(l) + " is not registered");
+    if (grads[i] != c->own_g[l] || (params && params[i] != c->own_p[l]))
+      return c->fail(GRASS_E_INVALID, "GRASS_DP_P2P: pass the buffers registered for layer " + std::to_string(l));
+  }
+  return GRASS_OK;
+}
+
+P2PSyncArgs p2p_args(grass_ctx* c, int32_t which) {
+  P2PSyncArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int q = 0; q < c->cfg.world; ++q) a.exch[q] = c->exch_peer[q];
+  a.rank = c->cfg.rank;
+  a.world = c->cfg.world;
+  a.which = which;
+  if (which >= 0) a.epoch = ++c->epoch[which];
+  a.err = reinterpret_cast<int*>(static_cast<char*>(c->d_mgn) + 16 * (size_t)c->nl + 4);
+  return a;
+}
+
+// Start of a P2P call: every rank's gradients are final (and every rank has
+// finished reading its gather rows of the previous call).
+grass_status p2p_start(grass_ctx* c, cudaStream_t s) {
+  if (!c->cfg.p2p_sync) return GRASS_OK;
+  TraceScope ts(c, s, GRASS_TRACE_P2P, -1, 0, 0);
+  CUDA_TRY(c, launch_p2p_sync(p2p_args(c, 0), s));
+  c->launches++;
+  return GRASS_OK;
+}
+
+// Fixed ascending-rank sum of the gather rows -> MGN (as cross_rank_finish).
+grass_status p2p_finish_layers(grass_ctx* c, const std::vector<int32_t>& layers, cudaStream_t s) {
+  const int n = (int)layers.size();
+  const double* gathered = reinterpret_cast<const double*>(c->d_exch + kExchGather);
+  for (int j0 = 0; j0 < n; j0 += kMaxSeg) {
+    RankSumArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.world = c->cfg.world;
+    a.total_slots = n;
+    a.slot0 = j0;
+    a.n = std::min(kMaxSeg, n - j0);
+    for (int j = 0; j < a.n; ++j) {
+      a.layer[j] = layers[j0 + j];
+      a.numel[j] = c->numel[a.layer[j]];
+    }
+    CUDA_TRY(c, launch_rank_sum(gathered, a, c->st, s));
+    c->launches++;
+  }
+  return GRASS_OK;
+}
+
+// End of a P2P call: publish this rank's shard norms into every rank's gather
+// row, end barrier (all ranks' updates and theta' stores complete), then the
+// rank-order sum (p2p_sync = 1) or leave it to grass_p2p_finish.
+grass_status p2p_end(grass_ctx* c, const int32_t* ids, const std::vector<int>& order, cudaStream_t s) {
+  std::vector<int32_t> layers(order.size());
+  for (size_t j = 0; j < order.size(); ++j) layers[j] = ids[order[j]];
+  {
+    P2PSyncArgs a = p2p_args(c, c->cfg.p2p_sync ? 1 : -1);
+    a.n = (int32_t)layers.size();
+    a.shard_ss = c->st.shard_ss;
+    TraceScope ts(c, s, GRASS_TRACE_P2P, -1, 0, a.n);
+    CUDA_TRY(c, launch_p2p_sync(a, s));
+    c->launches++;
+  }
+  if (!c->cfg.p2p_sync) {
+    c->p2p_pending = layers;
+    return GRASS_OK;
+  }
+  return p2p_finish_layers(c, layers, s);
 }
 
 // ---- data-parallel schedule on the comm stream --------------
@@ -866,6 +999,8 @@ void free_ctx(grass_ctx* c) {
   dfree(c->d_gring);
   dfree(c->d_cache);
   dfree(c->always_block);
+  dfree(c->d_exch);
+  dfree(c->d_ptab);
   if (c->state_block) {
     if (c->cfg.offload)
       cudaFreeHost(c->state_block);
@@ -1009,7 +1144,16 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   }
 
   CUDA_TRY(c, dalloc((void**)&c->d_coef, sizeof(float)));
-  c->dp = W > 1 || cfg->nccl_unique_id != nullptr;
+  c->p2p = cfg->dp_mode == GRASS_DP_P2P;
+  if (c->p2p) {
+    // its own allocation, so that it can be exported through CUDA IPC
+    c->exch_bytes = (size_t)kExchGather + sizeof(double) * (size_t)W * c->nl;
+    CUDA_TRY(c, dalloc((void**)&c->d_exch, c->exch_bytes));
+    CUDA_TRY(c, dalloc((void**)&c->d_ptab, sizeof(void*) * 2 * (size_t)W * c->nl));
+    c->own_g.assign(c->nl, nullptr);
+    c->own_p.assign(c->nl, nullptr);
+  }
+  c->dp = !c->p2p && (W > 1 || cfg->nccl_unique_id != nullptr);
   if (c->dp) {
     CUDA_TRY(c, dalloc((void**)&c->d_gather, sizeof(double) * (size_t)W * c->nl));
     // two shard buffers for the RS || update overlap; clipping keeps every
@@ -1042,7 +1186,21 @@ grass_status mgn_accumulate_impl(grass_ctx* c, bool bf16_call, const int32_t* id
   if (s != GRASS_OK) return s;
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (!c->dp) {
+  if (c->p2p) {
+    // start barrier -> K1 over the sum of every rank's gradient (peer reads) -> publish + end barrier
+    if ((s = p2p_check(c, ids, n, nullptr, grads)) != GRASS_OK) return s;
+    if ((s = p2p_start(c, st)) != GRASS_OK) return s;
+    Batch b = make_batch(c, kFinalizeShard);
+    for (int j = 0; j < (int)order.size(); ++j) {
+      const int l = ids[order[j]];
+      if (b.nseg == kMaxSeg && (s = flush(c, &b, false, st)) != GRASS_OK) return s;
+      Seg sg = range_seg(c, l, elem(grads[order[j]], c->shard_off[l], c->esz), 0, c->shard_len[l]);
+      sg.out_slot = j;
+      push_seg(&b, sg);
+    }
+    if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
+    if ((s = p2p_end(c, ids, order, st)) != GRASS_OK) return s;
+  } else if (!c->dp) {
     Batch b = make_batch(c, kFinalizeMgn);
     for (int i : order) {
       if (b.nseg == kMaxSeg && (s = flush(c, &b, false, st)) != GRASS_OK) return s;
@@ -1095,9 +1253,11 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   }
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const bool sharded = c->dp;
+  const bool sharded = c->dp;  // NCCL data parallelism
+  const bool p2p = c->p2p;     // P2P data parallelism: one fused kernel, no NCCL
   const bool clip = c->cfg.max_grad_norm > 0.0;
-  const int32_t mode = clip ? kFinalizeNone : (sharded ? kFinalizeShard : kFinalizeMgn);
+  const int32_t mode = clip ? kFinalizeNone : ((sharded || p2p) ? kFinalizeShard : kFinalizeMgn);
+  if (p2p && (s = p2p_check(c, ids, n, params, grads)) != GRASS_OK) return s;
   const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
   const int nact = (int)order.size();
   int ncached = 0;
@@ -1152,6 +1312,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     // write-backs read cache slots last written by earlier steps' updates
     if (c->cfg.overlap && (s = wait_pending(c, c->d2h)) != GRASS_OK) return s;
   }
+  if (p2p && (s = p2p_start(c, st)) != GRASS_OK) return s;
   Batch b = make_batch(c, mode);
   if (sharded) {
     if ((s = comm_begin(c, st)) != GRASS_OK) return s;
@@ -1164,7 +1325,9 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     c->master_valid[l] = 1;
     const int64_t off = c->shard_off[l], len = c->shard_len[l];
     const void* g = grads[i];
-    if (sharded && clip) {
+    if (p2p) {
+      g = elem(grads[i], off, c->esz);  // this rank's range (the kernel sums every rank's via Seg::gpeer)
+    } else if (sharded && clip) {
       g = gs_slot(c, j);  // averaged in pass 1
     } else if (sharded) {
       if (j + 1 < nact) {  // N1 of the next layer overlaps this layer's update
@@ -1212,6 +1375,16 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     if (sharded && (s = comm_after_update(c, j, params[i], off, len, st)) != GRASS_OK) return s;  // N2
   }
   if ((s = flush(c, &b, true, st)) != GRASS_OK) return s;
+  if (p2p) {
+    if (c->cfg.offload && c->cfg.overlap) {  // the barrier signals after the last write-back
+      cudaEvent_t e = take_event(c);
+      if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
+      CUDA_TRY(c, cudaEventRecord(e, c->d2h));
+      CUDA_TRY(c, cudaStreamWaitEvent(st, e, 0));
+      c->ev_free_list.push_back(e);
+    }
+    if ((s = p2p_end(c, ids, order, st)) != GRASS_OK) return s;
+  }
   if (sharded && (s = comm_end(c, st)) != GRASS_OK) return s;
   if (sharded && !clip && (s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
   if (c->cfg.offload && c->cfg.overlap) {
@@ -1766,6 +1939,127 @@ grass_status grass_nccl_get_unique_id(void* out) try {
   if (!out) return set_thread_err(GRASS_E_INVALID, "out is NULL");
   std::string err;
   if (!nccl_unique_id(out, &err)) return set_thread_err(GRASS_E_NCCL, err);
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
+}
+
+// ----- P2P data parallelism ---------------------------------------------------
+grass_status grass_p2p_exchange_block(grass_ctx* c, void** ptr, int64_t* bytes) try {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!c->p2p) return c->fail(GRASS_E_STATE, "not a GRASS_DP_P2P context");
+  if (ptr) *ptr = c->d_exch;
+  if (bytes) *bytes = (int64_t)c->exch_bytes;
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
+}
+
+grass_status grass_p2p_attach(grass_ctx* c, void* const* blocks) try {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!c->p2p) return c->fail(GRASS_E_STATE, "not a GRASS_DP_P2P context");
+  if (!blocks) return c->fail(GRASS_E_INVALID, "blocks is NULL");
+  const int W = c->cfg.world;
+  for (int q = 0; q < W; ++q)
+    if (!blocks[q] || reinterpret_cast<uintptr_t>(blocks[q]) % 16 != 0)
+      return c->fail(GRASS_E_INVALID, "every exchange block address must be non-NULL and 16-byte aligned");
+  if (blocks[c->cfg.rank] != c->d_exch)
+    return c->fail(GRASS_E_INVALID, "blocks[rank] must be this context's own exchange block");
+  c->exch_peer.assign(W, nullptr);
+  for (int q = 0; q < W; ++q) c->exch_peer[q] = static_cast<char*>(blocks[q]);
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
+}
+
+grass_status grass_p2p_register_layer(grass_ctx* c, int32_t layer, void* const* params, const void* const* grads) try {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!c->p2p) return c->fail(GRASS_E_STATE, "not a GRASS_DP_P2P context");
+  if (layer < 0 || layer >= c->nl) return c->fail(GRASS_E_INVALID, "layer id out of range");
+  if (!params || !grads) return c->fail(GRASS_E_INVALID, "params/grads is NULL");
+  const int W = c->cfg.world, r = c->cfg.rank;
+  const unsigned long long need = (unsigned long long)c->numel[layer] * c->esz;
+  grass_status s;
+  if ((s = check_device_buffer(c, params[r], need, "own parameters")) != GRASS_OK) return s;
+  if ((s = check_device_buffer(c, grads[r], need, "own gradients")) != GRASS_OK) return s;
+  std::vector<void*> tab(2 * (size_t)W);
+  for (int q = 0; q < W; ++q) {
+    if (!params[q] || !grads[q] || reinterpret_cast<uintptr_t>(params[q]) % 16 != 0 ||
+        reinterpret_cast<uintptr_t>(grads[q]) % 16 != 0)
+      return c->fail(GRASS_E_INVALID, "peer buffers must be non-NULL and 16-byte aligned");
+    tab[q] = const_cast<void*>(grads[q]);
+    tab[W + q] = params[q];
+  }
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  if ((s = drain(c, false)) != GRASS_OK) return s;  // no kernel in flight reads the table
+  CUDA_TRY(c, cudaMemcpy(c->d_ptab + (size_t)layer * 2 * W, tab.data(), sizeof(void*) * tab.size(),
+                         cudaMemcpyHostToDevice));
+  c->own_g[layer] = grads[r];
+  c->own_p[layer] = params[r];
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
+}
+
+grass_status grass_p2p_finish(grass_ctx* c, void* stream) try {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!c->p2p || c->cfg.p2p_sync) return c->fail(GRASS_E_STATE, "grass_p2p_finish is for p2p_sync = 0");
+  if (c->p2p_pending.empty()) return c->fail(GRASS_E_STATE, "no pending P2P call");
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<int32_t> layers;
+  layers.swap(c->p2p_pending);
+  grass_status s = p2p_finish_layers(c, layers, st);
+  if (s != GRASS_OK) return s;
+  return mark_pending(c, st);
+} catch (...) {
+  return api_exception(c);
+}
+
+grass_status grass_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out) try {
+  if (!ptr || !handle_out || !offset_out) return set_thread_err(GRASS_E_INVALID, "NULL argument");
+  AddressRangeFn fn = address_range_fn();
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (!fn || fn(&base, &size, reinterpret_cast<uintptr_t>(ptr)) != 0)
+    return set_thread_err(GRASS_E_INVALID, "not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_thread_err(GRASS_E_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  }
+  static_assert(sizeof(h) == GRASS_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - base);
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
+}
+
+grass_status grass_ipc_import(int32_t device, const void* handle, int64_t offset, void** ptr_out) try {
+  if (!handle || !ptr_out || offset < 0) return set_thread_err(GRASS_E_INVALID, "bad argument");
+  static std::mutex mu;
+  static std::map<std::pair<int, std::string>, char*> opened;  // each allocation opened once per process
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair((int)device, std::string(static_cast<const char*>(handle), GRASS_IPC_HANDLE_BYTES));
+  auto it = opened.find(key);
+  if (it == opened.end()) {
+    if (cudaSetDevice(device) != cudaSuccess) {
+      cudaGetLastError();
+      return set_thread_err(GRASS_E_INVALID, "bad device");
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return set_thread_err(GRASS_E_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    }
+    it = opened.emplace(key, static_cast<char*>(p)).first;
+  }
+  *ptr_out = it->second + offset;
   return GRASS_OK;
 } catch (...) {
   return api_exception(nullptr);

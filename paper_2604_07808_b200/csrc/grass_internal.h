@@ -53,6 +53,14 @@ struct Seg {
   // bf16 model copy (updated as RNE(master')) and the bf16 gradient
   uint16_t* theta16;
   const uint16_t* g16;
+  // P2P data parallelism (Batch::npeer > 0): the gradient is
+  // the sum over every rank's full-layer buffer and theta' is stored into every
+  // rank's buffer (peer-mapped addresses); element idx of this range is
+  // element poff + idx of the full layer.  The local theta / m / v above are
+  // this rank's shard as usual.
+  const void* const* gpeer;  // device [npeer]: full-layer gradient of each rank
+  void* const* tpeer;        // device [npeer]: full-layer parameters of each rank
+  int64_t poff;
 };
 
 struct Batch {
@@ -64,6 +72,7 @@ struct Batch {
   const float* coef;       // device scalar multiplying g in the update (clipping), or NULL
   int32_t bf16;            // 1: bf16 gradients / parameters with fp32 master (Seg::g16, theta16)
   float gscale;            // multiplies every gradient element on load (DP: 1/world), else 1
+  int32_t npeer;           // P2P: ranks whose gradients are summed (Seg::gpeer), else 0
 };
 
 // Device-resident MGN / reduction state (all arrays indexed by layer id unless noted).
@@ -101,6 +110,25 @@ struct ClipArgs {
   int32_t layer[kMaxClipLayers];
 };
 cudaError_t launch_clip_coef(const ClipArgs& a, const DevState& st, float* coef, cudaStream_t s);
+
+// ----- P2P data parallelism --------------------
+// Every rank owns an "exchange block" in its HBM, mapped into every peer:
+//   [0, 8*kMaxPeers)              start-barrier flags, one u64 per sending rank
+//   [8*kMaxPeers, 16*kMaxPeers)   end-barrier flags
+//   [kExchGather, ...)            gather rows: row r = rank r's shard squared
+//                                 norms of the current call (fp64)
+constexpr int kMaxPeers = 8;
+constexpr int64_t kExchGather = 16 * kMaxPeers;
+struct P2PSyncArgs {
+  char* exch[kMaxPeers];   // every rank's exchange block (valid addresses in this process)
+  int32_t rank, world;
+  int32_t n;               // shard norms to publish into every rank's row `rank` (0 = none)
+  int32_t which;           // barrier: 0 = start, 1 = end, -1 = none
+  uint64_t epoch;          // value every rank signals for this barrier
+  const double* shard_ss;  // [n] this rank's shard squared norms
+  int* err;                // set to 1 if a peer never arrives (timeout)
+};
+cudaError_t launch_p2p_sync(const P2PSyncArgs& a, cudaStream_t s);
 
 // host_policy.cpp
 uint64_t splitmix64(uint64_t x);

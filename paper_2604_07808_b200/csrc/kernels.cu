@@ -160,17 +160,6 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// Bulk-stores the theta, m, v results of one unit from its stage.
-__device__ __forceinline__ void store_unit(const Seg& sg, int64_t e0, uint32_t bytes, const float* stage,
-                                           int unit) {
-  if (bytes) {
-    bulk_store(sg.theta + e0, stage + unit, bytes);
-    bulk_store(sg.m + e0, stage + 2 * unit, bytes);
-    bulk_store(sg.v + e0, stage + 3 * unit, bytes);
-    bulk_commit();
-  }
-}
-
 // Barrier over the consumer warps only (the producer warp never waits on it).
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
@@ -252,6 +241,53 @@ __global__ void grass_rank_sum_kernel(const double* __restrict__ gathered,
   }
 }
 
+// P2P publication + barrier (one CTA).  Publishes this rank's shard norms into
+// row `rank` of every rank's gather block, then (which >= 0) signals flag
+// [which][rank] = epoch in every rank's block and waits until every rank has
+// signalled this rank's flags [which][*].  The signal is a system-scope release
+// after a system fence, the wait a system-scope acquire, so writes issued
+// before it (the fused kernel's peer stores of theta', the published norms)
+// are visible to every rank after it.  A peer that never arrives (crashed
+// rank) ends the wait after kP2PTimeoutNs with err = 1 (surfaced by the next
+// synchronising call) instead of hanging the GPU.
+constexpr unsigned long long kP2PTimeoutNs = 60ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__global__ void grass_p2p_sync_kernel(const __grid_constant__ P2PSyncArgs a) {
+  const int tid = threadIdx.x;
+  for (int k = tid; k < a.world * a.n; k += blockDim.x) {
+    const int q = k / a.n, j = k % a.n;
+    double* row = reinterpret_cast<double*>(a.exch[q] + kExchGather) + (int64_t)a.rank * a.n;
+    row[j] = a.shard_ss[j];
+  }
+  if (a.which < 0) return;
+  __syncthreads();
+  if (tid < a.world) {
+    __threadfence_system();
+    unsigned long long* peer_flag =
+        reinterpret_cast<unsigned long long*>(a.exch[tid]) + a.which * kMaxPeers + a.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer_flag), "l"((unsigned long long)a.epoch)
+                 : "memory");
+    const unsigned long long* mine =
+        reinterpret_cast<const unsigned long long*>(a.exch[a.rank]) + a.which * kMaxPeers + tid;
+    const unsigned long long t0 = global_ns();
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+      if (v >= a.epoch) break;
+      if (global_ns() - t0 > kP2PTimeoutNs) {
+        atomicExch(a.err, 1);
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const DevState st,
                                        float* coef) {
   if (threadIdx.x != 0) return;
@@ -273,13 +309,13 @@ __global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const
 constexpr int kUpdTPS = 1, kUpdStages = GRASS_UPD_STAGES;  // 4 arrays x 16 KiB per stage -> 128 KiB ring
 constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 96 KiB x 2 -> 192 KiB
 
-template <bool U, int TPS, int ST, bool BF16>
+template <bool U, int TPS, int ST, bool BF16, bool P2P = false>
 cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStream_t s) {
   constexpr size_t smem = (size_t)ST * StageLayout<U, BF16, TPS>::bytes;
   static_assert(smem <= 227 * 1024, "ring exceeds the 227 KiB shared-memory limit");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grass_stream_kernel<U, TPS, ST, BF16>,
+    cudaError_t e = cudaFuncSetAttribute(grass_stream_kernel<U, TPS, ST, BF16, P2P>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -287,7 +323,7 @@ cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStre
   int units = 0;
   for (int i = 0; i < b.nseg; ++i) units += (b.seg[i].tiles + TPS - 1) / TPS;
   const int g = grid < units ? grid : units;
-  grass_stream_kernel<U, TPS, ST, BF16><<<g, kStreamThreads, smem, s>>>(b, st);
+  grass_stream_kernel<U, TPS, ST, BF16, P2P><<<g, kStreamThreads, smem, s>>>(b, st);
   return cudaGetLastError();
 }
 
@@ -296,6 +332,13 @@ cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStre
 cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int grid,
                          cudaStream_t s) {
   if (b.nseg <= 0 || b.tile_prefix[b.nseg] <= 0) return cudaSuccess;
+  if (b.npeer > 0) {  // P2P data parallelism: one tile per unit, the gradient read from the peers
+    if (b.bf16)
+      return update ? launch_stream<true, 1, kUpdStages, true, true>(b, st, grid, s)
+                    : launch_stream<false, 1, 2, true, true>(b, st, grid, s);
+    return update ? launch_stream<true, 1, kUpdStages, false, true>(b, st, grid, s)
+                  : launch_stream<false, 1, 2, false, true>(b, st, grid, s);
+  }
   if (b.bf16)
     return update ? launch_stream<true, kUpdTPS, kUpdStages, true>(b, st, grid, s)
                   : launch_stream<false, kNormTPS, kNormStages, true>(b, st, grid, s);
@@ -307,6 +350,11 @@ cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const 
                             cudaStream_t s) {
   if (a.n <= 0) return cudaSuccess;
   grass_rank_sum_kernel<<<1, 64, 0, s>>>(gathered, a, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_sync(const P2PSyncArgs& a, cudaStream_t s) {
+  grass_p2p_sync_kernel<<<1, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -14,6 +14,12 @@
 //                  parameter, 2 B, instead), m, v (4 B each) and writes master,
 //                  m, v (4 B each) and the bf16 parameter RNE(master') (2 B):
 //                  28 B/param; K1 reads 2 B/param.
+//   P2P     true: data-parallel step over peer memory: the
+//           consumers read the gradient of every rank straight from its HBM
+//           (NVLink) and sum them in ascending rank order, and the producer
+//           bulk-stores theta' into every rank's parameter buffer — the
+//           reduce-scatter, the update and the all-gather in one kernel, tile
+//           by tile.  Each rank updates only its own element shard.
 //
 // Stage layout (bytes, every region 16-byte aligned):
 //   [g: kUnit*GB][theta/master: kUnit*4][m: kUnit*4][v: kUnit*4][bf16 theta: kUnit*2 (BF16)]
@@ -67,20 +73,61 @@ __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
   return BF16 ? bf2f(sg.g16[idx]) : sg.g[idx];
 }
 
+// P2P (Seg::gpeer): the gradient at full-layer element idx is the sum of the
+// npeer ranks' gradients in ascending rank order (fp32), read straight from
+// their HBM over NVLink.  `gp` holds the ranks' full-layer gradient pointers.
+template <bool BF16>
+__device__ __forceinline__ float4 peer_g4(const void* const* gp, int npeer, int64_t idx) {
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int q = 0; q < kMaxPeers; ++q) {
+    if (q < npeer) {
+      const float4 x = BF16 ? unpack_bf16x4(__ldg(reinterpret_cast<const uint2*>(
+                                  static_cast<const uint16_t*>(gp[q]) + idx)))
+                            : __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(gp[q]) + idx));
+      if (q == 0) {
+        a = x;
+      } else {
+        a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+      }
+    }
+  }
+  return a;
+}
+template <bool BF16>
+__device__ __forceinline__ float peer_g1(const void* const* gp, int npeer, int64_t idx) {
+  float a = 0.f;
+#pragma unroll
+  for (int q = 0; q < kMaxPeers; ++q) {
+    if (q >= npeer) break;
+    const float x = BF16 ? bf2f(static_cast<const uint16_t*>(gp[q])[idx]) : static_cast<const float*>(gp[q])[idx];
+    a = q == 0 ? x : a + x;
+  }
+  return a;
+}
+
 // Bulk-stores the results of one unit from its stage: master/theta, m, v
-// (and the bf16 parameter copy).
-template <bool BF16, class L>
-__device__ __forceinline__ void store_unit_t(const Seg& sg, int64_t e0, uint32_t nv, const char* stg) {
+// (and the bf16 parameter copy).  P2P: theta' (fp32) or the bf16 copy goes to
+// every rank's parameter buffer (this rank's included) over NVLink.
+template <bool BF16, bool P2P, class L>
+__device__ __forceinline__ void store_unit_t(const Seg& sg, int npeer, int64_t e0, uint32_t nv, const char* stg) {
   if (nv) {
-    bulk_store(sg.theta + e0, stg + L::o_t, nv * 4u);
+    if (BF16 || !P2P) bulk_store(sg.theta + e0, stg + L::o_t, nv * 4u);
     bulk_store(sg.m + e0, stg + L::o_m, nv * 4u);
     bulk_store(sg.v + e0, stg + L::o_v, nv * 4u);
-    if (BF16) bulk_store(sg.theta16 + e0, stg + L::o_tb, nv * 2u);
+    if (P2P) {
+      for (int q = 0; q < npeer; ++q) {
+        char* dst = static_cast<char*>(sg.tpeer[q]) + (sg.poff + e0) * (BF16 ? 2 : 4);
+        bulk_store(dst, stg + (BF16 ? L::o_tb : L::o_t), nv * (BF16 ? 2u : 4u));
+      }
+    } else if (BF16) {
+      bulk_store(sg.theta16 + e0, stg + L::o_tb, nv * 2u);
+    }
     bulk_commit();
   }
 }
 
-template <bool UPDATE, int TPS, int STAGES, bool BF16>
+template <bool UPDATE, int TPS, int STAGES, bool BF16, bool P2P>
 __global__ void __launch_bounds__(kStreamThreads, 1)
 grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   using L = StageLayout<UPDATE, BF16, TPS>;
@@ -129,7 +176,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         if (i >= STAGES) {
           mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
           if (TS) {
-            store_unit_t<BF16, L>(b.seg[pend_s[stage]], pend_e0[stage], pend_nv[stage], stg);
+            store_unit_t<BF16, P2P, L>(b.seg[pend_s[stage]], b.npeer, pend_e0[stage], pend_nv[stage], stg);
             if (!L::SEP) bulk_wait_read_all();  // stage reusable again
           }
         }
@@ -143,12 +190,14 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           pend_e0[stage] = e0;
           pend_nv[stage] = nv;
         }
-        if (nv) {
+        if (nv && (UPDATE || !P2P)) {
           const bool init = BF16 && UPDATE && sg.init_master;
-          const uint32_t tx = nv * (uint32_t)L::GB + (UPDATE ? nv * (init ? 2u : 4u) + 8u * nv : 0u);
+          // P2P: the consumers read the gradients from every rank directly
+          const uint32_t tx = (P2P ? 0u : nv * (uint32_t)L::GB) + (UPDATE ? nv * (init ? 2u : 4u) + 8u * nv : 0u);
           mbar_arrive_expect_tx(&full_bar[stage], tx);
-          bulk_load(stg + L::off_g, BF16 ? (const void*)(sg.g16 + e0) : (const void*)(sg.g + e0),
-                    nv * (uint32_t)L::GB, &full_bar[stage], pol);
+          if (!P2P)
+            bulk_load(stg + L::off_g, BF16 ? (const void*)(sg.g16 + e0) : (const void*)(sg.g + e0),
+                      nv * (uint32_t)L::GB, &full_bar[stage], pol);
           if (UPDATE) {
             if (init)
               bulk_load(stg + L::off_tb, sg.theta16 + e0, nv * 2u, &full_bar[stage], pol);
@@ -170,10 +219,14 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         for (int j = (n_units > STAGES ? n_units - STAGES : 0); j < n_units; ++j) {
           const int stage = j % STAGES;
           mbar_wait(&empty_bar[stage], (j / STAGES) & 1);
-          store_unit_t<BF16, L>(b.seg[pend_s[stage]], pend_e0[stage], pend_nv[stage],
-                                sbuf + (size_t)stage * L::bytes);
+          store_unit_t<BF16, P2P, L>(b.seg[pend_s[stage]], b.npeer, pend_e0[stage], pend_nv[stage],
+                                     sbuf + (size_t)stage * L::bytes);
         }
         bulk_wait_all();
+      }
+      if (P2P) {  // the peer writes are complete; order them before the end barrier's signal
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence_system();
       }
     }
     return;
@@ -198,9 +251,19 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     const int nv = ne & ~(L::vec - 1);  // bulk-copied prefix; the tail is read from HBM
     const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
     char* stg = sbuf + (size_t)stage * L::bytes;
+    const void* gp[kMaxPeers];   // P2P: every rank's full-layer gradient
+    void* tp[kMaxPeers];         // P2P: every rank's full-layer parameters
+    if (P2P) {
+#pragma unroll
+      for (int q = 0; q < kMaxPeers; ++q) {
+        gp[q] = q < b.npeer ? sg.gpeer[q] : nullptr;
+        tp[q] = q < b.npeer ? sg.tpeer[q] : nullptr;
+      }
+    }
+    const int64_t pe0 = P2P ? sg.poff + e0 : 0;  // full-layer index of the unit's element 0
     mbar_wait(&full_bar[stage], (i / STAGES) & 1);
     if (L::SEP) mbar_wait(&outfree_bar[stage], (i / STAGES) & 1);
-    if (!UPDATE && ne == kUnit) {
+    if (!UPDATE && !P2P && ne == kUnit) {
       // Full unit of the norm-only stream: branch-free, every shared-memory
       // read issued before the math.  Same element map and accumulation order
       // as the guarded path below.
@@ -241,7 +304,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           for (int q = 0; q < kUnroll; ++q) {
             const int e = k * (int)kTile + (q * kThreads + tid) * kVec;  // relative to e0
             if (e < nv) {
-              const float4 g4 = scale4(stage_g4<BF16>(stg + L::off_g, e), gs);
+              const float4 g4 = scale4(P2P ? peer_g4<BF16>(gp, b.npeer, pe0 + e) : stage_g4<BF16>(stg + L::off_g, e), gs);
               acc[0] = fma((double)g4.x, (double)g4.x, acc[0]);
               acc[1] = fma((double)g4.y, (double)g4.y, acc[1]);
               acc[2] = fma((double)g4.z, (double)g4.z, acc[2]);
@@ -261,10 +324,21 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
                   *reinterpret_cast<float4*>(stg + L::o_v + 4 * e) = v4;
                   if (BF16) *reinterpret_cast<uint2*>(stg + L::o_tb + 2 * e) = pack_bf16x4(t4);
                 } else {
-                  st_stream(sg.theta + e0 + e, t4);
+                  if (BF16 || !P2P) st_stream(sg.theta + e0 + e, t4);
                   st_stream(sg.m + e0 + e, m4);
                   st_stream(sg.v + e0 + e, v4);
-                  if (BF16) *reinterpret_cast<uint2*>(sg.theta16 + e0 + e) = pack_bf16x4(t4);
+                  if (P2P) {
+#pragma unroll
+                    for (int q = 0; q < kMaxPeers; ++q) {
+                      if (q >= b.npeer) break;
+                      if (BF16)
+                        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(tp[q]) + pe0 + e) = pack_bf16x4(t4);
+                      else
+                        st_stream(static_cast<float*>(tp[q]) + pe0 + e, t4);
+                    }
+                  } else if (BF16) {
+                    *reinterpret_cast<uint2*>(sg.theta16 + e0 + e) = pack_bf16x4(t4);
+                  }
                 }
               }
             } else if (e < ne) {
@@ -272,16 +346,27 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
               for (int j = 0; j < kVec; ++j) {
                 if (e + j < ne) {
                   const int64_t idx = e0 + e + j;
-                  const float g = seg_g<BF16>(sg, idx) * gs;
+                  const float g = (P2P ? peer_g1<BF16>(gp, b.npeer, pe0 + e + j) : seg_g<BF16>(sg, idx)) * gs;
                   acc[j] = fma((double)g, (double)g, acc[j]);
                   if (UPDATE) {
                     float th = init ? bf2f(sg.theta16[idx]) : sg.theta[idx];
                     float m = sg.m[idx], v = sg.v[idx];
                     adamw1(g, th, m, v, sc);
-                    sg.theta[idx] = th;
+                    sg.theta[idx] = th;  // P2P fp32: this rank's own buffer (also in tp below)
                     sg.m[idx] = m;
                     sg.v[idx] = v;
-                    if (BF16) sg.theta16[idx] = (uint16_t)f2bf(th);
+                    if (P2P) {
+#pragma unroll
+                      for (int q = 0; q < kMaxPeers; ++q) {
+                        if (q >= b.npeer) break;
+                        if (BF16)
+                          static_cast<uint16_t*>(tp[q])[pe0 + e + j] = (uint16_t)f2bf(th);
+                        else
+                          static_cast<float*>(tp[q])[pe0 + e + j] = th;
+                      }
+                    } else if (BF16) {
+                      sg.theta16[idx] = (uint16_t)f2bf(th);
+                    }
                   }
                 }
               }

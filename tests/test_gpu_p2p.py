@@ -1,0 +1,320 @@
+"""P2P data parallelism (cfg.dp_mode = GRASS_DP_P2P): one fused
+kernel reads every rank's gradient over peer memory, sums it in rank order,
+updates the rank's element shard and stores theta' into every rank's
+parameters; the shard norms are published into every rank's exchange block.
+
+The pool has one GPU, so the multi-rank cases run W contexts ("virtual
+ranks") on it with p2p_sync = 0: every buffer is local, the host orders the
+ranks' calls (all steps, then every rank's grass_p2p_finish), and no kernel
+ever waits on another.  The data path — peer-pointer loads, the rank-order
+sum, peer stores, the publication into every rank's gather row and the
+rank-order MGN sum — is exactly what runs across GPUs.  The two-process case
+does the same through CUDA IPC handles (grass_ipc_export / _import), the
+setup real ranks use.  world = 1 with p2p_sync = 1 also runs the device
+barrier kernel (trivially satisfied by the rank itself).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_07808_b200 as G
+from oracle import grass_oracle as O
+from synth import layer_grad, layer_params
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _np(t):
+    return t.detach().float().cpu().numpy()
+
+
+def dp_average_fp32(grads):
+    """The DP gradient as the P2P kernel (and an fp32 NCCL reduce-scatter) forms
+    it: fp32 sum in ascending rank order, then x fp32(1/W) (DESIGN R20).  It is
+    the INPUT the oracle's AdamW / Eq. 2 are fed; checked here against the fp64
+    mean of the oracle (O.dp_average) within fp32 summation error."""
+    acc = np.asarray(grads[0], np.float32).copy()
+    for g in grads[1:]:
+        acc = (acc + np.asarray(g, np.float32)).astype(np.float32)
+    out = (acc * np.float32(1.0 / len(grads))).astype(np.float32)
+    ref = O.dp_average(grads)
+    bound = len(grads) * 2.0 ** -23 * np.mean([np.abs(np.asarray(g, np.float64)) for g in grads], axis=0)
+    assert (np.abs(out - ref) <= bound + 1e-45).all()
+    return out
+
+
+def _mode_kw(mode, chunk=4096):
+    return {"resident": {}, "offload": dict(offload=True, chunk_elems=chunk),
+            "period": dict(offload=True, residency=G.RESIDENCY_PERIOD)}[mode]
+
+
+# ------------------------------------------------------------------ world = 1
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+@pytest.mark.parametrize("mode", ["resident", "offload", "period"])
+def test_p2p_one_rank_bit_identical_to_plain(dtype, mode):
+    """world = 1: the P2P kernels (peer-pointer gradient, peer stores, publish +
+    device barrier + rank sum) must reproduce the plain path bit for bit."""
+    tdt = torch.bfloat16 if dtype == G.DTYPE_BF16 else torch.float32
+    numel = [3 * 4096 + 8, 65_536, 4096 + 16]
+    kw = dict(gamma=2, weight_decay=0.01, param_dtype=dtype, **_mode_kw(mode))
+    ref = G.Grass(numel, **kw)
+    p2p = G.Grass(numel, dp_mode=G.DP_P2P, **kw)
+    blk, nbytes = p2p.p2p_exchange_block()
+    assert nbytes >= 128 + 8 * len(numel)
+    p2p.p2p_attach([blk])
+    p_ref = [layer_params(n, l, device=DEV).to(tdt) for l, n in enumerate(numel)]
+    p_p2p = [p.clone() for p in p_ref]
+    g_reg = [torch.zeros(n, device=DEV, dtype=tdt) for n in numel]     # registered gradient buffers
+    for l in range(len(numel)):
+        p2p.p2p_register_layer(l, [p_p2p[l]], [g_reg[l]])
+    for step in range(5):
+        ids = [[0, 1], [2, 0], [1, 2], [0, 2], [2, 1]][step]
+        for l in ids:
+            g_reg[l].copy_(layer_grad(numel[l], l, 1e-3, step=step, device=DEV).to(tdt))
+        ref.step_layers(ids, [p_ref[l] for l in ids], [g_reg[l] for l in ids], 1e-3)
+        p2p.step_layers(ids, [p_p2p[l] for l in ids], [g_reg[l] for l in ids], 1e-3)
+    for l in range(3):
+        g_reg[l].copy_(layer_grad(numel[l], l, 1e-3, step=9, device=DEV).to(tdt))
+    ref.mgn_accumulate([0, 1, 2], g_reg)
+    p2p.mgn_accumulate([0, 1, 2], g_reg)
+    ref.sync()
+    p2p.sync()
+    for l in range(3):
+        assert torch.equal(p_ref[l], p_p2p[l]), l
+        a, b = ref.read_state(l), p2p.read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+    sa, sb = ref.get_mgn(), p2p.get_mgn()
+    assert sa["S"] == sb["S"] and sa["c"] == sb["c"] and sa["last_ss"] == sb["last_ss"]
+
+
+def test_p2p_rejects_unregistered_and_misuse():
+    numel = [4096, 8192]
+    gr = G.Grass(numel, gamma=1, dp_mode=G.DP_P2P)
+    p = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    g = [torch.zeros(n, device=DEV) for n in numel]
+    with pytest.raises(G.GrassError, match="attach"):
+        gr.step_layers([0], [p[0]], [g[0]], 1e-3)
+    blk, _ = gr.p2p_exchange_block()
+    with pytest.raises(G.GrassError):
+        gr.p2p_attach([blk + 256])                      # not its own block
+    gr.p2p_attach([blk])
+    with pytest.raises(G.GrassError, match="not registered"):
+        gr.step_layers([0], [p[0]], [g[0]], 1e-3)
+    gr.p2p_register_layer(0, [p[0]], [g[0]])
+    other = torch.zeros(4096, device=DEV)
+    with pytest.raises(G.GrassError, match="registered"):
+        gr.step_layers([0], [p[0]], [other], 1e-3)     # a different gradient buffer
+    with pytest.raises(G.GrassError, match="aligned"):
+        gr.p2p_register_layer(1, [p[1].data_ptr() + 4], [g[1]])   # misaligned parameters
+    with pytest.raises(G.GrassError):
+        gr.p2p_finish()                                  # p2p_sync = 1 context
+    with pytest.raises(G.GrassError):
+        G.Grass(numel, gamma=1, dp_mode=G.DP_P2P, max_grad_norm=1.0)
+    with pytest.raises(G.GrassError):
+        G.Grass(numel, gamma=1, dp_mode=G.DP_P2P, world=9, rank=0)
+    gr.step_layers([0], [p[0]], [g[0]], 1e-3)
+    gr.sync()
+
+
+# --------------------------------------------- W virtual ranks on one GPU
+class VirtualRanks:
+    """W contexts (rank r of world W, p2p_sync = 0) whose buffers all live on
+    this GPU: rank r's parameters P[r][l] and gradients Gr[r][l]."""
+
+    def __init__(self, numel, W, dtype=G.DTYPE_FP32, **kw):
+        self.W, self.numel = W, numel
+        self.tdt = torch.bfloat16 if dtype == G.DTYPE_BF16 else torch.float32
+        self.ctx = [G.Grass(numel, rank=r, world=W, dp_mode=G.DP_P2P, p2p_sync=False,
+                            param_dtype=dtype, **kw) for r in range(W)]
+        blocks = [c.p2p_exchange_block()[0] for c in self.ctx]
+        base = [layer_params(n, l, device=DEV).to(self.tdt) for l, n in enumerate(numel)]
+        self.P = [[b.clone() for b in base] for _ in range(W)]
+        self.Gr = [[torch.zeros(n, device=DEV, dtype=self.tdt) for n in numel] for _ in range(W)]
+        for c in self.ctx:
+            c.p2p_attach(blocks)
+            for l in range(len(numel)):
+                c.p2p_register_layer(l, [self.P[r][l] for r in range(W)], [self.Gr[r][l] for r in range(W)])
+
+    def set_grads(self, ids, step, seed=0):
+        for r in range(self.W):
+            for l in ids:
+                self.Gr[r][l].copy_(layer_grad(self.numel[l], l, 1e-3, step=step, seed=seed, device=DEV,
+                                               rank=r).to(self.tdt))
+
+    def step(self, ids, lr):
+        for r, c in enumerate(self.ctx):          # every rank's fused kernel, in rank order
+            c.step_layers(ids, [self.P[r][l] for l in ids], [self.Gr[r][l] for l in ids], lr)
+        for c in self.ctx:                        # then every rank's MGN finish
+            c.p2p_finish()
+
+    def probe(self, ids):
+        for r, c in enumerate(self.ctx):
+            c.mgn_accumulate(ids, [self.Gr[r][l] for l in ids])
+        for c in self.ctx:
+            c.p2p_finish()
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_p2p_virtual_ranks_vs_oracle(W):
+    """W ranks: after each step every rank holds the same parameters (bit),
+    equal to the oracle's AdamW on the DP-averaged gradient within 1e-5; every
+    rank's MGN is bit-identical and within 1e-6 of the oracle's norms; each
+    rank's m/v are the oracle's for its element shard."""
+    numel = [8 * W * 1000 + 8 * W * 3, 65_536, 4096 * 3]
+    lr = 1e-3
+    vr = VirtualRanks(numel, W, gamma=2, weight_decay=0.01)
+    orc = O.GrassOracle(numel, gamma=2, weight_decay=0.01)
+    theta = [_np(vr.P[0][l]).copy() for l in range(3)]
+    for step in range(3):
+        ids = [[0, 1], [2, 0], [1, 2]][step]
+        vr.set_grads(ids, step)
+        gavg = {l: dp_average_fp32([_np(vr.Gr[r][l]) for r in range(W)]) for l in ids}
+        th_in = {l: theta[l].copy() for l in ids}
+        m_in = {l: orc.m[l].copy() for l in ids}
+        vr.step(ids, lr)
+        torch.cuda.synchronize()
+        orc.step_layers(ids, [theta[l] for l in ids], [gavg[l] for l in ids],
+                        float(np.float32(lr)))
+        for l in ids:
+            got = [_np(vr.P[r][l]) for r in range(W)]
+            for r in range(1, W):
+                assert np.array_equal(got[0], got[r]), (step, l, r)
+            scale = np.maximum(np.abs(theta[l]), np.abs(th_in[l]))
+            assert (np.abs(got[0] - theta[l]) <= 1e-5 * scale + 1e-30).all(), (step, l)
+            theta[l][...] = got[0]                 # re-seed the oracle from the GPU
+            for r, c in enumerate(vr.ctx):
+                off, cnt = G.shard_range(numel[l], W, r)
+                m, v, t = c.read_state(l)
+                assert t == orc.t[l]
+                sl = slice(off, off + cnt)
+                # scale of the rounding step's operands (tests/test_gpu_parity.py tolerances):
+                # m' = b1 m + (1-b1) g may cancel
+                s_m = np.maximum.reduce([np.abs(orc.m[l][sl]), np.abs(m_in[l][sl]), 0.1 * np.abs(gavg[l][sl])])
+                assert (np.abs(m - orc.m[l][sl]) <= 1e-5 * s_m + 1e-30).all(), (step, l, r)
+                assert (np.abs(v - orc.v[l][sl]) <= 1e-5 * np.abs(orc.v[l][sl]) + 1e-30).all(), (step, l, r)
+                orc.m[l][off:off + cnt], orc.v[l][off:off + cnt] = m, v
+    vr.set_grads([0, 1, 2], 7)
+    vr.probe([0, 1, 2])
+    orc.accumulate([0, 1, 2], [dp_average_fp32([_np(vr.Gr[r][l]) for r in range(W)]) for l in range(3)])
+    st = [c.get_mgn() for c in vr.ctx]
+    for r in range(1, W):
+        assert st[r]["S"] == st[0]["S"] and st[r]["c"] == st[0]["c"] and st[r]["last_ss"] == st[0]["last_ss"]
+    for l in range(3):
+        assert abs(st[0]["last_ss"][l] - orc.last_ss[l]) <= 1e-6 * orc.last_ss[l]
+    assert st[0]["c"] == orc.mgn.c
+
+
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+def test_p2p_virtual_ranks_offload_and_period_bit_identical(dtype):
+    """W = 4 virtual ranks: per-step offload and period residency give the
+    resident P2P result bit for bit (parameters, every rank's m/v, MGN)."""
+    W = 4
+    numel = [8 * W * 2048 + 8 * W, 65_536, 32 * 4096]
+    runs = []
+    for mode in ("resident", "offload", "period"):
+        vr = VirtualRanks(numel, W, dtype=dtype, gamma=2, weight_decay=0.01, **_mode_kw(mode, 8192))
+        for step in range(4):
+            ids = [[0, 1], [2, 0], [1, 2], [0, 2]][step]
+            vr.set_grads(ids, step, seed=3)
+            vr.step(ids, 1e-3)
+        torch.cuda.synchronize()
+        runs.append(vr)
+    for vr in runs[1:]:
+        for r in range(W):
+            for l in range(3):
+                assert torch.equal(runs[0].P[r][l], vr.P[r][l])
+                a, b = runs[0].ctx[r].read_state(l), vr.ctx[r].read_state(l)
+                assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2]
+            assert runs[0].ctx[r].get_mgn()["S"] == vr.ctx[r].get_mgn()["S"]
+
+
+def test_p2p_virtual_ranks_schedule_always_groups():
+    """The full schedule (probe, commit, sample, update) on 2 virtual ranks with
+    an always-active group: identical sampled ids and probabilities on both
+    ranks, always group updated every adaptive step."""
+    W = 2
+    numel = [8 * W * 512] * 4 + [8 * W * 100]
+    vr = VirtualRanks(numel, W, gamma=2, T_p=2, T_s=2, n_always=1, seed=11)
+    for step in range(8):
+        d = G.schedule_decision(step, 2, 2)
+        if d == G.DECIDE_PROBE:
+            vr.set_grads([0, 1, 2, 3], step)
+            vr.probe([0, 1, 2, 3])
+            continue
+        if d == G.DECIDE_COMMIT_RESAMPLE:
+            probs = [c.update_probs() for c in vr.ctx]
+            assert probs[0] == probs[1] and probs[0][4] == 0.0
+        ids = [c.sample_layers((step - 2) // 2) for c in vr.ctx]
+        assert ids[0] == ids[1] and 4 not in ids[0]
+        ids = ids[0] + [4]
+        vr.set_grads(ids, step)
+        vr.step(ids, 1e-3)
+    torch.cuda.synchronize()
+    assert vr.ctx[0].read_state(4)[2] == vr.ctx[1].read_state(4)[2] == 6
+    for l in range(5):
+        assert torch.equal(vr.P[0][l], vr.P[1][l])
+
+
+# ------------------------------------------ two processes, CUDA IPC setup
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ipc_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    numel = [8 * world * 1024 + 8 * world, 65_536]
+    gr = G.Grass(numel, gamma=2, rank=rank, world=world, dp_mode=G.DP_P2P, p2p_sync=False,
+                 weight_decay=0.01)
+    P = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    Gr = [layer_grad(n, l, 1e-3, step=0, device=DEV, rank=rank) for l, n in enumerate(numel)]
+    init = [_np(p).copy() for p in P]
+    gr.p2p_setup({l: (P[l], Gr[l]) for l in range(2)})   # IPC handles through the gloo group
+    torch.cuda.synchronize()
+    dist.barrier()
+    gr.step_layers([0, 1], P, Gr, 1e-3)                   # both processes' kernels may overlap:
+    torch.cuda.synchronize()                              # neither waits on the other
+    dist.barrier()                                        # every rank's publication is done
+    gr.p2p_finish()
+    gr.sync()
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), p0=_np(P[0]), p1=_np(P[1]), i0=init[0], i1=init[1],
+             g0=_np(Gr[0]), g1=_np(Gr[1]), S=np.array(gr.get_mgn()["S"]),
+             ss=np.array(gr.get_mgn()["last_ss"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_p2p_two_processes_ipc(tmp_path):
+    import torch.multiprocessing as mp
+    W = 2
+    mp.spawn(_ipc_worker, args=(W, _free_port(), str(tmp_path)), nprocs=W, join=True)
+    r = [np.load(tmp_path / f"r{q}.npz") for q in range(W)]
+    numel = [8 * W * 1024 + 8 * W, 65_536]
+    for l in range(2):
+        assert np.array_equal(r[0][f"p{l}"], r[1][f"p{l}"])   # theta' reached both processes
+        gavg = dp_average_fp32([r[q][f"g{l}"] for q in range(W)])
+        th0 = r[0][f"i{l}"]
+        assert np.array_equal(th0, r[1][f"i{l}"])
+        th, _, _ = O.adamw_step(th0, np.zeros_like(th0), np.zeros_like(th0), gavg, 1,
+                                float(np.float32(1e-3)), weight_decay=0.01)
+        scale = np.maximum(np.abs(th), np.abs(th0))
+        assert (np.abs(r[0][f"p{l}"] - th) <= 1e-5 * scale).all()
+        assert abs(r[0]["ss"][l] - O.sq_norm(gavg)) <= 1e-6 * O.sq_norm(gavg)
+    assert np.array_equal(r[0]["S"], r[1]["S"])
