@@ -42,7 +42,7 @@ METRIC = "active-layer params updated/s and offloaded step ms; % of HBM / host-l
 UNIT = "params/s"
 BYTES_PER_PARAM_UPDATE = 28      # read g, theta, m, v + write theta, m, v (fp32)
 BYTES_PER_PARAM_PROBE = 4        # read g
-DEFAULT_LEGS = "main,probe,offload,period,train,bf16,e2e,cpu"
+DEFAULT_LEGS = "main,probe,p2p,offload,period,train,bf16,e2e,cpu"
 FALLBACK_HBM_GBS = 6650.0        # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 
 
@@ -220,7 +220,7 @@ def run_grass(args, rank, world, local):
     if world > 1 and args.legs == DEFAULT_LEGS:
         # the north star's per-N numbers: resident step, e2e, and the offloaded
         # step (per-step round trip and period residency) on element shards
-        legs = {"main", "e2e", "offload", "period"}
+        legs = {"main", "e2e", "p2p", "offload", "period"}
     shape = MODELS[args.model]
     NL, n_p, gamma = shape.n_layers, shape.layer_numel, args.gamma
     sig = grad_sigmas(NL, 0)
@@ -346,6 +346,70 @@ def run_grass(args, rank, world, local):
     e2e = guarded("e2e", leg_e2e)
     ctx.close()                                 # frees its 51.8 GB of HBM state
     torch.cuda.empty_cache()
+
+    # ---- P2P data parallelism: the same step with ONE fused
+    # kernel per call reading every rank's gradient over peer memory and storing
+    # theta' into every rank (no NCCL on the data path).  At N > 1 the ranks'
+    # buffers are mapped through CUDA IPC.  Every rank takes the same branches:
+    # a failure on any rank is agreed on (all_reduce) before the next collective.
+    def all_ok(flag: bool) -> bool:
+        if world == 1:
+            return flag
+        t = torch.tensor([1 if flag else 0], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+        return bool(t.item())
+
+    def leg_p2p():
+        err = None
+        pctx = None
+        try:
+            pctx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, device=local,
+                           rank=rank, world=world, dp_mode=G.DP_P2P)
+            pctx.p2p_setup({l: (params[l], grads[l]) for l in range(NL)}) if world > 1 else None
+            if world == 1:
+                pctx.p2p_attach([pctx.p2p_exchange_block()[0]])
+                for l in range(NL):
+                    pctx.p2p_register_layer(l, [params[l]], [grads[l]])
+        except Exception as ex:
+            err = f"setup: {type(ex).__name__}: {ex}"[:300]
+        if not all_ok(err is None):
+            if pctx is not None:
+                pctx.close()
+            return {"error": err or "setup failed on another rank"}
+        pev = []
+        try:
+            pctx.mgn_accumulate(list(range(NL)), grads, stream=s)
+            pctx.update_probs()
+            pids = pctx.sample_layers(0)
+            for k in range(args.warmup + args.steps):
+                timed = k >= args.warmup
+                if timed:
+                    e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    e[0].record(s)
+                pctx.step_layers(pids, [params[l] for l in pids], [grads[l] for l in pids], args.lr, stream=s)
+                if timed:
+                    e[1].record(s)
+                    pev.append(e)
+                pctx.update_probs()
+                pids = pctx.sample_layers(k + 1)
+            torch.cuda.synchronize()
+            call_ms = statistics.mean(a.elapsed_time(b) for a, b in pev)
+        except Exception as ex:
+            err = f"run: {type(ex).__name__}: {ex}"[:300]
+            call_ms = 0.0
+        ok = all_ok(err is None)
+        call_ms = max_over_ranks(call_ms, world, dev)
+        pctx.close()
+        if not ok:
+            return {"error": err or "failed on another rank"}
+        hbm = BYTES_PER_PARAM_UPDATE * active / world          # per rank: local shard traffic
+        link = 8 * active * (world - 1) / world                 # per rank: peer grad reads + theta' stores
+        return {"workload": f"{args.model}-stack gamma={gamma}, P2P fused RS+update+AG kernel, dp{world}",
+                "call_ms": call_ms, "params_per_s": active / (call_ms / 1e3),
+                "hbm_GBps_per_rank": hbm / (call_ms / 1e3) / 1e9,
+                "nvlink_bytes_per_rank": link, "calls": len(pev)}
+
+    p2p = guarded("p2p", leg_p2p)
 
     # ---- offload leg: configs[2] (row a6)
     def leg_offload():
@@ -583,7 +647,7 @@ def run_grass(args, rank, world, local):
                          "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "probe": out.get("probe"), "offload": offload,
-            "offload_period": offload_period, "bf16": bf16, "train_step": train,
+            "offload_period": offload_period, "bf16": bf16, "train_step": train, "p2p": p2p,
         }
         if leg_errors:
             line["leg_errors"] = leg_errors

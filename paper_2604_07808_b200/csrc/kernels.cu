@@ -311,7 +311,10 @@ constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 96
 
 template <bool U, int TPS, int ST, bool BF16, bool P2P = false>
 cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStream_t s) {
-  constexpr size_t smem = (size_t)ST * StageLayout<U, BF16, TPS>::bytes;
+  constexpr size_t smem = (size_t)ST * StageLayout<U, BF16, TPS>::bytes +
+                         (P2P ? (size_t)P2PGSlots<BF16>::value * StageLayout<U, BF16, TPS>::kUnit *
+                                    StageLayout<U, BF16, TPS>::GB
+                              : 0);
   static_assert(smem <= 227 * 1024, "ring exceeds the 227 KiB shared-memory limit");
   static bool attr = false;
   if (!attr) {

@@ -73,27 +73,15 @@ __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
   return BF16 ? bf2f(sg.g16[idx]) : sg.g[idx];
 }
 
-// P2P (Seg::gpeer): the gradient at full-layer element idx is the sum of the
-// npeer ranks' gradients in ascending rank order (fp32), read straight from
-// their HBM over NVLink.  `gp` holds the ranks' full-layer gradient pointers.
+// P2P (Seg::gpeer): the gradient of a unit is the sum of the npeer ranks'
+// slices in ascending rank order (fp32).  The producer bulk-copies each rank's
+// slice (over NVLink for the peers) into a ring of P2PGSlots<BF16> gradient
+// slots; the consumers add the slices up in registers.  The 0-7 element tail of
+// a segment is summed straight from the ranks' memory (peer_g1).
 template <bool BF16>
-__device__ __forceinline__ float4 peer_g4(const void* const* gp, int npeer, int64_t idx) {
-  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-  for (int q = 0; q < kMaxPeers; ++q) {
-    if (q < npeer) {
-      const float4 x = BF16 ? unpack_bf16x4(__ldg(reinterpret_cast<const uint2*>(
-                                  static_cast<const uint16_t*>(gp[q]) + idx)))
-                            : __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(gp[q]) + idx));
-      if (q == 0) {
-        a = x;
-      } else {
-        a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
-      }
-    }
-  }
-  return a;
-}
+struct P2PGSlots {
+  static constexpr int value = BF16 ? 8 : 4;  // 4 x 16 KiB / 8 x 8 KiB next to the 2-stage ring
+};
 template <bool BF16>
 __device__ __forceinline__ float peer_g1(const void* const* gp, int npeer, int64_t idx) {
   float a = 0.f;
@@ -136,6 +124,12 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   __shared__ __align__(8) uint64_t full_bar[STAGES];
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
   __shared__ __align__(8) uint64_t outfree_bar[STAGES];  // L::SEP: output region writable
+  constexpr int NG = P2P ? P2PGSlots<BF16>::value : 1;     // P2P gradient ring
+  constexpr int kGSlot = kUnit * L::GB;
+  static_assert(!P2P || TPS == 1, "P2P units are one tile");
+  __shared__ __align__(8) uint64_t gfull_bar[NG];
+  __shared__ __align__(8) uint64_t gempty_bar[NG];
+  char* const gring = sbuf + (size_t)STAGES * L::bytes;
   __shared__ int unit_prefix[kMaxSeg + 1];
   __shared__ int seg_done[kMaxSeg];
   __shared__ double red[2][TPS][kConsumerWarps];
@@ -155,6 +149,10 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       mbar_init(&empty_bar[i], kConsumerWarps);
       mbar_init(&outfree_bar[i], 1);
     }
+    for (int i = 0; i < NG; ++i) {
+      mbar_init(&gfull_bar[i], 1);
+      mbar_init(&gempty_bar[i], kConsumerWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -169,7 +167,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       int pend_s[STAGES];
       int64_t pend_e0[STAGES];
       uint32_t pend_nv[STAGES];
-      int s = 0, i = 0;
+      int s = 0, i = 0, gcount = 0;
       for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
         const int stage = i % STAGES;
         char* stg = sbuf + (size_t)stage * L::bytes;
@@ -192,7 +190,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         }
         if (nv && (UPDATE || !P2P)) {
           const bool init = BF16 && UPDATE && sg.init_master;
-          // P2P: the consumers read the gradients from every rank directly
+          // P2P: the gradient slices go to the gradient ring (below)
           const uint32_t tx = (P2P ? 0u : nv * (uint32_t)L::GB) + (UPDATE ? nv * (init ? 2u : 4u) + 8u * nv : 0u);
           mbar_arrive_expect_tx(&full_bar[stage], tx);
           if (!P2P)
@@ -208,6 +206,16 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           }
         } else {
           mbar_arrive(&full_bar[stage]);
+        }
+        if (P2P && nv) {  // every rank's gradient slice of this unit, in rank order
+          for (int r = 0; r < b.npeer; ++r, ++gcount) {
+            const int gsl = gcount % NG;
+            if (gcount >= NG) mbar_wait(&gempty_bar[gsl], ((gcount / NG) & 1) ^ 1);
+            mbar_arrive_expect_tx(&gfull_bar[gsl], nv * (uint32_t)L::GB);
+            bulk_load(gring + (size_t)gsl * kGSlot,
+                      static_cast<const char*>(sg.gpeer[r]) + (sg.poff + e0) * L::GB, nv * (uint32_t)L::GB,
+                      &gfull_bar[gsl], pol);
+          }
         }
         if (L::SEP) {  // loads are in flight; now let the stores of unit i - STAGES finish reading
           if (i >= STAGES) bulk_wait_read_all();
@@ -235,7 +243,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   // ------------------------------ consumers -------------------------------
   const float cf = (UPDATE && b.coef) ? *b.coef : 1.0f;
   const float gs = b.gscale;  // DP: 1/world turns reduce-scattered sums into averages (exact x1 else)
-  int s = 0, i = 0;
+  int s = 0, i = 0, gcount = 0;
   for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
     const int stage = i % STAGES;
     while (u >= unit_prefix[s + 1]) ++s;
@@ -251,18 +259,30 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     const int nv = ne & ~(L::vec - 1);  // bulk-copied prefix; the tail is read from HBM
     const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
     char* stg = sbuf + (size_t)stage * L::bytes;
-    const void* gp[kMaxPeers];   // P2P: every rank's full-layer gradient
-    void* tp[kMaxPeers];         // P2P: every rank's full-layer parameters
-    if (P2P) {
-#pragma unroll
-      for (int q = 0; q < kMaxPeers; ++q) {
-        gp[q] = q < b.npeer ? sg.gpeer[q] : nullptr;
-        tp[q] = q < b.npeer ? sg.tpeer[q] : nullptr;
-      }
-    }
     const int64_t pe0 = P2P ? sg.poff + e0 : 0;  // full-layer index of the unit's element 0
     mbar_wait(&full_bar[stage], (i / STAGES) & 1);
     if (L::SEP) mbar_wait(&outfree_bar[stage], (i / STAGES) & 1);
+    float4 gacc[kUnroll];  // P2P: this thread's summed gradient of the unit
+    if (P2P && nv) {
+      for (int r = 0; r < b.npeer; ++r, ++gcount) {
+        const int gsl = gcount % NG;
+        mbar_wait(&gfull_bar[gsl], (gcount / NG) & 1);
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+          const int e = (q * kThreads + tid) * kVec;
+          if (e < nv) {
+            const float4 x = stage_g4<BF16>(gring + (size_t)gsl * kGSlot, e);
+            if (r == 0) {
+              gacc[q] = x;
+            } else {
+              gacc[q].x += x.x; gacc[q].y += x.y; gacc[q].z += x.z; gacc[q].w += x.w;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&gempty_bar[gsl]);
+      }
+    }
     if (!UPDATE && !P2P && ne == kUnit) {
       // Full unit of the norm-only stream: branch-free, every shared-memory
       // read issued before the math.  Same element map and accumulation order
@@ -304,7 +324,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           for (int q = 0; q < kUnroll; ++q) {
             const int e = k * (int)kTile + (q * kThreads + tid) * kVec;  // relative to e0
             if (e < nv) {
-              const float4 g4 = scale4(P2P ? peer_g4<BF16>(gp, b.npeer, pe0 + e) : stage_g4<BF16>(stg + L::off_g, e), gs);
+              const float4 g4 = scale4(P2P ? gacc[q] : stage_g4<BF16>(stg + L::off_g, e), gs);
               acc[0] = fma((double)g4.x, (double)g4.x, acc[0]);
               acc[1] = fma((double)g4.y, (double)g4.y, acc[1]);
               acc[2] = fma((double)g4.z, (double)g4.z, acc[2]);
@@ -332,9 +352,9 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
                     for (int q = 0; q < kMaxPeers; ++q) {
                       if (q >= b.npeer) break;
                       if (BF16)
-                        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(tp[q]) + pe0 + e) = pack_bf16x4(t4);
+                        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(sg.tpeer[q]) + pe0 + e) = pack_bf16x4(t4);
                       else
-                        st_stream(static_cast<float*>(tp[q]) + pe0 + e, t4);
+                        st_stream(static_cast<float*>(sg.tpeer[q]) + pe0 + e, t4);
                     }
                   } else if (BF16) {
                     *reinterpret_cast<uint2*>(sg.theta16 + e0 + e) = pack_bf16x4(t4);
@@ -346,7 +366,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
               for (int j = 0; j < kVec; ++j) {
                 if (e + j < ne) {
                   const int64_t idx = e0 + e + j;
-                  const float g = (P2P ? peer_g1<BF16>(gp, b.npeer, pe0 + e + j) : seg_g<BF16>(sg, idx)) * gs;
+                  const float g = (P2P ? peer_g1<BF16>(sg.gpeer, b.npeer, pe0 + e + j) : seg_g<BF16>(sg, idx)) * gs;
                   acc[j] = fma((double)g, (double)g, acc[j]);
                   if (UPDATE) {
                     float th = init ? bf2f(sg.theta16[idx]) : sg.theta[idx];
@@ -360,9 +380,9 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
                       for (int q = 0; q < kMaxPeers; ++q) {
                         if (q >= b.npeer) break;
                         if (BF16)
-                          static_cast<uint16_t*>(tp[q])[pe0 + e + j] = (uint16_t)f2bf(th);
+                          static_cast<uint16_t*>(sg.tpeer[q])[pe0 + e + j] = (uint16_t)f2bf(th);
                         else
-                          static_cast<float*>(tp[q])[pe0 + e + j] = th;
+                          static_cast<float*>(sg.tpeer[q])[pe0 + e + j] = th;
                       }
                     } else if (BF16) {
                       sg.theta16[idx] = (uint16_t)f2bf(th);
