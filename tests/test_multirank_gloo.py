@@ -1,7 +1,7 @@
 """World-size-2 CPU tests (gloo) of the data-parallel decomposition that
 libgrass runs over NCCL when world > 1 (include/grass.h, grass_step_layers):
 
-  N1  reduce-scatter (average) of each active layer's gradient -> rank shard
+  N1  reduce-scatter (sum, then x 1/W) of each active layer's gradient -> rank shard
   a1  fp64 squared norm of the shard, N3 all-gather of the shard partials,
       fixed ascending-rank sum -> identical ss_l on every rank
   a5  AdamW on the shard with this rank's m/v slice
@@ -53,7 +53,7 @@ def _worker(rank, world, port, q):
         shard_ss, new_params = [], {}
         for j, l in enumerate(sorted(ids)):
             off, cnt = G.shard_range(numel[l], world, rank)
-            # N1: reduce-scatter(avg) in fp32, as ncclReduceScatter(ncclAvg) does
+            # N1: fp32 reduce-scatter SUM, then x 1/W (as the library: ncclSum + Batch::gscale)
             chunks = [torch.from_numpy(local[l][r * cnt:(r + 1) * cnt].copy()) for r in range(world)]
             g_shard = torch.empty(cnt)
             dist.reduce_scatter(g_shard, chunks, op=dist.ReduceOp.SUM)
