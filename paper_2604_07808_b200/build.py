@@ -78,6 +78,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str | Non
         objs.append(obj)
     tmp = out_path + ".tmp"
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
+          "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map"),
           "-ldl", "-lpthread", "-lrt", "-lz"], verbose)
     os.replace(tmp, out_path)
     with open(os.path.join(build_dir, "ptxas.log"), "w") as fh:

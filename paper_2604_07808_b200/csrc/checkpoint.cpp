@@ -1,0 +1,201 @@
+// checkpoint.cpp — grass_save_state / grass_load_state (SURVEY 8(f) f4,
+// SPEC.md:192-199): self-describing header + per-layer blobs, 64-bit lengths,
+// CRC32 (zlib); verify-then-apply.
+#include <zlib.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "context.h"
+
+namespace gapi {
+
+// ---- checkpoint ------------------------------------------------------------
+const char kCkMagic[8] = {'G', 'R', 'A', 'S', 'S', 'C', 'K', '1'};
+const uint32_t kCkVersion = 2;  // 2: n_always in the header
+
+uint32_t crc_update(uint32_t crc, const void* p, size_t n) {
+  const Bytef* b = static_cast<const Bytef*>(p);
+  while (n > 0) {
+    const uInt k = (uInt)std::min<size_t>(n, 1u << 30);
+    crc = (uint32_t)crc32(crc, b, k);
+    b += k;
+    n -= k;
+  }
+  return crc;
+}
+
+template <class T>
+void put(std::vector<char>* h, const T* p, size_t n) {
+  const char* b = reinterpret_cast<const char*>(p);
+  h->insert(h->end(), b, b + sizeof(T) * n);
+}
+
+constexpr int kCkInts = 6;  // n_layers, world, rank, committed, dtype, n_always
+
+std::vector<char> ck_header(grass_ctx* c) {
+  std::vector<char> h;
+  const int32_t ints[kCkInts] = {c->nl,         c->cfg.world,         c->cfg.rank, c->committed ? 1 : 0,
+                                 c->cfg.param_dtype, c->cfg.n_always};
+  put(&h, ints, kCkInts);
+  put(&h, c->numel.data(), c->nl);
+  put(&h, c->shard_len.data(), c->nl);
+  put(&h, c->t.data(), c->nl);
+  put(&h, c->mgn.data(), c->nl);
+  put(&h, c->probs.data(), c->nl);
+  put(&h, h_S(c), c->nl);
+  put(&h, h_c(c), c->nl);
+  return h;
+}
+
+
+}  // namespace gapi
+
+using namespace gapi;
+
+extern "C" {
+
+grass_status grass_save_state(grass_ctx* c, const char* path) try {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!path) return c->fail(GRASS_E_INVALID, "path is NULL");
+  grass_status s = drain(c, false);
+  if (s == GRASS_OK) s = flush_cache(c);
+  if (s != GRASS_OK) return s;
+  const std::vector<char> hdr = ck_header(c);
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return c->fail(GRASS_E_IO, std::string("cannot open ") + path + " for writing");
+  bool ok = true;
+  const uint64_t hlen = hdr.size();
+  const uint32_t hcrc = crc_update(0, hdr.data(), hdr.size());
+  ok = ok && std::fwrite(kCkMagic, 1, 8, f) == 8;
+  ok = ok && std::fwrite(&kCkVersion, 4, 1, f) == 1;
+  ok = ok && std::fwrite(&hlen, 8, 1, f) == 1;
+  ok = ok && std::fwrite(&hcrc, 4, 1, f) == 1;
+  ok = ok && std::fwrite(hdr.data(), 1, hdr.size(), f) == hdr.size();
+  std::vector<float> tmp;
+  for (int l = 0; ok && l < c->nl; ++l) {
+    // one blob per layer: m, v [, master] shards, fp32
+    const size_t n = (size_t)c->shard_len[l];
+    tmp.resize((size_t)c->ns * n);
+    for (int a = 0; a < c->ns && s == GRASS_OK; ++a) s = copy_state_out(c, a, l, tmp.data() + a * n);
+    if (s != GRASS_OK) {
+      std::fclose(f);
+      return s;
+    }
+    const uint64_t len = 4 * (uint64_t)tmp.size();
+    const uint32_t crc = crc_update(0, tmp.data(), len);
+    ok = ok && std::fwrite(&len, 8, 1, f) == 1 && std::fwrite(&crc, 4, 1, f) == 1;
+    ok = ok && std::fwrite(tmp.data(), 4, tmp.size(), f) == tmp.size();
+  }
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) return c->fail(GRASS_E_IO, std::string("short write to ") + path);
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
+}
+
+grass_status grass_load_state(grass_ctx* c, const char* path) try {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!path) return c->fail(GRASS_E_INVALID, "path is NULL");
+  grass_status s = drain(c, false);
+  if (s != GRASS_OK) return s;
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return c->fail(GRASS_E_IO, std::string("cannot open ") + path);
+  auto bad = [&](grass_status st, const std::string& m) {
+    std::fclose(f);
+    return c->fail(st, m);
+  };
+  char magic[8];
+  uint32_t ver = 0, hcrc = 0;
+  uint64_t hlen = 0;
+  if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, kCkMagic, 8) != 0)
+    return bad(GRASS_E_IO, "not a GRASS checkpoint (bad magic)");
+  if (std::fread(&ver, 4, 1, f) != 1 || ver != kCkVersion) return bad(GRASS_E_IO, "unsupported version");
+  if (std::fread(&hlen, 8, 1, f) != 1 || std::fread(&hcrc, 4, 1, f) != 1) return bad(GRASS_E_IO, "truncated header");
+  const int nl = c->nl;
+  const size_t want = 4 * kCkInts + (size_t)nl * (3 * 8 + 4 * 8);
+  if (hlen != want) return bad(GRASS_E_INVALID, "checkpoint was written for a different layer count");
+  std::vector<char> hdr(hlen);
+  if (std::fread(hdr.data(), 1, hlen, f) != hlen) return bad(GRASS_E_IO, "truncated header");
+  if (crc_update(0, hdr.data(), hlen) != hcrc) return bad(GRASS_E_IO, "header CRC32 mismatch (integrity error)");
+  const char* p = hdr.data();
+  auto take = [&](void* dst, size_t k) {
+    std::memcpy(dst, p, k);
+    p += k;
+  };
+  int32_t ints[kCkInts];
+  take(ints, sizeof(ints));
+  std::vector<int64_t> numel(nl), slen(nl), t(nl);
+  std::vector<double> mgn(nl), probs(nl), S(nl);
+  std::vector<long long> cnt(nl);
+  take(numel.data(), 8 * nl);
+  take(slen.data(), 8 * nl);
+  take(t.data(), 8 * nl);
+  take(mgn.data(), 8 * nl);
+  take(probs.data(), 8 * nl);
+  take(S.data(), 8 * nl);
+  take(cnt.data(), 8 * nl);
+  if (ints[0] != nl || ints[1] != c->cfg.world || ints[2] != c->cfg.rank || ints[4] != c->cfg.param_dtype ||
+      ints[5] != c->cfg.n_always || numel != c->numel || slen != c->shard_len)
+    return bad(GRASS_E_INVALID,
+               "checkpoint does not match this context (N_L, n_always, N_p, dtype, world or rank)");
+  const long blobs = std::ftell(f);
+  // pass 1: verify every blob's length and CRC32 before touching the context
+  std::vector<char> buf(64u << 20);
+  for (int l = 0; l < nl; ++l) {
+    uint64_t len = 0;
+    uint32_t crc = 0;
+    if (std::fread(&len, 8, 1, f) != 1 || std::fread(&crc, 4, 1, f) != 1)
+      return bad(GRASS_E_IO, "truncated layer blob header");
+    if (len != 4 * (uint64_t)c->ns * (uint64_t)slen[l])
+      return bad(GRASS_E_IO, "corrupt layer blob length (integrity error)");
+    uint32_t got = 0;
+    for (uint64_t done = 0; done < len;) {
+      const size_t k = (size_t)std::min<uint64_t>(buf.size(), len - done);
+      if (std::fread(buf.data(), 1, k, f) != k) return bad(GRASS_E_IO, "truncated layer blob");
+      got = crc_update(got, buf.data(), k);
+      done += k;
+    }
+    if (got != crc) return bad(GRASS_E_IO, "layer " + std::to_string(l) + " CRC32 mismatch (integrity error)");
+  }
+  // pass 2: apply (cached copies are superseded by the checkpoint)
+  std::fseek(f, blobs, SEEK_SET);
+  if (c->cache_slots) {
+    for (int k = 0; k < c->cache_slots; ++k) {
+      c->slot_layer[k] = -1;
+      c->slot_dirty[k] = 0;
+    }
+    std::fill(c->layer_slot.begin(), c->layer_slot.end(), -1);
+  }
+  std::vector<float> tmp;
+  for (int l = 0; l < nl; ++l) {
+    std::fseek(f, 12, SEEK_CUR);
+    const size_t n = (size_t)slen[l];
+    tmp.resize((size_t)c->ns * n);
+    if (std::fread(tmp.data(), 4, tmp.size(), f) != tmp.size()) return bad(GRASS_E_IO, "read failed");
+    for (int a = 0; a < c->ns; ++a) {
+      if ((s = copy_state_in(c, a, l, tmp.data() + a * n)) != GRASS_OK) {
+        std::fclose(f);
+        return s;
+      }
+    }
+    if (c->bf16) c->master_valid[l] = t[l] > 0 ? 1 : 0;
+  }
+  std::fclose(f);
+  c->t = t;
+  c->mgn = mgn;
+  c->probs = probs;
+  c->committed = ints[3] != 0;
+  std::vector<char> blk(16 * (size_t)nl);
+  std::memcpy(blk.data(), S.data(), 8 * (size_t)nl);
+  std::memcpy(blk.data() + 8 * (size_t)nl, cnt.data(), 8 * (size_t)nl);
+  CUDA_TRY(c, cudaMemcpy(c->d_mgn, blk.data(), blk.size(), cudaMemcpyHostToDevice));
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,239 @@
+// hot_path.cpp — grass_mgn_accumulate / grass_step_layers: ordering, the
+// resident / offload / period / NCCL / P2P branches and clipping (R17).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "context.h"
+
+namespace gapi {
+
+// ---- the hot path ----------------------------------------------------------
+
+// Eq. 2 inner term for the listed layers (probing); fp32 or bf16 gradients.
+grass_status mgn_accumulate_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_t n,
+                                 const void* const* grads, void* stream) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!grads) return c->fail(GRASS_E_INVALID, "grads is NULL");
+  std::vector<int> order;
+  grass_status s = check_call(c, bf16_call, ids, n, grads, nullptr, &order);
+  if (s != GRASS_OK) return s;
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (c->p2p) {
+    // start barrier -> K1 over the sum of every rank's gradient (peer reads) -> publish + end barrier
+    if ((s = p2p_check(c, ids, n, nullptr, grads)) != GRASS_OK) return s;
+    if ((s = p2p_start(c, st)) != GRASS_OK) return s;
+    Batch b = make_batch(c, kFinalizeShard);
+    for (int j = 0; j < (int)order.size(); ++j) {
+      const int l = ids[order[j]];
+      if (b.nseg == kMaxSeg && (s = flush(c, &b, false, st)) != GRASS_OK) return s;
+      Seg sg = range_seg(c, l, elem(grads[order[j]], c->shard_off[l], c->esz), 0, c->shard_len[l]);
+      sg.out_slot = j;
+      push_seg(&b, sg);
+    }
+    if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
+    if ((s = p2p_end(c, ids, order, st)) != GRASS_OK) return s;
+  } else if (!c->dp) {
+    Batch b = make_batch(c, kFinalizeMgn);
+    for (int i : order) {
+      if (b.nseg == kMaxSeg && (s = flush(c, &b, false, st)) != GRASS_OK) return s;
+      push_seg(&b, range_seg(c, ids[i], grads[i], 0, c->numel[ids[i]]));
+    }
+    if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
+  } else {
+    // N1 of layer j+1 on the comm stream overlaps K1 of layer j
+    const int nact = (int)order.size();
+    if ((s = comm_begin(c, st)) != GRASS_OK) return s;
+    if ((s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
+    for (int j = 0; j < nact; ++j) {
+      const int l = ids[order[j]];
+      if (j + 1 < nact) {
+        const int l1 = ids[order[j + 1]];
+        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
+      }
+      if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
+      Batch b = make_batch(c, kFinalizeShard);
+      Seg sg = range_seg(c, l, rs_slot(c, j), 0, c->shard_len[l]);
+      sg.out_slot = j;
+      push_seg(&b, sg);
+      if ((s = flush(c, &b, false, st)) != GRASS_OK) return s;
+      if ((s = comm_after_update(c, j, nullptr, 0, 0, st)) != GRASS_OK) return s;
+    }
+    if ((s = comm_end(c, st)) != GRASS_OK) return s;
+    if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+  }
+  return mark_pending(c, st);
+}
+
+// Fused norm + AdamW of the listed layers, with offload / residency / DP /
+// clipping as configured; fp32 or bf16 (master in the context) parameters.
+grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_t n,
+                              void* const* params, const void* const* grads, float lr, void* stream) {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (!params || !grads) return c->fail(GRASS_E_INVALID, "params/grads is NULL");
+  if (!(lr >= 0.0f) || !std::isfinite(lr)) return c->fail(GRASS_E_INVALID, "lr must be finite, >= 0");
+  std::vector<int> order;
+  std::vector<char> g_host;
+  grass_status s = check_call(c, bf16_call, ids, n, reinterpret_cast<const void* const*>(params), grads, &order,
+                              &g_host);
+  if (s != GRASS_OK) return s;
+  const bool any_host = std::find(g_host.begin(), g_host.end(), 1) != g_host.end();
+  if (any_host && c->cfg.max_grad_norm > 0.0)
+    return c->fail(GRASS_E_INVALID, "clipping needs device gradients (pass 1 reads them twice)");
+  if (any_host && !c->d_gring) {  // first host-gradient call: the gradient ring
+    CUDA_TRY(c, cudaMalloc((void**)&c->d_gring, (size_t)c->slots * c->chunk * c->esz));
+    c->dev_bytes += (int64_t)((size_t)c->slots * c->chunk * c->esz);
+  }
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool sharded = c->dp;  // NCCL data parallelism
+  const bool p2p = c->p2p;     // P2P data parallelism: one fused kernel, no NCCL
+  const bool clip = c->cfg.max_grad_norm > 0.0;
+  const int32_t mode = clip ? kFinalizeNone : ((sharded || p2p) ? kFinalizeShard : kFinalizeMgn);
+  if (p2p && (s = p2p_check(c, ids, n, params, grads)) != GRASS_OK) return s;
+  const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
+  const int nact = (int)order.size();
+  int ncached = 0;
+  for (int i = 0; i < n; ++i) ncached += always_active(c, ids[i]) ? 0 : 1;
+  if (sharded && clip && nact > c->clip_slots)
+    return c->fail(GRASS_E_INVALID, "data-parallel clipping: at most gamma + n_always layers per call "
+                                    "(their averaged gradients are kept between the two passes)");
+  if (period && ncached > c->cache_slots)
+    return c->fail(GRASS_E_INVALID, "period residency: more layers in one call than cache slots "
+                                    "(raise cache_layers)");
+  struct CoefReset {  // the clip multiplier only applies inside this call
+    grass_ctx* c;
+    ~CoefReset() { c->cur_coef = nullptr; }
+  } coef_reset{c};
+  if (clip) {
+    // pass 1 (R17): raw norms of this call's (DP-averaged) gradients; they feed
+    // the MGN window (R9) and the global clip coefficient
+    if (!sharded) {
+      Batch b1 = make_batch(c, kFinalizeMgn);
+      for (int i : order) {
+        if (b1.nseg == kMaxSeg && (s = flush(c, &b1, false, st)) != GRASS_OK) return s;
+        push_seg(&b1, range_seg(c, ids[i], grads[i], 0, c->numel[ids[i]]));
+      }
+      if ((s = flush(c, &b1, false, st)) != GRASS_OK) return s;
+    } else {
+      for (int j = 0; j < nact; ++j) {
+        const int i = order[j], l = ids[i];
+        if (!c->comm.reduce_scatter_sum(grads[i], gs_slot(c, j), (size_t)c->shard_len[l], c->bf16, st, &c->err))
+          return GRASS_E_NCCL;
+        c->launches++;
+        Batch b1 = make_batch(c, kFinalizeShard);
+        Seg sg = range_seg(c, l, gs_slot(c, j), 0, c->shard_len[l]);
+        sg.out_slot = j;
+        push_seg(&b1, sg);
+        if ((s = flush(c, &b1, false, st)) != GRASS_OK) return s;
+      }
+      if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+    }
+    ClipArgs ca;
+    std::memset(&ca, 0, sizeof(ca));
+    ca.n = nact;
+    ca.max_norm = c->cfg.max_grad_norm;
+    for (int j = 0; j < ca.n; ++j) ca.layer[j] = ids[order[j]];
+    CUDA_TRY(c, launch_clip_coef(ca, c->st, c->d_coef, st));
+    c->launches++;
+    c->cur_coef = c->d_coef;
+  }
+  std::vector<int> slot_of, victim_of;
+  if (period) {
+    cache_plan(c, ids, order, &slot_of, &victim_of);
+    c->call_seq++;
+    // write-backs read cache slots last written by earlier steps' updates
+    if (c->cfg.overlap && (s = wait_pending(c, c->d2h)) != GRASS_OK) return s;
+  }
+  if (p2p && (s = p2p_start(c, st)) != GRASS_OK) return s;
+  Batch b = make_batch(c, mode);
+  if (sharded) {
+    if ((s = comm_begin(c, st)) != GRASS_OK) return s;
+    if (!clip && (s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
+  }
+  for (int j = 0; j < nact; ++j) {
+    const int i = order[j], l = ids[i];
+    c->t[l] += 1;  // per-layer step count (R2); validated above, so this step happens
+    const bool init = c->bf16 && !c->master_valid[l];
+    c->master_valid[l] = 1;
+    const int64_t off = c->shard_off[l], len = c->shard_len[l];
+    const void* g = grads[i];
+    if (p2p) {
+      g = elem(grads[i], off, c->esz);  // this rank's range (the kernel sums every rank's via Seg::gpeer)
+    } else if (sharded && clip) {
+      g = gs_slot(c, j);  // averaged in pass 1
+    } else if (sharded) {
+      if (j + 1 < nact) {  // N1 of the next layer overlaps this layer's update
+        const int l1 = ids[order[j + 1]];
+        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
+      }
+      if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
+      g = rs_slot(c, j);  // shard-local gradient: index 0 = element `off`
+    }
+    void* param = elem(params[i], off, c->esz);  // this rank's range of the layer
+    Seg base = range_seg(c, l, g, 0, len);
+    adam_scalars(c, l, lr, &base);
+    base.out_slot = j;
+    if (period && !always_active(c, l)) {
+      const int slot = slot_of[j];
+      if (c->slot_layer[slot] == l) {  // hit: update in place in HBM, no link traffic
+        if (c->slot_ready_pending[slot]) {  // prefetched: wait for its fill
+          CUDA_TRY(c, cudaStreamWaitEvent(st, c->ev_slot_ready[slot], 0));
+          c->slot_ready_pending[slot] = 0;
+        }
+        float* sp[3];
+        for (int a = 0; a < c->ns; ++a) sp[a] = cache_arr(c, slot, a);
+        set_update(c, &base, param, sp, init);
+        if (b.nseg == kMaxSeg && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+        push_seg(&b, base);
+        if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+      } else if ((s = swap_in_layer(c, l, slot, victim_of[j], base, param, g, init, mode, st)) != GRASS_OK) {
+        return s;
+      }
+      c->slot_use[slot] = c->call_seq;
+      c->slot_dirty[slot] = 1;
+    } else if (!home_on_device(c, l)) {
+      if ((s = offload_layer(c, l, base, param, g, init, mode, st, g_host[i] != 0)) != GRASS_OK) return s;
+    } else if (g_host[i]) {
+      if ((s = stream_grad_layer(c, l, base, param, g, init, mode, st)) != GRASS_OK) return s;
+    } else {
+      float* sp[3];
+      for (int a = 0; a < c->ns; ++a) sp[a] = c->arr[a][l];
+      set_update(c, &base, param, sp, init);
+      if (b.nseg == kMaxSeg && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+      push_seg(&b, base);
+      // DP launches per layer: the shard gradient slot is released after it
+      if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+    }
+    if (sharded && (s = comm_after_update(c, j, params[i], off, len, st)) != GRASS_OK) return s;  // N2
+  }
+  if ((s = flush(c, &b, true, st)) != GRASS_OK) return s;
+  if (p2p) {
+    if (c->cfg.offload && c->cfg.overlap) {  // the barrier signals after the last write-back
+      cudaEvent_t e = take_event(c);
+      if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
+      CUDA_TRY(c, cudaEventRecord(e, c->d2h));
+      CUDA_TRY(c, cudaStreamWaitEvent(st, e, 0));
+      c->ev_free_list.push_back(e);
+    }
+    if ((s = p2p_end(c, ids, order, st)) != GRASS_OK) return s;
+  }
+  if (sharded && (s = comm_end(c, st)) != GRASS_OK) return s;
+  if (sharded && !clip && (s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
+  if (c->cfg.offload && c->cfg.overlap) {
+    // join: the caller stream reaches "done" only after every write-back
+    cudaEvent_t e = take_event(c);
+    if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
+    CUDA_TRY(c, cudaEventRecord(e, c->d2h));
+    CUDA_TRY(c, cudaStreamWaitEvent(st, e, 0));
+    c->ev_free_list.push_back(e);
+  }
+  return mark_pending(c, st);
+}
+
+
+}  // namespace gapi
