@@ -318,3 +318,48 @@ def test_p2p_two_processes_ipc(tmp_path):
         assert (np.abs(r[0][f"p{l}"] - th) <= 1e-5 * scale).all()
         assert abs(r[0]["ss"][l] - O.sq_norm(gavg)) <= 1e-6 * O.sq_norm(gavg)
     assert np.array_equal(r[0]["S"], r[1]["S"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_p2p_fuzz_bit_identical_to_plain_on_the_averaged_gradient(seed):
+    """Random world (incl. non-powers of two), ragged layer sizes, random
+    active sets and residency modes: the W-rank P2P update of every element
+    equals, bit for bit, the single-GPU update fed with the same DP gradient
+    formed the way the kernel forms it (fp32 sum in rank order, x fp32(1/W));
+    the per-layer norms agree to fp64 summation order (1e-12)."""
+    rng = np.random.default_rng(200 + seed)
+    W = int(rng.choice([2, 3, 4, 5, 8]))
+    nl = int(rng.integers(2, 6))
+    numel = [8 * W * int(rng.integers(1, 3000)) for _ in range(nl)]
+    mode = ["resident", "offload", "period"][seed % 3]
+    kw = dict(gamma=nl, weight_decay=0.01, **_mode_kw(mode, 4096 * int(rng.integers(1, 4))))
+    vr = VirtualRanks(numel, W, **kw)
+    ref = G.Grass(numel, **{**kw, "offload": False, "residency": 0, "chunk_elems": 0})
+    p_ref = [p.clone() for p in vr.P[0]]
+    inv = torch.tensor(1.0 / W, dtype=torch.float32, device=DEV)
+    for step in range(5):
+        ids = [int(x) for x in rng.choice(nl, size=int(rng.integers(1, nl + 1)), replace=False)]
+        vr.set_grads(ids, step, seed=seed)
+        gavg = []
+        for l in ids:
+            acc = vr.Gr[0][l].clone()
+            for r in range(1, W):
+                acc += vr.Gr[r][l]
+            gavg.append(acc * inv)
+        vr.step(ids, 1e-3)
+        ref.step_layers(ids, [p_ref[l] for l in ids], gavg, 1e-3)
+    torch.cuda.synchronize()
+    for l in range(nl):
+        for r in range(W):
+            assert torch.equal(vr.P[r][l], p_ref[l]), (W, mode, l, r)
+        m_ref, v_ref, t_ref = ref.read_state(l)
+        for r, c in enumerate(vr.ctx):
+            off, cnt = G.shard_range(numel[l], W, r)
+            m, v, t = c.read_state(l)
+            assert t == t_ref and np.array_equal(m, m_ref[off:off + cnt]) and np.array_equal(v, v_ref[off:off + cnt])
+    s_ref = ref.get_mgn()
+    for c in vr.ctx:
+        st = c.get_mgn()
+        assert st["c"] == s_ref["c"]
+        for l in range(nl):
+            assert abs(st["S"][l] - s_ref["S"][l]) <= 1e-12 * abs(s_ref["S"][l]) + 1e-300
