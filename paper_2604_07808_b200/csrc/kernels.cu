@@ -33,6 +33,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <climits>
 #include <cstdint>
 
@@ -316,12 +317,18 @@ cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStre
                                     StageLayout<U, BF16, TPS>::GB
                               : 0);
   static_assert(smem <= 227 * 1024, "ring exceeds the 227 KiB shared-memory limit");
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(grass_stream_kernel<U, TPS, ST, BF16, P2P>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // the opt-in shared-memory size is a per-device function attribute: set it
+  // once per device (contexts on several GPUs / threads share this instance)
+  static std::atomic<unsigned long long> attr_set{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+  if (!bit || !(attr_set.load(std::memory_order_acquire) & bit)) {
+    e = cudaFuncSetAttribute(grass_stream_kernel<U, TPS, ST, BF16, P2P>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_set.fetch_or(bit, std::memory_order_release);
   }
   int units = 0;
   for (int i = 0; i < b.nseg; ++i) units += (b.seg[i].tiles + TPS - 1) / TPS;
