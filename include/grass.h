@@ -394,6 +394,15 @@ grass_status grass_nccl_get_unique_id(void* out);
  * hot-path calls; a call returns to the stream only after every rank's update
  * (and its theta' stores into this rank's buffers) is complete, so the caller
  * may overwrite its gradients and read its parameters afterwards. */
+/* Self-test of the P2P publication + barrier protocol on the current device:
+ * `world` (1..8) ranks are emulated as the co-resident CTAs of ONE cooperative
+ * launch (one GPU cannot host separately launched ranks that wait on one
+ * another); `rounds` rounds of publish + end barrier + row check + start
+ * barrier.  *mismatches = rows that did not hold the expected values after a
+ * barrier, *timed_out = 1 if a barrier wait timed out.  Synchronous. */
+grass_status grass_selftest_p2p(int32_t device, int32_t world, int32_t rounds, int64_t* mismatches,
+                                int32_t* timed_out);
+
 #define GRASS_IPC_HANDLE_BYTES 64
 grass_status grass_p2p_exchange_block(grass_ctx* ctx, void** ptr, int64_t* bytes);
 /* blocks: host [world] addresses of every rank's exchange block, valid in this

@@ -8,7 +8,7 @@ from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_CONTINUE, DECIDE_PROBE, DEC
                       POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM, Grass, GrassError,
                       exported_symbols, lib, nccl_unique_id, sample_from_probs,
                       schedule_decision, shard_range, softmax_probs, splitmix64, tile_elems,
-                      uniform, ipc_export, ipc_import)
+                      uniform, ipc_export, ipc_import, selftest_p2p)
 
 from .schedule import GrassSchedule  # noqa: E402
 
@@ -17,4 +17,4 @@ __all__ = ["Grass", "GrassSchedule", "GrassError", "lib", "exported_symbols", "n
            "splitmix64", "tile_elems", "uniform", "POLICY_ADAPTIVE", "POLICY_STATIC",
            "POLICY_UNIFORM", "DECIDE_PROBE", "DECIDE_COMMIT_RESAMPLE", "DECIDE_RESAMPLE",
            "DECIDE_CONTINUE", "RESIDENCY_STEP", "RESIDENCY_PERIOD", "DTYPE_FP32", "DTYPE_BF16",
-           "DP_NCCL", "DP_P2P", "ipc_export", "ipc_import"]
+           "DP_NCCL", "DP_P2P", "ipc_export", "ipc_import", "selftest_p2p"]

@@ -117,6 +117,8 @@ _SIGS = {
                                            C.POINTER(C.c_void_p)]),
     "grass_p2p_finish": (C.c_int, [C.c_void_p, C.c_void_p]),
     "grass_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "grass_selftest_p2p": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int32)]),
     "grass_ipc_import": (C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
 }
 
@@ -209,6 +211,13 @@ def _ptrs(tensors, itemsize: int = 4, host_ok: bool = False):
                              "elements (fp32, or bf16 for a bf16 context)")
         arr[i] = t.data_ptr()
     return arr
+
+
+def selftest_p2p(world: int, rounds: int = 100, device: int = 0):
+    """(mismatched rows, timed out) of the P2P barrier protocol, emulated on one GPU."""
+    mm, to = C.c_int64(), C.c_int32()
+    _check(lib().grass_selftest_p2p(device, world, rounds, C.byref(mm), C.byref(to)))
+    return mm.value, bool(to.value)
 
 
 def ipc_export(ptr: int):

@@ -434,6 +434,25 @@ grass_status grass_p2p_finish(grass_ctx* c, void* stream) try {
   return api_exception(c);
 }
 
+grass_status grass_selftest_p2p(int32_t device, int32_t world, int32_t rounds, int64_t* mismatches,
+                                int32_t* timed_out) try {
+  if (!mismatches || !timed_out) return set_thread_err(GRASS_E_INVALID, "NULL output");
+  if (world < 1 || world > kMaxPeers || rounds < 1) return set_thread_err(GRASS_E_INVALID, "world in [1, 8], rounds >= 1");
+  cudaError_t e = cudaSetDevice(device);
+  unsigned long long mm = 0;
+  int to = 0;
+  if (e == cudaSuccess) e = p2p_selftest(world, 64, rounds, &mm, &to);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_thread_err(GRASS_E_CUDA, std::string("P2P self-test: ") + cudaGetErrorString(e));
+  }
+  *mismatches = (int64_t)mm;
+  *timed_out = to;
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
+}
+
 grass_status grass_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out) try {
   if (!ptr || !handle_out || !offset_out) return set_thread_err(GRASS_E_INVALID, "NULL argument");
   AddressRangeFn fn = address_range_fn();

@@ -129,6 +129,9 @@ struct P2PSyncArgs {
   int* err;                // set to 1 if a peer never arrives (timeout)
 };
 cudaError_t launch_p2p_sync(const P2PSyncArgs& a, cudaStream_t s);
+// grass_selftest_p2p: the protocol above with `world` ranks emulated as the
+// co-resident CTAs of one cooperative launch (synchronous).
+cudaError_t p2p_selftest(int world, int n, int rounds, unsigned long long* mismatches, int* timed_out);
 
 // host_policy.cpp
 uint64_t splitmix64(uint64_t x);

@@ -257,7 +257,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__global__ void grass_p2p_sync_kernel(const __grid_constant__ P2PSyncArgs a) {
+// One rank's publication + barrier, executed by one CTA (rank = a.rank).
+__device__ void p2p_sync_cta(const P2PSyncArgs& a) {
   const int tid = threadIdx.x;
   for (int k = tid; k < a.world * a.n; k += blockDim.x) {
     const int q = k / a.n, j = k % a.n;
@@ -287,6 +288,56 @@ __global__ void grass_p2p_sync_kernel(const __grid_constant__ P2PSyncArgs a) {
     }
   }
   __syncthreads();
+}
+
+__global__ void grass_p2p_sync_kernel(const __grid_constant__ P2PSyncArgs a) { p2p_sync_cta(a); }
+
+// Self-test of the publication + barrier protocol (grass_selftest_p2p): W ranks
+// emulated as the W co-resident CTAs of ONE cooperative launch (the profiling
+// rules: ranks that wait on one another must not be separate launches on one
+// GPU).  Every round each rank writes round-dependent norms, publishes them
+// with the end barrier, checks that every rank's row arrived, then passes the
+// start barrier before the next round may overwrite the rows.
+struct P2PSelftestArgs {
+  char* exch[kMaxPeers];
+  double* ss;          // [world][n] per-rank "shard norms"
+  int32_t world, n, rounds;
+  int* err;
+  unsigned long long* mismatches;
+};
+__global__ void grass_p2p_selftest_kernel(const __grid_constant__ P2PSelftestArgs t) {
+  const int rank = blockIdx.x;
+  P2PSyncArgs a;
+  for (int q = 0; q < kMaxPeers; ++q) a.exch[q] = t.exch[q];
+  a.rank = rank;
+  a.world = t.world;
+  a.n = t.n;
+  a.shard_ss = t.ss + (int64_t)rank * t.n;
+  a.err = t.err;
+  double* mine = t.ss + (int64_t)rank * t.n;
+  const double* rows = reinterpret_cast<const double*>(t.exch[rank] + kExchGather);
+  for (int round = 1; round <= t.rounds; ++round) {
+    for (int j = threadIdx.x; j < t.n; j += blockDim.x) mine[j] = round * 1000.0 + rank * 10.0 + j;
+    __syncthreads();
+    a.which = 1;
+    a.epoch = (uint64_t)round;
+    p2p_sync_cta(a);  // publish + end barrier
+    // rank- and round-dependent skew (0-5 us) so that a missing barrier shows
+    if (threadIdx.x == 0) __nanosleep((unsigned)(((round * 7919 + rank * 104729) % 50) * 100));
+    __syncthreads();
+    for (int k = threadIdx.x; k < t.world * t.n; k += blockDim.x) {
+      const int r = k / t.n, j = k % t.n;
+      if (rows[k] != round * 1000.0 + r * 10.0 + j) atomicAdd(t.mismatches, 1ull);
+    }
+    __syncthreads();
+#ifndef GRASS_SELFTEST_MUTANT_NO_START  // mutation check of the self-test itself
+    a.which = 0;  // start barrier: every rank has read its rows of this round
+    const int n_save = a.n;
+    a.n = 0;
+    p2p_sync_cta(a);
+    a.n = n_save;
+#endif
+  }
 }
 
 __global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const DevState st,
@@ -366,6 +417,32 @@ cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const 
 cudaError_t launch_p2p_sync(const P2PSyncArgs& a, cudaStream_t s) {
   grass_p2p_sync_kernel<<<1, 256, 0, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t p2p_selftest(int world, int n, int rounds, unsigned long long* mismatches, int* timed_out) {
+  if (world < 1 || world > kMaxPeers || n < 1 || rounds < 1) return cudaErrorInvalidValue;
+  const size_t blk = (size_t)kExchGather + sizeof(double) * (size_t)world * n;
+  char* mem = nullptr;
+  cudaError_t e = cudaMalloc(&mem, blk * world + sizeof(double) * (size_t)world * n + 64);
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(mem, 0, blk * world + sizeof(double) * (size_t)world * n + 64);
+  P2PSelftestArgs t;
+  for (int q = 0; q < kMaxPeers; ++q) t.exch[q] = q < world ? mem + blk * q : nullptr;
+  t.ss = reinterpret_cast<double*>(mem + blk * world);
+  t.err = reinterpret_cast<int*>(mem + blk * world + sizeof(double) * (size_t)world * n);
+  t.mismatches = reinterpret_cast<unsigned long long*>(mem + blk * world + sizeof(double) * (size_t)world * n + 8);
+  t.world = world;
+  t.n = n;
+  t.rounds = rounds;
+  if (e == cudaSuccess) {
+    void* args[] = {&t};
+    e = cudaLaunchCooperativeKernel((const void*)grass_p2p_selftest_kernel, dim3(world), dim3(256), args, 0, nullptr);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(mismatches, t.mismatches, sizeof(*mismatches), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(timed_out, t.err, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(mem);
+  return e;
 }
 
 cudaError_t launch_clip_coef(const ClipArgs& a, const DevState& st, float* coef, cudaStream_t s) {

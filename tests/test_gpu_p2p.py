@@ -363,3 +363,13 @@ def test_p2p_fuzz_bit_identical_to_plain_on_the_averaged_gradient(seed):
         assert st["c"] == s_ref["c"]
         for l in range(nl):
             assert abs(st["S"][l] - s_ref["S"][l]) <= 1e-12 * abs(s_ref["S"][l]) + 1e-300
+
+
+@pytest.mark.parametrize("W", [1, 2, 4, 8])
+def test_p2p_barrier_protocol_selftest(W):
+    """The publication + end barrier + start barrier protocol of the P2P path
+    with W ranks emulated as the co-resident CTAs of one cooperative launch:
+    after every end barrier each rank holds every rank's row of that round,
+    and no rank overwrites a row before every rank has read it."""
+    mismatches, timed_out = G.selftest_p2p(W, rounds=2000)
+    assert mismatches == 0 and not timed_out
