@@ -173,6 +173,21 @@ def test_splitmix64_published_vectors(golden):
         assert O.splitmix64((k * gamma) & O.MASK64) == int(want, 16)
 
 
+def test_uniform_draws_published_splitmix64_outputs(golden):
+    # R7: u(seed, period, k) = (splitmix64(splitmix64(seed) ^ (period*2^16 + k)) >> 11) * 2^-53.
+    # With seed = 0 the key is the published output #0; choosing (period, k) so
+    # that key ^ (period*2^16 + k) = j*gamma makes the draw the published
+    # output #j — its top 53 bits scaled by 2^-53, exactly.
+    v = golden("splitmix64_vectors.json")
+    gamma = int(v["gamma"], 16)
+    outs = [int(x, 16) for x in v["outputs_from_state_0"]]
+    key = outs[0]
+    for j, out in enumerate(outs):
+        ctr = key ^ ((j * gamma) & O.MASK64)
+        period, k = ctr >> 16, ctr & 0xFFFF
+        assert O.uniform(0, period, k) == (out >> 11) * 2.0 ** -53
+
+
 def test_uniform_range_and_moments():
     us = [O.uniform(1234, p, k) for p in range(2000) for k in range(10)]
     assert all(0.0 <= u < 1.0 for u in us)
@@ -390,6 +405,9 @@ def test_always_groups_do_not_touch_mgn_or_sampling():
     for period in range(200):
         ids = b.sample(period)
         assert ids == a.sample(period) and max(ids) < 4
+    # degenerate sampled probabilities (all zero): the R = 0 fallback takes the
+    # last SAMPLED layer, never an always group
+    assert b.sample(0, probs=[0.0] * 6) == [3, 2]
 
 
 # ------------------------------------------------ R17: global-norm clipping
