@@ -43,6 +43,14 @@ namespace grass {
 namespace {
 
 constexpr int kConsumerWarps = kThreads / 32;  // 16
+
+// Mutation check of the GPU parity tests (tools/kernel_mutation.py): a
+// variant built with -DGRASS_MUTANT=k plants mistake k; 0 (the product) plants
+// nothing — every `kMutant == k` test below is a compile-time constant.
+#ifndef GRASS_MUTANT
+#define GRASS_MUTANT 0
+#endif
+constexpr int kMutant = GRASS_MUTANT;
 constexpr int kStreamThreads = kThreads + 32;  // + 1 producer warp
 
 __device__ __forceinline__ double warp_sum(double x) {
@@ -66,7 +74,7 @@ struct AdamScalars {
 __device__ __forceinline__ void adamw1(float g, float& th, float& m, float& v,
                                        const AdamScalars& s) {
   g *= s.cf;  // exact when cf == 1
-  const float t1 = th * s.decay;
+  const float t1 = kMutant == 1 ? th : th * s.decay;  // M1: weight decay dropped
   const float m1 = fmaf(s.b1, m, s.omb1 * g);
   const float v1 = fmaf(s.b2, v, (s.omb2 * g) * g);
 #ifdef GRASS_IEEE_MATH
@@ -75,7 +83,7 @@ __device__ __forceinline__ void adamw1(float g, float& th, float& m, float& v,
 #else
   float sq;
   asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(v1));
-  const float den = fmaf(sq, s.inv_bc2s, s.eps);
+  const float den = fmaf(sq, kMutant == 2 ? 1.0f : s.inv_bc2s, s.eps);  // M2: no bc2
   th = fmaf(-s.step, __fdividef(m1, den), t1);
 #endif
   m = m1;

@@ -51,6 +51,7 @@ struct StageLayout {
 
 __device__ __forceinline__ float bf2f(uint32_t b) { return __uint_as_float(b << 16); }
 __device__ __forceinline__ uint32_t f2bf(float f) {
+  if (kMutant == 7) return __float_as_uint(f) >> 16;  // M7: truncation instead of RNE
   return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 __device__ __forceinline__ float4 unpack_bf16x4(uint2 u) {
@@ -242,7 +243,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
 
   // ------------------------------ consumers -------------------------------
   const float cf = (UPDATE && b.coef) ? *b.coef : 1.0f;
-  const float gs = b.gscale;  // DP: 1/world turns reduce-scattered sums into averages (exact x1 else)
+  const float gs = kMutant == 5 ? 1.0f : b.gscale;  // DP: 1/world turns reduce-scattered sums into averages (M5: not)
   int s = 0, i = 0, gcount = 0;
   for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
     const int stage = i % STAGES;
@@ -275,7 +276,9 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
             if (r == 0) {
               gacc[q] = x;
             } else {
-              gacc[q].x += x.x; gacc[q].y += x.y; gacc[q].z += x.z; gacc[q].w += x.w;
+              if (!(kMutant == 6 && r == b.npeer - 1)) {  // M6: last rank's slice dropped
+                gacc[q].x += x.x; gacc[q].y += x.y; gacc[q].z += x.z; gacc[q].w += x.w;
+              }
             }
           }
         }
@@ -364,7 +367,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
             } else if (e < ne) {
 #pragma unroll
               for (int j = 0; j < kVec; ++j) {
-                if (e + j < ne) {
+                if (e + j < ne - (kMutant == 4 ? 1 : 0)) {  // M4: last tail element skipped
                   const int64_t idx = e0 + e + j;
                   const float g = (P2P ? peer_g1<BF16>(sg.gpeer, b.npeer, pe0 + e + j) : seg_g<BF16>(sg, idx)) * gs;
                   acc[j] = fma((double)g, (double)g, acc[j]);
@@ -404,7 +407,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     if (tid < ntiles) {  // lane k of warp 0 finishes tile k (warp sums in ascending order)
       double p = 0.0;
 #pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) p += red[i & 1][tid][w];
+      for (int w = 0; w < kConsumerWarps - (kMutant == 3 ? 1 : 0); ++w) p += red[i & 1][tid][w];  // M3
       st.partials[sg.part_index + (int64_t)ui * TPS + tid] = p;
     }
     if (tid == 0) seg_done[s] += ntiles;
