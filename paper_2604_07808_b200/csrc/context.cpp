@@ -527,8 +527,8 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     if (!c->comm.init(cfg->nccl_unique_id, cfg->rank, W, &c->err)) return GRASS_E_NCCL;
     c->has_comm = true;
   }
-  c->grid_update = fused_grid(true, cfg->device);
-  c->grid_norm = fused_grid(false, cfg->device);
+  c->grid_update = fused_grid(true, c->bf16, cfg->device);
+  c->grid_norm = fused_grid(false, c->bf16, cfg->device);
   if (c->grid_update < 1 || c->grid_norm < 1) return c->fail(GRASS_E_CUDA, "occupancy query failed");
   CUDA_TRY(c, cudaDeviceSynchronize());
   return GRASS_OK;

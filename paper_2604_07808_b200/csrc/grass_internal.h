@@ -101,7 +101,7 @@ struct RankSumArgs {
 };
 cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const DevState& st,
                             cudaStream_t s);
-int fused_grid(bool update, int device);
+int fused_grid(bool update, bool bf16, int device);
 // Global-norm clip coefficient of the listed layers from last_ss (fp64,
 // ascending layer order): coef = min(1, max_norm / (sqrt(sum) + 1e-6)).
 struct ClipArgs {

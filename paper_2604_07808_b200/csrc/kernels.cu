@@ -403,9 +403,9 @@ cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int gr
   if (b.nseg <= 0 || b.tile_prefix[b.nseg] <= 0) return cudaSuccess;
   if (b.npeer > 0) {  // P2P data parallelism: one tile per unit, the gradient read from the peers
     if (b.bf16)
-      return update ? launch_stream<true, 1, kUpdStages, true, true>(b, st, grid, s)
+      return update ? launch_stream<true, 1, 2, true, true>(b, st, grid, s)
                     : launch_stream<false, 1, 2, true, true>(b, st, grid, s);
-    return update ? launch_stream<true, 1, kUpdStages, false, true>(b, st, grid, s)
+    return update ? launch_stream<true, 1, 2, false, true>(b, st, grid, s)
                   : launch_stream<false, 1, 2, false, true>(b, st, grid, s);
   }
   if (b.bf16)
@@ -458,13 +458,24 @@ cudaError_t launch_clip_coef(const ClipArgs& a, const DevState& st, float* coef,
   return cudaGetLastError();
 }
 
-// Persistent grid: one streaming CTA per SM (results never depend on the grid
-// size — see kTile in grass_internal.h).
-int fused_grid(bool update, int device) {
-  (void)update;
+// Grid of the persistent kernels.  K1 (reads only) is fastest with one CTA on
+// every SM.  K2 (4 read + 3 write streams per CTA, 128 KiB in flight per CTA)
+// is fastest with FEWER CTAs: on B200 128 of 148 SMs for fp32 (1.72 vs
+// 1.785 ms at configs[1], +3.7%), 132 for bf16 — fewer concurrent streams keep
+// the DRAM pages better (profiles/r01_variants_k2_grid*.json; 3 stages, i.e.
+// more bytes in flight, measured 5% slower).  Results never depend on the grid.
+#ifndef GRASS_UPD_GRID_SUB
+#define GRASS_UPD_GRID_SUB -1  // A/B knob: SMs left out of K2's grid (-1: the tuned default)
+#endif
+#ifndef GRASS_NORM_GRID_SUB
+#define GRASS_NORM_GRID_SUB 0  // A/B knob: SMs left out of K1's grid
+#endif
+int fused_grid(bool update, bool bf16, int device) {
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
-  return sms;
+  if (!update) return sms - GRASS_NORM_GRID_SUB;
+  if (GRASS_UPD_GRID_SUB >= 0) return sms - GRASS_UPD_GRID_SUB;
+  return (sms * (bf16 ? 132 : 128) + 74) / 148;  // 128 / 132 of B200's 148
 }
 
 }  // namespace grass

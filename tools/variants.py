@@ -12,9 +12,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "sep_out": ["GRASS_K2_SEP_OUT"],
+    "norm140": ["GRASS_NORM_GRID_SUB=8"],
+    "norm132": ["GRASS_NORM_GRID_SUB=16"],
+    "norm128": ["GRASS_NORM_GRID_SUB=20"],
+    "norm120": ["GRASS_NORM_GRID_SUB=28"],
     "base_again": [],
-    "sep_out_again": ["GRASS_K2_SEP_OUT"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
