@@ -377,8 +377,16 @@ def run_grass(args, rank, world, local):
                 pctx.close()
             return {"error": err or "setup failed on another rank"}
         pev = []
+        probe_ms = 0.0
         try:
+            pe = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            pe[0].record(s)
+            pctx.mgn_accumulate(list(range(NL)), grads, stream=s)     # probing pass (K1 over peers)
+            pe[1].record(s)
             pctx.mgn_accumulate(list(range(NL)), grads, stream=s)
+            pe[2].record(s)
+            torch.cuda.synchronize()
+            probe_ms = pe[1].elapsed_time(pe[2])
             pctx.update_probs()
             pids = pctx.sample_layers(0)
             for k in range(args.warmup + args.steps):
@@ -404,8 +412,11 @@ def run_grass(args, rank, world, local):
             return {"error": err or "failed on another rank"}
         hbm = BYTES_PER_PARAM_UPDATE * active / world          # per rank: local shard traffic
         link = 8 * active * (world - 1) / world                 # per rank: peer grad reads + theta' stores
+        probe_ms = max_over_ranks(probe_ms, world, dev)
         return {"workload": f"{args.model}-stack gamma={gamma}, P2P fused RS+update+AG kernel, dp{world}",
                 "call_ms": call_ms, "params_per_s": active / (call_ms / 1e3),
+                "probe_call_ms": probe_ms,
+                "probe_hbm_GBps_per_rank": BYTES_PER_PARAM_PROBE * NL * n_p / world / (probe_ms / 1e3) / 1e9,
                 "hbm_GBps_per_rank": hbm / (call_ms / 1e3) / 1e9,
                 "nvlink_bytes_per_rank": link, "calls": len(pev)}
 

@@ -368,13 +368,17 @@ __global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const
 #endif
 constexpr int kUpdTPS = 1, kUpdStages = GRASS_UPD_STAGES;  // 4 arrays x 16 KiB per stage -> 128 KiB ring
 constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 96 KiB x 2 -> 192 KiB
+#ifndef GRASS_P2P_NORM_TPS
+#define GRASS_P2P_NORM_TPS 3
+#endif
+constexpr int kP2PNormTPS = GRASS_P2P_NORM_TPS;  // P2P probing: tiles per gradient-ring slot
 
 template <bool U, int TPS, int ST, bool BF16, bool P2P = false>
 cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStream_t s) {
-  constexpr size_t smem = (size_t)ST * StageLayout<U, BF16, TPS>::bytes +
-                         (P2P ? (size_t)P2PGSlots<BF16>::value * StageLayout<U, BF16, TPS>::kUnit *
-                                    StageLayout<U, BF16, TPS>::GB
-                              : 0);
+  using SL = StageLayout<U, BF16, TPS>;
+  using GS = P2PGSlots<U, BF16>;
+  constexpr size_t smem = (P2P && GS::kNoStageRing ? 0 : (size_t)ST * SL::bytes) +
+                          (P2P ? (size_t)GS::slots(SL::kUnit * SL::GB) * SL::kUnit * SL::GB : 0);
   static_assert(smem <= 227 * 1024, "ring exceeds the 227 KiB shared-memory limit");
   // the opt-in shared-memory size is a per-device function attribute: set it
   // once per device (contexts on several GPUs / threads share this instance)
@@ -404,9 +408,9 @@ cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int gr
   if (b.npeer > 0) {  // P2P data parallelism: one tile per unit, the gradient read from the peers
     if (b.bf16)
       return update ? launch_stream<true, 1, 2, true, true>(b, st, grid, s)
-                    : launch_stream<false, 1, 2, true, true>(b, st, grid, s);
+                    : launch_stream<false, kP2PNormTPS, 2, true, true>(b, st, grid, s);
     return update ? launch_stream<true, 1, 2, false, true>(b, st, grid, s)
-                  : launch_stream<false, 1, 2, false, true>(b, st, grid, s);
+                  : launch_stream<false, kP2PNormTPS, 2, false, true>(b, st, grid, s);
   }
   if (b.bf16)
     return update ? launch_stream<true, kUpdTPS, kUpdStages, true>(b, st, grid, s)

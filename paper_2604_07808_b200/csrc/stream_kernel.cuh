@@ -76,12 +76,16 @@ __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
 
 // P2P (Seg::gpeer): the gradient of a unit is the sum of the npeer ranks'
 // slices in ascending rank order (fp32).  The producer bulk-copies each rank's
-// slice (over NVLink for the peers) into a ring of P2PGSlots<BF16> gradient
-// slots; the consumers add the slices up in registers.  The 0-7 element tail of
-// a segment is summed straight from the ranks' memory (peer_g1).
-template <bool BF16>
+// slice (over NVLink for the peers) into a ring of P2PGSlots gradient slots;
+// the consumers add the slices up in registers.  The 0-7 element tail of a
+// segment is summed straight from the ranks' memory (peer_g1).
+template <bool UPDATE, bool BF16>
 struct P2PGSlots {
-  static constexpr int value = BF16 ? 8 : 4;  // 4 x 16 KiB / 8 x 8 KiB next to the 2-stage ring
+  // update (one-tile units): 64 KiB of slots next to the 2-stage theta/m/v
+  // ring; norm only: the stage ring is unused (nothing but gradients is read)
+  // and the slots take 192 KiB
+  __host__ __device__ static constexpr int slots(int slot_bytes) { return UPDATE ? 65536 / slot_bytes : 196608 / slot_bytes; }
+  static constexpr bool kNoStageRing = !UPDATE;  // (P2P) the stage ring holds no data
 };
 template <bool BF16>
 __device__ __forceinline__ float peer_g1(const void* const* gp, int npeer, int64_t idx) {
@@ -125,12 +129,15 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   __shared__ __align__(8) uint64_t full_bar[STAGES];
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
   __shared__ __align__(8) uint64_t outfree_bar[STAGES];  // L::SEP: output region writable
-  constexpr int NG = P2P ? P2PGSlots<BF16>::value : 1;     // P2P gradient ring
-  constexpr int kGSlot = kUnit * L::GB;
-  static_assert(!P2P || TPS == 1, "P2P units are one tile");
+  constexpr int kGSlot = kUnit * L::GB;  // one rank's slice of a unit
+  constexpr int NG = P2P ? P2PGSlots<UPDATE, BF16>::slots(kGSlot) : 1;  // P2P gradient ring
+  static_assert(!P2P || !UPDATE || TPS == 1, "P2P update units are one tile");
   __shared__ __align__(8) uint64_t gfull_bar[NG];
   __shared__ __align__(8) uint64_t gempty_bar[NG];
-  char* const gring = sbuf + (size_t)STAGES * L::bytes;
+  // P2P norm-only: the stage ring carries nothing, so it is not synchronised at
+  // all and the producer runs ahead as far as the gradient ring allows
+  constexpr bool kRing = !(P2P && P2PGSlots<UPDATE, BF16>::kNoStageRing);
+  char* const gring = sbuf + (kRing ? (size_t)STAGES * L::bytes : 0);
   __shared__ int unit_prefix[kMaxSeg + 1];
   __shared__ int seg_done[kMaxSeg];
   __shared__ double red[2][TPS][kConsumerWarps];
@@ -172,7 +179,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
         const int stage = i % STAGES;
         char* stg = sbuf + (size_t)stage * L::bytes;
-        if (i >= STAGES) {
+        if (kRing && i >= STAGES) {
           mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
           if (TS) {
             store_unit_t<BF16, P2P, L>(b.seg[pend_s[stage]], b.npeer, pend_e0[stage], pend_nv[stage], stg);
@@ -205,7 +212,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
             bulk_load(stg + L::off_m, sg.m + e0, nv * 4u, &full_bar[stage], pol);
             bulk_load(stg + L::off_v, sg.v + e0, nv * 4u, &full_bar[stage], pol);
           }
-        } else {
+        } else if (kRing) {
           mbar_arrive(&full_bar[stage]);
         }
         if (P2P && nv) {  // every rank's gradient slice of this unit, in rank order
@@ -261,23 +268,24 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
     char* stg = sbuf + (size_t)stage * L::bytes;
     const int64_t pe0 = P2P ? sg.poff + e0 : 0;  // full-layer index of the unit's element 0
-    mbar_wait(&full_bar[stage], (i / STAGES) & 1);
+    if (kRing) mbar_wait(&full_bar[stage], (i / STAGES) & 1);
     if (L::SEP) mbar_wait(&outfree_bar[stage], (i / STAGES) & 1);
-    float4 gacc[kUnroll];  // P2P: this thread's summed gradient of the unit
+    float4 gacc[P2P ? TPS : 1][kUnroll];  // P2P: this thread's summed gradient of the unit
     if (P2P && nv) {
       for (int r = 0; r < b.npeer; ++r, ++gcount) {
         const int gsl = gcount % NG;
         mbar_wait(&gfull_bar[gsl], (gcount / NG) & 1);
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-          const int e = (q * kThreads + tid) * kVec;
-          if (e < nv) {
-            const float4 x = stage_g4<BF16>(gring + (size_t)gsl * kGSlot, e);
-            if (r == 0) {
-              gacc[q] = x;
-            } else {
-              if (!(kMutant == 6 && r == b.npeer - 1)) {  // M6: last rank's slice dropped
-                gacc[q].x += x.x; gacc[q].y += x.y; gacc[q].z += x.z; gacc[q].w += x.w;
+        for (int k = 0; k < (P2P ? TPS : 1); ++k) {
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const int e = k * (int)kTile + (q * kThreads + tid) * kVec;
+            if (e < nv) {
+              const float4 x = stage_g4<BF16>(gring + (size_t)gsl * kGSlot, e);
+              if (r == 0) {
+                gacc[k][q] = x;
+              } else if (!(kMutant == 6 && r == b.npeer - 1)) {  // M6: last rank's slice dropped
+                gacc[k][q].x += x.x; gacc[k][q].y += x.y; gacc[k][q].z += x.z; gacc[k][q].w += x.w;
               }
             }
           }
@@ -327,7 +335,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           for (int q = 0; q < kUnroll; ++q) {
             const int e = k * (int)kTile + (q * kThreads + tid) * kVec;  // relative to e0
             if (e < nv) {
-              const float4 g4 = scale4(P2P ? gacc[q] : stage_g4<BF16>(stg + L::off_g, e), gs);
+              const float4 g4 = scale4(P2P ? gacc[P2P ? k : 0][q] : stage_g4<BF16>(stg + L::off_g, e), gs);
               acc[0] = fma((double)g4.x, (double)g4.x, acc[0]);
               acc[1] = fma((double)g4.y, (double)g4.y, acc[1]);
               acc[2] = fma((double)g4.z, (double)g4.z, acc[2]);
@@ -402,7 +410,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     }
     if (UPDATE && kTmaStore) fence_proxy_async_smem();  // results visible to the bulk store
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[stage]);  // this warp is done with the stage
+    if (kRing && lane == 0) mbar_arrive(&empty_bar[stage]);  // this warp is done with the stage
     consumer_sync();
     if (tid < ntiles) {  // lane k of warp 0 finishes tile k (warp sums in ascending order)
       double p = 0.0;

@@ -11,12 +11,11 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "base": [],
-    "norm140": ["GRASS_NORM_GRID_SUB=8"],
-    "norm132": ["GRASS_NORM_GRID_SUB=16"],
-    "norm128": ["GRASS_NORM_GRID_SUB=20"],
-    "norm120": ["GRASS_NORM_GRID_SUB=28"],
-    "base_again": [],
+    "p2pn3": [],
+    "p2pn2": ["GRASS_P2P_NORM_TPS=2"],
+    "p2pn4": ["GRASS_P2P_NORM_TPS=4"],
+    "p2pn6": ["GRASS_P2P_NORM_TPS=6"],
+    "p2pn1": ["GRASS_P2P_NORM_TPS=1"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
@@ -29,7 +28,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main,probe,bf16", extra=()):
+def run(legs="main,p2p", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
@@ -40,7 +39,9 @@ def run(legs="main,probe,bf16", extra=()):
             res[name] = {"kernel_ms": d["roofline"]["kernel_ms"], "frac": d["roofline"]["frac"],
                          "step_ms": d["ms_per_step"],
                          "probe_GBps": (d.get("probe") or {}).get("GBps"),
-                         "bf16_kernel_ms": (d.get("bf16") or {}).get("kernel_ms")}
+                         "bf16_kernel_ms": (d.get("bf16") or {}).get("kernel_ms"),
+                         "p2p_probe_ms": (d.get("p2p") or {}).get("probe_call_ms"),
+                         "p2p_call_ms": (d.get("p2p") or {}).get("call_ms")}
         except Exception:
             res[name] = {"error": r.stderr[-2000:]}
         print(name, res[name], flush=True)
