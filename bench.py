@@ -622,7 +622,15 @@ def run_grass(args, rank, world, local):
                for l in range(NL)]
         bctx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, device=local,
                        rank=rank, world=world, param_dtype=G.DTYPE_BF16)
-        bctx.mgn_accumulate(list(range(NL)), g16, stream=s)
+        bp = []
+        for _ in range(3):                       # bf16 probing pass (K1, 2 B/param)
+            e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            e[0].record(s)
+            bctx.mgn_accumulate(list(range(NL)), g16, stream=s)
+            e[1].record(s)
+            bp.append(e)
+        torch.cuda.synchronize()
+        bprobe_ms = min(a.elapsed_time(b) for a, b in bp[1:])
         bctx.update_probs()
         bids = bctx.sample_layers(0)
         bev = []
@@ -655,7 +663,8 @@ def run_grass(args, rank, world, local):
         return {"workload": f"{args.model}-stack gamma={gamma} bf16 params/grads, fp32 master+m+v, resident",
                 "params_per_s": args.steps * active / bt, "step_ms": bt / args.steps * 1e3,
                 "kernel_ms": bk, "GBps": bgbs, "frac_hbm": bgbs / hbm_peak,
-                "bytes_per_param": BYTES_PER_PARAM_UPDATE}
+                "bytes_per_param": BYTES_PER_PARAM_UPDATE,
+                "probe_ms": bprobe_ms, "probe_GBps": 2 * NL * n_p / world / (bprobe_ms / 1e3) / 1e9}
 
     bf16 = guarded("bf16", leg_bf16)
 

@@ -368,6 +368,10 @@ __global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const
 #endif
 constexpr int kUpdTPS = 1, kUpdStages = GRASS_UPD_STAGES;  // 4 arrays x 16 KiB per stage -> 128 KiB ring
 constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 96 KiB x 2 -> 192 KiB
+#ifndef GRASS_NORM_TPS_BF16
+#define GRASS_NORM_TPS_BF16 12  // 96 KiB units like fp32 (+17% over 6 tiles, profiles/r01_variants_bf16_k1_tps.json)
+#endif
+constexpr int kNormTPSBf16 = GRASS_NORM_TPS_BF16;  // bf16 probing: tiles per unit (2 B/element)
 #ifndef GRASS_P2P_NORM_TPS
 #define GRASS_P2P_NORM_TPS 3
 #endif
@@ -414,7 +418,7 @@ cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int gr
   }
   if (b.bf16)
     return update ? launch_stream<true, kUpdTPS, kUpdStages, true>(b, st, grid, s)
-                  : launch_stream<false, kNormTPS, kNormStages, true>(b, st, grid, s);
+                  : launch_stream<false, kNormTPSBf16, kNormStages, true>(b, st, grid, s);
   return update ? launch_stream<true, kUpdTPS, kUpdStages, false>(b, st, grid, s)
                 : launch_stream<false, kNormTPS, kNormStages, false>(b, st, grid, s);
 }

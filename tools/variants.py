@@ -11,11 +11,11 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "p2pn3": [],
-    "p2pn2": ["GRASS_P2P_NORM_TPS=2"],
-    "p2pn4": ["GRASS_P2P_NORM_TPS=4"],
-    "p2pn6": ["GRASS_P2P_NORM_TPS=6"],
-    "p2pn1": ["GRASS_P2P_NORM_TPS=1"],
+    "bn6": [],
+    "bn12": ["GRASS_NORM_TPS_BF16=12"],
+    "bn8": ["GRASS_NORM_TPS_BF16=8"],
+    "bn12_again": ["GRASS_NORM_TPS_BF16=12"],
+    "bn6_again": [],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
@@ -28,7 +28,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main,p2p", extra=()):
+def run(legs="main,bf16", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
@@ -41,6 +41,7 @@ def run(legs="main,p2p", extra=()):
                          "probe_GBps": (d.get("probe") or {}).get("GBps"),
                          "bf16_kernel_ms": (d.get("bf16") or {}).get("kernel_ms"),
                          "p2p_probe_ms": (d.get("p2p") or {}).get("probe_call_ms"),
+                         "bf16_probe_ms": (d.get("bf16") or {}).get("probe_ms"),
                          "p2p_call_ms": (d.get("p2p") or {}).get("call_ms")}
         except Exception:
             res[name] = {"error": r.stderr[-2000:]}
