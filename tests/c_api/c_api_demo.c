@@ -3,7 +3,9 @@
  *   - Eq. 2 on g = [3, 4]: r = sqrt(25 / 2);
  *   - one AdamW step with g = 1, lr = 0.1, theta = 0: theta' = -0.1 / (1 + 1e-8)
  *     (bias correction cancels at t = 1);
- *   - gamma = N_L sampling returns every layer once.
+ *   - gamma = N_L sampling returns every layer once;
+ *   - the P2P data-parallel path (world 1) gives the same AdamW step, and the
+ *     P2P barrier self-test reports no mismatch.
  * Exit code 0 on success.  Build: see tests/test_c_api.py. */
 #include <cuda_runtime_api.h>
 #include <math.h>
@@ -78,6 +80,35 @@ int main(void) {
   if (t != 1) return 6;
 
   grass_destroy(ctx);
+
+  /* P2P data parallelism at world 1: register the buffers, one step */
+  grass_config pc;
+  if (grass_config_init(&pc) != GRASS_OK) return 7;
+  pc.n_layers = 2;
+  pc.layer_numel = numel;
+  pc.gamma = 2;
+  pc.dp_mode = GRASS_DP_P2P;
+  CHECK(grass_create(&pc, &ctx));
+  void* blk = NULL;
+  int64_t blk_bytes = 0;
+  CHECK(grass_p2p_exchange_block(ctx, &blk, &blk_bytes));
+  CHECK(grass_p2p_attach(ctx, &blk));
+  cudaMemset(p1, 0, 4096 * sizeof(float));
+  void* pp[1] = {p1};
+  const void* gg[1] = {g1};
+  CHECK(grass_p2p_register_layer(ctx, 1, pp, gg));
+  CHECK(grass_step_layers(ctx, one, 1, params, g, 0.1f, NULL));
+  CHECK(grass_sync(ctx));
+  cudaMemcpy(h1, p1, 4096 * sizeof(float), cudaMemcpyDeviceToHost);
+  for (int i = 0; i < 4096; ++i)
+    if (fabs(h1[i] - want) > 1e-5 * fabs(want)) return 8;
+  grass_destroy(ctx);
+  ctx = NULL;
+  int64_t mismatches = -1;
+  int32_t timed_out = -1;
+  CHECK(grass_selftest_p2p(0, 4, 200, &mismatches, &timed_out));
+  if (mismatches != 0 || timed_out != 0) return 9;
+
   cudaFree(g0);
   cudaFree(g1);
   cudaFree(p1);
