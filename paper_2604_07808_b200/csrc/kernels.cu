@@ -161,6 +161,16 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t 
                : "memory");
 #endif
 }
+// L2 prefetch of a future unit (A/B knob GRASS_L2_PREFETCH_{NORM,UPD} = units ahead)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+#ifndef GRASS_L2_PREFETCH_NORM
+#define GRASS_L2_PREFETCH_NORM 0
+#endif
+#ifndef GRASS_L2_PREFETCH_UPD
+#define GRASS_L2_PREFETCH_UPD 0
+#endif
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

@@ -215,6 +215,22 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         } else if (kRing) {
           mbar_arrive(&full_bar[stage]);
         }
+        constexpr int kPf = P2P ? 0 : (UPDATE ? GRASS_L2_PREFETCH_UPD : GRASS_L2_PREFETCH_NORM);
+        if (kPf > 0) {  // warm L2 with this CTA's unit kPf rounds ahead (same segment only)
+          const int uf = u + kPf * (int)gridDim.x;
+          if (uf < total && uf < unit_prefix[s + 1]) {
+            const int64_t f0 = (int64_t)(uf - unit_prefix[s]) * kUnit;
+            const uint32_t fn = (uint32_t)(min((int64_t)kUnit, sg.n - f0) & ~(int64_t)(L::vec - 1));
+            if (fn) {
+              bulk_prefetch_l2(BF16 ? (const void*)(sg.g16 + f0) : (const void*)(sg.g + f0), fn * (uint32_t)L::GB);
+              if (UPDATE) {
+                bulk_prefetch_l2(sg.theta + f0, fn * 4u);
+                bulk_prefetch_l2(sg.m + f0, fn * 4u);
+                bulk_prefetch_l2(sg.v + f0, fn * 4u);
+              }
+            }
+          }
+        }
         if (P2P && nv) {  // every rank's gradient slice of this unit, in rank order
           for (int r = 0; r < b.npeer; ++r, ++gcount) {
             const int gsl = gcount % NG;

@@ -11,11 +11,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "bn6": [],
-    "bn12": ["GRASS_NORM_TPS_BF16=12"],
-    "bn8": ["GRASS_NORM_TPS_BF16=8"],
-    "bn12_again": ["GRASS_NORM_TPS_BF16=12"],
-    "bn6_again": [],
+    "base": [],
+    "pfn1": ["GRASS_L2_PREFETCH_NORM=1"],
+    "pfn2": ["GRASS_L2_PREFETCH_NORM=2"],
+    "pfu1": ["GRASS_L2_PREFETCH_UPD=1"],
+    "base_again": [],
+    "pfn1_again": ["GRASS_L2_PREFETCH_NORM=1"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
@@ -28,7 +29,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main,bf16", extra=()):
+def run(legs="main,probe", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
