@@ -147,6 +147,11 @@ typedef struct grass_config {
                                   0 = no barriers: the caller orders the ranks' calls and calls
                                   grass_p2p_finish on every rank afterwards (single-process,
                                   multi-context testing on one GPU). */
+  int32_t debug_check;         /* 1: grass_update_probs also verifies that every rank holds
+                                  bit-identical MGN and probabilities (a 64-bit hash of both
+                                  is all-gathered over NCCL / the P2P exchange blocks;
+                                  SURVEY 8(e) debug mode) and returns GRASS_E_STATE if not.
+                                  Makes grass_update_probs a collective.  0 = off (default). */
 } grass_config;
 
 typedef enum {

@@ -55,7 +55,7 @@ class GrassConfig(C.Structure):
         ("ring_slots", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("residency", C.c_int32), ("cache_layers", C.c_int32),
         ("max_grad_norm", C.c_double), ("param_dtype", C.c_int32), ("n_always", C.c_int32),
-        ("dp_mode", C.c_int32), ("p2p_sync", C.c_int32),
+        ("dp_mode", C.c_int32), ("p2p_sync", C.c_int32), ("debug_check", C.c_int32),
     ]
 
 
@@ -251,7 +251,8 @@ class Grass:
                  chunk_elems: int = 0, ring_slots: int = 0, rank: int = 0, world: int = 1,
                  process_group=None, force_nccl: bool = False, residency: int = RESIDENCY_STEP,
                  cache_layers: int = 0, max_grad_norm: float = 0.0, param_dtype: int = DTYPE_FP32,
-                 n_always: int = 0, dp_mode: int = DP_NCCL, p2p_sync: bool = True):
+                 n_always: int = 0, dp_mode: int = DP_NCCL, p2p_sync: bool = True,
+                 debug_check: bool = False):
         L = lib()
         self.layer_numel = [int(x) for x in layer_numel]
         self.n_layers = len(self.layer_numel)
@@ -279,6 +280,7 @@ class Grass:
         cfg.param_dtype = param_dtype
         cfg.n_always = self.n_always
         cfg.dp_mode, cfg.p2p_sync = dp_mode, int(p2p_sync)
+        cfg.debug_check = int(debug_check)
         self.dp_mode = dp_mode
         self.bf16 = param_dtype == DTYPE_BF16
         self._uid = None

@@ -228,6 +228,7 @@ grass_status comm_rs(grass_ctx* c, int j, const void* grad, int64_t len);
 grass_status comm_wait_rs(grass_ctx* c, int j, cudaStream_t s);
 grass_status comm_after_update(grass_ctx* c, int j, void* params, int64_t off, int64_t len, cudaStream_t s);
 grass_status comm_end(grass_ctx* c, cudaStream_t s);
+grass_status cross_rank_check(grass_ctx* c);
 
 // offload.cpp
 grass_status update_range(grass_ctx* c, int l, const Seg& base, void* param, const void* g, int64_t off, int64_t n, float* const* state, bool init, int32_t mode, cudaStream_t s, const void* g_chunk = nullptr);

@@ -176,4 +176,49 @@ grass_status comm_end(grass_ctx* c, cudaStream_t s) {
 }
 
 
+// Debug mode (cfg.debug_check): every rank must hold
+// bit-identical committed MGN and probabilities (they drive the sampler, so
+// identical ids follow).  A 64-bit FNV-1a hash of both is all-gathered — over
+// NCCL, or published through the P2P exchange blocks with an end barrier —
+// and compared with this rank's.
+grass_status cross_rank_check(grass_ctx* c) {
+  if (!c->cfg.debug_check) return GRASS_OK;
+  const bool nccl = c->dp, p2p = c->p2p && c->cfg.p2p_sync;
+  if (!nccl && !p2p) return GRASS_OK;  // one rank, or P2P without barriers
+  if (p2p && (int)c->exch_peer.size() != c->cfg.world)
+    return c->fail(GRASS_E_STATE, "debug check: call grass_p2p_attach first");
+  uint64_t h = 0xcbf29ce484222325ull;
+  auto mix = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+  };
+  mix(c->probs.data(), sizeof(double) * c->probs.size());
+  mix(c->mgn.data(), sizeof(double) * c->mgn.size());
+  double hd;
+  std::memcpy(&hd, &h, sizeof(hd));  // all-gathers copy bits, never add
+  const int W = c->cfg.world, r = c->cfg.rank;
+  std::vector<double> all(W, 0.0);
+  cudaStream_t s = c->aux;
+  if (nccl) {
+    CUDA_TRY(c, cudaMemcpy(c->d_gather + r, &hd, sizeof(hd), cudaMemcpyHostToDevice));
+    if (!c->comm.all_gather_f64(c->d_gather + r, c->d_gather, 1, s, &c->err)) return GRASS_E_NCCL;
+    c->launches++;
+    CUDA_TRY(c, cudaMemcpyAsync(all.data(), c->d_gather, sizeof(double) * W, cudaMemcpyDeviceToHost, s));
+  } else {
+    CUDA_TRY(c, cudaMemcpy(c->st.shard_ss, &hd, sizeof(hd), cudaMemcpyHostToDevice));
+    P2PSyncArgs a = p2p_args(c, 1);
+    a.n = 1;
+    a.shard_ss = c->st.shard_ss;
+    CUDA_TRY(c, launch_p2p_sync(a, s));
+    c->launches++;
+    CUDA_TRY(c, cudaMemcpyAsync(all.data(), c->d_exch + kExchGather, sizeof(double) * W, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  for (int q = 0; q < W; ++q)
+    if (std::memcmp(&all[q], &hd, sizeof(hd)) != 0)
+      return c->fail(GRASS_E_STATE, "debug check: rank " + std::to_string(q) + "'s MGN / probabilities differ from rank " +
+                                        std::to_string(r) + "'s (ranks diverged)");
+  return GRASS_OK;
+}
+
 }  // namespace gapi

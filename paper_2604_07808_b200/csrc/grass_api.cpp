@@ -141,6 +141,7 @@ grass_status grass_update_probs(grass_ctx* c, double* probs_out) try {
   } else if (c->cfg.policy == GRASS_POLICY_ADAPTIVE || first) {
     softmax_probs(c->mgn.data(), c->nsamp, c->cfg.tau, c->cfg.normalize_mgn != 0, c->probs.data());
   }
+  if ((s = cross_rank_check(c)) != GRASS_OK) return s;
   if (probs_out) std::memcpy(probs_out, c->probs.data(), sizeof(double) * c->nl);
   return GRASS_OK;
 } catch (...) {

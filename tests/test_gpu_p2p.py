@@ -408,3 +408,28 @@ def test_p2p_full_size_7b_layers_four_ranks():
         m_all = np.concatenate([c.read_state(l)[0] for c in vr.ctx])   # rank shards, in order
         s_m = np.maximum(np.abs(m_o), 0.1 * np.abs(g_s))
         assert (np.abs(m_all[idx] - m_o) <= 1e-5 * s_m + 1e-30).all()
+
+
+@pytest.mark.parametrize("path", ["nccl", "p2p"])
+def test_debug_check_world1(path):
+    """debug_check: grass_update_probs all-gathers a hash of the MGN and the
+    probabilities (NCCL, or the P2P exchange blocks + end barrier) and compares
+    them — at world 1 the path runs and agrees with itself."""
+    numel = [4096 * 3, 8192]
+    kw = dict(gamma=1, T_p=1, T_s=1, debug_check=True)
+    gr = (G.Grass(numel, force_nccl=True, **kw) if path == "nccl"
+          else G.Grass(numel, dp_mode=G.DP_P2P, **kw))
+    g = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
+    if path == "p2p":
+        gr.p2p_attach([gr.p2p_exchange_block()[0]])
+        p = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+        for l in range(2):
+            gr.p2p_register_layer(l, [p[l]], [g[l]])
+    before = gr.launch_count
+    gr.mgn_accumulate([0, 1], g)
+    probs = gr.update_probs()
+    assert abs(sum(probs) - 1.0) < 1e-12
+    assert gr.launch_count >= before + 2      # the norm launches plus the check's collective
+    plain = G.Grass(numel, **{k: v for k, v in kw.items() if k != "debug_check"})
+    plain.mgn_accumulate([0, 1], g)
+    assert plain.update_probs() == probs
