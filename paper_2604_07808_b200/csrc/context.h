@@ -3,6 +3,7 @@
 // offload.cpp, dataparallel.cpp, checkpoint.cpp, grass_api.cpp).  Not ABI.
 #pragma once
 #include <cuda_runtime_api.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <climits>
 #include <cstdint>
@@ -160,11 +161,32 @@ inline const void* elem(const void* p, int64_t off, size_t esz) {
 // ---- tracing ---------------------------------------------------------------
 // Brackets one device operation on stream `s`: `begin` before issuing it,
 // `end` after.  A no-op unless tracing is enabled.
+// Also an NVTX range (domain "grass", message = the operation, payload = the
+// layer id) around the host-side issue of the operation, so an nsys timeline
+// shows every fetch / update / write-back / collective the library enqueues
+// (SURVEY 5); NVTX calls are no-ops unless a tool is attached.
+inline nvtxDomainHandle_t nvtx_domain() {
+  static nvtxDomainHandle_t d = nvtxDomainCreateA("grass");
+  return d;
+}
+inline void nvtx_push(int kind, int layer) {
+  static const char* const names[] = {"grass.h2d", "grass.update", "grass.d2h", "grass.norm",
+                                      "grass.reduce_scatter", "grass.all_gather", "grass.p2p_sync"};
+  nvtxEventAttributes_t a = {};
+  a.version = NVTX_VERSION;
+  a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+  a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+  a.message.ascii = (kind >= 0 && kind < 7) ? names[kind] : "grass.op";
+  a.payloadType = NVTX_PAYLOAD_TYPE_INT64;
+  a.payload.llValue = layer;
+  nvtxDomainRangePushEx(nvtx_domain(), &a);
+}
 struct TraceScope {
   grass_ctx* c;
   cudaStream_t s;
   int idx = -1;
   TraceScope(grass_ctx* c_, cudaStream_t s_, int kind, int layer, int64_t off, int64_t n) : c(c_), s(s_) {
+    nvtx_push(kind, layer);
     if (!c->tracing) return;
     cudaEvent_t e[2];
     for (auto& x : e) {
@@ -181,6 +203,7 @@ struct TraceScope {
   }
   ~TraceScope() {
     if (idx >= 0) cudaEventRecord(c->trace[idx].e1, s);
+    nvtxDomainRangePop(nvtx_domain());
   }
 };
 

@@ -13,6 +13,10 @@
 Always-active groups (Grass(n_always=k): embedding / head, DESIGN R19) are not
 probed or sampled; they join every adaptive step's update.
 
+trace_path: optional JSON-lines log of the sampling state (SPEC.md:313's
+prob-trace): one record per commit {"step", "event": "commit", "m", "p"} and
+per resample {"step", "event": "resample", "period", "sampled"}.
+
 Host logic only: every step of the hot path runs in libgrass.so.
 
     sched = GrassSchedule(grass)
@@ -23,6 +27,7 @@ Host logic only: every step of the hot path runs in libgrass.so.
 """
 from __future__ import annotations
 
+import json
 from typing import Sequence
 
 from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_PROBE, DECIDE_RESAMPLE, Grass,
@@ -30,8 +35,9 @@ from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_PROBE, DECIDE_RESAMPLE, Gra
 
 
 class GrassSchedule:
-    def __init__(self, grass: Grass, prefetch: bool | None = None):
+    def __init__(self, grass: Grass, prefetch: bool | None = None, trace_path: str | None = None):
         self.g = grass
+        self.trace_path = trace_path
         cfg = grass.cfg
         self.T_p, self.T_s, self.T_u = cfg.T_p, cfg.T_s, cfg.T_u
         self.n_layers = grass.n_layers
@@ -55,9 +61,15 @@ class GrassSchedule:
             return list(range(self.n_sampled))
         if d == DECIDE_COMMIT_RESAMPLE:
             self.probs = self.g.update_probs()
+            if self.trace_path:
+                m = self.g.get_mgn()["m"] if hasattr(self.g, "get_mgn") else None
+                self._log({"step": step, "event": "commit", "m": m, "p": self.probs})
         if d in (DECIDE_COMMIT_RESAMPLE, DECIDE_RESAMPLE) or not self.trainable:
             self.period_index = (step - self.T_p) // self.T_s
             self.trainable = self.g.sample_layers(self.period_index)
+            if self.trace_path:
+                self._log({"step": step, "event": "resample", "period": self.period_index,
+                           "sampled": list(self.trainable)})
             if self.prefetch:
                 self.g.prefetch_layers(self.trainable, stream=stream)
         return list(self.trainable) + self.always
@@ -74,3 +86,7 @@ class GrassSchedule:
             if len(params) != len(layers):
                 raise ValueError("one parameter buffer per trainable layer")
             self.g.step_layers(layers, params, grads, lr, stream=stream)
+
+    def _log(self, rec: dict):
+        with open(self.trace_path, "a") as f:
+            f.write(json.dumps(rec) + "\n")

@@ -83,3 +83,19 @@ def test_schedule_always_groups_join_every_update_and_skip_probing():
     updates = [c[1] for c in g.calls if c[0] == "update"]
     assert all(u[-2:] == (4, 5) for u in updates) and len(updates) == 4
     assert [c for c in g.calls if c[0] == "probe"] == [("probe", 4), ("probe", 4)]
+
+
+def test_schedule_prob_trace_jsonl(tmp_path):
+    # SPEC.md:313 prob-trace: one JSON line per commit (m, p) and per resample (sampled ids)
+    import json
+    g = FakeGrass(4, T_p=2, T_s=2, T_u=4)
+    path = tmp_path / "probs.jsonl"
+    s = GrassSchedule(g, trace_path=str(path))
+    for step in range(9):
+        layers = s.begin_step(step)
+        s.end_step(step, [None] * len(layers), [None] * len(layers), 1e-3)
+    recs = [json.loads(line) for line in path.read_text().splitlines()]
+    assert [r["event"] for r in recs] == ["commit", "resample", "resample", "commit", "resample",
+                                         "resample"]
+    assert [r["step"] for r in recs] == [2, 2, 4, 6, 6, 8]
+    assert recs[0]["p"] == [0.25] * 4 and recs[1]["sampled"] == [0, 1] and recs[2]["period"] == 1
