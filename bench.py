@@ -418,7 +418,8 @@ def run_grass(args, rank, world, local):
                 "probe_call_ms": probe_ms,
                 "probe_hbm_GBps_per_rank": BYTES_PER_PARAM_PROBE * NL * n_p / world / (probe_ms / 1e3) / 1e9,
                 "hbm_GBps_per_rank": hbm / (call_ms / 1e3) / 1e9,
-                "nvlink_bytes_per_rank": link, "calls": len(pev)}
+                "nvlink_bytes_per_rank": link, "calls": len(pev),
+                "nvlink_GBps_per_rank": link / (call_ms / 1e3) / 1e9 if world > 1 else None}
 
 
     # ---- offload leg: configs[2] (row a6)
@@ -702,6 +703,11 @@ def run_grass(args, rank, world, local):
                          "kernel_ms": kernel_ms, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            # world > 1: NCCL reduce-scatter of the gradients + all-gather of the
+            # parameters, (W-1)/W of 4 B per active parameter each, per rank
+            "dp_comm": ({"bytes_per_rank_per_step": 8 * active * (world - 1) // world,
+                         "GBps_per_rank": 8 * active * (world - 1) / world / (elapsed / args.steps) / 1e9}
+                        if world > 1 else None),
             "clocks": clk.summary(), "probe": out.get("probe"), "offload": offload,
             "offload_period": offload_period, "bf16": bf16, "train_step": train, "p2p": p2p,
             "paper_context": {
