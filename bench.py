@@ -457,6 +457,7 @@ def run_grass(args, rank, world, local):
                "h2d_bytes": link_bytes, "d2h_bytes": link_bytes,
                "link_GBps_per_dir": link_bytes / ot / 1e9,
                "duplex_GBps_per_dir_measured": duplex,
+               "frac_of_pcie5_x16_nominal": link_bytes / ot / 1e9 / 63.0,  # 64 GT/s x16, 128b/130b
                "floor_ms": floor * 1e3, "frac_of_link_floor": floor / ot,
                "R1_within_10pct_of_link_floor": ot <= 1.10 * floor,
                "R2_offload_over_resident": ot / (elapsed / args.steps),
