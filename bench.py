@@ -693,10 +693,12 @@ def run_grass(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{args.model}-stack gamma={gamma} no-offload (configs[1])",
+            "config": {"workload": f"{args.model}-stack gamma={gamma} no-offload" +
+                                   (" (configs[1])" if (args.model, gamma) == ("llama2-7b", 2) else ""),
                        "n_layers": NL, "layer_numel": n_p, "gamma": gamma,
                        "active_params_per_step": active, "schedule": "resample every step (T_s=T_u=1)",
-                       "l2": "no flush: 11.3 GB streamed per step >> 126 MB L2",
+                       "l2": f"no flush: {BYTES_PER_PARAM_UPDATE * active / 1e9:.1f} GB streamed per step "
+                             ">> 126 MB L2",
                        "parallelism": f"dp{world} element-sharded" if world > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
