@@ -199,7 +199,9 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.model}-stack gamma={args.gamma} no-offload (configs[1]), oracle sample",
+        "config": {"workload": f"{args.model}-stack gamma={args.gamma} no-offload" +
+                               (" (configs[1])" if (args.model, args.gamma) == ("llama2-7b", 2) else "") +
+                               ", oracle sample",
                    "n_layers": 32, "layer_numel": n_p, "sample_per_layer": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
