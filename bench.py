@@ -181,6 +181,19 @@ def oracle_sample_time(n_p: int, gamma: int, sample_per_layer: int, lr: float, r
     return times
 
 
+def workload_config(model: str, gamma: int, world: int) -> dict:
+    """The `config` of the JSON line, identical for the GRASS and reference arms."""
+    from synth import MODELS
+    shape = MODELS[model]
+    active = gamma * shape.layer_numel
+    return {"workload": f"{model}-stack gamma={gamma} no-offload" +
+                        (" (configs[1])" if (model, gamma) == ("llama2-7b", 2) else ""),
+            "n_layers": shape.n_layers, "layer_numel": shape.layer_numel, "gamma": gamma,
+            "active_params_per_step": active, "schedule": "resample every step (T_s=T_u=1)",
+            "l2": f"no flush: {BYTES_PER_PARAM_UPDATE * active / 1e9:.1f} GB streamed per step >> 126 MB L2",
+            "parallelism": f"dp{world} element-sharded" if world > 1 else "single GPU"}
+
+
 # ------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
     if rank != 0:
@@ -199,10 +212,7 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{args.model}-stack gamma={args.gamma} no-offload" +
-                               (" (configs[1])" if (args.model, args.gamma) == ("llama2-7b", 2) else "") +
-                               ", oracle sample",
-                   "n_layers": 32, "layer_numel": n_p, "sample_per_layer": sample},
+        "config": workload_config(args.model, args.gamma, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -695,13 +705,7 @@ def run_grass(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{args.model}-stack gamma={gamma} no-offload" +
-                                   (" (configs[1])" if (args.model, gamma) == ("llama2-7b", 2) else ""),
-                       "n_layers": NL, "layer_numel": n_p, "gamma": gamma,
-                       "active_params_per_step": active, "schedule": "resample every step (T_s=T_u=1)",
-                       "l2": f"no flush: {BYTES_PER_PARAM_UPDATE * active / 1e9:.1f} GB streamed per step "
-                             ">> 126 MB L2",
-                       "parallelism": f"dp{world} element-sharded" if world > 1 else "single GPU"},
+            "config": workload_config(args.model, gamma, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "grass_stream_kernel<true,1,2> (fused Eq.2 norm + AdamW, TMA bulk-copy ring)",
