@@ -1210,3 +1210,36 @@ def test_example_training_loop_loss_decreases():
     losses = mod.train(steps=60, log=False)
     assert all(np.isfinite(losses))
     assert np.mean(losses[-10:]) < 0.7 * np.mean(losses[:5])
+
+
+@pytest.mark.parametrize("alpha,tau,normalize", [(0.0, 1.0, True), (1.0, 0.3, True), (0.5, 1e-4, False),
+                                                 (0.25, 50.0, False)])
+def test_commit_ema_softmax_parameter_sweep_vs_oracle(alpha, tau, normalize):
+    """Eq. 4 at its limits (alpha = 0: frozen estimate, alpha = 1: last window),
+    Eq. 3 with raw / max-normalised MGN and extreme temperatures, three commits
+    with partial observation (frozen layers retained): library == oracle."""
+    numel = [4096 * 2 + 4, 4096, 12_288, 8192, 4100]
+    gr = G.Grass(numel, gamma=2, T_p=1, T_s=1, tau=tau, alpha=alpha, normalize_mgn=normalize)
+    orc = O.GrassOracle(numel, gamma=2, tau=tau, alpha=alpha, normalize=normalize)
+    rng = np.random.default_rng(3)
+    for window in range(3):
+        observed = range(5) if window == 0 else sorted(rng.choice(5, 2, replace=False).tolist())
+        for rep in range(2):
+            gs = [layer_grad(numel[l], l, float(10.0 ** rng.uniform(-5, -2)), step=window * 10 + rep, device=DEV)
+                  for l in observed]
+            gr.mgn_accumulate(list(observed), gs)
+            orc.accumulate(list(observed), [_np(g) for g in gs])
+        p_gpu, p_orc = gr.update_probs(), orc.update_probs()
+        assert p_gpu == pytest.approx(p_orc, rel=1e-9, abs=1e-300), (window, p_gpu, p_orc)
+        assert gr.get_mgn()["m"] == pytest.approx(orc.mgn.m, rel=1e-7)
+        for period in range(20):
+            assert gr.sample_layers(period, p_gpu) == O.sample_layers(p_gpu, 2, 1234, period)
+
+
+def test_all_zero_gradients_give_uniform_probabilities():
+    """m = 0 everywhere under max-normalisation (R3, SPEC 8(c) #17) -> uniform p."""
+    numel = [4096, 8192, 4100]
+    gr = G.Grass(numel, gamma=1, T_p=1, T_s=1)
+    gr.mgn_accumulate([0, 1, 2], [torch.zeros(n, device=DEV) for n in numel])
+    assert gr.update_probs() == [1 / 3] * 3
+    assert gr.get_mgn()["last_ss"] == [0.0, 0.0, 0.0]
