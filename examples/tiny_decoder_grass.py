@@ -1,6 +1,7 @@
 """Training a tiny decoder-only transformer with GRASS through libgrass.
 
-What the caller does (the library's boundary, include/grass.h):
+What the caller does (the library's boundary, include/grass.h), here through
+paper_2604_07808_b200.GrassBlocks:
   * each decoder block's parameters live in ONE flat fp32 buffer (the
     parameters are views into it), and so do their gradients;
   * the schedule (GrassSchedule) says which blocks need gradients; the other
@@ -59,52 +60,28 @@ class TinyDecoder(nn.Module):
         return self.head(x)
 
 
-def flatten_params(params):
-    """Re-home parameters and their gradients into two flat fp32 buffers."""
-    params = list(params)
-    n = sum(p.numel() for p in params)
-    flat = torch.empty(n, device=params[0].device)
-    gflat = torch.zeros(n, device=params[0].device)
-    off = 0
-    for p in params:
-        k = p.numel()
-        flat[off:off + k].copy_(p.data.view(-1))
-        p.data = flat[off:off + k].view_as(p)
-        p.grad = gflat[off:off + k].view_as(p)   # autograd accumulates into it
-        off += k
-    return flat, gflat
-
-
-def train(steps=60, T_p=5, T_s=5, gamma=2, seed=0, device="cuda", log=True):
+def train(steps=60, T_p=5, T_s=5, gamma=2, seed=0, device="cuda", log=True, dtype=torch.float32):
     torch.manual_seed(seed)
-    model = TinyDecoder().to(device)
-    flats = [flatten_params(b.parameters()) for b in model.blocks]
-    outer = [model.emb.weight, model.pos, *model.head.parameters()]
-    flats.append(flatten_params(outer))           # always-active group: id len(blocks)
-    gr = G.Grass([f.numel() for f, _ in flats], gamma=gamma, T_p=T_p, T_s=T_s, seed=seed,
-                 offload=True, residency=G.RESIDENCY_PERIOD, n_always=1)
-    sched = G.GrassSchedule(gr)
+    model = TinyDecoder().to(device=device, dtype=dtype)   # bf16: fp32 master + m + v in libgrass
+    gb = G.GrassBlocks(model.blocks, always=[[model.emb.weight, model.pos, *model.head.parameters()]],
+                       gamma=gamma, T_p=T_p, T_s=T_s, seed=seed, offload=True,
+                       residency=G.RESIDENCY_PERIOD)
     # a learnable synthetic task: predict the next token of a fixed random walk
     data = torch.cumsum(torch.randint(-2, 3, (64, 65), generator=torch.Generator().manual_seed(seed)), 1) % 256
     data = data.to(device)
     losses = []
     for step in range(steps):
-        ids = sched.begin_step(step)   # end_step takes the buffers in THIS order
-        layers = set(ids)
-        for l, b in enumerate(model.blocks):
-            for p in b.parameters():
-                p.requires_grad_(l in layers)
+        ids = gb.begin_step(step)      # freezes the blocks that are not trained this step
         logits = model(data[:, :-1])
-        loss = nn.functional.cross_entropy(logits.reshape(-1, 256), data[:, 1:].reshape(-1))
+        loss = nn.functional.cross_entropy(logits.float().reshape(-1, 256), data[:, 1:].reshape(-1))
         loss.backward()
         # probing steps only record norms: no parameter update (PAPER.md:113)
-        sched.end_step(step, [flats[l][0] for l in ids], [flats[l][1] for l in ids], lr=1e-3)
-        for _, g in flats:
-            g.zero_()
+        gb.end_step(step, lr=1e-3)
+        gb.zero_grad()
         losses.append(float(loss.detach()))
         if log and step % 10 == 0:
             print(f"step {step:3d} loss {losses[-1]:.4f} trainable {ids if step >= T_p else 'none (probe)'}")
-    gr.sync()
+    gb.grass.sync()
     return losses
 
 

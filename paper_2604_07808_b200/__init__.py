@@ -11,8 +11,9 @@ from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_CONTINUE, DECIDE_PROBE, DEC
                       uniform, ipc_export, ipc_import, selftest_p2p)
 
 from .schedule import GrassSchedule  # noqa: E402
+from .torch_blocks import GrassBlocks, flatten_params  # noqa: E402
 
-__all__ = ["Grass", "GrassSchedule", "GrassError", "lib", "exported_symbols", "nccl_unique_id",
+__all__ = ["Grass", "GrassSchedule", "GrassBlocks", "flatten_params", "GrassError", "lib", "exported_symbols", "nccl_unique_id",
            "sample_from_probs", "schedule_decision", "shard_range", "softmax_probs",
            "splitmix64", "tile_elems", "uniform", "POLICY_ADAPTIVE", "POLICY_STATIC",
            "POLICY_UNIFORM", "DECIDE_PROBE", "DECIDE_COMMIT_RESAMPLE", "DECIDE_RESAMPLE",

@@ -1,0 +1,90 @@
+"""Attaching a PyTorch model to libgrass: layer-wise GRASS training with flat
+per-block buffers.
+
+GRASS samples whole decoder blocks.  The library's unit is one
+flat, contiguous buffer per block (include/grass.h), so `GrassBlocks`
+re-homes each block's parameters — and their gradients — into one flat buffer
+per block, registers them with a `Grass` context (blocks first, then the
+always-active groups such as embedding / head, DESIGN R19) and drives the
+schedule:
+
+    gb = GrassBlocks(model.blocks, always=[model.embed.parameters(), model.head.parameters()],
+                     gamma=2, T_p=150, T_s=25, offload=True, residency=G.RESIDENCY_PERIOD)
+    for step in range(n_steps):
+        gb.begin_step(step)          # freezes the blocks not trained this step
+        loss = model(batch).loss
+        loss.backward()
+        gb.end_step(step, lr)        # probing norms, or the fused norm + AdamW of the trainable set
+        gb.zero_grad()
+
+This is plumbing (PyTorch owns the buffers and autograd); every step of the
+hot path runs in libgrass.
+"""
+from __future__ import annotations
+
+from typing import Iterable, Sequence
+
+import torch
+
+from .binding import DTYPE_BF16, DTYPE_FP32, Grass
+from .schedule import GrassSchedule
+
+
+def flatten_params(params: Iterable[torch.nn.Parameter]):
+    """Re-homes the parameters (and gradients) into two flat buffers of the
+    parameters' dtype; the parameters become views.  Returns (flat, gflat)."""
+    params = [p for p in params]
+    if not params:
+        raise ValueError("no parameters")
+    dt, dev = params[0].dtype, params[0].device
+    if any(p.dtype != dt or p.device != dev for p in params):
+        raise ValueError("a flattened group needs one dtype and one device")
+    n = sum(p.numel() for p in params)
+    flat = torch.empty(n, dtype=dt, device=dev)
+    gflat = torch.zeros(n, dtype=dt, device=dev)
+    off = 0
+    for p in params:
+        k = p.numel()
+        flat[off:off + k].copy_(p.data.reshape(-1))
+        p.data = flat[off:off + k].view_as(p)
+        p.grad = gflat[off:off + k].view_as(p)   # autograd accumulates into the flat buffer
+        off += k
+    return flat, gflat
+
+
+class GrassBlocks:
+    """A model's decoder blocks (sampled by GRASS) and optional always-active
+    parameter groups, bound to one `Grass` context (keyword arguments are
+    `Grass`'s, e.g. gamma, T_p, T_s, offload, residency, param_dtype)."""
+
+    def __init__(self, blocks: Sequence[torch.nn.Module], always: Sequence[Iterable] = (), **grass_kw):
+        self.blocks = list(blocks)
+        groups = [list(b.parameters()) for b in self.blocks] + [list(a) for a in always]
+        self.flats = [flatten_params(g) for g in groups]
+        dt = self.flats[0][0].dtype
+        if dt not in (torch.float32, torch.bfloat16):
+            raise ValueError("fp32 or bf16 parameters")
+        grass_kw.setdefault("param_dtype", DTYPE_BF16 if dt == torch.bfloat16 else DTYPE_FP32)
+        grass_kw.setdefault("device", self.flats[0][0].device.index or 0)
+        self.grass = Grass([f.numel() for f, _ in self.flats], n_always=len(always), **grass_kw)
+        self.schedule = GrassSchedule(self.grass)
+        self.layers: list[int] = []
+
+    def begin_step(self, step: int) -> list[int]:
+        """Sets requires_grad for this step (trainable blocks + always groups;
+        every block while probing) and returns the layer ids of the step."""
+        self.layers = self.schedule.begin_step(step)
+        active = set(self.layers)
+        for l, b in enumerate(self.blocks):
+            for p in b.parameters():
+                p.requires_grad_(l in active)
+        return list(self.layers)
+
+    def end_step(self, step: int, lr: float, stream=None):
+        ids = self.layers
+        self.schedule.end_step(step, [self.flats[l][0] for l in ids], [self.flats[l][1] for l in ids], lr,
+                               stream=stream)
+
+    def zero_grad(self):
+        for _, g in self.flats:
+            g.zero_()

@@ -1207,9 +1207,10 @@ def test_example_training_loop_loss_decreases():
     spec = importlib.util.spec_from_file_location("tiny_decoder_grass", path)
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
-    losses = mod.train(steps=60, log=False)
-    assert all(np.isfinite(losses))
-    assert np.mean(losses[-10:]) < 0.7 * np.mean(losses[:5])
+    for dtype in (torch.float32, torch.bfloat16):   # GrassBlocks picks the library dtype
+        losses = mod.train(steps=60, log=False, dtype=dtype)
+        assert all(np.isfinite(losses))
+        assert np.mean(losses[-10:]) < 0.7 * np.mean(losses[:5]), dtype
 
 
 @pytest.mark.parametrize("alpha,tau,normalize", [(0.0, 1.0, True), (1.0, 0.3, True), (0.5, 1e-4, False),
