@@ -73,6 +73,10 @@ struct AdamScalars {
 // parity bar, and the IEEE sequences cost ~3% of K2's time (measured A/B).
 __device__ __forceinline__ void adamw1(float g, float& th, float& m, float& v,
                                        const AdamScalars& s) {
+#ifdef GRASS_K2_NOMATH  // A/B only: the same data movement with trivial arithmetic (speed of light)
+  th += g; m += g; v += g;
+  return;
+#endif
   g *= s.cf;  // exact when cf == 1
   const float t1 = kMutant == 1 ? th : th * s.decay;  // M1: weight decay dropped
   const float m1 = fmaf(s.b1, m, s.omb1 * g);

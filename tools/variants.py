@@ -12,11 +12,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "pfn1": ["GRASS_L2_PREFETCH_NORM=1"],
-    "pfn2": ["GRASS_L2_PREFETCH_NORM=2"],
-    "pfu1": ["GRASS_L2_PREFETCH_UPD=1"],
+    "nomath": ["GRASS_K2_NOMATH"],
+    "nomath_grid148": ["GRASS_K2_NOMATH", "GRASS_UPD_GRID_SUB=0"],
     "base_again": [],
-    "pfn1_again": ["GRASS_L2_PREFETCH_NORM=1"],
+    "nomath_again": ["GRASS_K2_NOMATH"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
@@ -29,7 +28,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main,probe", extra=()):
+def run(legs="main", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
