@@ -120,6 +120,16 @@ __device__ __forceinline__ void store_unit_t(const Seg& sg, int npeer, int64_t e
   }
 }
 
+// Unit order of a CTA: rounds of kUB consecutive units per CTA (kUB = 1: unit
+// b, b + grid, b + 2 grid, ...).  Any order gives the same results.
+#ifndef GRASS_UNIT_BLOCK
+#define GRASS_UNIT_BLOCK 1
+#endif
+constexpr int kUB = GRASS_UNIT_BLOCK;
+__device__ __forceinline__ int unit_of(int i, int ub) {
+  return (i / ub) * ((int)gridDim.x * ub) + (int)blockIdx.x * ub + (i % ub);
+}
+
 template <bool UPDATE, int TPS, int STAGES, bool BF16, bool P2P>
 __global__ void __launch_bounds__(kStreamThreads, 1)
 grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
@@ -176,7 +186,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       int64_t pend_e0[STAGES];
       uint32_t pend_nv[STAGES];
       int s = 0, i = 0, gcount = 0;
-      for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
+      for (int u = unit_of(0, kUB); u < total; ++i, u = unit_of(i, kUB)) {
         const int stage = i % STAGES;
         char* stg = sbuf + (size_t)stage * L::bytes;
         if (kRing && i >= STAGES) {
@@ -268,7 +278,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   const float cf = (UPDATE && b.coef) ? *b.coef : 1.0f;
   const float gs = kMutant == 5 ? 1.0f : b.gscale;  // DP: 1/world turns reduce-scattered sums into averages (M5: not)
   int s = 0, i = 0, gcount = 0;
-  for (int u = blockIdx.x; u < total; u += gridDim.x, ++i) {
+  for (int u = unit_of(0, kUB); u < total; ++i, u = unit_of(i, kUB)) {
     const int stage = i % STAGES;
     while (u >= unit_prefix[s + 1]) ++s;
     const Seg& sg = b.seg[s];

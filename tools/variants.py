@@ -12,10 +12,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "base": [],
-    "nomath": ["GRASS_K2_NOMATH"],
-    "nomath_grid148": ["GRASS_K2_NOMATH", "GRASS_UPD_GRID_SUB=0"],
+    "ub2": ["GRASS_UNIT_BLOCK=2"],
+    "ub4": ["GRASS_UNIT_BLOCK=4"],
+    "ub8": ["GRASS_UNIT_BLOCK=8"],
     "base_again": [],
-    "nomath_again": ["GRASS_K2_NOMATH"],
+    "ub2_again": ["GRASS_UNIT_BLOCK=2"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
@@ -28,7 +29,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main", extra=()):
+def run(legs="main,probe", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
