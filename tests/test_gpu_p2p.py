@@ -25,6 +25,8 @@ from oracle import grass_oracle as O
 from synth import layer_grad, layer_params
 
 pytestmark = pytest.mark.gpu
+# GRASS_FUZZ=k multiplies the fuzz seeds (extended runs: profiles/r01_fuzz_extended.txt)
+FUZZ = int(os.environ.get("GRASS_FUZZ", "1"))
 DEV = "cuda:0"
 
 
@@ -320,7 +322,7 @@ def test_p2p_two_processes_ipc(tmp_path):
     assert np.array_equal(r[0]["S"], r[1]["S"])
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(FUZZ * 6))
 def test_p2p_fuzz_bit_identical_to_plain_on_the_averaged_gradient(seed):
     """Random world (incl. non-powers of two), ragged layer sizes, random
     active sets and residency modes: the W-rank P2P update of every element

@@ -13,6 +13,7 @@ Tolerances (BASELINE.json north_star):
   * offload on vs off: bit-identical.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -23,6 +24,8 @@ from oracle import grass_oracle as O
 from synth import grad_sigmas, integer_grad, layer_grad, layer_params, MODELS
 
 pytestmark = pytest.mark.gpu
+# GRASS_FUZZ=k multiplies the fuzz seeds (extended runs: profiles/r01_fuzz_extended.txt)
+FUZZ = int(os.environ.get("GRASS_FUZZ", "1"))
 
 DEV = "cuda:0"
 B1, B2, EPS = 0.9, 0.999, 1e-8
@@ -783,7 +786,7 @@ def test_trace_period_residency_and_dp():
 
 
 # --------------------------------------------------------- fuzz / edge cases
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(FUZZ * 4))
 def test_fuzz_pipelines_bit_identical(seed):
     """Random layer counts and sizes (ragged), random trainable sets, random
     chunk / ring / cache sizes, overlap on and off: offload (step and period)
@@ -856,7 +859,7 @@ def test_single_layer_single_element():
     assert gr.get_mgn()["S"] == [2.0]
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(FUZZ * 8))
 def test_fuzz_dtypes_clip_checkpoint(seed, tmp_path):
     """Like the pipeline fuzz, over both dtypes, random clipping and random
     always-active groups (R19), with a checkpoint written by one path and
