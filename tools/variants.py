@@ -11,12 +11,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
-    "base": [],
-    "ub2": ["GRASS_UNIT_BLOCK=2"],
-    "ub4": ["GRASS_UNIT_BLOCK=4"],
-    "ub8": ["GRASS_UNIT_BLOCK=8"],
-    "base_again": [],
-    "ub2_again": ["GRASS_UNIT_BLOCK=2"],
+    "alu_widen": [],
+    "f2f": ["GRASS_F2F_WIDEN=1"],
+    "alu_widen_again": [],
+    "f2f_again": ["GRASS_F2F_WIDEN=1"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
@@ -29,7 +27,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main,probe", extra=()):
+def run(legs="main,probe,bf16", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
