@@ -1,3 +1,7 @@
+"""Reproducer (raw NCCL through ctypes, no libgrass): on NCCL 2.28.9 a 1-rank
+ncclReduceScatter(ncclAvg, fp32) drops the last 16 elements for counts = 16
+(mod 64) from ~300 K elements up, while ncclSum is correct — why libgrass
+reduce-scatters with ncclSum and scales by 1/W in the kernel."""
 import ctypes as C, torch
 nccl = C.CDLL("libnccl.so.2")
 class UID(C.Structure):

@@ -1,3 +1,6 @@
+"""Probe of CUDA multicast (NVLS) support on the GPU box through cuda-python:
+cuMulticastCreate with each handle type (profiles/r01_multicast_probe*.json;
+DESIGN §13 explains why the fused kernel uses plain peer memory instead)."""
 import json
 import torch
 try:
