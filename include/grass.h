@@ -249,6 +249,20 @@ grass_status grass_step_layers(grass_ctx* ctx, const int32_t* layer_ids, int32_t
                                float* const* params, const float* const* grads, float lr,
                                void* stream);
 
+/* Learning rate from device memory: with lr_device != NULL every later
+ * grass_step_layers reads eta from *lr_device when its update runs (the `lr`
+ * argument is then ignored), so a learning-rate schedule can change eta
+ * between replays of a captured CUDA graph.  NULL restores the argument.
+ *
+ * CUDA graphs: grass_step_layers / grass_mgn_accumulate may be captured
+ * (stream capture, e.g. torch.cuda.graph) when the optimizer states are
+ * HBM-resident and the gradients are device memory (no offload, no P2P,
+ * tracing off): the per-layer step counts t_l, this step's bias corrections,
+ * the bf16 master-initialisation flags and the MGN window all live on the
+ * device, so every replay performs one full step.  Synchronising calls after
+ * replays wait for the whole device. */
+grass_status grass_set_lr_device(grass_ctx* ctx, const float* lr_device);
+
 /* Mixed-precision variants for a context created with GRASS_DTYPE_BF16
  * (SURVEY 8(f) f3, R18).  Same semantics as the fp32 calls; params/grads are
  * arrays of DEVICE pointers to bf16 (uint16_t bit patterns), 16-byte aligned.

@@ -117,6 +117,7 @@ _SIGS = {
                                            C.POINTER(C.c_void_p)]),
     "grass_p2p_finish": (C.c_int, [C.c_void_p, C.c_void_p]),
     "grass_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "grass_set_lr_device": (C.c_int, [C.c_void_p, C.c_void_p]),
     "grass_selftest_p2p": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
                                      C.POINTER(C.c_int32)]),
     "grass_ipc_import": (C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
@@ -348,6 +349,13 @@ class Grass:
 
     def sync(self):
         _check(lib().grass_sync(self._h), self._h)
+
+    def set_lr_device(self, lr_tensor=None):
+        """Read eta from a device float32 scalar (e.g. a torch tensor a captured
+        graph's schedule updates); None restores the step_layers argument."""
+        self._lr_tensor = lr_tensor          # keep it alive
+        ptr = None if lr_tensor is None else lr_tensor.data_ptr()
+        _check(lib().grass_set_lr_device(self._h, ptr), self._h)
 
     # state ------------------------------------------------------------------
     def shard(self, layer: int):

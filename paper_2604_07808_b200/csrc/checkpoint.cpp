@@ -64,6 +64,8 @@ grass_status grass_save_state(grass_ctx* c, const char* path) try {
   grass_status s = drain(c, false);
   if (s == GRASS_OK) s = flush_cache(c);
   if (s != GRASS_OK) return s;
+  // t_l lives on the device (it advances in captured graphs too)
+  CUDA_TRY(c, cudaMemcpy(c->t.data(), c->st.t, sizeof(long long) * c->nl, cudaMemcpyDeviceToHost));
   const std::vector<char> hdr = ck_header(c);
   FILE* f = std::fopen(path, "wb");
   if (!f) return c->fail(GRASS_E_IO, std::string("cannot open ") + path + " for writing");
@@ -186,6 +188,12 @@ grass_status grass_load_state(grass_ctx* c, const char* path) try {
   }
   std::fclose(f);
   c->t = t;
+  CUDA_TRY(c, cudaMemcpy(c->st.t, t.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice));
+  if (c->bf16) {
+    std::vector<int> mv(nl);
+    for (int l = 0; l < nl; ++l) mv[l] = c->master_valid[l];
+    CUDA_TRY(c, cudaMemcpy(c->st.mvalid, mv.data(), sizeof(int) * nl, cudaMemcpyHostToDevice));
+  }
   c->mgn = mgn;
   c->probs = probs;
   c->committed = ints[3] != 0;

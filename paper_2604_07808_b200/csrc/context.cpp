@@ -54,6 +54,9 @@ grass_status wait_pending(grass_ctx* c, cudaStream_t s) {
 // zeroes the window (S, c) and/or the flag, then synchronises once.
 grass_status fetch_mgn(grass_ctx* c, bool reset_window, bool take_flag) {
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  // work replayed from a captured CUDA graph is not tracked by the pending
+  // events: wait for the whole device instead
+  if (c->captured) CUDA_TRY(c, cudaDeviceSynchronize());
   grass_status s = wait_pending(c, c->aux);
   if (s != GRASS_OK) return s;
   CUDA_TRY(c, cudaMemcpyAsync(c->h_mgn, c->d_mgn, c->mgn_bytes, cudaMemcpyDeviceToHost, c->aux));
@@ -316,26 +319,17 @@ Seg range_seg(const grass_ctx* c, int l, const void* g, int64_t off, int64_t n) 
 
 // Update operands of a range: `param` is element 0 of the range in the
 // caller's parameter buffer; state[a] the m, v (, master) of the range.
-void set_update(const grass_ctx* c, Seg* s, void* param, float* const* state, bool init_master) {
+void set_update(const grass_ctx* c, Seg* s, void* param, float* const* state, bool /*init_master: device flag*/) {
   s->m = state[0];
   s->v = state[1];
   if (c->bf16) {
     s->theta = state[2];
     s->theta16 = static_cast<uint16_t*>(param);
-    s->init_master = init_master ? 1 : 0;
   } else {
     s->theta = static_cast<float*>(param);
   }
 }
 
-void adam_scalars(const grass_ctx* c, int l, float lr, Seg* s) {
-  const double t = (double)c->t[l];
-  const double bc1 = 1.0 - std::pow(c->cfg.beta1, t);
-  const double bc2 = 1.0 - std::pow(c->cfg.beta2, t);
-  s->decay = (float)(1.0 - (double)lr * c->cfg.weight_decay);
-  s->step_size = (float)((double)lr / bc1);
-  s->inv_bc2_sqrt = (float)(1.0 / std::sqrt(bc2));
-}
 
 
 void free_ctx(grass_ctx* c) {
@@ -352,6 +346,10 @@ void free_ctx(grass_ctx* c) {
   dfree(c->st.last_ss);
   if (c->h_mgn) cudaFreeHost(c->h_mgn);
   dfree(c->st.shard_ss);
+  dfree(c->st.t);
+  dfree(c->st.scal);
+  dfree(c->st.init_now);
+  dfree(c->st.mvalid);
   dfree(c->d_gather);
   dfree(c->d_gscratch);
   dfree(c->d_coef);
@@ -440,6 +438,10 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   c->st.flag = reinterpret_cast<int*>(static_cast<char*>(c->d_mgn) + 16 * (size_t)c->nl);
   CUDA_TRY(c, dalloc((void**)&c->st.last_ss, sizeof(double) * c->nl));
   CUDA_TRY(c, dalloc((void**)&c->st.shard_ss, sizeof(double) * c->nl));
+  CUDA_TRY(c, dalloc((void**)&c->st.t, sizeof(long long) * c->nl));
+  CUDA_TRY(c, dalloc((void**)&c->st.scal, sizeof(float) * 3 * (size_t)c->nl));
+  CUDA_TRY(c, dalloc((void**)&c->st.init_now, sizeof(int) * c->nl));
+  CUDA_TRY(c, dalloc((void**)&c->st.mvalid, sizeof(int) * c->nl));
 
   // optimizer state (m, v [, master]) for this rank's shard of every layer, zeroed
   const size_t state_bytes = sizeof(float) * (size_t)c->ns * (size_t)state_elems;

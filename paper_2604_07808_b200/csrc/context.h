@@ -55,7 +55,9 @@ struct grass_ctx {
   float* state_block = nullptr;
   float* always_block = nullptr;  // offload: the always-active groups' states stay in HBM (R19)
   std::vector<float*> arr[3];
-  std::vector<char> master_valid;
+  std::vector<char> master_valid;  // host mirror of DevState::mvalid (offload copy decisions)
+  const float* lr_ptr = nullptr;   // grass_set_lr_device: lr read on the device each step
+  bool captured = false;           // a hot-path call was captured into a CUDA graph
   std::vector<int64_t> t;
 
   // offload ring (step residency)
@@ -232,7 +234,6 @@ void push_seg(Batch* b, const Seg& s);
 grass_status flush(grass_ctx* c, Batch* b, bool update, cudaStream_t s);
 Seg range_seg(const grass_ctx* c, int l, const void* g, int64_t off, int64_t n);
 void set_update(const grass_ctx* c, Seg* s, void* param, float* const* state, bool init_master);
-void adam_scalars(const grass_ctx* c, int l, float lr, Seg* s);
 void free_ctx(grass_ctx* c);
 grass_status create_impl(const grass_config* cfg, grass_ctx* c);
 grass_status api_exception(grass_ctx* c) noexcept;

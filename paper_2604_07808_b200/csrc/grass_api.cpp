@@ -166,7 +166,11 @@ grass_status grass_read_state(grass_ctx* c, int32_t layer, float* m_out, float* 
   grass_status s = drain(c, false);
   if (s == GRASS_OK && m_out) s = copy_state_out(c, 0, layer, m_out);
   if (s == GRASS_OK && v_out) s = copy_state_out(c, 1, layer, v_out);
-  if (s == GRASS_OK && t_out) *t_out = c->t[layer];
+  if (s == GRASS_OK && t_out) {
+    long long t = 0;
+    CUDA_TRY(c, cudaMemcpy(&t, c->st.t + layer, sizeof(t), cudaMemcpyDeviceToHost));
+    *t_out = t;
+  }
   return s;
 } catch (...) {
   return api_exception(c);
@@ -179,7 +183,10 @@ grass_status grass_write_state(grass_ctx* c, int32_t layer, const float* m_in, c
   grass_status s = drain(c, false);
   if (s == GRASS_OK && m_in) s = copy_state_in(c, 0, layer, m_in);
   if (s == GRASS_OK && v_in) s = copy_state_in(c, 1, layer, v_in);
-  if (s == GRASS_OK) c->t[layer] = t_in;
+  if (s == GRASS_OK) {
+    const long long t = t_in;
+    CUDA_TRY(c, cudaMemcpy(c->st.t + layer, &t, sizeof(t), cudaMemcpyHostToDevice));
+  }
   return s;
 } catch (...) {
   return api_exception(c);
@@ -189,8 +196,11 @@ grass_status grass_read_master(grass_ctx* c, int32_t layer, float* out) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
   if (layer < 0 || layer >= c->nl || !out) return c->fail(GRASS_E_INVALID, "bad layer or NULL output");
   if (!c->bf16) return c->fail(GRASS_E_STATE, "fp32 context: the parameters are the master");
-  if (!c->master_valid[layer]) return c->fail(GRASS_E_STATE, "master of this layer not initialised yet");
   grass_status s = drain(c, false);
+  if (s != GRASS_OK) return s;
+  int valid = 0;
+  CUDA_TRY(c, cudaMemcpy(&valid, c->st.mvalid + layer, sizeof(valid), cudaMemcpyDeviceToHost));
+  if (!valid) return c->fail(GRASS_E_STATE, "master of this layer not initialised yet");
   return s == GRASS_OK ? copy_state_out(c, 2, layer, out) : s;
 } catch (...) {
   return api_exception(c);
@@ -202,7 +212,11 @@ grass_status grass_write_master(grass_ctx* c, int32_t layer, const float* in) tr
   if (!c->bf16) return c->fail(GRASS_E_STATE, "fp32 context: the parameters are the master");
   grass_status s = drain(c, false);
   if (s == GRASS_OK) s = copy_state_in(c, 2, layer, in);
-  if (s == GRASS_OK) c->master_valid[layer] = 1;
+  if (s == GRASS_OK) {
+    const int one = 1;
+    CUDA_TRY(c, cudaMemcpy(c->st.mvalid + layer, &one, sizeof(one), cudaMemcpyHostToDevice));
+    c->master_valid[layer] = 1;
+  }
   return s;
 } catch (...) {
   return api_exception(c);
@@ -415,6 +429,25 @@ grass_status grass_p2p_register_layer(grass_ctx* c, int32_t layer, void* const* 
                          cudaMemcpyHostToDevice));
   c->own_g[layer] = grads[r];
   c->own_p[layer] = params[r];
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(c);
+}
+
+grass_status grass_set_lr_device(grass_ctx* c, const float* lr_device) try {
+  if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (lr_device) {
+    cudaPointerAttributes at;
+    const bool ok = reinterpret_cast<uintptr_t>(lr_device) % alignof(float) == 0 &&
+                    cudaPointerGetAttributes(&at, lr_device) == cudaSuccess &&
+                    (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) &&
+                    at.device == c->cfg.device;
+    if (!ok) {
+      cudaGetLastError();
+      return c->fail(GRASS_E_INVALID, "lr_device must be an aligned float in device memory of the context's GPU");
+    }
+  }
+  c->lr_ptr = lr_device;
   return GRASS_OK;
 } catch (...) {
   return api_exception(c);

@@ -45,10 +45,8 @@ struct Seg {
   int32_t layer_tiles;     // tiles of the whole layer (shard) this step
   int32_t layer;           // layer id
   int32_t out_slot;        // kFinalizeShard: slot in shard_ss
-  float decay;             // 1 - lr*wd           (fp64 on host, rounded once)
-  float step_size;         // lr / (1 - b1^t)
-  float inv_bc2_sqrt;      // 1 / sqrt(1 - b2^t)
-  int32_t init_master;     // bf16 mode: first update of the layer, master := bf16 param
+  // (the AdamW scalars of the layer and its bf16 master-initialisation flag
+  // are read from DevState::scal / init_now, written by the step prologue)
   // bf16 mode: `theta` is the fp32 master, these are the
   // bf16 model copy (updated as RNE(master')) and the bf16 gradient
   uint16_t* theta16;
@@ -84,7 +82,26 @@ struct DevState {
   double* last_ss;         // last squared norm
   int* flag;               // INT_MAX - (smallest layer id with a non-finite norm), 0 = none
   double* shard_ss;        // [slot] this rank's shard squared norm (world > 1)
+  // per-layer optimizer step state, on the device so that a captured CUDA
+  // graph of grass_step_layers advances it on every replay
+  long long* t;            // t_l: updates applied to layer l (R2)
+  float* scal;             // [3 l + k]: 1 - lr*wd, lr/(1-b1^t), 1/sqrt(1-b2^t) of this step
+  int* init_now;           // bf16: 1 if this step initialises the layer's master from the bf16 param
+  int* mvalid;             // bf16: the layer's fp32 master holds a value
 };
+
+// Step prologue: for each listed layer t_l += 1 and the AdamW scalars of the
+// new t_l (fp64, rounded once to fp32), lr from `lr_ptr` if set (a device
+// scalar the caller may change between graph replays) else `lr`.
+struct PrologueArgs {
+  int32_t n;
+  int32_t layer[kMaxSeg];
+  float lr;
+  const float* lr_ptr;
+  double beta1, beta2, wd;
+  int32_t bf16;
+};
+cudaError_t launch_step_prologue(const PrologueArgs& a, const DevState& st, cudaStream_t s);
 
 // kernels.cu
 cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int grid,

@@ -11,6 +11,23 @@
 
 namespace gapi {
 
+// Is `stream` being captured into a CUDA graph?  Captured hot-path calls are
+// replayed by the caller; the step state (t_l, AdamW scalars, the bf16 master
+// flag, the MGN window) lives on the device so every replay advances it.
+// Supported for HBM-resident optimizer states with device gradients (no
+// offload, no P2P, no tracing): the offload pipelines keep host-side ring and
+// hazard state, P2P barriers host-side epochs.
+grass_status capture_check(grass_ctx* c, cudaStream_t st, bool any_host, bool* capturing) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_TRY(c, cudaStreamIsCapturing(st, &cap));
+  *capturing = cap == cudaStreamCaptureStatusActive;
+  if (*capturing && (c->cfg.offload || c->p2p || any_host || c->tracing))
+    return c->fail(GRASS_E_INVALID, "CUDA-graph capture needs HBM-resident optimizer states and device "
+                                    "gradients (no offload, no P2P, tracing off)");
+  if (*capturing) c->captured = true;
+  return GRASS_OK;
+}
+
 // ---- the hot path ----------------------------------------------------------
 
 // Eq. 2 inner term for the listed layers (probing); fp32 or bf16 gradients.
@@ -23,6 +40,8 @@ grass_status mgn_accumulate_impl(grass_ctx* c, bool bf16_call, const int32_t* id
   if (s != GRASS_OK) return s;
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bool capturing = false;
+  if ((s = capture_check(c, st, false, &capturing)) != GRASS_OK) return s;
   if (c->p2p) {
     // start barrier -> K1 over the sum of every rank's gradient (peer reads) -> publish + end barrier
     if ((s = p2p_check(c, ids, n, nullptr, grads)) != GRASS_OK) return s;
@@ -66,7 +85,7 @@ grass_status mgn_accumulate_impl(grass_ctx* c, bool bf16_call, const int32_t* id
     if ((s = comm_end(c, st)) != GRASS_OK) return s;
     if ((s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
   }
-  return mark_pending(c, st);
+  return capturing ? GRASS_OK : mark_pending(c, st);
 }
 
 // Fused norm + AdamW of the listed layers, with offload / residency / DP /
@@ -82,6 +101,9 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
                               &g_host);
   if (s != GRASS_OK) return s;
   const bool any_host = std::find(g_host.begin(), g_host.end(), 1) != g_host.end();
+  bool capturing = false;
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  if ((s = capture_check(c, reinterpret_cast<cudaStream_t>(stream), any_host, &capturing)) != GRASS_OK) return s;
   if (any_host && c->cfg.max_grad_norm > 0.0)
     return c->fail(GRASS_E_INVALID, "clipping needs device gradients (pass 1 reads them twice)");
   if (any_host && !c->d_gring) {  // first host-gradient call: the gradient ring
@@ -149,6 +171,23 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     // write-backs read cache slots last written by earlier steps' updates
     if (c->cfg.overlap && (s = wait_pending(c, c->d2h)) != GRASS_OK) return s;
   }
+  // step prologue (device): t_l += 1 and this step's AdamW scalars of every
+  // listed layer — on the device, so a captured graph of this call advances
+  // them on every replay
+  for (int j0 = 0; j0 < nact; j0 += kMaxSeg) {
+    PrologueArgs pa;
+    std::memset(&pa, 0, sizeof(pa));
+    pa.n = std::min(kMaxSeg, nact - j0);
+    for (int j = 0; j < pa.n; ++j) pa.layer[j] = ids[order[j0 + j]];
+    pa.lr = lr;
+    pa.lr_ptr = c->lr_ptr;
+    pa.beta1 = c->cfg.beta1;
+    pa.beta2 = c->cfg.beta2;
+    pa.wd = c->cfg.weight_decay;
+    pa.bf16 = c->bf16 ? 1 : 0;
+    CUDA_TRY(c, launch_step_prologue(pa, c->st, st));
+    c->launches++;
+  }
   if (p2p && (s = p2p_start(c, st)) != GRASS_OK) return s;
   Batch b = make_batch(c, mode);
   if (sharded) {
@@ -157,7 +196,8 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   }
   for (int j = 0; j < nact; ++j) {
     const int i = order[j], l = ids[i];
-    c->t[l] += 1;  // per-layer step count (R2); validated above, so this step happens
+    // host mirror of the bf16 master flag (copy decisions of the offload paths;
+    // the kernels read the device flag set by the prologue)
     const bool init = c->bf16 && !c->master_valid[l];
     c->master_valid[l] = 1;
     const int64_t off = c->shard_off[l], len = c->shard_len[l];
@@ -176,7 +216,6 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     }
     void* param = elem(params[i], off, c->esz);  // this rank's range of the layer
     Seg base = range_seg(c, l, g, 0, len);
-    adam_scalars(c, l, lr, &base);
     base.out_slot = j;
     if (period && !always_active(c, l)) {
       const int slot = slot_of[j];
@@ -232,7 +271,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     CUDA_TRY(c, cudaStreamWaitEvent(st, e, 0));
     c->ev_free_list.push_back(e);
   }
-  return mark_pending(c, st);
+  return capturing ? GRASS_OK : mark_pending(c, st);
 }
 
 

@@ -362,6 +362,24 @@ __global__ void grass_p2p_selftest_kernel(const __grid_constant__ P2PSelftestArg
   }
 }
 
+__global__ void grass_step_prologue_kernel(const __grid_constant__ PrologueArgs a, const DevState st) {
+  const int j = threadIdx.x;
+  if (j >= a.n) return;
+  const int l = a.layer[j];
+  const long long t = st.t[l] + 1;
+  st.t[l] = t;
+  const double lr = a.lr_ptr ? (double)*a.lr_ptr : (double)a.lr;
+  const double bc1 = 1.0 - pow(a.beta1, (double)t);
+  const double bc2 = 1.0 - pow(a.beta2, (double)t);
+  st.scal[3 * l + 0] = (float)(1.0 - lr * a.wd);
+  st.scal[3 * l + 1] = (float)(lr / bc1);
+  st.scal[3 * l + 2] = (float)(1.0 / sqrt(bc2));
+  if (a.bf16) {
+    st.init_now[l] = st.mvalid[l] ? 0 : 1;
+    st.mvalid[l] = 1;
+  }
+}
+
 __global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const DevState st,
                                        float* coef) {
   if (threadIdx.x != 0) return;
@@ -473,6 +491,12 @@ cudaError_t p2p_selftest(int world, int n, int rounds, unsigned long long* misma
   if (e == cudaSuccess) e = cudaMemcpy(timed_out, t.err, sizeof(int), cudaMemcpyDeviceToHost);
   cudaFree(mem);
   return e;
+}
+
+cudaError_t launch_step_prologue(const PrologueArgs& a, const DevState& st, cudaStream_t s) {
+  if (a.n <= 0) return cudaSuccess;
+  grass_step_prologue_kernel<<<1, 64, 0, s>>>(a, st);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_clip_coef(const ClipArgs& a, const DevState& st, float* coef, cudaStream_t s) {

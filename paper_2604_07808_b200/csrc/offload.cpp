@@ -25,9 +25,6 @@ grass_status update_range(grass_ctx* c, int l, const Seg& base, void* param, con
       sg.g = static_cast<const float*>(g_chunk);
   }
   set_update(c, &sg, elem(param, off, c->esz), state, init);
-  sg.decay = base.decay;
-  sg.step_size = base.step_size;
-  sg.inv_bc2_sqrt = base.inv_bc2_sqrt;
   sg.out_slot = base.out_slot;
   Batch b = make_batch(c, mode);
   push_seg(&b, sg);

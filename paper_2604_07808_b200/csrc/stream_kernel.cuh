@@ -207,7 +207,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           pend_nv[stage] = nv;
         }
         if (nv && (UPDATE || !P2P)) {
-          const bool init = BF16 && UPDATE && sg.init_master;
+          const bool init = BF16 && UPDATE && st.init_now[sg.layer];
           // P2P: the gradient slices go to the gradient ring (below)
           const uint32_t tx = (P2P ? 0u : nv * (uint32_t)L::GB) + (UPDATE ? nv * (init ? 2u : 4u) + 8u * nv : 0u);
           mbar_arrive_expect_tx(&full_bar[stage], tx);
@@ -284,9 +284,14 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     const Seg& sg = b.seg[s];
     AdamScalars sc;
     sc.b1 = b.beta1; sc.omb1 = b.one_minus_beta1; sc.b2 = b.beta2; sc.omb2 = b.one_minus_beta2;
-    sc.eps = b.eps; sc.decay = sg.decay; sc.step = sg.step_size; sc.inv_bc2s = sg.inv_bc2_sqrt;
+    sc.eps = b.eps;
+    if (UPDATE) {  // this step's AdamW scalars of the layer (step prologue)
+      sc.decay = st.scal[3 * sg.layer];
+      sc.step = st.scal[3 * sg.layer + 1];
+      sc.inv_bc2s = st.scal[3 * sg.layer + 2];
+    }
     sc.cf = cf;
-    const bool init = BF16 && UPDATE && sg.init_master;
+    const bool init = BF16 && UPDATE && st.init_now[sg.layer];
     const int ui = u - unit_prefix[s];
     const int64_t e0 = (int64_t)ui * kUnit;
     const int ne = (int)min((int64_t)kUnit, sg.n - e0);

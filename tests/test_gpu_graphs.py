@@ -1,0 +1,106 @@
+"""CUDA graphs: grass_step_layers captured once (torch.cuda.graph) and replayed
+k times must equal k eager calls bit for bit — parameters, m, v, the device
+step counts t_l, the bf16 master initialisation on the first replay, the
+clipped update and the MGN window — and the learning rate can come from a
+device scalar changed between replays (grass_set_lr_device)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_07808_b200 as G
+from synth import layer_grad, layer_params
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _pair(numel, dtype, **kw):
+    tdt = torch.bfloat16 if dtype == G.DTYPE_BF16 else torch.float32
+    eager = G.Grass(numel, gamma=2, weight_decay=0.01, param_dtype=dtype, **kw)
+    graph = G.Grass(numel, gamma=2, weight_decay=0.01, param_dtype=dtype, **kw)
+    base = [layer_params(n, l, device=DEV).to(tdt) for l, n in enumerate(numel)]
+    grads = [layer_grad(n, l, 1e-3, device=DEV).to(tdt) for l, n in enumerate(numel)]
+    return eager, graph, [b.clone() for b in base], [b.clone() for b in base], grads
+
+
+def _same(eager, graph, pe, pg, ids):
+    torch.cuda.synchronize()
+    for l in ids:
+        assert torch.equal(pe[l], pg[l]), l
+        a, b = eager.read_state(l), graph.read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2], l
+    sa, sb = eager.get_mgn(), graph.get_mgn()
+    assert sa["S"] == sb["S"] and sa["c"] == sb["c"] and sa["last_ss"] == sb["last_ss"]
+
+
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+@pytest.mark.parametrize("clip", [0.0, 1e-3])
+def test_captured_step_replays_equal_eager_steps(dtype, clip):
+    numel = [4096 * 5 + 8, 65_536, 4096 * 3]
+    ids = [2, 0]
+    eager, graph, pe, pg, grads = _pair(numel, dtype, max_grad_norm=clip)
+    k = 5
+    for _ in range(k):
+        eager.step_layers(ids, [pe[l] for l in ids], [grads[l] for l in ids], 1e-3)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graph.step_layers(ids, [pg[l] for l in ids], [grads[l] for l in ids], 1e-3,
+                          stream=torch.cuda.current_stream())
+    for _ in range(k):
+        g.replay()
+    _same(eager, graph, pe, pg, ids)
+    assert graph.read_state(0)[2] == k                     # t advanced on every replay
+    if dtype == G.DTYPE_BF16:
+        assert np.array_equal(eager.read_master(0), graph.read_master(0))
+
+
+def test_captured_step_with_device_learning_rate():
+    numel = [8192, 4096 * 3 + 4]
+    ids = [0, 1]
+    eager, graph, pe, pg, grads = _pair(numel, G.DTYPE_FP32)
+    lrs = [1e-3, 5e-4, 2e-3, 1e-4]
+    lr_t = torch.zeros((), dtype=torch.float32, device=DEV)
+    graph.set_lr_device(lr_t)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graph.step_layers(ids, pg, grads, 123.0, stream=torch.cuda.current_stream())  # lr argument ignored
+    for lr in lrs:
+        eager.step_layers(ids, pe, grads, lr)
+        lr_t.fill_(lr)
+        g.replay()
+    _same(eager, graph, pe, pg, ids)
+    graph.set_lr_device(None)
+
+
+def test_commit_after_replays_sees_every_replay():
+    numel = [8192, 8192, 8192]
+    gr = G.Grass(numel, gamma=2, T_p=1, T_s=1)
+    p = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    g = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        gr.step_layers([0, 2], [p[0], p[2]], [g[0], g[2]], 1e-3, stream=torch.cuda.current_stream())
+    for _ in range(7):
+        graph.replay()
+    st = gr.get_mgn()                                     # no explicit synchronisation before
+    assert st["c"] == [7, 0, 7]
+    probs = gr.update_probs()
+    assert abs(sum(probs) - 1.0) < 1e-12 and gr.get_mgn()["c"] == [0, 0, 0]   # window consumed
+
+
+def test_capture_rejected_where_unsupported():
+    numel = [8192, 8192]
+    p = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    g = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
+    off = G.Grass(numel, gamma=2, offload=True)
+    graph = torch.cuda.CUDAGraph()
+    with pytest.raises(G.GrassError, match="capture"):
+        with torch.cuda.graph(graph):
+            off.step_layers([0, 1], p, g, 1e-3, stream=torch.cuda.current_stream())

@@ -48,4 +48,31 @@ for k in range(2000):
 e1.record()
 torch.cuda.synchronize()
 res["loop_us_per_step"] = e0.elapsed_time(e1) / 2000 * 1e3
+
+# the same small update (2 layers x 4096) eager vs one captured CUDA graph
+# replayed: launch-bound regime, where graphs pay off
+ids = [3, 17]
+gs = torch.cuda.Stream()
+def eager_steps(n):
+    for _ in range(n):
+        gr.step_layers(ids, [p[l] for l in ids], [g[l] for l in ids], 1e-3, stream=gs)
+with torch.cuda.stream(gs):
+    eager_steps(50)
+torch.cuda.synchronize()
+t = time.perf_counter()
+with torch.cuda.stream(gs):
+    eager_steps(2000)
+torch.cuda.synchronize()
+res["eager_step_us_wall"] = (time.perf_counter() - t) / 2000 * 1e6
+graph = torch.cuda.CUDAGraph()
+with torch.cuda.graph(graph):
+    gr.step_layers(ids, [p[l] for l in ids], [g[l] for l in ids], 1e-3, stream=torch.cuda.current_stream())
+for _ in range(50):
+    graph.replay()
+torch.cuda.synchronize()
+t = time.perf_counter()
+for _ in range(2000):
+    graph.replay()
+torch.cuda.synchronize()
+res["graph_replay_step_us_wall"] = (time.perf_counter() - t) / 2000 * 1e6
 print(json.dumps(res, indent=1))
