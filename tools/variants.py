@@ -10,11 +10,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-VARIANTS = {
-    "alu_widen": [],
-    "f2f": ["GRASS_F2F_WIDEN=1"],
-    "alu_widen_again": [],
-    "f2f_again": ["GRASS_F2F_WIDEN=1"],
+VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
+    "base": [],
+    "base_again": [],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
