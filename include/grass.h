@@ -256,11 +256,12 @@ grass_status grass_step_layers(grass_ctx* ctx, const int32_t* layer_ids, int32_t
  *
  * CUDA graphs: grass_step_layers / grass_mgn_accumulate may be captured
  * (stream capture, e.g. torch.cuda.graph) when the optimizer states are
- * HBM-resident and the gradients are device memory (no offload, no P2P,
- * tracing off): the per-layer step counts t_l, this step's bias corrections,
- * the bf16 master-initialisation flags and the MGN window all live on the
- * device, so every replay performs one full step.  Synchronising calls after
- * replays wait for the whole device. */
+ * HBM-resident and the gradients are device memory (no offload, tracing off;
+ * NCCL, or P2P with p2p_sync = 1): the per-layer step counts t_l, this step's
+ * bias corrections, the bf16 master-initialisation flags, the MGN window and
+ * the P2P barrier generations all live on the device, so every replay
+ * performs one full step.  Synchronising calls after replays wait for the
+ * whole device. */
 grass_status grass_set_lr_device(grass_ctx* ctx, const float* lr_device);
 
 /* Mixed-precision variants for a context created with GRASS_DTYPE_BF16

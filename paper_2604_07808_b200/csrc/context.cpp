@@ -359,6 +359,7 @@ void free_ctx(grass_ctx* c) {
   dfree(c->always_block);
   dfree(c->d_exch);
   dfree(c->d_ptab);
+  dfree(c->d_epoch);
   if (c->state_block) {
     if (c->cfg.offload)
       cudaFreeHost(c->state_block);
@@ -512,6 +513,7 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     c->exch_bytes = (size_t)kExchGather + sizeof(double) * (size_t)W * c->nl;
     CUDA_TRY(c, dalloc((void**)&c->d_exch, c->exch_bytes));
     CUDA_TRY(c, dalloc((void**)&c->d_ptab, sizeof(void*) * 2 * (size_t)W * c->nl));
+    CUDA_TRY(c, dalloc((void**)&c->d_epoch, 2 * sizeof(unsigned long long)));
     c->own_g.assign(c->nl, nullptr);
     c->own_p.assign(c->nl, nullptr);
   }

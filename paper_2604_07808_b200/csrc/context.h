@@ -121,7 +121,7 @@ struct grass_ctx {
   std::vector<char*> exch_peer;  // every rank's block (after grass_p2p_attach)
   void** d_ptab = nullptr;       // device [nl][2][world]: gradient then parameter pointers
   std::vector<const void*> own_g, own_p;  // this rank's registered full-layer buffers
-  uint64_t epoch[2] = {0, 0};    // start / end barrier generations
+  unsigned long long* d_epoch = nullptr;  // device [2]: start / end barrier generations
   std::vector<int32_t> p2p_pending;  // p2p_sync = 0: layers whose MGN finish is pending
 
   Comm comm;

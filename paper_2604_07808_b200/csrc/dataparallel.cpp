@@ -61,7 +61,7 @@ P2PSyncArgs p2p_args(grass_ctx* c, int32_t which) {
   a.rank = c->cfg.rank;
   a.world = c->cfg.world;
   a.which = which;
-  if (which >= 0) a.epoch = ++c->epoch[which];
+  a.epoch_ctr = c->d_epoch;  // generations advance on the device (graph replays included)
   a.err = reinterpret_cast<int*>(static_cast<char*>(c->d_mgn) + 16 * (size_t)c->nl + 4);
   return a;
 }

@@ -141,7 +141,9 @@ struct P2PSyncArgs {
   int32_t rank, world;
   int32_t n;               // shard norms to publish into every rank's row `rank` (0 = none)
   int32_t which;           // barrier: 0 = start, 1 = end, -1 = none
-  uint64_t epoch;          // value every rank signals for this barrier
+  uint64_t epoch;          // value every rank signals for this barrier (if epoch_ctr is NULL)
+  unsigned long long* epoch_ctr;  // device [2]: start / end generations, advanced by the kernel
+                                  // itself (so a captured graph's replays advance them too)
   const double* shard_ss;  // [n] this rank's shard squared norms
   int* err;                // set to 1 if a peer never arrives (timeout)
 };

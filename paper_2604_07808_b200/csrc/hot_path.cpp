@@ -15,15 +15,15 @@ namespace gapi {
 // replayed by the caller; the step state (t_l, AdamW scalars, the bf16 master
 // flag, the MGN window) lives on the device so every replay advances it.
 // Supported for HBM-resident optimizer states with device gradients (no
-// offload, no P2P, no tracing): the offload pipelines keep host-side ring and
-// hazard state, P2P barriers host-side epochs.
+// offload, no tracing; P2P with its device barriers): the offload pipelines
+// keep host-side ring and hazard state.
 grass_status capture_check(grass_ctx* c, cudaStream_t st, bool any_host, bool* capturing) {
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   CUDA_TRY(c, cudaStreamIsCapturing(st, &cap));
   *capturing = cap == cudaStreamCaptureStatusActive;
-  if (*capturing && (c->cfg.offload || c->p2p || any_host || c->tracing))
+  if (*capturing && (c->cfg.offload || (c->p2p && !c->cfg.p2p_sync) || any_host || c->tracing))
     return c->fail(GRASS_E_INVALID, "CUDA-graph capture needs HBM-resident optimizer states and device "
-                                    "gradients (no offload, no P2P, tracing off)");
+                                    "gradients (no offload, P2P only with p2p_sync, tracing off)");
   if (*capturing) c->captured = true;
   return GRASS_OK;
 }

@@ -285,6 +285,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // One rank's publication + barrier, executed by one CTA (rank = a.rank).
 __device__ void p2p_sync_cta(const P2PSyncArgs& a) {
   const int tid = threadIdx.x;
+  __shared__ unsigned long long epoch;
+  if (tid == 0 && a.which >= 0) epoch = a.epoch_ctr ? ++a.epoch_ctr[a.which] : a.epoch;
   for (int k = tid; k < a.world * a.n; k += blockDim.x) {
     const int q = k / a.n, j = k % a.n;
     double* row = reinterpret_cast<double*>(a.exch[q] + kExchGather) + (int64_t)a.rank * a.n;
@@ -296,15 +298,14 @@ __device__ void p2p_sync_cta(const P2PSyncArgs& a) {
     __threadfence_system();
     unsigned long long* peer_flag =
         reinterpret_cast<unsigned long long*>(a.exch[tid]) + a.which * kMaxPeers + a.rank;
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer_flag), "l"((unsigned long long)a.epoch)
-                 : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer_flag), "l"(epoch) : "memory");
     const unsigned long long* mine =
         reinterpret_cast<const unsigned long long*>(a.exch[a.rank]) + a.which * kMaxPeers + tid;
     const unsigned long long t0 = global_ns();
     while (true) {
       unsigned long long v;
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
-      if (v >= a.epoch) break;
+      if (v >= epoch) break;
       if (global_ns() - t0 > kP2PTimeoutNs) {
         atomicExch(a.err, 1);
         break;
@@ -333,6 +334,7 @@ struct P2PSelftestArgs {
 __global__ void grass_p2p_selftest_kernel(const __grid_constant__ P2PSelftestArgs t) {
   const int rank = blockIdx.x;
   P2PSyncArgs a;
+  a.epoch_ctr = nullptr;  // explicit generations (the round)
   for (int q = 0; q < kMaxPeers; ++q) a.exch[q] = t.exch[q];
   a.rank = rank;
   a.world = t.world;

@@ -104,3 +104,31 @@ def test_capture_rejected_where_unsupported():
     with pytest.raises(G.GrassError, match="capture"):
         with torch.cuda.graph(graph):
             off.step_layers([0, 1], p, g, 1e-3, stream=torch.cuda.current_stream())
+
+
+def test_captured_p2p_step_replays_equal_eager_steps():
+    """The fused P2P data-parallel step (world 1, device barriers whose
+    generations advance on the device) captured and replayed == eager."""
+    numel = [4096 * 3 + 8, 65_536]
+    ids = [1, 0]
+    ctxs, P = [], []
+    grads = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
+    base = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    for _ in range(2):
+        c = G.Grass(numel, gamma=2, weight_decay=0.01, dp_mode=G.DP_P2P)
+        c.p2p_attach([c.p2p_exchange_block()[0]])
+        p = [b.clone() for b in base]
+        for l in range(2):
+            c.p2p_register_layer(l, [p[l]], [grads[l]])
+        ctxs.append(c)
+        P.append(p)
+    eager, graph = ctxs
+    for _ in range(4):
+        eager.step_layers(ids, [P[0][l] for l in ids], [grads[l] for l in ids], 1e-3)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graph.step_layers(ids, [P[1][l] for l in ids], [grads[l] for l in ids], 1e-3,
+                          stream=torch.cuda.current_stream())
+    for _ in range(4):
+        g.replay()
+    _same(eager, graph, P[0], P[1], ids)
