@@ -101,7 +101,7 @@ def test_capture_rejected_where_unsupported():
     g = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
     off = G.Grass(numel, gamma=2, offload=True)
     graph = torch.cuda.CUDAGraph()
-    with pytest.raises(G.GrassError, match="capture"):
+    with pytest.raises(G.GrassError, match="capture"), pytest.warns(UserWarning):
         with torch.cuda.graph(graph):
             off.step_layers([0, 1], p, g, 1e-3, stream=torch.cuda.current_stream())
 
@@ -132,3 +132,19 @@ def test_captured_p2p_step_replays_equal_eager_steps():
     for _ in range(4):
         g.replay()
     _same(eager, graph, P[0], P[1], ids)
+
+
+def test_captured_nccl_step_replays_equal_eager_steps():
+    """The NCCL data-parallel step (1-rank communicator: reduce-scatter, K2,
+    all-gather on the comm stream, fp64 partial all-gather) captured == eager."""
+    numel = [4096 * 4, 8192 + 64]
+    ids = [0, 1]
+    eager, graph, pe, pg, grads = _pair(numel, G.DTYPE_FP32, force_nccl=True)
+    for _ in range(3):
+        eager.step_layers(ids, pe, grads, 1e-3)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graph.step_layers(ids, pg, grads, 1e-3, stream=torch.cuda.current_stream())
+    for _ in range(3):
+        g.replay()
+    _same(eager, graph, pe, pg, ids)
