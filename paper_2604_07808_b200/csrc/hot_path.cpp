@@ -110,7 +110,6 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     CUDA_TRY(c, cudaMalloc((void**)&c->d_gring, (size_t)c->slots * c->chunk * c->esz));
     c->dev_bytes += (int64_t)((size_t)c->slots * c->chunk * c->esz);
   }
-  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool sharded = c->dp;  // NCCL data parallelism
   const bool p2p = c->p2p;     // P2P data parallelism: one fused kernel, no NCCL
