@@ -572,11 +572,27 @@ def run_grass(args, rank, world, local):
                 for _ in range(n_mm):
                     torch.matmul(a, bm, out=cm)
 
+        # the same GEMMs split as a forward (1/3) and a per-layer backward (2/3,
+        # layer NL-1 first), so an update can be issued as soon as its layer's
+        # gradient is ready (offload "layer by layer")
+        n_f = n_mm // 3
+        cuts = [n_f + round((n_mm - n_f) * (NL - l) / NL) for l in range(NL + 1)]  # cuts[l] .. cuts[l+1]
+        side = torch.cuda.Stream(device=dev)
+
+        def fwd_bwd_layerwise(on_grad_ready):
+            with torch.cuda.stream(s):
+                for _ in range(n_f):
+                    torch.matmul(a, bm, out=cm)
+                for l in reversed(range(NL)):
+                    for _ in range(cuts[l] - cuts[l + 1]):
+                        torch.matmul(a, bm, out=cm)
+                    on_grad_ready(l)
+
         def run(mode):
             kw = dict(T_p=1, T_s=T_s, T_u=T_s, seed=1234, device=local, rank=rank, world=world)
             if mode == "prefetch":
                 kw.update(offload=True, residency=G.RESIDENCY_PERIOD)
-            elif mode == "offload":
+            elif mode in ("offload", "offload_bwd"):
                 kw.update(offload=True)
             tc = G.Grass([n_p] * NL, gamma=gamma, **kw)
             tc.mgn_accumulate(list(range(NL)), grads, stream=s)
@@ -590,6 +606,19 @@ def run_grass(args, rank, world, local):
                     cur = tc.sample_layers(k // T_s + 1)
                     if mode == "prefetch":
                         tc.prefetch_layers(cur, stream=s)   # moves during fwd/bwd
+                if mode == "offload_bwd":
+                    # per-step round trip of each trainable layer's m/v, issued on a
+                    # side stream the moment backward has produced its gradient:
+                    # fetch / update / write-back overlap the rest of the backward
+                    def ready(l):
+                        if l in cur:
+                            e = torch.cuda.Event()
+                            e.record(s)
+                            side.wait_event(e)
+                            tc.step_layers([l], [params[l]], [grads[l]], args.lr, stream=side)
+                    fwd_bwd_layerwise(ready)
+                    s.wait_stream(side)
+                    return
                 fwd_bwd()
                 tc.step_layers(cur, [params[l] for l in cur], [grads[l] for l in cur], args.lr, stream=s)
             for k in range(1, 4):                     # warm (no boundary: the window was just committed)
@@ -615,10 +644,11 @@ def run_grass(args, rank, world, local):
         res = {"standin": f"{n_mm} bf16 GEMMs 8192^3 = {n_mm * 2 * 8192 ** 3:.3g} FLOP "
                           "(LLaMA-2-7B fwd+bwd, 4 x 1024 tokens; SYNTHETIC)",
                "standin_ms": e0_.elapsed_time(e1_), "schedule": f"T_s=T_u={T_s}, {nsteps} steps"}
-        for mode in ("resident", "prefetch", "offload"):
+        for mode in ("resident", "prefetch", "offload", "offload_bwd"):
             res[f"{mode}_step_ms"] = run(mode)
         res["period_prefetch_over_resident"] = res["prefetch_step_ms"] / res["resident_step_ms"]
         res["per_step_offload_over_resident"] = res["offload_step_ms"] / res["resident_step_ms"]
+        res["per_step_offload_during_backward_over_resident"] = res["offload_bwd_step_ms"] / res["resident_step_ms"]
         res["offloaded_within_10pct_of_resident"] = res["period_prefetch_over_resident"] <= 1.10
         return res
 
