@@ -174,8 +174,9 @@ grass_status grass_config_init(grass_config* cfg);
 
 /* Validates cfg, allocates: per layer m/v (HBM, or pinned host when offload;
  * when world > 1 only this rank's shard), zeroed, t_l = 0; MGN accumulators;
- * staging ring and copy streams (offload); NCCL communicator (world > 1, which
- * requires every N_p divisible by 4*world).  *out receives the context.
+ * staging ring and copy streams (offload); NCCL communicator (world > 1 with
+ * GRASS_DP_NCCL) or the P2P exchange block (GRASS_DP_P2P); world > 1 requires
+ * every N_p divisible by 4*world (8*world for bf16).  *out receives the context.
  * Errors: GRASS_E_INVALID (bad config: gamma > N_L, tau <= 0
  * (SPEC.md:270), alpha outside [0,1], ...), GRASS_E_OOM,
  * GRASS_E_CUDA, GRASS_E_NCCL.  On error *out = NULL. */
@@ -232,9 +233,13 @@ grass_status grass_sample_layers(grass_ctx* ctx, const double* probs, uint64_t p
  *   v = b2*v + (1-b2)*g^2; theta -= lr/(1-b1^t) * m / (sqrt(v)/sqrt(1-b2^t) + eps)
  * With cfg.offload the layer's m/v stream from pinned host memory through the
  * device staging ring and back; results are bit-identical
- * to offload = 0 (R12).  World > 1: gradients are reduce-scattered (average)
- * over NCCL, each rank updates its element shard with its own m/v slice, and
- * parameters are all-gathered back into params[i].
+ * to offload = 0 (R12).  World > 1: each rank updates its element shard with
+ * its own m/v slice; with GRASS_DP_NCCL the gradients are reduce-scattered
+ * (sum, x 1/W) and the parameters all-gathered back into params[i] over NCCL;
+ * with GRASS_DP_P2P one fused kernel reads every rank's gradient over peer
+ * memory and stores theta' into every rank's params (the registered buffers).
+ * t_l and the bias corrections are advanced on the device by a prologue
+ * kernel on `stream` (capturable, see grass_set_lr_device).
  *   params: host [n] array of DEVICE pointers (fp32, N_p each, updated in place)
  *   grads:  host [n] array of DEVICE pointers (fp32, N_p each, read only), or
  *           of PINNED HOST pointers (world = 1, resident or per-step offload,
