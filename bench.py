@@ -12,9 +12,12 @@ states resident (no offload), 1 B200:
     window commit + Eq. 4 EMA + Eq. 3 softmax              (a2 + a3, host fp64)
     gamma-of-N_L resampling                                (a4, host)
 i.e. the bench resamples EVERY step (T_s = T_u = 1), the most expensive legal
-schedule.  Row a6 (layer-wise offload, configs[2]) is measured in the same run
-and reported under "offload"; the probing pass (a1 alone over all 32 layers)
-under "probe".
+schedule.  Further legs in the same JSON line (--legs): "probe" (a1 alone over
+all 32 layers), "offload" (row a6, configs[2], + Fig. 4 vanilla), "period"
+(f1, T_s = 25), "train" (synthetic 7B fwd+bwd with resident / period+prefetch
+/ per-step offload after and during the backward), "p2p" (f2, the fused
+peer-memory data-parallel kernel), "bf16" (f3), "e2e" (gradients from pinned
+host memory through the public call), "cpu" (the oracle, single thread).
 
 Timing: CUDA events on the stream the library launches on, W untimed warm-up
 steps, K timed steps bracketed by barrier + synchronize, max over ranks.  Every
