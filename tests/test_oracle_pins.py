@@ -426,6 +426,33 @@ def test_clip_coefficient_matches_torch_clip_grad_norm():
         assert coef <= 1.0 and (coef == 1.0) == (max_norm >= float(total) + 1e-6)
 
 
+def test_clipped_step_is_torch_clip_then_adamw_and_mgn_sees_raw_norm():
+    # R17 + R9: GrassOracle.step_layers(max_grad_norm) == torch clip_grad_norm_ over the
+    # call's gradients followed by torch.optim.AdamW (fp64); the MGN window records
+    # the RAW (unclipped) norms.
+    rng = np.random.default_rng(12)
+    numel = [33, 100, 7, 64]
+    ids = [3, 1]
+    lr, wd, max_norm = 1e-2, 0.01, 0.05
+    orc = O.GrassOracle(numel, gamma=2, weight_decay=wd)
+    params = [(rng.standard_normal(k) * 0.02).astype(np.float32) for k in numel]
+    tp = {l: torch.nn.Parameter(torch.from_numpy(params[l].astype(np.float64))) for l in ids}
+    opt = torch.optim.AdamW([tp[l] for l in ids], lr=lr, weight_decay=wd, foreach=False)
+    for step in range(3):
+        grads = {l: (rng.standard_normal(numel[l]) * 0.05).astype(np.float32) for l in ids}
+        orc.step_layers(ids, [params[l] for l in ids], [grads[l] for l in ids], lr, max_grad_norm=max_norm)
+        for l in ids:
+            tp[l].grad = torch.from_numpy(grads[l].astype(np.float64))
+        torch.nn.utils.clip_grad_norm_([tp[l] for l in ids], max_norm)
+        opt.step()
+        for l in ids:
+            np.testing.assert_allclose(params[l], tp[l].detach().numpy(), rtol=1e-6, atol=1e-9)
+            assert orc.last_ss[l] == O.sq_norm(grads[l])                     # raw norm
+    for l in ids:
+        assert orc.mgn.c[l] == 3
+    assert orc.mgn.c[0] == orc.mgn.c[2] == 0
+
+
 # ------------------------------------------------ R18: bf16 mixed precision
 def test_bf16_conversions_match_torch():
     rng = np.random.default_rng(4)

@@ -55,6 +55,11 @@ MUTATIONS = [
     ("clip: no epsilon and no cap", "return min(1.0, max_norm / (total + 1e-6))", "return max_norm / total"),
     ("schedule: resample at T_u", "    if d % T_s == 0:\n        return \"resample\"", "    if d % T_u == 0:\n        return \"resample\""),
     ("schedule: probe includes T_p", "    if step < T_p:", "    if step <= T_p:"),
+    ("clip: MGN records the clipped norm", "        self.accumulate(layer_ids, grads)\n        return params",
+     "        self.accumulate(layer_ids, eff)\n        return params"),
+    ("clip: coefficient from the first layer only",
+     "coef = clip_coefficient([sq_norm(g) for g in grads], max_grad_norm)",
+     "coef = clip_coefficient([sq_norm(grads[0])], max_grad_norm)"),
     ("always groups sampled", "        return sample_layers(list(p)[:self.n_s], self.gamma, self.seed, period)",
      "        return sample_layers(list(p), self.gamma, self.seed, period)"),
 ]
