@@ -60,6 +60,13 @@ MUTATIONS = [
     ("clip: coefficient from the first layer only",
      "coef = clip_coefficient([sq_norm(g) for g in grads], max_grad_norm)",
      "coef = clip_coefficient([sq_norm(grads[0])], max_grad_norm)"),
+    ("bf16: master not initialised from the bf16 parameter",
+     "    if theta_bits is not None:\n        master = bf16_to_f32(theta_bits)", "    if False:\n        pass"),
+    ("bf16: widening drops the low mantissa bits",
+     "    b = np.asarray(bits, dtype=np.uint16).astype(np.uint32) << np.uint32(16)",
+     "    b = (np.asarray(bits, dtype=np.uint16).astype(np.uint32) & np.uint32(0xFFF0)) << np.uint32(16)"),
+    ("always groups recorded in the MGN window", "            if l < self.n_s:                  # always-active groups are not sampled (R19)\n                self.mgn.record(",
+     "            if l < self.n:\n                self.mgn.record("),
     ("always groups sampled", "        return sample_layers(list(p)[:self.n_s], self.gamma, self.seed, period)",
      "        return sample_layers(list(p), self.gamma, self.seed, period)"),
 ]
