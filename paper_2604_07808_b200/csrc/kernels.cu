@@ -219,7 +219,7 @@ __device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, 
         st.S[sg.layer] += sqrt(ss / (double)sg.layer_numel);  // Eq. 2 inner term
         st.c[sg.layer] += 1;
       } else {
-        atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins
+        if (kMutant != 11) atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins (M11: not flagged)
       }
     } else if (mode == kFinalizeShard) {
       st.shard_ss[sg.out_slot] = ss;
@@ -372,7 +372,7 @@ __global__ void grass_step_prologue_kernel(const __grid_constant__ PrologueArgs 
   if (j >= a.n) return;
   const int l = a.layer[j];
   const long long t = st.t[l] + 1;
-  st.t[l] = t;
+  if (kMutant != 8) st.t[l] = t;  // M8: step count not advanced
   const double lr = a.lr_ptr ? (double)*a.lr_ptr : (double)a.lr;
   const double bc1 = 1.0 - pow(a.beta1, (double)t);
   const double bc2 = 1.0 - pow(a.beta2, (double)t);

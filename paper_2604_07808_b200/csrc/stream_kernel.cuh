@@ -109,7 +109,7 @@ __device__ __forceinline__ void store_unit_t(const Seg& sg, int npeer, int64_t e
     bulk_store(sg.m + e0, stg + L::o_m, nv * 4u);
     bulk_store(sg.v + e0, stg + L::o_v, nv * 4u);
     if (P2P) {
-      for (int q = 0; q < npeer; ++q) {
+      for (int q = 0; q < npeer - (kMutant == 9 ? 1 : 0); ++q) {  // M9: theta' not stored to the last rank
         char* dst = static_cast<char*>(sg.tpeer[q]) + (sg.poff + e0) * (BF16 ? 2 : 4);
         bulk_store(dst, stg + (BF16 ? L::o_tb : L::o_t), nv * (BF16 ? 2u : 4u));
       }
@@ -207,7 +207,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           pend_nv[stage] = nv;
         }
         if (nv && (UPDATE || !P2P)) {
-          const bool init = BF16 && UPDATE && st.init_now[sg.layer];
+          const bool init = BF16 && UPDATE && kMutant != 10 && st.init_now[sg.layer];  // M10: master never initialised
           // P2P: the gradient slices go to the gradient ring (below)
           const uint32_t tx = (P2P ? 0u : nv * (uint32_t)L::GB) + (UPDATE ? nv * (init ? 2u : 4u) + 8u * nv : 0u);
           mbar_arrive_expect_tx(&full_bar[stage], tx);
@@ -291,7 +291,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       sc.inv_bc2s = st.scal[3 * sg.layer + 2];
     }
     sc.cf = cf;
-    const bool init = BF16 && UPDATE && st.init_now[sg.layer];
+    const bool init = BF16 && UPDATE && kMutant != 10 && st.init_now[sg.layer];
     const int ui = u - unit_prefix[s];
     const int64_t e0 = (int64_t)ui * kUnit;
     const int ne = (int)min((int64_t)kUnit, sg.n - e0);

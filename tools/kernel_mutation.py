@@ -22,10 +22,14 @@ MUTANTS = {
     5: "DP: gradient not scaled by 1/W",
     6: "P2P: last rank's gradient slice not summed",
     7: "bf16: parameter copy truncated instead of RNE",
+    8: "step prologue: t_l not advanced (bias corrections of step 1 forever)",
+    9: "P2P: theta' not stored into the last rank's parameters",
+    10: "bf16: master never initialised from the bf16 parameter",
+    11: "non-finite norm not flagged",
 }
 TESTS = ("test_step_layers_vs_oracle_multi_step or test_norms_ragged_sizes_vs_oracle or "
          "test_bf16_mixed_precision_vs_oracle or test_p2p_virtual_ranks_vs_oracle or "
-         "test_zero_grad_zero_state_is_identity_on_theta")
+         "test_zero_grad_zero_state_is_identity_on_theta or test_nonfinite_gradient_reported_and_not_recorded")
 
 
 def build():
