@@ -69,6 +69,17 @@ __device__ __forceinline__ float4 stage_g4(const char* stg, int e) {
   if (BF16) return unpack_bf16x4(*reinterpret_cast<const uint2*>(stg + 2 * e));
   return *reinterpret_cast<const float4*>(stg + 4 * e);
 }
+// Element (relative to the unit) of consumer thread `tid`'s vector q in tile
+// k — the fixed map of the norm decomposition (grass_internal.h).  A/B knob
+// GRASS_BF16_MAP8: bf16 threads own 8 ADJACENT elements (one 16-byte read).
+#ifndef GRASS_BF16_MAP8
+#define GRASS_BF16_MAP8 0
+#endif
+template <bool BF16>
+__device__ __forceinline__ int tile_elem(int k, int q, int tid) {
+  if (BF16 && GRASS_BF16_MAP8) return k * (int)kTile + tid * 2 * kVec + q * kVec;
+  return k * (int)kTile + (q * kThreads + tid) * kVec;
+}
 template <bool BF16>
 __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
   return BF16 ? bf2f(sg.g16[idx]) : sg.g[idx];
@@ -310,7 +321,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         for (int k = 0; k < (P2P ? TPS : 1); ++k) {
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
-            const int e = k * (int)kTile + (q * kThreads + tid) * kVec;
+            const int e = tile_elem<BF16>(k, q, tid);
             if (e < nv) {
               const float4 x = stage_g4<BF16>(gring + (size_t)gsl * kGSlot, e);
               if (r == 0) {
@@ -335,7 +346,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       for (int k = 0; k < kPre; ++k)
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q)
-          g4[k][q] = stage_g4<BF16>(stg + L::off_g, k * (int)kTile + (q * kThreads + tid) * kVec);
+          g4[k][q] = stage_g4<BF16>(stg + L::off_g, tile_elem<BF16>(k, q, tid));
 #pragma unroll
       for (int k = 0; k < TPS; ++k) {
         double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
@@ -345,7 +356,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         if (k + kPre < TPS) {  // refill the slot just consumed
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q)
-            g4[k % kPre][q] = stage_g4<BF16>(stg + L::off_g, (k + kPre) * (int)kTile + (q * kThreads + tid) * kVec);
+            g4[k % kPre][q] = stage_g4<BF16>(stg + L::off_g, tile_elem<BF16>(k + kPre, q, tid));
         }
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
@@ -364,7 +375,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
-            const int e = k * (int)kTile + (q * kThreads + tid) * kVec;  // relative to e0
+            const int e = tile_elem<BF16>(k, q, tid);  // relative to e0
             if (e < nv) {
               const float4 g4 = scale4(P2P ? gacc[P2P ? k : 0][q] : stage_g4<BF16>(stg + L::off_g, e), gs);
               acc[0] = fma((double)g4.x, (double)g4.x, acc[0]);
