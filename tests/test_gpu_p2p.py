@@ -435,3 +435,33 @@ def test_debug_check_world1(path):
     plain = G.Grass(numel, **{k: v for k, v in kw.items() if k != "debug_check"})
     plain.mgn_accumulate([0, 1], g)
     assert plain.update_probs() == probs
+
+
+def test_p2p_checkpoint_roundtrip_virtual_ranks(tmp_path):
+    """Every virtual rank writes its checkpoint; fresh P2P contexts restored from
+    them continue bit-identically to the uninterrupted run."""
+    W = 2
+    numel = [8 * W * 700, 8 * W * 1300]
+    vr = VirtualRanks(numel, W, gamma=2, weight_decay=0.01)
+    for step in range(2):
+        vr.set_grads([0, 1], step)
+        vr.step([0, 1], 1e-3)
+    torch.cuda.synchronize()
+    for r, c in enumerate(vr.ctx):
+        c.save_state(str(tmp_path / f"r{r}"))
+    snap = [[p.clone() for p in vr.P[r]] for r in range(W)]
+    vr2 = VirtualRanks(numel, W, gamma=2, weight_decay=0.01)
+    for r, c in enumerate(vr2.ctx):
+        c.load_state(str(tmp_path / f"r{r}"))
+        for l in range(2):
+            vr2.P[r][l].copy_(snap[r][l])
+    for step in range(2, 4):
+        for v in (vr, vr2):
+            v.set_grads([0, 1], step)
+            v.step([0, 1], 1e-3)
+    torch.cuda.synchronize()
+    for r in range(W):
+        for l in range(2):
+            assert torch.equal(vr.P[r][l], vr2.P[r][l])
+            a, b = vr.ctx[r].read_state(l), vr2.ctx[r].read_state(l)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2] == 4
