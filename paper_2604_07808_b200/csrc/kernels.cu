@@ -22,10 +22,11 @@
 //
 // Compile-time A/B knobs (tools/variants.py; defaults are the measured best):
 // GRASS_IEEE_MATH, GRASS_K2_STG_STORE, GRASS_K2_LOAD_EF, GRASS_K2_STORE_EF,
-// GRASS_K2_SEP_OUT, GRASS_K2_NOMATH, GRASS_UPD_STAGES, GRASS_NORM_TPS,
+// GRASS_K2_SEP_OUT, GRASS_K2_NOMATH, GRASS_K1_NOMATH, GRASS_UPD_STAGES, GRASS_NORM_TPS,
 // GRASS_NORM_TPS_BF16, GRASS_NORM_STAGES, GRASS_P2P_NORM_TPS,
 // GRASS_UPD_GRID_SUB, GRASS_NORM_GRID_SUB, GRASS_L2_PREFETCH_{NORM,UPD},
-// GRASS_UNIT_BLOCK; GRASS_MUTANT=k plants mistake k (tools/kernel_mutation.py).
+// GRASS_UNIT_BLOCK, GRASS_BF16_MAP8; GRASS_MUTANT=k plants mistake k
+// (tools/kernel_mutation.py).
 //
 // The tile partial (grass_internal.h) is a FIXED function of the tile's data:
 // consumer thread t owns elements (q*kThreads + t)*4 + j, j = 0..3, q = 0..

@@ -360,10 +360,14 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         }
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q) {
+#ifdef GRASS_K1_NOMATH  // A/B only: the same data movement with trivial arithmetic (speed of light)
+          acc[0] += fabsf(cur[q].x) + fabsf(cur[q].y) + fabsf(cur[q].z) + fabsf(cur[q].w);
+#else
           acc[0] = fma((double)cur[q].x, (double)cur[q].x, acc[0]);
           acc[1] = fma((double)cur[q].y, (double)cur[q].y, acc[1]);
           acc[2] = fma((double)cur[q].z, (double)cur[q].z, acc[2]);
           acc[3] = fma((double)cur[q].w, (double)cur[q].w, acc[3]);
+#endif
         }
         const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
         if (lane == 0) red[i & 1][k][warp] = t;

@@ -11,10 +11,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
-    "map4": [],
-    "map8": ["GRASS_BF16_MAP8=1"],
-    "map4_again": [],
-    "map8_again": ["GRASS_BF16_MAP8=1"],
+    "base": [],
+    "k1_nomath": ["GRASS_K1_NOMATH"],
+    "base_again": [],
+    "k1_nomath_again": ["GRASS_K1_NOMATH"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
