@@ -597,6 +597,8 @@ def run_grass(args, rank, world, local):
                 kw.update(offload=True, residency=G.RESIDENCY_PERIOD)
             elif mode in ("offload", "offload_bwd"):
                 kw.update(offload=True)
+            elif mode == "step_prefetch":
+                kw.update(offload=True, residency=G.RESIDENCY_STEP_PREFETCH)
             tc = G.Grass([n_p] * NL, gamma=gamma, **kw)
             tc.mgn_accumulate(list(range(NL)), grads, stream=s)
             tc.update_probs()
@@ -609,7 +611,12 @@ def run_grass(args, rank, world, local):
                     cur = tc.sample_layers(k // T_s + 1)
                     if mode == "prefetch":
                         tc.prefetch_layers(cur, stream=s)   # moves during fwd/bwd
-                if mode == "offload_bwd":
+                if mode == "step_prefetch":
+                    # the paper's per-step round trip with its prefetch: fetch the
+                    # trainable layers' m/v during the forward, update each as soon
+                    # as the backward has produced its gradient, write back at once
+                    tc.prefetch_layers(cur, stream=s)
+                if mode in ("offload_bwd", "step_prefetch"):
                     # per-step round trip of each trainable layer's m/v, issued on a
                     # side stream the moment backward has produced its gradient:
                     # fetch / update / write-back overlap the rest of the backward
@@ -647,11 +654,12 @@ def run_grass(args, rank, world, local):
         res = {"standin": f"{n_mm} bf16 GEMMs 8192^3 = {n_mm * 2 * 8192 ** 3:.3g} FLOP "
                           "(LLaMA-2-7B fwd+bwd, 4 x 1024 tokens; SYNTHETIC)",
                "standin_ms": e0_.elapsed_time(e1_), "schedule": f"T_s=T_u={T_s}, {nsteps} steps"}
-        for mode in ("resident", "prefetch", "offload", "offload_bwd"):
+        for mode in ("resident", "prefetch", "offload", "offload_bwd", "step_prefetch"):
             res[f"{mode}_step_ms"] = run(mode)
         res["period_prefetch_over_resident"] = res["prefetch_step_ms"] / res["resident_step_ms"]
         res["per_step_offload_over_resident"] = res["offload_step_ms"] / res["resident_step_ms"]
         res["per_step_offload_during_backward_over_resident"] = res["offload_bwd_step_ms"] / res["resident_step_ms"]
+        res["per_step_round_trip_with_prefetch_over_resident"] = res["step_prefetch_step_ms"] / res["resident_step_ms"]
         res["offloaded_within_10pct_of_resident"] = res["period_prefetch_over_resident"] <= 1.10
         return res
 

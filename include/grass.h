@@ -111,7 +111,8 @@ typedef struct grass_config {
                                   GRASS_RESIDENCY_PERIOD (a layer's m/v stay
                                   in HBM while it stays trainable; swapped only when the
                                   sampled set changes) */
-  int32_t cache_layers;        /* GRASS_RESIDENCY_PERIOD: device layer slots (>= gamma; 0 = gamma) */
+  int32_t cache_layers;        /* GRASS_RESIDENCY_PERIOD / _STEP_PREFETCH: device layer slots
+                                  (>= gamma; 0 = gamma) */
   double max_grad_norm;        /* > 0: clip each grass_step_layers call's gradients by their
                                   global norm, coef = min(1, max/(||g||+1e-6)) (torch
                                   clip_grad_norm_; paper silent; DESIGN R17).
@@ -166,7 +167,12 @@ typedef enum {
 
 typedef enum {
   GRASS_RESIDENCY_STEP = 0,
-  GRASS_RESIDENCY_PERIOD = 1
+  GRASS_RESIDENCY_PERIOD = 1,
+  /* the paper's per-step round trip with whole-layer prefetch:
+     grass_prefetch_layers fetches the step's trainable layers ahead (e.g.
+     during the forward), grass_step_layers updates them and writes their m/v
+     back to host right after the update; device slots as for PERIOD */
+  GRASS_RESIDENCY_STEP_PREFETCH = 2
 } grass_residency;
 
 /* Fills *cfg with the defaults above (layer_numel = NULL, n_layers = 0). */
@@ -295,7 +301,7 @@ grass_status grass_write_master(grass_ctx* ctx, int32_t layer, const float* in);
 grass_status grass_read_state(grass_ctx* ctx, int32_t layer, float* m_out, float* v_out,
                               int64_t* t_out);
 
-/* GRASS_RESIDENCY_PERIOD: starts bringing the optimizer states of the listed
+/* GRASS_RESIDENCY_PERIOD / _STEP_PREFETCH: starts bringing the optimizer states of the listed
  * layers into the HBM cache now (evicting least-recently-used layers that are
  * not listed), on the context's copy streams, without updating anything.
  * Call it right after grass_sample_layers at a period boundary: the transfers

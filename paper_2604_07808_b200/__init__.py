@@ -4,7 +4,7 @@ The product is libgrass.so (C ABI, include/grass.h) built from csrc/; this
 package is its thin ctypes binding.  It never imports oracle/.
 """
 from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_CONTINUE, DECIDE_PROBE, DECIDE_RESAMPLE,
-                      RESIDENCY_PERIOD, RESIDENCY_STEP, DTYPE_BF16, DTYPE_FP32, DP_NCCL, DP_P2P,
+                      RESIDENCY_PERIOD, RESIDENCY_STEP, RESIDENCY_STEP_PREFETCH, DTYPE_BF16, DTYPE_FP32, DP_NCCL, DP_P2P,
                       POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM, Grass, GrassError,
                       exported_symbols, lib, nccl_unique_id, sample_from_probs,
                       schedule_decision, shard_range, softmax_probs, splitmix64, tile_elems,
@@ -17,5 +17,5 @@ __all__ = ["Grass", "GrassSchedule", "GrassBlocks", "flatten_params", "GrassErro
            "sample_from_probs", "schedule_decision", "shard_range", "softmax_probs",
            "splitmix64", "tile_elems", "uniform", "POLICY_ADAPTIVE", "POLICY_STATIC",
            "POLICY_UNIFORM", "DECIDE_PROBE", "DECIDE_COMMIT_RESAMPLE", "DECIDE_RESAMPLE",
-           "DECIDE_CONTINUE", "RESIDENCY_STEP", "RESIDENCY_PERIOD", "DTYPE_FP32", "DTYPE_BF16",
+           "DECIDE_CONTINUE", "RESIDENCY_STEP", "RESIDENCY_PERIOD", "RESIDENCY_STEP_PREFETCH", "DTYPE_FP32", "DTYPE_BF16",
            "DP_NCCL", "DP_P2P", "ipc_export", "ipc_import", "selftest_p2p"]

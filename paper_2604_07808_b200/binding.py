@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("GRASS_LIB_PATH") or os.path.join(_PKG, "libgrass.so")
 OK, E_INVALID, E_STATE, E_CUDA, E_NCCL, E_OOM, E_NONFINITE, E_IO = range(8)
 POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM = range(3)
 DECIDE_PROBE, DECIDE_COMMIT_RESAMPLE, DECIDE_RESAMPLE, DECIDE_CONTINUE = range(4)
-RESIDENCY_STEP, RESIDENCY_PERIOD = range(2)
+RESIDENCY_STEP, RESIDENCY_PERIOD, RESIDENCY_STEP_PREFETCH = range(3)
 DTYPE_FP32, DTYPE_BF16 = range(2)
 DP_NCCL, DP_P2P = range(2)
 IPC_HANDLE_BYTES = 64

@@ -132,7 +132,8 @@ grass_status validate_config(const grass_config* cfg, std::string* why) {
     if (cfg->chunk_elems < 0 || cfg->chunk_elems % kTile != 0)
       return bad("chunk_elems must be a non-negative multiple of grass_tile_elems()");
     if (cfg->ring_slots < 0) return bad("ring_slots must be >= 0");
-    if (cfg->residency != GRASS_RESIDENCY_STEP && cfg->residency != GRASS_RESIDENCY_PERIOD)
+    if (cfg->residency != GRASS_RESIDENCY_STEP && cfg->residency != GRASS_RESIDENCY_PERIOD &&
+        cfg->residency != GRASS_RESIDENCY_STEP_PREFETCH)
       return bad("unknown residency");
     if (cfg->cache_layers < 0 || cfg->cache_layers > nsamp)
       return bad("cache_layers must lie in [0, N_L]");
@@ -222,7 +223,7 @@ grass_status check_call(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_
         return c->fail(GRASS_E_INVALID, "not a CUDA pointer");
       }
       if (a == p2 && host_p2 && at.type == cudaMemoryTypeHost) {
-        if (c->dp || c->p2p || (c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD))
+        if (c->dp || c->p2p || (c->cfg.offload && c->cfg.residency != GRASS_RESIDENCY_STEP))
           return c->fail(GRASS_E_INVALID, "host gradients need world = 1 and resident or per-step "
                                           "offloaded optimizer states");
         (*host_p2)[i] = 1;  // pinned host gradient: streamed through the gradient ring
@@ -366,7 +367,8 @@ void free_ctx(grass_ctx* c) {
     else
       cudaFree(c->state_block);
   }
-  for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free, &c->ev_layer_done, &c->ev_free_list, &c->ev_slot_ready})
+  for (auto* v : {&c->ev_h2d, &c->ev_comp, &c->ev_free, &c->ev_layer_done, &c->ev_free_list, &c->ev_slot_ready,
+                  &c->ev_slot_wb})
     for (cudaEvent_t e : *v)
       if (e) cudaEventDestroy(e);
   for (auto& pe : c->ev_pending) cudaEventDestroy(pe.second);
@@ -484,7 +486,8 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
   }
   c->slot_used.assign(c->slots, 0);
   if (cfg->offload) {
-    if (cfg->residency == GRASS_RESIDENCY_PERIOD) {
+    if (cfg->residency != GRASS_RESIDENCY_STEP) {  // whole-layer slots (PERIOD, STEP_PREFETCH)
+      c->write_through = cfg->residency == GRASS_RESIDENCY_STEP_PREFETCH;
       c->cache_slots = std::max(cfg->gamma, cfg->cache_layers);
       CUDA_TRY(c, dalloc((void**)&c->d_cache,
                          sizeof(float) * (size_t)c->ns * (size_t)c->slot_stride * c->cache_slots));
@@ -497,6 +500,9 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
       c->ev_slot_ready.assign(c->cache_slots, nullptr);
       for (auto& e : c->ev_slot_ready) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       c->slot_ready_pending.assign(c->cache_slots, 0);
+      c->ev_slot_wb.assign(c->cache_slots, nullptr);
+      for (auto& e : c->ev_slot_wb) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->slot_wb_pending.assign(c->cache_slots, 0);
     } else {
       CUDA_TRY(c, dalloc((void**)&c->d_ring, sizeof(float) * (size_t)c->ns * (size_t)c->chunk * c->slots));
     }

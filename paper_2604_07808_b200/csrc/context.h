@@ -82,6 +82,9 @@ struct grass_ctx {
   cudaEvent_t ev_evict = nullptr, ev_fill = nullptr;
   std::vector<cudaEvent_t> ev_slot_ready;  // grass_prefetch_layers: fill of the slot done
   std::vector<char> slot_ready_pending;
+  bool write_through = false;              // GRASS_RESIDENCY_STEP_PREFETCH: write back after each update
+  std::vector<cudaEvent_t> ev_slot_wb;     // write-through: the slot's write-back has read it
+  std::vector<char> slot_wb_pending;
 
   // outstanding stream-ordered work (for the synchronising calls): the last
   // event recorded on each stream the caller used
@@ -263,6 +266,7 @@ void cache_plan(grass_ctx* c, const int32_t* ids, const std::vector<int>& order,
 grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, const Seg& base, void* param, const void* g, bool init, int32_t mode, cudaStream_t s);
 grass_status prefetch_into(grass_ctx* c, int l, int slot, int victim);
 grass_status flush_cache(grass_ctx* c);
+grass_status writeback_release(grass_ctx* c, int l, int slot, cudaStream_t s);
 float* state_ptr(grass_ctx* c, int a, int layer, bool* on_device);
 grass_status copy_state_out(grass_ctx* c, int a, int layer, float* out);
 grass_status copy_state_in(grass_ctx* c, int a, int layer, const float* in);

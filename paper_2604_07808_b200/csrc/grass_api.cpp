@@ -224,7 +224,8 @@ grass_status grass_write_master(grass_ctx* c, int32_t layer, const float* in) tr
 
 grass_status grass_prefetch_layers(grass_ctx* c, const int32_t* ids, int32_t n, void* stream) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
-  if (c->cache_slots == 0) return c->fail(GRASS_E_STATE, "prefetch needs GRASS_RESIDENCY_PERIOD");
+  if (c->cache_slots == 0)
+    return c->fail(GRASS_E_STATE, "prefetch needs GRASS_RESIDENCY_PERIOD or GRASS_RESIDENCY_STEP_PREFETCH");
   std::vector<int> order;
   grass_status s = check_call(c, c->bf16, ids, n, nullptr, nullptr, &order);
   if (s != GRASS_OK) return s;

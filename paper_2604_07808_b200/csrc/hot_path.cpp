@@ -116,7 +116,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   const bool clip = c->cfg.max_grad_norm > 0.0;
   const int32_t mode = clip ? kFinalizeNone : ((sharded || p2p) ? kFinalizeShard : kFinalizeMgn);
   if (p2p && (s = p2p_check(c, ids, n, params, grads)) != GRASS_OK) return s;
-  const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
+  const bool period = c->cfg.offload && c->cfg.residency != GRASS_RESIDENCY_STEP;  // whole-layer slots
   const int nact = (int)order.size();
   int ncached = 0;
   for (int i = 0; i < n; ++i) ncached += always_active(c, ids[i]) ? 0 : 1;
@@ -228,12 +228,13 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
         set_update(c, &base, param, sp, init);
         if (b.nseg == kMaxSeg && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
         push_seg(&b, base);
-        if (sharded && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
+        if ((sharded || c->write_through) && (s = flush(c, &b, true, st)) != GRASS_OK) return s;
       } else if ((s = swap_in_layer(c, l, slot, victim_of[j], base, param, g, init, mode, st)) != GRASS_OK) {
         return s;
       }
       c->slot_use[slot] = c->call_seq;
       c->slot_dirty[slot] = 1;
+      if (c->write_through && (s = writeback_release(c, l, slot, st)) != GRASS_OK) return s;
     } else if (!home_on_device(c, l)) {
       if ((s = offload_layer(c, l, base, param, g, init, mode, st, g_host[i] != 0)) != GRASS_OK) return s;
     } else if (g_host[i]) {

@@ -168,6 +168,10 @@ grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, const Seg&
   const int64_t lv = (victim >= 0 && c->slot_dirty[slot]) ? c->shard_len[victim] : 0;
   if (overlap && c->layer_done_valid[l])  // l's host copy must be final
     CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_layer_done[l], 0));
+  if (c->slot_wb_pending[slot]) {  // write-through: the slot's previous write-back must have read it
+    CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_slot_wb[slot], 0));
+    c->slot_wb_pending[slot] = 0;
+  }
   for (int64_t off = 0; off < std::max(ll, lv); off += c->chunk) {
     if (off < lv) {
       const size_t vb = sizeof(float) * (size_t)std::min(c->chunk, lv - off);
@@ -219,6 +223,10 @@ grass_status prefetch_into(grass_ctx* c, int l, int slot, int victim) {
   const int64_t ll = c->shard_len[l];
   const int64_t lv = (victim >= 0 && c->slot_dirty[slot]) ? c->shard_len[victim] : 0;
   if (c->layer_done_valid[l]) CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, c->ev_layer_done[l], 0));
+  if (c->slot_wb_pending[slot]) {  // write-through: the slot's previous write-back must have read it
+    CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, c->ev_slot_wb[slot], 0));
+    c->slot_wb_pending[slot] = 0;
+  }
   for (int64_t off = 0; off < std::max(ll, lv); off += c->chunk) {
     if (off < lv) {
       const size_t vb = sizeof(float) * (size_t)std::min(c->chunk, lv - off);
@@ -252,6 +260,33 @@ grass_status prefetch_into(grass_ctx* c, int l, int slot, int victim) {
   c->slot_layer[slot] = l;
   c->layer_slot[l] = slot;
   c->slot_dirty[slot] = 0;  // the cached copy equals the host copy
+  return GRASS_OK;
+}
+
+// GRASS_RESIDENCY_STEP_PREFETCH: after layer l's update in `slot` (enqueued on
+// s), write its states home on the d2h stream and release the slot — the
+// paper's per-step round trip over the prefetch slots.
+grass_status writeback_release(grass_ctx* c, int l, int slot, cudaStream_t s) {
+  const bool overlap = c->cfg.overlap != 0;
+  cudaStream_t sd = overlap ? c->d2h : s;
+  if (overlap) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_evict, s));  // the update has finished with the slot
+    CUDA_TRY(c, cudaStreamWaitEvent(sd, c->ev_evict, 0));
+  }
+  const int64_t len = c->shard_len[l];
+  for (int64_t off = 0; off < len; off += c->chunk) {
+    const size_t bytes = sizeof(float) * (size_t)std::min(c->chunk, len - off);
+    TraceScope ts(c, sd, GRASS_TRACE_D2H, l, off, (int64_t)(bytes / sizeof(float)));
+    for (int a = 0; a < c->ns; ++a)
+      CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][l] + off, cache_arr(c, slot, a) + off, bytes, cudaMemcpyDeviceToHost, sd));
+  }
+  CUDA_TRY(c, cudaEventRecord(c->ev_layer_done[l], sd));  // next fetch of l waits for it
+  c->layer_done_valid[l] = 1;
+  CUDA_TRY(c, cudaEventRecord(c->ev_slot_wb[slot], sd));  // next fill of the slot waits for it
+  c->slot_wb_pending[slot] = 1;
+  c->slot_layer[slot] = -1;
+  c->layer_slot[l] = -1;
+  c->slot_dirty[slot] = 0;
   return GRASS_OK;
 }
 

@@ -43,9 +43,11 @@ class GrassSchedule:
         self.n_layers = grass.n_layers
         self.always = list(getattr(grass, "always_ids", []))
         self.n_sampled = self.n_layers - len(self.always)
-        # prefetch only makes sense with period residency
-        period = bool(cfg.offload) and cfg.residency == 1
-        self.prefetch = period if prefetch is None else (prefetch and period)
+        # prefetch needs whole-layer device slots: period residency prefetches at
+        # each resample, the per-step round trip (STEP_PREFETCH) at every step
+        slots = bool(cfg.offload) and cfg.residency in (1, 2)   # PERIOD, STEP_PREFETCH
+        self.prefetch = slots if prefetch is None else (prefetch and slots)
+        self.prefetch_every_step = bool(cfg.offload) and cfg.residency == 2
         self.trainable: list[int] = []
         self.probs: list[float] | None = None
         self.period_index = -1
@@ -70,8 +72,10 @@ class GrassSchedule:
             if self.trace_path:
                 self._log({"step": step, "event": "resample", "period": self.period_index,
                            "sampled": list(self.trainable)})
-            if self.prefetch:
+            if self.prefetch and not self.prefetch_every_step:
                 self.g.prefetch_layers(self.trainable, stream=stream)
+        if self.prefetch and self.prefetch_every_step:
+            self.g.prefetch_layers(self.trainable, stream=stream)   # fetched during this step's forward
         return list(self.trainable) + self.always
 
     def end_step(self, step: int, params: Sequence, grads: Sequence, lr: float, stream=None):

@@ -799,7 +799,9 @@ def test_fuzz_pipelines_bit_identical(seed):
     kws = [dict(), dict(offload=True, chunk_elems=chunk, ring_slots=int(rng.integers(1, 4)),
                         overlap=bool(rng.integers(0, 2))),
            dict(offload=True, chunk_elems=chunk, residency=G.RESIDENCY_PERIOD,
-                cache_layers=int(rng.integers(0, nl + 1)), overlap=bool(rng.integers(0, 2)))]
+                cache_layers=int(rng.integers(0, nl + 1)), overlap=bool(rng.integers(0, 2))),
+           dict(offload=True, chunk_elems=chunk, residency=G.RESIDENCY_STEP_PREFETCH,
+                overlap=bool(rng.integers(0, 2)))]
     if seed % 2:
         kws.append(dict(force_nccl=True))
     ctxs = [G.Grass(numel, gamma=gamma, weight_decay=0.01, **kw) for kw in kws]
@@ -1247,3 +1249,32 @@ def test_all_zero_gradients_give_uniform_probabilities():
     gr.mgn_accumulate([0, 1, 2], [torch.zeros(n, device=DEV) for n in numel])
     assert gr.update_probs() == [1 / 3] * 3
     assert gr.get_mgn()["last_ss"] == [0.0, 0.0, 0.0]
+
+
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("prefetch", [True, False])
+def test_step_prefetch_residency_bit_identical_to_resident(dtype, overlap, prefetch):
+    """GRASS_RESIDENCY_STEP_PREFETCH (the paper's per-step round trip with
+    whole-layer prefetch): states fetched (ahead, or inside the call), updated,
+    written home right after the update — bit-identical to resident states."""
+    tdt = torch.bfloat16 if dtype == G.DTYPE_BF16 else torch.float32
+    numel = [4096 * 7 + 8, 65_536, 4096 * 3, 4096]
+    kw = dict(gamma=2, weight_decay=0.01, param_dtype=dtype)
+    ref = G.Grass(numel, **kw)
+    sp = G.Grass(numel, offload=True, residency=G.RESIDENCY_STEP_PREFETCH, overlap=overlap,
+                 chunk_elems=8192, **kw)
+    base = [layer_params(n, l, device=DEV).to(tdt) for l, n in enumerate(numel)]
+    pr, ps = [b.clone() for b in base], [b.clone() for b in base]
+    for step, ids in enumerate([[0, 1], [1, 2], [1, 2], [3, 0], [2, 3]]):
+        if prefetch:
+            sp.prefetch_layers(ids)
+        g = [layer_grad(numel[l], l, 1e-3, step=step, device=DEV).to(tdt) for l in ids]
+        ref.step_layers(ids, [pr[l] for l in ids], g, 1e-3)
+        sp.step_layers(ids, [ps[l] for l in ids], g, 1e-3)
+    torch.cuda.synchronize()
+    for l in range(4):
+        assert torch.equal(pr[l], ps[l]), l
+        a, b = ref.read_state(l), sp.read_state(l)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and a[2] == b[2], l
+    assert ref.get_mgn()["S"] == sp.get_mgn()["S"]
