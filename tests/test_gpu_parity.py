@@ -879,7 +879,8 @@ def test_fuzz_dtypes_clip_checkpoint(seed, tmp_path):
     common = dict(gamma=gamma, weight_decay=0.01, max_grad_norm=clip, param_dtype=dtype, n_always=n_alw)
     kws = [dict(), dict(offload=True, chunk_elems=chunk, ring_slots=int(rng.integers(1, 4))),
            dict(offload=True, chunk_elems=chunk, residency=G.RESIDENCY_PERIOD),
-           dict(force_nccl=True)]
+           dict(force_nccl=True),
+           dict(offload=True, chunk_elems=chunk, residency=G.RESIDENCY_STEP_PREFETCH)]
     ctxs = [G.Grass(numel, **common, **kw) for kw in kws]
     base = [layer_params(n, l, device=DEV).to(tdt) for l, n in enumerate(numel)]
     ps = [[p.clone() for p in base] for _ in ctxs]
@@ -892,6 +893,8 @@ def test_fuzz_dtypes_clip_checkpoint(seed, tmp_path):
             ctxs[2].prefetch_layers(ids)
         elif r < 0.5:   # prefetch a different set (evicted or reused before use)
             ctxs[2].prefetch_layers([int(x) for x in rng.choice(nl, size=min(gamma, nl), replace=False)])
+        if rng.random() < 0.6:   # the per-step round trip prefetches the step's layers (or not)
+            ctxs[4].prefetch_layers(ids)
         for gr, p in zip(ctxs, ps):
             gr.step_layers(ids, [p[l] for l in ids], grads, 1e-3)
         if step == 4:   # checkpoint the offload context, restore into a fresh period context
