@@ -437,11 +437,27 @@ def run_grass(args, rank, world, local):
                 "nvlink_GBps_per_rank": link / (call_ms / 1e3) / 1e9 if world > 1 else None}
 
 
+    def agreed_ctx(**kw):
+        """A context every rank created (pinned-host allocations can fail on one
+        rank only): None on every rank if any rank failed, so no rank is left
+        waiting in a later collective."""
+        c_, err_ = None, None
+        try:
+            c_ = G.Grass([n_p] * NL, device=local, rank=rank, world=world, **kw)
+        except Exception as ex:
+            err_ = f"{type(ex).__name__}: {ex}"[:300]
+        if all_ok(c_ is not None):
+            return c_, None
+        if c_ is not None:
+            c_.close()
+        return None, err_ or "context creation failed on another rank"
+
     # ---- offload leg: configs[2] (row a6)
     def leg_offload():
         t_pin = time.perf_counter()
-        octx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, device=local,
-                       offload=True, rank=rank, world=world)
+        octx, err = agreed_ctx(gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, offload=True)
+        if octx is None:
+            return {"error": err}
         t_pin = time.perf_counter() - t_pin
         duplex = measure_duplex(dev)
         octx.mgn_accumulate(list(range(NL)), grads, stream=s)
@@ -482,8 +498,10 @@ def run_grass(args, rank, world, local):
         # Fig. 4 "vanilla" (HtoD -> update -> DtoH serially, overlap = 0) on the
         # same workload: the overlap speedup the paper quotes as 1.08x on a full
         # training step
-        vctx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, device=local,
-                       offload=True, overlap=False, rank=rank, world=world)
+        vctx, err = agreed_ctx(gamma=gamma, T_p=1, T_s=1, T_u=1, seed=1234, offload=True, overlap=False)
+        if vctx is None:
+            res["vanilla_error"] = err
+            return res
         vctx.mgn_accumulate(list(range(NL)), grads, stream=s)
         vctx.update_probs()
         vids = vctx.sample_layers(0)
@@ -505,8 +523,10 @@ def run_grass(args, rank, world, local):
         vctx.close()
         # optimizer-state HBM with offload as gamma grows (paper: LISA +1.63 GB vs
         # GRASS +0.14 GB from gamma 2 to 4): the ring does not grow
-        g4 = G.Grass([n_p] * NL, gamma=min(2 * gamma, NL), T_p=1, T_s=1, T_u=1, device=local,
-                     offload=True, rank=rank, world=world)
+        g4, err = agreed_ctx(gamma=min(2 * gamma, NL), T_p=1, T_s=1, T_u=1, offload=True)
+        if g4 is None:
+            res["device_state_bytes_2x_gamma_error"] = err
+            return res
         res["device_state_bytes_2x_gamma"] = g4.device_bytes
         g4.close()
         return res
@@ -517,8 +537,10 @@ def run_grass(args, rank, world, local):
     def leg_period():
         torch.cuda.empty_cache()
         T_s = 25
-        pctx = G.Grass([n_p] * NL, gamma=gamma, T_p=1, T_s=T_s, T_u=T_s, seed=1234, device=local,
-                       offload=True, residency=G.RESIDENCY_PERIOD, rank=rank, world=world)
+        pctx, err = agreed_ctx(gamma=gamma, T_p=1, T_s=T_s, T_u=T_s, seed=1234, offload=True,
+                               residency=G.RESIDENCY_PERIOD)
+        if pctx is None:
+            return {"error": err}
         pctx.mgn_accumulate(list(range(NL)), grads, stream=s)
         pctx.update_probs()
         pids = pctx.sample_layers(0)
