@@ -148,3 +148,35 @@ def test_captured_nccl_step_replays_equal_eager_steps():
     for _ in range(3):
         g.replay()
     _same(eager, graph, pe, pg, ids)
+
+
+def test_captured_schedule_period_with_always_group_and_commit():
+    """A whole sampling period captured once: the trainable set plus an
+    always-active group, replayed T_s times, then a commit — equal to the
+    same period run eagerly (MGN, probabilities, states)."""
+    numel = [8192] * 4 + [4096 * 3]
+    T_s = 5
+    ctxs, P = [], []
+    base = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    grads = [layer_grad(n, l, 10.0 ** (-3 - (l % 3)), device=DEV) for l, n in enumerate(numel)]
+    for _ in range(2):
+        c = G.Grass(numel, gamma=2, T_p=1, T_s=T_s, n_always=1, seed=4, weight_decay=0.01)
+        c.mgn_accumulate([0, 1, 2, 3], grads[:4])
+        c.update_probs()
+        ctxs.append(c)
+        P.append([b.clone() for b in base])
+    eager, graph = ctxs
+    ids = eager.sample_layers(0)
+    assert ids == graph.sample_layers(0)
+    layers = ids + [4]
+    for _ in range(T_s):
+        eager.step_layers(layers, [P[0][l] for l in layers], [grads[l] for l in layers], 1e-3)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graph.step_layers(layers, [P[1][l] for l in layers], [grads[l] for l in layers], 1e-3,
+                          stream=torch.cuda.current_stream())
+    for _ in range(T_s):
+        g.replay()
+    assert eager.update_probs() == graph.update_probs()
+    _same(eager, graph, P[0], P[1], layers)
+    assert eager.sample_layers(1) == graph.sample_layers(1)
