@@ -58,6 +58,7 @@ struct grass_ctx {
   std::vector<char> master_valid;  // host mirror of DevState::mvalid (offload copy decisions)
   const float* lr_ptr = nullptr;   // grass_set_lr_device: lr read on the device each step
   bool captured = false;           // a hot-path call was captured into a CUDA graph
+  bool captured_offload = false;   // the last offloaded step_layers was captured
   std::vector<int64_t> t;
 
   // offload ring (step residency)

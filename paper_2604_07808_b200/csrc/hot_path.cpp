@@ -14,17 +14,46 @@ namespace gapi {
 // Is `stream` being captured into a CUDA graph?  Captured hot-path calls are
 // replayed by the caller; the step state (t_l, AdamW scalars, the bf16 master
 // flag, the MGN window) lives on the device so every replay advances it.
-// Supported for HBM-resident optimizer states with device gradients (no
-// offload, no tracing; P2P with its device barriers): the offload pipelines
-// keep host-side ring and hazard state.
+// Supported with device gradients and tracing off, for HBM-resident states
+// and for the per-step offload pipeline (GRASS_RESIDENCY_STEP): its copy
+// streams are forked into the capture and every hazard of the captured call
+// is an event recorded inside it.  Period residency keeps a host-side cache
+// plan and is not capturable; P2P needs p2p_sync (device barrier generations).
 grass_status capture_check(grass_ctx* c, cudaStream_t st, bool any_host, bool* capturing) {
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   CUDA_TRY(c, cudaStreamIsCapturing(st, &cap));
   *capturing = cap == cudaStreamCaptureStatusActive;
-  if (*capturing && (c->cfg.offload || (c->p2p && !c->cfg.p2p_sync) || any_host || c->tracing))
-    return c->fail(GRASS_E_INVALID, "CUDA-graph capture needs HBM-resident optimizer states and device "
-                                    "gradients (no offload, P2P only with p2p_sync, tracing off)");
+  const bool step_offload = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_STEP;
+  if (*capturing && ((c->cfg.offload && !step_offload) || (c->p2p && !c->cfg.p2p_sync) || any_host || c->tracing))
+    return c->fail(GRASS_E_INVALID, "CUDA-graph capture needs device gradients, tracing off, HBM-resident "
+                                    "or per-step offloaded states (not period residency), P2P only with p2p_sync");
+  if (*capturing && step_offload && !c->ev_pending.empty())
+    return c->fail(GRASS_E_STATE, "capturing an offloaded step: call grass_sync first (earlier copies "
+                                  "must be complete)");
   if (*capturing) c->captured = true;
+  return GRASS_OK;
+}
+
+// Offload hazards around CUDA-graph capture: events recorded outside a
+// capture cannot be waited on inside it and vice versa.  Inside a capture
+// (after grass_sync) every earlier copy is complete, so the host-side hazard
+// flags start clean and the copy streams are forked into the capture; eager
+// calls after captured ones wait for the device once and start clean too.
+grass_status offload_capture_fence(grass_ctx* c, cudaStream_t st, bool capturing) {
+  if (!c->cfg.offload || c->cfg.residency != GRASS_RESIDENCY_STEP) return GRASS_OK;
+  if (!capturing && !c->captured_offload) return GRASS_OK;
+  if (!capturing) CUDA_TRY(c, cudaDeviceSynchronize());
+  std::fill(c->layer_done_valid.begin(), c->layer_done_valid.end(), 0);
+  std::fill(c->slot_used.begin(), c->slot_used.end(), 0);
+  c->captured_offload = capturing;
+  if (capturing && c->cfg.overlap) {
+    cudaEvent_t e = take_event(c);
+    if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
+    CUDA_TRY(c, cudaEventRecord(e, st));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, e, 0));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->d2h, e, 0));
+    c->ev_free_list.push_back(e);
+  }
   return GRASS_OK;
 }
 
@@ -126,6 +155,8 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   if (period && ncached > c->cache_slots)
     return c->fail(GRASS_E_INVALID, "period residency: more layers in one call than cache slots "
                                     "(raise cache_layers)");
+  // (all arguments validated: from here on work is enqueued)
+  if ((s = offload_capture_fence(c, st, capturing)) != GRASS_OK) return s;
   struct CoefReset {  // the clip multiplier only applies inside this call
     grass_ctx* c;
     ~CoefReset() { c->cur_coef = nullptr; }

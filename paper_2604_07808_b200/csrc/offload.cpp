@@ -56,9 +56,12 @@ grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, co
     char* gslot = g_host ? c->d_gring + (size_t)slot * c->chunk * c->esz : nullptr;
     {
       TraceScope ts(c, sh, GRASS_TRACE_H2D, l, off, n);
+      // every state array is fetched, the bf16 master too even on the layer's
+      // first update (then the kernel initialises it from the bf16 parameter
+      // and never reads it): the decision is the device's (DevState::init_now),
+      // so a captured graph of this call stays right on every replay
       for (int a = 0; a < c->ns; ++a)
-        if (!(a == 2 && init))  // an uninitialised master is written, not read
-          CUDA_TRY(c, cudaMemcpyAsync(ring[a], c->arr[a][l] + off, bytes, cudaMemcpyHostToDevice, sh));
+        CUDA_TRY(c, cudaMemcpyAsync(ring[a], c->arr[a][l] + off, bytes, cudaMemcpyHostToDevice, sh));
       if (g_host)
         CUDA_TRY(c, cudaMemcpyAsync(gslot, elem(g, off, c->esz), (size_t)n * c->esz, cudaMemcpyHostToDevice, sh));
     }

@@ -99,7 +99,7 @@ def test_capture_rejected_where_unsupported():
     numel = [8192, 8192]
     p = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
     g = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
-    off = G.Grass(numel, gamma=2, offload=True)
+    off = G.Grass(numel, gamma=2, offload=True, residency=G.RESIDENCY_PERIOD)   # host-side cache plan
     graph = torch.cuda.CUDAGraph()
     with pytest.raises(G.GrassError, match="capture"), pytest.warns(UserWarning):
         with torch.cuda.graph(graph):
@@ -180,3 +180,29 @@ def test_captured_schedule_period_with_always_group_and_commit():
     assert eager.update_probs() == graph.update_probs()
     _same(eager, graph, P[0], P[1], layers)
     assert eager.sample_layers(1) == graph.sample_layers(1)
+
+
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+@pytest.mark.parametrize("overlap", [True, False])
+def test_captured_offloaded_step_replays_equal_eager_steps(dtype, overlap):
+    """The per-step offload pipeline (fetch -> update -> write-back through the
+    chunk ring, copy streams forked into the capture) captured once and
+    replayed == eager steps; eager steps after the replays stay identical."""
+    numel = [4096 * 9 + 8, 65_536, 4096 * 3]
+    ids = [0, 1]
+    eager, graph, pe, pg, grads = _pair(numel, dtype, offload=True, overlap=overlap, chunk_elems=8192,
+                                        ring_slots=2)
+    k = 4
+    for _ in range(k):
+        eager.step_layers(ids, [pe[l] for l in ids], [grads[l] for l in ids], 1e-3)
+    graph.sync()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graph.step_layers(ids, [pg[l] for l in ids], [grads[l] for l in ids], 1e-3,
+                          stream=torch.cuda.current_stream())
+    for _ in range(k):
+        g.replay()
+    _same(eager, graph, pe, pg, ids)
+    for c, p in ((eager, pe), (graph, pg)):                # eager after replays
+        c.step_layers([2, 0], [p[2], p[0]], [grads[2], grads[0]], 1e-3)
+    _same(eager, graph, pe, pg, [0, 1, 2])
