@@ -206,3 +206,21 @@ def test_captured_offloaded_step_replays_equal_eager_steps(dtype, overlap):
     for c, p in ((eager, pe), (graph, pg)):                # eager after replays
         c.step_layers([2, 0], [p[2], p[0]], [grads[2], grads[0]], 1e-3)
     _same(eager, graph, pe, pg, [0, 1, 2])
+
+
+def test_captured_nccl_offloaded_step_replays_equal_eager_steps():
+    """NCCL data parallelism (1-rank communicator) with per-step offload,
+    captured and replayed == eager."""
+    numel = [4096 * 6, 8192 + 64]
+    ids = [1, 0]
+    eager, graph, pe, pg, grads = _pair(numel, G.DTYPE_FP32, force_nccl=True, offload=True, chunk_elems=8192)
+    for _ in range(3):
+        eager.step_layers(ids, [pe[l] for l in ids], [grads[l] for l in ids], 1e-3)
+    graph.sync()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graph.step_layers(ids, [pg[l] for l in ids], [grads[l] for l in ids], 1e-3,
+                          stream=torch.cuda.current_stream())
+    for _ in range(3):
+        g.replay()
+    _same(eager, graph, pe, pg, ids)
