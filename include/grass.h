@@ -267,9 +267,11 @@ grass_status grass_step_layers(grass_ctx* ctx, const int32_t* layer_ids, int32_t
  *
  * CUDA graphs: grass_step_layers / grass_mgn_accumulate may be captured
  * (stream capture, e.g. torch.cuda.graph) with device gradients and tracing
- * off, for HBM-resident states or the per-step offload pipeline
- * (GRASS_RESIDENCY_STEP; call grass_sync before capturing it) — not period
- * residency — single GPU, NCCL, or P2P with p2p_sync = 1: the per-layer step counts t_l, this step's
+ * off, for HBM-resident states, the per-step offload pipeline
+ * (GRASS_RESIDENCY_STEP) or period residency with every listed layer already
+ * cached (call grass_sync before capturing an offloaded step; not
+ * GRASS_RESIDENCY_STEP_PREFETCH) — single GPU, NCCL, or P2P with p2p_sync = 1:
+ * the per-layer step counts t_l, this step's
  * bias corrections, the bf16 master-initialisation flags, the MGN window and
  * the P2P barrier generations all live on the device, so every replay
  * performs one full step.  Synchronising calls after replays wait for the

@@ -24,10 +24,12 @@ grass_status capture_check(grass_ctx* c, cudaStream_t st, bool any_host, bool* c
   CUDA_TRY(c, cudaStreamIsCapturing(st, &cap));
   *capturing = cap == cudaStreamCaptureStatusActive;
   const bool step_offload = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_STEP;
-  if (*capturing && ((c->cfg.offload && !step_offload) || (c->p2p && !c->cfg.p2p_sync) || any_host || c->tracing))
-    return c->fail(GRASS_E_INVALID, "CUDA-graph capture needs device gradients, tracing off, HBM-resident "
-                                    "or per-step offloaded states (not period residency), P2P only with p2p_sync");
-  if (*capturing && step_offload && !c->ev_pending.empty())
+  const bool period = c->cfg.offload && c->cfg.residency == GRASS_RESIDENCY_PERIOD;
+  if (*capturing && ((c->cfg.offload && !step_offload && !period) || (c->p2p && !c->cfg.p2p_sync) || any_host ||
+                     c->tracing))
+    return c->fail(GRASS_E_INVALID, "CUDA-graph capture needs device gradients, tracing off, and HBM-resident, "
+                                    "per-step offloaded or period-resident (cached) states; P2P only with p2p_sync");
+  if (*capturing && c->cfg.offload && !c->ev_pending.empty())
     return c->fail(GRASS_E_STATE, "capturing an offloaded step: call grass_sync first (earlier copies "
                                   "must be complete)");
   if (*capturing) c->captured = true;
@@ -40,11 +42,13 @@ grass_status capture_check(grass_ctx* c, cudaStream_t st, bool any_host, bool* c
 // flags start clean and the copy streams are forked into the capture; eager
 // calls after captured ones wait for the device once and start clean too.
 grass_status offload_capture_fence(grass_ctx* c, cudaStream_t st, bool capturing) {
-  if (!c->cfg.offload || c->cfg.residency != GRASS_RESIDENCY_STEP) return GRASS_OK;
+  if (!c->cfg.offload) return GRASS_OK;
   if (!capturing && !c->captured_offload) return GRASS_OK;
   if (!capturing) CUDA_TRY(c, cudaDeviceSynchronize());
-  std::fill(c->layer_done_valid.begin(), c->layer_done_valid.end(), 0);
-  std::fill(c->slot_used.begin(), c->slot_used.end(), 0);
+  if (c->cfg.residency == GRASS_RESIDENCY_STEP) {  // ring hazards: all earlier copies are complete
+    std::fill(c->layer_done_valid.begin(), c->layer_done_valid.end(), 0);
+    std::fill(c->slot_used.begin(), c->slot_used.end(), 0);
+  }
   c->captured_offload = capturing;
   if (capturing && c->cfg.overlap) {
     cudaEvent_t e = take_event(c);
@@ -155,6 +159,18 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   if (period && ncached > c->cache_slots)
     return c->fail(GRASS_E_INVALID, "period residency: more layers in one call than cache slots "
                                     "(raise cache_layers)");
+  if (capturing && period) {
+    // a captured period-resident step is replayed as is: every sampled layer
+    // must already be cached (prefetched / trained this period, then
+    // grass_sync), so the graph holds updates in HBM slots and no swap
+    std::vector<int> so, vo;
+    cache_plan(c, ids, order, &so, &vo);
+    for (int j = 0; j < nact; ++j)
+      if (!always_active(c, ids[order[j]]) && c->slot_layer[so[j]] != ids[order[j]])
+        return c->fail(GRASS_E_STATE, "capturing a period-resident step: layer " + std::to_string(ids[order[j]]) +
+                                          " is not cached (prefetch it and grass_sync first)");
+    std::fill(c->slot_ready_pending.begin(), c->slot_ready_pending.end(), 0);  // fills done (synced)
+  }
   // (all arguments validated: from here on work is enqueued)
   if ((s = offload_capture_fence(c, st, capturing)) != GRASS_OK) return s;
   struct CoefReset {  // the clip multiplier only applies inside this call

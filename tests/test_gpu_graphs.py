@@ -99,7 +99,7 @@ def test_capture_rejected_where_unsupported():
     numel = [8192, 8192]
     p = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
     g = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
-    off = G.Grass(numel, gamma=2, offload=True, residency=G.RESIDENCY_PERIOD)   # host-side cache plan
+    off = G.Grass(numel, gamma=2, offload=True, residency=G.RESIDENCY_STEP_PREFETCH)  # fetches every step
     graph = torch.cuda.CUDAGraph()
     with pytest.raises(G.GrassError, match="capture"), pytest.warns(UserWarning):
         with torch.cuda.graph(graph):
@@ -223,4 +223,31 @@ def test_captured_nccl_offloaded_step_replays_equal_eager_steps():
                           stream=torch.cuda.current_stream())
     for _ in range(3):
         g.replay()
+    _same(eager, graph, pe, pg, ids)
+
+
+def test_captured_period_resident_step_replays_equal_eager_steps():
+    """Period residency: once the period's layers are cached (prefetched, then
+    grass_sync), a captured step is updates in HBM slots only; replays ==
+    eager; a step with an uncached layer cannot be captured."""
+    numel = [8192 * 3, 8192, 4096 * 5 + 8]
+    ids = [2, 0]
+    eager, graph, pe, pg, grads = _pair(numel, G.DTYPE_FP32, offload=True, residency=G.RESIDENCY_PERIOD)
+    for c in (eager, graph):
+        c.prefetch_layers(ids)
+    graph.sync()
+    with pytest.raises(G.GrassError, match="not cached"), pytest.warns(UserWarning):
+        with torch.cuda.graph(torch.cuda.CUDAGraph()):
+            graph.step_layers([1], [pg[1]], [grads[1]], 1e-3, stream=torch.cuda.current_stream())
+    for _ in range(4):
+        eager.step_layers(ids, [pe[l] for l in ids], [grads[l] for l in ids], 1e-3)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graph.step_layers(ids, [pg[l] for l in ids], [grads[l] for l in ids], 1e-3,
+                          stream=torch.cuda.current_stream())
+    for _ in range(4):
+        g.replay()
+    _same(eager, graph, pe, pg, ids)
+    eager.flush_states()
+    graph.flush_states()
     _same(eager, graph, pe, pg, ids)
