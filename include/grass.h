@@ -15,7 +15,7 @@
  *                         (Fig. 4),
  *                         fused with the Eq. 2 norm of the same gradients.
  *
- * Readings where the paper is silent are DESIGN.md R1-R14 (referenced below).
+ * Readings where the paper is silent are DESIGN.md R1-R20 (referenced below).
  *
  * Conventions (all calls):
  *   - Every entry point returns a grass_status; no C++ exception ever crosses
@@ -24,8 +24,9 @@
  *     grass_last_error() describes the failure.
  *   - A context is not thread-safe: calls on one context must not overlap.
  *     Distinct contexts are independent.
- *   - A "layer" is ONE flat, contiguous, 16-byte aligned fp32 buffer of N_p(l)
- *     elements in device memory (the decoder block's tensors viewed back to back).
+ *   - A "layer" is ONE flat, contiguous, 16-byte aligned fp32 (or bf16, see
+ *     param_dtype) buffer of N_p(l) elements in device memory (the decoder
+ *     block's tensors viewed back to back).
  *   - Every layer buffer is checked before anything is enqueued: 16-byte
  *     alignment, device memory of the context's GPU, and that its allocation
  *     (cuMemGetAddressRange; a caching allocator's segment) holds N_p elements.
