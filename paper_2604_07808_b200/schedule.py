@@ -13,6 +13,12 @@
 Always-active groups (Grass(n_always=k): embedding / head, DESIGN R19) are not
 probed or sampled; they join every adaptive step's update.
 
+graphs=True: the update of an adaptive step is a CUDA graph captured once
+per trainable set (i.e. once per sampling period) and replayed on the other
+steps of the period, with eta read from a device scalar (grass_set_lr_device)
+— for HBM-resident states, the per-step offload pipeline and period
+residency (the period's layers are prefetched, so they are cached).
+
 trace_path: optional JSON-lines log of the sampling state (SPEC.md:313's
 prob-trace): one record per commit {"step", "event": "commit", "m", "p"} and
 per resample {"step", "event": "resample", "period", "sampled"}.
@@ -35,10 +41,19 @@ from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_PROBE, DECIDE_RESAMPLE, Gra
 
 
 class GrassSchedule:
-    def __init__(self, grass: Grass, prefetch: bool | None = None, trace_path: str | None = None):
+    def __init__(self, grass: Grass, prefetch: bool | None = None, trace_path: str | None = None,
+                 graphs: bool = False):
         self.g = grass
         self.trace_path = trace_path
         cfg = grass.cfg
+        self.graphs = graphs
+        self._graph, self._gkey, self._lr = None, None, None
+        if graphs:
+            if cfg.offload and cfg.residency == 2:
+                raise ValueError("graphs: GRASS_RESIDENCY_STEP_PREFETCH fetches every step (not capturable)")
+            import torch
+            self._lr = torch.zeros((), dtype=torch.float32, device=torch.device("cuda", cfg.device))
+            grass.set_lr_device(self._lr)
         self.T_p, self.T_s, self.T_u = cfg.T_p, cfg.T_s, cfg.T_u
         self.n_layers = grass.n_layers
         self.always = list(getattr(grass, "always_ids", []))
@@ -89,7 +104,22 @@ class GrassSchedule:
         else:
             if len(params) != len(layers):
                 raise ValueError("one parameter buffer per trainable layer")
-            self.g.step_layers(layers, params, grads, lr, stream=stream)
+            if not self.graphs:
+                self.g.step_layers(layers, params, grads, lr, stream=stream)
+                return
+            import torch
+            key = (tuple(layers), tuple(p.data_ptr() for p in params), tuple(g.data_ptr() for g in grads))
+            if key != self._gkey:                 # new trainable set (or buffers): capture once
+                torch.cuda.synchronize()
+                self.g.sync()                     # capture preconditions (copies / fills complete)
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    self.g.step_layers(layers, params, grads, 0.0, stream=torch.cuda.current_stream())
+                self._graph, self._gkey = graph, key
+            s = torch.cuda.current_stream() if stream is None else stream
+            with torch.cuda.stream(s):
+                self._lr.fill_(lr)
+                self._graph.replay()
 
     def _log(self, rec: dict):
         with open(self.trace_path, "a") as f:

@@ -251,3 +251,30 @@ def test_captured_period_resident_step_replays_equal_eager_steps():
     eager.flush_states()
     graph.flush_states()
     _same(eager, graph, pe, pg, ids)
+
+
+@pytest.mark.parametrize("mode", ["resident", "offload", "period"])
+def test_schedule_graph_mode_equals_eager_schedule(mode):
+    """GrassSchedule(graphs=True): one captured update per sampling period,
+    replayed on its other steps with eta from a device scalar (a changing
+    schedule) — identical to the eager schedule."""
+    numel = [8192] * 4 + [4096 * 3]
+    kw = {"resident": {}, "offload": dict(offload=True, chunk_elems=8192),
+          "period": dict(offload=True, residency=G.RESIDENCY_PERIOD)}[mode]
+    T_p, T_s = 2, 3
+    runs = []
+    for graphs in (False, True):
+        gr = G.Grass(numel, gamma=2, T_p=T_p, T_s=T_s, seed=9, n_always=1, weight_decay=0.01, **kw)
+        sched = G.GrassSchedule(gr, graphs=graphs)
+        P = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+        Gb = [torch.zeros(n, device=DEV) for n in numel]          # persistent gradient buffers
+        for step in range(T_p + 3 * T_s):
+            layers = sched.begin_step(step)
+            for l in layers:
+                Gb[l].copy_(layer_grad(numel[l], l, 10.0 ** (-3 - l % 2), step=step, device=DEV))
+            sched.end_step(step, [P[l] for l in layers], [Gb[l] for l in layers], 1e-3 * (1 + 0.1 * step))
+        gr.sync()
+        runs.append((gr, P))
+    (ea, pa), (eb, pb) = runs
+    _same(ea, eb, pa, pb, list(range(5)))
+    assert ea.get_mgn()["m"] == eb.get_mgn()["m"]
