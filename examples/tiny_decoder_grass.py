@@ -60,12 +60,13 @@ class TinyDecoder(nn.Module):
         return self.head(x)
 
 
-def train(steps=60, T_p=5, T_s=5, gamma=2, seed=0, device="cuda", log=True, dtype=torch.float32):
+def train(steps=60, T_p=5, T_s=5, gamma=2, seed=0, device="cuda", log=True, dtype=torch.float32,
+          graphs=False):
     torch.manual_seed(seed)
     model = TinyDecoder().to(device=device, dtype=dtype)   # bf16: fp32 master + m + v in libgrass
     gb = G.GrassBlocks(model.blocks, always=[[model.emb.weight, model.pos, *model.head.parameters()]],
                        gamma=gamma, T_p=T_p, T_s=T_s, seed=seed, offload=True,
-                       residency=G.RESIDENCY_PERIOD)
+                       residency=G.RESIDENCY_PERIOD, graphs=graphs)
     # a learnable synthetic task: predict the next token of a fixed random walk
     data = torch.cumsum(torch.randint(-2, 3, (64, 65), generator=torch.Generator().manual_seed(seed)), 1) % 256
     data = data.to(device)

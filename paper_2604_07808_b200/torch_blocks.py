@@ -57,7 +57,8 @@ class GrassBlocks:
     parameter groups, bound to one `Grass` context (keyword arguments are
     `Grass`'s, e.g. gamma, T_p, T_s, offload, residency, param_dtype)."""
 
-    def __init__(self, blocks: Sequence[torch.nn.Module], always: Sequence[Iterable] = (), **grass_kw):
+    def __init__(self, blocks: Sequence[torch.nn.Module], always: Sequence[Iterable] = (), graphs: bool = False,
+                 **grass_kw):
         self.blocks = list(blocks)
         groups = [list(b.parameters()) for b in self.blocks] + [list(a) for a in always]
         self.flats = [flatten_params(g) for g in groups]
@@ -67,7 +68,7 @@ class GrassBlocks:
         grass_kw.setdefault("param_dtype", DTYPE_BF16 if dt == torch.bfloat16 else DTYPE_FP32)
         grass_kw.setdefault("device", self.flats[0][0].device.index or 0)
         self.grass = Grass([f.numel() for f, _ in self.flats], n_always=len(always), **grass_kw)
-        self.schedule = GrassSchedule(self.grass)
+        self.schedule = GrassSchedule(self.grass, graphs=graphs)   # graphs: one captured update per period
         self.layers: list[int] = []
 
     def begin_step(self, step: int) -> list[int]:

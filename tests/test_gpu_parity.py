@@ -1215,10 +1215,14 @@ def test_example_training_loop_loss_decreases():
     spec = importlib.util.spec_from_file_location("tiny_decoder_grass", path)
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
-    for dtype in (torch.float32, torch.bfloat16):   # GrassBlocks picks the library dtype
-        losses = mod.train(steps=60, log=False, dtype=dtype)
+    runs = {}
+    for dtype, graphs in ((torch.float32, False), (torch.bfloat16, False), (torch.float32, True)):
+        losses = mod.train(steps=60, log=False, dtype=dtype, graphs=graphs)   # GrassBlocks picks the dtype
         assert all(np.isfinite(losses))
-        assert np.mean(losses[-10:]) < 0.7 * np.mean(losses[:5]), dtype
+        assert np.mean(losses[-10:]) < 0.7 * np.mean(losses[:5]), (dtype, graphs)
+        runs[(dtype, graphs)] = losses
+    # the captured per-period update is the same update: identical training curve
+    assert runs[(torch.float32, True)] == runs[(torch.float32, False)]
 
 
 @pytest.mark.parametrize("alpha,tau,normalize", [(0.0, 1.0, True), (1.0, 0.3, True), (0.5, 1e-4, False),
