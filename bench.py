@@ -359,6 +359,28 @@ def run_grass(args, rank, world, local):
                 "d2h_bytes_per_step": d2h, "ms_per_step": et / ksteps * 1e3, "steps": ksteps}
 
     e2e = guarded("e2e", leg_e2e)
+
+    # ---- the same resident step on the paper's schedule (T_s = T_u = 25:
+    # commit + resample once per 25 steps) — what a training run
+    # sees per step, next to the every-step-resample `value`
+    def leg_paper_schedule():
+        nonlocal ids
+        T = 25
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record(s)
+        for k in range(2 * T):
+            if k and k % T == 0:                  # period boundary (the window holds T steps)
+                ctx.update_probs()
+                ids = ctx.sample_layers(10_000 + k // T)
+            ctx.step_layers(ids, [params[l] for l in ids], [grads[l] for l in ids], args.lr, stream=s)
+        e1.record(s)
+        torch.cuda.synchronize()
+        t = max_over_ranks(e0.elapsed_time(e1) / 1e3, world, dev) / (2 * T)
+        return {"schedule": f"T_s=T_u={T} (2 periods)", "step_ms": t * 1e3, "params_per_s": active / t}
+
+    paper_schedule = guarded("main", leg_paper_schedule)
     ctx.close()                                 # frees its 51.8 GB of HBM state
     torch.cuda.empty_cache()
 
@@ -787,6 +809,7 @@ def run_grass(args, rank, world, local):
                         if world > 1 else None),
             "clocks": clk.summary(), "probe": out.get("probe"), "offload": offload,
             "offload_period": offload_period, "bf16": bf16, "train_step": train, "p2p": p2p,
+            "paper_schedule": paper_schedule,
             "paper_context": {
                 "hardware": "2 x H100 80GB, precision not stated (PAPER.md:410)",
                 "overlap_speedup": {"paper": 1.08, "what": "training throughput, overlapped vs "
