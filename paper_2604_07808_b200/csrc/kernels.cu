@@ -25,7 +25,7 @@
 // GRASS_K2_SEP_OUT, GRASS_K2_NOMATH, GRASS_K1_NOMATH, GRASS_UPD_STAGES, GRASS_NORM_TPS,
 // GRASS_NORM_TPS_BF16, GRASS_NORM_STAGES, GRASS_P2P_NORM_TPS,
 // GRASS_UPD_GRID_SUB, GRASS_NORM_GRID_SUB, GRASS_L2_PREFETCH_{NORM,UPD},
-// GRASS_UNIT_BLOCK, GRASS_BF16_MAP8; GRASS_MUTANT=k plants mistake k
+// GRASS_UNIT_BLOCK, GRASS_BF16_MAP8, GRASS_BF16_FP64_SQ, GRASS_BF16_SQ_PAIR; GRASS_MUTANT=k plants mistake k
 // (tools/kernel_mutation.py).
 //
 // The tile partial (grass_internal.h) is a FIXED function of the tile's data:

@@ -84,6 +84,42 @@ template <bool BF16>
 __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
   return BF16 ? bf2f(sg.g16[idx]) : sg.g[idx];
 }
+// Eq. 2 squared-norm accumulation of a thread's 4 gradient values into
+// acc[0..3] (fp64).  fp32 gradients: every square exact in fp64.  bf16
+// gradients: a bf16 value's square (<= 16 significant bits) is exact in fp32,
+// so the 4 squares are summed in fp32 (three roundings, <= 3 * 2^-24 relative;
+// one more when a DP scale gs != 1 is applied) and widened once — a quarter of
+// the fp32->fp64 conversions and fp64 adds of per-element fp64 squares, which
+// held the 2 B/param probe ~20 % above its no-math time (profiles/
+// r01_variants_bf16_*).  All terms are >= 0, so the relative error of the sum
+// stays <= 4 * 2^-24 = 2.4e-7, inside the 1e-6 bar; integer-valued
+// gradients of magnitude < 2048 stay exact (sums < 2^24).  A/B knobs:
+// GRASS_BF16_FP64_SQ=1 per-element fp64 squares, GRASS_BF16_SQ_PAIR=1 pairs.
+#ifndef GRASS_BF16_FP64_SQ
+#define GRASS_BF16_FP64_SQ 0
+#endif
+#ifndef GRASS_BF16_SQ_PAIR
+#define GRASS_BF16_SQ_PAIR 0
+#endif
+template <bool BF16>
+__device__ __forceinline__ void sq_acc4(double (&acc)[kVec], float4 g) {
+  if (BF16 && !GRASS_BF16_FP64_SQ && !GRASS_BF16_SQ_PAIR) {
+    acc[0] += (double)__fmaf_rn(g.w, g.w, __fmaf_rn(g.z, g.z, __fmaf_rn(g.y, g.y, __fmul_rn(g.x, g.x))));
+  } else if (BF16 && !GRASS_BF16_FP64_SQ) {
+    acc[0] += (double)__fmaf_rn(g.y, g.y, __fmul_rn(g.x, g.x));
+    acc[1] += (double)__fmaf_rn(g.w, g.w, __fmul_rn(g.z, g.z));
+  } else {
+    acc[0] = fma((double)g.x, (double)g.x, acc[0]);
+    acc[1] = fma((double)g.y, (double)g.y, acc[1]);
+    acc[2] = fma((double)g.z, (double)g.z, acc[2]);
+    acc[3] = fma((double)g.w, (double)g.w, acc[3]);
+  }
+}
+template <bool BF16>
+__device__ __forceinline__ void sq_acc1(double& a, float g) {  // ragged-tail element
+  if (BF16 && !GRASS_BF16_FP64_SQ) a += (double)__fmul_rn(g, g);
+  else a = fma((double)g, (double)g, a);
+}
 
 // P2P (Seg::gpeer): the gradient of a unit is the sum of the npeer ranks'
 // slices in ascending rank order (fp32).  The producer bulk-copies each rank's
@@ -363,10 +399,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
 #ifdef GRASS_K1_NOMATH  // A/B only: the same data movement with trivial arithmetic (speed of light)
           acc[0] += fabsf(cur[q].x) + fabsf(cur[q].y) + fabsf(cur[q].z) + fabsf(cur[q].w);
 #else
-          acc[0] = fma((double)cur[q].x, (double)cur[q].x, acc[0]);
-          acc[1] = fma((double)cur[q].y, (double)cur[q].y, acc[1]);
-          acc[2] = fma((double)cur[q].z, (double)cur[q].z, acc[2]);
-          acc[3] = fma((double)cur[q].w, (double)cur[q].w, acc[3]);
+          sq_acc4<BF16>(acc, cur[q]);
 #endif
         }
         const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
@@ -382,10 +415,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
             const int e = tile_elem<BF16>(k, q, tid);  // relative to e0
             if (e < nv) {
               const float4 g4 = scale4(P2P ? gacc[P2P ? k : 0][q] : stage_g4<BF16>(stg + L::off_g, e), gs);
-              acc[0] = fma((double)g4.x, (double)g4.x, acc[0]);
-              acc[1] = fma((double)g4.y, (double)g4.y, acc[1]);
-              acc[2] = fma((double)g4.z, (double)g4.z, acc[2]);
-              acc[3] = fma((double)g4.w, (double)g4.w, acc[3]);
+              sq_acc4<BF16>(acc, g4);
               if (UPDATE) {
                 float4 t4 = init ? unpack_bf16x4(*reinterpret_cast<const uint2*>(stg + L::off_tb + 2 * e))
                                  : *reinterpret_cast<const float4*>(stg + L::off_t + 4 * e);
@@ -424,7 +454,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
                 if (e + j < ne - (kMutant == 4 ? 1 : 0)) {  // M4: last tail element skipped
                   const int64_t idx = e0 + e + j;
                   const float g = (P2P ? peer_g1<BF16>(sg.gpeer, b.npeer, pe0 + e + j) : seg_g<BF16>(sg, idx)) * gs;
-                  acc[j] = fma((double)g, (double)g, acc[j]);
+                  sq_acc1<BF16>(acc[j], g);
                   if (UPDATE) {
                     float th = init ? bf2f(sg.theta16[idx]) : sg.theta[idx];
                     float m = sg.m[idx], v = sg.v[idx];

@@ -89,6 +89,25 @@ def test_norms_integer_grads_exact():
         assert st["S"][l] == math.sqrt(exact / numel[l])     # Eq. 2 inner term, fp64 IEEE sqrt
 
 
+def test_norms_integer_grads_exact_bf16():
+    """bf16 gradients: squares summed four at a time in fp32 (stream_kernel.cuh
+    sq_acc4) must stay exact for integers |g| <= 255 (quad sums < 2^24), in the
+    probing kernel (K1), the fused update (K2) and the ragged tails."""
+    numel = [65_536, 65_536 + 5, 2_000_000 + 3]
+    gr = G.Grass(numel, gamma=3, param_dtype=G.DTYPE_BF16)
+    grads = [integer_grad(n, l, lo=-255, hi=255, device=DEV).to(torch.bfloat16) for l, n in enumerate(numel)]
+    exact = [int((_np(g.float()).astype(np.int64) ** 2).sum()) for g in grads]
+    gr.mgn_accumulate([2, 0, 1], [grads[2], grads[0], grads[1]])
+    st = gr.get_mgn()
+    for l in range(3):
+        assert st["last_ss"][l] == float(exact[l])
+    params = [torch.zeros(n, dtype=torch.bfloat16, device=DEV) for n in numel]
+    gr.step_layers([1, 2, 0], [params[1], params[2], params[0]], [grads[1], grads[2], grads[0]], 1e-3)
+    st = gr.get_mgn()
+    for l in range(3):
+        assert st["last_ss"][l] == float(exact[l])
+
+
 def test_norms_special_cases():
     gr = G.Grass([4096, 8, 2], gamma=1)
     z = torch.zeros(4096, device=DEV)

@@ -12,9 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
     "base": [],
-    "k1_nomath": ["GRASS_K1_NOMATH"],
+    "bf16_sq_quad": ["GRASS_BF16_SQ_QUAD=1"],
     "base_again": [],
-    "k1_nomath_again": ["GRASS_K1_NOMATH"],
+    "bf16_sq_quad_again": ["GRASS_BF16_SQ_QUAD=1"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
