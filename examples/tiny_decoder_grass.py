@@ -61,24 +61,34 @@ class TinyDecoder(nn.Module):
 
 
 def train(steps=60, T_p=5, T_s=5, gamma=2, seed=0, device="cuda", log=True, dtype=torch.float32,
-          graphs=False):
+          graphs=False, step_graphs=False):
+    """graphs: the library update of each period is one captured CUDA graph;
+    step_graphs: the whole step (forward, backward, update) is, through
+    GrassBlocks.train_step."""
     torch.manual_seed(seed)
     model = TinyDecoder().to(device=device, dtype=dtype)   # bf16: fp32 master + m + v in libgrass
     gb = G.GrassBlocks(model.blocks, always=[[model.emb.weight, model.pos, *model.head.parameters()]],
                        gamma=gamma, T_p=T_p, T_s=T_s, seed=seed, offload=True,
-                       residency=G.RESIDENCY_PERIOD, graphs=graphs)
+                       residency=G.RESIDENCY_PERIOD, graphs=graphs, step_graphs=step_graphs)
     # a learnable synthetic task: predict the next token of a fixed random walk
     data = torch.cumsum(torch.randint(-2, 3, (64, 65), generator=torch.Generator().manual_seed(seed)), 1) % 256
     data = data.to(device)
     losses = []
-    for step in range(steps):
-        ids = gb.begin_step(step)      # freezes the blocks that are not trained this step
+    def loss_fn():                     # reads the static batch `data`
         logits = model(data[:, :-1])
-        loss = nn.functional.cross_entropy(logits.float().reshape(-1, 256), data[:, 1:].reshape(-1))
-        loss.backward()
-        # probing steps only record norms: no parameter update
-        gb.end_step(step, lr=1e-3)
-        gb.zero_grad()
+        return nn.functional.cross_entropy(logits.float().reshape(-1, 256), data[:, 1:].reshape(-1))
+
+    for step in range(steps):
+        if step_graphs:
+            loss = gb.train_step(step, loss_fn, lr=1e-3)
+            ids = gb.layers
+        else:
+            ids = gb.begin_step(step)      # freezes the blocks that are not trained this step
+            loss = loss_fn()
+            loss.backward()
+            # probing steps only record norms: no parameter update (PAPER.md:113)
+            gb.end_step(step, lr=1e-3)
+            gb.zero_grad()
         losses.append(float(loss.detach()))
         if log and step % 10 == 0:
             print(f"step {step:3d} loss {losses[-1]:.4f} trainable {ids if step >= T_p else 'none (probe)'}")

@@ -1235,13 +1235,18 @@ def test_example_training_loop_loss_decreases():
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     runs = {}
-    for dtype, graphs in ((torch.float32, False), (torch.bfloat16, False), (torch.float32, True)):
-        losses = mod.train(steps=60, log=False, dtype=dtype, graphs=graphs)   # GrassBlocks picks the dtype
+    for dtype, graphs in ((torch.float32, False), (torch.bfloat16, False), (torch.float32, True),
+                          (torch.float32, "step"), (torch.bfloat16, "step")):
+        losses = mod.train(steps=60, log=False, dtype=dtype, graphs=graphs is True,
+                           step_graphs=graphs == "step")   # GrassBlocks picks the dtype
         assert all(np.isfinite(losses))
         assert np.mean(losses[-10:]) < 0.7 * np.mean(losses[:5]), (dtype, graphs)
         runs[(dtype, graphs)] = losses
-    # the captured per-period update is the same update: identical training curve
+    # the captured per-period update / whole step is the same computation: the
+    # training curve of the captured runs is the eager one
     assert runs[(torch.float32, True)] == runs[(torch.float32, False)]
+    assert runs[(torch.float32, "step")] == runs[(torch.float32, False)]
+    assert runs[(torch.bfloat16, "step")] == runs[(torch.bfloat16, False)]
 
 
 @pytest.mark.parametrize("alpha,tau,normalize", [(0.0, 1.0, True), (1.0, 0.3, True), (0.5, 1e-4, False),
