@@ -686,6 +686,7 @@ def run_grass(args, rank, world, local):
             t0_.record(s)
             for k in range(nsteps):
                 tstep(T_s + k)                        # two period boundaries in the window
+            tc.sync()                                 # + background write-backs (STEP_PREFETCH) of the last step
             t1_.record(s)
             torch.cuda.synchronize()
             return max_over_ranks(t0_.elapsed_time(t1_) / 1e3, world, dev) / nsteps * 1e3

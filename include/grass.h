@@ -172,7 +172,8 @@ typedef enum {
   /* the paper's per-step round trip with whole-layer prefetch:
      grass_prefetch_layers fetches the step's trainable layers ahead (e.g.
      during the forward), grass_step_layers updates them and writes their m/v
-     back to host right after the update; device slots as for PERIOD */
+     back to host right after the update (in the background: the caller's
+     stream does not wait for the write-back); device slots as for PERIOD */
   GRASS_RESIDENCY_STEP_PREFETCH = 2
 } grass_residency;
 
@@ -256,7 +257,10 @@ grass_status grass_sample_layers(grass_ctx* ctx, const double* probs, uint64_t p
  *           is rejected
  *   lr:     learning rate eta for this step (> 0 or == 0)
  * Stream-ordered on `stream`: when `stream` reaches this point the update, the
- * write-back of m/v to host and the MGN accumulation have all completed. */
+ * write-back of m/v to host and the MGN accumulation have all completed —
+ * except under GRASS_RESIDENCY_STEP_PREFETCH, whose write-backs complete in
+ * the background on the context's copy stream (ordered before the layer's next
+ * fetch and drained by grass_sync and every call that reads host state). */
 grass_status grass_step_layers(grass_ctx* ctx, const int32_t* layer_ids, int32_t n,
                                float* const* params, const float* const* grads, float lr,
                                void* stream);

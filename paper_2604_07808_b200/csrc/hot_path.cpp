@@ -310,8 +310,14 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   }
   if (sharded && (s = comm_end(c, st)) != GRASS_OK) return s;
   if (sharded && !clip && (s = cross_rank_finish(c, ids, order, st)) != GRASS_OK) return s;
-  if (c->cfg.offload && c->cfg.overlap) {
-    // join: the caller stream reaches "done" only after every write-back
+  if (c->cfg.offload && c->cfg.overlap && !c->write_through) {
+    // join: the caller stream reaches "done" only after every write-back.
+    // Write-through (GRASS_RESIDENCY_STEP_PREFETCH) does not join: its
+    // write-backs finish on the d2h stream in the background, ordered before
+    // the next fetch of the layer (ev_layer_done) and the next fill of the slot
+    // (ev_slot_wb) and drained by every call that reads host state, so the D2H
+    // of the last-updated layers overlaps the caller's next forward instead of
+    // extending this step.
     cudaEvent_t e = take_event(c);
     if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
     CUDA_TRY(c, cudaEventRecord(e, c->d2h));
