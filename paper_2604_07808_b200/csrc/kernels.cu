@@ -25,7 +25,8 @@
 // GRASS_K2_SEP_OUT, GRASS_K2_NOMATH, GRASS_K1_NOMATH, GRASS_UPD_STAGES, GRASS_NORM_TPS,
 // GRASS_NORM_TPS_BF16, GRASS_NORM_STAGES, GRASS_P2P_NORM_TPS,
 // GRASS_UPD_GRID_SUB, GRASS_NORM_GRID_SUB, GRASS_L2_PREFETCH_{NORM,UPD},
-// GRASS_UNIT_BLOCK, GRASS_BF16_MAP8, GRASS_BF16_FP64_SQ, GRASS_BF16_SQ_PAIR; GRASS_MUTANT=k plants mistake k
+// GRASS_UNIT_BLOCK, GRASS_BF16_MAP8, GRASS_BF16_FP64_SQ, GRASS_BF16_SQ_PAIR,
+// GRASS_K1_TILE_REDUCE; GRASS_MUTANT=k plants mistake k
 // (tools/kernel_mutation.py).
 //
 // The tile partial (grass_internal.h) is a FIXED function of the tile's data:
@@ -61,6 +62,32 @@ __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
   return x;  // lane 0 holds the fixed-tree sum
+}
+
+// warp_sum of N <= 16 per-lane values at once (one per tile of a unit): a
+// transposed butterfly.  At offset o every lane keeps half of its values and
+// trades the other half with lane ^ o, so each value is summed by the same
+// pairs of lane groups as warp_sum (level o adds the groups of lanes i and
+// i + o; IEEE addition is commutative), i.e. every result is bit-identical to
+// warp_sum of that value — for 16 + 15 exchanged values instead of 5N.
+// Lane i returns the sum of value (i >> 1) & 15 (valid for (i >> 1) < N).
+template <int N>
+__device__ __forceinline__ double warp_sum_multi(const double (&in)[N], int lane) {
+  static_assert(N >= 1 && N <= 16, "one value per tile of a unit");
+  double v[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) v[t] = t < N ? in[t] : 0.0;
+#pragma unroll
+  for (int c = 16, o = 16; c > 1; c >>= 1, o >>= 1) {
+    const bool up = (lane & o) != 0;  // this lane keeps the upper half
+#pragma unroll
+    for (int j = 0; j < c / 2; ++j) {
+      const double send = up ? v[j] : v[j + c / 2];
+      const double keep = up ? v[j + c / 2] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
 struct AdamScalars {

@@ -95,6 +95,9 @@ __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
 // stays <= 4 * 2^-24 = 2.4e-7, inside the 1e-6 bar; integer-valued
 // gradients of magnitude < 2048 stay exact (sums < 2^24).  A/B knobs:
 // GRASS_BF16_FP64_SQ=1 per-element fp64 squares, GRASS_BF16_SQ_PAIR=1 pairs.
+#ifndef GRASS_K1_TILE_REDUCE  // A/B: K1 full units reduce tile by tile (warp_sum per tile)
+#define GRASS_K1_TILE_REDUCE 0
+#endif
 #ifndef GRASS_BF16_FP64_SQ
 #define GRASS_BF16_FP64_SQ 0
 #endif
@@ -383,12 +386,17 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
 #pragma unroll
         for (int q = 0; q < kUnroll; ++q)
           g4[k][q] = stage_g4<BF16>(stg + L::off_g, tile_elem<BF16>(k, q, tid));
+      double tv[TPS];  // this thread's value of each tile
 #pragma unroll
       for (int k = 0; k < TPS; ++k) {
         double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
         float4 cur[kUnroll];
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q) cur[q] = scale4(g4[k % kPre][q], gs);
+        for (int q = 0; q < kUnroll; ++q) cur[q] = g4[k % kPre][q];
+        if (gs != 1.f) {  // DP average (warp-uniform; x * 1 == x, so skipping it is exact)
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) cur[q] = scale4(cur[q], gs);
+        }
         if (k + kPre < TPS) {  // refill the slot just consumed
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q)
@@ -402,8 +410,15 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           sq_acc4<BF16>(acc, cur[q]);
 #endif
         }
-        const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
-        if (lane == 0) red[i & 1][k][warp] = t;
+        tv[k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        if (GRASS_K1_TILE_REDUCE) {
+          const double t = warp_sum(tv[k]);
+          if (lane == 0) red[i & 1][k][warp] = t;
+        }
+      }
+      if (!GRASS_K1_TILE_REDUCE) {  // all tiles' warp sums at once (bit-identical to warp_sum)
+        const double t = warp_sum_multi<TPS>(tv, lane);
+        if ((lane & 1) == 0 && (lane >> 1) < TPS) red[i & 1][lane >> 1][warp] = t;
       }
     } else {
 #pragma unroll

@@ -108,6 +108,30 @@ def test_norms_integer_grads_exact_bf16():
         assert st["last_ss"][l] == float(exact[l])
 
 
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+def test_norms_probe_equals_update_bitwise(dtype):
+    """The fixed tile decomposition: the norm of a gradient is the
+    same bits whether the probing kernel (K1: multi-tile units, all tile sums
+    of a unit reduced at once by warp_sum_multi) or the fused update (K2: one
+    tile per unit, warp_sum) computes it — full units, partial units, ragged
+    tails, and a DP-style scale (world 2 virtual ranks are not needed: the
+    scale is 1 here, the skip of the multiply is exact)."""
+    tdt = torch.bfloat16 if dtype == G.DTYPE_BF16 else torch.float32
+    numel = [4096 * 12 * 5, 4096 * 12 * 3 + 4096 * 7 + 13, 4096 * 6 * 4 + 5, 3]
+    gr = G.Grass(numel, gamma=4, param_dtype=dtype)
+    grads = [layer_grad(n, l, 10.0 ** (-l), device=DEV).to(tdt) for l, n in enumerate(numel)]
+    gr.mgn_accumulate(list(range(4)), grads)
+    k1 = gr.get_mgn()["last_ss"]
+    params = [layer_params(n, l, device=DEV).to(tdt) for l, n in enumerate(numel)]
+    gr.step_layers([3, 1, 0, 2], [params[3], params[1], params[0], params[2]],
+                   [grads[3], grads[1], grads[0], grads[2]], 1e-4)
+    k2 = gr.get_mgn()["last_ss"]
+    assert k1 == k2
+    for l in range(4):
+        g = _np(grads[l].float()).astype(np.float64)
+        assert_ss_close(k1[l], O.sq_norm(g))
+
+
 def test_norms_special_cases():
     gr = G.Grass([4096, 8, 2], gamma=1)
     z = torch.zeros(4096, device=DEV)

@@ -12,11 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
     "base": [],
-    "st3_tps8": ["GRASS_NORM_STAGES=3", "GRASS_NORM_TPS_BF16=8", "GRASS_NORM_TPS=4"],
-    "st4_tps6": ["GRASS_NORM_STAGES=4", "GRASS_NORM_TPS_BF16=6", "GRASS_NORM_TPS=3"],
-    "tps13": ["GRASS_NORM_TPS_BF16=13"],
-    "grid_sub8": ["GRASS_NORM_GRID_SUB=8"],
+    "tile_reduce": ["GRASS_K1_TILE_REDUCE=1"],
     "base_again": [],
+    "tile_reduce_again": ["GRASS_K1_TILE_REDUCE=1"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
