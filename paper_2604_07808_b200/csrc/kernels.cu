@@ -438,7 +438,7 @@ constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 96
 #endif
 constexpr int kNormTPSBf16 = GRASS_NORM_TPS_BF16;  // bf16 probing: tiles per unit (2 B/element)
 #ifndef GRASS_P2P_NORM_TPS
-#define GRASS_P2P_NORM_TPS 3
+#define GRASS_P2P_NORM_TPS 6  // 2 x 96 KiB gradient slots (4.1 vs 5.1 ms for 3, profiles/r01_variants_p2p_norm_tps_multi.json)
 #endif
 constexpr int kP2PNormTPS = GRASS_P2P_NORM_TPS;  // P2P probing: tiles per gradient-ring slot
 

@@ -420,6 +420,19 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         const double t = warp_sum_multi<TPS>(tv, lane);
         if ((lane & 1) == 0 && (lane >> 1) < TPS) red[i & 1][lane >> 1][warp] = t;
       }
+    } else if (!UPDATE && P2P && ne == kUnit && !GRASS_K1_TILE_REDUCE) {
+      // Full unit of the P2P norm stream: the ranks' summed gradient is in
+      // gacc; same element map and accumulation order as the guarded path.
+      double tv[TPS];
+#pragma unroll
+      for (int k = 0; k < TPS; ++k) {
+        double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) sq_acc4<BF16>(acc, gs != 1.f ? scale4(gacc[P2P ? k : 0][q], gs) : gacc[P2P ? k : 0][q]);
+        tv[k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      }
+      const double t = warp_sum_multi<TPS>(tv, lane);
+      if ((lane & 1) == 0 && (lane >> 1) < TPS) red[i & 1][lane >> 1][warp] = t;
     } else {
 #pragma unroll
       for (int k = 0; k < TPS; ++k) {

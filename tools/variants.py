@@ -12,9 +12,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
     "base": [],
-    "tile_reduce": ["GRASS_K1_TILE_REDUCE=1"],
+    "p2pn4": ["GRASS_P2P_NORM_TPS=4"],
+    "p2pn6": ["GRASS_P2P_NORM_TPS=6"],
+    "p2pn2": ["GRASS_P2P_NORM_TPS=2"],
     "base_again": [],
-    "tile_reduce_again": ["GRASS_K1_TILE_REDUCE=1"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
