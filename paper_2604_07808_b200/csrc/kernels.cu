@@ -79,7 +79,7 @@ __device__ __forceinline__ double warp_sum_multi(const double (&in)[N], int lane
   for (int t = 0; t < 16; ++t) v[t] = t < N ? in[t] : 0.0;
 #pragma unroll
   for (int c = 16, o = 16; c > 1; c >>= 1, o >>= 1) {
-    const bool up = (lane & o) != 0;  // this lane keeps the upper half
+    const bool up = kMutant != 12 && (lane & o) != 0;  // this lane keeps the upper half (M12: never)
 #pragma unroll
     for (int j = 0; j < c / 2; ++j) {
       const double send = up ? v[j] : v[j + c / 2];

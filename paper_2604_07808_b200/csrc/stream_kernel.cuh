@@ -107,7 +107,8 @@ __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
 template <bool BF16>
 __device__ __forceinline__ void sq_acc4(double (&acc)[kVec], float4 g) {
   if (BF16 && !GRASS_BF16_FP64_SQ && !GRASS_BF16_SQ_PAIR) {
-    acc[0] += (double)__fmaf_rn(g.w, g.w, __fmaf_rn(g.z, g.z, __fmaf_rn(g.y, g.y, __fmul_rn(g.x, g.x))));
+    const float w2 = kMutant == 13 ? 0.f : g.w;  // M13: the 4th square of the fp32 sum dropped
+    acc[0] += (double)__fmaf_rn(w2, w2, __fmaf_rn(g.z, g.z, __fmaf_rn(g.y, g.y, __fmul_rn(g.x, g.x))));
   } else if (BF16 && !GRASS_BF16_FP64_SQ) {
     acc[0] += (double)__fmaf_rn(g.y, g.y, __fmul_rn(g.x, g.x));
     acc[1] += (double)__fmaf_rn(g.w, g.w, __fmul_rn(g.z, g.z));

@@ -26,10 +26,13 @@ MUTANTS = {
     9: "P2P: theta' not stored into the last rank's parameters",
     10: "bf16: master never initialised from the bf16 parameter",
     11: "non-finite norm not flagged",
+    12: "norm: all-tiles warp reduction (warp_sum_multi) pairs the wrong halves",
+    13: "bf16 norm: the 4th square of each fp32 quad sum dropped",
 }
 TESTS = ("test_step_layers_vs_oracle_multi_step or test_norms_ragged_sizes_vs_oracle or "
          "test_bf16_mixed_precision_vs_oracle or test_p2p_virtual_ranks_vs_oracle or "
-         "test_zero_grad_zero_state_is_identity_on_theta or test_nonfinite_gradient_reported_and_not_recorded")
+         "test_zero_grad_zero_state_is_identity_on_theta or test_nonfinite_gradient_reported_and_not_recorded or "
+         "test_norms_probe_equals_update_bitwise or test_norms_integer_grads_exact_bf16")
 
 
 def build():
