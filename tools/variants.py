@@ -12,10 +12,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
     "base": [],
-    "p2pn4": ["GRASS_P2P_NORM_TPS=4"],
-    "p2pn6": ["GRASS_P2P_NORM_TPS=6"],
-    "p2pn2": ["GRASS_P2P_NORM_TPS=2"],
+    "bf16_tps13": ["GRASS_NORM_TPS_BF16=13"],
+    "bf16_tps10": ["GRASS_NORM_TPS_BF16=10"],
+    "fp32_tps7": ["GRASS_NORM_TPS=7"],
     "base_again": [],
+    "bf16_tps13_again": ["GRASS_NORM_TPS_BF16=13"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
