@@ -82,8 +82,37 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index, self.rows, self.proc = index, [], None
+        self.stop = threading.Event()
+        self.thread = None
+
+    def _nvml_poll(self, h, nv, ready):
+        """Poll NVML every 2 ms: the timed region is ~0.1 s, far below nvidia-smi's start-up."""
+        bits = [nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap]
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while True:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+            except Exception:
+                pass
+            ready.set()
+            if self.stop.wait(0.002):
+                return
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            ready = threading.Event()
+            self.thread = threading.Thread(target=self._nvml_poll, args=(h, nv, ready), daemon=True)
+            self.thread.start()
+            ready.wait(2.0)  # first sample taken before the timed region starts
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -101,6 +130,9 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def __exit__(self, *a):
+        if self.thread:
+            self.stop.set()
+            self.thread.join(timeout=1.0)
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
