@@ -135,10 +135,14 @@ class MgnState:
     def window(self):
         return [self.S[l] / self.c[l] if self.c[l] > 0 else None for l in range(self.n)]
 
-    def commit(self, alpha: float) -> list:
+    def commit(self, alpha: float, empty_first_ok: bool = False) -> list:
+        """empty_first_ok: a schedule without probing (T_p = 0, SPEC.md:451's
+        degenerate configuration) commits its first window before any
+        observation: m = 0 (uniform probabilities under Eq. 3); every other
+        commit needs observations."""
         if not (0.0 <= alpha <= 1.0):
             raise ValueError("alpha must lie in [0, 1]")
-        if sum(self.c) == 0:
+        if sum(self.c) == 0 and not (empty_first_ok and not self.committed):
             raise ValueError("commit with zero observations")
         w = self.window()
         if not self.committed:
@@ -364,7 +368,7 @@ class GrassOracle:
     when listed."""
 
     def __init__(self, layer_numel, gamma, tau=1.0, alpha=0.5, normalize=True,
-                 beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, seed=0, n_always=0):
+                 beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, seed=0, n_always=0, T_p=None):
         self.numel = list(layer_numel)
         self.n = len(self.numel)
         self.n_s = self.n - n_always          # sampled layers [0, n_s)
@@ -373,6 +377,7 @@ class GrassOracle:
         self.tau, self.alpha, self.normalize = tau, alpha, normalize
         self.beta1, self.beta2, self.eps, self.wd = beta1, beta2, eps, weight_decay
         self.seed = seed
+        self.T_p = T_p
         self.mgn = MgnState(self.n_s)
         self.probs = [1.0 / self.n_s] * self.n_s + [0.0] * (self.n - self.n_s)
         self.m = [np.zeros(k, np.float32) for k in self.numel]
@@ -389,7 +394,7 @@ class GrassOracle:
                 self.mgn.record(l, rms_norm(ss, self.numel[l]))
 
     def update_probs(self):
-        m = self.mgn.commit(self.alpha)
+        m = self.mgn.commit(self.alpha, empty_first_ok=self.T_p == 0)
         self.probs = list(softmax_probs(m, self.tau, self.normalize)) + [0.0] * (self.n - self.n_s)
         return list(self.probs)
 

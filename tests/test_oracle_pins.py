@@ -127,6 +127,22 @@ def test_commit_errors():
         st.record(1, float("nan"))
 
 
+def test_first_commit_without_probing_is_uniform():
+    """SPEC.md:451 (gamma = N_L, T_p = 0): a schedule without probing commits
+    its first window before any observation — m = 0, Eq. 3 gives exactly 1/N
+    (closed form); a later empty commit is still the SPEC.md:252 usage error,
+    and T_p > 0 keeps the error for the first commit too."""
+    for normalize in (True, False):
+        orc = O.GrassOracle([8, 8, 8, 8, 8], gamma=2, T_p=0, normalize=normalize)
+        assert orc.update_probs() == [0.2] * 5
+        with pytest.raises(ValueError):
+            orc.update_probs()
+    with pytest.raises(ValueError):
+        O.GrassOracle([8, 8], gamma=1, T_p=1).update_probs()
+    st = O.MgnState(3)
+    assert st.commit(0.5, empty_first_ok=True) == [0.0, 0.0, 0.0] and st.committed
+
+
 # ----------------------------------------------------------------- Eq. 3 softmax
 def test_softmax_spec_examples(golden):
     for ex in golden("spec_examples.json")["softmax"]:
