@@ -13,11 +13,13 @@ states resident (no offload), 1 B200:
     gamma-of-N_L resampling                                (a4, host)
 i.e. the bench resamples EVERY step (T_s = T_u = 1), the most expensive legal
 schedule.  Further legs in the same JSON line (--legs): "probe" (a1 alone over
-all 32 layers), "offload" (row a6, configs[2], + Fig. 4 vanilla), "period"
-(f1, T_s = 25), "train" (synthetic 7B fwd+bwd with resident / period+prefetch
-/ per-step offload after and during the backward), "p2p" (f2, the fused
-peer-memory data-parallel kernel), "bf16" (f3), "e2e" (gradients from pinned
-host memory through the public call), "cpu" (the oracle, single thread).
+all 32 layers, against the measured read-only HBM ceiling), "offload" (row
+a6, configs[2], + Fig. 4 vanilla), "period" (f1, T_s = 25), "p2p" (f2, the
+fused peer-memory data-parallel kernel), "bf16" (f3), "e2e" (gradients from
+pinned host memory through the public call), "cpu" (the oracle on one core
+and on all host cores); opt-in: "train" (synthetic 7B fwd+bwd with resident /
+period+prefetch / per-step offload after and during the backward, ~10 s of
+GEMMs).
 
 Timing: CUDA events on the stream the library launches on, W untimed warm-up
 steps, K timed steps bracketed by barrier + synchronize, max over ranks.  Every
@@ -45,7 +47,7 @@ METRIC = "active-layer params updated/s and offloaded step ms; % of HBM / host-l
 UNIT = "params/s"
 BYTES_PER_PARAM_UPDATE = 28      # read g, theta, m, v + write theta, m, v (fp32)
 BYTES_PER_PARAM_PROBE = 4        # read g
-DEFAULT_LEGS = "main,probe,p2p,offload,period,train,bf16,e2e,cpu"
+DEFAULT_LEGS = "main,probe,p2p,offload,period,bf16,e2e,cpu"   # "train" (R4, ~10 s of GEMMs) is opt-in
 FALLBACK_HBM_GBS = 6650.0        # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 
 
@@ -89,7 +91,10 @@ class ClockSampler:
         """Poll NVML every 2 ms: the timed region is ~0.1 s, far below nvidia-smi's start-up."""
         bits = [nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
                 nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap]
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception:
+            return               # no sample: __enter__ falls back to nvidia-smi
         while True:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
@@ -101,21 +106,50 @@ class ClockSampler:
             if self.stop.wait(0.002):
                 return
 
+    def _nvml_handle(self, nv):
+        """The NVML handle of THIS process's CUDA device: NVML enumerates every
+        GPU of the box and ignores CUDA_VISIBLE_DEVICES, so resolve it by PCI
+        bus id (then UUID); the bare index only if neither is available."""
+        import torch
+        prop = torch.cuda.get_device_properties(self.index)
+        dom, bus, dv = (getattr(prop, k, None) for k in ("pci_domain_id", "pci_bus_id", "pci_device_id"))
+        if bus is not None and dv is not None:
+            try:
+                return nv.nvmlDeviceGetHandleByPciBusId(f"{dom or 0:08X}:{bus:02X}:{dv:02X}.0".encode())
+            except Exception:
+                pass
+        uuid = getattr(prop, "uuid", None)
+        if uuid is not None:
+            try:
+                return nv.nvmlDeviceGetHandleByUUID(f"GPU-{uuid}".encode())
+            except Exception:
+                pass
+        return nv.nvmlDeviceGetHandleByIndex(self.index)
+
     def __enter__(self):
+        self.nv = None
         try:
             import pynvml as nv
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.nv = nv
+            h = self._nvml_handle(nv)
+            self.bus_id = nv.nvmlDeviceGetPciInfo(h).busId
             ready = threading.Event()
             self.thread = threading.Thread(target=self._nvml_poll, args=(h, nv, ready), daemon=True)
             self.thread.start()
-            ready.wait(2.0)  # first sample taken before the timed region starts
-            return self
+            if ready.wait(2.0):  # first sample taken before the timed region starts
+                return self
+            self.stop.set()      # the poll never sampled: fall back to nvidia-smi
+            self.thread.join(timeout=1.0)
+            self.stop.clear()
         except Exception:
-            self.thread = None
+            pass
+        self.thread = None
         try:
+            sel = getattr(self, "bus_id", None)
+            sel = sel.decode() if isinstance(sel, bytes) else (sel or str(self.index))
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                ["nvidia-smi", "-i", sel, f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
@@ -140,6 +174,11 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.nv is not None:
+            try:
+                self.nv.nvmlShutdown()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
@@ -214,6 +253,89 @@ def oracle_sample_time(n_p: int, gamma: int, sample_per_layer: int, lr: float, r
             O.sample_layers(p, gamma, 1234, r)
             times.append(time.perf_counter() - t0)
     return times
+
+
+def _oracle_chunk(args):
+    """One worker of the all-core oracle timing: Eq. 2 norm + AdamW over its
+    element chunk of the step's sample (single-threaded numpy)."""
+    n, layer, lr, reps = args
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle import grass_oracle as O
+    from synth import grad_sigmas, layer_grad, layer_params
+    sig = grad_sigmas(32, 0)
+    th = layer_params(n, layer).numpy()
+    g = layer_grad(n, layer, sig[layer]).numpy()
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        for r in range(reps):
+            O.sq_norm(g)
+            O.adamw_step(th, m, v, g, r + 1, lr, weight_decay=0.0)
+        return time.perf_counter() - t0
+
+
+def oracle_all_cores(gamma: int, sample_per_layer: int, lr: float):
+    """The same bounded sample split into element chunks over every host core
+    (multiprocessing, one numpy thread per worker): params/s of the slowest
+    worker's wall time (the per-layer commit / softmax / sampling over 32
+    layers is microseconds and omitted)."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    per = max(1, gamma * sample_per_layer // cores)
+    jobs = [(per, k % gamma, lr, 2) for k in range(cores)]
+    with mp.get_context("spawn").Pool(cores) as pool:
+        pool.map(_oracle_chunk, [(1024, 0, lr, 1)] * cores)          # workers imported and warm
+        t0 = time.perf_counter()
+        times = pool.map(_oracle_chunk, jobs)
+        wall = time.perf_counter() - t0
+    return {"value": 2 * per * cores / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{cores} workers x {per} elements x 2 steps (fp64 norm + AdamW), spawn pool, "
+                      f"threadpoolctl 1 thread each; slowest worker {max(times):.2f} s, wall {wall:.2f} s"}
+
+
+def measure_read_ceiling(dev, gib: int = 8) -> dict:
+    """Read-only HBM ceiling: hand-written streaming reads
+    of an 8 GiB buffer (>> 126 MB L2) — LDG.128 (no-allocate, 8 loads in flight
+    per thread) over a grid sweep and TMA bulk copies into a shared-memory ring
+    (K1's data movement, no arithmetic) over a unit / stage sweep
+    (paper_2604_07808_b200/diag/read_ceiling.cu); best of 3 per config, CUDA
+    events on the launching stream.  The probe's denominator."""
+    import ctypes as C
+
+    import torch
+    from paper_2604_07808_b200 import build as B
+    lib = C.CDLL(B.DIAG_OUT)
+    f = lib.grass_diag_read
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_ulonglong, C.c_int, C.c_int, C.c_uint, C.c_int, C.c_void_p, C.c_void_p]
+    nbytes = gib << 30
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    buf.fill_(7)
+    sink = torch.zeros(1, dtype=torch.int64, device=dev)
+    s = torch.cuda.Stream(device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    cfgs = [("ldg", 0, sms * k, 0, 0) for k in (2, 4, 8)] + \
+           [("tma", 1, sms, u << 10, st) for u, st in ((16, 12), (32, 6), (64, 3), (96, 2))]
+    sweep = {}
+    for name, mode, grid, unit, st in cfgs:
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            rc = f(buf.data_ptr(), nbytes, mode, grid, unit, st, sink.data_ptr(), s.cuda_stream)
+            e1.record(s)
+            torch.cuda.synchronize()
+            if rc != 0:
+                raise RuntimeError(f"grass_diag_read {name}: cuda error {rc}")
+            best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        sweep[f"{name} grid={grid}" + (f" unit={unit >> 10}KiB x{st}" if mode else "")] = round(best, 1)
+    del buf
+    torch.cuda.empty_cache()
+    k = max(sweep, key=sweep.get)
+    return {"GBps": sweep[k], "best": k, "sweep": sweep, "bytes": nbytes}
 
 
 def workload_config(model: str, gamma: int, world: int) -> dict:
@@ -291,10 +413,18 @@ def run_grass(args, rank, world, local):
         probe_ms.append(ev[0].elapsed_time(ev[1]))
     probs = ctx.update_probs()
     ids = ctx.sample_layers(0)
+    read_ceiling = None
     if "probe" in legs:
         t = min(probe_ms[1:]) / 1e3
         gbs = BYTES_PER_PARAM_PROBE * NL * n_p / world / t / 1e9
+        try:
+            read_ceiling = measure_read_ceiling(dev)
+        except Exception as ex:  # recorded, never fatal to the line
+            read_ceiling = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+        rc = read_ceiling.get("GBps")
         out["probe"] = {"ms": t * 1e3, "layers": NL, "GBps": gbs, "frac_hbm": gbs / hbm_peak,
+                        "read_ceiling_GBps": rc, "frac_read_peak": gbs / rc if rc else None,
+                        "read_ceiling": read_ceiling,
                         "bytes": BYTES_PER_PARAM_PROBE * NL * n_p // world}
 
     # ---- main leg: configs[1]
@@ -388,7 +518,11 @@ def run_grass(args, rank, world, local):
         torch.cuda.synchronize()
         et = max_over_ranks(e0.elapsed_time(e1) / 1e3, world, dev)
         return {"value": ksteps * active / et, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": et / ksteps * 1e3, "steps": ksteps}
+                "d2h_bytes_per_step": d2h, "ms_per_step": et / ksteps * 1e3, "steps": ksteps,
+                "note": "the step's gradients enter from pinned host memory (the same gamma host buffers "
+                        "stand for whichever layers were sampled: their values do not change the timing); "
+                        "the result read back is the committed MGN window (S, c, flag); theta' and m/v "
+                        "stay in HBM"}
 
     e2e = guarded("e2e", leg_e2e)
 
@@ -800,7 +934,10 @@ def run_grass(args, rank, world, local):
                 "params_per_s": args.steps * active / bt, "step_ms": bt / args.steps * 1e3,
                 "kernel_ms": bk, "GBps": bgbs, "frac_hbm": bgbs / hbm_peak,
                 "bytes_per_param": BYTES_PER_PARAM_UPDATE,
-                "probe_ms": bprobe_ms, "probe_GBps": 2 * NL * n_p / world / (bprobe_ms / 1e3) / 1e9}
+                "probe_ms": bprobe_ms, "probe_GBps": 2 * NL * n_p / world / (bprobe_ms / 1e3) / 1e9,
+                "probe_frac_read_peak": (2 * NL * n_p / world / (bprobe_ms / 1e3) / 1e9 / read_ceiling["GBps"]
+                                         if read_ceiling and read_ceiling.get("GBps") else None),
+                "probe_frac_nominal_8TBps": 2 * NL * n_p / world / (bprobe_ms / 1e3) / 1e9 / 8000.0}
 
     # P2P runs after the other multi-GPU legs: at N > 1 it is the one leg whose
     # data path (peer memory over CUDA IPC) could not be run on the 1-GPU pool,
@@ -816,9 +953,14 @@ def run_grass(args, rank, world, local):
         sample = 1 << 23
         times = oracle_sample_time(n_p, gamma, sample, args.lr, reps=2)
         v = gamma * sample / min(times)
-        return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                "sample": f"{gamma} x {sample} elements of one step (fp64 norm + AdamW) + commit/"
-                          f"softmax/sampling over {NL} layers, best of 2, single thread"}
+        res = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "host_cores": os.cpu_count(),
+               "sample": f"{gamma} x {sample} elements of one step (fp64 norm + AdamW) + commit/"
+                         f"softmax/sampling over {NL} layers, best of 2, single thread"}
+        try:
+            res["all_cores"] = oracle_all_cores(gamma, sample, args.lr)
+        except Exception as ex:
+            res["all_cores"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+        return res
 
     cpu = guarded("cpu", leg_cpu) if (rank == 0 and world == 1) else None
 
@@ -835,8 +977,9 @@ def run_grass(args, rank, world, local):
                          "kernel_ms": kernel_ms, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            # world > 1: NCCL reduce-scatter of the gradients + all-gather of the
-            # parameters, (W-1)/W of 4 B per active parameter each, per rank
+            # world > 1: the NCCL gradient exchange (grouped send/recv of the
+            # slices, summed in rank order by the update kernel) + all-gather of
+            # the parameters, (W-1)/W of 4 B per active parameter each, per rank
             "dp_comm": ({"bytes_per_rank_per_step": 8 * active * (world - 1) // world,
                          "GBps_per_rank": 8 * active * (world - 1) / world / (elapsed / args.steps) / 1e9}
                         if world > 1 else None),

@@ -48,13 +48,17 @@ def _run(cmd, verbose):
     return r.stdout + r.stderr
 
 
-def build(verbose: bool = False, force: bool = False, defines=(), out: str | None = None) -> str:
-    """defines/out: developer A/B variants (e.g. tools/variants.py); the product is OUT."""
+def build(verbose: bool = False, force: bool = False, defines=(), out: str | None = None,
+          src_dir: str | None = None) -> str:
+    """defines/out: developer A/B variants (e.g. tools/variants.py); src_dir: a
+    patched copy of csrc/ (tools/kernel_mutation.py); the product is OUT built
+    from CSRC."""
     out_path = out or OUT
+    csrc = src_dir or CSRC
     cuda = _cuda_home()
     nvcc = os.path.join(cuda, "bin", "nvcc")
-    srcs = sorted(os.listdir(CSRC))
-    deps = [os.path.join(CSRC, f) for f in srcs] + [os.path.join(ROOT, "include", "grass.h"), __file__]
+    srcs = sorted(os.listdir(csrc))
+    deps = [os.path.join(csrc, f) for f in srcs] + [os.path.join(ROOT, "include", "grass.h"), __file__]
     if not force and os.path.exists(out_path) and os.path.getmtime(out_path) >= max(os.path.getmtime(d) for d in deps):
         return out_path
     build_dir = BUILD if out is None else os.path.join(BUILD, "variant_" + os.path.basename(out_path).replace(".so", ""))
@@ -64,7 +68,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str | Non
     objs = []
     log = []
     for f in srcs:
-        src = os.path.join(CSRC, f)
+        src = os.path.join(csrc, f)
         obj = os.path.join(build_dir, f + ".o")
         if f.endswith(".cu"):
             log.append(_run([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--fmad=false",
@@ -78,12 +82,33 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str | Non
         objs.append(obj)
     tmp = out_path + ".tmp"
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
-          "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map"),
+          "-Xlinker", "--version-script=" + os.path.join(csrc, "exports.map"),
           "-ldl", "-lpthread", "-lrt", "-lz"], verbose)
     os.replace(tmp, out_path)
     with open(os.path.join(build_dir, "ptxas.log"), "w") as fh:
         fh.write("\n".join(log))
+    if out is None:
+        build_diag(verbose, force)
     return out_path
+
+
+DIAG = os.path.join(PKG, "diag")
+DIAG_OUT = os.path.join(PKG, "libgrass_diag.so")
+
+
+def build_diag(verbose: bool = False, force: bool = False) -> str:
+    """libgrass_diag.so: measurement kernels of bench.py (the read-only HBM
+    ceiling, diag/read_ceiling.cu) — not part of the hot path."""
+    srcs = [os.path.join(DIAG, f) for f in sorted(os.listdir(DIAG)) if f.endswith(".cu")]
+    if not force and os.path.exists(DIAG_OUT) and os.path.getmtime(DIAG_OUT) >= max(
+            [os.path.getmtime(x) for x in srcs] + [os.path.getmtime(__file__)]):
+        return DIAG_OUT
+    nvcc = os.path.join(_cuda_home(), "bin", "nvcc")
+    tmp = DIAG_OUT + ".tmp"
+    _run([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-cudart", "static",
+          "-Xcompiler", "-fPIC", *srcs, "-o", tmp], verbose)
+    os.replace(tmp, DIAG_OUT)
+    return DIAG_OUT
 
 
 if __name__ == "__main__":

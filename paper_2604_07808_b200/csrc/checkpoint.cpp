@@ -15,7 +15,7 @@ namespace gapi {
 
 // ---- checkpoint ------------------------------------------------------------
 const char kCkMagic[8] = {'G', 'R', 'A', 'S', 'S', 'C', 'K', '1'};
-const uint32_t kCkVersion = 2;  // 2: n_always in the header
+const uint32_t kCkVersion = 3;  // 2: n_always in the header; 3: bf16 master flags + config fingerprint
 
 uint32_t crc_update(uint32_t crc, const void* p, size_t n) {
   const Bytef* b = static_cast<const Bytef*>(p);
@@ -36,11 +36,47 @@ void put(std::vector<char>* h, const T* p, size_t n) {
 
 constexpr int kCkInts = 6;  // n_layers, world, rank, committed, dtype, n_always
 
-std::vector<char> ck_header(grass_ctx* c) {
+// The hyperparameters a checkpoint's state depends on (a load into a context
+// configured differently is rejected): Eq. 3/4 (tau, alpha, normalisation),
+// AdamW (betas, eps, weight decay), the sampler (gamma, seed, policy) and the
+// schedule (T_p, T_s, T_u).
+struct CkFingerprint {
+  double tau, alpha, beta1, beta2, eps, weight_decay;
+  int32_t normalize_mgn, gamma, T_p, T_s, T_u, policy;
+  uint64_t seed;
+};
+static_assert(sizeof(CkFingerprint) == 80, "fingerprint layout");
+CkFingerprint ck_fingerprint(const grass_ctx* c) {
+  CkFingerprint f;
+  std::memset(&f, 0, sizeof(f));
+  const grass_config& k = c->cfg;
+  f.tau = k.tau;
+  f.alpha = k.alpha;
+  f.beta1 = k.beta1;
+  f.beta2 = k.beta2;
+  f.eps = k.eps;
+  f.weight_decay = k.weight_decay;
+  f.normalize_mgn = k.normalize_mgn;
+  f.gamma = k.gamma;
+  f.T_p = k.T_p;
+  f.T_s = k.T_s;
+  f.T_u = k.T_u;
+  f.policy = k.policy;
+  f.seed = k.seed;
+  return f;
+}
+
+// mvalid: the bf16 master flags (DevState::mvalid, read from the device by
+// the caller) — a master written by grass_write_master before any update
+// (t = 0) is valid and must survive a save / load.
+std::vector<char> ck_header(grass_ctx* c, const std::vector<int32_t>& mvalid) {
   std::vector<char> h;
   const int32_t ints[kCkInts] = {c->nl,         c->cfg.world,         c->cfg.rank, c->committed ? 1 : 0,
                                  c->cfg.param_dtype, c->cfg.n_always};
   put(&h, ints, kCkInts);
+  const CkFingerprint fp = ck_fingerprint(c);
+  put(&h, &fp, 1);
+  put(&h, mvalid.data(), c->nl);
   put(&h, c->numel.data(), c->nl);
   put(&h, c->shard_len.data(), c->nl);
   put(&h, c->t.data(), c->nl);
@@ -66,7 +102,9 @@ grass_status grass_save_state(grass_ctx* c, const char* path) try {
   if (s != GRASS_OK) return s;
   // t_l lives on the device (it advances in captured graphs too)
   CUDA_TRY(c, cudaMemcpy(c->t.data(), c->st.t, sizeof(long long) * c->nl, cudaMemcpyDeviceToHost));
-  const std::vector<char> hdr = ck_header(c);
+  std::vector<int32_t> mvalid(c->nl, 0);
+  CUDA_TRY(c, cudaMemcpy(mvalid.data(), c->st.mvalid, sizeof(int32_t) * c->nl, cudaMemcpyDeviceToHost));
+  const std::vector<char> hdr = ck_header(c, mvalid);
   FILE* f = std::fopen(path, "wb");
   if (!f) return c->fail(GRASS_E_IO, std::string("cannot open ") + path + " for writing");
   bool ok = true;
@@ -118,7 +156,7 @@ grass_status grass_load_state(grass_ctx* c, const char* path) try {
   if (std::fread(&ver, 4, 1, f) != 1 || ver != kCkVersion) return bad(GRASS_E_IO, "unsupported version");
   if (std::fread(&hlen, 8, 1, f) != 1 || std::fread(&hcrc, 4, 1, f) != 1) return bad(GRASS_E_IO, "truncated header");
   const int nl = c->nl;
-  const size_t want = 4 * kCkInts + (size_t)nl * (3 * 8 + 4 * 8);
+  const size_t want = 4 * kCkInts + sizeof(CkFingerprint) + (size_t)nl * (4 + 3 * 8 + 4 * 8);
   if (hlen != want) return bad(GRASS_E_INVALID, "checkpoint was written for a different layer count");
   std::vector<char> hdr(hlen);
   if (std::fread(hdr.data(), 1, hlen, f) != hlen) return bad(GRASS_E_IO, "truncated header");
@@ -130,6 +168,10 @@ grass_status grass_load_state(grass_ctx* c, const char* path) try {
   };
   int32_t ints[kCkInts];
   take(ints, sizeof(ints));
+  CkFingerprint fp;
+  take(&fp, sizeof(fp));
+  std::vector<int32_t> mvalid(nl);
+  take(mvalid.data(), 4 * nl);
   std::vector<int64_t> numel(nl), slen(nl), t(nl);
   std::vector<double> mgn(nl), probs(nl), S(nl);
   std::vector<long long> cnt(nl);
@@ -144,6 +186,10 @@ grass_status grass_load_state(grass_ctx* c, const char* path) try {
       ints[5] != c->cfg.n_always || numel != c->numel || slen != c->shard_len)
     return bad(GRASS_E_INVALID,
                "checkpoint does not match this context (N_L, n_always, N_p, dtype, world or rank)");
+  const CkFingerprint mine = ck_fingerprint(c);
+  if (std::memcmp(&fp, &mine, sizeof(fp)) != 0)
+    return bad(GRASS_E_INVALID, "checkpoint was written by a context with other hyperparameters (tau, alpha, "
+                                "normalisation, betas, eps, weight decay, gamma, seed, policy or T_p/T_s/T_u)");
   const long blobs = std::ftell(f);
   // pass 1: verify every blob's length and CRC32 before touching the context
   std::vector<char> buf(64u << 20);
@@ -184,7 +230,7 @@ grass_status grass_load_state(grass_ctx* c, const char* path) try {
         return s;
       }
     }
-    if (c->bf16) c->master_valid[l] = t[l] > 0 ? 1 : 0;
+    if (c->bf16) c->master_valid[l] = mvalid[l] ? 1 : 0;
   }
   std::fclose(f);
   c->t = t;

@@ -7,6 +7,8 @@
 
 #include <dlfcn.h>
 
+#include <cuda_runtime.h>
+
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -20,8 +22,10 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
-                                ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -49,7 +53,10 @@ NcclApi& api() {
     GRASS_SYM(GetUniqueId, "ncclGetUniqueId");
     GRASS_SYM(CommInitRank, "ncclCommInitRank");
     GRASS_SYM(CommDestroy, "ncclCommDestroy");
-    GRASS_SYM(ReduceScatter, "ncclReduceScatter");
+    GRASS_SYM(Send, "ncclSend");
+    GRASS_SYM(Recv, "ncclRecv");
+    GRASS_SYM(GroupStart, "ncclGroupStart");
+    GRASS_SYM(GroupEnd, "ncclGroupEnd");
     GRASS_SYM(AllGather, "ncclAllGather");
     GRASS_SYM(GetErrorString, "ncclGetErrorString");
 #undef GRASS_SYM
@@ -102,12 +109,48 @@ void Comm::destroy() {
   comm = nullptr;
 }
 
-bool Comm::reduce_scatter_sum(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
-                              std::string* err) {
-  ncclResult_t r = api().ReduceScatter(send, recv, count, bf16 ? ncclBfloat16 : ncclFloat32, ncclSum,
-                                       comm, s);
+bool Comm::exchange_slices(const void* send, void* recv, size_t count, size_t stride, bool bf16, cudaStream_t s,
+                           std::string* err) {
+  const ncclDataType_t dt = bf16 ? ncclBfloat16 : ncclFloat32;
+  const size_t esz = bf16 ? 2 : 4;
+  // this rank's own slice: a device copy on the same stream (no NCCL
+  // self-send: at world 1 the exchange issues no NCCL call at all)
+  const cudaError_t ce = cudaMemcpyAsync(static_cast<char*>(recv) + (size_t)rank * stride * esz,
+                                         static_cast<const char*>(send) + (size_t)rank * count * esz, count * esz,
+                                         cudaMemcpyDeviceToDevice, s);
+  if (ce != cudaSuccess) {
+    *err = std::string("exchange: own slice copy: ") + cudaGetErrorString(ce);
+    return false;
+  }
+  if (world == 1) return true;
+  ncclResult_t r = api().GroupStart();
   if (r != ncclSuccess) {
-    *err = nccl_msg("ncclReduceScatter", r);
+    *err = nccl_msg("ncclGroupStart", r);
+    return false;
+  }
+  ncclResult_t first = ncclSuccess;
+  const char* what = "";
+  for (int q = 0; q < world && first == ncclSuccess; ++q) {
+    if (q == rank) continue;
+    r = api().Send(static_cast<const char*>(send) + (size_t)q * count * esz, count, dt, q, comm, s);
+    if (r != ncclSuccess) {
+      first = r;
+      what = "ncclSend";
+      break;
+    }
+    r = api().Recv(static_cast<char*>(recv) + (size_t)q * stride * esz, count, dt, q, comm, s);
+    if (r != ncclSuccess) {
+      first = r;
+      what = "ncclRecv";
+    }
+  }
+  r = api().GroupEnd();  // always closes the group
+  if (first == ncclSuccess && r != ncclSuccess) {
+    first = r;
+    what = "ncclGroupEnd";
+  }
+  if (first != ncclSuccess) {
+    *err = nccl_msg(what, first);
     return false;
   }
   return true;

@@ -6,7 +6,7 @@
 #include <cstring>
 #include <string>
 
-#include "../../include/grass.h"
+#include "grass.h"  // include/ (-I)
 
 namespace grass {
 
@@ -18,12 +18,16 @@ struct Comm {
   int rank = 0, world = 1;
   bool init(const void* unique_id, int rank, int world, std::string* err);
   void destroy();
-  // N1: gradient sum, element-sharded (recv = this rank's shard); fp32 or bf16.
-  // The 1/world of the average is applied by the kernels (Batch::gscale): NCCL
-  // 2.28.9's ncclAvg reduce-scatter drops the last 16 elements for counts
-  // = 16 (mod 64) on a 1-rank communicator (tools/dbg_nccl.py).
-  bool reduce_scatter_sum(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
-                          std::string* err);
+  // N1: gradient exchange, element-sharded.  Rank r sends slice q of its
+  // gradient (elements [q*count, (q+1)*count)) to rank q and receives every
+  // rank q's slice r into recv + q*stride elements (one grouped ncclSend /
+  // ncclRecv per peer; its own slice by a device copy) — the bytes of a reduce-scatter, but
+  // the SUM is left to the update kernel, which adds the W slices in ascending
+  // rank order in fp32 (reading R20) for fp32 and bf16 gradients alike,
+  // bit-identical to the P2P path.  (A bf16 ncclReduceScatter would round the
+  // partial sums to bf16 W-1 times.)
+  bool exchange_slices(const void* send, void* recv, size_t count, size_t stride, bool bf16, cudaStream_t s,
+                       std::string* err);
   // N2: parameter shards back to every rank (in place when send = recv + rank*count).
   bool all_gather(const void* send, void* recv, size_t count, bool bf16, cudaStream_t s,
                   std::string* err);

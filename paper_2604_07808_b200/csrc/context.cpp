@@ -264,10 +264,12 @@ Batch make_batch(const grass_ctx* c, int32_t mode) {
   b.eps = (float)c->cfg.eps;
   b.coef = c->cur_coef;
   b.bf16 = c->bf16 ? 1 : 0;
-  // DP: the kernels read reduce-scattered SUMS; x 1/W makes them the average
-  // (exact for power-of-two W)
+  // DP: the kernels sum the W ranks' gradients in ascending rank order (fp32)
+  // and x 1/W makes the sum the average (exact for power-of-two W) — R20, the
+  // same arithmetic for the NCCL and the P2P path
   b.gscale = (c->dp || c->p2p) ? (float)(1.0 / (double)c->cfg.world) : 1.0f;
-  b.npeer = c->p2p ? c->cfg.world : 0;
+  b.npeer = (c->p2p || c->dp) ? c->cfg.world : 0;
+  b.ntpeer = c->p2p ? c->cfg.world : 0;  // NCCL: theta' to this rank's buffer, then ncclAllGather
   return b;
 }
 
@@ -314,6 +316,10 @@ Seg range_seg(const grass_ctx* c, int l, const void* g, int64_t off, int64_t n) 
     s.gpeer = const_cast<const void* const*>(c->d_ptab + (size_t)l * 2 * W);
     s.tpeer = c->d_ptab + (size_t)l * 2 * W + W;
     s.poff = c->shard_off[l] + off;
+    s.gpoff = s.poff;
+  } else if (c->dp) {  // `g` is a gradient slot (gs_slot): the W received slices of the shard
+    s.gpeer = const_cast<const void* const*>(c->d_rtab + (size_t)gs_slot_index(c, g) * c->cfg.world);
+    s.gpoff = off;
   }
   return s;
 }
@@ -353,6 +359,7 @@ void free_ctx(grass_ctx* c) {
   dfree(c->st.mvalid);
   dfree(c->d_gather);
   dfree(c->d_gscratch);
+  dfree(c->d_rtab);
   dfree(c->d_coef);
   dfree(c->d_ring);
   dfree(c->d_gring);
@@ -533,7 +540,12 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     CUDA_TRY(c, cudaStreamCreateWithFlags(&c->comm_s, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&c->ev_cs_start, &c->ev_cs_end, &c->ev_rs[0], &c->ev_rs[1], &c->ev_k2[0], &c->ev_k2[1]})
       CUDA_TRY(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    CUDA_TRY(c, dalloc((void**)&c->d_gscratch, c->esz * (size_t)c->slot_stride * nslots));
+    CUDA_TRY(c, dalloc((void**)&c->d_gscratch, c->esz * (size_t)c->slot_stride * W * nslots));
+    std::vector<void*> tab((size_t)W * nslots);
+    for (size_t k = 0; k < nslots; ++k)
+      for (int q = 0; q < W; ++q) tab[k * W + q] = c->d_gscratch + ((k * W + q) * (size_t)c->slot_stride) * c->esz;
+    CUDA_TRY(c, dalloc((void**)&c->d_rtab, sizeof(void*) * tab.size()));
+    CUDA_TRY(c, cudaMemcpy(c->d_rtab, tab.data(), sizeof(void*) * tab.size(), cudaMemcpyHostToDevice));
     if (!c->comm.init(cfg->nccl_unique_id, cfg->rank, W, &c->err)) return GRASS_E_NCCL;
     c->has_comm = true;
   }

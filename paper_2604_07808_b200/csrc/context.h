@@ -47,7 +47,8 @@ struct grass_ctx {
   void* h_mgn = nullptr;  // pinned host mirror of d_mgn
   size_t mgn_bytes = 0;
   double* d_gather = nullptr;  // world x N_L fp64 (all-gathered shard partials)
-  char* d_gscratch = nullptr;  // DP: averaged-gradient shards (2, or clip_slots when clipping)
+  char* d_gscratch = nullptr;  // DP: gradient slots (2, or clip_slots when clipping) x W slices of the shard
+  void** d_rtab = nullptr;     // DP: device [slot][W] addresses of the slots' slices (Seg::gpeer)
   int clip_slots = 0;          // DP + clipping: layers one call may list (gamma + n_always)
 
   // optimizer state of this rank's shard of every layer: arr[0] = m,
@@ -59,6 +60,7 @@ struct grass_ctx {
   const float* lr_ptr = nullptr;   // grass_set_lr_device: lr read on the device each step
   bool captured = false;           // a hot-path call was captured into a CUDA graph
   bool captured_offload = false;   // the last offloaded step_layers was captured
+  bool ever_captured_offload = false;  // some offloaded step_layers was captured (sticky)
   std::vector<int64_t> t;
 
   // offload ring (step residency)
@@ -251,8 +253,10 @@ grass_status p2p_finish_layers(grass_ctx* c, const std::vector<int32_t>& layers,
 grass_status p2p_end(grass_ctx* c, const int32_t* ids, const std::vector<int>& order, cudaStream_t s);
 void* gs_slot(grass_ctx* c, int k);
 void* rs_slot(grass_ctx* c, int j);
+int gs_slot_index(const grass_ctx* c, const void* slot);
+grass_status comm_exchange(grass_ctx* c, const void* grad, int l, void* slot, cudaStream_t s);
 grass_status comm_begin(grass_ctx* c, cudaStream_t s);
-grass_status comm_rs(grass_ctx* c, int j, const void* grad, int64_t len);
+grass_status comm_rs(grass_ctx* c, int j, const void* grad, int l);
 grass_status comm_wait_rs(grass_ctx* c, int j, cudaStream_t s);
 grass_status comm_after_update(grass_ctx* c, int j, void* params, int64_t off, int64_t len, cudaStream_t s);
 grass_status comm_end(grass_ctx* c, cudaStream_t s);
@@ -278,6 +282,6 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
 
 // checkpoint.cpp
 uint32_t crc_update(uint32_t crc, const void* p, size_t n);
-std::vector<char> ck_header(grass_ctx* c);
+std::vector<char> ck_header(grass_ctx* c, const std::vector<int32_t>& mvalid);
 
 }  // namespace gapi

@@ -119,9 +119,27 @@ grass_status p2p_end(grass_ctx* c, const int32_t* ids, const std::vector<int>& o
 }
 
 // ---- data-parallel schedule on the comm stream --------------
-// Shard buffer of slot k (2 double-buffered slots; gamma slots when clipping).
-void* gs_slot(grass_ctx* c, int k) { return c->d_gscratch + (size_t)k * c->slot_stride * c->esz; }
+// Gradient slot k (2 double-buffered slots; gamma + n_always when clipping):
+// W slices of this rank's shard, slice q (rank q's gradient) at q*slot_stride
+// elements.  The returned pointer (slice 0) stands for the slot in range_seg,
+// which points the kernel at the slot's slice table (DevState-independent
+// device array d_rtab[k][W]).
+void* gs_slot(grass_ctx* c, int k) {
+  return c->d_gscratch + (size_t)k * c->cfg.world * c->slot_stride * c->esz;
+}
 void* rs_slot(grass_ctx* c, int j) { return gs_slot(c, j & 1); }
+int gs_slot_index(const grass_ctx* c, const void* slot) {
+  return (int)((static_cast<const char*>(slot) - c->d_gscratch) / ((int64_t)c->cfg.world * c->slot_stride * c->esz));
+}
+
+// N1 into gradient slot k: every rank's slice of this rank's shard of layer l.
+grass_status comm_exchange(grass_ctx* c, const void* grad, int l, void* slot, cudaStream_t s) {
+  TraceScope ts(c, s, GRASS_TRACE_RS, l, 0, c->shard_len[l]);
+  if (!c->comm.exchange_slices(grad, slot, (size_t)c->shard_len[l], (size_t)c->slot_stride, c->bf16, s, &c->err))
+    return GRASS_E_NCCL;
+  c->launches++;
+  return GRASS_OK;
+}
 
 // Comm stream starts after everything already enqueued on the caller stream
 // (the gradients are produced there).
@@ -131,17 +149,13 @@ grass_status comm_begin(grass_ctx* c, cudaStream_t s) {
   return GRASS_OK;
 }
 
-// N1 for the j-th layer of the call: reduce-scatter(avg) into its slot once
-// the update that last read the slot (layer j-2) has finished.
-grass_status comm_rs(grass_ctx* c, int j, const void* grad, int64_t len) {
+// N1 for the j-th layer of the call (layer l): the gradient exchange into its
+// slot once the update that last read the slot (layer j-2) has finished.
+grass_status comm_rs(grass_ctx* c, int j, const void* grad, int l) {
   const int k = j & 1;
   if (j >= 2) CUDA_TRY(c, cudaStreamWaitEvent(c->comm_s, c->ev_k2[k], 0));
-  {
-    TraceScope ts(c, c->comm_s, GRASS_TRACE_RS, -1, 0, len);
-    if (!c->comm.reduce_scatter_sum(grad, rs_slot(c, j), (size_t)len, c->bf16, c->comm_s, &c->err))
-      return GRASS_E_NCCL;
-  }
-  c->launches++;
+  grass_status st = comm_exchange(c, grad, l, rs_slot(c, j), c->comm_s);
+  if (st != GRASS_OK) return st;
   CUDA_TRY(c, cudaEventRecord(c->ev_rs[k], c->comm_s));
   return GRASS_OK;
 }

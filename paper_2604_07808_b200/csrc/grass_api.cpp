@@ -122,7 +122,11 @@ grass_status grass_update_probs(grass_ctx* c, double* probs_out) try {
     CUDA_TRY(c, cudaMemcpy(c->d_mgn, c->h_mgn, 16 * (size_t)c->nl, cudaMemcpyHostToDevice));
     return s;
   }
-  if (total == 0) return c->fail(GRASS_E_STATE, "commit with zero observations in the window");
+  // a commit needs observations — except the first commit of a
+  // schedule without probing (T_p = 0, SPEC.md:451's degenerate configuration):
+  // there is no probing window, m = 0 and Eq. 3 gives uniform probabilities
+  if (total == 0 && (c->committed || c->cfg.T_p != 0))
+    return c->fail(GRASS_E_STATE, "commit with zero observations in the window");
   // Eq. 2 window mean (R4), first commit (R8) / Eq. 4 EMA (R5), retention of frozen layers
   const double a = c->cfg.alpha;
   for (int l = 0; l < c->nsamp; ++l) {

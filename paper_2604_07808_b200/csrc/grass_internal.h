@@ -2,7 +2,7 @@
 #pragma once
 #include <cstdint>
 
-#include "../../include/grass.h"
+#include "grass.h"  // include/ (-I)
 
 #ifdef __CUDACC__
 #include <cuda_runtime.h>
@@ -51,14 +51,20 @@ struct Seg {
   // bf16 model copy (updated as RNE(master')) and the bf16 gradient
   uint16_t* theta16;
   const uint16_t* g16;
-  // P2P data parallelism (Batch::npeer > 0): the gradient is
-  // the sum over every rank's full-layer buffer and theta' is stored into every
-  // rank's buffer (peer-mapped addresses); element idx of this range is
-  // element poff + idx of the full layer.  The local theta / m / v above are
-  // this rank's shard as usual.
-  const void* const* gpeer;  // device [npeer]: full-layer gradient of each rank
-  void* const* tpeer;        // device [npeer]: full-layer parameters of each rank
+  // Data parallelism with the gradient summed in the kernel (Batch::npeer >
+  // 0): the gradient of element idx of this range is the ascending-rank fp32
+  // sum of gpeer[r][gpoff + idx] over the npeer ranks, and (Batch::ntpeer > 0,
+  // P2P) theta' is stored into tpeer[r][poff + idx] of every
+  // rank.  P2P: gpeer / tpeer are every rank's full-layer buffers (peer-mapped
+  // addresses) and gpoff = poff = the range's element offset in the full
+  // layer.  NCCL: gpeer are the W slices of this rank's shard received by the
+  // gradient all-to-all (gpoff = offset in the shard), ntpeer = 0 (theta' goes
+  // to this rank's buffer, then ncclAllGather).  The local theta / m / v above
+  // are this rank's shard as usual.
+  const void* const* gpeer;  // device [npeer]: gradient of each rank
+  void* const* tpeer;        // device [ntpeer]: full-layer parameters of each rank
   int64_t poff;
+  int64_t gpoff;
 };
 
 struct Batch {
@@ -70,7 +76,8 @@ struct Batch {
   const float* coef;       // device scalar multiplying g in the update (clipping), or NULL
   int32_t bf16;            // 1: bf16 gradients / parameters with fp32 master (Seg::g16, theta16)
   float gscale;            // multiplies every gradient element on load (DP: 1/world), else 1
-  int32_t npeer;           // P2P: ranks whose gradients are summed (Seg::gpeer), else 0
+  int32_t npeer;           // DP: ranks whose gradients are summed in the kernel (Seg::gpeer), else 0
+  int32_t ntpeer;          // P2P: ranks whose parameter buffers receive theta' (Seg::tpeer), else 0
 };
 
 // Device-resident MGN / reduction state (all arrays indexed by layer id unless noted).

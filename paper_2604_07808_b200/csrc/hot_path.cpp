@@ -39,18 +39,29 @@ grass_status capture_check(grass_ctx* c, cudaStream_t st, bool any_host, bool* c
 // Offload hazards around CUDA-graph capture: events recorded outside a
 // capture cannot be waited on inside it and vice versa.  Inside a capture
 // (after grass_sync) every earlier copy is complete, so the host-side hazard
-// flags start clean and the copy streams are forked into the capture; eager
-// calls after captured ones wait for the device once and start clean too.
+// flags start clean and the copy streams are forked into the capture.  The
+// host never sees the graph's replays, so EVERY eager offloaded call after a
+// capture (not only the first) orders its copy streams after everything
+// already enqueued on the caller's stream — the replays included, whose copy
+// nodes complete with the graph — before a fetch can overwrite a ring slot a
+// replay still reads or a write-back can read host state a replay is still
+// writing (replays must be stream-ordered before later eager calls, as any
+// work on the caller's buffers).  The first eager call after a capture also
+// waits for the device once and clears the flags that refer to events
+// recorded inside the capture.
 grass_status offload_capture_fence(grass_ctx* c, cudaStream_t st, bool capturing) {
   if (!c->cfg.offload) return GRASS_OK;
-  if (!capturing && !c->captured_offload) return GRASS_OK;
-  if (!capturing) CUDA_TRY(c, cudaDeviceSynchronize());
-  if (c->cfg.residency == GRASS_RESIDENCY_STEP) {  // ring hazards: all earlier copies are complete
-    std::fill(c->layer_done_valid.begin(), c->layer_done_valid.end(), 0);
-    std::fill(c->slot_used.begin(), c->slot_used.end(), 0);
+  if (!capturing && !c->ever_captured_offload) return GRASS_OK;
+  if (capturing || c->captured_offload) {
+    if (!capturing) CUDA_TRY(c, cudaDeviceSynchronize());
+    if (c->cfg.residency == GRASS_RESIDENCY_STEP) {  // ring hazards: all earlier copies are complete
+      std::fill(c->layer_done_valid.begin(), c->layer_done_valid.end(), 0);
+      std::fill(c->slot_used.begin(), c->slot_used.end(), 0);
+    }
+    c->captured_offload = capturing;
   }
-  c->captured_offload = capturing;
-  if (capturing && c->cfg.overlap) {
+  if (capturing) c->ever_captured_offload = true;
+  if (c->cfg.overlap) {
     cudaEvent_t e = take_event(c);
     if (!e) return c->fail(GRASS_E_CUDA, "cudaEventCreate failed");
     CUDA_TRY(c, cudaEventRecord(e, st));
@@ -100,12 +111,11 @@ grass_status mgn_accumulate_impl(grass_ctx* c, bool bf16_call, const int32_t* id
     // N1 of layer j+1 on the comm stream overlaps K1 of layer j
     const int nact = (int)order.size();
     if ((s = comm_begin(c, st)) != GRASS_OK) return s;
-    if ((s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
+    if ((s = comm_rs(c, 0, grads[order[0]], ids[order[0]])) != GRASS_OK) return s;
     for (int j = 0; j < nact; ++j) {
       const int l = ids[order[j]];
       if (j + 1 < nact) {
-        const int l1 = ids[order[j + 1]];
-        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
+        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], ids[order[j + 1]])) != GRASS_OK) return s;
       }
       if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
       Batch b = make_batch(c, kFinalizeShard);
@@ -190,9 +200,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     } else {
       for (int j = 0; j < nact; ++j) {
         const int i = order[j], l = ids[i];
-        if (!c->comm.reduce_scatter_sum(grads[i], gs_slot(c, j), (size_t)c->shard_len[l], c->bf16, st, &c->err))
-          return GRASS_E_NCCL;
-        c->launches++;
+        if ((s = comm_exchange(c, grads[i], l, gs_slot(c, j), st)) != GRASS_OK) return s;
         Batch b1 = make_batch(c, kFinalizeShard);
         Seg sg = range_seg(c, l, gs_slot(c, j), 0, c->shard_len[l]);
         sg.out_slot = j;
@@ -238,7 +246,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
   Batch b = make_batch(c, mode);
   if (sharded) {
     if ((s = comm_begin(c, st)) != GRASS_OK) return s;
-    if (!clip && (s = comm_rs(c, 0, grads[order[0]], c->shard_len[ids[order[0]]])) != GRASS_OK) return s;
+    if (!clip && (s = comm_rs(c, 0, grads[order[0]], ids[order[0]])) != GRASS_OK) return s;
   }
   for (int j = 0; j < nact; ++j) {
     const int i = order[j], l = ids[i];
@@ -251,14 +259,13 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     if (p2p) {
       g = elem(grads[i], off, c->esz);  // this rank's range (the kernel sums every rank's via Seg::gpeer)
     } else if (sharded && clip) {
-      g = gs_slot(c, j);  // averaged in pass 1
+      g = gs_slot(c, j);  // exchanged in pass 1 (the kernels sum the slices)
     } else if (sharded) {
       if (j + 1 < nact) {  // N1 of the next layer overlaps this layer's update
-        const int l1 = ids[order[j + 1]];
-        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], c->shard_len[l1])) != GRASS_OK) return s;
+        if ((s = comm_rs(c, j + 1, grads[order[j + 1]], ids[order[j + 1]])) != GRASS_OK) return s;
       }
       if ((s = comm_wait_rs(c, j, st)) != GRASS_OK) return s;
-      g = rs_slot(c, j);  // shard-local gradient: index 0 = element `off`
+      g = rs_slot(c, j);  // the W ranks' slices of this rank's shard (summed by the kernel)
     }
     void* param = elem(params[i], off, c->esz);  // this rank's range of the layer
     Seg base = range_seg(c, l, g, 0, len);

@@ -26,8 +26,9 @@
 // GRASS_NORM_TPS_BF16, GRASS_NORM_STAGES, GRASS_P2P_NORM_TPS,
 // GRASS_UPD_GRID_SUB, GRASS_NORM_GRID_SUB, GRASS_L2_PREFETCH_{NORM,UPD},
 // GRASS_UNIT_BLOCK, GRASS_BF16_MAP8, GRASS_BF16_FP64_SQ, GRASS_BF16_SQ_PAIR,
-// GRASS_K1_TILE_REDUCE; GRASS_MUTANT=k plants mistake k
-// (tools/kernel_mutation.py).
+// GRASS_K1_TILE_REDUCE.  The mutation check of the GPU tests
+// (tools/kernel_mutation.py) plants its mistakes into a patched copy of this
+// source; the product source carries none.
 //
 // The tile partial (grass_internal.h) is a FIXED function of the tile's data:
 // consumer thread t owns elements (q*kThreads + t)*4 + j, j = 0..3, q = 0..
@@ -41,6 +42,7 @@
 #include <atomic>
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "grass_internal.h"
 
@@ -49,13 +51,6 @@ namespace {
 
 constexpr int kConsumerWarps = kThreads / 32;  // 16
 
-// Mutation check of the GPU parity tests (tools/kernel_mutation.py): a
-// variant built with -DGRASS_MUTANT=k plants mistake k; 0 (the product) plants
-// nothing — every `kMutant == k` test below is a compile-time constant.
-#ifndef GRASS_MUTANT
-#define GRASS_MUTANT 0
-#endif
-constexpr int kMutant = GRASS_MUTANT;
 constexpr int kStreamThreads = kThreads + 32;  // + 1 producer warp
 
 __device__ __forceinline__ double warp_sum(double x) {
@@ -65,29 +60,40 @@ __device__ __forceinline__ double warp_sum(double x) {
 }
 
 // warp_sum of N <= 16 per-lane values at once (one per tile of a unit): a
-// transposed butterfly.  At offset o every lane keeps half of its values and
-// trades the other half with lane ^ o, so each value is summed by the same
-// pairs of lane groups as warp_sum (level o adds the groups of lanes i and
-// i + o; IEEE addition is commutative), i.e. every result is bit-identical to
-// warp_sum of that value — for 16 + 15 exchanged values instead of 5N.
-// Lane i returns the sum of value (i >> 1) & 15 (valid for (i >> 1) < N).
+// transposed butterfly over C = next power of two >= N slots, with the values
+// PRE-PERMUTED per lane: slot t of lane L holds tile t ^ m(L), m(L) = (L >>
+// (5 - log2 C)) & (C - 1) (the caller reads its tiles in that order; tiles
+// >= N are 0).  At the first log2(C) offsets o = 16, 8, ... every lane keeps
+// the lower half of its slots and adds the partner's upper half, which holds
+// the same tiles (the partner's m differs exactly in the bit of this level),
+// so no lane-dependent selects are needed; the remaining offsets are a plain
+// butterfly on the one slot left.  Each tile is summed by the same pairs of
+// lane groups as warp_sum (level o adds the groups of lanes i and i + o; IEEE
+// addition is commutative): every result is bit-identical to warp_sum of that
+// tile, for C - 1 + 5 - log2(C) exchanges instead of 5N.  Lane L ends with the
+// sum of tile m(L): *slot = m(L) in the lowest lane of each group holding it
+// (and < N), else -1.
 template <int N>
-__device__ __forceinline__ double warp_sum_multi(const double (&in)[N], int lane) {
+struct MultiSlots {
   static_assert(N >= 1 && N <= 16, "one value per tile of a unit");
-  double v[16];
+  static constexpr int C = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : 16;
+  static constexpr int LOG = C == 1 ? 0 : C == 2 ? 1 : C == 4 ? 2 : C == 8 ? 3 : 4;
+  static constexpr int SHIFT = 5 - LOG;
+};
+template <int N>
+__device__ __forceinline__ double warp_sum_perm(double (&w)[MultiSlots<N>::C], int lane, int* slot) {
+  constexpr int C = MultiSlots<N>::C;
 #pragma unroll
-  for (int t = 0; t < 16; ++t) v[t] = t < N ? in[t] : 0.0;
+  for (int c = C, o = 16; c > 1; c >>= 1, o >>= 1) {
 #pragma unroll
-  for (int c = 16, o = 16; c > 1; c >>= 1, o >>= 1) {
-    const bool up = kMutant != 12 && (lane & o) != 0;  // this lane keeps the upper half (M12: never)
-#pragma unroll
-    for (int j = 0; j < c / 2; ++j) {
-      const double send = up ? v[j] : v[j + c / 2];
-      const double keep = up ? v[j + c / 2] : v[j];
-      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
+    for (int j = 0; j < c / 2; ++j) w[j] = w[j] + __shfl_xor_sync(0xffffffffu, w[j + c / 2], o);
   }
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+#pragma unroll
+  for (int o = 16 >> MultiSlots<N>::LOG; o > 0; o >>= 1) w[0] += __shfl_xor_sync(0xffffffffu, w[0], o);
+  constexpr int SH = MultiSlots<N>::SHIFT;
+  const int idx = (lane >> SH) & (C - 1);
+  *slot = ((lane & ((1 << SH) - 1)) == 0 && idx < N) ? idx : -1;
+  return w[0];
 }
 
 struct AdamScalars {
@@ -109,7 +115,7 @@ __device__ __forceinline__ void adamw1(float g, float& th, float& m, float& v,
   return;
 #endif
   g *= s.cf;  // exact when cf == 1
-  const float t1 = kMutant == 1 ? th : th * s.decay;  // M1: weight decay dropped
+  const float t1 = th * s.decay;
   const float m1 = fmaf(s.b1, m, s.omb1 * g);
   const float v1 = fmaf(s.b2, v, (s.omb2 * g) * g);
 #ifdef GRASS_IEEE_MATH
@@ -118,7 +124,7 @@ __device__ __forceinline__ void adamw1(float g, float& th, float& m, float& v,
 #else
   float sq;
   asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(v1));
-  const float den = fmaf(sq, kMutant == 2 ? 1.0f : s.inv_bc2s, s.eps);  // M2: no bc2
+  const float den = fmaf(sq, s.inv_bc2s, s.eps);
   th = fmaf(-s.step, __fdividef(m1, den), t1);
 #endif
   m = m1;
@@ -247,7 +253,7 @@ __device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, 
         st.S[sg.layer] += sqrt(ss / (double)sg.layer_numel);  // Eq. 2 inner term
         st.c[sg.layer] += 1;
       } else {
-        if (kMutant != 11) atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins (M11: not flagged)
+        atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins
       }
     } else if (mode == kFinalizeShard) {
       st.shard_ss[sg.out_slot] = ss;
@@ -385,13 +391,11 @@ __global__ void grass_p2p_selftest_kernel(const __grid_constant__ P2PSelftestArg
       if (rows[k] != round * 1000.0 + r * 10.0 + j) atomicAdd(t.mismatches, 1ull);
     }
     __syncthreads();
-#ifndef GRASS_SELFTEST_MUTANT_NO_START  // mutation check of the self-test itself
     a.which = 0;  // start barrier: every rank has read its rows of this round
     const int n_save = a.n;
     a.n = 0;
     p2p_sync_cta(a);
     a.n = n_save;
-#endif
   }
 }
 
@@ -400,7 +404,7 @@ __global__ void grass_step_prologue_kernel(const __grid_constant__ PrologueArgs 
   if (j >= a.n) return;
   const int l = a.layer[j];
   const long long t = st.t[l] + 1;
-  if (kMutant != 8) st.t[l] = t;  // M8: step count not advanced
+  st.t[l] = t;
   const double lr = a.lr_ptr ? (double)*a.lr_ptr : (double)a.lr;
   const double bc1 = 1.0 - pow(a.beta1, (double)t);
   const double bc2 = 1.0 - pow(a.beta2, (double)t);
@@ -434,11 +438,15 @@ __global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const
 constexpr int kUpdTPS = 1, kUpdStages = GRASS_UPD_STAGES;  // 4 arrays x 16 KiB per stage -> 128 KiB ring
 constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 96 KiB x 2 -> 192 KiB
 #ifndef GRASS_NORM_TPS_BF16
-#define GRASS_NORM_TPS_BF16 12  // 96 KiB units like fp32 (+17% over 6 tiles, profiles/r01_variants_bf16_k1_tps.json)
+#define GRASS_NORM_TPS_BF16 8  // 64 KiB units x 3 stages (a power of two: the all-tiles reduction has no empty slots)
 #endif
 constexpr int kNormTPSBf16 = GRASS_NORM_TPS_BF16;  // bf16 probing: tiles per unit (2 B/element)
+#ifndef GRASS_NORM_STAGES_BF16
+#define GRASS_NORM_STAGES_BF16 3
+#endif
+constexpr int kNormStagesBf16 = GRASS_NORM_STAGES_BF16;
 #ifndef GRASS_P2P_NORM_TPS
-#define GRASS_P2P_NORM_TPS 6  // 2 x 96 KiB gradient slots (4.1 vs 5.1 ms for 3, profiles/r01_variants_p2p_norm_tps_multi.json)
+#define GRASS_P2P_NORM_TPS 4  // 3 x 64 KiB fp32 / 6 x 32 KiB bf16 gradient slots: 6 tiles spill at the 96-register limit
 #endif
 constexpr int kP2PNormTPS = GRASS_P2P_NORM_TPS;  // P2P probing: tiles per gradient-ring slot
 
@@ -483,7 +491,7 @@ cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int gr
   }
   if (b.bf16)
     return update ? launch_stream<true, kUpdTPS, kUpdStages, true>(b, st, grid, s)
-                  : launch_stream<false, kNormTPSBf16, kNormStages, true>(b, st, grid, s);
+                  : launch_stream<false, kNormTPSBf16, kNormStagesBf16, true>(b, st, grid, s);
   return update ? launch_stream<true, kUpdTPS, kUpdStages, false>(b, st, grid, s)
                 : launch_stream<false, kNormTPS, kNormStages, false>(b, st, grid, s);
 }

@@ -51,7 +51,6 @@ struct StageLayout {
 
 __device__ __forceinline__ float bf2f(uint32_t b) { return __uint_as_float(b << 16); }
 __device__ __forceinline__ uint32_t f2bf(float f) {
-  if (kMutant == 7) return __float_as_uint(f) >> 16;  // M7: truncation instead of RNE
   return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 __device__ __forceinline__ float4 unpack_bf16x4(uint2 u) {
@@ -70,59 +69,98 @@ __device__ __forceinline__ float4 stage_g4(const char* stg, int e) {
   return *reinterpret_cast<const float4*>(stg + 4 * e);
 }
 // Element (relative to the unit) of consumer thread `tid`'s vector q in tile
-// k — the fixed map of the norm decomposition (grass_internal.h).  A/B knob
-// GRASS_BF16_MAP8: bf16 threads own 8 ADJACENT elements (one 16-byte read).
-#ifndef GRASS_BF16_MAP8
-#define GRASS_BF16_MAP8 0
-#endif
-template <bool BF16>
+// k — the fixed map of the norm decomposition (grass_internal.h).
 __device__ __forceinline__ int tile_elem(int k, int q, int tid) {
-  if (BF16 && GRASS_BF16_MAP8) return k * (int)kTile + tid * 2 * kVec + q * kVec;
   return k * (int)kTile + (q * kThreads + tid) * kVec;
 }
 template <bool BF16>
 __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
   return BF16 ? bf2f(sg.g16[idx]) : sg.g[idx];
 }
-// Eq. 2 squared-norm accumulation of a thread's 4 gradient values into
-// acc[0..3] (fp64).  fp32 gradients: every square exact in fp64.  bf16
-// gradients: a bf16 value's square (<= 16 significant bits) is exact in fp32,
-// so the 4 squares are summed in fp32 (three roundings, <= 3 * 2^-24 relative;
-// one more when a DP scale gs != 1 is applied) and widened once — a quarter of
-// the fp32->fp64 conversions and fp64 adds of per-element fp64 squares, which
-// held the 2 B/param probe ~20 % above its no-math time (profiles/
-// r01_variants_bf16_*).  All terms are >= 0, so the relative error of the sum
-// stays <= 4 * 2^-24 = 2.4e-7, inside the 1e-6 bar; integer-valued
-// gradients of magnitude < 2048 stay exact (sums < 2^24).  A/B knobs:
-// GRASS_BF16_FP64_SQ=1 per-element fp64 squares, GRASS_BF16_SQ_PAIR=1 pairs.
-#ifndef GRASS_K1_TILE_REDUCE  // A/B: K1 full units reduce tile by tile (warp_sum per tile)
-#define GRASS_K1_TILE_REDUCE 0
-#endif
-#ifndef GRASS_BF16_FP64_SQ
-#define GRASS_BF16_FP64_SQ 0
-#endif
-#ifndef GRASS_BF16_SQ_PAIR
-#define GRASS_BF16_SQ_PAIR 0
+
+// Eq. 2: the value of one consumer thread in one tile — the sum of the squares
+// of its kUnroll x 4 gradient values g[q].{x,y,z,w} (elements (q*kThreads +
+// t)*4 + j; an element beyond a ragged end is 0 and adds nothing).
+//  * fp32 gradients: every square is exact in fp64; acc_j = fma chains over q,
+//    value (acc_0 + acc_1) + (acc_2 + acc_3).
+//  * bf16 gradients: a bf16 value has 8 significant bits, so its square is
+//    exact in fp32; the 8 squares are summed in fp32 in element order (one FMUL
+//    + 7 FFMA: at most 7 roundings of a sum of non-negative terms, <= 7 * 2^-24
+//    = 4.2e-7 relative, inside the 1e-6 bar) and widened ONCE — one conversion
+//    per 8 elements instead of per element, which held the 2 B/param probe
+//    above its no-math time (profiles/r01_variants_bf16_*).  Integer-valued
+//    gradients stay exact while the sum is < 2^24.  The fp32 chain is only
+//    used where it cannot underflow or overflow: a sum below 2^-100
+//    (squares of magnitude < 2^-134 lose bits as fp32 subnormals, and < 2^-150
+//    vanish) or above FLT_MAX (|g| > ~1.8e19) — and a NaN — takes the exact
+//    fp64 squares instead, so the bound holds for every finite gradient and a
+//    non-finite one still yields a non-finite norm.
+#ifndef GRASS_BF16_GUARD  // A/B only: 0 = no exact fallback (wrong for tiny / huge gradients)
+#define GRASS_BF16_GUARD 1
 #endif
 template <bool BF16>
-__device__ __forceinline__ void sq_acc4(double (&acc)[kVec], float4 g) {
-  if (BF16 && !GRASS_BF16_FP64_SQ && !GRASS_BF16_SQ_PAIR) {
-    const float w2 = kMutant == 13 ? 0.f : g.w;  // M13: the 4th square of the fp32 sum dropped
-    acc[0] += (double)__fmaf_rn(w2, w2, __fmaf_rn(g.z, g.z, __fmaf_rn(g.y, g.y, __fmul_rn(g.x, g.x))));
-  } else if (BF16 && !GRASS_BF16_FP64_SQ) {
-    acc[0] += (double)__fmaf_rn(g.y, g.y, __fmul_rn(g.x, g.x));
-    acc[1] += (double)__fmaf_rn(g.w, g.w, __fmul_rn(g.z, g.z));
-  } else {
-    acc[0] = fma((double)g.x, (double)g.x, acc[0]);
-    acc[1] = fma((double)g.y, (double)g.y, acc[1]);
-    acc[2] = fma((double)g.z, (double)g.z, acc[2]);
-    acc[3] = fma((double)g.w, (double)g.w, acc[3]);
+__device__ __forceinline__ double tile_value_exact(const float4 (&g)[kUnroll]) {
+  double a = 0.0;
+#pragma unroll
+  for (int q = 0; q < kUnroll; ++q) {
+    a = fma((double)g[q].x, (double)g[q].x, a);
+    a = fma((double)g[q].y, (double)g[q].y, a);
+    a = fma((double)g[q].z, (double)g[q].z, a);
+    a = fma((double)g[q].w, (double)g[q].w, a);
   }
+  return a;
+}
+// A bf16 8-square fp32 sum is used where it is in [2^-100, FLT_MAX] (see
+// above): one unsigned compare of the bits (false for 0, inf, NaN).
+__device__ __forceinline__ bool sq_sum_in_range(float s) {
+  return __float_as_uint(s) - 0x0D800000u <= 0x7F7FFFFFu - 0x0D800000u;
+}
+// The same fp32 chain straight from the packed bf16 words of a thread's two
+// 4-element vectors (element order x.lo, x.hi, y.lo, y.hi): FHFMA.BF16 — the
+// mixed-precision fma, bf16 operands taken as register halves, fp32
+// accumulate — computes RN(x*x + s) with the exact product, i.e. the bits of
+// __fmaf_rn on the widened values, with no unpack instructions.
+__device__ __forceinline__ float bf16_sq_acc(uint32_t w, float s) {
+  unsigned short lo, hi;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(w));
+  asm("fma.rn.f32.bf16 %0, %1, %1, %0;" : "+f"(s) : "h"(lo));
+  asm("fma.rn.f32.bf16 %0, %1, %1, %0;" : "+f"(s) : "h"(hi));
+  return s;
+}
+__device__ __forceinline__ float bf16_sq8(uint2 a, uint2 b) {
+  float s = 0.f;
+  s = bf16_sq_acc(a.x, s);
+  s = bf16_sq_acc(a.y, s);
+  s = bf16_sq_acc(b.x, s);
+  return bf16_sq_acc(b.y, s);
 }
 template <bool BF16>
-__device__ __forceinline__ void sq_acc1(double& a, float g) {  // ragged-tail element
-  if (BF16 && !GRASS_BF16_FP64_SQ) a += (double)__fmul_rn(g, g);
-  else a = fma((double)g, (double)g, a);
+__device__ __forceinline__ double tile_value(const float4 (&g)[kUnroll]) {
+  if (BF16) {
+    float s = __fmul_rn(g[0].x, g[0].x);
+    s = __fmaf_rn(g[0].y, g[0].y, s);
+    s = __fmaf_rn(g[0].z, g[0].z, s);
+    s = __fmaf_rn(g[0].w, g[0].w, s);
+#pragma unroll
+    for (int q = 1; q < kUnroll; ++q) {
+      s = __fmaf_rn(g[q].x, g[q].x, s);
+      s = __fmaf_rn(g[q].y, g[q].y, s);
+      s = __fmaf_rn(g[q].z, g[q].z, s);
+      const float w = g[q].w;
+      s = __fmaf_rn(w, w, s);
+    }
+    if (!GRASS_BF16_GUARD || sq_sum_in_range(s)) return (double)s;
+    return tile_value_exact<BF16>(g);
+  }
+  double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int q = 0; q < kUnroll; ++q) {
+    acc[0] = fma((double)g[q].x, (double)g[q].x, acc[0]);
+    acc[1] = fma((double)g[q].y, (double)g[q].y, acc[1]);
+    acc[2] = fma((double)g[q].z, (double)g[q].z, acc[2]);
+    acc[3] = fma((double)g[q].w, (double)g[q].w, acc[3]);
+  }
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 // P2P (Seg::gpeer): the gradient of a unit is the sum of the npeer ranks'
@@ -151,22 +189,20 @@ __device__ __forceinline__ float peer_g1(const void* const* gp, int npeer, int64
 }
 
 // Bulk-stores the results of one unit from its stage: master/theta, m, v
-// (and the bf16 parameter copy).  P2P: theta' (fp32) or the bf16 copy goes to
-// every rank's parameter buffer (this rank's included) over NVLink.
-template <bool BF16, bool P2P, class L>
-__device__ __forceinline__ void store_unit_t(const Seg& sg, int npeer, int64_t e0, uint32_t nv, const char* stg) {
+// (and the bf16 parameter copy).  ntp > 0 (P2P): theta' (fp32) or the bf16
+// copy goes to every rank's parameter buffer (this rank's included) over
+// NVLink; ntp = 0: to this rank's buffers only.
+template <bool BF16, class L>
+__device__ __forceinline__ void store_unit_t(const Seg& sg, int ntp, int64_t e0, uint32_t nv, const char* stg) {
   if (nv) {
-    if (BF16 || !P2P) bulk_store(sg.theta + e0, stg + L::o_t, nv * 4u);
+    if (BF16 || ntp == 0) bulk_store(sg.theta + e0, stg + L::o_t, nv * 4u);
     bulk_store(sg.m + e0, stg + L::o_m, nv * 4u);
     bulk_store(sg.v + e0, stg + L::o_v, nv * 4u);
-    if (P2P) {
-      for (int q = 0; q < npeer - (kMutant == 9 ? 1 : 0); ++q) {  // M9: theta' not stored to the last rank
-        char* dst = static_cast<char*>(sg.tpeer[q]) + (sg.poff + e0) * (BF16 ? 2 : 4);
-        bulk_store(dst, stg + (BF16 ? L::o_tb : L::o_t), nv * (BF16 ? 2u : 4u));
-      }
-    } else if (BF16) {
-      bulk_store(sg.theta16 + e0, stg + L::o_tb, nv * 2u);
+    for (int q = 0; q < ntp; ++q) {
+      char* dst = static_cast<char*>(sg.tpeer[q]) + (sg.poff + e0) * (BF16 ? 2 : 4);
+      bulk_store(dst, stg + (BF16 ? L::o_tb : L::o_t), nv * (BF16 ? 2u : 4u));
     }
+    if (BF16 && ntp == 0) bulk_store(sg.theta16 + e0, stg + L::o_tb, nv * 2u);
     bulk_commit();
   }
 }
@@ -243,7 +279,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         if (kRing && i >= STAGES) {
           mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
           if (TS) {
-            store_unit_t<BF16, P2P, L>(b.seg[pend_s[stage]], b.npeer, pend_e0[stage], pend_nv[stage], stg);
+            store_unit_t<BF16, L>(b.seg[pend_s[stage]], P2P ? b.ntpeer : 0, pend_e0[stage], pend_nv[stage], stg);
             if (!L::SEP) bulk_wait_read_all();  // stage reusable again
           }
         }
@@ -258,7 +294,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           pend_nv[stage] = nv;
         }
         if (nv && (UPDATE || !P2P)) {
-          const bool init = BF16 && UPDATE && kMutant != 10 && st.init_now[sg.layer];  // M10: master never initialised
+          const bool init = BF16 && UPDATE && st.init_now[sg.layer];
           // P2P: the gradient slices go to the gradient ring (below)
           const uint32_t tx = (P2P ? 0u : nv * (uint32_t)L::GB) + (UPDATE ? nv * (init ? 2u : 4u) + 8u * nv : 0u);
           mbar_arrive_expect_tx(&full_bar[stage], tx);
@@ -298,7 +334,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
             if (gcount >= NG) mbar_wait(&gempty_bar[gsl], ((gcount / NG) & 1) ^ 1);
             mbar_arrive_expect_tx(&gfull_bar[gsl], nv * (uint32_t)L::GB);
             bulk_load(gring + (size_t)gsl * kGSlot,
-                      static_cast<const char*>(sg.gpeer[r]) + (sg.poff + e0) * L::GB, nv * (uint32_t)L::GB,
+                      static_cast<const char*>(sg.gpeer[r]) + (sg.gpoff + e0) * L::GB, nv * (uint32_t)L::GB,
                       &gfull_bar[gsl], pol);
           }
         }
@@ -312,12 +348,12 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         for (int j = (n_units > STAGES ? n_units - STAGES : 0); j < n_units; ++j) {
           const int stage = j % STAGES;
           mbar_wait(&empty_bar[stage], (j / STAGES) & 1);
-          store_unit_t<BF16, P2P, L>(b.seg[pend_s[stage]], b.npeer, pend_e0[stage], pend_nv[stage],
-                                     sbuf + (size_t)stage * L::bytes);
+          store_unit_t<BF16, L>(b.seg[pend_s[stage]], P2P ? b.ntpeer : 0, pend_e0[stage], pend_nv[stage],
+                                sbuf + (size_t)stage * L::bytes);
         }
         bulk_wait_all();
       }
-      if (P2P) {  // the peer writes are complete; order them before the end barrier's signal
+      if (P2P && b.ntpeer > 0) {  // the peer writes are complete; order them before the end barrier's signal
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __threadfence_system();
       }
@@ -327,7 +363,8 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
 
   // ------------------------------ consumers -------------------------------
   const float cf = (UPDATE && b.coef) ? *b.coef : 1.0f;
-  const float gs = kMutant == 5 ? 1.0f : b.gscale;  // DP: 1/world turns reduce-scattered sums into averages (M5: not)
+  const float gs = b.gscale;  // DP: 1/world turns the summed gradients into averages
+  const int ntp = P2P ? b.ntpeer : 0;  // ranks whose parameter buffers receive theta' (P2P)
   int s = 0, i = 0, gcount = 0;
   for (int u = unit_of(0, kUB); u < total; ++i, u = unit_of(i, kUB)) {
     const int stage = i % STAGES;
@@ -342,7 +379,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       sc.inv_bc2s = st.scal[3 * sg.layer + 2];
     }
     sc.cf = cf;
-    const bool init = BF16 && UPDATE && kMutant != 10 && st.init_now[sg.layer];
+    const bool init = BF16 && UPDATE && st.init_now[sg.layer];
     const int ui = u - unit_prefix[s];
     const int64_t e0 = (int64_t)ui * kUnit;
     const int ne = (int)min((int64_t)kUnit, sg.n - e0);
@@ -352,22 +389,28 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     const int64_t pe0 = P2P ? sg.poff + e0 : 0;  // full-layer index of the unit's element 0
     if (kRing) mbar_wait(&full_bar[stage], (i / STAGES) & 1);
     if (L::SEP) mbar_wait(&outfree_bar[stage], (i / STAGES) & 1);
+    // full norm-only units: slot t of this lane holds tile t ^ pm — the order
+    // in which warp_sum_perm keeps them (pm = the tile the lane ends with)
+    using MS = MultiSlots<TPS>;
+    const int pm = (!UPDATE && ne == kUnit) ? (lane >> MS::SHIFT) & (MS::C - 1) : 0;
     float4 gacc[P2P ? TPS : 1][kUnroll];  // P2P: this thread's summed gradient of the unit
     if (P2P && nv) {
+      static_assert(!P2P || UPDATE || MultiSlots<TPS>::C == TPS, "P2P norm units: a power-of-two tile count");
       for (int r = 0; r < b.npeer; ++r, ++gcount) {
         const int gsl = gcount % NG;
         mbar_wait(&gfull_bar[gsl], (gcount / NG) & 1);
 #pragma unroll
-        for (int k = 0; k < (P2P ? TPS : 1); ++k) {
+        for (int k0 = 0; k0 < (P2P ? TPS : 1); ++k0) {
+          const int k = k0 ^ pm;  // gacc[k0] holds tile k
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
-            const int e = tile_elem<BF16>(k, q, tid);
+            const int e = tile_elem(k, q, tid);
             if (e < nv) {
               const float4 x = stage_g4<BF16>(gring + (size_t)gsl * kGSlot, e);
               if (r == 0) {
-                gacc[k][q] = x;
-              } else if (!(kMutant == 6 && r == b.npeer - 1)) {  // M6: last rank's slice dropped
-                gacc[k][q].x += x.x; gacc[k][q].y += x.y; gacc[k][q].z += x.z; gacc[k][q].w += x.w;
+                gacc[k0][q] = x;
+              } else {
+                gacc[k0][q].x += x.x; gacc[k0][q].y += x.y; gacc[k0][q].z += x.z; gacc[k0][q].w += x.w;
               }
             }
           }
@@ -376,75 +419,96 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         if (lane == 0) mbar_arrive(&gempty_bar[gsl]);
       }
     }
+    bool released = false;  // this warp has handed the stage back already
     if (!UPDATE && !P2P && ne == kUnit) {
-      // Full unit of the norm-only stream: branch-free, every shared-memory
-      // read issued before the math.  Same element map and accumulation order
-      // as the guarded path below.
-      constexpr int kPre = (TPS < 3 ? TPS : 3);  // tiles whose reads are issued ahead
-      float4 g4[kPre][kUnroll];
+      // Full unit of the norm-only stream: each lane reads its tiles in the
+      // order warp_sum_perm keeps them (slot t = tile t ^ pm), so the
+      // all-tiles reduction needs no selects.  Same element map and tile
+      // values as the guarded path below.
+      double w[MS::C];
+      bool done = false;
+      if constexpr (BF16 && MS::C == TPS) {
+        if (gs == 1.f) {
+          // bf16 fast path: the unit's data to registers, the 8-square fp32
+          // sums with FHFMA.BF16 straight from the packed words; if every sum
+          // of the warp is in fp32's normal range (it always is outside
+          // pathological gradients), the stage is handed back at once — the
+          // producer refills it while the widening and the reduction run —
+          // else the generic path below (exact fallback) re-reads the stage.
+          uint2 raw[TPS][kUnroll];
 #pragma unroll
-      for (int k = 0; k < kPre; ++k)
+          for (int t = 0; t < TPS; ++t)
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q)
-          g4[k][q] = stage_g4<BF16>(stg + L::off_g, tile_elem<BF16>(k, q, tid));
-      double tv[TPS];  // this thread's value of each tile
+            for (int q = 0; q < kUnroll; ++q)
+              raw[t][q] = *reinterpret_cast<const uint2*>(stg + L::off_g + 2 * tile_elem(t ^ pm, q, tid));
+          float s8[TPS];
+          uint32_t lo = 0xffffffffu, hi = 0u;
 #pragma unroll
-      for (int k = 0; k < TPS; ++k) {
-        double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
-        float4 cur[kUnroll];
+          for (int t = 0; t < TPS; ++t) {
+            s8[t] = bf16_sq8(raw[t][0], raw[t][1]);
+            lo = min(lo, __float_as_uint(s8[t]));
+            hi = max(hi, __float_as_uint(s8[t]));
+          }
+          const bool ok = !GRASS_BF16_GUARD || (sq_sum_in_range(__uint_as_float(lo)) && sq_sum_in_range(__uint_as_float(hi)));
+          if (__all_sync(0xffffffffu, ok)) {
+            if (lane == 0) mbar_arrive(&empty_bar[stage]);
+            released = true;
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q) cur[q] = g4[k % kPre][q];
-        if (gs != 1.f) {  // DP average (warp-uniform; x * 1 == x, so skipping it is exact)
-#pragma unroll
-          for (int q = 0; q < kUnroll; ++q) cur[q] = scale4(cur[q], gs);
-        }
-        if (k + kPre < TPS) {  // refill the slot just consumed
-#pragma unroll
-          for (int q = 0; q < kUnroll; ++q)
-            g4[k % kPre][q] = stage_g4<BF16>(stg + L::off_g, tile_elem<BF16>(k + kPre, q, tid));
-        }
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-#ifdef GRASS_K1_NOMATH  // A/B only: the same data movement with trivial arithmetic (speed of light)
-          acc[0] += fabsf(cur[q].x) + fabsf(cur[q].y) + fabsf(cur[q].z) + fabsf(cur[q].w);
-#else
-          sq_acc4<BF16>(acc, cur[q]);
-#endif
-        }
-        tv[k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-        if (GRASS_K1_TILE_REDUCE) {
-          const double t = warp_sum(tv[k]);
-          if (lane == 0) red[i & 1][k][warp] = t;
+            for (int t = 0; t < TPS; ++t) w[t] = (double)s8[t];
+            done = true;
+          }
         }
       }
-      if (!GRASS_K1_TILE_REDUCE) {  // all tiles' warp sums at once (bit-identical to warp_sum)
-        const double t = warp_sum_multi<TPS>(tv, lane);
-        if ((lane & 1) == 0 && (lane >> 1) < TPS) red[i & 1][lane >> 1][warp] = t;
+      if (!done) {
+#pragma unroll
+        for (int t = 0; t < MS::C; ++t) {
+          const int k = t ^ pm;
+          w[t] = 0.0;
+          if (MS::C == TPS || k < TPS) {
+            float4 g4[kUnroll];
+#pragma unroll
+            for (int q = 0; q < kUnroll; ++q) g4[q] = stage_g4<BF16>(stg + L::off_g, tile_elem(k, q, tid));
+            if (gs != 1.f) {  // DP average (warp-uniform; x * 1 == x, so skipping it is exact)
+#pragma unroll
+              for (int q = 0; q < kUnroll; ++q) g4[q] = scale4(g4[q], gs);
+            }
+            w[t] = tile_value<BF16>(g4);
+          }
+        }
       }
-    } else if (!UPDATE && P2P && ne == kUnit && !GRASS_K1_TILE_REDUCE) {
+      int slot;
+      const double tsum = warp_sum_perm<TPS>(w, lane, &slot);  // all tiles at once (bit-identical to warp_sum)
+      if (slot >= 0) red[i & 1][slot][warp] = tsum;
+    } else if (!UPDATE && P2P && ne == kUnit) {
       // Full unit of the P2P norm stream: the ranks' summed gradient is in
-      // gacc; same element map and accumulation order as the guarded path.
-      double tv[TPS];
+      // gacc (slot t = tile t ^ pm); same element map and tile values as the
+      // guarded path.
+      double w[MS::C];  // (P2P norm units have C == TPS tiles)
 #pragma unroll
-      for (int k = 0; k < TPS; ++k) {
-        double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
+      for (int t = 0; t < MS::C; ++t) {
+        w[t] = 0.0;
+        if (t < TPS) {
+          float4 g4[kUnroll];
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q) sq_acc4<BF16>(acc, gs != 1.f ? scale4(gacc[P2P ? k : 0][q], gs) : gacc[P2P ? k : 0][q]);
-        tv[k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+          for (int q = 0; q < kUnroll; ++q) g4[q] = gs != 1.f ? scale4(gacc[P2P ? t : 0][q], gs) : gacc[P2P ? t : 0][q];
+          w[t] = tile_value<BF16>(g4);
+        }
       }
-      const double t = warp_sum_multi<TPS>(tv, lane);
-      if ((lane & 1) == 0 && (lane >> 1) < TPS) red[i & 1][lane >> 1][warp] = t;
+      int slot;
+      const double tsum = warp_sum_perm<TPS>(w, lane, &slot);
+      if (slot >= 0) red[i & 1][slot][warp] = tsum;
     } else {
 #pragma unroll
       for (int k = 0; k < TPS; ++k) {
         if (k < ntiles) {
-          double acc[kVec] = {0.0, 0.0, 0.0, 0.0};
+          float4 gq[kUnroll];  // this thread's gradient values of the tile (0 beyond a ragged end)
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
-            const int e = tile_elem<BF16>(k, q, tid);  // relative to e0
+            gq[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int e = tile_elem(k, q, tid);  // relative to e0
             if (e < nv) {
               const float4 g4 = scale4(P2P ? gacc[P2P ? k : 0][q] : stage_g4<BF16>(stg + L::off_g, e), gs);
-              sq_acc4<BF16>(acc, g4);
+              gq[q] = g4;
               if (UPDATE) {
                 float4 t4 = init ? unpack_bf16x4(*reinterpret_cast<const uint2*>(stg + L::off_tb + 2 * e))
                                  : *reinterpret_cast<const float4*>(stg + L::off_t + 4 * e);
@@ -460,67 +524,63 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
                   *reinterpret_cast<float4*>(stg + L::o_v + 4 * e) = v4;
                   if (BF16) *reinterpret_cast<uint2*>(stg + L::o_tb + 2 * e) = pack_bf16x4(t4);
                 } else {
-                  if (BF16 || !P2P) st_stream(sg.theta + e0 + e, t4);
+                  if (BF16 || ntp == 0) st_stream(sg.theta + e0 + e, t4);
                   st_stream(sg.m + e0 + e, m4);
                   st_stream(sg.v + e0 + e, v4);
-                  if (P2P) {
 #pragma unroll
-                    for (int q = 0; q < kMaxPeers; ++q) {
-                      if (q >= b.npeer) break;
-                      if (BF16)
-                        *reinterpret_cast<uint2*>(static_cast<uint16_t*>(sg.tpeer[q]) + pe0 + e) = pack_bf16x4(t4);
-                      else
-                        st_stream(static_cast<float*>(sg.tpeer[q]) + pe0 + e, t4);
-                    }
-                  } else if (BF16) {
-                    *reinterpret_cast<uint2*>(sg.theta16 + e0 + e) = pack_bf16x4(t4);
+                  for (int q2 = 0; q2 < kMaxPeers; ++q2) {
+                    if (q2 >= ntp) break;
+                    if (BF16)
+                      *reinterpret_cast<uint2*>(static_cast<uint16_t*>(sg.tpeer[q2]) + pe0 + e) = pack_bf16x4(t4);
+                    else
+                      st_stream(static_cast<float*>(sg.tpeer[q2]) + pe0 + e, t4);
                   }
+                  if (BF16 && ntp == 0) *reinterpret_cast<uint2*>(sg.theta16 + e0 + e) = pack_bf16x4(t4);
                 }
               }
             } else if (e < ne) {
+              float gt[kVec] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
               for (int j = 0; j < kVec; ++j) {
-                if (e + j < ne - (kMutant == 4 ? 1 : 0)) {  // M4: last tail element skipped
+                if (e + j < ne) {
                   const int64_t idx = e0 + e + j;
-                  const float g = (P2P ? peer_g1<BF16>(sg.gpeer, b.npeer, pe0 + e + j) : seg_g<BF16>(sg, idx)) * gs;
-                  sq_acc1<BF16>(acc[j], g);
+                  const float g = (P2P ? peer_g1<BF16>(sg.gpeer, b.npeer, sg.gpoff + e0 + e + j) : seg_g<BF16>(sg, idx)) * gs;
+                  gt[j] = g;
                   if (UPDATE) {
                     float th = init ? bf2f(sg.theta16[idx]) : sg.theta[idx];
                     float m = sg.m[idx], v = sg.v[idx];
                     adamw1(g, th, m, v, sc);
-                    sg.theta[idx] = th;  // P2P fp32: this rank's own buffer (also in tp below)
+                    if (BF16 || ntp == 0) sg.theta[idx] = th;
                     sg.m[idx] = m;
                     sg.v[idx] = v;
-                    if (P2P) {
 #pragma unroll
-                      for (int q = 0; q < kMaxPeers; ++q) {
-                        if (q >= b.npeer) break;
-                        if (BF16)
-                          static_cast<uint16_t*>(sg.tpeer[q])[pe0 + e + j] = (uint16_t)f2bf(th);
-                        else
-                          static_cast<float*>(sg.tpeer[q])[pe0 + e + j] = th;
-                      }
-                    } else if (BF16) {
-                      sg.theta16[idx] = (uint16_t)f2bf(th);
+                    for (int q2 = 0; q2 < kMaxPeers; ++q2) {
+                      if (q2 >= ntp) break;
+                      if (BF16)
+                        static_cast<uint16_t*>(sg.tpeer[q2])[pe0 + e + j] = (uint16_t)f2bf(th);
+                      else
+                        static_cast<float*>(sg.tpeer[q2])[pe0 + e + j] = th;
                     }
+                    if (BF16 && ntp == 0) sg.theta16[idx] = (uint16_t)f2bf(th);
                   }
                 }
               }
+              gq[q] = make_float4(gt[0], gt[1], gt[2], gt[3]);
             }
           }
-          const double t = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+          const double t = warp_sum(tile_value<BF16>(gq));
           if (lane == 0) red[i & 1][k][warp] = t;
         }
       }
     }
     if (UPDATE && kTmaStore) fence_proxy_async_smem();  // results visible to the bulk store
     __syncwarp();
-    if (kRing && lane == 0) mbar_arrive(&empty_bar[stage]);  // this warp is done with the stage
+    if (kRing && !released && lane == 0) mbar_arrive(&empty_bar[stage]);  // this warp is done with the stage
     consumer_sync();
     if (tid < ntiles) {  // lane k of warp 0 finishes tile k (warp sums in ascending order)
       double p = 0.0;
 #pragma unroll
-      for (int w = 0; w < kConsumerWarps - (kMutant == 3 ? 1 : 0); ++w) p += red[i & 1][tid][w];  // M3
+      for (int w = 0; w < kConsumerWarps; ++w) p += red[i & 1][tid][w];
       st.partials[sg.part_index + (int64_t)ui * TPS + tid] = p;
     }
     if (tid == 0) seg_done[s] += ntiles;

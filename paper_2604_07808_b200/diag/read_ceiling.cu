@@ -1,0 +1,123 @@
+// read_ceiling.cu — measurement only (bench.py `probe` leg), not part of the
+// hot path: the READ-ONLY HBM ceiling of this B200, the denominator of the
+// probing kernel K1 (a pure read, 4 or 2 B/param), which the
+// 1R1W copy peak of MEASURED_PEAKS.json does not bound.
+//
+// Two hand-written streaming reads of one buffer, each with a trivial
+// accumulate that keeps every load alive:
+//   mode 0  LDG.128: ld.global.nc.L1::no_allocate.v4, 8 independent loads in
+//           flight per thread, grid-stride, `grid` CTAs x 512 threads;
+//   mode 1  TMA bulk: one CTA per SM (`grid` CTAs), one producer thread
+//           streams `unit`-byte pieces HBM -> shared memory with
+//           cp.async.bulk into a ring of `stages` slots (mbarrier complete_tx),
+//           one consumer warp reads one word per slot and hands it back —
+//           K1's data movement with no arithmetic.
+// C ABI: grass_diag_read(ptr, bytes, mode, grid, unit, stages, sink, stream).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace {
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(512) read_ldg(const uint4* __restrict__ p, size_t n16,
+                                                unsigned long long* sink) {
+  uint32_t acc = 0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 7 * stride < n16; i += 8 * stride) {
+    uint4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = ld_stream(p + i + j * stride);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc ^= v[j].x ^ v[j].y ^ v[j].z ^ v[j].w;
+  }
+  for (; i < n16; i += stride) {
+    const uint4 v = ld_stream(p + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9E3779B9u) atomicAdd(sink, 1ull);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(64, 1) read_tma(const char* __restrict__ p, size_t bytes, uint32_t unit,
+                                                  int stages, unsigned long long* sink) {
+  extern __shared__ __align__(1024) char ring[];
+  __shared__ __align__(8) uint64_t full[16], empty[16];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const size_t units = bytes / unit;  // (the caller passes a multiple of unit)
+  if (tid == 0) {  // producer
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    int k = 0;
+    for (size_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+      const int s = k % stages;
+      if (k >= stages) {
+        const uint32_t par = ((k / stages) & 1) ^ 1;
+        asm volatile("{\n.reg .pred q;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W_%=;\n}\n" ::"r"(
+                         smem_u32(&empty[s])),
+                     "r"(par)
+                     : "memory");
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(unit)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+              smem_u32(ring + (size_t)s * unit)),
+          "l"(p + u * unit), "r"(unit), "r"(smem_u32(&full[s])), "l"(pol)
+          : "memory");
+    }
+  } else if (tid == 32) {  // consumer: one word per slot, then hand it back
+    uint32_t acc = 0;
+    int k = 0;
+    for (size_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+      const int s = k % stages;
+      const uint32_t par = (k / stages) & 1;
+      asm volatile("{\n.reg .pred q;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W_%=;\n}\n" ::"r"(
+                       smem_u32(&full[s])),
+                   "r"(par)
+                   : "memory");
+      acc ^= *reinterpret_cast<const volatile uint32_t*>(ring + (size_t)s * unit + (k & 255) * 4);
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+    }
+    if (acc == 0x9E3779B9u) atomicAdd(sink, 1ull);
+  }
+}
+
+}  // namespace
+
+extern "C" int grass_diag_read(const void* ptr, unsigned long long bytes, int mode, int grid, unsigned int unit,
+                               int stages, unsigned long long* sink, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!ptr || !sink || grid < 1 || reinterpret_cast<uintptr_t>(ptr) % 16 != 0) return (int)cudaErrorInvalidValue;
+  if (mode == 0) {
+    read_ldg<<<grid, 512, 0, s>>>(static_cast<const uint4*>(ptr), (size_t)bytes / 16, sink);
+  } else {
+    if (unit % 16 != 0 || stages < 1 || stages > 16 || (size_t)unit * stages > 227u * 1024u ||
+        bytes % unit != 0)
+      return (int)cudaErrorInvalidValue;
+    const size_t smem = (size_t)unit * stages;
+    cudaError_t e = cudaFuncSetAttribute(read_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    read_tma<<<grid, 64, smem, s>>>(static_cast<const char*>(ptr), (size_t)bytes, unit, stages, sink);
+  }
+  return (int)cudaGetLastError();
+}

@@ -59,3 +59,18 @@ def test_nvml_poll_rows_decode_reason_bits():
     assert all(len(r) == 6 for r in c.rows)
     s = c.summary()
     assert s["sm_max_mhz"] == 1965.0 and s["reasons"] == ["sw_power_cap"]
+
+
+def test_nvml_poll_without_max_clock_returns_unsampled():
+    """if NVML fails before the first sample the poll thread exits
+    without signalling `ready`, so __enter__ falls back to nvidia-smi instead
+    of timing a region with no clock record."""
+    class Broken(FakeNVML):
+        def nvmlDeviceGetMaxClockInfo(self, h, kind):
+            raise RuntimeError("NVML_ERROR_NOT_SUPPORTED")
+    c = bench.ClockSampler(0)
+    ready = threading.Event()
+    t = threading.Thread(target=c._nvml_poll, args=(None, Broken(), ready), daemon=True)
+    t.start()
+    t.join(2.0)
+    assert not t.is_alive() and not ready.is_set() and c.rows == []

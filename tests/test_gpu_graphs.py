@@ -208,6 +208,38 @@ def test_captured_offloaded_step_replays_equal_eager_steps(dtype, overlap):
     _same(eager, graph, pe, pg, [0, 1, 2])
 
 
+@pytest.mark.parametrize("residency", ["step", "period"])
+def test_offloaded_replays_interleaved_with_eager_steps(residency):
+    """capture -> replay -> eager -> replay -> eager -> ... with no host sync in
+    between: every eager offloaded call after a capture orders its
+    copy streams after the replays already on the caller stream, so no fetch
+    overwrites a ring slot a replay still reads and no write-back reads state
+    a replay still writes.  Layers of 8 Mi elements (32 MiB per state array)
+    keep each replay's copies in flight long enough for a missing fence to
+    show; the result must equal the same sequence of eager steps bit for bit."""
+    numel = [8 << 20, 8 << 20, 4096 * 3]
+    ids = [0, 1]
+    kw = dict(offload=True, chunk_elems=1 << 20, ring_slots=2)
+    if residency == "period":
+        kw.update(residency=G.RESIDENCY_PERIOD, cache_layers=3)
+    eager, graph, pe, pg, grads = _pair(numel, G.DTYPE_FP32, **kw)
+    if residency == "period":
+        for c in (eager, graph):
+            c.prefetch_layers(ids)
+    graph.sync()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        graph.step_layers(ids, [pg[l] for l in ids], [grads[l] for l in ids], 1e-3,
+                          stream=torch.cuda.current_stream())
+    other = [1, 2] if residency == "step" else [0, 1]   # period: stay within the cached set
+    for _ in range(4):
+        g.replay()
+        eager.step_layers(ids, [pe[l] for l in ids], [grads[l] for l in ids], 1e-3)
+        for c, p in ((eager, pe), (graph, pg)):
+            c.step_layers(other, [p[l] for l in other], [grads[l] for l in other], 1e-3)
+    _same(eager, graph, pe, pg, [0, 1, 2])
+
+
 def test_captured_nccl_offloaded_step_replays_equal_eager_steps():
     """NCCL data parallelism (1-rank communicator) with per-step offload,
     captured and replayed == eager."""

@@ -20,10 +20,20 @@ def warp_sum_down(x):
     return x[0]
 
 
+def slots(n):
+    """C = next power of two >= n (the kernel's MultiSlots<N>::C), its log2."""
+    c = 1
+    while c < n:
+        c *= 2
+    return c, c.bit_length() - 1
+
+
 def warp_sum_multi(vals, n):
-    """vals[lane][t], t < n.  Returns out[lane] as the kernel's lanes hold it."""
-    v = [[vals[l][t] if t < n else 0.0 for t in range(16)] for l in range(32)]
-    c, o = 16, 16
+    """vals[lane][t], t < n.  Returns out[lane] as the kernel's lanes hold it:
+    split levels at o = 16, 8, ... (log2 C of them), then a plain butterfly."""
+    C, LOG = slots(n)
+    v = [[vals[l][t] if t < n else 0.0 for t in range(C)] for l in range(32)]
+    c, o = C, 16
     while c > 1:
         new = [row[:] for row in v]
         for lane in range(32):
@@ -37,7 +47,20 @@ def warp_sum_multi(vals, n):
         v = new
         c //= 2
         o //= 2
-    return [v[lane][0] + v[lane ^ 1][0] for lane in range(32)]
+    x = [v[lane][0] for lane in range(32)]
+    o = 16 >> LOG
+    while o > 0:
+        x = [x[lane] + x[lane ^ o] for lane in range(32)]
+        o //= 2
+    return x
+
+
+def holder(lane, n):
+    """(tile index, writes?) of a lane after warp_sum_multi: the kernel's *slot."""
+    C, LOG = slots(n)
+    sh = 5 - LOG
+    idx = (lane >> sh) & (C - 1)
+    return idx, (lane & ((1 << sh) - 1)) == 0 and idx < n
 
 
 @pytest.mark.parametrize("n", list(range(1, 17)))
@@ -50,13 +73,14 @@ def test_multi_equals_per_tile_tree_bitwise(n):
         out = warp_sum_multi(vals, n)
         for t in range(n):
             want = warp_sum_down([vals[l][t] for l in range(32)])
-            lanes = [l for l in range(32) if (l >> 1) == t]      # the lanes that hold tile t
+            lanes = [l for l in range(32) if holder(l, n)[0] == t]     # the lanes that hold tile t
+            assert sum(holder(l, n)[1] for l in lanes) == 1            # exactly one writes it
             for l in lanes:
                 assert out[l] == want, (n, t, l)
 
 
 def test_multi_result_lane_map():
-    """Tile t's sum lands in lanes 2t and 2t + 1 (the kernel writes from the even one)."""
+    """N = 16: tile t's sum lands in lanes 2t and 2t + 1 (the kernel writes from the even one)."""
     vals = [[float(1 << l) * (t + 1) for t in range(16)] for l in range(32)]
     out = warp_sum_multi(vals, 16)
     for l in range(32):

@@ -1,51 +1,99 @@
-"""Mutation check of the GPU parity tests: libgrass variants built with
--DGRASS_MUTANT=k each plant one plausible kernel mistake (kernels.cu /
-stream_kernel.cuh, `kMutant`); a fast subset of tests/test_gpu_parity.py and
-tests/test_gpu_p2p.py must FAIL for every one of them.
+"""Mutation check of the GPU parity tests: each mutant is a copy of
+paper_2604_07808_b200/csrc/ with ONE plausible kernel mistake patched in (a
+text replacement below), built into its own libgrass; a fast subset of the GPU
+tests must FAIL for every one of them.  The product source carries no mutation
+hooks: the mistakes exist only in the patched copies under build/msrc/.
 
     python tools/kernel_mutation.py build      # here (nvcc cross-compiles)
     python tools/kernel_mutation.py run        # on the GPU box
 """
 import json
 import os
+import shutil
 import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+CSRC = os.path.join(ROOT, "paper_2604_07808_b200", "csrc")
 OUTDIR = os.path.join(ROOT, "build", "mutants")
+SRCDIR = os.path.join(ROOT, "build", "msrc")
+K = "kernels.cu"
+S = "stream_kernel.cuh"
+
+# k: (what, [(file, product text, mutated text), ...]) — every product text
+# must occur in the file (all occurrences are replaced)
 MUTANTS = {
-    1: "AdamW: weight decay dropped",
-    2: "AdamW: bias correction 1/sqrt(1-b2^t) dropped",
-    3: "norm: one warp's partial left out of each tile sum",
-    4: "ragged tail: last element of a segment skipped",
-    5: "DP: gradient not scaled by 1/W",
-    6: "P2P: last rank's gradient slice not summed",
-    7: "bf16: parameter copy truncated instead of RNE",
-    8: "step prologue: t_l not advanced (bias corrections of step 1 forever)",
-    9: "P2P: theta' not stored into the last rank's parameters",
-    10: "bf16: master never initialised from the bf16 parameter",
-    11: "non-finite norm not flagged",
-    12: "norm: all-tiles warp reduction (warp_sum_multi) pairs the wrong halves",
-    13: "bf16 norm: the 4th square of each fp32 quad sum dropped",
+    1: ("AdamW: weight decay dropped",
+        [(K, "const float t1 = th * s.decay;", "const float t1 = th;")]),
+    2: ("AdamW: bias correction 1/sqrt(1-b2^t) dropped",
+        [(K, "const float den = fmaf(sq, s.inv_bc2s, s.eps);", "const float den = fmaf(sq, 1.0f, s.eps);")]),
+    3: ("norm: one warp's partial left out of each tile sum",
+        [(S, "for (int w = 0; w < kConsumerWarps; ++w) p += red[i & 1][tid][w];",
+          "for (int w = 0; w < kConsumerWarps - 1; ++w) p += red[i & 1][tid][w];")]),
+    4: ("ragged tail: last element of a segment skipped",
+        [(S, "if (e + j < ne) {", "if (e + j < ne - 1) {")]),
+    5: ("DP: gradient not scaled by 1/W",
+        [(S, "const float gs = b.gscale;", "const float gs = 1.0f;")]),
+    6: ("DP: last rank's gradient slice not summed",
+        [(S, "gacc[k0][q].x += x.x; gacc[k0][q].y += x.y; gacc[k0][q].z += x.z; gacc[k0][q].w += x.w;",
+          "if (r != b.npeer - 1) { gacc[k0][q].x += x.x; gacc[k0][q].y += x.y; gacc[k0][q].z += x.z; gacc[k0][q].w += x.w; }")]),
+    7: ("bf16: parameter copy truncated instead of RNE",
+        [(S, "__device__ __forceinline__ uint32_t f2bf(float f) {",
+          "__device__ __forceinline__ uint32_t f2bf(float f) {\n  return __float_as_uint(f) >> 16;")]),
+    8: ("step prologue: t_l not advanced (bias corrections of step 1 forever)",
+        [(K, "  st.t[l] = t;\n", "\n")]),
+    9: ("P2P: theta' not stored into the last rank's parameters",
+        [(S, "for (int q = 0; q < ntp; ++q) {", "for (int q = 0; q < ntp - 1; ++q) {")]),
+    10: ("bf16: master never initialised from the bf16 parameter",
+         [(S, "const bool init = BF16 && UPDATE && st.init_now[sg.layer];", "const bool init = false;")]),
+    11: ("non-finite norm not flagged",
+         [(K, "atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins", "(void)0;")]),
+    12: ("norm: all-tiles warp reduction (warp_sum_perm) fed in tile order instead of the lane's permuted order",
+         [(S, "const int pm = (!UPDATE && ne == kUnit) ? (lane >> MS::SHIFT) & (MS::C - 1) : 0;", "const int pm = 0;")]),
+    16: ("bf16 K1 fast path: the stage handed back even when a sum left fp32's range (fallback re-reads a refilled stage)",
+         [(S, "          if (__all_sync(0xffffffffu, ok)) {", "          if (true) {")]),
+    13: ("bf16 norm: the last square of each thread's fp32 8-square sum dropped",
+         [(S, "      s = __fmaf_rn(w, w, s);", "      s = __fmaf_rn(w, 0.f, s);")]),
+    15: ("bf16 norm: the fp32 8-square sum used even where it underflows (no exact fallback)",
+         [(S, "  return __float_as_uint(s) - 0x0D800000u <= 0x7F7FFFFFu - 0x0D800000u;", "  return true;")]),
+    14: ("P2P barrier self-test: start barrier removed",
+         [(K, "    a.which = 0;  // start barrier: every rank has read its rows of this round\n"
+              "    const int n_save = a.n;\n    a.n = 0;\n    p2p_sync_cta(a);\n    a.n = n_save;\n", "")]),
 }
 TESTS = ("test_step_layers_vs_oracle_multi_step or test_norms_ragged_sizes_vs_oracle or "
          "test_bf16_mixed_precision_vs_oracle or test_p2p_virtual_ranks_vs_oracle or "
          "test_zero_grad_zero_state_is_identity_on_theta or test_nonfinite_gradient_reported_and_not_recorded or "
-         "test_norms_probe_equals_update_bitwise or test_norms_integer_grads_exact_bf16")
+         "test_norms_probe_equals_update_bitwise or test_norms_integer_grads_exact_bf16 or "
+         "test_p2p_barrier_protocol_selftest or test_bf16_norms_tiny_and_huge_gradients")
+
+
+def patched_source(k: int) -> str:
+    """A copy of csrc/ with mutant k's replacements applied (fails loudly if a
+    product text is missing, so the patch set cannot silently go stale)."""
+    d = os.path.join(SRCDIR, f"m{k}")
+    shutil.rmtree(d, ignore_errors=True)
+    shutil.copytree(CSRC, d)
+    for fname, old, new in MUTANTS[k][1]:
+        p = os.path.join(d, fname)
+        s = open(p).read()
+        if old not in s:
+            raise SystemExit(f"mutant {k}: product text not found in {fname}: {old!r}")
+        open(p, "w").write(s.replace(old, new))
+    return d
 
 
 def build():
     from paper_2604_07808_b200 import build as b
     os.makedirs(OUTDIR, exist_ok=True)
     for k in MUTANTS:
-        b.build(force=True, defines=[f"GRASS_MUTANT={k}"], out=os.path.join(OUTDIR, f"libgrass_m{k}.so"))
+        b.build(force=True, src_dir=patched_source(k), out=os.path.join(OUTDIR, f"libgrass_m{k}.so"))
         print("built mutant", k, flush=True)
 
 
 def run():
     res = {}
-    for k, what in MUTANTS.items():
+    for k, (what, _) in MUTANTS.items():
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_m{k}.so"))
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                             "tests/test_gpu_parity.py", "tests/test_gpu_p2p.py", "-k", TESTS],
@@ -62,4 +110,9 @@ def run():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["check"]:  # CPU: every patch still applies to the product source
+        for k in MUTANTS:
+            patched_source(k)
+        print(f"{len(MUTANTS)} mutant patches apply")
+        sys.exit(0)
     sys.exit(build() if sys.argv[1:] == ["build"] else run())

@@ -12,11 +12,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
     "base": [],
-    "bf16_tps13": ["GRASS_NORM_TPS_BF16=13"],
-    "bf16_tps10": ["GRASS_NORM_TPS_BF16=10"],
-    "fp32_tps7": ["GRASS_NORM_TPS=7"],
+    "bf16_tps8_st2": ["GRASS_NORM_STAGES_BF16=2"],
+    "bf16_tps4_st6": ["GRASS_NORM_TPS_BF16=4", "GRASS_NORM_STAGES_BF16=6"],
+    "bf16_tps12_st2": ["GRASS_NORM_TPS_BF16=12", "GRASS_NORM_STAGES_BF16=2"],
     "base_again": [],
-    "bf16_tps13_again": ["GRASS_NORM_TPS_BF16=13"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
@@ -29,7 +28,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main,probe,bf16", extra=()):
+def run(legs="main,probe,bf16,p2p", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
