@@ -290,6 +290,29 @@ grass_status flush(grass_ctx* c, Batch* b, bool update, cudaStream_t s) {
     CUDA_TRY(c, launch_fused(update, *b, c->st, update ? c->grid_update : c->grid_norm, s));
   }
   c->launches++;
+  // K3 for the layers (shards) whose last tiles this launch wrote (a layer may
+  // span several launches: offload chunks)
+  FinalizeArgs fa;
+  std::memset(&fa, 0, sizeof(fa));
+  fa.mode = b->mode;
+  for (int i = 0; i < b->nseg; ++i) {
+    const Seg& sg = b->seg[i];
+    int64_t& done = c->tiles_launched[sg.layer];
+    done += sg.tiles;
+    if (done < sg.layer_tiles) continue;
+    done = 0;
+    if (b->mode == kFinalizeNone) continue;  // clipping pass 2: the norm was finished in pass 1
+    fa.layer[fa.n] = sg.layer;
+    fa.tiles[fa.n] = sg.layer_tiles;
+    fa.out_slot[fa.n] = sg.out_slot;
+    fa.base[fa.n] = sg.part_layer_base;
+    fa.numel[fa.n] = sg.layer_numel;
+    fa.n++;
+  }
+  if (fa.n > 0) {
+    CUDA_TRY(c, launch_finalize(fa, c->st, s));
+    c->launches++;
+  }
   const int32_t mode = b->mode;
   *b = make_batch(c, mode);
   return GRASS_OK;
@@ -348,7 +371,6 @@ void free_ctx(grass_ctx* c) {
     if (p) cudaFree(p);
   };
   dfree(c->st.partials);
-  dfree(c->st.counters);
   dfree(c->d_mgn);
   dfree(c->st.last_ss);
   if (c->h_mgn) cudaFreeHost(c->h_mgn);
@@ -438,7 +460,7 @@ grass_status create_impl(const grass_config* cfg, grass_ctx* c) {
     return e;
   };
   CUDA_TRY(c, dalloc((void**)&c->st.partials, sizeof(double) * (size_t)std::max<int64_t>(parts, 1)));
-  CUDA_TRY(c, dalloc((void**)&c->st.counters, sizeof(unsigned) * c->nl));
+  c->tiles_launched.assign(c->nl, 0);
   c->mgn_bytes = 16 * (size_t)c->nl + 8;
   CUDA_TRY(c, dalloc(&c->d_mgn, c->mgn_bytes));
   CUDA_TRY(c, cudaHostAlloc(&c->h_mgn, c->mgn_bytes, cudaHostAllocDefault));

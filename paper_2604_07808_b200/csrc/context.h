@@ -135,6 +135,7 @@ struct grass_ctx {
   bool dp = false;  // data-parallel (NCCL) path: world > 1, or world = 1 with a unique id
   int grid_update = 0, grid_norm = 0;
   int64_t launches = 0, dev_bytes = 0, host_bytes = 0;
+  std::vector<int64_t> tiles_launched;  // per layer: tiles launched since its last K3 (flush)
   std::string err;
 
   grass_status fail(grass_status s, const std::string& msg) {

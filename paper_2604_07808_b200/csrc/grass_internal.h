@@ -83,7 +83,6 @@ struct Batch {
 // Device-resident MGN / reduction state (all arrays indexed by layer id unless noted).
 struct DevState {
   double* partials;        // tile partials, all layers back to back
-  unsigned int* counters;  // tiles finished per layer (reset by the finalizer)
   double* S;               // window sum of r_l   (Eq. 2)
   long long* c;            // window count
   double* last_ss;         // last squared norm
@@ -113,6 +112,17 @@ cudaError_t launch_step_prologue(const PrologueArgs& a, const DevState& st, cuda
 // kernels.cu
 cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int grid,
                          cudaStream_t s);
+// K3 for the layers whose last tiles a stream launch wrote: one CTA each.
+struct FinalizeArgs {
+  int32_t n;               // layers
+  int32_t mode;            // FinalizeMode (kFinalizeMgn / kFinalizeShard)
+  int32_t layer[kMaxSeg];
+  int32_t tiles[kMaxSeg];  // tile partials of the layer (shard)
+  int32_t out_slot[kMaxSeg];
+  int64_t base[kMaxSeg];   // index of the layer's tile 0 in DevState::partials
+  int64_t numel[kMaxSeg];  // N_p(l)
+};
+cudaError_t launch_finalize(const FinalizeArgs& a, const DevState& st, cudaStream_t s);
 // world > 1: per-layer total = fixed ascending-rank sum of the all-gathered
 // shard partials gathered[r * total_slots + slot], then the MGN update.
 struct RankSumArgs {

@@ -80,6 +80,10 @@ struct MultiSlots {
   static constexpr int LOG = C == 1 ? 0 : C == 2 ? 1 : C == 4 ? 2 : C == 8 ? 3 : 4;
   static constexpr int SHIFT = 5 - LOG;
 };
+// Tiles of a unit reduced together by one warp_sum_perm: the whole unit when
+// TPS is a power of two, else groups of 4 or 2 (no empty slots either way).
+template <int TPS>
+constexpr int kPermGroup = (TPS & (TPS - 1)) == 0 ? TPS : (TPS % 4 == 0 ? 4 : (TPS % 2 == 0 ? 2 : 1));
 template <int N>
 __device__ __forceinline__ double warp_sum_perm(double (&w)[MultiSlots<N>::C], int lane, int* slot) {
   constexpr int C = MultiSlots<N>::C;
@@ -225,42 +229,48 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
 }
 
-// Fixed-shape reduction over the consumer threads; result valid in thread 0.
-__device__ __forceinline__ double consumer_sum(double x, double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  x = warp_sum(x);
-  if (lane == 0) red[warp] = x;
-  consumer_sync();
-  double t = 0.0;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) t += red[w];
-  }
-  return t;
-}
-
-// K3: the layer total is the fixed-order sum of its tile partials.
-__device__ void finalize_layer(const Seg& sg, const DevState& st, int32_t mode, double* red) {
-  __threadfence();
-  const double* P = st.partials + sg.part_layer_base;
+// K3: the layer total is the fixed-order sum of its tile partials — thread t
+// adds tiles t, t + 512, ... in ascending order (loads batched 8 deep, the
+// additions in the same order), then the fixed warp / block tree.  One CTA
+// per completed layer of the preceding stream launch (grass_finalize_kernel):
+// the layers finish in parallel, not one after another in the CTA that
+// completed them last (up to ~0.4 ms at the end of a 32-layer probing pass).
+__global__ void __launch_bounds__(kThreads) grass_finalize_kernel(const __grid_constant__ FinalizeArgs fa,
+                                                                  const DevState st) {
+  __shared__ double red[kConsumerWarps];
+  const int j = blockIdx.x;
+  const int layer = fa.layer[j], n = fa.tiles[j];
+  const double* P = st.partials + fa.base[j];
   double a = 0.0;
-  for (int i = threadIdx.x; i < sg.layer_tiles; i += kThreads) a += __ldcg(P + i);
-  const double ss = consumer_sum(a, red);
-  if (threadIdx.x == 0) {
-    if (mode == kFinalizeMgn) {
-      st.last_ss[sg.layer] = ss;
-      if (isfinite(ss)) {
-        st.S[sg.layer] += sqrt(ss / (double)sg.layer_numel);  // Eq. 2 inner term
-        st.c[sg.layer] += 1;
-      } else {
-        atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins
-      }
-    } else if (mode == kFinalizeShard) {
-      st.shard_ss[sg.out_slot] = ss;
-    }
-    st.counters[sg.layer] = 0u;  // ready for the next step
+  int i = threadIdx.x;
+  for (; i + 7 * kThreads < n; i += 8 * kThreads) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __ldcg(P + i + k * kThreads);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a += x[k];
   }
-  consumer_sync();
+  for (; i < n; i += kThreads) a += __ldcg(P + i);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double w = warp_sum(a);
+  if (lane == 0) red[warp] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ss = 0.0;
+#pragma unroll
+    for (int k = 0; k < kConsumerWarps; ++k) ss += red[k];
+    if (fa.mode == kFinalizeMgn) {
+      st.last_ss[layer] = ss;
+      if (isfinite(ss)) {
+        st.S[layer] += sqrt(ss / (double)fa.numel[j]);  // Eq. 2 inner term
+        st.c[layer] += 1;
+      } else {
+        atomicMax(st.flag, INT_MAX - layer);  // smallest id wins
+      }
+    } else if (fa.mode == kFinalizeShard) {
+      st.shard_ss[fa.out_slot[j]] = ss;
+    }
+  }
 }
 
 // K2 writes its results back into the stage and the producer bulk-stores them
@@ -438,11 +448,11 @@ __global__ void grass_clip_coef_kernel(const __grid_constant__ ClipArgs a, const
 constexpr int kUpdTPS = 1, kUpdStages = GRASS_UPD_STAGES;  // 4 arrays x 16 KiB per stage -> 128 KiB ring
 constexpr int kNormTPS = GRASS_NORM_TPS, kNormStages = GRASS_NORM_STAGES;  // 96 KiB x 2 -> 192 KiB
 #ifndef GRASS_NORM_TPS_BF16
-#define GRASS_NORM_TPS_BF16 8  // 64 KiB units x 3 stages (a power of two: the all-tiles reduction has no empty slots)
+#define GRASS_NORM_TPS_BF16 4  // 32 KiB units x 6 stages: 1.77 ms vs 1.86 (12 x 2) / 1.95 (8 x 3), profiles/r02_variants_k3_split.json
 #endif
 constexpr int kNormTPSBf16 = GRASS_NORM_TPS_BF16;  // bf16 probing: tiles per unit (2 B/element)
 #ifndef GRASS_NORM_STAGES_BF16
-#define GRASS_NORM_STAGES_BF16 3
+#define GRASS_NORM_STAGES_BF16 6
 #endif
 constexpr int kNormStagesBf16 = GRASS_NORM_STAGES_BF16;
 #ifndef GRASS_P2P_NORM_TPS
@@ -494,6 +504,12 @@ cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int gr
                   : launch_stream<false, kNormTPSBf16, kNormStagesBf16, true>(b, st, grid, s);
   return update ? launch_stream<true, kUpdTPS, kUpdStages, false>(b, st, grid, s)
                 : launch_stream<false, kNormTPS, kNormStages, false>(b, st, grid, s);
+}
+
+cudaError_t launch_finalize(const FinalizeArgs& a, const DevState& st, cudaStream_t s) {
+  if (a.n <= 0) return cudaSuccess;
+  grass_finalize_kernel<<<a.n, kThreads, 0, s>>>(a, st);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rank_sum(const double* gathered, const RankSumArgs& a, const DevState& st,

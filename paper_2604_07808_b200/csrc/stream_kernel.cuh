@@ -78,6 +78,13 @@ __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
   return BF16 ? bf2f(sg.g16[idx]) : sg.g[idx];
 }
 
+#ifndef GRASS_K1_DRAIN  // A/B only (wrong norms): K1 consumers hand every full unit back untouched
+#define GRASS_K1_DRAIN 0
+#endif
+#ifndef GRASS_WAIT_ONE_LANE  // A/B: one lane per warp polls the full barrier
+#define GRASS_WAIT_ONE_LANE 0
+#endif
+
 // Eq. 2: the value of one consumer thread in one tile — the sum of the squares
 // of its kUnroll x 4 gradient values g[q].{x,y,z,w} (elements (q*kThreads +
 // t)*4 + j; an element beyond a ragged end is 0 and adds nothing).
@@ -236,18 +243,13 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   constexpr bool kRing = !(P2P && P2PGSlots<UPDATE, BF16>::kNoStageRing);
   char* const gring = sbuf + (kRing ? (size_t)STAGES * L::bytes : 0);
   __shared__ int unit_prefix[kMaxSeg + 1];
-  __shared__ int seg_done[kMaxSeg];
   __shared__ double red[2][TPS][kConsumerWarps];
-  __shared__ double fred[kConsumerWarps];
-  __shared__ int fin[kMaxSeg];
-  __shared__ int nfin;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     unit_prefix[0] = 0;
     for (int s = 0; s < b.nseg; ++s) {
       unit_prefix[s + 1] = unit_prefix[s] + (b.seg[s].tiles + TPS - 1) / TPS;
-      seg_done[s] = 0;
     }
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full_bar[i], 1);
@@ -387,21 +389,32 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
     char* stg = sbuf + (size_t)stage * L::bytes;
     const int64_t pe0 = P2P ? sg.poff + e0 : 0;  // full-layer index of the unit's element 0
-    if (kRing) mbar_wait(&full_bar[stage], (i / STAGES) & 1);
+    if (kRing) {
+      if (GRASS_WAIT_ONE_LANE) {  // A/B: one lane polls the barrier, the warp follows
+        if (lane == 0) mbar_wait(&full_bar[stage], (i / STAGES) & 1);
+        __syncwarp();
+        mbar_wait(&full_bar[stage], (i / STAGES) & 1);  // completes at once; orders the warp's reads after the phase
+      } else {
+        mbar_wait(&full_bar[stage], (i / STAGES) & 1);
+      }
+    }
     if (L::SEP) mbar_wait(&outfree_bar[stage], (i / STAGES) & 1);
-    // full norm-only units: slot t of this lane holds tile t ^ pm — the order
-    // in which warp_sum_perm keeps them (pm = the tile the lane ends with)
-    using MS = MultiSlots<TPS>;
-    const int pm = (!UPDATE && ne == kUnit) ? (lane >> MS::SHIFT) & (MS::C - 1) : 0;
+    // full norm-only units: the TPS tiles form groups of GS (a power of two);
+    // slot t of this lane holds tile perm(t) = (t / GS) * GS + ((t % GS) ^ pm)
+    // — the order in which warp_sum_perm keeps them (pm = the tile of each
+    // group the lane ends with)
+    constexpr int GS = kPermGroup<TPS>;
+    using MS = MultiSlots<GS>;
+    const int pm = (!UPDATE && ne == kUnit) ? (lane >> MS::SHIFT) & (GS - 1) : 0;
+    auto perm = [&](int t) { return (t / GS) * GS + ((t % GS) ^ pm); };
     float4 gacc[P2P ? TPS : 1][kUnroll];  // P2P: this thread's summed gradient of the unit
     if (P2P && nv) {
-      static_assert(!P2P || UPDATE || MultiSlots<TPS>::C == TPS, "P2P norm units: a power-of-two tile count");
       for (int r = 0; r < b.npeer; ++r, ++gcount) {
         const int gsl = gcount % NG;
         mbar_wait(&gfull_bar[gsl], (gcount / NG) & 1);
 #pragma unroll
         for (int k0 = 0; k0 < (P2P ? TPS : 1); ++k0) {
-          const int k = k0 ^ pm;  // gacc[k0] holds tile k
+          const int k = perm(k0);  // gacc[k0] holds tile k
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
             const int e = tile_elem(k, q, tid);
@@ -420,14 +433,19 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       }
     }
     bool released = false;  // this warp has handed the stage back already
-    if (!UPDATE && !P2P && ne == kUnit) {
-      // Full unit of the norm-only stream: each lane reads its tiles in the
-      // order warp_sum_perm keeps them (slot t = tile t ^ pm), so the
-      // all-tiles reduction needs no selects.  Same element map and tile
-      // values as the guarded path below.
-      double w[MS::C];
+    if (GRASS_K1_DRAIN && !UPDATE && !P2P && ne == kUnit) {  // A/B only: the ring without any consumer work
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[stage]);
+      released = true;
+      if (lane < TPS) red[i & 1][lane][warp] = 0.0;
+    } else if (!UPDATE && ne == kUnit) {
+      // Full unit of the norm-only stream: each lane reads (or, P2P, summed)
+      // its tiles in the order warp_sum_perm keeps them (slot t = tile
+      // perm(t)), so the all-tiles reduction needs no selects.  Same element
+      // map and tile values as the guarded path below.
+      double w[TPS];
       bool done = false;
-      if constexpr (BF16 && MS::C == TPS) {
+      if constexpr (BF16 && !P2P) {
         if (gs == 1.f) {
           // bf16 fast path: the unit's data to registers, the 8-square fp32
           // sums with FHFMA.BF16 straight from the packed words; if every sum
@@ -440,7 +458,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           for (int t = 0; t < TPS; ++t)
 #pragma unroll
             for (int q = 0; q < kUnroll; ++q)
-              raw[t][q] = *reinterpret_cast<const uint2*>(stg + L::off_g + 2 * tile_elem(t ^ pm, q, tid));
+              raw[t][q] = *reinterpret_cast<const uint2*>(stg + L::off_g + 2 * tile_elem(perm(t), q, tid));
           float s8[TPS];
           uint32_t lo = 0xffffffffu, hi = 0u;
 #pragma unroll
@@ -461,42 +479,29 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       }
       if (!done) {
 #pragma unroll
-        for (int t = 0; t < MS::C; ++t) {
-          const int k = t ^ pm;
-          w[t] = 0.0;
-          if (MS::C == TPS || k < TPS) {
-            float4 g4[kUnroll];
-#pragma unroll
-            for (int q = 0; q < kUnroll; ++q) g4[q] = stage_g4<BF16>(stg + L::off_g, tile_elem(k, q, tid));
-            if (gs != 1.f) {  // DP average (warp-uniform; x * 1 == x, so skipping it is exact)
-#pragma unroll
-              for (int q = 0; q < kUnroll; ++q) g4[q] = scale4(g4[q], gs);
-            }
-            w[t] = tile_value<BF16>(g4);
-          }
-        }
-      }
-      int slot;
-      const double tsum = warp_sum_perm<TPS>(w, lane, &slot);  // all tiles at once (bit-identical to warp_sum)
-      if (slot >= 0) red[i & 1][slot][warp] = tsum;
-    } else if (!UPDATE && P2P && ne == kUnit) {
-      // Full unit of the P2P norm stream: the ranks' summed gradient is in
-      // gacc (slot t = tile t ^ pm); same element map and tile values as the
-      // guarded path.
-      double w[MS::C];  // (P2P norm units have C == TPS tiles)
-#pragma unroll
-      for (int t = 0; t < MS::C; ++t) {
-        w[t] = 0.0;
-        if (t < TPS) {
+        for (int t = 0; t < TPS; ++t) {
           float4 g4[kUnroll];
 #pragma unroll
-          for (int q = 0; q < kUnroll; ++q) g4[q] = gs != 1.f ? scale4(gacc[P2P ? t : 0][q], gs) : gacc[P2P ? t : 0][q];
+          for (int q = 0; q < kUnroll; ++q) {
+            if constexpr (P2P) g4[q] = gacc[t][q];
+            else g4[q] = stage_g4<BF16>(stg + L::off_g, tile_elem(perm(t), q, tid));
+          }
+          if (gs != 1.f) {  // DP average (warp-uniform; x * 1 == x, so skipping it is exact)
+#pragma unroll
+            for (int q = 0; q < kUnroll; ++q) g4[q] = scale4(g4[q], gs);
+          }
           w[t] = tile_value<BF16>(g4);
         }
       }
-      int slot;
-      const double tsum = warp_sum_perm<TPS>(w, lane, &slot);
-      if (slot >= 0) red[i & 1][slot][warp] = tsum;
+#pragma unroll
+      for (int g = 0; g < TPS / GS; ++g) {  // all tiles of each group at once (bit-identical to warp_sum)
+        double wg[GS];
+#pragma unroll
+        for (int j = 0; j < GS; ++j) wg[j] = w[g * GS + j];
+        int slot;
+        const double tsum = warp_sum_perm<GS>(wg, lane, &slot);
+        if (slot >= 0) red[i & 1][g * GS + slot][warp] = tsum;
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < TPS; ++k) {
@@ -583,22 +588,8 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
       for (int w = 0; w < kConsumerWarps; ++w) p += red[i & 1][tid][w];
       st.partials[sg.part_index + (int64_t)ui * TPS + tid] = p;
     }
-    if (tid == 0) seg_done[s] += ntiles;
   }
-  // Publish this CTA's partials (one fence, one atomic per segment) and
-  // detect the layers this CTA completed.
-  consumer_sync();
-  if (tid == 0) {
-    __threadfence();
-    int nf = 0;
-    for (int s2 = 0; s2 < b.nseg; ++s2) {
-      const int c = seg_done[s2];
-      if (c == 0) continue;
-      const unsigned prev = atomicAdd(st.counters + b.seg[s2].layer, (unsigned)c);
-      if (prev + (unsigned)c == (unsigned)b.seg[s2].layer_tiles) fin[nf++] = s2;
-    }
-    nfin = nf;
-  }
-  consumer_sync();
-  for (int f = 0; f < nfin; ++f) finalize_layer(b.seg[fin[f]], st, b.mode, fred);
+  // (K3, the per-layer sum of the tile partials, is grass_finalize_kernel,
+  // launched after this kernel for the layers it completed — in parallel over
+  // the layers instead of in whichever CTA finished last)
 }

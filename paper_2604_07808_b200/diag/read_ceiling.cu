@@ -11,7 +11,9 @@
 //           streams `unit`-byte pieces HBM -> shared memory with
 //           cp.async.bulk into a ring of `stages` slots (mbarrier complete_tx),
 //           one consumer warp reads one word per slot and hands it back —
-//           K1's data movement with no arithmetic.
+//           K1's data movement with no arithmetic;
+//   mode 2/3 K1's consumer protocol (16 warps, per-warp release, mode 3: a
+//           named barrier per unit) on the same ring — diagnostics.
 // C ABI: grass_diag_read(ptr, bytes, mode, grid, unit, stages, sink, stream).
 #include <cuda_runtime.h>
 
@@ -102,6 +104,67 @@ __global__ void __launch_bounds__(64, 1) read_tma(const char* __restrict__ p, si
   }
 }
 
+// mode 2 / 3: K1's protocol with no arithmetic — 16 consumer warps all wait
+// on the full barrier, each warp hands the slot back (empty barrier count 16),
+// and (mode 3) the consumers meet at a named barrier once per unit, as K1's
+// per-unit tile-partial reduction does.
+template <bool BAR>
+__global__ void __launch_bounds__(544, 1) read_k1proto(const char* __restrict__ p, size_t bytes, uint32_t unit,
+                                                       int stages, unsigned long long* sink) {
+  extern __shared__ __align__(1024) char ring[];
+  __shared__ __align__(8) uint64_t full[16], empty[16];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 16;" ::"r"(smem_u32(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const size_t units = bytes / unit;
+  if (warp == 16) {
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int k = 0;
+      for (size_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+        const int s = k % stages;
+        if (k >= stages) {
+          const uint32_t par = ((k / stages) & 1) ^ 1;
+          asm volatile("{\n.reg .pred q;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W_%=;\n}\n" ::"r"(
+                           smem_u32(&empty[s])),
+                       "r"(par)
+                       : "memory");
+        }
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(unit)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                smem_u32(ring + (size_t)s * unit)),
+            "l"(p + u * unit), "r"(unit), "r"(smem_u32(&full[s])), "l"(pol)
+            : "memory");
+      }
+    }
+    return;
+  }
+  uint32_t acc = 0;
+  int k = 0;
+  for (size_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+    const int s = k % stages;
+    const uint32_t par = (k / stages) & 1;
+    asm volatile("{\n.reg .pred q;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W_%=;\n}\n" ::"r"(
+                     smem_u32(&full[s])),
+                 "r"(par)
+                 : "memory");
+    acc ^= *reinterpret_cast<const volatile uint32_t*>(ring + (size_t)s * unit + tid * 4);
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+    if (BAR) asm volatile("bar.sync 1, 512;" ::: "memory");
+  }
+  if (acc == 0x9E3779B9u) atomicAdd(sink, 1ull);
+}
+
 }  // namespace
 
 extern "C" int grass_diag_read(const void* ptr, unsigned long long bytes, int mode, int grid, unsigned int unit,
@@ -110,6 +173,14 @@ extern "C" int grass_diag_read(const void* ptr, unsigned long long bytes, int mo
   if (!ptr || !sink || grid < 1 || reinterpret_cast<uintptr_t>(ptr) % 16 != 0) return (int)cudaErrorInvalidValue;
   if (mode == 0) {
     read_ldg<<<grid, 512, 0, s>>>(static_cast<const uint4*>(ptr), (size_t)bytes / 16, sink);
+  } else if (mode >= 2) {
+    if (unit % 16 != 0 || stages < 1 || stages > 16 || (size_t)unit * stages > 227u * 1024u || bytes % unit != 0)
+      return (int)cudaErrorInvalidValue;
+    const size_t smem = (size_t)unit * stages;
+    auto kern = mode == 2 ? read_k1proto<false> : read_k1proto<true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    kern<<<grid, 544, smem, s>>>(static_cast<const char*>(ptr), (size_t)bytes, unit, stages, sink);
   } else {
     if (unit % 16 != 0 || stages < 1 || stages > 16 || (size_t)unit * stages > 227u * 1024u ||
         bytes % unit != 0)

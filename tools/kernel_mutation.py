@@ -50,7 +50,7 @@ MUTANTS = {
     11: ("non-finite norm not flagged",
          [(K, "atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins", "(void)0;")]),
     12: ("norm: all-tiles warp reduction (warp_sum_perm) fed in tile order instead of the lane's permuted order",
-         [(S, "const int pm = (!UPDATE && ne == kUnit) ? (lane >> MS::SHIFT) & (MS::C - 1) : 0;", "const int pm = 0;")]),
+         [(S, "const int pm = (!UPDATE && ne == kUnit) ? (lane >> MS::SHIFT) & (GS - 1) : 0;", "const int pm = 0;")]),
     16: ("bf16 K1 fast path: the stage handed back even when a sum left fp32's range (fallback re-reads a refilled stage)",
          [(S, "          if (__all_sync(0xffffffffu, ok)) {", "          if (true) {")]),
     13: ("bf16 norm: the last square of each thread's fp32 8-square sum dropped",

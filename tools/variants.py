@@ -12,9 +12,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
     "base": [],
-    "bf16_tps8_st2": ["GRASS_NORM_STAGES_BF16=2"],
-    "bf16_tps4_st6": ["GRASS_NORM_TPS_BF16=4", "GRASS_NORM_STAGES_BF16=6"],
     "bf16_tps12_st2": ["GRASS_NORM_TPS_BF16=12", "GRASS_NORM_STAGES_BF16=2"],
+    "bf16_tps4_st6": ["GRASS_NORM_TPS_BF16=4", "GRASS_NORM_STAGES_BF16=6"],
+    "fp32_tps4_st3": ["GRASS_NORM_TPS=4", "GRASS_NORM_STAGES=3"],
+    "fp32_tps2_st6": ["GRASS_NORM_TPS=2", "GRASS_NORM_STAGES=6"],
     "base_again": [],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
