@@ -165,7 +165,56 @@ __global__ void __launch_bounds__(544, 1) read_k1proto(const char* __restrict__ 
   if (acc == 0x9E3779B9u) atomicAdd(sink, 1ull);
 }
 
+// 4-read / 3-write elementwise stream (K2's HBM mix: g, theta, m, v in;
+// theta, m, v out) with plain per-thread 128-bit loads and streaming stores,
+// U float4 of each array in flight per thread: the mixed read/write ceiling
+// K2's TMA ring is compared with.
+template <int U>
+__global__ void __launch_bounds__(512) rw43(const float4* __restrict__ g, float4* __restrict__ th,
+                                           float4* __restrict__ m, float4* __restrict__ v, size_t n4) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n4; i += U * stride) {
+    float4 a[U], b[U], c[U], d[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      a[k] = __ldcs(g + i + k * stride);
+      b[k] = __ldcs(th + i + k * stride);
+      c[k] = __ldcs(m + i + k * stride);
+      d[k] = __ldcs(v + i + k * stride);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      b[k].x += a[k].x; b[k].y += a[k].y; b[k].z += a[k].z; b[k].w += a[k].w;
+      c[k].x += a[k].y; d[k].x += a[k].z;
+      __stcs(th + i + k * stride, b[k]);
+      __stcs(m + i + k * stride, c[k]);
+      __stcs(v + i + k * stride, d[k]);
+    }
+  }
+  for (; i < n4; i += stride) {
+    float4 a = __ldcs(g + i), b = __ldcs(th + i);
+    b.x += a.x;
+    __stcs(th + i, b);
+    __stcs(m + i, __ldcs(m + i));
+    __stcs(v + i, __ldcs(v + i));
+  }
+}
+
 }  // namespace
+
+extern "C" int grass_diag_rw43(void* const* bufs, unsigned long long n, int unroll, int grid, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const float4* g = static_cast<const float4*>(bufs[0]);
+  float4* th = static_cast<float4*>(bufs[1]);
+  float4* m = static_cast<float4*>(bufs[2]);
+  float4* v = static_cast<float4*>(bufs[3]);
+  const size_t n4 = (size_t)n / 4;
+  if (unroll == 1) rw43<1><<<grid, 512, 0, s>>>(g, th, m, v, n4);
+  else if (unroll == 2) rw43<2><<<grid, 512, 0, s>>>(g, th, m, v, n4);
+  else rw43<4><<<grid, 512, 0, s>>>(g, th, m, v, n4);
+  return (int)cudaGetLastError();
+}
 
 extern "C" int grass_diag_read(const void* ptr, unsigned long long bytes, int mode, int grid, unsigned int unit,
                                int stages, unsigned long long* sink, void* stream) {
