@@ -15,7 +15,7 @@
  *                         (Fig. 4),
  *                         fused with the Eq. 2 norm of the same gradients.
  *
- * Readings where the paper is silent are DESIGN.md R1-R20 (referenced below).
+ * Readings where the paper is silent are DESIGN.md R1-R22 (referenced below).
  *
  * Conventions (all calls):
  *   - Every entry point returns a grass_status; no C++ exception ever crosses
@@ -135,7 +135,9 @@ typedef struct grass_config {
                                   n_always; gamma, cache_layers, probabilities and the commit
                                   refer to those only.  0 = none (default). */
   int32_t dp_mode;             /* world >= 1 data parallelism:
-                                  GRASS_DP_NCCL: NCCL reduce-scatter -> update -> all-gather
+                                  GRASS_DP_NCCL: NCCL exchange of the gradient slices
+                                  (grouped ncclSend / ncclRecv) -> the update kernel sums the
+                                  W slices in ascending rank order in fp32 (R20) -> ncclAllGather
                                   (needs nccl_unique_id when world > 1);
                                   GRASS_DP_P2P: ONE fused kernel per call reads every rank's
                                   gradient over peer memory (NVLink), sums them in rank order,
@@ -242,8 +244,10 @@ grass_status grass_sample_layers(grass_ctx* ctx, const double* probs, uint64_t p
  * With cfg.offload the layer's m/v stream from pinned host memory through the
  * device staging ring and back; results are bit-identical
  * to offload = 0 (R12).  World > 1: each rank updates its element shard with
- * its own m/v slice; with GRASS_DP_NCCL the gradients are reduce-scattered
- * (sum, x 1/W) and the parameters all-gathered back into params[i] over NCCL;
+ * its own m/v slice; with GRASS_DP_NCCL every rank's slice of this rank's
+ * shard arrives over NCCL (grouped send/recv), the update kernel sums the W
+ * slices in ascending rank order in fp32 and x 1/W (R20: the same bits as
+ * GRASS_DP_P2P), and the parameters are all-gathered back into params[i];
  * with GRASS_DP_P2P one fused kernel reads every rank's gradient over peer
  * memory and stores theta' into every rank's params (the registered buffers).
  * t_l and the bias corrections are advanced on the device by a prologue
@@ -354,7 +358,7 @@ typedef enum {
   GRASS_TRACE_UPDATE = 1, /* fused norm + AdamW launch (K2)                     */
   GRASS_TRACE_D2H = 2,    /* optimizer states device -> host (write-back/evict) */
   GRASS_TRACE_NORM = 3,   /* norm-only launch (K1)                              */
-  GRASS_TRACE_RS = 4,     /* NCCL reduce-scatter of gradients                   */
+  GRASS_TRACE_RS = 4,     /* NCCL gradient-slice exchange (reduce-scatter bytes) */
   GRASS_TRACE_AG = 5,     /* NCCL all-gather of parameters                      */
   GRASS_TRACE_P2P = 6     /* P2P norm publication + barrier                     */
 } grass_trace_kind;
@@ -462,6 +466,12 @@ grass_status grass_ipc_export(const void* ptr, void* handle_out, int64_t* offset
 /* Opens an IPC handle exported by another process (cached: each allocation is
  * opened once per process) and returns base + offset. */
 grass_status grass_ipc_import(int32_t device, const void* handle, int64_t offset, void** ptr_out);
+/* Several ranks in ONE process (one thread per GPU, GRASS_DP_P2P): lets
+ * `device` access `peer`'s memory directly (cudaDeviceEnablePeerAccess; an
+ * already enabled pair is not an error), so that the peers' exchange blocks
+ * and layer buffers can be passed to grass_p2p_attach / _register_layer as
+ * plain device pointers.  GRASS_E_CUDA if the pair cannot access each other. */
+grass_status grass_enable_peer_access(int32_t device, int32_t peer);
 
 #ifdef __cplusplus
 }

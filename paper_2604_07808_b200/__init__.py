@@ -8,7 +8,7 @@ from .binding import (DECIDE_COMMIT_RESAMPLE, DECIDE_CONTINUE, DECIDE_PROBE, DEC
                       POLICY_ADAPTIVE, POLICY_STATIC, POLICY_UNIFORM, Grass, GrassError,
                       exported_symbols, lib, nccl_unique_id, sample_from_probs,
                       schedule_decision, shard_range, softmax_probs, splitmix64, tile_elems,
-                      uniform, ipc_export, ipc_import, selftest_p2p)
+                      uniform, ipc_export, ipc_import, selftest_p2p, enable_peer_access)
 
 from .schedule import GrassSchedule  # noqa: E402
 from .torch_blocks import GrassBlocks, flatten_params  # noqa: E402
@@ -18,4 +18,5 @@ __all__ = ["Grass", "GrassSchedule", "GrassBlocks", "flatten_params", "GrassErro
            "splitmix64", "tile_elems", "uniform", "POLICY_ADAPTIVE", "POLICY_STATIC",
            "POLICY_UNIFORM", "DECIDE_PROBE", "DECIDE_COMMIT_RESAMPLE", "DECIDE_RESAMPLE",
            "DECIDE_CONTINUE", "RESIDENCY_STEP", "RESIDENCY_PERIOD", "RESIDENCY_STEP_PREFETCH", "DTYPE_FP32", "DTYPE_BF16",
-           "DP_NCCL", "DP_P2P", "ipc_export", "ipc_import", "selftest_p2p"]
+           "DP_NCCL", "DP_P2P", "ipc_export", "ipc_import", "selftest_p2p",
+           "enable_peer_access"]

@@ -121,6 +121,7 @@ _SIGS = {
     "grass_selftest_p2p": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
                                      C.POINTER(C.c_int32)]),
     "grass_ipc_import": (C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    "grass_enable_peer_access": (C.c_int, [C.c_int32, C.c_int32]),
 }
 
 
@@ -236,6 +237,12 @@ def ipc_import(device: int, handle: bytes, offset: int) -> int:
     return out.value
 
 
+def enable_peer_access(device: int, peer: int):
+    """Several ranks in one process (one thread per GPU): device may read /
+    write peer's memory through plain pointers (P2P data path)."""
+    _check(lib().grass_enable_peer_access(device, peer))
+
+
 class Grass:
     """One GRASS hot-path context (one per process / GPU).
 
@@ -253,7 +260,7 @@ class Grass:
                  process_group=None, force_nccl: bool = False, residency: int = RESIDENCY_STEP,
                  cache_layers: int = 0, max_grad_norm: float = 0.0, param_dtype: int = DTYPE_FP32,
                  n_always: int = 0, dp_mode: int = DP_NCCL, p2p_sync: bool = True,
-                 debug_check: bool = False):
+                 debug_check: bool = False, nccl_id: bytes | None = None):
         L = lib()
         self.layer_numel = [int(x) for x in layer_numel]
         self.n_layers = len(self.layer_numel)
@@ -285,7 +292,11 @@ class Grass:
         self.dp_mode = dp_mode
         self.bf16 = param_dtype == DTYPE_BF16
         self._uid = None
-        if world == 1 and force_nccl:
+        if nccl_id is not None and dp_mode == DP_NCCL:
+            # the caller distributed the id (e.g. several ranks as threads of one process)
+            self._uid = C.create_string_buffer(bytes(nccl_id), NCCL_ID_BYTES)
+            cfg.nccl_unique_id = C.cast(self._uid, C.c_void_p)
+        elif world == 1 and force_nccl:
             self._uid = C.create_string_buffer(nccl_unique_id(), NCCL_ID_BYTES)
             cfg.nccl_unique_id = C.cast(self._uid, C.c_void_p)
         elif world > 1 and dp_mode == DP_NCCL:

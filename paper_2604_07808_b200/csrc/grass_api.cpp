@@ -513,6 +513,34 @@ grass_status grass_ipc_export(const void* ptr, void* handle_out, int64_t* offset
   return api_exception(nullptr);
 }
 
+grass_status grass_enable_peer_access(int32_t device, int32_t peer) try {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || peer < 0 || device >= n || peer >= n) {
+    cudaGetLastError();
+    return set_thread_err(GRASS_E_INVALID, "bad device / peer");
+  }
+  if (device == peer) return GRASS_OK;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, device, peer) != cudaSuccess || !can) {
+    cudaGetLastError();
+    return set_thread_err(GRASS_E_CUDA, "device " + std::to_string(device) + " cannot access peer " +
+                                            std::to_string(peer));
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return set_thread_err(GRASS_E_CUDA, "cudaSetDevice failed");
+  }
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return set_thread_err(GRASS_E_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+  }
+  cudaGetLastError();
+  return GRASS_OK;
+} catch (...) {
+  return api_exception(nullptr);
+}
+
 grass_status grass_ipc_import(int32_t device, const void* handle, int64_t offset, void** ptr_out) try {
   if (!handle || !ptr_out || offset < 0) return set_thread_err(GRASS_E_INVALID, "bad argument");
   static std::mutex mu;

@@ -178,6 +178,34 @@ def test_norms_probe_equals_update_bitwise(dtype):
         assert_ss_close(k1[l], O.sq_norm(g))
 
 
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+def test_norms_all_tiles_reduction_keeps_each_tile_apart(dtype):
+    """K1 reduces all tiles of a unit at once (warp_sum_perm); each tile's sum
+    must still pair the lanes of THAT tile (the tree of warp_sum), not another
+    tile's — on random data a reassociation hides below the layer total's ulp,
+    so the data here is built to expose it: tile 0 holds 1.0 (lane 0) and s
+    (lane 16), tile 1 holds s (lane 0), s = 0.39 ulp(1).  Per tile: (1 + s) + s
+    = 1; a tile-0/tile-1 mix gives 1 + 2s = 1 + ulp.  K1 must equal K2 (one
+    tile per unit, warp_sum) bit for bit, and both the exact definition up to
+    that one rounding."""
+    tdt = torch.bfloat16 if dtype == G.DTYPE_BF16 else torch.float32
+    n = 4096 * 6 * 2 if dtype == G.DTYPE_FP32 else 4096 * 4 * 2       # two full K1 units
+    g = torch.zeros(n, dtype=torch.float32, device=DEV)
+    small = 1.25 * 2.0 ** -27                                            # small^2 = 0.390625 * 2^-52
+    for u in range(2):
+        base = u * (n // 2)
+        g[base + 0] = 1.0                  # tile 0, thread 0 (lane 0 of warp 0)
+        g[base + 16 * 4] = small           # tile 0, thread 16 (lane 16)
+        g[base + 4096] = small             # tile 1, thread 0
+    g = g.to(tdt)
+    gr = G.Grass([n], gamma=1, param_dtype=dtype)
+    gr.mgn_accumulate([0], [g])
+    k1 = gr.get_mgn()["last_ss"][0]
+    gr.step_layers([0], [torch.zeros(n, dtype=tdt, device=DEV)], [g], 1e-4)
+    k2 = gr.get_mgn()["last_ss"][0]
+    assert k1 == k2 == 2.0, (k1, k2)
+
+
 def test_norms_special_cases():
     gr = G.Grass([4096, 8, 2], gamma=1)
     z = torch.zeros(4096, device=DEV)

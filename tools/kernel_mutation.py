@@ -48,7 +48,7 @@ MUTANTS = {
     10: ("bf16: master never initialised from the bf16 parameter",
          [(S, "const bool init = BF16 && UPDATE && st.init_now[sg.layer];", "const bool init = false;")]),
     11: ("non-finite norm not flagged",
-         [(K, "atomicMax(st.flag, INT_MAX - sg.layer);  // smallest id wins", "(void)0;")]),
+         [(K, "atomicMax(st.flag, INT_MAX - layer);  // smallest id wins", "(void)0;")]),
     12: ("norm: all-tiles warp reduction (warp_sum_perm) fed in tile order instead of the lane's permuted order",
          [(S, "const int pm = (!UPDATE && ne == kUnit) ? (lane >> MS::SHIFT) & (GS - 1) : 0;", "const int pm = 0;")]),
     16: ("bf16 K1 fast path: the stage handed back even when a sum left fp32's range (fallback re-reads a refilled stage)",
@@ -65,7 +65,8 @@ TESTS = ("test_step_layers_vs_oracle_multi_step or test_norms_ragged_sizes_vs_or
          "test_bf16_mixed_precision_vs_oracle or test_p2p_virtual_ranks_vs_oracle or "
          "test_zero_grad_zero_state_is_identity_on_theta or test_nonfinite_gradient_reported_and_not_recorded or "
          "test_norms_probe_equals_update_bitwise or test_norms_integer_grads_exact_bf16 or "
-         "test_p2p_barrier_protocol_selftest or test_bf16_norms_tiny_and_huge_gradients")
+         "test_p2p_barrier_protocol_selftest or test_bf16_norms_tiny_and_huge_gradients or "
+         "test_norms_all_tiles_reduction_keeps_each_tile_apart")
 
 
 def patched_source(k: int) -> str:
@@ -83,10 +84,10 @@ def patched_source(k: int) -> str:
     return d
 
 
-def build():
+def build(only=()):
     from paper_2604_07808_b200 import build as b
     os.makedirs(OUTDIR, exist_ok=True)
-    for k in MUTANTS:
+    for k in (only or MUTANTS):
         b.build(force=True, src_dir=patched_source(k), out=os.path.join(OUTDIR, f"libgrass_m{k}.so"))
         print("built mutant", k, flush=True)
 
@@ -115,4 +116,6 @@ if __name__ == "__main__":
             patched_source(k)
         print(f"{len(MUTANTS)} mutant patches apply")
         sys.exit(0)
-    sys.exit(build() if sys.argv[1:] == ["build"] else run())
+    if sys.argv[1:2] == ["build"]:
+        sys.exit(build([int(x) for x in sys.argv[2:]]))
+    sys.exit(run())

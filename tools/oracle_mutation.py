@@ -31,6 +31,11 @@ MUTATIONS = [
     ("first commit with EMA", "            self.m = [w[l] if w[l] is not None else 0.0 for l in range(self.n)]",
      "            self.m = [alpha * w[l] if w[l] is not None else 0.0 for l in range(self.n)]"),
     ("window not reset", "        self.S = [0.0] * self.n\n        self.c = [0] * self.n\n", ""),
+    ("T_p = 0: empty commits allowed after the first (R22)",
+     "if sum(self.c) == 0 and not (empty_first_ok and not self.committed):",
+     "if sum(self.c) == 0 and not empty_first_ok:"),
+    ("T_p = 0: first empty commit rejected (R22)", "m = self.mgn.commit(self.alpha, empty_first_ok=self.T_p == 0)",
+     "m = self.mgn.commit(self.alpha)"),
     ("softmax: tau multiplies", "e = [math.exp((x - mx) / tau) for x in mt]", "e = [math.exp((x - mx) * tau) for x in mt]"),
     ("softmax: sign flipped", "e = [math.exp((x - mx) / tau) for x in mt]", "e = [math.exp((mx - x) / tau) for x in mt]"),
     ("softmax: no max-normalisation", "mt = [x / M for x in m] if M > 0.0 else [0.0] * len(m)", "mt = m"),

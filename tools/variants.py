@@ -12,10 +12,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
     "base": [],
-    "bf16_tps12_st2": ["GRASS_NORM_TPS_BF16=12", "GRASS_NORM_STAGES_BF16=2"],
-    "bf16_tps4_st6": ["GRASS_NORM_TPS_BF16=4", "GRASS_NORM_STAGES_BF16=6"],
-    "fp32_tps4_st3": ["GRASS_NORM_TPS=4", "GRASS_NORM_STAGES=3"],
-    "fp32_tps2_st6": ["GRASS_NORM_TPS=2", "GRASS_NORM_STAGES=6"],
+    "k2_grid148": ["GRASS_UPD_GRID_SUB=0"],
+    "k2_grid140": ["GRASS_UPD_GRID_SUB=8"],
+    "k2_grid120": ["GRASS_UPD_GRID_SUB=28"],
+    "k2_grid112": ["GRASS_UPD_GRID_SUB=36"],
+    "k2_stages3": ["GRASS_UPD_STAGES=3"],
     "base_again": [],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
@@ -29,7 +30,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main,probe,bf16,p2p", extra=()):
+def run(legs="main,bf16", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
