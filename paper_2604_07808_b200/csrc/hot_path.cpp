@@ -86,6 +86,7 @@ grass_status mgn_accumulate_impl(grass_ctx* c, bool bf16_call, const int32_t* id
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bool capturing = false;
   if ((s = capture_check(c, st, false, &capturing)) != GRASS_OK) return s;
+  std::fill(c->tiles_launched.begin(), c->tiles_launched.end(), 0);  // K3 bookkeeping starts clean
   if (c->p2p) {
     // start barrier -> K1 over the sum of every rank's gradient (peer reads) -> publish + end barrier
     if ((s = p2p_check(c, ids, n, nullptr, grads)) != GRASS_OK) return s;
@@ -182,6 +183,7 @@ grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, 
     std::fill(c->slot_ready_pending.begin(), c->slot_ready_pending.end(), 0);  // fills done (synced)
   }
   // (all arguments validated: from here on work is enqueued)
+  std::fill(c->tiles_launched.begin(), c->tiles_launched.end(), 0);  // K3 bookkeeping starts clean
   if ((s = offload_capture_fence(c, st, capturing)) != GRASS_OK) return s;
   struct CoefReset {  // the clip multiplier only applies inside this call
     grass_ctx* c;
