@@ -5,9 +5,10 @@
 //   K2  grass_stream_kernel<true>:  single-pass Eq. 2 norm + AdamW (DESIGN.md
 //       R1/R2) of the trainable layers — reads g, theta, m, v,
 //       writes theta, m, v (28 B/param).
-//   K3  finalize (inside K1/K2, by the CTA that completes a layer): fixed-order
-//       fp64 sum of the layer's tile partials, then S_l += sqrt(ss_l / N_p),
-//       c_l += 1 (Eq. 2), or the shard value for the rank sum.
+//   K3  grass_finalize_kernel (after each K1/K2 launch, one CTA per layer the
+//       launch completed): fixed-order fp64 sum of the layer's tile partials,
+//       then S_l += sqrt(ss_l / N_p), c_l += 1 (Eq. 2), or the
+//       shard value for the rank sum.
 //   K4  grass_rank_sum_kernel (world > 1): ascending-rank fp64 sum of the
 //       all-gathered shard partials, then the same MGN update.
 //
@@ -22,12 +23,13 @@
 //
 // Compile-time A/B knobs (tools/variants.py; defaults are the measured best):
 // GRASS_IEEE_MATH, GRASS_K2_STG_STORE, GRASS_K2_LOAD_EF, GRASS_K2_STORE_EF,
-// GRASS_K2_SEP_OUT, GRASS_K2_NOMATH, GRASS_K1_NOMATH, GRASS_UPD_STAGES, GRASS_NORM_TPS,
-// GRASS_NORM_TPS_BF16, GRASS_NORM_STAGES, GRASS_P2P_NORM_TPS,
-// GRASS_UPD_GRID_SUB, GRASS_NORM_GRID_SUB, GRASS_L2_PREFETCH_{NORM,UPD},
-// GRASS_UNIT_BLOCK, GRASS_BF16_MAP8, GRASS_BF16_FP64_SQ, GRASS_BF16_SQ_PAIR,
-// GRASS_K1_TILE_REDUCE.  The mutation check of the GPU tests
-// (tools/kernel_mutation.py) plants its mistakes into a patched copy of this
+// GRASS_K2_SEP_OUT, GRASS_K2_NOMATH, GRASS_UPD_STAGES, GRASS_NORM_TPS,
+// GRASS_NORM_TPS_BF16, GRASS_NORM_STAGES, GRASS_NORM_STAGES_BF16,
+// GRASS_P2P_NORM_TPS, GRASS_UPD_GRID_SUB, GRASS_NORM_GRID_SUB,
+// GRASS_L2_PREFETCH_{NORM,UPD}, GRASS_UNIT_BLOCK, GRASS_BF16_GUARD (0: no exact
+// fallback — wrong for tiny / huge gradients), GRASS_K1_DRAIN (diagnostic).
+// The mutation check of the GPU tests (tools/kernel_mutation.py) plants its
+// mistakes into a patched copy of this
 // source; the product source carries none.
 //
 // The tile partial (grass_internal.h) is a FIXED function of the tile's data:

@@ -14,12 +14,17 @@
 //                  parameter, 2 B, instead), m, v (4 B each) and writes master,
 //                  m, v (4 B each) and the bf16 parameter RNE(master') (2 B):
 //                  28 B/param; K1 reads 2 B/param.
-//   P2P     true: data-parallel step over peer memory: the
-//           consumers read the gradient of every rank straight from its HBM
-//           (NVLink) and sum them in ascending rank order, and the producer
-//           bulk-stores theta' into every rank's parameter buffer — the
-//           reduce-scatter, the update and the all-gather in one kernel, tile
-//           by tile.  Each rank updates only its own element shard.
+//   P2P     true: data-parallel step with the gradient summed in the kernel
+//           (R20): the producer bulk-copies every rank's gradient slice of the
+//           unit into a gradient ring and the consumers add them in ascending
+//           rank order in fp32.  GRASS_DP_P2P (Batch::ntpeer = W, SURVEY 8(f)
+//           f2): the slices are read straight from the peers' HBM (NVLink) and
+//           theta' is bulk-stored into every rank's parameter buffer — the
+//           gradient reduction, the update and the all-gather in one kernel,
+//           tile by tile.  GRASS_DP_NCCL (ntpeer = 0): the slices are the
+//           local copies the NCCL exchange received; theta' goes to this
+//           rank's buffer (then ncclAllGather).  Each rank updates only its
+//           own element shard.
 //
 // Stage layout (bytes, every region 16-byte aligned):
 //   [g: kUnit*GB][theta/master: kUnit*4][m: kUnit*4][v: kUnit*4][bf16 theta: kUnit*2 (BF16)]
@@ -78,11 +83,8 @@ __device__ __forceinline__ float seg_g(const Seg& sg, int64_t idx) {
   return BF16 ? bf2f(sg.g16[idx]) : sg.g[idx];
 }
 
-#ifndef GRASS_K1_DRAIN  // A/B only (wrong norms): K1 consumers hand every full unit back untouched
-#define GRASS_K1_DRAIN 0
-#endif
-#ifndef GRASS_WAIT_ONE_LANE  // A/B: one lane per warp polls the full barrier
-#define GRASS_WAIT_ONE_LANE 0
+#ifndef GRASS_K1_DRAIN  // diagnostic only (wrong norms): K1 consumers hand every full unit back
+#define GRASS_K1_DRAIN 0  // untouched — the ring's own speed (the K3 finding)
 #endif
 
 // Eq. 2: the value of one consumer thread in one tile — the sum of the squares
@@ -389,15 +391,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     const int ntiles = (ne + (int)kTile - 1) / (int)kTile;
     char* stg = sbuf + (size_t)stage * L::bytes;
     const int64_t pe0 = P2P ? sg.poff + e0 : 0;  // full-layer index of the unit's element 0
-    if (kRing) {
-      if (GRASS_WAIT_ONE_LANE) {  // A/B: one lane polls the barrier, the warp follows
-        if (lane == 0) mbar_wait(&full_bar[stage], (i / STAGES) & 1);
-        __syncwarp();
-        mbar_wait(&full_bar[stage], (i / STAGES) & 1);  // completes at once; orders the warp's reads after the phase
-      } else {
-        mbar_wait(&full_bar[stage], (i / STAGES) & 1);
-      }
-    }
+    if (kRing) mbar_wait(&full_bar[stage], (i / STAGES) & 1);
     if (L::SEP) mbar_wait(&outfree_bar[stage], (i / STAGES) & 1);
     // full norm-only units: the TPS tiles form groups of GS (a power of two);
     // slot t of this lane holds tile perm(t) = (t / GS) * GS + ((t % GS) ^ pm)
