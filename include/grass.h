@@ -352,7 +352,9 @@ grass_status grass_load_state(grass_ctx* ctx, const char* path);
  * When enabled, every device operation the context issues is bracketed by
  * timing events on the stream it runs on; grass_trace_read returns them as
  * [start, end) in ms relative to the enable / previous read, in issue order,
- * and clears the trace.  Tracing adds two event records per operation. */
+ * and clears the trace — one event per (layer, range) an operation touches (a
+ * multi-layer update launch yields one event per layer, same times).  Tracing
+ * adds two event records per operation. */
 typedef enum {
   GRASS_TRACE_H2D = 0,    /* optimizer states host -> device (offload fetch)   */
   GRASS_TRACE_UPDATE = 1, /* fused norm + AdamW launch (K2)                     */
@@ -365,10 +367,17 @@ typedef enum {
 
 typedef struct grass_trace_event {
   int32_t kind;     /* grass_trace_kind */
-  int32_t layer;    /* layer id (first layer of a multi-layer launch) */
+  int32_t layer;    /* layer id (norm-only launches: the first layer of the launch) */
   int64_t offset;   /* first element of the range within the layer shard */
   int64_t count;    /* elements */
   float start_ms, end_ms;
+  /* the optimizer-state range the operation touches, as addresses of its m
+   * array (v / master follow the same layout): state_dev = device copy (ring
+   * slot, cache slot or resident state; 0 if none), state_host = pinned host
+   * copy (0 if none).  Lets a checker find every pair of operations on the
+   * same state and verify their order on the GPU timeline (race check of the
+   * offload pipeline, tests/test_gpu_parity.py). */
+  uint64_t state_dev, state_host;
 } grass_trace_event;
 
 grass_status grass_trace_enable(grass_ctx* ctx, int32_t on);

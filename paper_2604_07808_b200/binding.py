@@ -37,7 +37,8 @@ class GrassError(RuntimeError):
 
 class TraceEvent(C.Structure):
     _fields_ = [("kind", C.c_int32), ("layer", C.c_int32), ("offset", C.c_int64),
-                ("count", C.c_int64), ("start_ms", C.c_float), ("end_ms", C.c_float)]
+                ("count", C.c_int64), ("start_ms", C.c_float), ("end_ms", C.c_float),
+                ("state_dev", C.c_uint64), ("state_host", C.c_uint64)]
 
 
 TRACE_KINDS = {0: "h2d", 1: "update", 2: "d2h", 3: "norm", 4: "rs", 5: "ag", 6: "p2p"}
@@ -460,7 +461,8 @@ class Grass:
         n = C.c_int32()
         _check(lib().grass_trace_read(self._h, buf, capacity, C.byref(n)), self._h)
         return [{"kind": TRACE_KINDS[e.kind], "layer": e.layer, "offset": e.offset,
-                 "count": e.count, "start_ms": e.start_ms, "end_ms": e.end_ms}
+                 "count": e.count, "start_ms": e.start_ms, "end_ms": e.end_ms,
+                 "state_dev": e.state_dev, "state_host": e.state_host}
                 for e in buf[:min(n.value, capacity)]]
 
     def prefetch_layers(self, layer_ids: Sequence[int], stream=None):

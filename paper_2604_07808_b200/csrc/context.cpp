@@ -286,7 +286,11 @@ grass_status flush(grass_ctx* c, Batch* b, bool update, cudaStream_t s) {
     for (int i = 0; i < b->nseg; ++i) n += b->seg[i].n;
     const Seg& s0 = b->seg[0];
     TraceScope ts(c, s, update ? GRASS_TRACE_UPDATE : GRASS_TRACE_NORM, s0.layer,
-                  (s0.part_index - s0.part_layer_base) * kTile, n);
+                  (s0.part_index - s0.part_layer_base) * kTile, update ? s0.n : n, update ? s0.m : nullptr);
+    for (int i = 1; update && i < b->nseg; ++i) {  // every layer range the update touches
+      const Seg& si = b->seg[i];
+      ts.add(si.layer, (si.part_index - si.part_layer_base) * kTile, si.n, si.m);
+    }
     CUDA_TRY(c, launch_fused(update, *b, c->st, update ? c->grid_update : c->grid_norm, s));
   }
   c->launches++;

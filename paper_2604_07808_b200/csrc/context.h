@@ -110,10 +110,16 @@ struct grass_ctx {
               ev_k2[2] = {nullptr, nullptr};
 
   // tracing (grass_trace_enable): timing events around every device operation
-  struct TraceRec {
-    int32_t kind, layer;
+  struct TraceAccess {  // one (layer, range) an operation touches
+    int32_t layer;
     int64_t off, n;
+    const void* dev;   // m-array address of the touched state range (device copy), or NULL
+    const void* host;  // m-array address of the touched state range (pinned host copy), or NULL
+  };
+  struct TraceRec {  // one device operation: one event per access in grass_trace_read
+    int32_t kind;
     cudaEvent_t e0, e1;
+    std::vector<TraceAccess> acc;
   };
   bool tracing = false;
   cudaEvent_t trace_base = nullptr;
@@ -194,7 +200,9 @@ struct TraceScope {
   grass_ctx* c;
   cudaStream_t s;
   int idx = -1;
-  TraceScope(grass_ctx* c_, cudaStream_t s_, int kind, int layer, int64_t off, int64_t n) : c(c_), s(s_) {
+  TraceScope(grass_ctx* c_, cudaStream_t s_, int kind, int layer, int64_t off, int64_t n,
+             const void* dev = nullptr, const void* host = nullptr)
+      : c(c_), s(s_) {
     nvtx_push(kind, layer);
     if (!c->tracing) return;
     cudaEvent_t e[2];
@@ -207,8 +215,12 @@ struct TraceScope {
       }
     }
     if (cudaEventRecord(e[0], s) != cudaSuccess) return;
-    c->trace.push_back({kind, layer, off, n, e[0], e[1]});
+    c->trace.push_back({kind, e[0], e[1], {{layer, off, n, dev, host}}});
     idx = (int)c->trace.size() - 1;
+  }
+  // a further (layer, range) of the same operation (multi-segment launches)
+  void add(int layer, int64_t off, int64_t n, const void* dev, const void* host = nullptr) {
+    if (idx >= 0) c->trace[idx].acc.push_back({layer, off, n, dev, host});
   }
   ~TraceScope() {
     if (idx >= 0) cudaEventRecord(c->trace[idx].e1, s);

@@ -305,21 +305,29 @@ grass_status grass_trace_read(grass_ctx* c, grass_trace_event* out, int32_t capa
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
   CUDA_TRY(c, cudaDeviceSynchronize());
-  *count = (int32_t)c->trace.size();
-  for (int i = 0; i < (int)c->trace.size(); ++i) {
-    const auto& r = c->trace[i];
-    if (i < capacity) {
-      grass_trace_event& e = out[i];
-      e.kind = r.kind;
-      e.layer = r.layer;
-      e.offset = r.off;
-      e.count = r.n;
-      CUDA_TRY(c, cudaEventElapsedTime(&e.start_ms, c->trace_base, r.e0));
-      CUDA_TRY(c, cudaEventElapsedTime(&e.end_ms, c->trace_base, r.e1));
+  int32_t k = 0;
+  for (const auto& r : c->trace) {
+    float t0 = 0.f, t1 = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&t0, c->trace_base, r.e0));
+    CUDA_TRY(c, cudaEventElapsedTime(&t1, c->trace_base, r.e1));
+    for (const auto& a : r.acc) {  // one event per (layer, range) the operation touched
+      if (k < capacity) {
+        grass_trace_event& e = out[k];
+        e.kind = r.kind;
+        e.layer = a.layer;
+        e.offset = a.off;
+        e.count = a.n;
+        e.state_dev = reinterpret_cast<uintptr_t>(a.dev);
+        e.state_host = reinterpret_cast<uintptr_t>(a.host);
+        e.start_ms = t0;
+        e.end_ms = t1;
+      }
+      ++k;
     }
     c->trace_pool.push_back(r.e0);
     c->trace_pool.push_back(r.e1);
   }
+  *count = k;
   c->trace.clear();
   CUDA_TRY(c, cudaEventRecord(c->trace_base, c->aux));
   return GRASS_OK;

@@ -55,7 +55,7 @@ grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, co
     if (overlap && c->slot_used[slot]) CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_free[slot], 0));
     char* gslot = g_host ? c->d_gring + (size_t)slot * c->chunk * c->esz : nullptr;
     {
-      TraceScope ts(c, sh, GRASS_TRACE_H2D, l, off, n);
+      TraceScope ts(c, sh, GRASS_TRACE_H2D, l, off, n, ring[0], c->arr[0][l] + off);
       // every state array is fetched, the bf16 master too even on the layer's
       // first update (then the kernel initialises it from the bf16 parameter
       // and never reads it): the decision is the device's (DevState::init_now),
@@ -76,7 +76,7 @@ grass_status offload_layer(grass_ctx* c, int l, const Seg& base, void* param, co
       CUDA_TRY(c, cudaStreamWaitEvent(sd, c->ev_comp[slot], 0));
     }
     {
-      TraceScope ts(c, sd, GRASS_TRACE_D2H, l, off, n);
+      TraceScope ts(c, sd, GRASS_TRACE_D2H, l, off, n, ring[0], c->arr[0][l] + off);
       for (int a = 0; a < c->ns; ++a)
         CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][l] + off, ring[a], bytes, cudaMemcpyDeviceToHost, sd));
     }
@@ -178,7 +178,8 @@ grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, const Seg&
   for (int64_t off = 0; off < std::max(ll, lv); off += c->chunk) {
     if (off < lv) {
       const size_t vb = sizeof(float) * (size_t)std::min(c->chunk, lv - off);
-      TraceScope ts(c, sd, GRASS_TRACE_D2H, victim, off, (int64_t)(vb / sizeof(float)));
+      TraceScope ts(c, sd, GRASS_TRACE_D2H, victim, off, (int64_t)(vb / sizeof(float)), cache_arr(c, slot, 0) + off,
+                    c->arr[0][victim] + off);
       for (int a = 0; a < c->ns; ++a)
         CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][victim] + off, cache_arr(c, slot, a) + off, vb,
                                     cudaMemcpyDeviceToHost, sd));
@@ -191,7 +192,7 @@ grass_status swap_in_layer(grass_ctx* c, int l, int slot, int victim, const Seg&
       const int64_t n = std::min(c->chunk, ll - off);
       const size_t bytes = sizeof(float) * (size_t)n;
       {
-        TraceScope ts(c, sh, GRASS_TRACE_H2D, l, off, n);
+        TraceScope ts(c, sh, GRASS_TRACE_H2D, l, off, n, cache_arr(c, slot, 0) + off, c->arr[0][l] + off);
         for (int a = 0; a < c->ns; ++a)
           if (!(a == 2 && init))
             CUDA_TRY(c, cudaMemcpyAsync(cache_arr(c, slot, a) + off, c->arr[a][l] + off, bytes,
@@ -233,7 +234,8 @@ grass_status prefetch_into(grass_ctx* c, int l, int slot, int victim) {
   for (int64_t off = 0; off < std::max(ll, lv); off += c->chunk) {
     if (off < lv) {
       const size_t vb = sizeof(float) * (size_t)std::min(c->chunk, lv - off);
-      TraceScope ts(c, c->d2h, GRASS_TRACE_D2H, victim, off, (int64_t)(vb / sizeof(float)));
+      TraceScope ts(c, c->d2h, GRASS_TRACE_D2H, victim, off, (int64_t)(vb / sizeof(float)),
+                    cache_arr(c, slot, 0) + off, c->arr[0][victim] + off);
       for (int a = 0; a < c->ns; ++a)
         CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][victim] + off, cache_arr(c, slot, a) + off, vb,
                                     cudaMemcpyDeviceToHost, c->d2h));
@@ -244,7 +246,7 @@ grass_status prefetch_into(grass_ctx* c, int l, int slot, int victim) {
     }
     if (off < ll) {
       const int64_t n = std::min(c->chunk, ll - off);
-      TraceScope ts(c, c->h2d, GRASS_TRACE_H2D, l, off, n);
+      TraceScope ts(c, c->h2d, GRASS_TRACE_H2D, l, off, n, cache_arr(c, slot, 0) + off, c->arr[0][l] + off);
       for (int a = 0; a < c->ns; ++a)
         if (!(a == 2 && !c->master_valid[l]))
           CUDA_TRY(c, cudaMemcpyAsync(cache_arr(c, slot, a) + off, c->arr[a][l] + off,
@@ -279,7 +281,8 @@ grass_status writeback_release(grass_ctx* c, int l, int slot, cudaStream_t s) {
   const int64_t len = c->shard_len[l];
   for (int64_t off = 0; off < len; off += c->chunk) {
     const size_t bytes = sizeof(float) * (size_t)std::min(c->chunk, len - off);
-    TraceScope ts(c, sd, GRASS_TRACE_D2H, l, off, (int64_t)(bytes / sizeof(float)));
+    TraceScope ts(c, sd, GRASS_TRACE_D2H, l, off, (int64_t)(bytes / sizeof(float)), cache_arr(c, slot, 0) + off,
+                  c->arr[0][l] + off);
     for (int a = 0; a < c->ns; ++a)
       CUDA_TRY(c, cudaMemcpyAsync(c->arr[a][l] + off, cache_arr(c, slot, a) + off, bytes, cudaMemcpyDeviceToHost, sd));
   }

@@ -1,4 +1,4 @@
 set -x
 cd $GRAFT_REPO_ROOT
-timeout 600 python tools/e2e_chunk_sweep.py > gpurun_out/r17_e2e_chunks.log 2>&1
-timeout 900 python bench.py --legs main,train --steps 10 > gpurun_out/r17_bench_train.json 2> gpurun_out/r17_bench_train.err
+timeout 900 python -m pytest tests/test_gpu_race.py -q -p no:cacheprovider --timeout 300 > gpurun_out/r19_race.log 2>&1; echo "rc=$?" >> gpurun_out/r19_race.log
+timeout 1200 python tools/kernel_mutation.py run 17 18 19 > gpurun_out/r19_mut.log 2>&1

@@ -20,6 +20,8 @@ OUTDIR = os.path.join(ROOT, "build", "mutants")
 SRCDIR = os.path.join(ROOT, "build", "msrc")
 K = "kernels.cu"
 S = "stream_kernel.cuh"
+OFF = "offload.cpp"
+HOT = "hot_path.cpp"
 
 # k: (what, [(file, product text, mutated text), ...]) — every product text
 # must occur in the file (all occurrences are replaced)
@@ -57,6 +59,13 @@ MUTANTS = {
          [(S, "      s = __fmaf_rn(w, w, s);", "      s = __fmaf_rn(w, 0.f, s);")]),
     15: ("bf16 norm: the fp32 8-square sum used even where it underflows (no exact fallback)",
          [(S, "  return __float_as_uint(s) - 0x0D800000u <= 0x7F7FFFFFu - 0x0D800000u;", "  return true;")]),
+    17: ("offload: a chunk's fetch does not wait for the ring slot's previous write-back",
+         [(OFF, "    if (overlap && c->slot_used[slot]) CUDA_TRY(c, cudaStreamWaitEvent(sh, c->ev_free[slot], 0));\n", "")]),
+    18: ("offload: a layer's fetch does not wait for its previous step's write-back",
+         [(OFF, "  if (overlap && c->layer_done_valid[l])  // previous write-back of this layer\n"
+                "    CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, c->ev_layer_done[l], 0));\n", "")]),
+    19: ("period residency: a victim's write-back does not wait for the updates before it",
+         [(HOT, "    if (c->cfg.overlap && (s = wait_pending(c, c->d2h)) != GRASS_OK) return s;\n", "")]),
     14: ("P2P barrier self-test: start barrier removed",
          [(K, "    a.which = 0;  // start barrier: every rank has read its rows of this round\n"
               "    const int n_save = a.n;\n    a.n = 0;\n    p2p_sync_cta(a);\n    a.n = n_save;\n", "")]),
@@ -66,7 +75,7 @@ TESTS = ("test_step_layers_vs_oracle_multi_step or test_norms_ragged_sizes_vs_or
          "test_zero_grad_zero_state_is_identity_on_theta or test_nonfinite_gradient_reported_and_not_recorded or "
          "test_norms_probe_equals_update_bitwise or test_norms_integer_grads_exact_bf16 or "
          "test_p2p_barrier_protocol_selftest or test_bf16_norms_tiny_and_huge_gradients or "
-         "test_norms_all_tiles_reduction_keeps_each_tile_apart")
+         "test_norms_all_tiles_reduction_keeps_each_tile_apart or test_offload_pipeline_happens_before_under_stress")
 
 
 def patched_source(k: int) -> str:
@@ -92,18 +101,21 @@ def build(only=()):
         print("built mutant", k, flush=True)
 
 
-def run():
+def run(only=()):
     res = {}
     for k, (what, _) in MUTANTS.items():
+        if only and k not in only:
+            continue
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_m{k}.so"))
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                            "tests/test_gpu_parity.py", "tests/test_gpu_p2p.py", "-k", TESTS],
+                            "tests/test_gpu_parity.py", "tests/test_gpu_p2p.py", "tests/test_gpu_race.py",
+                            "-k", TESTS],
                            cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
         failed = [l for l in r.stdout.splitlines() if l.startswith("FAILED")]
         res[k] = {"mutation": what, "killed": r.returncode != 0, "by": failed[:1]}
         print(k, res[k], flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "kernel_mutation.json"), "w") as f:
+    with open(os.path.join(ROOT, "gpurun_out", "kernel_mutation" + ("_subset" if only else "") + ".json"), "w") as f:
         json.dump(res, f, indent=1)
     killed = sum(v["killed"] for v in res.values())
     print(f"{killed}/{len(res)} kernel mutations killed by the GPU parity tests")
@@ -118,4 +130,4 @@ if __name__ == "__main__":
         sys.exit(0)
     if sys.argv[1:2] == ["build"]:
         sys.exit(build([int(x) for x in sys.argv[2:]]))
-    sys.exit(run())
+    sys.exit(run([int(x) for x in sys.argv[2:]]))
