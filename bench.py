@@ -979,6 +979,9 @@ def run_grass(args, rank, world, local):
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "grass_stream_kernel<true,1,2> (fused Eq.2 norm + AdamW, TMA bulk-copy ring)",
                          "kernel_ms": kernel_ms, "peak_kind": peak_kind,
+                         "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of this "
+                                           "kernel at this config (profiles/ncu_traffic.json, from "
+                                           "profiles/r02_ncu_full.md)" if traffic else None,
                          "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             # world > 1: the NCCL gradient exchange (grouped send/recv of the
