@@ -12,11 +12,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
     "base": [],
-    "k2_grid148": ["GRASS_UPD_GRID_SUB=0"],
-    "k2_grid140": ["GRASS_UPD_GRID_SUB=8"],
-    "k2_grid120": ["GRASS_UPD_GRID_SUB=28"],
-    "k2_grid112": ["GRASS_UPD_GRID_SUB=36"],
-    "k2_stages3": ["GRASS_UPD_STAGES=3"],
+    "p2p_norm_tps6": ["GRASS_P2P_NORM_TPS=6"],
+    "p2p_norm_tps8": ["GRASS_P2P_NORM_TPS=8"],
+    "p2p_norm_tps2": ["GRASS_P2P_NORM_TPS=2"],
     "base_again": [],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
@@ -30,7 +28,7 @@ def build():
         print("built", name)
 
 
-def run(legs="main,bf16", extra=()):
+def run(legs="main,p2p", extra=()):
     res = {}
     for name in VARIANTS:
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_{name}.so"))
