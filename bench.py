@@ -431,8 +431,13 @@ def run_grass(args, rank, world, local):
                         "read_ceiling": read_ceiling,
                         "bytes": BYTES_PER_PARAM_PROBE * NL * n_p // world}
 
-    # ---- main leg: configs[1]
-    def one_step(step, timing):
+    # ---- main leg: configs[1].  World 1: the device-resident schedule — each
+    # step is grass_device_step (update of the layers sampled on the device,
+    # commit, resample of the next period), no host round trip between steps.
+    # World > 1: the host-driven loop (step_layers, update_probs, sample_layers).
+    use_dev = world == 1
+
+    def host_step(step, timing):
         nonlocal ids
         if timing is not None:
             timing[0].record(s)
@@ -441,6 +446,18 @@ def run_grass(args, rank, world, local):
             timing[1].record(s)
         ctx.update_probs()
         ids = ctx.sample_layers(step + 1)
+
+    def dev_step(step, timing):
+        if timing is not None:
+            timing[0].record(s)
+        ctx.device_step(args.lr, stream=s)
+        if timing is not None:
+            timing[1].record(s)
+
+    one_step = dev_step if use_dev else host_step
+    if use_dev:
+        ctx.register_layers(params, grads)
+        ctx.device_schedule_begin(0, stream=s)
 
     for w in range(args.warmup):
         one_step(w, None)
@@ -458,10 +475,33 @@ def run_grass(args, rank, world, local):
         t1.record(s)
         torch.cuda.synchronize()
     launches = ctx.launch_count - launches0
+    if use_dev:
+        ids = ctx.device_schedule_end()
     barrier(world)
     elapsed = max_over_ranks(t0.elapsed_time(t1) / 1e3, world, dev)
     kernel_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
     active = gamma * n_p
+    host_schedule = None
+    if use_dev and "main" in legs:
+        # the same step driven from the host (grass_step_layers + grass_update_probs
+        # + grass_sample_layers): the host round trip per step, for comparison
+        for w in range(3):
+            host_step(10_000 + w, None)
+        torch.cuda.synchronize()
+        hev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(s)
+        for k in range(args.steps):
+            host_step(10_100 + k, hev[k])
+        h1.record(s)
+        torch.cuda.synchronize()
+        hms = h0.elapsed_time(h1) / args.steps
+        gaps = [hev[i][1].elapsed_time(hev[i + 1][0]) for i in range(args.steps - 1)]
+        host_schedule = {"step_ms": hms, "params_per_s": active / (hms / 1e3),
+                         "gpu_idle_between_steps_us": statistics.median(gaps) * 1e3 if gaps else None,
+                         "what": "the same step through grass_step_layers + grass_update_probs + "
+                                 "grass_sample_layers (host commit and sampler, one host round trip per step)"}
     value = args.steps * active / elapsed
     achieved = BYTES_PER_PARAM_UPDATE * active / world / (kernel_ms / 1e3) / 1e9
     traffic = None
@@ -977,13 +1017,18 @@ def run_grass(args, rank, world, local):
             "config": workload_config(args.model, gamma, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "grass_stream_kernel<true,1,2> (fused Eq.2 norm + AdamW, TMA bulk-copy ring)",
+                         "kernel": "grass_stream_kernel<true,1,2> (fused Eq.2 norm + AdamW, TMA bulk-copy ring); "
+                                   "kernel_ms = events around one step's launches (prologue, K2, K3"
+                                   + (", commit + resample)" if use_dev else ")"),
                          "kernel_ms": kernel_ms, "peak_kind": peak_kind,
                          "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of this "
                                            "kernel at this config (profiles/ncu_traffic.json, from "
                                            "profiles/r02_ncu_full.md)" if traffic else None,
                          "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "step_driver": ("grass_device_step: update of the layers sampled on the device, then the commit "
+                            "(Eq. 2/4/3) and resample kernel — no host round trip between steps"
+                            if use_dev else "host: grass_step_layers + grass_update_probs + grass_sample_layers"),
             # world > 1: the NCCL gradient exchange (grouped send/recv of the
             # slices, summed in rank order by the update kernel) + all-gather of
             # the parameters, (W-1)/W of 4 B per active parameter each, per rank
@@ -992,7 +1037,7 @@ def run_grass(args, rank, world, local):
                         if world > 1 else None),
             "clocks": clk.summary(), "probe": out.get("probe"), "offload": offload,
             "offload_period": offload_period, "bf16": bf16, "train_step": train, "p2p": p2p,
-            "paper_schedule": paper_schedule,
+            "paper_schedule": paper_schedule, "host_schedule": host_schedule,
             "paper_context": {
                 "hardware": "2 x H100 80GB, precision not stated (PAPER.md:410)",
                 "overlap_speedup": {"paper": 1.08, "what": "training throughput, overlapped vs "

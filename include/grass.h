@@ -323,6 +323,41 @@ grass_status grass_read_state(grass_ctx* ctx, int32_t layer, float* m_out, float
  * after the caller's earlier work.  GRASS_E_STATE without period residency. */
 grass_status grass_prefetch_layers(grass_ctx* ctx, const int32_t* layer_ids, int32_t n, void* stream);
 
+/* ----- device-resident schedule (DESIGN.md §8 "Device-resident schedule") -
+ * The adaptive step — update of the sampled layers (+ always-active groups),
+ * then commit (Eq. 2 window mean, Eq. 4 EMA, Eq. 3 softmax) and resample
+ * — with the sampled ids, m, p and the window kept in device
+ * memory, so consecutive steps need no host round trip and a whole step is
+ * one capturable sequence of launches (CUDA graphs).  The arithmetic is the
+ * host path's (grass_update_probs / grass_sample_layers) in the same order;
+ * only exp() may differ from the host's by an ulp.  HBM-resident states,
+ * world = 1, no clipping.
+ *
+ * grass_register_layers: the parameter / gradient buffers of ALL n = n_layers
+ * layers (device pointers, N_p elements each, fp32 or bf16 by param_dtype;
+ * caller-owned, must stay valid while the schedule runs).  Validated once.
+ *
+ * grass_device_schedule_begin: copies the host MGN state (m, p, committed) to
+ * the device and samples the ids of `period` there (stream-ordered).
+ *
+ * grass_device_step: stream-ordered, no synchronisation: t_l += 1 and the
+ * fused norm + AdamW of the layers sampled on the device (+ the always-active
+ * groups), then, if do_commit, the commit, and, if do_resample, the ids of
+ * `next_period` — GRASS_PERIOD_NEXT: the period after the current one, kept
+ * on the device, so a captured step replays with advancing periods.  lr as
+ * grass_step_layers (grass_set_lr_device applies).
+ *
+ * grass_device_schedule_end: synchronises; copies m, p, committed and the
+ * current ids (ids_out: host [gamma], may be NULL) back to the host context;
+ * GRASS_E_NONFINITE / GRASS_E_STATE if a commit met a non-finite norm or an
+ * empty window (the schedule stopped committing there). */
+#define GRASS_PERIOD_NEXT 0xFFFFFFFFFFFFFFFFull
+grass_status grass_register_layers(grass_ctx* ctx, int32_t n, void* const* params, const void* const* grads);
+grass_status grass_device_schedule_begin(grass_ctx* ctx, uint64_t period, void* stream);
+grass_status grass_device_step(grass_ctx* ctx, float lr, int32_t do_commit, int32_t do_resample,
+                               uint64_t next_period, void* stream);
+grass_status grass_device_schedule_end(grass_ctx* ctx, int32_t* ids_out);
+
 /* GRASS_RESIDENCY_PERIOD: writes the m/v of every layer cached in HBM back to
  * its pinned host home (the cache stays valid).  No-op otherwise.
  * Synchronises. */

@@ -123,6 +123,10 @@ _SIGS = {
                                      C.POINTER(C.c_int32)]),
     "grass_ipc_import": (C.c_int, [C.c_int32, C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
     "grass_enable_peer_access": (C.c_int, [C.c_int32, C.c_int32]),
+    "grass_register_layers": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "grass_device_schedule_begin": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p]),
+    "grass_device_step": (C.c_int, [C.c_void_p, C.c_float, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p]),
+    "grass_device_schedule_end": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
 }
 
 
@@ -358,6 +362,34 @@ class Grass:
         isz = 2 if self.bf16 else 4
         _check(f(self._h, ids, len(layer_ids), _ptrs(params, isz), _ptrs(grads, isz, host_ok=True),
                  float(lr), _stream_ptr(stream)), self._h)
+
+    # device-resident schedule ------------------------------------------------
+    PERIOD_NEXT = (1 << 64) - 1
+
+    def register_layers(self, params, grads):
+        """The buffers of every layer (the device schedule reads them by id)."""
+        isz = 2 if self.bf16 else 4
+        if len(params) != self.n_layers or len(grads) != self.n_layers:
+            raise ValueError("one parameter and one gradient buffer per layer")
+        self._registered = (list(params), list(grads))      # keep them alive
+        _check(lib().grass_register_layers(self._h, self.n_layers, _ptrs(params, isz), _ptrs(grads, isz)), self._h)
+
+    def device_schedule_begin(self, period: int, stream=None):
+        _check(lib().grass_device_schedule_begin(self._h, period, _stream_ptr(stream)), self._h)
+
+    def device_step(self, lr: float, commit: bool = True, resample: bool = True,
+                    next_period: int | None = None, stream=None):
+        """Update the device-sampled layers, then (optionally) commit and
+        resample — no host synchronisation; next_period None = the next one."""
+        per = self.PERIOD_NEXT if next_period is None else int(next_period)
+        _check(lib().grass_device_step(self._h, float(lr), int(commit), int(resample), per,
+                                       _stream_ptr(stream)), self._h)
+
+    def device_schedule_end(self):
+        """Synchronises; the current sampled ids (host state updated)."""
+        out = (C.c_int32 * self.gamma)()
+        _check(lib().grass_device_schedule_end(self._h, out), self._h)
+        return list(out)
 
     def sync(self):
         _check(lib().grass_sync(self._h), self._h)

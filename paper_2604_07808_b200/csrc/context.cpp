@@ -386,6 +386,11 @@ void free_ctx(grass_ctx* c) {
   dfree(c->d_gather);
   dfree(c->d_gscratch);
   dfree(c->d_rtab);
+  dfree(c->d_segtab);
+  dfree(c->d_sched);
+  dfree(c->d_mgn_m);
+  dfree(c->d_probs);
+  dfree(c->d_period);
   dfree(c->d_coef);
   dfree(c->d_ring);
   dfree(c->d_gring);

@@ -136,6 +136,15 @@ struct grass_ctx {
   unsigned long long* d_epoch = nullptr;  // device [2]: start / end barrier generations
   std::vector<int32_t> p2p_pending;  // p2p_sync = 0: layers whose MGN finish is pending
 
+  // device-resident schedule (device_schedule.cpp)
+  Seg* d_segtab = nullptr;      // device [nl]: whole-layer segment of every registered layer
+  std::vector<char> registered;
+  int32_t* d_sched = nullptr;   // device block: ids [kMaxDevSeg] | avail [nl] | committed | err
+  double* d_mgn_m = nullptr;    // device [nl] committed MGN
+  double* d_probs = nullptr;    // device [nl]
+  unsigned long long* d_period = nullptr;  // device: sampling period of the current ids
+  bool dev_sched = false;       // between grass_device_schedule_begin and _end
+
   Comm comm;
   bool has_comm = false;
   bool dp = false;  // data-parallel (NCCL) path: world > 1, or world = 1 with a unique id

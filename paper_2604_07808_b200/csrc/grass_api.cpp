@@ -110,6 +110,7 @@ grass_status grass_step_layers_bf16(grass_ctx* c, const int32_t* ids, int32_t n,
 
 grass_status grass_update_probs(grass_ctx* c, double* probs_out) try {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (c->dev_sched) return c->fail(GRASS_E_STATE, "a device schedule is running (grass_device_schedule_end first)");
   // one stream-ordered snapshot: S, c, flag -> host; window and flag reset
   grass_status s = fetch_mgn(c, true, true);
   if (s != GRASS_OK) return s;

@@ -78,7 +78,14 @@ struct Batch {
   float gscale;            // multiplies every gradient element on load (DP: 1/world), else 1
   int32_t npeer;           // DP: ranks whose gradients are summed in the kernel (Seg::gpeer), else 0
   int32_t ntpeer;          // P2P: ranks whose parameter buffers receive theta' (Seg::tpeer), else 0
+  // device-resident schedule (grass_device_step): the launch's segments are
+  // dev_table[dev_ids[j]] for j < dev_n (ids read on the device, ascending),
+  // instead of seg[] / nseg
+  const Seg* dev_table;    // device [n_layers]: the whole-layer segment of every layer
+  const int32_t* dev_ids;  // device [dev_n]
+  int32_t dev_n;
 };
+constexpr int kMaxDevSeg = 32;  // layers one device-scheduled launch may update (gamma + n_always)
 
 // Device-resident MGN / reduction state (all arrays indexed by layer id unless noted).
 struct DevState {
@@ -102,6 +109,7 @@ struct DevState {
 struct PrologueArgs {
   int32_t n;
   int32_t layer[kMaxSeg];
+  const int32_t* dev_ids;  // device-resident schedule: layer j = dev_ids[j] (instead of layer[])
   float lr;
   const float* lr_ptr;
   double beta1, beta2, wd;
@@ -112,6 +120,8 @@ cudaError_t launch_step_prologue(const PrologueArgs& a, const DevState& st, cuda
 // kernels.cu
 cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int grid,
                          cudaStream_t s);
+// K2 of the device-resident schedule (Batch::dev_table / dev_ids).
+cudaError_t launch_fused_dev(const Batch& b, const DevState& st, int grid, cudaStream_t s);
 // K3 for the layers whose last tiles a stream launch wrote: one CTA each.
 struct FinalizeArgs {
   int32_t n;               // layers
@@ -121,7 +131,25 @@ struct FinalizeArgs {
   int32_t out_slot[kMaxSeg];
   int64_t base[kMaxSeg];   // index of the layer's tile 0 in DevState::partials
   int64_t numel[kMaxSeg];  // N_p(l)
+  const Seg* dev_table;    // device-resident schedule: layer j = dev_ids[j], geometry from dev_table
+  const int32_t* dev_ids;
 };
+// Device-resident commit + resample (grass_device_step): the host's
+// grass_update_probs + grass_sample_layers arithmetic, in fp64 on one thread.
+struct CommitArgs {
+  int32_t nsamp, nl, gamma, policy, normalize, T_p;
+  int32_t do_commit, do_sample;
+  double alpha, tau;
+  uint64_t seed, period;
+  double* m;               // device [nl] committed MGN
+  double* probs;           // device [nl]
+  int32_t* committed;      // device: a commit has happened
+  int32_t* ids;            // device [gamma]: the sampled layers (draw order)
+  int32_t* avail;          // device [nl] scratch
+  int32_t* err;            // device: 1 = commit with zero observations, 2 = non-finite gradient (sticky)
+  unsigned long long* period_ctr;  // device: the period of the current ids; period == ~0: resample for ++ctr
+};
+cudaError_t launch_commit_sample(const CommitArgs& a, const DevState& st, cudaStream_t s);
 cudaError_t launch_finalize(const FinalizeArgs& a, const DevState& st, cudaStream_t s);
 // world > 1: per-layer total = fixed ascending-rank sum of the all-gathered
 // shard partials gathered[r * total_slots + slot], then the MGN update.

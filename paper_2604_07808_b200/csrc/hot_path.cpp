@@ -78,6 +78,7 @@ grass_status offload_capture_fence(grass_ctx* c, cudaStream_t st, bool capturing
 grass_status mgn_accumulate_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_t n,
                                  const void* const* grads, void* stream) {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (c->dev_sched) return c->fail(GRASS_E_STATE, "a device schedule is running (grass_device_schedule_end first)");
   if (!grads) return c->fail(GRASS_E_INVALID, "grads is NULL");
   std::vector<int> order;
   grass_status s = check_call(c, bf16_call, ids, n, grads, nullptr, &order);
@@ -137,6 +138,7 @@ grass_status mgn_accumulate_impl(grass_ctx* c, bool bf16_call, const int32_t* id
 grass_status step_layers_impl(grass_ctx* c, bool bf16_call, const int32_t* ids, int32_t n,
                               void* const* params, const void* const* grads, float lr, void* stream) {
   if (!c) return set_thread_err(GRASS_E_INVALID, "ctx is NULL");
+  if (c->dev_sched) return c->fail(GRASS_E_STATE, "a device schedule is running (grass_device_schedule_end first)");
   if (!params || !grads) return c->fail(GRASS_E_INVALID, "params/grads is NULL");
   if (!(lr >= 0.0f) || !std::isfinite(lr)) return c->fail(GRASS_E_INVALID, "lr must be finite, >= 0");
   std::vector<int> order;

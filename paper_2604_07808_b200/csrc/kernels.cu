@@ -232,27 +232,31 @@ __device__ __forceinline__ void consumer_sync() {
 }
 
 // K3: the layer total is the fixed-order sum of its tile partials — thread t
-// adds tiles t, t + 512, ... in ascending order (loads batched 8 deep, the
-// additions in the same order), then the fixed warp / block tree.  One CTA
+// (of 1024) adds tiles t, t + 1024, ... in ascending order (loads batched 16
+// deep, the additions in the same order), then the fixed warp tree and the 32
+// warp sums in ascending order.  One CTA
 // per completed layer of the preceding stream launch (grass_finalize_kernel):
 // the layers finish in parallel, not one after another in the CTA that
 // completed them last (up to ~0.4 ms at the end of a 32-layer probing pass).
-__global__ void __launch_bounds__(kThreads) grass_finalize_kernel(const __grid_constant__ FinalizeArgs fa,
-                                                                  const DevState st) {
-  __shared__ double red[kConsumerWarps];
+constexpr int kFinThreads = 1024;  // K3 threads per layer (32 warps)
+__global__ void __launch_bounds__(kFinThreads) grass_finalize_kernel(const __grid_constant__ FinalizeArgs fa,
+                                                                     const DevState st) {
+  constexpr int kW = kFinThreads / 32;
+  __shared__ double red[kW];
   const int j = blockIdx.x;
-  const int layer = fa.layer[j], n = fa.tiles[j];
-  const double* P = st.partials + fa.base[j];
+  const int layer = fa.dev_ids ? fa.dev_ids[j] : fa.layer[j];
+  const int n = fa.dev_ids ? fa.dev_table[layer].layer_tiles : fa.tiles[j];
+  const double* P = st.partials + (fa.dev_ids ? fa.dev_table[layer].part_layer_base : fa.base[j]);
   double a = 0.0;
   int i = threadIdx.x;
-  for (; i + 7 * kThreads < n; i += 8 * kThreads) {
-    double x[8];
+  for (; i + 15 * kFinThreads < n; i += 16 * kFinThreads) {  // 16 loads in flight per thread
+    double x[16];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = __ldcg(P + i + k * kThreads);
+    for (int k = 0; k < 16; ++k) x[k] = __ldcg(P + i + k * kFinThreads);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) a += x[k];
+    for (int k = 0; k < 16; ++k) a += x[k];
   }
-  for (; i < n; i += kThreads) a += __ldcg(P + i);
+  for (; i < n; i += kFinThreads) a += __ldcg(P + i);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double w = warp_sum(a);
   if (lane == 0) red[warp] = w;
@@ -260,11 +264,11 @@ __global__ void __launch_bounds__(kThreads) grass_finalize_kernel(const __grid_c
   if (threadIdx.x == 0) {
     double ss = 0.0;
 #pragma unroll
-    for (int k = 0; k < kConsumerWarps; ++k) ss += red[k];
+    for (int k = 0; k < kW; ++k) ss += red[k];
     if (fa.mode == kFinalizeMgn) {
       st.last_ss[layer] = ss;
       if (isfinite(ss)) {
-        st.S[layer] += sqrt(ss / (double)fa.numel[j]);  // Eq. 2 inner term
+        st.S[layer] += sqrt(ss / (double)(fa.dev_ids ? fa.dev_table[layer].layer_numel : fa.numel[j]));  // Eq. 2 inner term
         st.c[layer] += 1;
       } else {
         atomicMax(st.flag, INT_MAX - layer);  // smallest id wins
@@ -274,6 +278,133 @@ __global__ void __launch_bounds__(kThreads) grass_finalize_kernel(const __grid_c
     }
   }
 }
+
+// Device-resident commit + resample (grass_device_step): exactly the host's
+// grass_update_probs (Eq. 2 window mean, first commit / Eq. 4 EMA with frozen
+// retention, Eq. 3 softmax per policy, window reset) and grass_sample_layers
+// (R6 / R7: gamma sequential draws with renormalisation, counter-based
+// SplitMix64) in fp64, on one thread, in the host's operation order (the
+// library is built with --fmad=false: no contraction); only exp() may differ
+// from the host's by an ulp.  A non-finite norm or an empty commit is
+// recorded in *err (sticky) and reported by grass_device_schedule_end.
+__device__ __forceinline__ uint64_t d_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr int kCommitThreads = 256;
+__global__ void __launch_bounds__(kCommitThreads) grass_commit_sample_kernel(const __grid_constant__ CommitArgs a,
+                                                                             const DevState st) {
+  // every operand staged in shared memory by all threads; thread 0 then runs
+  // the host's sequential fp64 arithmetic on it (a single thread walking
+  // global memory paid a full memory latency per access: ~25 us per commit)
+  extern __shared__ double sm[];  // S [nl] | m [nl] | p [nl] | c [nl] (int64) | avail [nl] (int32)
+  double* sS = sm;
+  double* sM = sS + a.nl;
+  double* sP = sM + a.nl;
+  long long* sC = reinterpret_cast<long long*>(sP + a.nl);
+  int* sAv = reinterpret_cast<int*>(sC + a.nl);
+  __shared__ int s_flag, s_err, s_committed;
+  __shared__ unsigned long long s_period;
+  const int tid = threadIdx.x;
+  for (int l = tid; l < a.nl; l += blockDim.x) {
+    sS[l] = st.S[l];
+    sC[l] = st.c[l];
+    sM[l] = a.m[l];
+    sP[l] = a.probs[l];
+  }
+  if (tid == 0) {
+    s_flag = *st.flag;
+    s_err = *a.err;
+    s_committed = *a.committed;
+    s_period = *a.period_ctr;
+  }
+  __syncthreads();
+  if (s_err) return;  // a previous error stops the schedule
+  bool reset = false;
+  if (tid == 0) {
+    bool ok = true;
+    if (a.do_commit) {
+      long long total = 0;
+      for (int l = 0; l < a.nsamp; ++l) total += sC[l];
+      const bool committed = s_committed != 0;
+      if (s_flag != 0) {
+        s_err = 2;
+        ok = false;
+      } else if (total == 0 && (committed || a.T_p != 0)) {
+        s_err = 1;
+        ok = false;
+      } else {
+        for (int l = 0; l < a.nsamp; ++l) {
+          if (sC[l] > 0) {
+            const double w = sS[l] / (double)sC[l];
+            sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;
+          } else if (!committed) {
+            sM[l] = 0.0;
+          }
+        }
+        s_committed = 1;
+        if (a.policy == GRASS_POLICY_UNIFORM) {
+          for (int l = 0; l < a.nsamp; ++l) sP[l] = 1.0 / a.nsamp;
+        } else if (a.policy == GRASS_POLICY_ADAPTIVE || !committed) {
+          double M = sM[0];
+          for (int i = 1; i < a.nsamp; ++i) M = sM[i] > M ? sM[i] : M;
+          auto mt = [&](int i) { return a.normalize ? (M > 0.0 ? sM[i] / M : 0.0) : sM[i]; };
+          double mx = mt(0);
+          for (int i = 1; i < a.nsamp; ++i) mx = mt(i) > mx ? mt(i) : mx;
+          double tot = 0.0;
+          for (int i = 0; i < a.nsamp; ++i) {
+            sP[i] = exp((mt(i) - mx) / a.tau);
+            tot += sP[i];
+          }
+          for (int i = 0; i < a.nsamp; ++i) sP[i] = sP[i] / tot;
+        }
+        reset = true;
+      }
+    }
+    if (ok && a.do_sample) {
+      const uint64_t period = a.period == ~0ull ? s_period + 1 : a.period;
+      s_period = period;
+      int navail = a.nsamp;
+      for (int i = 0; i < navail; ++i) sAv[i] = i;
+      const uint64_t key = d_splitmix64(a.seed);
+      for (int k = 0; k < a.gamma; ++k) {
+        const uint64_t ctr = (period << 16) + (uint64_t)k;
+        const double u = (double)(d_splitmix64(key ^ ctr) >> 11) * 0x1.0p-53;
+        double R = 0.0;
+        for (int j = 0; j < navail; ++j) R += sP[sAv[j]];
+        const double x = u * R;
+        double c = 0.0;
+        int pick = navail - 1;
+        for (int j = 0; j < navail; ++j) {
+          c += sP[sAv[j]];
+          if (x < c) {
+            pick = j;
+            break;
+          }
+        }
+        a.ids[k] = sAv[pick];
+        for (int j = pick; j + 1 < navail; ++j) sAv[j] = sAv[j + 1];
+        --navail;
+      }
+      *a.period_ctr = period;
+    }
+    *a.err = s_err;
+    *a.committed = s_committed;
+    s_flag = reset ? 1 : 0;  // (reused: write the commit back)
+  }
+  __syncthreads();
+  if (s_flag) {  // the commit happened: m, p back, the window restarts (every layer, as the host's reset)
+    for (int l = tid; l < a.nl; l += blockDim.x) {
+      a.m[l] = sM[l];
+      a.probs[l] = sP[l];
+      st.S[l] = 0.0;
+      st.c[l] = 0;
+    }
+  }
+}
+
 
 // K2 writes its results back into the stage and the producer bulk-stores them
 // (TMA, SASS UBLKCP.G.S): measured 2.4% faster than per-thread 128-bit stores.
@@ -414,7 +545,7 @@ __global__ void grass_p2p_selftest_kernel(const __grid_constant__ P2PSelftestArg
 __global__ void grass_step_prologue_kernel(const __grid_constant__ PrologueArgs a, const DevState st) {
   const int j = threadIdx.x;
   if (j >= a.n) return;
-  const int l = a.layer[j];
+  const int l = a.dev_ids ? a.dev_ids[j] : a.layer[j];
   const long long t = st.t[l] + 1;
   st.t[l] = t;
   const double lr = a.lr_ptr ? (double)*a.lr_ptr : (double)a.lr;
@@ -462,7 +593,7 @@ constexpr int kNormStagesBf16 = GRASS_NORM_STAGES_BF16;
 #endif
 constexpr int kP2PNormTPS = GRASS_P2P_NORM_TPS;  // P2P probing: tiles per gradient-ring slot
 
-template <bool U, int TPS, int ST, bool BF16, bool P2P = false>
+template <bool U, int TPS, int ST, bool BF16, bool P2P = false, bool DEVB = false>
 cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStream_t s) {
   using SL = StageLayout<U, BF16, TPS>;
   using GS = P2PGSlots<U, BF16>;
@@ -477,15 +608,15 @@ cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStre
   if (e != cudaSuccess) return e;
   const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
   if (!bit || !(attr_set.load(std::memory_order_acquire) & bit)) {
-    e = cudaFuncSetAttribute(grass_stream_kernel<U, TPS, ST, BF16, P2P>,
+    e = cudaFuncSetAttribute(grass_stream_kernel<U, TPS, ST, BF16, P2P, DEVB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit, std::memory_order_release);
   }
   int units = 0;
   for (int i = 0; i < b.nseg; ++i) units += (b.seg[i].tiles + TPS - 1) / TPS;
-  const int g = grid < units ? grid : units;
-  grass_stream_kernel<U, TPS, ST, BF16, P2P><<<g, kStreamThreads, smem, s>>>(b, st);
+  const int g = DEVB ? grid : (grid < units ? grid : units);  // DEVB: the units are known on the device only
+  grass_stream_kernel<U, TPS, ST, BF16, P2P, DEVB><<<g, kStreamThreads, smem, s>>>(b, st);
   return cudaGetLastError();
 }
 
@@ -510,7 +641,24 @@ cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int gr
 
 cudaError_t launch_finalize(const FinalizeArgs& a, const DevState& st, cudaStream_t s) {
   if (a.n <= 0) return cudaSuccess;
-  grass_finalize_kernel<<<a.n, kThreads, 0, s>>>(a, st);
+  grass_finalize_kernel<<<a.n, kFinThreads, 0, s>>>(a, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused_dev(const Batch& b, const DevState& st, int grid, cudaStream_t s) {
+  if (b.dev_n <= 0) return cudaSuccess;
+  return b.bf16 ? launch_stream<true, kUpdTPS, kUpdStages, true, false, true>(b, st, grid, s)
+                : launch_stream<true, kUpdTPS, kUpdStages, false, false, true>(b, st, grid, s);
+}
+
+cudaError_t launch_commit_sample(const CommitArgs& a, const DevState& st, cudaStream_t s) {
+  const size_t smem = (size_t)a.nl * (4 * sizeof(double) + sizeof(int));
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(grass_commit_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  grass_commit_sample_kernel<<<1, kCommitThreads, smem, s>>>(a, st);
   return cudaGetLastError();
 }
 

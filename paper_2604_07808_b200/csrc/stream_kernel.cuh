@@ -226,7 +226,7 @@ __device__ __forceinline__ int unit_of(int i, int ub) {
   return (i / ub) * ((int)gridDim.x * ub) + (int)blockIdx.x * ub + (i % ub);
 }
 
-template <bool UPDATE, int TPS, int STAGES, bool BF16, bool P2P>
+template <bool UPDATE, int TPS, int STAGES, bool BF16, bool P2P, bool DEVB = false>
 __global__ void __launch_bounds__(kStreamThreads, 1)
 grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   using L = StageLayout<UPDATE, BF16, TPS>;
@@ -246,12 +246,38 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   char* const gring = sbuf + (kRing ? (size_t)STAGES * L::bytes : 0);
   __shared__ int unit_prefix[kMaxSeg + 1];
   __shared__ double red[2][TPS][kConsumerWarps];
+  // DEVB (device-resident schedule): this launch's segments, built from the
+  // layer ids in device memory — the sampled set is never seen by the host
+  __shared__ __align__(16) Seg dsegs[DEVB ? kMaxDevSeg : 1];
+  __shared__ int dids[DEVB ? kMaxDevSeg : 1];
+  __shared__ int dn;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (DEVB) {
+    if (tid == 0) {  // ids ascending (R12), insertion sort of <= kMaxDevSeg entries
+      const int n = b.dev_n < kMaxDevSeg ? b.dev_n : kMaxDevSeg;
+      for (int j = 0; j < n; ++j) {
+        const int x = b.dev_ids[j];
+        int k = j;
+        for (; k > 0 && dids[k - 1] > x; --k) dids[k] = dids[k - 1];
+        dids[k] = x;
+      }
+      dn = n;
+    }
+    __syncthreads();
+    constexpr int kWords = (int)(sizeof(Seg) / 8);
+    static_assert(sizeof(Seg) % 8 == 0, "Seg copied in 8-byte words");
+    for (int w = tid; w < dn * kWords; w += blockDim.x)
+      reinterpret_cast<unsigned long long*>(dsegs)[w] =
+          reinterpret_cast<const unsigned long long*>(b.dev_table + dids[w / kWords])[w % kWords];
+    __syncthreads();
+  }
+  const Seg* const segs = DEVB ? dsegs : b.seg;
+  const int nseg = DEVB ? dn : b.nseg;
   if (tid == 0) {
     unit_prefix[0] = 0;
-    for (int s = 0; s < b.nseg; ++s) {
-      unit_prefix[s + 1] = unit_prefix[s] + (b.seg[s].tiles + TPS - 1) / TPS;
+    for (int s = 0; s < nseg; ++s) {
+      unit_prefix[s + 1] = unit_prefix[s] + (segs[s].tiles + TPS - 1) / TPS;
     }
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full_bar[i], 1);
@@ -265,7 +291,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int total = unit_prefix[b.nseg];
+  const int total = unit_prefix[nseg];
 
   if (warp == kConsumerWarps) {
     // ------------------------------ producer ------------------------------
@@ -283,12 +309,12 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         if (kRing && i >= STAGES) {
           mbar_wait(&empty_bar[stage], ((i / STAGES) & 1) ^ 1);
           if (TS) {
-            store_unit_t<BF16, L>(b.seg[pend_s[stage]], P2P ? b.ntpeer : 0, pend_e0[stage], pend_nv[stage], stg);
+            store_unit_t<BF16, L>(segs[pend_s[stage]], P2P ? b.ntpeer : 0, pend_e0[stage], pend_nv[stage], stg);
             if (!L::SEP) bulk_wait_read_all();  // stage reusable again
           }
         }
         while (u >= unit_prefix[s + 1]) ++s;
-        const Seg& sg = b.seg[s];
+        const Seg& sg = segs[s];
         const int64_t e0 = (int64_t)(u - unit_prefix[s]) * kUnit;
         const int64_t ne = min((int64_t)kUnit, sg.n - e0);
         const uint32_t nv = (uint32_t)(ne & ~(int64_t)(L::vec - 1));
@@ -352,7 +378,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
         for (int j = (n_units > STAGES ? n_units - STAGES : 0); j < n_units; ++j) {
           const int stage = j % STAGES;
           mbar_wait(&empty_bar[stage], (j / STAGES) & 1);
-          store_unit_t<BF16, L>(b.seg[pend_s[stage]], P2P ? b.ntpeer : 0, pend_e0[stage], pend_nv[stage],
+          store_unit_t<BF16, L>(segs[pend_s[stage]], P2P ? b.ntpeer : 0, pend_e0[stage], pend_nv[stage],
                                 sbuf + (size_t)stage * L::bytes);
         }
         bulk_wait_all();
@@ -373,7 +399,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   for (int u = unit_of(0, kUB); u < total; ++i, u = unit_of(i, kUB)) {
     const int stage = i % STAGES;
     while (u >= unit_prefix[s + 1]) ++s;
-    const Seg& sg = b.seg[s];
+    const Seg& sg = segs[s];
     AdamScalars sc;
     sc.b1 = b.beta1; sc.omb1 = b.one_minus_beta1; sc.b2 = b.beta2; sc.omb2 = b.one_minus_beta2;
     sc.eps = b.eps;
