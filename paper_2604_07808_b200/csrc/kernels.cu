@@ -296,18 +296,19 @@ __device__ __forceinline__ uint64_t d_splitmix64(uint64_t x) {
 constexpr int kCommitThreads = 256;
 __global__ void __launch_bounds__(kCommitThreads) grass_commit_sample_kernel(const __grid_constant__ CommitArgs a,
                                                                              const DevState st) {
-  // every operand staged in shared memory by all threads; thread 0 then runs
-  // the host's sequential fp64 arithmetic on it (a single thread walking
-  // global memory paid a full memory latency per access: ~25 us per commit)
+  // operands staged in shared memory; the elementwise steps (window mean,
+  // EMA, exp, the final division) run one layer per thread, the order-
+  // dependent ones (the maxima, the ascending sum, the sampler) on thread 0 —
+  // every value computed by the same operations as the host's loops
   extern __shared__ double sm[];  // S [nl] | m [nl] | p [nl] | c [nl] (int64) | avail [nl] (int32)
   double* sS = sm;
   double* sM = sS + a.nl;
   double* sP = sM + a.nl;
   long long* sC = reinterpret_cast<long long*>(sP + a.nl);
   int* sAv = reinterpret_cast<int*>(sC + a.nl);
-  __shared__ int s_flag, s_err, s_committed;
-  __shared__ unsigned long long s_period;
-  const int tid = threadIdx.x;
+  __shared__ int s_err, s_committed, s_commit, s_soft;
+  __shared__ double s_M, s_mx, s_tot;
+  const int tid = threadIdx.x, ns = a.nsamp;
   for (int l = tid; l < a.nl; l += blockDim.x) {
     sS[l] = st.S[l];
     sC[l] = st.c[l];
@@ -315,58 +316,67 @@ __global__ void __launch_bounds__(kCommitThreads) grass_commit_sample_kernel(con
     sP[l] = a.probs[l];
   }
   if (tid == 0) {
-    s_flag = *st.flag;
     s_err = *a.err;
     s_committed = *a.committed;
-    s_period = *a.period_ctr;
+    s_commit = 0;
+    if (!s_err && a.do_commit) {
+      long long total = 0;
+      for (int l = 0; l < ns; ++l) total += st.c[l];
+      if (*st.flag != 0) s_err = 2;
+      else if (total == 0 && (s_committed || a.T_p != 0)) s_err = 1;
+      else s_commit = 1;
+    }
+    s_soft = s_commit && (a.policy == GRASS_POLICY_ADAPTIVE || !s_committed) && a.policy != GRASS_POLICY_UNIFORM;
   }
   __syncthreads();
-  if (s_err) return;  // a previous error stops the schedule
-  bool reset = false;
-  if (tid == 0) {
-    bool ok = true;
-    if (a.do_commit) {
-      long long total = 0;
-      for (int l = 0; l < a.nsamp; ++l) total += sC[l];
-      const bool committed = s_committed != 0;
-      if (s_flag != 0) {
-        s_err = 2;
-        ok = false;
-      } else if (total == 0 && (committed || a.T_p != 0)) {
-        s_err = 1;
-        ok = false;
-      } else {
-        for (int l = 0; l < a.nsamp; ++l) {
-          if (sC[l] > 0) {
-            const double w = sS[l] / (double)sC[l];
-            sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;
-          } else if (!committed) {
-            sM[l] = 0.0;
-          }
-        }
-        s_committed = 1;
-        if (a.policy == GRASS_POLICY_UNIFORM) {
-          for (int l = 0; l < a.nsamp; ++l) sP[l] = 1.0 / a.nsamp;
-        } else if (a.policy == GRASS_POLICY_ADAPTIVE || !committed) {
-          double M = sM[0];
-          for (int i = 1; i < a.nsamp; ++i) M = sM[i] > M ? sM[i] : M;
-          auto mt = [&](int i) { return a.normalize ? (M > 0.0 ? sM[i] / M : 0.0) : sM[i]; };
-          double mx = mt(0);
-          for (int i = 1; i < a.nsamp; ++i) mx = mt(i) > mx ? mt(i) : mx;
-          double tot = 0.0;
-          for (int i = 0; i < a.nsamp; ++i) {
-            sP[i] = exp((mt(i) - mx) / a.tau);
-            tot += sP[i];
-          }
-          for (int i = 0; i < a.nsamp; ++i) sP[i] = sP[i] / tot;
-        }
-        reset = true;
+  if (s_err) {  // an error stops the schedule (reported by grass_device_schedule_end)
+    if (tid == 0) *a.err = s_err;
+    return;
+  }
+  const bool committed = s_committed != 0;
+  if (s_commit) {  // Eq. 2 window mean, first commit / Eq. 4 EMA, frozen retention
+    for (int l = tid; l < ns; l += blockDim.x) {
+      if (sC[l] > 0) {
+        const double w = sS[l] / (double)sC[l];
+        sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;
+      } else if (!committed) {
+        sM[l] = 0.0;
       }
+      if (a.policy == GRASS_POLICY_UNIFORM) sP[l] = 1.0 / ns;
     }
-    if (ok && a.do_sample) {
-      const uint64_t period = a.period == ~0ull ? s_period + 1 : a.period;
-      s_period = period;
-      int navail = a.nsamp;
+  }
+  __syncthreads();
+  if (s_soft && tid == 0) {  // Eq. 3: the maxima (host order)
+    double M = sM[0];
+    for (int i = 1; i < ns; ++i) M = sM[i] > M ? sM[i] : M;
+    s_M = M;
+    auto mt = [&](int i) { return a.normalize ? (M > 0.0 ? sM[i] / M : 0.0) : sM[i]; };
+    double mx = mt(0);
+    for (int i = 1; i < ns; ++i) mx = mt(i) > mx ? mt(i) : mx;
+    s_mx = mx;
+  }
+  __syncthreads();
+  if (s_soft) {
+    const double M = s_M, mx = s_mx;
+    for (int i = tid; i < ns; i += blockDim.x) {
+      const double mti = a.normalize ? (M > 0.0 ? sM[i] / M : 0.0) : sM[i];
+      sP[i] = exp((mti - mx) / a.tau);
+    }
+  }
+  __syncthreads();
+  if (s_soft && tid == 0) {  // the ascending sum
+    double tot = 0.0;
+    for (int i = 0; i < ns; ++i) tot += sP[i];
+    s_tot = tot;
+  }
+  __syncthreads();
+  if (s_soft)
+    for (int i = tid; i < ns; i += blockDim.x) sP[i] = sP[i] / s_tot;
+  __syncthreads();
+  if (tid == 0) {
+    if (a.do_sample) {  // R6 / R7, as grass_sample_layers
+      const uint64_t period = a.period == ~0ull ? *a.period_ctr + 1 : a.period;
+      int navail = ns;
       for (int i = 0; i < navail; ++i) sAv[i] = i;
       const uint64_t key = d_splitmix64(a.seed);
       for (int k = 0; k < a.gamma; ++k) {
@@ -390,12 +400,9 @@ __global__ void __launch_bounds__(kCommitThreads) grass_commit_sample_kernel(con
       }
       *a.period_ctr = period;
     }
-    *a.err = s_err;
-    *a.committed = s_committed;
-    s_flag = reset ? 1 : 0;  // (reused: write the commit back)
+    if (s_commit) *a.committed = 1;
   }
-  __syncthreads();
-  if (s_flag) {  // the commit happened: m, p back, the window restarts (every layer, as the host's reset)
+  if (s_commit) {  // m, p back; the window restarts (every layer, as the host's reset)
     for (int l = tid; l < a.nl; l += blockDim.x) {
       a.m[l] = sM[l];
       a.probs[l] = sP[l];

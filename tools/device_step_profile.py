@@ -36,8 +36,9 @@ with torch.cuda.stream(s):
     with torch.cuda.graph(g, stream=s):
         ctx.device_step(3e-5, stream=s)
 e[2].record(s)
-for _ in range(20):
-    g.replay()
+with torch.cuda.stream(s):
+    for _ in range(20):
+        g.replay()
 e[3].record(s)
 torch.cuda.synchronize()
 print(f"eager {e[0].elapsed_time(e[1]) / 20:.4f} ms/step, graph {e[2].elapsed_time(e[3]) / 20:.4f} ms/step")
