@@ -66,6 +66,14 @@ MUTANTS = {
                 "    CUDA_TRY(c, cudaStreamWaitEvent(c->h2d, c->ev_layer_done[l], 0));\n", "")]),
     19: ("period residency: a victim's write-back does not wait for the updates before it",
          [(HOT, "    if (c->cfg.overlap && (s = wait_pending(c, c->d2h)) != GRASS_OK) return s;\n", "")]),
+    20: ("device schedule: Eq. 4 EMA weights swapped (alpha on the old MGN)",
+         [(K, "sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;",
+           "sM[l] = committed ? (1.0 - a.alpha) * w + a.alpha * sM[l] : w;")]),
+    21: ("device schedule: sampler boundary x <= c instead of x < c",
+         [(K, "          if (x < c) {", "          if (x <= c) {")]),
+    22: ("device schedule: the sampling period not advanced",
+         [(K, "const uint64_t period = a.period == ~0ull ? *a.period_ctr + 1 : a.period;",
+           "const uint64_t period = a.period == ~0ull ? *a.period_ctr : a.period;")]),
     14: ("P2P barrier self-test: start barrier removed",
          [(K, "    a.which = 0;  // start barrier: every rank has read its rows of this round\n"
               "    const int n_save = a.n;\n    a.n = 0;\n    p2p_sync_cta(a);\n    a.n = n_save;\n", "")]),
@@ -75,7 +83,8 @@ TESTS = ("test_step_layers_vs_oracle_multi_step or test_norms_ragged_sizes_vs_or
          "test_zero_grad_zero_state_is_identity_on_theta or test_nonfinite_gradient_reported_and_not_recorded or "
          "test_norms_probe_equals_update_bitwise or test_norms_integer_grads_exact_bf16 or "
          "test_p2p_barrier_protocol_selftest or test_bf16_norms_tiny_and_huge_gradients or "
-         "test_norms_all_tiles_reduction_keeps_each_tile_apart or test_offload_pipeline_happens_before_under_stress")
+         "test_norms_all_tiles_reduction_keeps_each_tile_apart or test_offload_pipeline_happens_before_under_stress or "
+         "test_device_schedule_equals_host_schedule or test_device_schedule_commit_and_sampler_against_oracle")
 
 
 def patched_source(k: int) -> str:
@@ -109,6 +118,7 @@ def run(only=()):
         env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_m{k}.so"))
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                             "tests/test_gpu_parity.py", "tests/test_gpu_p2p.py", "tests/test_gpu_race.py",
+                            "tests/test_gpu_device_schedule.py",
                             "-k", TESTS],
                            cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
         failed = [l for l in r.stdout.splitlines() if l.startswith("FAILED")]
