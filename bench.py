@@ -536,7 +536,7 @@ def run_grass(args, rank, world, local):
         h2d = sum(h.numel() * 4 for h in host_g)
         d2h = NL * 16 + 4
         for w in range(2):
-            one_step(w, None)
+            host_step(w, None)                  # the device schedule has ended: the host API
         torch.cuda.synchronize()
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -110,26 +110,37 @@ def build(only=()):
         print("built mutant", k, flush=True)
 
 
+def _subset(lib):
+    env = dict(os.environ)
+    if lib:
+        env["GRASS_LIB_PATH"] = lib
+    return subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                           "tests/test_gpu_parity.py", "tests/test_gpu_p2p.py", "tests/test_gpu_race.py",
+                           "tests/test_gpu_device_schedule.py",
+                           "-k", TESTS],
+                          cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+
+
 def run(only=()):
     res = {}
+    r = _subset(None)                      # control: the product library passes the subset
+    res["product"] = {"passed": r.returncode == 0, "summary": (r.stdout.strip().splitlines() or [""])[-1]}
+    print("product", res["product"], flush=True)
     for k, (what, _) in MUTANTS.items():
         if only and k not in only:
             continue
-        env = dict(os.environ, GRASS_LIB_PATH=os.path.join(OUTDIR, f"libgrass_m{k}.so"))
-        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                            "tests/test_gpu_parity.py", "tests/test_gpu_p2p.py", "tests/test_gpu_race.py",
-                            "tests/test_gpu_device_schedule.py",
-                            "-k", TESTS],
-                           cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+        r = _subset(os.path.join(OUTDIR, f"libgrass_m{k}.so"))
         failed = [l for l in r.stdout.splitlines() if l.startswith("FAILED")]
         res[k] = {"mutation": what, "killed": r.returncode != 0, "by": failed[:1]}
         print(k, res[k], flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "kernel_mutation" + ("_subset" if only else "") + ".json"), "w") as f:
         json.dump(res, f, indent=1)
-    killed = sum(v["killed"] for v in res.values())
-    print(f"{killed}/{len(res)} kernel mutations killed by the GPU parity tests")
-    return 0 if killed == len(res) else 1
+    muts = [v for k, v in res.items() if k != "product"]
+    killed = sum(v["killed"] for v in muts)
+    print(f"{killed}/{len(muts)} kernel mutations killed by the GPU parity tests; product passes: "
+          f"{res['product']['passed']}")
+    return 0 if killed == len(muts) and res["product"]["passed"] else 1
 
 
 if __name__ == "__main__":
