@@ -541,7 +541,7 @@ def run_grass(args, rank, world, local):
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ksteps = max(3, min(args.steps, 10))
-        def host_step(step):
+        def e2e_step(step):
             nonlocal ids
             if world == 1:
                 # the public call with the step's gradients in pinned HOST memory: the
@@ -557,7 +557,7 @@ def run_grass(args, rank, world, local):
             ids = ctx.sample_layers(step + 1)
         e0.record(s)
         for k in range(ksteps):
-            host_step(1000 + k)
+            e2e_step(1000 + k)
         e1.record(s)
         torch.cuda.synchronize()
         et = max_over_ranks(e0.elapsed_time(e1) / 1e3, world, dev)

@@ -14,7 +14,9 @@
 //           K1's data movement with no arithmetic;
 //   mode 2/3 K1's consumer protocol (16 warps, per-warp release, mode 3: a
 //           named barrier per unit) on the same ring — diagnostics.
-// C ABI: grass_diag_read(ptr, bytes, mode, grid, unit, stages, sink, stream).
+// C ABI: grass_diag_read(ptr, bytes, mode, grid, unit, stages, sink, stream);
+// and the 4-read / 3-write mixes of K2: grass_diag_rw43 (LDG/STG) and
+// grass_diag_rw43_tma (K2's TMA ring, no arithmetic).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -201,6 +203,79 @@ __global__ void __launch_bounds__(512) rw43(const float4* __restrict__ g, float4
   }
 }
 
+// K2's data movement with no arithmetic: one CTA per SM, a ring of `stages`
+// slots each holding one unit of `elems` fp32 of g, theta, m, v (16 B/elem in
+// shared memory).  Thread 0 streams the four pieces HBM -> smem with
+// cp.async.bulk (mbarrier complete_tx); thread 32 waits for the slot and
+// bulk-stores theta, m, v back smem -> HBM (cp.async.bulk.global.shared::cta,
+// one bulk group per unit) and hands the slot back once the stores of the
+// PREVIOUS unit have finished reading shared memory.  The 4R3W TMA ceiling
+// K2 (the same ring plus the Eq. 2 / AdamW arithmetic) is compared with.
+__global__ void __launch_bounds__(64, 1) rw43_tma(const float* __restrict__ g, float* __restrict__ th,
+                                                  float* __restrict__ m, float* __restrict__ v, size_t n,
+                                                  uint32_t elems, int stages) {
+  extern __shared__ __align__(1024) char ring[];
+  __shared__ __align__(8) uint64_t full[16], empty[16];
+  const int tid = threadIdx.x;
+  const uint32_t piece = elems * 4u;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const size_t units = n / elems;
+  if (tid == 0) {  // loads
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    int k = 0;
+    for (size_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+      const int s = k % stages;
+      if (k >= stages) {
+        const uint32_t par = ((k / stages) & 1) ^ 1;
+        asm volatile("{\n.reg .pred q;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W_%=;\n}\n" ::"r"(
+                         smem_u32(&empty[s])),
+                     "r"(par)
+                     : "memory");
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(4 * piece)
+                   : "memory");
+      const float* src[4] = {g, th, m, v};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                smem_u32(ring + ((size_t)s * 4 + a) * piece)),
+            "l"(src[a] + u * elems), "r"(piece), "r"(smem_u32(&full[s])), "l"(pol)
+            : "memory");
+    }
+  } else if (tid == 32) {  // stores
+    int k = 0;
+    float* dst[3] = {th, m, v};
+    for (size_t u = blockIdx.x; u < units; u += gridDim.x, ++k) {
+      const int s = k % stages;
+      const uint32_t par = (k / stages) & 1;
+      asm volatile("{\n.reg .pred q;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 q, [%0], %1;\n@!q bra W_%=;\n}\n" ::"r"(
+                       smem_u32(&full[s])),
+                   "r"(par)
+                   : "memory");
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[a] + u * elems),
+                     "r"(smem_u32(ring + ((size_t)s * 4 + 1 + a) * piece)), "r"(piece)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (k >= 1) {  // unit k-1's stores have read their slot
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[(k - 1) % stages])) : "memory");
+      }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
 }  // namespace
 
 extern "C" int grass_diag_rw43(void* const* bufs, unsigned long long n, int unroll, int grid, void* stream) {
@@ -213,6 +288,21 @@ extern "C" int grass_diag_rw43(void* const* bufs, unsigned long long n, int unro
   if (unroll == 1) rw43<1><<<grid, 512, 0, s>>>(g, th, m, v, n4);
   else if (unroll == 2) rw43<2><<<grid, 512, 0, s>>>(g, th, m, v, n4);
   else rw43<4><<<grid, 512, 0, s>>>(g, th, m, v, n4);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int grass_diag_rw43_tma(void* const* bufs, unsigned long long n, unsigned int elems, int stages,
+                                   int grid, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!bufs || grid < 1 || elems == 0 || elems % 4 != 0 || n % elems != 0 || stages < 2 || stages > 16 ||
+      (size_t)elems * 16 * stages > 227u * 1024u)
+    return (int)cudaErrorInvalidValue;
+  const size_t smem = (size_t)elems * 16 * stages;
+  cudaError_t e = cudaFuncSetAttribute(rw43_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  rw43_tma<<<grid, 64, smem, s>>>(static_cast<const float*>(bufs[0]), static_cast<float*>(bufs[1]),
+                                  static_cast<float*>(bufs[2]), static_cast<float*>(bufs[3]), (size_t)n, elems,
+                                  stages);
   return (int)cudaGetLastError();
 }
 

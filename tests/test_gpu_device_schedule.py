@@ -61,9 +61,10 @@ def _same(host, dev, P, numel):
 
 
 @pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
-@pytest.mark.parametrize("T_s,T_u,n_always", [(1, 1, 0), (3, 6, 1), (2, 2, 2)])
-def test_device_schedule_equals_host_schedule(dtype, T_s, T_u, n_always):
-    host, dev, P, Gr, numel, sig, tdt = _setup(dtype, n_always, T_s, T_u)
+@pytest.mark.parametrize("T_s,T_u,n_always,alpha", [(1, 1, 0, 0.3), (3, 6, 1, 0.5), (2, 2, 2, 0.8)])
+def test_device_schedule_equals_host_schedule(dtype, T_s, T_u, n_always, alpha):
+    # alpha != 1/2 in two cases: Eq. 4's two weights are told apart
+    host, dev, P, Gr, numel, sig, tdt = _setup(dtype, n_always, T_s, T_u, alpha=alpha)
     nl, ns = len(numel), len(numel) - n_always
     always = list(range(ns, nl))
     T_p, steps, lr = 2, 20, 1e-3

@@ -1,7 +1,8 @@
-"""K2's HBM mix (4 reads + 3 writes per element, 28 B) with plain per-thread
-loads / streaming stores (paper_2604_07808_b200/diag, grass_diag_rw43) over
-the bench's configs[1] element count, grid x unroll sweep: the mixed
-read/write ceiling next to K2.  -> stdout JSON"""
+"""K2's HBM mix (4 reads + 3 writes per element, 28 B) over the bench's
+configs[1] element count: plain per-thread loads / streaming stores
+(grass_diag_rw43, grid x unroll sweep) and K2's own TMA ring with no
+arithmetic (grass_diag_rw43_tma, unit x stages x grid sweep) — the mixed
+read/write ceilings next to K2.  -> stdout JSON"""
 import ctypes as C
 import json
 import os
@@ -17,6 +18,9 @@ lib = C.CDLL(B.DIAG_OUT)
 f = lib.grass_diag_rw43
 f.restype = C.c_int
 f.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_int, C.c_int, C.c_void_p]
+ft = lib.grass_diag_rw43_tma
+ft.restype = C.c_int
+ft.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_uint, C.c_int, C.c_int, C.c_void_p]
 dev = torch.device("cuda", 0)
 n = 2 * 202_383_360
 bufs = [torch.randn(n, device=dev) * 1e-3 for _ in range(4)]
@@ -24,17 +28,32 @@ ptrs = (C.c_void_p * 4)(*[b.data_ptr() for b in bufs])
 s = torch.cuda.Stream(device=dev)
 sms = torch.cuda.get_device_properties(dev).multi_processor_count
 res = {}
-for u in (1, 2, 4):
-    for k in (1, 2, 4, 8):
-        ts = []
-        for _ in range(5):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
-            assert f(ptrs, n, u, sms * k, s.cuda_stream) == 0
-            e1.record(s)
-            torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        ms = sorted(ts)[2]
-        res[f"unroll={u} grid={sms * k}"] = {"ms": round(ms, 4), "GBps": round(28 * n / ms / 1e6, 1)}
-        print(f"unroll={u} grid={sms*k}", res[f"unroll={u} grid={sms * k}"], flush=True)
+
+
+def timed(key, call):
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        assert call() == 0, key
+        e1.record(s)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = sorted(ts)[2]
+    res[key] = {"ms": round(ms, 4), "GBps": round(28 * n / ms / 1e6, 1)}
+    print(key, res[key], flush=True)
+
+
+if "--tma-only" not in sys.argv:
+    for u in (1, 2, 4):
+        for k in (1, 2, 4, 8):
+            timed(f"ldg unroll={u} grid={sms * k}", lambda: f(ptrs, n, u, sms * k, s.cuda_stream))
+for elems, stages in ((1024, 4), (1024, 8), (2048, 2), (2048, 3), (2048, 6), (4096, 2), (4096, 3)):
+    for grid in (128, sms, 2 * sms):
+        if grid == 2 * sms and elems * 16 * stages > 113 * 1024:
+            continue
+        timed(f"tma unit={elems} x{stages} grid={grid}",
+              lambda: ft(ptrs, n, elems, stages, grid, s.cuda_stream))
+best = max((v["GBps"], k) for k, v in res.items())
+res["best"] = {"GBps": best[0], "what": best[1]}
 print(json.dumps(res))

@@ -69,8 +69,8 @@ MUTANTS = {
     20: ("device schedule: Eq. 4 EMA weights swapped (alpha on the old MGN)",
          [(K, "sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;",
            "sM[l] = committed ? (1.0 - a.alpha) * w + a.alpha * sM[l] : w;")]),
-    21: ("device schedule: sampler boundary x <= c instead of x < c",
-         [(K, "          if (x < c) {", "          if (x <= c) {")]),
+    21: ("device schedule: sampler mass R not renormalised over the still-available layers (R6)",
+         [(K, "for (int j = 0; j < navail; ++j) R += sP[sAv[j]];", "for (int j = 0; j < ns; ++j) R += sP[j];")]),
     22: ("device schedule: the sampling period not advanced",
          [(K, "const uint64_t period = a.period == ~0ull ? *a.period_ctr + 1 : a.period;",
            "const uint64_t period = a.period == ~0ull ? *a.period_ctr : a.period;")]),
