@@ -342,6 +342,55 @@ def measure_read_ceiling(dev, gib: int = 8) -> dict:
     return {"GBps": sweep[k], "best": k, "sweep": sweep, "bytes": nbytes, **({"errors": errors} if errors else {})}
 
 
+def measure_mix_ceiling(dev, n: int = 2 * 202_383_360) -> dict:
+    """K2's own traffic-mix ceiling: 4 reads + 3 writes per element (g, theta,
+    m, v in; theta, m, v out — 28 B) with NO arithmetic, over 4 fp32 arrays of
+    n elements (configs[1]'s gamma x N_p: 11.3 GB moved per launch, >> L2; not
+    a power of two — four 2^k-byte arrays would start on the same HBM channels
+    and measure channel conflicts, not the mix): K2's TMA ring (bulk loads into
+    a shared-memory ring, bulk stores back; diag `rw43_tma`) over a small
+    unit / stage / grid set, and plain LDG/STG (`rw43`); best of 3 each, CUDA
+    events on the launching stream.  K2 at this number is at the ceiling of the
+    data movement it must do."""
+    import ctypes as C
+
+    import torch
+    from paper_2604_07808_b200 import build as B
+    lib = C.CDLL(B.DIAG_OUT)
+    ft, fl = lib.grass_diag_rw43_tma, lib.grass_diag_rw43
+    ft.restype = fl.restype = C.c_int
+    ft.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_uint, C.c_int, C.c_int, C.c_void_p]
+    fl.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_int, C.c_int, C.c_void_p]
+    bufs = [torch.full((n,), 1e-3, device=dev) for _ in range(4)]
+    ptrs = (C.c_void_p * 4)(*[b.data_ptr() for b in bufs])
+    s = torch.cuda.Stream(device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    cfgs = [(f"tma unit={e} x{st} grid={g}", lambda e=e, st=st, g=g: ft(ptrs, n, e, st, g, s.cuda_stream))
+            for e, st, g in ((4096, 3, 128), (2048, 3, sms), (2048, 6, 128), (1024, 4, sms), (2048, 2, 2 * sms))]
+    cfgs += [(f"ldg unroll={u} grid={g}", lambda u=u, g=g: fl(ptrs, n, u, g, s.cuda_stream))
+             for u, g in ((2, sms), (4, 8 * sms))]
+    sweep, errors = {}, {}
+    for key, call in cfgs:
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            rc = call()
+            e1.record(s)
+            torch.cuda.synchronize()
+            if rc != 0:
+                errors[key] = f"cuda error {rc}"
+                break
+            best = max(best, 28 * n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        if best:
+            sweep[key] = round(best, 1)
+    del bufs
+    torch.cuda.empty_cache()
+    k = max(sweep, key=sweep.get)
+    return {"GBps": sweep[k], "best": k, "sweep": sweep, "bytes_per_launch": 28 * n,
+            **({"errors": errors} if errors else {})}
+
+
 def workload_config(model: str, gamma: int, world: int) -> dict:
     """The `config` of the JSON line, identical for the GRASS and reference arms."""
     from synth import MODELS
@@ -592,6 +641,10 @@ def run_grass(args, rank, world, local):
 
     paper_schedule = guarded("main", leg_paper_schedule)
     ctx.close()                                 # frees its 51.8 GB of HBM state
+    try:
+        mix_ceiling = measure_mix_ceiling(dev)
+    except Exception as ex:  # recorded, never fatal to the line
+        mix_ceiling = {"error": f"{type(ex).__name__}: {ex}"[:300]}
     torch.cuda.empty_cache()
 
     # ---- P2P data parallelism: the same step with ONE fused
@@ -1024,7 +1077,9 @@ def run_grass(args, rank, world, local):
                          "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of this "
                                            "kernel at this config (profiles/ncu_traffic.json, from "
                                            "profiles/r02_ncu_full.md)" if traffic else None,
-                         "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world},
+                         "algorithmic_bytes_per_launch": BYTES_PER_PARAM_UPDATE * active // world,
+                         "mix_ceiling": mix_ceiling,
+                         "frac_mix_ceiling": achieved / mix_ceiling["GBps"] if mix_ceiling.get("GBps") else None},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "step_driver": ("grass_device_step: update of the layers sampled on the device, then the commit "
                             "(Eq. 2/4/3) and resample kernel — no host round trip between steps"

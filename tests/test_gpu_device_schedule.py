@@ -160,6 +160,46 @@ def test_captured_device_step_replays_equal_eager_steps():
     _same(host, eager, P, numel)
 
 
+@pytest.mark.parametrize("dtype", [G.DTYPE_FP32, G.DTYPE_BF16])
+def test_device_schedule_full_size_layers_equal_host(dtype):
+    """At the bench's layer size (a LLaMA-2-7B block, 202,383,360 parameters —
+    49,410 tiles, K2 at its 128-CTA launch configuration) over 4 layers, the
+    device schedule equals the host one bit for bit after 3 steps with commit
+    + resample, and its sampled norm equals the oracle's fp64 norm of the
+    same gradient (1e-6)."""
+    from synth import MODELS
+    n = MODELS["llama2-7b"].layer_numel
+    numel = [n] * 4
+    tdt = torch.bfloat16 if dtype == G.DTYPE_BF16 else torch.float32
+    host = G.Grass(numel, gamma=2, T_p=1, T_s=1, seed=11, param_dtype=dtype)
+    dev = G.Grass(numel, gamma=2, T_p=1, T_s=1, seed=11, param_dtype=dtype)
+    sig = grad_sigmas(4, 2)
+    Gr = [layer_grad(n, l, sig[l], step=0, device=DEV).to(tdt) for l in range(4)]
+    Ph = [layer_params(n, l, device=DEV).to(tdt) for l in range(4)]
+    Pd = [p.clone() for p in Ph]
+    for c in (host, dev):
+        c.mgn_accumulate([0, 1, 2, 3], Gr)
+        c.update_probs()
+    dev.register_layers(Pd, Gr)
+    dev.device_schedule_begin(0)
+    ids = host.sample_layers(0)
+    for k in range(3):
+        dev.device_step(3e-5)
+        host.step_layers(ids, [Ph[l] for l in ids], [Gr[l] for l in ids], 3e-5)
+        host.update_probs()
+        ids = host.sample_layers(k + 1)
+    assert dev.device_schedule_end() == ids
+    torch.cuda.synchronize()
+    for l in range(4):
+        assert torch.equal(Ph[l], Pd[l]), l
+    sa, sb = host.get_mgn(), dev.get_mgn()
+    assert sa["last_ss"] == sb["last_ss"] and sa["S"] == sb["S"]
+    np.testing.assert_allclose(sb["probs"], sa["probs"], rtol=1e-14, atol=0)   # device exp vs libm exp
+    l = ids[0]
+    ss = O.sq_norm(Gr[l].float().cpu().numpy().astype(np.float64))
+    assert abs(sb["last_ss"][l] - ss) <= 1e-6 * ss
+
+
 def test_device_schedule_misuse_rejected():
     numel = [8192, 8192, 4096]
     off = G.Grass(numel, gamma=2, offload=True)
