@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python bench.py > gpurun_out/r34_bench.log 2> gpurun_out/r34_bench.err; echo "rc=$?" >> gpurun_out/r34_bench.err
+timeout 600 python tools/diag_zero_copy.py > gpurun_out/r35_zc.log 2>&1; echo "rc=$?" >> gpurun_out/r35_zc.log
