@@ -400,7 +400,9 @@ def workload_config(model: str, gamma: int, world: int) -> dict:
                         (" (configs[1])" if (model, gamma) == ("llama2-7b", 2) else ""),
             "n_layers": shape.n_layers, "layer_numel": shape.layer_numel, "gamma": gamma,
             "active_params_per_step": active, "schedule": "resample every step (T_s=T_u=1)",
-            "l2": f"no flush: {BYTES_PER_PARAM_UPDATE * active / 1e9:.1f} GB streamed per step >> 126 MB L2",
+            "l2": (f"no flush: {BYTES_PER_PARAM_UPDATE * active / 1e9:.1f} GB streamed per step >> 126 MB L2"
+                   if BYTES_PER_PARAM_UPDATE * active > 4 * 126e6 else
+                   "L2-resident: a small test stack, not a measurement configuration"),
             "parallelism": f"dp{world} element-sharded" if world > 1 else "single GPU"}
 
 

@@ -49,6 +49,8 @@ MODELS = {
     "llama2-7b": ModelShape("llama2-7b", 32, 4096, 32, 32, 11008),
     "llama3-8b": ModelShape("llama3-8b", 32, 4096, 32, 8, 14336),
     "llama2-13b": ModelShape("llama2-13b", 40, 5120, 40, 40, 13824),
+    # a small stack with the same block layout: bench.py's legs exercised in seconds (tests/test_gpu_bench.py)
+    "tiny-bench": ModelShape("tiny-bench", 8, 256, 4, 4, 688),
 }
 
 TINY_NUMEL = 65_536
