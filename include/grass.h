@@ -345,7 +345,9 @@ grass_status grass_prefetch_layers(grass_ctx* ctx, const int32_t* layer_ids, int
  * groups), then, if do_commit, the commit, and, if do_resample, the ids of
  * `next_period` — GRASS_PERIOD_NEXT: the period after the current one, kept
  * on the device, so a captured step replays with advancing periods.  lr as
- * grass_step_layers (grass_set_lr_device applies).
+ * grass_step_layers (grass_set_lr_device applies).  Two kernel launches: the
+ * update (which computes the step's AdamW scalars itself) and the per-layer
+ * finalize (window, t_l, and the commit + resample in its last CTA).
  *
  * grass_device_schedule_end: synchronises; copies m, p, committed and the
  * current ids (ids_out: host [gamma], may be NULL) back to the host context;

@@ -3,7 +3,9 @@
 // grass_device_schedule_end): the sampled ids, m, p and the MGN window stay on
 // the device; a step is [prologue -> K2 -> K3 -> commit + resample], all
 // stream-ordered launches with no host synchronisation (
-// DESIGN.md §8).
+// DESIGN.md §8).  Two launches per step: K2 (which computes the step
+// prologue's AdamW scalars itself) and K3 (which advances t_l and, in its
+// last CTA, runs the commit + resample).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -14,11 +16,15 @@
 
 namespace gapi {
 
-// device block d_sched: ids [kMaxDevSeg] | avail [nl] | committed | err
+// device block d_sched: ids [kMaxDevSeg] | avail [nl] | committed | err | K3 done counter
+static size_t sched_words(grass_ctx* c) { return kMaxDevSeg + (size_t)c->nl + 3; }
 static int32_t* sched_ids(grass_ctx* c) { return c->d_sched; }
 static int32_t* sched_avail(grass_ctx* c) { return c->d_sched + kMaxDevSeg; }
 static int32_t* sched_committed(grass_ctx* c) { return c->d_sched + kMaxDevSeg + c->nl; }
 static int32_t* sched_err(grass_ctx* c) { return c->d_sched + kMaxDevSeg + c->nl + 1; }
+static unsigned int* sched_done(grass_ctx* c) {
+  return reinterpret_cast<unsigned int*>(c->d_sched + kMaxDevSeg + c->nl + 2);
+}
 
 static grass_status check_schedulable(grass_ctx* c) {
   if (c->cfg.offload) return c->fail(GRASS_E_STATE, "device schedule: needs HBM-resident states (offload = 0)");
@@ -96,13 +102,13 @@ grass_status grass_device_schedule_begin(grass_ctx* c, uint64_t period, void* st
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if ((s = drain(c, false)) != GRASS_OK) return s;
   if (!c->d_sched) {
-    CUDA_TRY(c, cudaMalloc((void**)&c->d_sched, sizeof(int32_t) * (kMaxDevSeg + (size_t)c->nl + 2)));
+    CUDA_TRY(c, cudaMalloc((void**)&c->d_sched, sizeof(int32_t) * sched_words(c)));
     CUDA_TRY(c, cudaMalloc((void**)&c->d_mgn_m, sizeof(double) * (size_t)c->nl));
     CUDA_TRY(c, cudaMalloc((void**)&c->d_probs, sizeof(double) * (size_t)c->nl));
     CUDA_TRY(c, cudaMalloc((void**)&c->d_period, sizeof(unsigned long long)));
   }
   // the host MGN state -> device; the always-active groups follow the gamma sampled ids
-  std::vector<int32_t> blk(kMaxDevSeg + (size_t)c->nl + 2, 0);
+  std::vector<int32_t> blk(sched_words(c), 0);
   for (int k = 0; k < c->nl - c->nsamp; ++k) blk[c->cfg.gamma + k] = c->nsamp + k;
   blk[kMaxDevSeg + c->nl] = c->committed ? 1 : 0;
   CUDA_TRY(c, cudaMemcpy(c->d_sched, blk.data(), sizeof(int32_t) * blk.size(), cudaMemcpyHostToDevice));
@@ -130,40 +136,36 @@ grass_status grass_device_step(grass_ctx* c, float lr, int32_t do_commit, int32_
     c->captured = true;
   }
   const int n = c->cfg.gamma + (c->nl - c->nsamp);
-  // prologue: t_l += 1 and this step's AdamW scalars of the device ids
-  PrologueArgs pa;
-  std::memset(&pa, 0, sizeof(pa));
-  pa.n = n;
-  pa.dev_ids = sched_ids(c);
-  pa.lr = lr;
-  pa.lr_ptr = c->lr_ptr;
-  pa.beta1 = c->cfg.beta1;
-  pa.beta2 = c->cfg.beta2;
-  pa.wd = c->cfg.weight_decay;
-  pa.bf16 = c->bf16 ? 1 : 0;
-  CUDA_TRY(c, launch_step_prologue(pa, c->st, st));
-  // K2 over the device-sampled layers
+  // K2 over the device-sampled layers, with the step prologue's AdamW scalars
+  // of t_l + 1 computed in each CTA
   Batch b = make_batch(c, kFinalizeMgn);
   b.dev_table = c->d_segtab;
   b.dev_ids = sched_ids(c);
   b.dev_n = n;
+  b.dev_lr = lr;
+  b.dev_lr_ptr = c->lr_ptr;
+  b.dev_beta1 = c->cfg.beta1;
+  b.dev_beta2 = c->cfg.beta2;
+  b.dev_wd = c->cfg.weight_decay;
   {
     TraceScope ts(c, st, GRASS_TRACE_UPDATE, -1, 0, 0);
     CUDA_TRY(c, launch_fused_dev(b, c->st, c->grid_update, st));
   }
-  // K3 of those layers
+  // K3 of those layers: the MGN window, t_l += 1 (bf16: master flag), and
+  // in the CTA that completes last the commit + resample
   FinalizeArgs fa;
   std::memset(&fa, 0, sizeof(fa));
   fa.n = n;
   fa.mode = kFinalizeMgn;
   fa.dev_table = c->d_segtab;
   fa.dev_ids = sched_ids(c);
+  fa.advance = 1;
+  fa.bf16 = c->bf16 ? 1 : 0;
+  fa.fuse_commit = (do_commit || do_resample) ? 1 : 0;
+  fa.done_ctr = sched_done(c);
+  fa.ca = commit_args(c, do_commit != 0, do_resample != 0, next_period);
   CUDA_TRY(c, launch_finalize(fa, c->st, st));
-  c->launches += 3;
-  if (do_commit || do_resample) {
-    CUDA_TRY(c, launch_commit_sample(commit_args(c, do_commit != 0, do_resample != 0, next_period), c->st, st));
-    c->launches++;
-  }
+  c->launches += 2;
   return cap == cudaStreamCaptureStatusActive ? GRASS_OK : mark_pending(c, st);
 } catch (...) {
   return api_exception(c);
@@ -174,7 +176,7 @@ grass_status grass_device_schedule_end(grass_ctx* c, int32_t* ids_out) try {
   if (!c->dev_sched) return c->fail(GRASS_E_STATE, "device schedule is not running");
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
-  std::vector<int32_t> blk(kMaxDevSeg + (size_t)c->nl + 2);
+  std::vector<int32_t> blk(sched_words(c));
   CUDA_TRY(c, cudaMemcpy(blk.data(), c->d_sched, sizeof(int32_t) * blk.size(), cudaMemcpyDeviceToHost));
   CUDA_TRY(c, cudaMemcpy(c->mgn.data(), c->d_mgn_m, sizeof(double) * (size_t)c->nl, cudaMemcpyDeviceToHost));
   CUDA_TRY(c, cudaMemcpy(c->probs.data(), c->d_probs, sizeof(double) * (size_t)c->nl, cudaMemcpyDeviceToHost));

@@ -84,6 +84,12 @@ struct Batch {
   const Seg* dev_table;    // device [n_layers]: the whole-layer segment of every layer
   const int32_t* dev_ids;  // device [dev_n]
   int32_t dev_n;
+  // ... and no step-prologue launch: every CTA computes the step's AdamW
+  // scalars of its (<= kMaxDevSeg) layers from t_l + 1 into shared memory, by
+  // the prologue kernel's arithmetic; K3 then advances t_l (FinalizeArgs::advance)
+  float dev_lr;
+  const float* dev_lr_ptr;  // device scalar (set_lr_device), else dev_lr
+  double dev_beta1, dev_beta2, dev_wd;
 };
 constexpr int kMaxDevSeg = 32;  // layers one device-scheduled launch may update (gamma + n_always)
 
@@ -122,18 +128,6 @@ cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int gr
                          cudaStream_t s);
 // K2 of the device-resident schedule (Batch::dev_table / dev_ids).
 cudaError_t launch_fused_dev(const Batch& b, const DevState& st, int grid, cudaStream_t s);
-// K3 for the layers whose last tiles a stream launch wrote: one CTA each.
-struct FinalizeArgs {
-  int32_t n;               // layers
-  int32_t mode;            // FinalizeMode (kFinalizeMgn / kFinalizeShard)
-  int32_t layer[kMaxSeg];
-  int32_t tiles[kMaxSeg];  // tile partials of the layer (shard)
-  int32_t out_slot[kMaxSeg];
-  int64_t base[kMaxSeg];   // index of the layer's tile 0 in DevState::partials
-  int64_t numel[kMaxSeg];  // N_p(l)
-  const Seg* dev_table;    // device-resident schedule: layer j = dev_ids[j], geometry from dev_table
-  const int32_t* dev_ids;
-};
 // Device-resident commit + resample (grass_device_step): the host's
 // grass_update_probs + grass_sample_layers arithmetic, in fp64 on one thread.
 struct CommitArgs {
@@ -149,6 +143,26 @@ struct CommitArgs {
   int32_t* err;            // device: 1 = commit with zero observations, 2 = non-finite gradient (sticky)
   unsigned long long* period_ctr;  // device: the period of the current ids; period == ~0: resample for ++ctr
 };
+// K3 for the layers whose last tiles a stream launch wrote: one CTA each.
+struct FinalizeArgs {
+  int32_t n;               // layers
+  int32_t mode;            // FinalizeMode (kFinalizeMgn / kFinalizeShard)
+  int32_t layer[kMaxSeg];
+  int32_t tiles[kMaxSeg];  // tile partials of the layer (shard)
+  int32_t out_slot[kMaxSeg];
+  int64_t base[kMaxSeg];   // index of the layer's tile 0 in DevState::partials
+  int64_t numel[kMaxSeg];  // N_p(l)
+  const Seg* dev_table;    // device-resident schedule: layer j = dev_ids[j], geometry from dev_table
+  const int32_t* dev_ids;
+  // device-resident schedule: advance = 1: t_l += 1 (and, bf16, the master
+  // flag set) for each layer — the step prologue's state update, after K2
+  // has read the old t_l; fuse_commit = 1: the CTA that completes last
+  // (done_ctr) then runs the commit + resample of `ca` (one launch less)
+  int32_t advance, bf16, fuse_commit;
+  unsigned int* done_ctr;  // device counter, 0 between launches
+  CommitArgs ca;
+};
+size_t commit_smem_bytes(int nl);
 cudaError_t launch_commit_sample(const CommitArgs& a, const DevState& st, cudaStream_t s);
 cudaError_t launch_finalize(const FinalizeArgs& a, const DevState& st, cudaStream_t s);
 // world > 1: per-layer total = fixed ascending-rank sum of the all-gathered

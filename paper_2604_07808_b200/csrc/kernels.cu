@@ -238,6 +238,167 @@ __device__ __forceinline__ void consumer_sync() {
 // per completed layer of the preceding stream launch (grass_finalize_kernel):
 // the layers finish in parallel, not one after another in the CTA that
 // completed them last (up to ~0.4 ms at the end of a 32-layer probing pass).
+// Device-resident commit + resample (grass_device_step): exactly the host's
+// grass_update_probs (Eq. 2 window mean, first commit / Eq. 4 EMA with frozen
+// retention, Eq. 3 softmax per policy, window reset) and grass_sample_layers
+// (R6 / R7: gamma sequential draws with renormalisation, counter-based
+// SplitMix64) in fp64, on one thread, in the host's operation order (the
+// library is built with --fmad=false: no contraction); only exp() may differ
+// from the host's by an ulp.  A non-finite norm or an empty commit is
+// recorded in *err (sticky) and reported by grass_device_schedule_end.
+__device__ __forceinline__ uint64_t d_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr int kCommitThreads = 256;
+// The commit + resample body, run by one whole CTA (the stand-alone kernel at
+// grass_device_schedule_begin, or the last K3 CTA of a device step).  `sm` is
+// dynamic shared memory of commit_smem_bytes(nl).  S, c and the flag are read
+// through L2: in the fused form they were written by other CTAs of the same
+// launch.
+__device__ void commit_sample_body(const CommitArgs& a, const DevState& st, double* sm) {
+  // operands staged in shared memory; the elementwise steps (window mean,
+  // EMA, exp, the final division) run one layer per thread, the order-
+  // dependent ones (the maxima, the ascending sum, the sampler) on thread 0 —
+  // every value computed by the same operations as the host's loops
+  // sm: S [nl] | m [nl] | p [nl] | c [nl] (int64) | picked [nl] (int32)
+  double* sS = sm;
+  double* sM = sS + a.nl;
+  double* sP = sM + a.nl;
+  long long* sC = reinterpret_cast<long long*>(sP + a.nl);
+  int* sAv = reinterpret_cast<int*>(sC + a.nl);
+  __shared__ int s_err, s_committed, s_commit, s_soft;
+  __shared__ double s_M, s_mx, s_tot;
+  const int tid = threadIdx.x, ns = a.nsamp;
+  for (int l = tid; l < a.nl; l += blockDim.x) {
+    sS[l] = __ldcg(st.S + l);
+    sC[l] = __ldcg(st.c + l);
+    sM[l] = a.m[l];
+    sP[l] = a.probs[l];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s_err = *a.err;
+    s_committed = *a.committed;
+    s_commit = 0;
+    if (!s_err && a.do_commit) {
+      long long total = 0;
+      for (int l = 0; l < ns; ++l) total += sC[l];
+      if (__ldcg(st.flag) != 0) s_err = 2;
+      else if (total == 0 && (s_committed || a.T_p != 0)) s_err = 1;
+      else s_commit = 1;
+    }
+    s_soft = s_commit && (a.policy == GRASS_POLICY_ADAPTIVE || !s_committed) && a.policy != GRASS_POLICY_UNIFORM;
+  }
+  __syncthreads();
+  if (s_err) {  // an error stops the schedule (reported by grass_device_schedule_end)
+    if (tid == 0) *a.err = s_err;
+    return;
+  }
+  const bool committed = s_committed != 0;
+  if (s_commit) {  // Eq. 2 window mean, first commit / Eq. 4 EMA, frozen retention
+    for (int l = tid; l < ns; l += blockDim.x) {
+      if (sC[l] > 0) {
+        const double w = sS[l] / (double)sC[l];
+        sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;
+      } else if (!committed) {
+        sM[l] = 0.0;
+      }
+      if (a.policy == GRASS_POLICY_UNIFORM) sP[l] = 1.0 / ns;
+    }
+  }
+  __syncthreads();
+  if (s_soft && tid < 32) {  // Eq. 3: the maxima — exact, so one warp's tree gives the host loop's values
+    double M = -INFINITY;
+    for (int i = tid; i < ns; i += 32) M = sM[i] > M ? sM[i] : M;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, M, o);
+      M = y > M ? y : M;
+    }
+    double mx = -INFINITY;
+    for (int i = tid; i < ns; i += 32) {
+      const double mti = a.normalize ? (M > 0.0 ? sM[i] / M : 0.0) : sM[i];
+      mx = mti > mx ? mti : mx;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = y > mx ? y : mx;
+    }
+    if (tid == 0) {
+      s_M = M;
+      s_mx = mx;
+    }
+  }
+  __syncthreads();
+  if (s_soft) {
+    const double M = s_M, mx = s_mx;
+    for (int i = tid; i < ns; i += blockDim.x) {
+      const double mti = a.normalize ? (M > 0.0 ? sM[i] / M : 0.0) : sM[i];
+      sP[i] = exp((mti - mx) / a.tau);
+    }
+  }
+  __syncthreads();
+  if (s_soft && tid == 0) {  // the ascending sum
+    double tot = 0.0;
+    for (int i = 0; i < ns; ++i) tot += sP[i];
+    s_tot = tot;
+  }
+  __syncthreads();
+  if (s_soft)
+    for (int i = tid; i < ns; i += blockDim.x) sP[i] = sP[i] / s_tot;
+  __syncthreads();
+  if (tid == 0) {
+    if (a.do_sample) {  // R6 / R7, as grass_sample_layers
+      const uint64_t period = a.period == ~0ull ? *a.period_ctr + 1 : a.period;
+      // the available layers are those not yet picked (sAv[j] = 0), walked
+      // ascending; a picked layer adds +0.0 to R, which leaves it unchanged
+      // (R >= +0), so R and the walk are the host's sums over its avail list
+      for (int j = 0; j < ns; ++j) sAv[j] = 0;
+      const uint64_t key = d_splitmix64(a.seed);
+      for (int k = 0; k < a.gamma; ++k) {
+        const uint64_t ctr = (period << 16) + (uint64_t)k;
+        const double u = (double)(d_splitmix64(key ^ ctr) >> 11) * 0x1.0p-53;
+        double R = 0.0;
+        for (int j = 0; j < ns; ++j) R += sAv[j] ? 0.0 : sP[j];
+        const double x = u * R;
+        double c = 0.0;
+        int pick = -1;
+        for (int j = 0; j < ns; ++j) {
+          if (sAv[j]) continue;
+          c += sP[j];
+          if (x < c) {
+            pick = j;
+            break;
+          }
+        }
+        if (pick < 0)  // none (R == 0): the last available layer
+          for (int j = ns - 1; j >= 0 && pick < 0; --j)
+            if (!sAv[j]) pick = j;
+        a.ids[k] = pick;
+        sAv[pick] = 1;
+      }
+      *a.period_ctr = period;
+    }
+    if (s_commit) *a.committed = 1;
+  }
+  if (s_commit) {  // m, p back; the window restarts (every layer, as the host's reset)
+    for (int l = tid; l < a.nl; l += blockDim.x) {
+      a.m[l] = sM[l];
+      a.probs[l] = sP[l];
+      st.S[l] = 0.0;
+      st.c[l] = 0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCommitThreads) grass_commit_sample_kernel(const __grid_constant__ CommitArgs a,
+                                                                             const DevState st) {
+  extern __shared__ double csm[];
+  commit_sample_body(a, st, csm);
+}
+
 constexpr int kFinThreads = 1024;  // K3 threads per layer (32 warps)
 __global__ void __launch_bounds__(kFinThreads) grass_finalize_kernel(const __grid_constant__ FinalizeArgs fa,
                                                                      const DevState st) {
@@ -276,141 +437,27 @@ __global__ void __launch_bounds__(kFinThreads) grass_finalize_kernel(const __gri
     } else if (fa.mode == kFinalizeShard) {
       st.shard_ss[fa.out_slot[j]] = ss;
     }
+    if (fa.advance) {  // the step prologue's state update (device-resident schedule)
+      st.t[layer] += 1;
+      if (fa.bf16) st.mvalid[layer] = 1;
+    }
+  }
+  if (fa.fuse_commit) {  // the CTA that completes last runs the commit + resample
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(fa.done_ctr, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      extern __shared__ double fsm[];
+      commit_sample_body(fa.ca, st, fsm);
+      if (threadIdx.x == 0) *fa.done_ctr = 0;
+    }
   }
 }
 
-// Device-resident commit + resample (grass_device_step): exactly the host's
-// grass_update_probs (Eq. 2 window mean, first commit / Eq. 4 EMA with frozen
-// retention, Eq. 3 softmax per policy, window reset) and grass_sample_layers
-// (R6 / R7: gamma sequential draws with renormalisation, counter-based
-// SplitMix64) in fp64, on one thread, in the host's operation order (the
-// library is built with --fmad=false: no contraction); only exp() may differ
-// from the host's by an ulp.  A non-finite norm or an empty commit is
-// recorded in *err (sticky) and reported by grass_device_schedule_end.
-__device__ __forceinline__ uint64_t d_splitmix64(uint64_t x) {
-  uint64_t z = x + 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
-}
-constexpr int kCommitThreads = 256;
-__global__ void __launch_bounds__(kCommitThreads) grass_commit_sample_kernel(const __grid_constant__ CommitArgs a,
-                                                                             const DevState st) {
-  // operands staged in shared memory; the elementwise steps (window mean,
-  // EMA, exp, the final division) run one layer per thread, the order-
-  // dependent ones (the maxima, the ascending sum, the sampler) on thread 0 —
-  // every value computed by the same operations as the host's loops
-  extern __shared__ double sm[];  // S [nl] | m [nl] | p [nl] | c [nl] (int64) | avail [nl] (int32)
-  double* sS = sm;
-  double* sM = sS + a.nl;
-  double* sP = sM + a.nl;
-  long long* sC = reinterpret_cast<long long*>(sP + a.nl);
-  int* sAv = reinterpret_cast<int*>(sC + a.nl);
-  __shared__ int s_err, s_committed, s_commit, s_soft;
-  __shared__ double s_M, s_mx, s_tot;
-  const int tid = threadIdx.x, ns = a.nsamp;
-  for (int l = tid; l < a.nl; l += blockDim.x) {
-    sS[l] = st.S[l];
-    sC[l] = st.c[l];
-    sM[l] = a.m[l];
-    sP[l] = a.probs[l];
-  }
-  if (tid == 0) {
-    s_err = *a.err;
-    s_committed = *a.committed;
-    s_commit = 0;
-    if (!s_err && a.do_commit) {
-      long long total = 0;
-      for (int l = 0; l < ns; ++l) total += st.c[l];
-      if (*st.flag != 0) s_err = 2;
-      else if (total == 0 && (s_committed || a.T_p != 0)) s_err = 1;
-      else s_commit = 1;
-    }
-    s_soft = s_commit && (a.policy == GRASS_POLICY_ADAPTIVE || !s_committed) && a.policy != GRASS_POLICY_UNIFORM;
-  }
-  __syncthreads();
-  if (s_err) {  // an error stops the schedule (reported by grass_device_schedule_end)
-    if (tid == 0) *a.err = s_err;
-    return;
-  }
-  const bool committed = s_committed != 0;
-  if (s_commit) {  // Eq. 2 window mean, first commit / Eq. 4 EMA, frozen retention
-    for (int l = tid; l < ns; l += blockDim.x) {
-      if (sC[l] > 0) {
-        const double w = sS[l] / (double)sC[l];
-        sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;
-      } else if (!committed) {
-        sM[l] = 0.0;
-      }
-      if (a.policy == GRASS_POLICY_UNIFORM) sP[l] = 1.0 / ns;
-    }
-  }
-  __syncthreads();
-  if (s_soft && tid == 0) {  // Eq. 3: the maxima (host order)
-    double M = sM[0];
-    for (int i = 1; i < ns; ++i) M = sM[i] > M ? sM[i] : M;
-    s_M = M;
-    auto mt = [&](int i) { return a.normalize ? (M > 0.0 ? sM[i] / M : 0.0) : sM[i]; };
-    double mx = mt(0);
-    for (int i = 1; i < ns; ++i) mx = mt(i) > mx ? mt(i) : mx;
-    s_mx = mx;
-  }
-  __syncthreads();
-  if (s_soft) {
-    const double M = s_M, mx = s_mx;
-    for (int i = tid; i < ns; i += blockDim.x) {
-      const double mti = a.normalize ? (M > 0.0 ? sM[i] / M : 0.0) : sM[i];
-      sP[i] = exp((mti - mx) / a.tau);
-    }
-  }
-  __syncthreads();
-  if (s_soft && tid == 0) {  // the ascending sum
-    double tot = 0.0;
-    for (int i = 0; i < ns; ++i) tot += sP[i];
-    s_tot = tot;
-  }
-  __syncthreads();
-  if (s_soft)
-    for (int i = tid; i < ns; i += blockDim.x) sP[i] = sP[i] / s_tot;
-  __syncthreads();
-  if (tid == 0) {
-    if (a.do_sample) {  // R6 / R7, as grass_sample_layers
-      const uint64_t period = a.period == ~0ull ? *a.period_ctr + 1 : a.period;
-      int navail = ns;
-      for (int i = 0; i < navail; ++i) sAv[i] = i;
-      const uint64_t key = d_splitmix64(a.seed);
-      for (int k = 0; k < a.gamma; ++k) {
-        const uint64_t ctr = (period << 16) + (uint64_t)k;
-        const double u = (double)(d_splitmix64(key ^ ctr) >> 11) * 0x1.0p-53;
-        double R = 0.0;
-        for (int j = 0; j < navail; ++j) R += sP[sAv[j]];
-        const double x = u * R;
-        double c = 0.0;
-        int pick = navail - 1;
-        for (int j = 0; j < navail; ++j) {
-          c += sP[sAv[j]];
-          if (x < c) {
-            pick = j;
-            break;
-          }
-        }
-        a.ids[k] = sAv[pick];
-        for (int j = pick; j + 1 < navail; ++j) sAv[j] = sAv[j + 1];
-        --navail;
-      }
-      *a.period_ctr = period;
-    }
-    if (s_commit) *a.committed = 1;
-  }
-  if (s_commit) {  // m, p back; the window restarts (every layer, as the host's reset)
-    for (int l = tid; l < a.nl; l += blockDim.x) {
-      a.m[l] = sM[l];
-      a.probs[l] = sP[l];
-      st.S[l] = 0.0;
-      st.c[l] = 0;
-    }
-  }
-}
 
 
 // K2 writes its results back into the stage and the producer bulk-stores them
@@ -646,9 +693,17 @@ cudaError_t launch_fused(bool update, const Batch& b, const DevState& st, int gr
                 : launch_stream<false, kNormTPS, kNormStages, false>(b, st, grid, s);
 }
 
+size_t commit_smem_bytes(int nl) { return (size_t)nl * (4 * sizeof(double) + sizeof(int)); }
+
 cudaError_t launch_finalize(const FinalizeArgs& a, const DevState& st, cudaStream_t s) {
   if (a.n <= 0) return cudaSuccess;
-  grass_finalize_kernel<<<a.n, kFinThreads, 0, s>>>(a, st);
+  const size_t smem = a.fuse_commit ? commit_smem_bytes(a.ca.nl) : 0;
+  if (smem > 40 * 1024) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(grass_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024);
+    if (e != cudaSuccess) return e;
+  }
+  grass_finalize_kernel<<<a.n, kFinThreads, smem, s>>>(a, st);
   return cudaGetLastError();
 }
 
@@ -659,7 +714,7 @@ cudaError_t launch_fused_dev(const Batch& b, const DevState& st, int grid, cudaS
 }
 
 cudaError_t launch_commit_sample(const CommitArgs& a, const DevState& st, cudaStream_t s) {
-  const size_t smem = (size_t)a.nl * (4 * sizeof(double) + sizeof(int));
+  const size_t smem = commit_smem_bytes(a.nl);
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(grass_commit_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)smem);

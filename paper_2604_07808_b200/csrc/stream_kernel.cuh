@@ -251,6 +251,10 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
   __shared__ __align__(16) Seg dsegs[DEVB ? kMaxDevSeg : 1];
   __shared__ int dids[DEVB ? kMaxDevSeg : 1];
   __shared__ int dn;
+  // ... and their AdamW scalars and bf16 master-initialisation flags (the
+  // step prologue's arithmetic, per CTA; K3 advances t_l after this launch)
+  __shared__ float dscal[DEVB ? kMaxDevSeg : 1][3];
+  __shared__ int dinit[DEVB ? kMaxDevSeg : 1];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (DEVB) {
@@ -270,6 +274,17 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     for (int w = tid; w < dn * kWords; w += blockDim.x)
       reinterpret_cast<unsigned long long*>(dsegs)[w] =
           reinterpret_cast<const unsigned long long*>(b.dev_table + dids[w / kWords])[w % kWords];
+    if (UPDATE && tid < dn) {  // as grass_step_prologue_kernel, for t = t_l + 1
+      const int l = dids[tid];
+      const long long t = st.t[l] + 1;
+      const double lr = b.dev_lr_ptr ? (double)*b.dev_lr_ptr : (double)b.dev_lr;
+      const double bc1 = 1.0 - pow(b.dev_beta1, (double)t);
+      const double bc2 = 1.0 - pow(b.dev_beta2, (double)t);
+      dscal[tid][0] = (float)(1.0 - lr * b.dev_wd);
+      dscal[tid][1] = (float)(lr / bc1);
+      dscal[tid][2] = (float)(1.0 / sqrt(bc2));
+      dinit[tid] = BF16 && !st.mvalid[l] ? 1 : 0;
+    }
     __syncthreads();
   }
   const Seg* const segs = DEVB ? dsegs : b.seg;
@@ -324,7 +339,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
           pend_nv[stage] = nv;
         }
         if (nv && (UPDATE || !P2P)) {
-          const bool init = BF16 && UPDATE && st.init_now[sg.layer];
+          const bool init = BF16 && UPDATE && (DEVB ? dinit[s] : st.init_now[sg.layer]);
           // P2P: the gradient slices go to the gradient ring (below)
           const uint32_t tx = (P2P ? 0u : nv * (uint32_t)L::GB) + (UPDATE ? nv * (init ? 2u : 4u) + 8u * nv : 0u);
           mbar_arrive_expect_tx(&full_bar[stage], tx);
@@ -404,12 +419,12 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
     sc.b1 = b.beta1; sc.omb1 = b.one_minus_beta1; sc.b2 = b.beta2; sc.omb2 = b.one_minus_beta2;
     sc.eps = b.eps;
     if (UPDATE) {  // this step's AdamW scalars of the layer (step prologue)
-      sc.decay = st.scal[3 * sg.layer];
-      sc.step = st.scal[3 * sg.layer + 1];
-      sc.inv_bc2s = st.scal[3 * sg.layer + 2];
+      sc.decay = DEVB ? dscal[s][0] : st.scal[3 * sg.layer];
+      sc.step = DEVB ? dscal[s][1] : st.scal[3 * sg.layer + 1];
+      sc.inv_bc2s = DEVB ? dscal[s][2] : st.scal[3 * sg.layer + 2];
     }
     sc.cf = cf;
-    const bool init = BF16 && UPDATE && st.init_now[sg.layer];
+    const bool init = BF16 && UPDATE && (DEVB ? dinit[s] : st.init_now[sg.layer]);
     const int ui = u - unit_prefix[s];
     const int64_t e0 = (int64_t)ui * kUnit;
     const int ne = (int)min((int64_t)kUnit, sg.n - e0);

@@ -48,7 +48,8 @@ MUTANTS = {
     9: ("P2P: theta' not stored into the last rank's parameters",
         [(S, "for (int q = 0; q < ntp; ++q) {", "for (int q = 0; q < ntp - 1; ++q) {")]),
     10: ("bf16: master never initialised from the bf16 parameter",
-         [(S, "const bool init = BF16 && UPDATE && st.init_now[sg.layer];", "const bool init = false;")]),
+         [(S, "const bool init = BF16 && UPDATE && (DEVB ? dinit[s] : st.init_now[sg.layer]);",
+           "const bool init = false;")]),
     11: ("non-finite norm not flagged",
          [(K, "atomicMax(st.flag, INT_MAX - layer);  // smallest id wins", "(void)0;")]),
     12: ("norm: all-tiles warp reduction (warp_sum_perm) fed in tile order instead of the lane's permuted order",
@@ -70,10 +71,17 @@ MUTANTS = {
          [(K, "sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;",
            "sM[l] = committed ? (1.0 - a.alpha) * w + a.alpha * sM[l] : w;")]),
     21: ("device schedule: sampler mass R not renormalised over the still-available layers (R6)",
-         [(K, "for (int j = 0; j < navail; ++j) R += sP[sAv[j]];", "for (int j = 0; j < ns; ++j) R += sP[j];")]),
+         [(K, "for (int j = 0; j < ns; ++j) R += sAv[j] ? 0.0 : sP[j];", "for (int j = 0; j < ns; ++j) R += sP[j];")]),
     22: ("device schedule: the sampling period not advanced",
          [(K, "const uint64_t period = a.period == ~0ull ? *a.period_ctr + 1 : a.period;",
            "const uint64_t period = a.period == ~0ull ? *a.period_ctr : a.period;")]),
+    23: ("device step: K3 does not advance t_l (the step prologue's state update)",
+         [(K, "      st.t[layer] += 1;\n", "\n")]),
+    24: ("device step: K2's inline prologue takes t_l instead of t_l + 1",
+         [(S, "const long long t = st.t[l] + 1;\n      const double lr = b.dev_lr_ptr",
+           "const long long t = st.t[l];\n      const double lr = b.dev_lr_ptr")]),
+    25: ("device step: the fused commit's done counter not reset (no commit after the first step)",
+         [(K, "if (threadIdx.x == 0) *fa.done_ctr = 0;", "(void)0;")]),
     14: ("P2P barrier self-test: start barrier removed",
          [(K, "    a.which = 0;  // start barrier: every rank has read its rows of this round\n"
               "    const int n_save = a.n;\n    a.n = 0;\n    p2p_sync_cta(a);\n    a.n = n_save;\n", "")]),
