@@ -307,7 +307,7 @@ def measure_read_ceiling(dev, gib: int = 8) -> dict:
 
     import torch
     from paper_2604_07808_b200 import build as B
-    lib = C.CDLL(B.DIAG_OUT)
+    lib = C.CDLL(B.build_diag())                 # built in-tree by __graft_entry__.build()
     f = lib.grass_diag_read
     f.restype = C.c_int
     f.argtypes = [C.c_void_p, C.c_ulonglong, C.c_int, C.c_int, C.c_uint, C.c_int, C.c_void_p, C.c_void_p]
@@ -356,7 +356,7 @@ def measure_mix_ceiling(dev, n: int = 2 * 202_383_360) -> dict:
 
     import torch
     from paper_2604_07808_b200 import build as B
-    lib = C.CDLL(B.DIAG_OUT)
+    lib = C.CDLL(B.build_diag())                 # built in-tree by __graft_entry__.build()
     ft, fl = lib.grass_diag_rw43_tma, lib.grass_diag_rw43
     ft.restype = fl.restype = C.c_int
     ft.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_uint, C.c_int, C.c_int, C.c_void_p]
