@@ -45,6 +45,7 @@
 #include <climits>
 #include <cstdint>
 #include <type_traits>
+#include <utility>
 
 #include "grass_internal.h"
 
@@ -54,6 +55,10 @@ namespace {
 constexpr int kConsumerWarps = kThreads / 32;  // 16
 
 constexpr int kStreamThreads = kThreads + 32;  // + 1 producer warp
+
+// griddepcontrol.wait: a no-op unless the grid was launched as a programmatic
+// dependent of the previous kernel on the stream (launch_pdl)
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
@@ -404,6 +409,7 @@ __global__ void __launch_bounds__(kFinThreads) grass_finalize_kernel(const __gri
                                                                      const DevState st) {
   constexpr int kW = kFinThreads / 32;
   __shared__ double red[kW];
+  grid_dependency_wait();  // PDL (device step): K2's partials are complete and visible
   const int j = blockIdx.x;
   const int layer = fa.dev_ids ? fa.dev_ids[j] : fa.layer[j];
   const int n = fa.dev_ids ? fa.dev_table[layer].layer_tiles : fa.tiles[j];
@@ -647,6 +653,27 @@ constexpr int kNormStagesBf16 = GRASS_NORM_STAGES_BF16;
 #endif
 constexpr int kP2PNormTPS = GRASS_P2P_NORM_TPS;  // P2P probing: tiles per gradient-ring slot
 
+// Programmatic dependent launch (the device-resident schedule's two kernels):
+// the grid may be launched while the previous kernel on the stream drains;
+// the kernel's griddepcontrol.wait (grid_dependency_wait) holds every read of
+// the previous kernel's results until that kernel has completed and its
+// writes are visible.  No kernel triggers early, so the dependency is full
+// completion; what overlaps is the launch and CTA ramp.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int threads, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 template <bool U, int TPS, int ST, bool BF16, bool P2P = false, bool DEVB = false>
 cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStream_t s) {
   using SL = StageLayout<U, BF16, TPS>;
@@ -670,6 +697,7 @@ cudaError_t launch_stream(const Batch& b, const DevState& st, int grid, cudaStre
   int units = 0;
   for (int i = 0; i < b.nseg; ++i) units += (b.seg[i].tiles + TPS - 1) / TPS;
   const int g = DEVB ? grid : (grid < units ? grid : units);  // DEVB: the units are known on the device only
+  if (DEVB) return launch_pdl(grass_stream_kernel<U, TPS, ST, BF16, P2P, DEVB>, g, kStreamThreads, smem, s, b, st);
   grass_stream_kernel<U, TPS, ST, BF16, P2P, DEVB><<<g, kStreamThreads, smem, s>>>(b, st);
   return cudaGetLastError();
 }
@@ -703,6 +731,7 @@ cudaError_t launch_finalize(const FinalizeArgs& a, const DevState& st, cudaStrea
         cudaFuncSetAttribute(grass_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024);
     if (e != cudaSuccess) return e;
   }
+  if (a.dev_ids) return launch_pdl(grass_finalize_kernel, a.n, kFinThreads, smem, s, a, st);
   grass_finalize_kernel<<<a.n, kFinThreads, smem, s>>>(a, st);
   return cudaGetLastError();
 }

@@ -258,6 +258,7 @@ grass_stream_kernel(const __grid_constant__ Batch b, const DevState st) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (DEVB) {
+    grid_dependency_wait();  // PDL: the previous step's K3 (ids, t_l, window) is complete and visible
     if (tid == 0) {  // ids ascending (R12), insertion sort of <= kMaxDevSeg entries
       const int n = b.dev_n < kMaxDevSeg ? b.dev_n : kMaxDevSeg;
       for (int j = 0; j < n; ++j) {
