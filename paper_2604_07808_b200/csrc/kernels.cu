@@ -274,9 +274,17 @@ __device__ void commit_sample_body(const CommitArgs& a, const DevState& st, doub
   double* sP = sM + a.nl;
   long long* sC = reinterpret_cast<long long*>(sP + a.nl);
   int* sAv = reinterpret_cast<int*>(sC + a.nl);
-  __shared__ int s_err, s_committed, s_commit, s_soft;
+  __shared__ int s_err, s_committed, s_commit, s_soft, s_flag;
+  __shared__ unsigned long long s_pctr;
   __shared__ double s_M, s_mx, s_tot;
   const int tid = threadIdx.x, ns = a.nsamp;
+  // every operand load issued at once (the scalars by threads of their own —
+  // they sit in HBM after K2's stream, so a chain of them would cost a DRAM
+  // round trip each)
+  if (tid == 32) s_err = *a.err;
+  if (tid == 33) s_committed = *a.committed;
+  if (tid == 34) s_flag = __ldcg(st.flag);
+  if (tid == 35) s_pctr = a.do_sample ? *a.period_ctr : 0ull;
   for (int l = tid; l < a.nl; l += blockDim.x) {
     sS[l] = __ldcg(st.S + l);
     sC[l] = __ldcg(st.c + l);
@@ -285,13 +293,11 @@ __device__ void commit_sample_body(const CommitArgs& a, const DevState& st, doub
   }
   __syncthreads();
   if (tid == 0) {
-    s_err = *a.err;
-    s_committed = *a.committed;
     s_commit = 0;
     if (!s_err && a.do_commit) {
       long long total = 0;
       for (int l = 0; l < ns; ++l) total += sC[l];
-      if (__ldcg(st.flag) != 0) s_err = 2;
+      if (s_flag != 0) s_err = 2;
       else if (total == 0 && (s_committed || a.T_p != 0)) s_err = 1;
       else s_commit = 1;
     }
@@ -354,40 +360,51 @@ __device__ void commit_sample_body(const CommitArgs& a, const DevState& st, doub
   if (s_soft)
     for (int i = tid; i < ns; i += blockDim.x) sP[i] = sP[i] / s_tot;
   __syncthreads();
-  if (tid == 0) {
-    if (a.do_sample) {  // R6 / R7, as grass_sample_layers
-      const uint64_t period = a.period == ~0ull ? *a.period_ctr + 1 : a.period;
-      // the available layers are those not yet picked (sAv[j] = 0), walked
-      // ascending; a picked layer adds +0.0 to R, which leaves it unchanged
-      // (R >= +0), so R and the walk are the host's sums over its avail list
-      for (int j = 0; j < ns; ++j) sAv[j] = 0;
-      const uint64_t key = d_splitmix64(a.seed);
-      for (int k = 0; k < a.gamma; ++k) {
-        const uint64_t ctr = (period << 16) + (uint64_t)k;
-        const double u = (double)(d_splitmix64(key ^ ctr) >> 11) * 0x1.0p-53;
-        double R = 0.0;
-        for (int j = 0; j < ns; ++j) R += sAv[j] ? 0.0 : sP[j];
-        const double x = u * R;
+  if (tid < 32 && a.do_sample) {  // R6 / R7, as grass_sample_layers, by warp 0
+    const uint64_t period = a.period == ~0ull ? s_pctr + 1 : a.period;
+    // the available layers are those not yet picked (sAv[j] = 0), ascending.
+    // Lane 0 forms the running sum over them in order — a picked layer adds
+    // +0.0, which leaves the sum unchanged (>= +0) — into sS[j] (the window
+    // sums are no longer needed): sS[j] is the host walk's c at layer j and
+    // sS[ns-1] its R.  The pick is the first available j with x < c_j (a
+    // ballot), else the last available layer (only when R == 0).
+    for (int j = tid; j < ns; j += 32) sAv[j] = 0;
+    __syncwarp();
+    const uint64_t key = d_splitmix64(a.seed);
+    for (int k = 0; k < a.gamma; ++k) {
+      const uint64_t ctr = (period << 16) + (uint64_t)k;
+      const double u = (double)(d_splitmix64(key ^ ctr) >> 11) * 0x1.0p-53;
+      if (tid == 0) {
         double c = 0.0;
-        int pick = -1;
         for (int j = 0; j < ns; ++j) {
-          if (sAv[j]) continue;
-          c += sP[j];
-          if (x < c) {
-            pick = j;
-            break;
-          }
+          c += sAv[j] ? 0.0 : sP[j];
+          sS[j] = c;
         }
-        if (pick < 0)  // none (R == 0): the last available layer
-          for (int j = ns - 1; j >= 0 && pick < 0; --j)
-            if (!sAv[j]) pick = j;
+      }
+      __syncwarp();
+      const double R = sS[ns - 1];
+      const double x = u * R;
+      int pick = -1;
+      for (int base = 0; base < ns && pick < 0; base += 32) {
+        const int j = base + tid;
+        const unsigned hit = __ballot_sync(0xffffffffu, j < ns && !sAv[j] && x < sS[j]);
+        if (hit) pick = base + __ffs(hit) - 1;
+      }
+      for (int base = (ns - 1) & ~31; base >= 0 && pick < 0; base -= 32) {  // none: the last available layer
+        const int j = base + tid;
+        const unsigned av = __ballot_sync(0xffffffffu, j < ns && !sAv[j]);
+        if (av) pick = base + 31 - __clz(av);
+      }
+      __syncwarp();
+      if (tid == 0) {
         a.ids[k] = pick;
         sAv[pick] = 1;
       }
-      *a.period_ctr = period;
+      __syncwarp();
     }
-    if (s_commit) *a.committed = 1;
+    if (tid == 0) *a.period_ctr = period;
   }
+  if (tid == 0 && s_commit) *a.committed = 1;
   if (s_commit) {  // m, p back; the window restarts (every layer, as the host's reset)
     for (int l = tid; l < a.nl; l += blockDim.x) {
       a.m[l] = sM[l];
@@ -414,6 +431,15 @@ __global__ void __launch_bounds__(kFinThreads) grass_finalize_kernel(const __gri
   const int layer = fa.dev_ids ? fa.dev_ids[j] : fa.layer[j];
   const int n = fa.dev_ids ? fa.dev_table[layer].layer_tiles : fa.tiles[j];
   const double* P = st.partials + (fa.dev_ids ? fa.dev_table[layer].part_layer_base : fa.base[j]);
+  // thread 0's operands of the window update, loaded alongside the partials
+  // (only this CTA writes them; the kernels before it have completed)
+  double S0 = 0.0, numel = 1.0;
+  long long c0 = 0;
+  if (threadIdx.x == 0 && fa.mode == kFinalizeMgn) {
+    S0 = st.S[layer];
+    c0 = st.c[layer];
+    numel = (double)(fa.dev_ids ? fa.dev_table[layer].layer_numel : fa.numel[j]);
+  }
   double a = 0.0;
   int i = threadIdx.x;
   for (; i + 15 * kFinThreads < n; i += 16 * kFinThreads) {  // 16 loads in flight per thread
@@ -435,8 +461,8 @@ __global__ void __launch_bounds__(kFinThreads) grass_finalize_kernel(const __gri
     if (fa.mode == kFinalizeMgn) {
       st.last_ss[layer] = ss;
       if (isfinite(ss)) {
-        st.S[layer] += sqrt(ss / (double)(fa.dev_ids ? fa.dev_table[layer].layer_numel : fa.numel[j]));  // Eq. 2 inner term
-        st.c[layer] += 1;
+        st.S[layer] = S0 + sqrt(ss / numel);  // Eq. 2 inner term
+        st.c[layer] = c0 + 1;
       } else {
         atomicMax(st.flag, INT_MAX - layer);  // smallest id wins
       }

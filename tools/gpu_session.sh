@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for i in 1 2; do timeout 600 python bench.py --legs main > gpurun_out/r42_bench$i.log 2> gpurun_out/r42_bench$i.err; done
+timeout 900 ncu --section SourceCounters --section WarpStateStats --warp-sampling-interval 0 --clock-control none --import-source on -k regex:grass_finalize -s 5 -c 1 -o gpurun_out/r45_k3 python tools/device_step_profile.py > gpurun_out/r45_ncu_k3.log 2>&1
+timeout 900 ncu --section SourceCounters --section WarpStateStats --warp-sampling-interval 0 --clock-control none --import-source on -k regex:grass_commit -c 1 -o gpurun_out/r45_cm python tools/device_step_profile.py > gpurun_out/r45_ncu_cm.log 2>&1

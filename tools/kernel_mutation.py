@@ -71,10 +71,11 @@ MUTANTS = {
          [(K, "sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;",
            "sM[l] = committed ? (1.0 - a.alpha) * w + a.alpha * sM[l] : w;")]),
     21: ("device schedule: sampler mass R not renormalised over the still-available layers (R6)",
-         [(K, "for (int j = 0; j < ns; ++j) R += sAv[j] ? 0.0 : sP[j];", "for (int j = 0; j < ns; ++j) R += sP[j];")]),
+         [(K, "      const double R = sS[ns - 1];",
+           "      double R = 0.0;\n      for (int j = 0; j < ns; ++j) R += sP[j];")]),
     22: ("device schedule: the sampling period not advanced",
-         [(K, "const uint64_t period = a.period == ~0ull ? *a.period_ctr + 1 : a.period;",
-           "const uint64_t period = a.period == ~0ull ? *a.period_ctr : a.period;")]),
+         [(K, "const uint64_t period = a.period == ~0ull ? s_pctr + 1 : a.period;",
+           "const uint64_t period = a.period == ~0ull ? s_pctr : a.period;")]),
     23: ("device step: K3 does not advance t_l (the step prologue's state update)",
          [(K, "      st.t[layer] += 1;\n", "\n")]),
     24: ("device step: K2's inline prologue takes t_l instead of t_l + 1",
