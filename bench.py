@@ -631,16 +631,26 @@ def run_grass(args, rank, world, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         barrier(world)
+        if use_dev:                               # the device-resident schedule, as the main leg
+            ctx.device_schedule_begin(10_000, stream=s)
+            torch.cuda.synchronize()
         e0.record(s)
         for k in range(2 * T):
+            if use_dev:                           # commit + resample after the period's last step
+                last = (k + 1) % T == 0
+                ctx.device_step(args.lr, commit=last, resample=last, stream=s)
+                continue
             if k and k % T == 0:                  # period boundary (the window holds T steps)
                 ctx.update_probs()
                 ids = ctx.sample_layers(10_000 + k // T)
             ctx.step_layers(ids, [params[l] for l in ids], [grads[l] for l in ids], args.lr, stream=s)
         e1.record(s)
         torch.cuda.synchronize()
+        if use_dev:
+            ids = ctx.device_schedule_end()
         t = max_over_ranks(e0.elapsed_time(e1) / 1e3, world, dev) / (2 * T)
-        return {"schedule": f"T_s=T_u={T} (2 periods)", "step_ms": t * 1e3, "params_per_s": active / t}
+        return {"schedule": f"T_s=T_u={T} (2 periods)", "step_ms": t * 1e3, "params_per_s": active / t,
+                "driver": "grass_device_step" if use_dev else "grass_step_layers + host commit / sampler"}
 
     paper_schedule = guarded("main", leg_paper_schedule)
     ctx.close()                                 # frees its 51.8 GB of HBM state
