@@ -27,7 +27,9 @@
 // GRASS_NORM_TPS_BF16, GRASS_NORM_STAGES, GRASS_NORM_STAGES_BF16,
 // GRASS_P2P_NORM_TPS, GRASS_UPD_GRID_SUB, GRASS_NORM_GRID_SUB,
 // GRASS_L2_PREFETCH_{NORM,UPD}, GRASS_UNIT_BLOCK, GRASS_BF16_GUARD (0: no exact
-// fallback — wrong for tiny / huge gradients), GRASS_K1_DRAIN (diagnostic).
+// fallback — wrong for tiny / huge gradients), GRASS_K1_DRAIN (diagnostic),
+// GRASS_K3_DIAG (diagnostic: 1 = the fused commit's last CTA skips the body,
+// 2 = no done counter / fence either, 3 = the body without the sampler).
 // The mutation check of the GPU tests (tools/kernel_mutation.py) plants its
 // mistakes into a patched copy of this
 // source; the product source carries none.
@@ -360,29 +362,39 @@ __device__ void commit_sample_body(const CommitArgs& a, const DevState& st, doub
   if (s_soft)
     for (int i = tid; i < ns; i += blockDim.x) sP[i] = sP[i] / s_tot;
   __syncthreads();
-  if (tid < 32 && a.do_sample) {  // R6 / R7, as grass_sample_layers, by warp 0
+#ifndef GRASS_K3_DIAG
+#define GRASS_K3_DIAG 0
+#endif
+  if (tid < 32 && a.do_sample && GRASS_K3_DIAG != 3) {  // R6 / R7, as grass_sample_layers, by warp 0
     const uint64_t period = a.period == ~0ull ? s_pctr + 1 : a.period;
     // the available layers are those not yet picked (sAv[j] = 0), ascending.
-    // Lane 0 forms the running sum over them in order — a picked layer adds
-    // +0.0, which leaves the sum unchanged (>= +0) — into sS[j] (the window
-    // sums are no longer needed): sS[j] is the host walk's c at layer j and
-    // sS[ns-1] its R.  The pick is the first available j with x < c_j (a
-    // ballot), else the last available layer (only when R == 0).
+    // The warp forms the running sum over them in order — layer j's term
+    // broadcast from its lane, so the chain of additions waits on no memory;
+    // a picked layer adds +0.0, which leaves the sum unchanged (>= +0) — and
+    // lane j keeps it in sS[j] (the window sums are no longer needed): sS[j]
+    // is the host walk's c at layer j and the final sum its R.  The pick is
+    // the first available j with x < c_j (a ballot), else the last available
+    // layer (only when R == 0).
     for (int j = tid; j < ns; j += 32) sAv[j] = 0;
     __syncwarp();
     const uint64_t key = d_splitmix64(a.seed);
     for (int k = 0; k < a.gamma; ++k) {
       const uint64_t ctr = (period << 16) + (uint64_t)k;
       const double u = (double)(d_splitmix64(key ^ ctr) >> 11) * 0x1.0p-53;
-      if (tid == 0) {
-        double c = 0.0;
-        for (int j = 0; j < ns; ++j) {
-          c += sAv[j] ? 0.0 : sP[j];
-          sS[j] = c;
+      double c = 0.0;
+      for (int base = 0; base < ns; base += 32) {
+        const int j = base + tid;
+        const double term = j < ns && !sAv[j] ? sP[j] : 0.0;
+        double cj = 0.0;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {  // lanes past ns hold +0.0: the sum is unchanged
+          c += __shfl_sync(0xffffffffu, term, q);
+          cj = tid == q ? c : cj;
         }
+        if (j < ns) sS[j] = cj;
       }
       __syncwarp();
-      const double R = sS[ns - 1];
+      const double R = c;
       const double x = u * R;
       int pick = -1;
       for (int base = 0; base < ns && pick < 0; base += 32) {
@@ -474,7 +486,10 @@ __global__ void __launch_bounds__(kFinThreads) grass_finalize_kernel(const __gri
       if (fa.bf16) st.mvalid[layer] = 1;
     }
   }
-  if (fa.fuse_commit) {  // the CTA that completes last runs the commit + resample
+#ifndef GRASS_K3_DIAG
+#define GRASS_K3_DIAG 0
+#endif
+  if (fa.fuse_commit && GRASS_K3_DIAG != 2) {  // the CTA that completes last runs the commit + resample
     __shared__ int last;
     if (threadIdx.x == 0) {
       __threadfence();
@@ -484,7 +499,7 @@ __global__ void __launch_bounds__(kFinThreads) grass_finalize_kernel(const __gri
     if (last) {
       __threadfence();
       extern __shared__ double fsm[];
-      commit_sample_body(fa.ca, st, fsm);
+      if (GRASS_K3_DIAG != 1) commit_sample_body(fa.ca, st, fsm);
       if (threadIdx.x == 0) *fa.done_ctr = 0;
     }
   }

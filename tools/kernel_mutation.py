@@ -71,7 +71,7 @@ MUTANTS = {
          [(K, "sM[l] = committed ? a.alpha * w + (1.0 - a.alpha) * sM[l] : w;",
            "sM[l] = committed ? (1.0 - a.alpha) * w + a.alpha * sM[l] : w;")]),
     21: ("device schedule: sampler mass R not renormalised over the still-available layers (R6)",
-         [(K, "      const double R = sS[ns - 1];",
+         [(K, "      const double R = c;",
            "      double R = 0.0;\n      for (int j = 0; j < ns; ++j) R += sP[j];")]),
     22: ("device schedule: the sampling period not advanced",
          [(K, "const uint64_t period = a.period == ~0ull ? s_pctr + 1 : a.period;",

@@ -12,10 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {   # edit per experiment; the knobs are listed at the top of csrc/kernels.cu
     "base": [],
-    "p2p_norm_tps6": ["GRASS_P2P_NORM_TPS=6"],
-    "p2p_norm_tps8": ["GRASS_P2P_NORM_TPS=8"],
-    "p2p_norm_tps2": ["GRASS_P2P_NORM_TPS=2"],
-    "base_again": [],
+    "k3_nosampler": ["GRASS_K3_DIAG=3"],
 }
 OUTDIR = os.path.join(ROOT, "build", "variants")
 
