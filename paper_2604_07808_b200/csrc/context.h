@@ -139,7 +139,7 @@ struct grass_ctx {
   // device-resident schedule (device_schedule.cpp)
   Seg* d_segtab = nullptr;      // device [nl]: whole-layer segment of every registered layer
   std::vector<char> registered;
-  int32_t* d_sched = nullptr;   // device block: ids [kMaxDevSeg] | avail [nl] | committed | err
+  int32_t* d_sched = nullptr;   // device block: ids [kMaxDevSeg] | committed | err | K3 done counter
   double* d_mgn_m = nullptr;    // device [nl] committed MGN
   double* d_probs = nullptr;    // device [nl]
   unsigned long long* d_period = nullptr;  // device: sampling period of the current ids

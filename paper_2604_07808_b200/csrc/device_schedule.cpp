@@ -16,15 +16,12 @@
 
 namespace gapi {
 
-// device block d_sched: ids [kMaxDevSeg] | avail [nl] | committed | err | K3 done counter
-static size_t sched_words(grass_ctx* c) { return kMaxDevSeg + (size_t)c->nl + 3; }
+// device block d_sched: ids [kMaxDevSeg] | committed | err | K3 done counter
+enum : int { kSchedCommitted = kMaxDevSeg, kSchedErr, kSchedDone, kSchedWords };
 static int32_t* sched_ids(grass_ctx* c) { return c->d_sched; }
-static int32_t* sched_avail(grass_ctx* c) { return c->d_sched + kMaxDevSeg; }
-static int32_t* sched_committed(grass_ctx* c) { return c->d_sched + kMaxDevSeg + c->nl; }
-static int32_t* sched_err(grass_ctx* c) { return c->d_sched + kMaxDevSeg + c->nl + 1; }
-static unsigned int* sched_done(grass_ctx* c) {
-  return reinterpret_cast<unsigned int*>(c->d_sched + kMaxDevSeg + c->nl + 2);
-}
+static int32_t* sched_committed(grass_ctx* c) { return c->d_sched + kSchedCommitted; }
+static int32_t* sched_err(grass_ctx* c) { return c->d_sched + kSchedErr; }
+static unsigned int* sched_done(grass_ctx* c) { return reinterpret_cast<unsigned int*>(c->d_sched + kSchedDone); }
 
 static grass_status check_schedulable(grass_ctx* c) {
   if (c->cfg.offload) return c->fail(GRASS_E_STATE, "device schedule: needs HBM-resident states (offload = 0)");
@@ -54,7 +51,6 @@ static CommitArgs commit_args(grass_ctx* c, bool commit, bool sample, uint64_t p
   a.probs = c->d_probs;
   a.committed = sched_committed(c);
   a.ids = sched_ids(c);
-  a.avail = sched_avail(c);
   a.err = sched_err(c);
   a.period_ctr = c->d_period;
   return a;
@@ -102,15 +98,15 @@ grass_status grass_device_schedule_begin(grass_ctx* c, uint64_t period, void* st
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if ((s = drain(c, false)) != GRASS_OK) return s;
   if (!c->d_sched) {
-    CUDA_TRY(c, cudaMalloc((void**)&c->d_sched, sizeof(int32_t) * sched_words(c)));
+    CUDA_TRY(c, cudaMalloc((void**)&c->d_sched, sizeof(int32_t) * kSchedWords));
     CUDA_TRY(c, cudaMalloc((void**)&c->d_mgn_m, sizeof(double) * (size_t)c->nl));
     CUDA_TRY(c, cudaMalloc((void**)&c->d_probs, sizeof(double) * (size_t)c->nl));
     CUDA_TRY(c, cudaMalloc((void**)&c->d_period, sizeof(unsigned long long)));
   }
   // the host MGN state -> device; the always-active groups follow the gamma sampled ids
-  std::vector<int32_t> blk(sched_words(c), 0);
+  std::vector<int32_t> blk(kSchedWords, 0);
   for (int k = 0; k < c->nl - c->nsamp; ++k) blk[c->cfg.gamma + k] = c->nsamp + k;
-  blk[kMaxDevSeg + c->nl] = c->committed ? 1 : 0;
+  blk[kSchedCommitted] = c->committed ? 1 : 0;
   CUDA_TRY(c, cudaMemcpy(c->d_sched, blk.data(), sizeof(int32_t) * blk.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(c, cudaMemcpy(c->d_mgn_m, c->mgn.data(), sizeof(double) * (size_t)c->nl, cudaMemcpyHostToDevice));
   CUDA_TRY(c, cudaMemcpy(c->d_probs, c->probs.data(), sizeof(double) * (size_t)c->nl, cudaMemcpyHostToDevice));
@@ -176,7 +172,7 @@ grass_status grass_device_schedule_end(grass_ctx* c, int32_t* ids_out) try {
   if (!c->dev_sched) return c->fail(GRASS_E_STATE, "device schedule is not running");
   grass_status s = drain(c, false);
   if (s != GRASS_OK) return s;
-  std::vector<int32_t> blk(sched_words(c));
+  std::vector<int32_t> blk(kSchedWords);
   CUDA_TRY(c, cudaMemcpy(blk.data(), c->d_sched, sizeof(int32_t) * blk.size(), cudaMemcpyDeviceToHost));
   CUDA_TRY(c, cudaMemcpy(c->mgn.data(), c->d_mgn_m, sizeof(double) * (size_t)c->nl, cudaMemcpyDeviceToHost));
   CUDA_TRY(c, cudaMemcpy(c->probs.data(), c->d_probs, sizeof(double) * (size_t)c->nl, cudaMemcpyDeviceToHost));
@@ -185,10 +181,10 @@ grass_status grass_device_schedule_end(grass_ctx* c, int32_t* ids_out) try {
     CUDA_TRY(c, cudaMemcpy(mv.data(), c->st.mvalid, sizeof(int) * c->nl, cudaMemcpyDeviceToHost));
     for (int l = 0; l < c->nl; ++l) c->master_valid[l] = mv[l] ? 1 : 0;
   }
-  c->committed = blk[kMaxDevSeg + c->nl] != 0;
+  c->committed = blk[kSchedCommitted] != 0;
   if (ids_out) std::memcpy(ids_out, blk.data(), sizeof(int32_t) * c->cfg.gamma);
   c->dev_sched = false;
-  const int err = blk[kMaxDevSeg + c->nl + 1];
+  const int err = blk[kSchedErr];
   if (err == 2) {  // the non-finite flag is taken (reset) as grass_update_probs does
     if ((s = fetch_mgn(c, false, true)) != GRASS_OK) return s;
     return report_flag(c);

@@ -115,7 +115,6 @@ struct DevState {
 struct PrologueArgs {
   int32_t n;
   int32_t layer[kMaxSeg];
-  const int32_t* dev_ids;  // device-resident schedule: layer j = dev_ids[j] (instead of layer[])
   float lr;
   const float* lr_ptr;
   double beta1, beta2, wd;
@@ -139,7 +138,6 @@ struct CommitArgs {
   double* probs;           // device [nl]
   int32_t* committed;      // device: a commit has happened
   int32_t* ids;            // device [gamma]: the sampled layers (draw order)
-  int32_t* avail;          // device [nl] scratch
   int32_t* err;            // device: 1 = commit with zero observations, 2 = non-finite gradient (sticky)
   unsigned long long* period_ctr;  // device: the period of the current ids; period == ~0: resample for ++ctr
 };

@@ -646,7 +646,7 @@ __global__ void grass_p2p_selftest_kernel(const __grid_constant__ P2PSelftestArg
 __global__ void grass_step_prologue_kernel(const __grid_constant__ PrologueArgs a, const DevState st) {
   const int j = threadIdx.x;
   if (j >= a.n) return;
-  const int l = a.dev_ids ? a.dev_ids[j] : a.layer[j];
+  const int l = a.layer[j];
   const long long t = st.t[l] + 1;
   st.t[l] = t;
   const double lr = a.lr_ptr ? (double)*a.lr_ptr : (double)a.lr;
