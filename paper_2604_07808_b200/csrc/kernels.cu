@@ -11,6 +11,12 @@
 //       shard value for the rank sum.
 //   K4  grass_rank_sum_kernel (world > 1): ascending-rank fp64 sum of the
 //       all-gathered shard partials, then the same MGN update.
+//   Device-resident schedule (grass_device_step): K2 with
+//       DEVB = true (segments and step-prologue scalars from the device ids)
+//       and K3 with t_l advanced and, in its last CTA, commit_sample_body —
+//       Eq. 2 window mean, Eq. 4 EMA, Eq. 3 softmax and the gamma draws
+//        in the host's operation order; both launched as
+//       programmatic dependent launches (launch_pdl).
 //
 // Nothing here is a contraction: K1/K2 are HBM-bound streams (~0.5 flop/B),
 // so there are no tensor cores.  The Blackwell-native part is the data
