@@ -342,7 +342,7 @@ def measure_read_ceiling(dev, gib: int = 8) -> dict:
     return {"GBps": sweep[k], "best": k, "sweep": sweep, "bytes": nbytes, **({"errors": errors} if errors else {})}
 
 
-def measure_mix_ceiling(dev, n: int = 2 * 202_383_360) -> dict:
+def measure_mix_ceiling(dev, n: int = 2 * 202_383_360, bf16: bool = False) -> dict:
     """K2's own traffic-mix ceiling: 4 reads + 3 writes per element (g, theta,
     m, v in; theta, m, v out — 28 B) with NO arithmetic, over 4 fp32 arrays of
     n elements (configs[1]'s gamma x N_p: 11.3 GB moved per launch, >> L2; not
@@ -359,16 +359,23 @@ def measure_mix_ceiling(dev, n: int = 2 * 202_383_360) -> dict:
     lib = C.CDLL(B.build_diag())                 # built in-tree by __graft_entry__.build()
     ft, fl = lib.grass_diag_rw43_tma, lib.grass_diag_rw43
     ft.restype = fl.restype = C.c_int
-    ft.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_uint, C.c_int, C.c_int, C.c_void_p]
+    ft.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_uint, C.c_int, C.c_int, C.c_int, C.c_void_p]
     fl.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_int, C.c_int, C.c_void_p]
-    bufs = [torch.full((n,), 1e-3, device=dev) for _ in range(4)]
-    ptrs = (C.c_void_p * 4)(*[b.data_ptr() for b in bufs])
+    # bf16 (K2's R18 mode): bf16 gradient read, fp32 master / m / v read and
+    # written, bf16 parameter copy written — 14 + 14 B per element
+    n -= n % 4096                                # whole units of every swept size
+    bufs = [torch.full((n,), 1e-3, device=dev, dtype=torch.bfloat16 if bf16 else torch.float32)]
+    bufs += [torch.full((n,), 1e-3, device=dev) for _ in range(3)]
+    if bf16:
+        bufs.append(torch.empty(n, device=dev, dtype=torch.bfloat16))
+    ptrs = (C.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs])
     s = torch.cuda.Stream(device=dev)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    cfgs = [(f"tma unit={e} x{st} grid={g}", lambda e=e, st=st, g=g: ft(ptrs, n, e, st, g, s.cuda_stream))
+    cfgs = [(f"tma unit={e} x{st} grid={g}", lambda e=e, st=st, g=g: ft(ptrs, n, e, st, g, int(bf16), s.cuda_stream))
             for e, st, g in ((4096, 3, 128), (2048, 3, sms), (2048, 6, 128), (1024, 4, sms), (2048, 2, 2 * sms))]
-    cfgs += [(f"ldg unroll={u} grid={g}", lambda u=u, g=g: fl(ptrs, n, u, g, s.cuda_stream))
-             for u, g in ((2, sms), (4, 8 * sms))]
+    if not bf16:
+        cfgs += [(f"ldg unroll={u} grid={g}", lambda u=u, g=g: fl(ptrs, n, u, g, s.cuda_stream))
+                 for u, g in ((2, sms), (4, 8 * sms))]
     sweep, errors = {}, {}
     for key, call in cfgs:
         best = 0.0
@@ -1040,7 +1047,13 @@ def run_grass(args, rank, world, local):
         bk = statistics.mean(a.elapsed_time(b) for a, b in bev)
         bgbs = BYTES_PER_PARAM_UPDATE * active / world / (bk / 1e3) / 1e9
         bctx.close()
+        try:
+            bmix = measure_mix_ceiling(dev, n=gamma * n_p // world, bf16=True)
+        except Exception as ex:  # recorded, never fatal to the leg
+            bmix = {"error": f"{type(ex).__name__}: {ex}"[:300]}
         return {"workload": f"{args.model}-stack gamma={gamma} bf16 params/grads, fp32 master+m+v, resident",
+                "mix_ceiling": bmix,
+                "frac_mix_ceiling": bgbs / bmix["GBps"] if bmix.get("GBps") else None,
                 "params_per_s": args.steps * active / bt, "step_ms": bt / args.steps * 1e3,
                 "kernel_ms": bk, "GBps": bgbs, "frac_hbm": bgbs / hbm_peak,
                 "bytes_per_param": BYTES_PER_PARAM_UPDATE,

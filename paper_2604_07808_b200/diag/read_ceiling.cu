@@ -211,13 +211,21 @@ __global__ void __launch_bounds__(512) rw43(const float4* __restrict__ g, float4
 // one bulk group per unit) and hands the slot back once the stores of the
 // PREVIOUS unit have finished reading shared memory.  The 4R3W TMA ceiling
 // K2 (the same ring plus the Eq. 2 / AdamW arithmetic) is compared with.
+// BF16 = true: K2's bf16 mode instead (R18: bf16 gradient and parameter,
+// fp32 master + m + v): g is bf16 (2 B, read), th / m / v are the fp32
+// master, m, v (read and written), and the bf16 parameter copy `p16` is
+// written (2 B, from the gradient's slot) — 14 B read + 14 B written per
+// element, the same 28 B as the fp32 mix in another read / write split.
+template <bool BF16>
 __global__ void __launch_bounds__(64, 1) rw43_tma(const float* __restrict__ g, float* __restrict__ th,
-                                                  float* __restrict__ m, float* __restrict__ v, size_t n,
-                                                  uint32_t elems, int stages) {
+                                                  float* __restrict__ m, float* __restrict__ v,
+                                                  uint16_t* __restrict__ p16, size_t n, uint32_t elems,
+                                                  int stages) {
   extern __shared__ __align__(1024) char ring[];
   __shared__ __align__(8) uint64_t full[16], empty[16];
   const int tid = threadIdx.x;
   const uint32_t piece = elems * 4u;
+  const uint32_t gpiece = BF16 ? elems * 2u : piece;
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
@@ -240,15 +248,17 @@ __global__ void __launch_bounds__(64, 1) rw43_tma(const float* __restrict__ g, f
                      "r"(par)
                      : "memory");
       }
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(4 * piece)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
+                   "r"(3 * piece + gpiece)
                    : "memory");
-      const float* src[4] = {g, th, m, v};
+      const char* src[4] = {reinterpret_cast<const char*>(g) + u * gpiece, reinterpret_cast<const char*>(th + u * elems),
+                            reinterpret_cast<const char*>(m + u * elems), reinterpret_cast<const char*>(v + u * elems)};
 #pragma unroll
       for (int a = 0; a < 4; ++a)
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
                 smem_u32(ring + ((size_t)s * 4 + a) * piece)),
-            "l"(src[a] + u * elems), "r"(piece), "r"(smem_u32(&full[s])), "l"(pol)
+            "l"(src[a]), "r"(a == 0 ? gpiece : piece), "r"(smem_u32(&full[s])), "l"(pol)
             : "memory");
     }
   } else if (tid == 32) {  // stores
@@ -265,6 +275,10 @@ __global__ void __launch_bounds__(64, 1) rw43_tma(const float* __restrict__ g, f
       for (int a = 0; a < 3; ++a)
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[a] + u * elems),
                      "r"(smem_u32(ring + ((size_t)s * 4 + 1 + a) * piece)), "r"(piece)
+                     : "memory");
+      if (BF16)  // the bf16 parameter copy, from the gradient's slot
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p16 + u * elems),
+                     "r"(smem_u32(ring + (size_t)s * 4 * piece)), "r"(gpiece)
                      : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       if (k >= 1) {  // unit k-1's stores have read their slot
@@ -291,18 +305,20 @@ extern "C" int grass_diag_rw43(void* const* bufs, unsigned long long n, int unro
   return (int)cudaGetLastError();
 }
 
+// bufs: g, theta (master), m, v [, p16 when bf16]; bf16: g is bf16 (n x 2 B)
 extern "C" int grass_diag_rw43_tma(void* const* bufs, unsigned long long n, unsigned int elems, int stages,
-                                   int grid, void* stream) {
+                                   int grid, int bf16, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (!bufs || grid < 1 || elems == 0 || elems % 4 != 0 || n % elems != 0 || stages < 2 || stages > 16 ||
+  if (!bufs || grid < 1 || elems == 0 || elems % 8 != 0 || n % elems != 0 || stages < 2 || stages > 16 ||
       (size_t)elems * 16 * stages > 227u * 1024u)
     return (int)cudaErrorInvalidValue;
   const size_t smem = (size_t)elems * 16 * stages;
-  cudaError_t e = cudaFuncSetAttribute(rw43_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = bf16 ? rw43_tma<true> : rw43_tma<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
-  rw43_tma<<<grid, 64, smem, s>>>(static_cast<const float*>(bufs[0]), static_cast<float*>(bufs[1]),
-                                  static_cast<float*>(bufs[2]), static_cast<float*>(bufs[3]), (size_t)n, elems,
-                                  stages);
+  kern<<<grid, 64, smem, s>>>(static_cast<const float*>(bufs[0]), static_cast<float*>(bufs[1]),
+                              static_cast<float*>(bufs[2]), static_cast<float*>(bufs[3]),
+                              bf16 ? static_cast<uint16_t*>(bufs[4]) : nullptr, (size_t)n, elems, stages);
   return (int)cudaGetLastError();
 }
 

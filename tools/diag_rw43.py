@@ -20,7 +20,7 @@ f.restype = C.c_int
 f.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_int, C.c_int, C.c_void_p]
 ft = lib.grass_diag_rw43_tma
 ft.restype = C.c_int
-ft.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_uint, C.c_int, C.c_int, C.c_void_p]
+ft.argtypes = [C.POINTER(C.c_void_p), C.c_ulonglong, C.c_uint, C.c_int, C.c_int, C.c_int, C.c_void_p]
 dev = torch.device("cuda", 0)
 n = 2 * 202_383_360
 bufs = [torch.randn(n, device=dev) * 1e-3 for _ in range(4)]
@@ -53,7 +53,7 @@ for elems, stages in ((1024, 4), (1024, 8), (2048, 2), (2048, 3), (2048, 6), (40
         if grid == 2 * sms and elems * 16 * stages > 113 * 1024:
             continue
         timed(f"tma unit={elems} x{stages} grid={grid}",
-              lambda: ft(ptrs, n, elems, stages, grid, s.cuda_stream))
+              lambda: ft(ptrs, n, elems, stages, grid, 0, s.cuda_stream))
 best = max((v["GBps"], k) for k, v in res.items())
 res["best"] = {"GBps": best[0], "what": best[1]}
 print(json.dumps(res))
