@@ -392,7 +392,6 @@ __device__ void commit_sample_body(const CommitArgs& a, const DevState& st, doub
         const int j = base + tid;
         const double term = j < ns && !sAv[j] ? sP[j] : 0.0;
         double cj = 0.0;
-#pragma unroll
         for (int q = 0; q < 32; ++q) {  // lanes past ns hold +0.0: the sum is unchanged
           c += __shfl_sync(0xffffffffu, term, q);
           cj = tid == q ? c : cj;
@@ -440,7 +439,7 @@ __global__ void __launch_bounds__(kCommitThreads) grass_commit_sample_kernel(con
 }
 
 constexpr int kFinThreads = 1024;  // K3 threads per layer (32 warps)
-__global__ void __launch_bounds__(kFinThreads) grass_finalize_kernel(const __grid_constant__ FinalizeArgs fa,
+__global__ void __launch_bounds__(kFinThreads, 1) grass_finalize_kernel(const __grid_constant__ FinalizeArgs fa,
                                                                      const DevState st) {
   constexpr int kW = kFinThreads / 32;
   __shared__ double red[kW];
