@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 > gpurun_out/r54_gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/r54_gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as e; e.smoke()" > gpurun_out/r54_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/r54_smoke.log
-timeout 600 python bench.py > gpurun_out/r54_bench.log 2> gpurun_out/r54_bench.err; echo "rc=$?" >> gpurun_out/r54_bench.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r54_ref.log 2> gpurun_out/r54_ref.err; echo "rc=$?" >> gpurun_out/r54_ref.err
+timeout 900 python -m pytest tests/test_gpu_device_schedule.py tests/test_gpu_graphs.py -q -p no:cacheprovider > gpurun_out/r55_devsched.log 2>&1; echo "rc=$?" >> gpurun_out/r55_devsched.log
+for i in 1 2; do timeout 300 python tools/device_step_profile.py >> gpurun_out/r55_devstep.log 2>&1; done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r55_launches_dev.csv python tools/device_step_profile.py > gpurun_out/r55_ncu_dev.log 2>&1
