@@ -103,6 +103,36 @@ def test_device_schedule_equals_host_schedule(dtype, T_s, T_u, n_always, alpha):
     _same(host, dev, P, numel)
 
 
+@pytest.mark.parametrize("policy", [G.POLICY_STATIC, G.POLICY_UNIFORM])
+@pytest.mark.parametrize("normalize", [True, False])
+def test_device_schedule_policies_equal_host(policy, normalize):
+    """GRASS* (probabilities frozen after the first commit)
+    and LISA-uniform, with and without the MGN normalisation of
+    Eq. 3: the device commit takes the same branch as grass_update_probs —
+    parameters, m, p and the sampled ids equal the host schedule's."""
+    host, dev, P, Gr, numel, sig, tdt = _setup(G.DTYPE_FP32, 0, 1, 1, policy=policy, normalize_mgn=normalize,
+                                               alpha=0.3)
+    nl = len(numel)
+    dev.register_layers(P[1], Gr)
+    for c in (host, dev):
+        _fill(Gr, numel, sig, 0, tdt)
+        c.mgn_accumulate(list(range(nl)), Gr)
+        c.update_probs()
+    ids = host.sample_layers(0)
+    dev.device_schedule_begin(0)
+    for step in range(1, 8):
+        _fill(Gr, numel, sig, step, tdt)
+        host.step_layers(ids, [P[0][l] for l in ids], [Gr[l] for l in ids], 1e-3)
+        dev.device_step(1e-3)
+        host.update_probs()
+        ids = host.sample_layers(step)
+        torch.cuda.synchronize()
+    assert dev.device_schedule_end() == ids
+    _same(host, dev, P, numel)
+    if policy == G.POLICY_UNIFORM:
+        np.testing.assert_array_equal(dev.get_mgn()["probs"], np.full(nl, 1.0 / nl))
+
+
 def test_device_schedule_commit_and_sampler_against_oracle():
     """The device commit + sampler against the ORACLE directly (not only the
     host path): probe all layers, start the device schedule (ids of period 0
