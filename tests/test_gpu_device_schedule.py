@@ -230,6 +230,32 @@ def test_device_schedule_full_size_layers_equal_host(dtype):
     assert abs(sb["last_ss"][l] - ss) <= 1e-6 * ss
 
 
+def test_device_schedule_nonfinite_gradient_stops_commits_and_is_reported():
+    """A non-finite gradient in a device step: its norm is not
+    recorded, the step's commit is skipped and the schedule stops committing,
+    and grass_device_schedule_end reports GRASS_E_NONFINITE with the layer —
+    m and p stay those of the last good commit."""
+    numel = [8192, 4096 * 3, 8192, 4096]
+    gr = G.Grass(numel, gamma=2, T_p=1, T_s=1, seed=5)
+    g = [layer_grad(n, l, 1e-3, device=DEV) for l, n in enumerate(numel)]
+    p = [layer_params(n, l, device=DEV) for l, n in enumerate(numel)]
+    gr.register_layers(p, g)
+    gr.mgn_accumulate([0, 1, 2, 3], g)
+    gr.update_probs()
+    before = gr.get_mgn()
+    gr.device_schedule_begin(0)
+    for x in g:                                        # whichever layers were sampled
+        x[3] = float("nan")
+    gr.device_step(1e-3)
+    gr.device_step(1e-3)                               # a later commit is not taken either
+    with pytest.raises(G.GrassError) as e:
+        gr.device_schedule_end()
+    assert e.value.status == G.binding.E_NONFINITE and "layer" in str(e.value)
+    after = gr.get_mgn()
+    np.testing.assert_array_equal(after["m"], before["m"])
+    np.testing.assert_array_equal(after["probs"], before["probs"])
+
+
 def test_device_schedule_misuse_rejected():
     numel = [8192, 8192, 4096]
     off = G.Grass(numel, gamma=2, offload=True)
