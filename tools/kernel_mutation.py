@@ -83,6 +83,8 @@ MUTANTS = {
            "const long long t = st.t[l];\n      const double lr = b.dev_lr_ptr")]),
     25: ("device step: the fused commit's done counter not reset (no commit after the first step)",
          [(K, "if (threadIdx.x == 0) *fa.done_ctr = 0;", "(void)0;")]),
+    26: ("device schedule: the commit ignores the non-finite flag (commits a window missing the layer)",
+         [(K, "      if (s_flag != 0) s_err = 2;", "      if (false) s_err = 2;")]),
     14: ("P2P barrier self-test: start barrier removed",
          [(K, "    a.which = 0;  // start barrier: every rank has read its rows of this round\n"
               "    const int n_save = a.n;\n    a.n = 0;\n    p2p_sync_cta(a);\n    a.n = n_save;\n", "")]),
@@ -93,7 +95,8 @@ TESTS = ("test_step_layers_vs_oracle_multi_step or test_norms_ragged_sizes_vs_or
          "test_norms_probe_equals_update_bitwise or test_norms_integer_grads_exact_bf16 or "
          "test_p2p_barrier_protocol_selftest or test_bf16_norms_tiny_and_huge_gradients or "
          "test_norms_all_tiles_reduction_keeps_each_tile_apart or test_offload_pipeline_happens_before_under_stress or "
-         "test_device_schedule_equals_host_schedule or test_device_schedule_commit_and_sampler_against_oracle")
+         "test_device_schedule_equals_host_schedule or test_device_schedule_commit_and_sampler_against_oracle or "
+         "test_device_schedule_policies_equal_host or test_device_schedule_nonfinite_gradient_stops_commits_and_is_reported")
 
 
 def patched_source(k: int) -> str:
