@@ -22,6 +22,7 @@ K = "kernels.cu"
 S = "stream_kernel.cuh"
 OFF = "offload.cpp"
 HOT = "hot_path.cpp"
+CK = "checkpoint.cpp"
 
 # k: (what, [(file, product text, mutated text), ...]) — every product text
 # must occur in the file (all occurrences are replaced)
@@ -85,6 +86,15 @@ MUTANTS = {
          [(K, "if (threadIdx.x == 0) *fa.done_ctr = 0;", "(void)0;")]),
     26: ("device schedule: the commit ignores the non-finite flag (commits a window missing the layer)",
          [(K, "      if (s_flag != 0) s_err = 2;", "      if (false) s_err = 2;")]),
+    27: ("clipping: the update ignores the clip coefficient (R17)",
+         [(S, "const float cf = (UPDATE && b.coef) ? *b.coef : 1.0f;", "const float cf = 1.0f;")]),
+    28: ("clipping: coefficient without min(1, .) (small gradients scaled up)",
+         [(K, "coef[0] = (float)fmin(1.0, a.max_norm / (sqrt(tot) + 1e-6));",
+           "coef[0] = (float)(a.max_norm / (sqrt(tot) + 1e-6));")]),
+    29: ("checkpoint: a load into a context with other hyperparameters accepted (fingerprint not checked)",
+         [(CK, "if (std::memcmp(&fp, &mine, sizeof(fp)) != 0)", "if (false)")]),
+    30: ("checkpoint: t_l restored on the host only (the device step counts keep their old values)",
+         [(CK, "  CUDA_TRY(c, cudaMemcpy(c->st.t, t.data(), sizeof(long long) * nl, cudaMemcpyHostToDevice));\n", "")]),
     14: ("P2P barrier self-test: start barrier removed",
          [(K, "    a.which = 0;  // start barrier: every rank has read its rows of this round\n"
               "    const int n_save = a.n;\n    a.n = 0;\n    p2p_sync_cta(a);\n    a.n = n_save;\n", "")]),
@@ -96,7 +106,9 @@ TESTS = ("test_step_layers_vs_oracle_multi_step or test_norms_ragged_sizes_vs_or
          "test_p2p_barrier_protocol_selftest or test_bf16_norms_tiny_and_huge_gradients or "
          "test_norms_all_tiles_reduction_keeps_each_tile_apart or test_offload_pipeline_happens_before_under_stress or "
          "test_device_schedule_equals_host_schedule or test_device_schedule_commit_and_sampler_against_oracle or "
-         "test_device_schedule_policies_equal_host or test_device_schedule_nonfinite_gradient_stops_commits_and_is_reported")
+         "test_device_schedule_policies_equal_host or test_device_schedule_nonfinite_gradient_stops_commits_and_is_reported or "
+         "test_clipping_vs_oracle or test_checkpoint_roundtrip_and_integrity or "
+         "test_checkpoint_keeps_written_master_and_rejects_other_hyperparameters")
 
 
 def patched_source(k: int) -> str:
